@@ -1,0 +1,169 @@
+// Shared device helpers: error plumbing, launch accounting, and the
+// reference's random streams (rng.hpp:14-54) bit-exact on the GPU.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+
+namespace tictac_dev {
+
+extern std::atomic<int64_t> g_launches;
+
+struct CudaError {
+  int code;
+};
+
+// Every CUDA call goes through CK; a failure becomes a message in `err`.
+#define CK(call)                                                                   \
+  do {                                                                             \
+    cudaError_t e_ = (call);                                                       \
+    if (e_ != cudaSuccess) {                                                       \
+      std::snprintf(err, 256, "CUDA error %s at %s:%d (%s)", cudaGetErrorString(e_), \
+                    __FILE__, __LINE__, #call);                                    \
+      return 1;                                                                    \
+    }                                                                              \
+  } while (0)
+
+#define LAUNCHED() tictac_dev::g_launches.fetch_add(1, std::memory_order_relaxed)
+
+int ensure_device(char* err);  // selects/initialises the current device
+
+// ---------------------------------------------------------------- RNG ----
+constexpr uint64_t kMtMul = 6364136223846793005ULL;
+constexpr uint64_t kMtMatrix = 0xB5026F5AA96619E9ULL;
+constexpr uint64_t kUpper = 0xFFFFFFFF80000000ULL;
+constexpr uint64_t kLower = 0x7FFFFFFFULL;
+constexpr uint64_t kPhi = 0x9e3779b97f4a7c15ULL;
+
+__host__ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+  x += 0x9e3779b97f4a7c15ULL;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+  return x ^ (x >> 31);
+}
+
+// mt19937_64 seeding recurrence: s[i] = K * (s[i-1] ^ (s[i-1] >> 62)) + i.
+__device__ __forceinline__ uint64_t mt_step(uint64_t prev, uint32_t i) {
+  return kMtMul * (prev ^ (prev >> 62)) + i;
+}
+// One twist element: c ^ ((a&U | b&L) >> 1) ^ (odd ? MATRIX : 0).
+__device__ __forceinline__ uint64_t mt_twist(uint64_t a, uint64_t b, uint64_t c) {
+  const uint64_t x = (a & kUpper) | (b & kLower);
+  return c ^ (x >> 1) ^ ((x & 1) ? kMtMatrix : 0ULL);
+}
+__device__ __forceinline__ uint64_t mt_temper(uint64_t y) {
+  y ^= (y >> 29) & 0x5555555555555555ULL;
+  y ^= (y << 17) & 0x71D67FFFEDA60000ULL;
+  y ^= (y << 37) & 0xFFF7EEE000000000ULL;
+  return y ^ (y >> 43);
+}
+
+// Full-state engine for streams of any length (state in memory owned by the
+// caller: 312 words). Used by single-lane consumers.
+struct MtFull {
+  uint64_t* mt;
+  int idx;
+  __device__ void seed(uint64_t s) {
+    mt[0] = s;
+    for (uint32_t i = 1; i < 312; ++i) mt[i] = mt_step(mt[i - 1], i);
+    idx = 312;
+  }
+  __device__ uint64_t next() {
+    if (idx >= 312) {
+      for (int i = 0; i < 312; ++i) mt[i] = mt_twist(mt[i], mt[(i + 1) % 312], mt[(i + 156) % 312]);
+      idx = 0;
+    }
+    return mt_temper(mt[idx++]);
+  }
+};
+
+// Register-only engine for the first 311 outputs (SURVEY §7 hard part 2:
+// every random order with R <= 312 lives in the first block). Outputs
+// i < 156 need s[i], s[i+1], s[i+156]; outputs 156 <= i < 311 need the
+// already-twisted t[i-156] = s[i] ^ f(s[i-156], s[i-155]). Two seeding
+// cursors run 156 apart, so no state array is stored.
+struct MtLazy {
+  uint64_t seed, a0, a1, b, c0, c1;
+  int i;
+  __device__ __forceinline__ void init(uint64_t s) {
+    seed = s;
+    a0 = s;
+    a1 = mt_step(s, 1);
+    b = s;
+#pragma unroll 4
+    for (uint32_t k = 1; k <= 156; ++k) b = mt_step(b, k);
+    c0 = c1 = 0;
+    i = 0;
+  }
+  __device__ __forceinline__ bool exhausted() const { return i >= 311; }
+  __device__ __forceinline__ uint64_t next_raw() {
+    uint64_t t;
+    if (i < 156) {
+      t = mt_twist(a0, a1, b);
+      a0 = a1;
+      a1 = mt_step(a1, static_cast<uint32_t>(i + 2));
+      b = mt_step(b, static_cast<uint32_t>(i + 157));
+      if (i == 155) {
+        c0 = seed;
+        c1 = mt_step(seed, 1);
+      }
+    } else {
+      const uint64_t back = mt_twist(c0, c1, a0);  // t[i-156]
+      t = mt_twist(a0, a1, back);
+      a0 = a1;
+      a1 = mt_step(a1, static_cast<uint32_t>(i + 2));
+      c0 = c1;
+      c1 = mt_step(c1, static_cast<uint32_t>(i - 154));
+    }
+    ++i;
+    return mt_temper(t);
+  }
+};
+
+// Bounded draw (rng.hpp:21-30) with host-precomputed per-n constants:
+// limit = UINT64_MAX - (2^64 mod n), magic = floor(2^64 / n).
+__device__ __forceinline__ uint64_t fastmod(uint64_t v, uint64_t n, uint64_t magic) {
+  const uint64_t q = __umul64hi(v, magic);
+  uint64_t r = v - q * n;
+  if (r >= n) r -= n;
+  return r;
+}
+
+inline void bounded_consts(uint64_t n, uint64_t* limit, uint64_t* magic) {
+  if (n < 2) {
+    *limit = ~0ULL;
+    *magic = 0;
+    return;
+  }
+  const uint64_t rem = (UINT64_MAX % n + 1) % n;
+  *limit = UINT64_MAX - rem;
+  *magic = static_cast<uint64_t>((static_cast<unsigned __int128>(1) << 64) / n);
+}
+
+// ----------------------------------------------------------- warp ops ----
+__device__ __forceinline__ int64_t warp_min64(int64_t v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v = min(v, static_cast<int64_t>(__shfl_xor_sync(~0u, v, o)));
+  return v;
+}
+__device__ __forceinline__ int64_t warp_max64(int64_t v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v = max(v, static_cast<int64_t>(__shfl_xor_sync(~0u, v, o)));
+  return v;
+}
+__device__ __forceinline__ int warp_sum(int v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(~0u, v, o);
+  return v;
+}
+// position of the k-th (0-based) set bit of x
+__device__ __forceinline__ int nth_bit(uint32_t x, int k) {
+  for (int j = 0; j < k; ++j) x &= x - 1;
+  return __ffs(x) - 1;
+}
+
+}  // namespace tictac_dev

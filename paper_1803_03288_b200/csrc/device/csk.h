@@ -1,0 +1,98 @@
+/* Internal C ABI between the host library (csrc/host) and the sm_100a
+ * kernels (csrc/device). Plain pointers and sizes only; host arrays in,
+ * host arrays out unless a name starts with d_ (device pointer).
+ *
+ * Every entry returns 0 on success or a nonzero code with a message in
+ * `err` (256 bytes); CUDA failures are reported, never silently skipped.
+ */
+#ifndef TICTAC_CSK_H
+#define TICTAC_CSK_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct DeviceGraph DeviceGraph;
+
+/* Structure only (durations travel per call, they belong to the oracle). */
+DeviceGraph* csk_graph_upload(int32_t n, const int32_t* pred_off, const int32_t* pred_idx,
+                              const int32_t* succ_off, const int32_t* succ_idx,
+                              const int8_t* kind, const int32_t* res, int32_t n_res,
+                              const int8_t* res_channel, const int32_t* res_device,
+                              int32_t n_dev, char* err);
+void csk_graph_free(DeviceGraph* g);
+
+/* Exact event simulator (reference sim.cpp:61-256), one warp per run.
+ * prio: B*n priorities (-1 unprioritized) in host memory, or NULL with
+ * orders != NULL: orders[b*R + i] = recv column holding priority i
+ * (recv columns = recv ops ascending). seeds: per-run choice_seed.
+ * start/end (n each) are filled for run 0 when non-NULL; dev_end (B*n_dev)
+ * gets the max event end per device when non-NULL.
+ * status[b]: 0 ok, 2 stalled ("simulation stalled with no runnable op"). */
+int csk_event_sim(DeviceGraph* g, const int64_t* dur, int32_t B, const int32_t* prio,
+                  const int32_t* orders, int32_t R, const uint64_t* seeds, int gated,
+                  double noise, int64_t* makespan, int64_t* violations, int32_t* status,
+                  int64_t* start, int64_t* end, int64_t* dev_end, char* err);
+/* Random sweep through the exact event simulator (cases outside the closed
+ * form): run b uses seed seed_lo+b for both its random schedule (per-worker
+ * derived seeds when `cluster`) and its choice stream. dev_end (B*n_dev,
+ * max event end per device) may be NULL. recv_worker[c] = index of recv
+ * column c's device in worker_devices() order (all 0 for worker graphs). */
+int csk_event_sweep(DeviceGraph* g, const int64_t* dur, uint64_t seed_lo, int32_t B,
+                    int cluster, const int32_t* recv_worker, int32_t n_workers, int gated,
+                    double noise, int64_t* makespan, int64_t* violations, int32_t* status,
+                    int64_t* dev_end, char* err);
+
+/* Brute force: all R! lexicographic permutations of the recv columns, each
+ * simulated gated with the same choice seed / noise (metrics.cpp:37-72).
+ * makespans has R! entries, in lexicographic order. */
+int csk_brute_force(DeviceGraph* g, const int64_t* dur, int32_t R, uint64_t choice_seed,
+                    double noise, int64_t* makespans, char* err);
+
+/* Dependency closure + properties with every recv outstanding
+ * (properties.cpp:19-109). dep_bits: n * words64 uint64 (bit c = recv column
+ * c); M: n; P, Mplus: R (INT64_MAX = nullopt). mode 0 literal, 1 amended. */
+int csk_properties(DeviceGraph* g, const int64_t* dur, int mode, uint64_t* dep_bits,
+                   int64_t* M, int64_t* P, int64_t* Mplus, char* err);
+
+/* tic (schedule.cpp:21-42): dense ranks per recv column; *total = flag. */
+int csk_tic(DeviceGraph* g, int mode, int32_t* prio, int* total, char* err);
+
+/* tac (schedule.cpp:44-71): rank per recv column. */
+int csk_tac(DeviceGraph* g, const int64_t* dur, int32_t* prio, char* err);
+
+/* random_schedule (schedule.cpp:73-84) for several seeds at once:
+ * perms[s*R + k] = recv column at rank k for seeds[s]. */
+int csk_random_orders(int32_t R, int32_t S, const uint64_t* seeds, int32_t* perms, char* err);
+
+/* ---- closed-form batched sweep -------------------- */
+typedef struct SweepPlan SweepPlan;
+
+/* Per-worker chain plan: R recv columns with durations d (int64), first[c]
+ * = index of the first chain class containing recv c (nc = none), suffix
+ * class weights pwsuf[0..nc]. send_total = total send time on the worker's
+ * channel (0 for worker graphs). W workers share the layout; worker w uses
+ * tables at offset w. seed derivation: worker graphs use the seed itself;
+ * clusters use splitmix64(seed ^ phi*(w+1)) (cluster.cpp:112-113). */
+SweepPlan* csk_sweep_plan(int32_t W, int32_t R, int32_t nc, const int64_t* d,
+                          const int32_t* first, const int64_t* pwsuf, const int64_t* send_total,
+                          int cluster, int64_t U, int64_t L, char* err);
+void csk_sweep_plan_free(SweepPlan* p);
+/* Stats layout documented in include/commsched.h (CS_DSTATS_*). */
+int csk_sweep_reset(SweepPlan* p, void* stream, int64_t* d_i64, double* d_f64, char* err);
+int csk_sweep_run(SweepPlan* p, uint64_t seed_lo, int64_t count, uint64_t key_base,
+                  void* stream, int64_t* d_makespans, int64_t* d_worker_makespans,
+                  int64_t* d_i64, double* d_f64, char* err);
+/* Explicit orders on device (int32, [n][R]) instead of seeds; W must be 1. */
+int csk_sweep_orders(SweepPlan* p, const int32_t* d_orders, int64_t n, void* stream,
+                     int64_t* d_makespans, char* err);
+
+/* Launch counter (kernels launched by this library, process-wide). */
+int64_t csk_launches(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,610 @@
+// Exact event simulator on the GPU — a warp-cooperative replica of the
+// reference's discrete-event loop (sim.cpp:61-256), one warp per run.
+//
+// Per-resource ready queues are bitsets over that resource's ops (ascending
+// op index = the reference's sorted queue), so candidate selection is a
+// ballot/popc scan; the k-th candidate of the seeded uniform draw is found
+// with a warp prefix sum. The choice stream is the reference's mt19937_64
+// (shared by all resources, consumed in round order), the reorder-noise
+// stream is Rng(splitmix64(choice_seed ^ salt)) consumed in resource order.
+// Used for every cs_simulate call, brute force, and sweeps outside the
+// closed form of SURVEY Appendix A.2.
+#include <algorithm>
+#include <vector>
+
+#include "common.cuh"
+#include "csk.h"
+#include "devgraph.cuh"
+
+namespace tictac_dev {
+
+namespace {
+
+constexpr int kWarpsPerBlock = 4;
+constexpr uint64_t kNoiseSalt = 0x9e3779b97f4a7c15ULL;  // sim.cpp:14
+
+struct GraphView {
+  int32_t n, nres, ndev, R;
+  const int32_t *pred_off, *succ_off, *succ_idx, *res, *res_dev, *rops_off, *rops, *lidx, *rb_off,
+      *recv_ops;
+  const int8_t* chan;
+  const int64_t* dur;
+};
+
+// How a run obtains its priorities.
+enum PrioMode : int { kPrioExplicit = 0, kPrioOrders = 1, kPrioRandom = 2, kPrioLex = 3 };
+
+struct RunSpec {
+  int mode;
+  const int32_t* prio;    // kPrioExplicit: [B][n]
+  const int32_t* orders;  // kPrioOrders: [B][R]
+  uint64_t seed_lo;       // kPrioRandom: seed = seed_lo + b ; kPrioLex: choice seed
+  const uint64_t* seeds;  // per-run choice seeds (explicit/orders modes)
+  int cluster;            // kPrioRandom: derive per-worker seeds
+  const int32_t* wcols_off;  // kPrioRandom: worker w's recv columns
+  const int32_t* wcols;
+  int32_t n_workers;
+  const uint64_t* lim;    // bounded() constants for n = 0..R
+  const uint64_t* mag;
+  int gated;
+  double noise;
+  int64_t* makespan;
+  int64_t* violations;
+  int32_t* status;
+  int64_t* start;  // run 0 only
+  int64_t* end;
+  int64_t* dev_end;  // [B][ndev]
+};
+
+// Scratch carved per warp slot.
+struct Slot {
+  int32_t *missing, *gate, *orig, *seq, *prio, *items, *comp, *running, *comp_len, *ready_cnt;
+  uint32_t *ready, *forced;
+  int64_t *run_end, *counter, *dev_end;
+  uint64_t *mt, *mt2;
+};
+
+__host__ __device__ inline size_t align8(size_t x) { return (x + 7) & ~size_t(7); }
+
+__host__ __device__ inline size_t slot_bytes(int n, int nres, int ndev, int rbw, int R) {
+  size_t b = 0;
+  b += align8(4ull * n) * 6;         // missing gate orig seq prio comp
+  b += align8(4ull * (R + 1));       // items
+  b += align8(4ull * nres) * 3;      // running comp_len ready_cnt
+  b += align8(4ull * (rbw + 1));     // ready
+  b += align8(4ull * ((n + 31) / 32 + 1));  // forced
+  b += align8(8ull * nres) * 2;      // run_end counter
+  b += align8(8ull * (ndev + 1));    // dev_end
+  b += 8ull * 312 * 2;               // mt mt2
+  return b;
+}
+
+__device__ Slot carve(char* base, int n, int nres, int ndev, int rbw, int R) {
+  Slot s;
+  auto take = [&](size_t bytes) {
+    char* p = base;
+    base += align8(bytes);
+    return p;
+  };
+  s.missing = reinterpret_cast<int32_t*>(take(4ull * n));
+  s.gate = reinterpret_cast<int32_t*>(take(4ull * n));
+  s.orig = reinterpret_cast<int32_t*>(take(4ull * n));
+  s.seq = reinterpret_cast<int32_t*>(take(4ull * n));
+  s.prio = reinterpret_cast<int32_t*>(take(4ull * n));
+  s.comp = reinterpret_cast<int32_t*>(take(4ull * n));
+  s.items = reinterpret_cast<int32_t*>(take(4ull * (R + 1)));
+  s.running = reinterpret_cast<int32_t*>(take(4ull * nres));
+  s.comp_len = reinterpret_cast<int32_t*>(take(4ull * nres));
+  s.ready_cnt = reinterpret_cast<int32_t*>(take(4ull * nres));
+  s.ready = reinterpret_cast<uint32_t*>(take(4ull * (rbw + 1)));
+  s.forced = reinterpret_cast<uint32_t*>(take(4ull * ((n + 31) / 32 + 1)));
+  s.run_end = reinterpret_cast<int64_t*>(take(8ull * nres));
+  s.counter = reinterpret_cast<int64_t*>(take(8ull * nres));
+  s.dev_end = reinterpret_cast<int64_t*>(take(8ull * (ndev + 1)));
+  s.mt = reinterpret_cast<uint64_t*>(take(8ull * 312));
+  s.mt2 = reinterpret_cast<uint64_t*>(take(8ull * 312));
+  return s;
+}
+
+// Lane-0 helpers over a full mt19937_64 state in scratch.
+__device__ uint64_t bounded_full(MtFull& m, uint64_t n, const RunSpec& rs) {
+  if (n < 2) return 0;
+  uint64_t lim, mag;
+  if (n <= static_cast<uint64_t>(0x7fffffff) && rs.lim && n < 4096) {
+    lim = rs.lim[n];
+    mag = rs.mag[n];
+    uint64_t v;
+    do v = m.next();
+    while (v > lim);
+    return fastmod(v, n, mag);
+  }
+  const uint64_t limit = UINT64_MAX - (UINT64_MAX % n + 1) % n;
+  uint64_t v;
+  do v = m.next();
+  while (v > limit);
+  return v % n;
+}
+
+__device__ __forceinline__ bool admitted(const Slot& s, int op, int r, int gated) {
+  const int gt = s.gate[op];
+  if (!gated || gt < 0) return true;
+  if ((s.forced[op >> 5] >> (op & 31)) & 1u) return true;
+  return static_cast<int64_t>(gt) <= s.counter[r];
+}
+
+__device__ void fill_priorities(const GraphView& G, const RunSpec& rs, const Slot& s, int64_t b,
+                                int lane, uint64_t* choice_seed) {
+  const int n = G.n;
+  if (rs.mode == kPrioExplicit) {
+    const int32_t* p = rs.prio + b * n;
+    for (int i = lane; i < n; i += 32) s.prio[i] = p[i];
+    *choice_seed = rs.seeds[b];
+    return;
+  }
+  for (int i = lane; i < n; i += 32) s.prio[i] = -1;
+  __syncwarp();
+  if (rs.mode == kPrioOrders) {
+    const int32_t* o = rs.orders + b * G.R;
+    for (int k = lane; k < G.R; k += 32) s.prio[G.recv_ops[o[k]]] = k;
+    *choice_seed = rs.seeds[b];
+  } else if (rs.mode == kPrioLex) {
+    *choice_seed = rs.seed_lo;
+    if (lane == 0) {  // unrank b in the factorial number system
+      const int R = G.R;
+      for (int k = 0; k < R; ++k) s.items[k] = k;
+      int64_t f = 1;
+      for (int k = 2; k < R; ++k) f *= k;
+      int64_t rem = b;
+      for (int pos = 0; pos < R; ++pos) {
+        const int64_t q = f ? rem / f : 0;
+        rem = f ? rem % f : 0;
+        const int pick = s.items[q];
+        for (int k = static_cast<int>(q); k + 1 < R - pos; ++k) s.items[k] = s.items[k + 1];
+        s.prio[G.recv_ops[pick]] = pos;
+        if (R - 1 - pos > 0) f /= (R - 1 - pos);
+      }
+    }
+  } else {  // kPrioRandom: random_schedule per worker (schedule_for)
+    const uint64_t seed = rs.seed_lo + static_cast<uint64_t>(b);
+    *choice_seed = seed;
+    if (lane == 0) {
+      for (int w = 0; w < rs.n_workers; ++w) {
+        const int c0 = rs.wcols_off[w], Rw = rs.wcols_off[w + 1] - c0;
+        const uint64_t ws = rs.cluster ? splitmix64(seed ^ (kPhi * static_cast<uint64_t>(w + 1))) : seed;
+        for (int k = 0; k < Rw; ++k) s.items[k] = k;
+        MtFull m{s.mt2, 0};
+        m.seed(ws);
+        for (int i = Rw; i > 1; --i) {
+          const int j = static_cast<int>(bounded_full(m, static_cast<uint64_t>(i), rs));
+          const int t = s.items[i - 1];
+          s.items[i - 1] = s.items[j];
+          s.items[j] = t;
+        }
+        for (int k = 0; k < Rw; ++k) s.prio[G.recv_ops[rs.wcols[c0 + s.items[k]]]] = k;
+      }
+    }
+  }
+  __syncwarp();
+}
+
+__global__ void __launch_bounds__(32 * kWarpsPerBlock)
+    event_sim_kernel(GraphView G, RunSpec rs, int64_t B, char* scratch, size_t slot_sz, int rbw) {
+  const int lane = threadIdx.x & 31;
+  const int64_t slot_id = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nslots = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const Slot s = carve(scratch + slot_id * slot_sz, G.n, G.nres, G.ndev, rbw, G.R);
+  const int n = G.n, nres = G.nres;
+
+  for (int64_t b = slot_id; b < B; b += nslots) {
+    uint64_t choice_seed = 0;
+    fill_priorities(G, rs, s, b, lane, &choice_seed);
+    // ---- setup (sim.cpp:74-123)
+    for (int i = lane; i < n; i += 32) {
+      s.missing[i] = G.pred_off[i + 1] - G.pred_off[i];
+      s.gate[i] = -1;
+      s.orig[i] = -1;
+    }
+    for (int w = lane; w < rbw; w += 32) s.ready[w] = 0;
+    for (int w = lane; w < (n + 31) / 32; w += 32) s.forced[w] = 0;
+    for (int r = lane; r < nres; r += 32) {
+      s.running[r] = -1;
+      s.run_end[r] = 0;
+      s.counter[r] = 0;
+      s.comp_len[r] = 0;
+      s.ready_cnt[r] = 0;
+    }
+    for (int d = lane; d < G.ndev; d += 32) s.dev_end[d] = 0;
+    __syncwarp();
+    for (int i = lane; i < n; i += 32)
+      if (s.missing[i] == 0) {
+        const int r = G.res[i], l = G.lidx[i];
+        atomicOr(&s.ready[G.rb_off[r] + (l >> 5)], 1u << (l & 31));
+        atomicAdd(&s.ready_cnt[r], 1);
+      }
+    // dense per-channel ranks from (priority, id), then noise swaps
+    MtFull noise{s.mt2, 0};
+    const bool noisy = rs.gated && rs.noise > 0.0;
+    if (lane == 0 && noisy) noise.seed(splitmix64(choice_seed ^ kNoiseSalt));
+    for (int r = 0; r < nres; ++r) {
+      if (!G.chan[r]) continue;
+      const int o0 = G.rops_off[r], o1 = G.rops_off[r + 1];
+      int mine = 0;
+      for (int a = o0 + lane; a < o1; a += 32) {
+        const int i = G.rops[a];
+        const int pi = s.prio[i];
+        if (pi < 0) continue;
+        int rank = 0;
+        for (int c = o0; c < o1; ++c) {
+          const int j = G.rops[c];
+          const int pj = s.prio[j];
+          rank += (pj >= 0) && (pj < pi || (pj == pi && j < i));
+        }
+        s.orig[i] = rank;
+        s.seq[o0 + rank] = i;
+        ++mine;
+      }
+      const int k = warp_sum(mine);
+      __syncwarp();
+      if (!rs.gated) continue;
+      if (lane == 0 && noisy)
+        for (int p = 1; p < k; ++p) {
+          const double u = static_cast<double>(noise.next() >> 11) * 0x1.0p-53;
+          if (u < rs.noise) {
+            const int t = s.seq[o0 + p - 1];
+            s.seq[o0 + p - 1] = s.seq[o0 + p];
+            s.seq[o0 + p] = t;
+          }
+        }
+      __syncwarp();
+      for (int p = lane; p < k; p += 32) s.gate[s.seq[o0 + p]] = p;
+      __syncwarp();
+    }
+    MtFull choice{s.mt, 0};
+    if (lane == 0) choice.seed(choice_seed);
+    __syncwarp();
+
+    // ---- event loop (sim.cpp:194-233)
+    int64_t t = 0, mk = 0, nforced = 0;
+    int finished = 0, stalled = 0;
+    const int gated = rs.gated;
+    const bool rec = (b == 0) && rs.start;
+
+    auto start_op = [&](int r, int op) {
+      if (lane == 0) {
+        const int l = G.lidx[op];
+        atomicAnd(&s.ready[G.rb_off[r] + (l >> 5)], ~(1u << (l & 31)));
+        s.ready_cnt[r] -= 1;
+        s.running[r] = op;
+        const int64_t e = t + G.dur[op];
+        s.run_end[r] = e;
+        if (rec) {
+          rs.start[op] = t;
+          rs.end[op] = e;
+        }
+        const int d = G.res_dev[r];
+        if (e > s.dev_end[d]) s.dev_end[d] = e;
+      }
+      const int64_t e = t + G.dur[op];
+      mk = max(mk, e);
+      __syncwarp();
+    };
+
+    // candidate mask of one ready word (word w of resource r)
+    auto cand_mask = [&](int r, int w, int best) -> uint32_t {
+      uint32_t bits = s.ready[G.rb_off[r] + w], m = 0;
+      const int base = G.rops_off[r] + (w << 5);
+      while (bits) {
+        const int bit = __ffs(bits) - 1;
+        bits &= bits - 1;
+        const int op = G.rops[base + bit];
+        const int p = s.prio[op];
+        if (p < 0 || (p == best && admitted(s, op, r, gated))) m |= 1u << bit;
+      }
+      return m;
+    };
+
+    auto try_start = [&](int r) -> bool {  // sim.cpp:163-192
+      if (s.running[r] >= 0 || s.ready_cnt[r] == 0) return false;
+      const int nw = G.rb_off[r + 1] - G.rb_off[r];
+      int best = 0x7fffffff;
+      for (int w = lane; w < nw; w += 32) {
+        uint32_t bits = s.ready[G.rb_off[r] + w];
+        const int base = G.rops_off[r] + (w << 5);
+        while (bits) {
+          const int bit = __ffs(bits) - 1;
+          bits &= bits - 1;
+          const int op = G.rops[base + bit];
+          const int p = s.prio[op];
+          if (p >= 0 && p < best && admitted(s, op, r, gated)) best = p;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) best = min(best, __shfl_xor_sync(~0u, best, o));
+      int total = 0;
+      for (int c = 0; c < nw; c += 32) {
+        const uint32_t m = (c + lane < nw) ? cand_mask(r, c + lane, best) : 0u;
+        total += warp_sum(__popc(m));
+      }
+      if (total == 0) return false;
+      int k = 0;
+      if (total > 1) {
+        uint64_t kk = 0;
+        if (lane == 0) kk = bounded_full(choice, static_cast<uint64_t>(total), rs);
+        k = static_cast<int>(__shfl_sync(~0u, kk, 0));
+      }
+      int pick = -1;
+      for (int c = 0; c < nw && pick < 0; c += 32) {
+        const uint32_t m = (c + lane < nw) ? cand_mask(r, c + lane, best) : 0u;
+        const int cnt = __popc(m);
+        int incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(~0u, incl, o);
+          if (lane >= o) incl += y;
+        }
+        const int chunk = __shfl_sync(~0u, incl, 31);
+        if (k < chunk) {
+          const int excl = incl - cnt;
+          const bool here = k >= excl && k < incl;
+          const unsigned who = __ballot_sync(~0u, here);
+          const int src = __ffs(who) - 1;
+          int op = -1;
+          if (here) op = G.rops[G.rops_off[r] + ((c + lane) << 5) + nth_bit(m, k - excl)];
+          pick = __shfl_sync(~0u, op, src);
+        } else {
+          k -= chunk;
+        }
+      }
+      start_op(r, pick);
+      return true;
+    };
+
+    auto complete_now = [&]() -> bool {  // sim.cpp:144-161
+      bool any = false;
+      for (int r = 0; r < nres; ++r) {
+        const int i = s.running[r];
+        if (i < 0 || s.run_end[r] != t) continue;
+        __syncwarp();
+        any = true;
+        ++finished;
+        if (lane == 0) {
+          s.running[r] = -1;
+          if (s.prio[i] >= 0 && G.chan[r]) {
+            s.counter[r] += 1;
+            s.comp[G.rops_off[r] + s.comp_len[r]] = s.orig[i];
+            s.comp_len[r] += 1;
+          }
+        }
+        for (int e = G.succ_off[i] + lane; e < G.succ_off[i + 1]; e += 32) {
+          const int w = G.succ_idx[e];
+          if (atomicSub(&s.missing[w], 1) == 1) {
+            const int rw = G.res[w], l = G.lidx[w];
+            atomicOr(&s.ready[G.rb_off[rw] + (l >> 5)], 1u << (l & 31));
+            atomicAdd(&s.ready_cnt[rw], 1);
+          }
+        }
+        __syncwarp();
+      }
+      return any;
+    };
+
+    while (finished < n) {
+      bool progress = true;
+      while (progress) {
+        progress = false;
+        for (int r = 0; r < nres; ++r) progress = try_start(r) || progress;
+        progress = complete_now() || progress;
+      }
+      if (finished == n) break;
+      int64_t next_t = INT64_MAX;
+      for (int r = lane; r < nres; r += 32)
+        if (s.running[r] >= 0) next_t = min(next_t, s.run_end[r]);
+      next_t = warp_min64(next_t);
+      if (next_t == INT64_MAX) {  // forced release, sim.cpp:211-229
+        int64_t key = INT64_MAX;
+        for (int r = 0; r < nres; ++r) {
+          const int nw = G.rb_off[r + 1] - G.rb_off[r];
+          for (int w = lane; w < nw; w += 32) {
+            uint32_t bits = s.ready[G.rb_off[r] + w];
+            const int base = G.rops_off[r] + (w << 5);
+            while (bits) {
+              const int bit = __ffs(bits) - 1;
+              bits &= bits - 1;
+              const int op = G.rops[base + bit];
+              if (s.gate[op] < 0 || admitted(s, op, r, gated)) continue;
+              key = min(key, (static_cast<int64_t>(s.gate[op]) << 32) | op);
+            }
+          }
+        }
+        key = warp_min64(key);
+        if (key == INT64_MAX) {
+          stalled = 1;
+          break;
+        }
+        const int victim = static_cast<int>(key & 0xffffffff);
+        if (lane == 0) s.forced[victim >> 5] |= 1u << (victim & 31);
+        ++nforced;
+        __syncwarp();
+        continue;
+      }
+      t = next_t;
+      complete_now();
+    }
+
+    // violations: rank inversions per channel completion sequence + forced
+    int64_t inv = 0;
+    for (int r = 0; r < nres; ++r) {
+      if (!G.chan[r]) continue;
+      const int* seq = s.comp + G.rops_off[r];
+      const int len = s.comp_len[r];
+      for (int a = lane; a < len; a += 32)
+        for (int c = a + 1; c < len; ++c) inv += seq[a] > seq[c];
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) inv += __shfl_xor_sync(~0u, inv, o);
+    if (lane == 0) {
+      rs.makespan[b] = mk;
+      rs.violations[b] = inv + nforced;
+      rs.status[b] = stalled ? 2 : 0;
+      if (rs.dev_end)
+        for (int d = 0; d < G.ndev; ++d) rs.dev_end[b * G.ndev + d] = s.dev_end[d];
+    }
+    __syncwarp();
+  }
+}
+
+struct DevBuf {
+  void* p = nullptr;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+};
+
+template <typename T>
+int dev_copy(DevBuf& buf, const T* src, size_t count, char* err) {
+  CK(cudaMalloc(&buf.p, sizeof(T) * (count ? count : 1)));
+  if (count && src) CK(cudaMemcpy(buf.p, src, sizeof(T) * count, cudaMemcpyHostToDevice));
+  return 0;
+}
+
+int run_event(DeviceGraph* g, const int64_t* dur, int64_t B, RunSpec rs, int64_t* makespan,
+              int64_t* violations, int32_t* status, int64_t* start, int64_t* end, int64_t* dev_end,
+              char* err) {
+  if (ensure_device(err)) return 1;
+  if (B <= 0) return 0;
+  DevBuf d_dur, d_ms, d_vio, d_st, d_start, d_end, d_dev, d_scr, d_lim, d_mag;
+  if (dev_copy(d_dur, dur, g->n, err)) return 1;
+  std::vector<uint64_t> lim(4096), mag(4096);
+  for (uint64_t k = 0; k < 4096; ++k) bounded_consts(k, &lim[k], &mag[k]);
+  if (dev_copy(d_lim, lim.data(), lim.size(), err) || dev_copy(d_mag, mag.data(), mag.size(), err))
+    return 1;
+  rs.lim = static_cast<uint64_t*>(d_lim.p);
+  rs.mag = static_cast<uint64_t*>(d_mag.p);
+  if (dev_copy<int64_t>(d_ms, nullptr, B, err) || dev_copy<int64_t>(d_vio, nullptr, B, err) ||
+      dev_copy<int32_t>(d_st, nullptr, B, err))
+    return 1;
+  rs.makespan = static_cast<int64_t*>(d_ms.p);
+  rs.violations = static_cast<int64_t*>(d_vio.p);
+  rs.status = static_cast<int32_t*>(d_st.p);
+  rs.start = rs.end = nullptr;
+  if (start) {
+    if (dev_copy<int64_t>(d_start, nullptr, g->n, err) || dev_copy<int64_t>(d_end, nullptr, g->n, err))
+      return 1;
+    rs.start = static_cast<int64_t*>(d_start.p);
+    rs.end = static_cast<int64_t*>(d_end.p);
+  }
+  rs.dev_end = nullptr;
+  if (dev_end) {
+    if (dev_copy<int64_t>(d_dev, nullptr, static_cast<size_t>(B) * g->ndev, err)) return 1;
+    rs.dev_end = static_cast<int64_t*>(d_dev.p);
+  }
+  GraphView G{g->n,        g->nres,     g->ndev,     g->R,        g->pred_off, g->succ_off,
+              g->succ_idx, g->res,      g->res_dev,  g->rops_off, g->rops,     g->lidx,
+              g->rb_off,   g->recv_ops, g->chan,     static_cast<int64_t*>(d_dur.p)};
+  int sms = 148;
+  {
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  }
+  const int64_t max_slots = static_cast<int64_t>(sms) * 16;
+  const int64_t slots = std::min<int64_t>(B, max_slots);
+  const int blocks = static_cast<int>((slots + kWarpsPerBlock - 1) / kWarpsPerBlock);
+  const int64_t total_slots = static_cast<int64_t>(blocks) * kWarpsPerBlock;
+  const size_t ssz = align8(slot_bytes(g->n, g->nres, g->ndev, g->rb_words, g->R));
+  CK(cudaMalloc(&d_scr.p, ssz * static_cast<size_t>(total_slots)));
+  event_sim_kernel<<<blocks, 32 * kWarpsPerBlock>>>(G, rs, B, static_cast<char*>(d_scr.p), ssz,
+                                                    g->rb_words);
+  LAUNCHED();
+  CK(cudaGetLastError());
+  CK(cudaDeviceSynchronize());
+  CK(cudaMemcpy(makespan, d_ms.p, 8 * B, cudaMemcpyDeviceToHost));
+  if (violations) CK(cudaMemcpy(violations, d_vio.p, 8 * B, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(status, d_st.p, 4 * B, cudaMemcpyDeviceToHost));
+  if (start) {
+    CK(cudaMemcpy(start, d_start.p, 8ull * g->n, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(end, d_end.p, 8ull * g->n, cudaMemcpyDeviceToHost));
+  }
+  if (dev_end) CK(cudaMemcpy(dev_end, d_dev.p, 8ull * B * g->ndev, cudaMemcpyDeviceToHost));
+  return 0;
+}
+
+}  // namespace
+
+}  // namespace tictac_dev
+
+using namespace tictac_dev;
+
+extern "C" int csk_event_sim(DeviceGraph* g, const int64_t* dur, int32_t B, const int32_t* prio,
+                             const int32_t* orders, int32_t R, const uint64_t* seeds, int gated,
+                             double noise, int64_t* makespan, int64_t* violations, int32_t* status,
+                             int64_t* start, int64_t* end, int64_t* dev_end, char* err) {
+  if (ensure_device(err)) return 1;
+  DevBuf d_p, d_s;
+  RunSpec rs{};
+  if (prio) {
+    if (dev_copy(d_p, prio, static_cast<size_t>(B) * g->n, err)) return 1;
+    rs.mode = kPrioExplicit;
+    rs.prio = static_cast<int32_t*>(d_p.p);
+  } else {
+    if (R != g->R) {
+      std::snprintf(err, 256, "orders have %d recvs, graph has %d", R, g->R);
+      return 4;
+    }
+    if (dev_copy(d_p, orders, static_cast<size_t>(B) * R, err)) return 1;
+    rs.mode = kPrioOrders;
+    rs.orders = static_cast<int32_t*>(d_p.p);
+  }
+  if (dev_copy(d_s, seeds, B, err)) return 1;
+  rs.seeds = static_cast<uint64_t*>(d_s.p);
+  rs.gated = gated;
+  rs.noise = noise;
+  return run_event(g, dur, B, rs, makespan, violations, status, start, end, dev_end, err);
+}
+
+extern "C" int csk_event_sweep(DeviceGraph* g, const int64_t* dur, uint64_t seed_lo, int32_t B,
+                               int cluster, const int32_t* recv_worker, int32_t n_workers, int gated,
+                               double noise, int64_t* makespan, int64_t* violations, int32_t* status,
+                               int64_t* dev_end, char* err) {
+  if (ensure_device(err)) return 1;
+  std::vector<int32_t> off(n_workers + 1, 0), cols(g->R);
+  for (int c = 0; c < g->R; ++c) off[recv_worker[c] + 1]++;
+  for (int w = 0; w < n_workers; ++w) off[w + 1] += off[w];
+  std::vector<int32_t> fill(off.begin(), off.end() - 1);
+  for (int c = 0; c < g->R; ++c) cols[fill[recv_worker[c]]++] = c;
+  DevBuf d_off, d_cols;
+  if (dev_copy(d_off, off.data(), off.size(), err) || dev_copy(d_cols, cols.data(), cols.size(), err))
+    return 1;
+  RunSpec rs{};
+  rs.mode = kPrioRandom;
+  rs.seed_lo = seed_lo;
+  rs.cluster = cluster;
+  rs.wcols_off = static_cast<int32_t*>(d_off.p);
+  rs.wcols = static_cast<int32_t*>(d_cols.p);
+  rs.n_workers = n_workers;
+  rs.gated = gated;
+  rs.noise = noise;
+  return run_event(g, dur, B, rs, makespan, violations, status, nullptr, nullptr, dev_end, err);
+}
+
+extern "C" int csk_brute_force(DeviceGraph* g, const int64_t* dur, int32_t R, uint64_t choice_seed,
+                               double noise, int64_t* makespans, char* err) {
+  if (ensure_device(err)) return 1;
+  if (R != g->R || R > 20) {
+    std::snprintf(err, 256, "brute force over %d recvs unsupported", R);
+    return 4;
+  }
+  int64_t perms = 1;
+  for (int k = 2; k <= R; ++k) perms *= k;
+  std::vector<int32_t> status(static_cast<size_t>(perms));
+  RunSpec rs{};
+  rs.mode = kPrioLex;
+  rs.seed_lo = choice_seed;
+  rs.gated = 1;
+  rs.noise = noise;
+  if (run_event(g, dur, perms, rs, makespans, nullptr, status.data(), nullptr, nullptr, nullptr, err))
+    return 1;
+  for (int64_t k = 0; k < perms; ++k)
+    if (status[k]) makespans[k] = -1;
+  return 0;
+}

@@ -1,0 +1,551 @@
+// TIC / TAC / property kernels (reference properties.cpp:19-109,
+// schedule.cpp:12-71) on the GPU.
+//
+// Design (restated on groups):
+//  * Row aliasing: a non-recv op with exactly one predecessor has that
+//    predecessor's dependency set, so it shares its row. Rows are built in
+//    topological order; each row's recv-dependency bitset (bit c = recv
+//    column c) is the OR of its predecessor rows (plus itself for recvs) —
+//    `closure_*_kernel`, one thread per 32-bit word walking the rows.
+//  * Groups = rows with at least one non-recv member. All members of a group
+//    share cnt = |dep ∩ outstanding|, M = Σ T over it, and the owner (XOR of
+//    columns when cnt == 1), so P and M+ fold over groups with weight
+//    W_g = Σ T(members).
+//  * Column lists col[c] = groups containing recv c (CSR) drive the literal
+//    and amended M+ (min of M over col[c] with cnt ≥ 2 / ≥ 1) and TAC's
+//    retire step (cnt−−, M −= T(c), xr ^= c over col[c]; P[owner] += W_g
+//    when a group drops to one outstanding recv).
+//  * TAC rounds run in one cooperative persistent kernel: amended M+ from
+//    each outstanding recv's direct-successor groups (exact because recvs
+//    are roots in every graph tac() sees), the reference's left fold as a
+//    find-first-beater chain (exact for the non-transitive comparator;
+//    SURVEY A.3), then the retire step. Three grid syncs per round (one
+//    block for small graphs, so they are block barriers there).
+#include <cooperative_groups.h>
+
+#include <algorithm>
+#include <cub/cub.cuh>
+#include <mutex>
+#include <vector>
+
+#include "common.cuh"
+#include "csk.h"
+#include "devgraph.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace tictac_dev {
+namespace {
+
+constexpr int64_t kInf = INT64_MAX;
+
+struct DevArr {
+  void* p = nullptr;
+  DevArr() = default;
+  DevArr(const DevArr&) = delete;
+  ~DevArr() {
+    if (p) cudaFree(p);
+  }
+  template <typename T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+template <typename T>
+int alloc(DevArr& a, size_t count, char* err) {
+  CK(cudaMalloc(&a.p, sizeof(T) * (count ? count : 1)));
+  return 0;
+}
+template <typename T>
+int put(DevArr& a, const std::vector<T>& v, char* err) {
+  CK(cudaMalloc(&a.p, sizeof(T) * (v.empty() ? 1 : v.size())));
+  if (!v.empty()) CK(cudaMemcpy(a.p, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice));
+  return 0;
+}
+
+// Host-side row structure (graph-only; built once per call — O(V+E)).
+struct Rows {
+  int32_t nrows = 0, W = 1;             // W = 32-bit words per row
+  std::vector<int32_t> row_of;          // per op
+  std::vector<int32_t> self_col;        // per row: recv column or -1
+  std::vector<int32_t> pre_off, pre;    // per row: predecessor rows
+  std::vector<int32_t> succ_off, succ;  // per recv column: direct-successor rows (TAC)
+};
+
+void build_rows(const DeviceGraph* g, Rows& rw) {
+  const int32_t n = g->n;
+  std::vector<int32_t> order, missing(n);
+  order.reserve(n);
+  for (int32_t i = 0; i < n; ++i)
+    if ((missing[i] = g->h_pred_off[i + 1] - g->h_pred_off[i]) == 0) order.push_back(i);
+  for (size_t h = 0; h < order.size(); ++h) {
+    const int32_t v = order[h];
+    for (int32_t e = g->h_succ_off[v]; e < g->h_succ_off[v + 1]; ++e)
+      if (--missing[g->h_succ_idx[e]] == 0) order.push_back(g->h_succ_idx[e]);
+  }
+  rw.row_of.assign(n, -1);
+  rw.pre_off.assign(1, 0);
+  std::vector<int32_t> tmp;
+  for (int32_t v : order) {
+    const int32_t np = g->h_pred_off[v + 1] - g->h_pred_off[v];
+    const bool recv = g->h_kind[v] == 1;
+    if (!recv && np == 1) {
+      rw.row_of[v] = rw.row_of[g->h_pred_idx[g->h_pred_off[v]]];
+      continue;
+    }
+    tmp.clear();
+    for (int32_t e = g->h_pred_off[v]; e < g->h_pred_off[v + 1]; ++e)
+      tmp.push_back(rw.row_of[g->h_pred_idx[e]]);
+    std::sort(tmp.begin(), tmp.end());
+    tmp.erase(std::unique(tmp.begin(), tmp.end()), tmp.end());
+    if (!recv && tmp.size() == 1) {  // all preds share one row
+      rw.row_of[v] = tmp[0];
+      continue;
+    }
+    rw.row_of[v] = rw.nrows++;
+    rw.self_col.push_back(recv ? g->h_col[v] : -1);
+    rw.pre.insert(rw.pre.end(), tmp.begin(), tmp.end());
+    rw.pre_off.push_back(static_cast<int32_t>(rw.pre.size()));
+  }
+  rw.W = std::max(1, (g->R + 31) / 32);
+  rw.succ_off.assign(1, 0);
+  for (int32_t c = 0; c < g->R; ++c) {
+    const int32_t r = g->h_recv_ops[c];
+    tmp.clear();
+    for (int32_t e = g->h_succ_off[r]; e < g->h_succ_off[r + 1]; ++e)
+      if (g->h_kind[g->h_succ_idx[e]] != 1) tmp.push_back(rw.row_of[g->h_succ_idx[e]]);
+    std::sort(tmp.begin(), tmp.end());
+    tmp.erase(std::unique(tmp.begin(), tmp.end()), tmp.end());
+    rw.succ.insert(rw.succ.end(), tmp.begin(), tmp.end());
+    rw.succ_off.push_back(static_cast<int32_t>(rw.succ.size()));
+  }
+}
+
+// ---- closure: thread q owns word q of every row; rows in topo order ------
+__global__ void closure_smem_kernel(int32_t nrows, int32_t W, const int32_t* __restrict__ self_col,
+                                    const int32_t* __restrict__ pre_off,
+                                    const int32_t* __restrict__ pre, uint32_t* __restrict__ out) {
+  extern __shared__ uint32_t sm[];
+  for (int q = threadIdx.x; q < W; q += blockDim.x) {
+    for (int32_t k = 0; k < nrows; ++k) {
+      uint32_t w = 0;
+      for (int32_t e = pre_off[k]; e < pre_off[k + 1]; ++e) w |= sm[pre[e] * W + q];
+      const int32_t c = self_col[k];
+      if (c >= 0 && (c >> 5) == q) w |= 1u << (c & 31);
+      sm[k * W + q] = w;
+    }
+  }
+  __syncthreads();
+  for (int64_t i = threadIdx.x; i < static_cast<int64_t>(nrows) * W; i += blockDim.x) out[i] = sm[i];
+}
+
+__global__ void closure_global_kernel(int32_t nrows, int32_t W, const int32_t* __restrict__ self_col,
+                                      const int32_t* __restrict__ pre_off,
+                                      const int32_t* __restrict__ pre, uint32_t* __restrict__ out) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= W) return;
+  for (int32_t k = 0; k < nrows; ++k) {
+    uint32_t w = 0;
+    for (int32_t e = pre_off[k]; e < pre_off[k + 1]; ++e)
+      w |= out[static_cast<int64_t>(pre[e]) * W + q];
+    const int32_t c = self_col[k];
+    if (c >= 0 && (c >> 5) == q) w |= 1u << (c & 31);
+    out[static_cast<int64_t>(k) * W + q] = w;
+  }
+}
+
+// Group weights W_g = Σ T(non-recv member); has[g] marks groups.
+__global__ void weights_kernel(int32_t n, const int32_t* __restrict__ row_of,
+                               const int8_t* __restrict__ kind, const int64_t* __restrict__ dur,
+                               unsigned long long* __restrict__ wsum, int32_t* __restrict__ has) {
+  for (int32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    if (kind[v] == 1) continue;
+    atomicAdd(&wsum[row_of[v]], static_cast<unsigned long long>(dur[v]));
+    has[row_of[v]] = 1;
+  }
+}
+
+// Per row (warp): cnt, M, xr with every recv outstanding; count col lists.
+__global__ void rowstate_kernel(int32_t nrows, int32_t W, const uint32_t* __restrict__ bits,
+                                const int64_t* __restrict__ tcol, const int32_t* __restrict__ has,
+                                int32_t* __restrict__ cnt, int64_t* __restrict__ M,
+                                int32_t* __restrict__ xr, int32_t* __restrict__ colcount) {
+  const int lane = threadIdx.x & 31;
+  const int64_t wid = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t k = wid; k < nrows; k += nw) {
+    int c_cnt = 0, c_xr = 0;
+    int64_t m = 0;
+    for (int q = lane; q < W; q += 32) {
+      uint32_t w = bits[k * W + q];
+      while (w) {
+        const int c = (q << 5) + __ffs(w) - 1;
+        w &= w - 1;
+        ++c_cnt;
+        c_xr ^= c;
+        m += tcol[c];
+        if (has[k]) atomicAdd(&colcount[c], 1);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      c_cnt += __shfl_xor_sync(~0u, c_cnt, o);
+      c_xr ^= __shfl_xor_sync(~0u, c_xr, o);
+      m += __shfl_xor_sync(~0u, m, o);
+    }
+    if (lane == 0) {
+      cnt[k] = c_cnt;
+      M[k] = m;
+      xr[k] = c_xr;
+    }
+  }
+}
+
+__global__ void colfill_kernel(int32_t nrows, int32_t W, const uint32_t* __restrict__ bits,
+                               const int32_t* __restrict__ has, int32_t* __restrict__ cursor,
+                               int32_t* __restrict__ col) {
+  const int lane = threadIdx.x & 31;
+  const int64_t wid = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t k = wid; k < nrows; k += nw) {
+    if (!has[k]) continue;
+    for (int q = lane; q < W; q += 32) {
+      uint32_t w = bits[k * W + q];
+      while (w) {
+        const int c = (q << 5) + __ffs(w) - 1;
+        w &= w - 1;
+        col[atomicAdd(&cursor[c], 1)] = static_cast<int32_t>(k);
+      }
+    }
+  }
+}
+
+// P and M+ with every recv outstanding (properties.cpp:92-107 on groups).
+__global__ void props_kernel(int32_t R, int amended, const int32_t* __restrict__ col_off,
+                             const int32_t* __restrict__ col, const int32_t* __restrict__ cnt,
+                             const int64_t* __restrict__ M, const int32_t* __restrict__ xr,
+                             const unsigned long long* __restrict__ wsum, int64_t* __restrict__ P,
+                             int64_t* __restrict__ Mp) {
+  for (int32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < R; c += gridDim.x * blockDim.x) {
+    int64_t mp = kInf, p = 0;
+    for (int32_t e = col_off[c]; e < col_off[c + 1]; ++e) {
+      const int32_t g = col[e];
+      const int k = cnt[g];
+      if (k >= 2 || (amended && k == 1)) mp = min(mp, M[g]);
+      if (k == 1 && xr[g] == c) p += static_cast<int64_t>(wsum[g]);
+    }
+    P[c] = p;
+    Mp[c] = mp;
+  }
+}
+
+// precedes (schedule.cpp:12-19); kInf = nullopt sorts last.
+__device__ __forceinline__ bool precedes(int a, int64_t ap, int64_t am, int64_t amp, int b, int64_t bp,
+                                         int64_t bm, int64_t bmp) {
+  const int64_t ab = min(bp, am), ba = min(ap, bm);
+  if (ab != ba) return ab < ba;
+  if (amp != bmp) return amp < bmp;
+  return a < b;
+}
+
+struct TacArgs {
+  int32_t R;
+  const int64_t* tcol;      // T(recv column)
+  const int32_t* succ_off;  // direct-successor groups per column
+  const int32_t* succ;
+  const int32_t* col_off;   // groups per column
+  const int32_t* col;
+  const unsigned long long* wsum;
+  int32_t* cnt;
+  int64_t* M;
+  int32_t* xr;
+  int64_t* P;
+  int64_t* mp;
+  uint8_t* out;
+  int32_t* prio;
+};
+
+__device__ __forceinline__ int block_min_int(int v, int* red) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v = min(v, __shfl_xor_sync(~0u, v, o));
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  int r = 0x7fffffff;
+  for (int w = 0; w < (blockDim.x + 31) / 32; ++w) r = min(r, red[w]);
+  return r;
+}
+
+__global__ void __launch_bounds__(1024) tac_kernel(TacArgs a) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ int red[32];
+  const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t nthreads = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int R = a.R;
+  for (int round = 0; round < R; ++round) {
+    // Phase A: amended M+ of every outstanding recv = min M over its
+    // direct-successor groups.
+    for (int64_t c = tid; c < R; c += nthreads) {
+      if (!a.out[c]) continue;
+      int64_t m = kInf;
+      for (int32_t e = a.succ_off[c]; e < a.succ_off[c + 1]; ++e) m = min(m, a.M[a.succ[e]]);
+      a.mp[c] = m;
+    }
+    grid.sync();
+    // Phase B (every block, redundantly): the reference's left fold over
+    // outstanding recvs in id order == find-first-beater chain.
+    int best = 0x7fffffff;
+    for (int c = threadIdx.x; c < R; c += blockDim.x)
+      if (a.out[c]) best = min(best, c);
+    best = block_min_int(best, red);
+    for (;;) {
+      const int64_t bp = a.P[best], bm = a.tcol[best], bmp = a.mp[best];
+      int nxt = 0x7fffffff;
+      for (int c = best + 1 + threadIdx.x; c < R; c += blockDim.x)
+        if (a.out[c] && precedes(c, a.P[c], a.tcol[c], a.mp[c], best, bp, bm, bmp)) {
+          nxt = c;
+          break;
+        }
+      nxt = block_min_int(nxt, red);
+      if (nxt == 0x7fffffff) break;
+      best = nxt;
+    }
+    grid.sync();  // every block has read P/out before anyone retires
+    // Phase C: retire `best`.
+    const int64_t t = a.tcol[best];
+    for (int64_t e = a.col_off[best] + tid; e < a.col_off[best + 1]; e += nthreads) {
+      const int32_t g = a.col[e];
+      const int k = --a.cnt[g];
+      a.M[g] -= t;
+      const int x = (a.xr[g] ^= best);
+      if (k == 1) atomicAdd(reinterpret_cast<unsigned long long*>(&a.P[x]), a.wsum[g]);
+    }
+    if (tid == 0) {
+      a.prio[best] = round;
+      a.out[best] = 0;
+    }
+    grid.sync();
+  }
+}
+
+// Shared setup for properties / tic / tac: rows, closure, group state,
+// column lists. `dur` per op (host).
+struct GroupState {
+  Rows rw;
+  DevArr d_self, d_preoff, d_pre, d_bits, d_rowof, d_wsum, d_has, d_cnt, d_M, d_xr, d_colcount,
+      d_coloff, d_col, d_tcol, d_dur, d_tmp;
+  int64_t nnz = 0;
+};
+
+int group_setup(DeviceGraph* g, const int64_t* dur, GroupState& S, char* err) {
+  if (ensure_device(err)) return 1;
+  build_rows(g, S.rw);
+  const Rows& rw = S.rw;
+  const int32_t nrows = std::max(rw.nrows, 1), W = rw.W;
+  std::vector<int64_t> tcol(std::max(g->R, 1));
+  for (int c = 0; c < g->R; ++c) tcol[c] = dur[g->h_recv_ops[c]];
+  std::vector<int64_t> hd(dur, dur + g->n);
+  if (put(S.d_self, rw.self_col, err) || put(S.d_preoff, rw.pre_off, err) || put(S.d_pre, rw.pre, err) ||
+      put(S.d_rowof, rw.row_of, err) || put(S.d_tcol, tcol, err) || put(S.d_dur, hd, err))
+    return 1;
+  if (alloc<uint32_t>(S.d_bits, static_cast<size_t>(nrows) * W, err) ||
+      alloc<unsigned long long>(S.d_wsum, nrows, err) || alloc<int32_t>(S.d_has, nrows, err) ||
+      alloc<int32_t>(S.d_cnt, nrows, err) || alloc<int64_t>(S.d_M, nrows, err) ||
+      alloc<int32_t>(S.d_xr, nrows, err) || alloc<int32_t>(S.d_colcount, g->R + 1, err) ||
+      alloc<int32_t>(S.d_coloff, g->R + 1, err))
+    return 1;
+  CK(cudaMemset(S.d_wsum.p, 0, 8ull * nrows));
+  CK(cudaMemset(S.d_has.p, 0, 4ull * nrows));
+  CK(cudaMemset(S.d_colcount.p, 0, 4ull * (g->R + 1)));
+  const size_t smem = static_cast<size_t>(rw.nrows) * W * 4;
+  if (rw.nrows > 0) {
+    if (smem <= 200 * 1024) {
+      CK(cudaFuncSetAttribute(closure_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              static_cast<int>(std::max<size_t>(smem, 4))));
+      closure_smem_kernel<<<1, 256, smem>>>(rw.nrows, W, S.d_self.as<int32_t>(),
+                                            S.d_preoff.as<int32_t>(), S.d_pre.as<int32_t>(),
+                                            S.d_bits.as<uint32_t>());
+    } else {
+      closure_global_kernel<<<(W + 127) / 128, 128>>>(rw.nrows, W, S.d_self.as<int32_t>(),
+                                                     S.d_preoff.as<int32_t>(), S.d_pre.as<int32_t>(),
+                                                     S.d_bits.as<uint32_t>());
+    }
+    LAUNCHED();
+    CK(cudaGetLastError());
+  }
+  weights_kernel<<<std::max(1, std::min((g->n + 255) / 256, 1184)), 256>>>(
+      g->n, S.d_rowof.as<int32_t>(), g->kind, S.d_dur.as<int64_t>(), S.d_wsum.as<unsigned long long>(),
+      S.d_has.as<int32_t>());
+  LAUNCHED();
+  const int rblocks = std::max(1, std::min((rw.nrows * 32 + 255) / 256, 2368));
+  if (rw.nrows > 0) {
+    rowstate_kernel<<<rblocks, 256>>>(rw.nrows, W, S.d_bits.as<uint32_t>(), S.d_tcol.as<int64_t>(),
+                                      S.d_has.as<int32_t>(), S.d_cnt.as<int32_t>(),
+                                      S.d_M.as<int64_t>(), S.d_xr.as<int32_t>(),
+                                      S.d_colcount.as<int32_t>());
+    LAUNCHED();
+  }
+  CK(cudaGetLastError());
+  // exclusive scan of column counts -> offsets (R+1 entries)
+  size_t tmp_bytes = 0;
+  CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, S.d_colcount.as<int32_t>(),
+                                   S.d_coloff.as<int32_t>(), g->R + 1));
+  CK(cudaMalloc(&S.d_tmp.p, std::max<size_t>(tmp_bytes, 16)));
+  CK(cub::DeviceScan::ExclusiveSum(S.d_tmp.p, tmp_bytes, S.d_colcount.as<int32_t>(),
+                                   S.d_coloff.as<int32_t>(), g->R + 1));
+  LAUNCHED();
+  int32_t nnz = 0;
+  CK(cudaMemcpy(&nnz, S.d_coloff.as<int32_t>() + g->R, 4, cudaMemcpyDeviceToHost));
+  S.nnz = nnz;
+  if (alloc<int32_t>(S.d_col, nnz, err)) return 1;
+  CK(cudaMemcpy(S.d_colcount.p, S.d_coloff.p, 4ull * (g->R + 1), cudaMemcpyDeviceToDevice));
+  if (rw.nrows > 0) {
+    colfill_kernel<<<rblocks, 256>>>(rw.nrows, W, S.d_bits.as<uint32_t>(), S.d_has.as<int32_t>(),
+                                     S.d_colcount.as<int32_t>(), S.d_col.as<int32_t>());
+    LAUNCHED();
+  }
+  CK(cudaGetLastError());
+  return 0;
+}
+
+__global__ void dense_rank_kernel(int32_t R, const int64_t* __restrict__ sorted_unique, int32_t u,
+                                  const int64_t* __restrict__ vals, int32_t* __restrict__ prio) {
+  for (int32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < R; c += gridDim.x * blockDim.x) {
+    int32_t lo = 0, hi = u;
+    const int64_t v = vals[c];
+    while (lo < hi) {
+      const int32_t mid = (lo + hi) >> 1;
+      if (sorted_unique[mid] < v) lo = mid + 1;
+      else hi = mid;
+    }
+    prio[c] = lo;
+  }
+}
+
+}  // namespace
+}  // namespace tictac_dev
+
+using namespace tictac_dev;
+
+extern "C" int csk_properties(DeviceGraph* g, const int64_t* dur, int mode, uint64_t* dep_bits,
+                              int64_t* M, int64_t* P, int64_t* Mplus, char* err) {
+  GroupState S;
+  if (group_setup(g, dur, S, err)) return 1;
+  const int R = g->R;
+  DevArr d_P, d_Mp;
+  if (alloc<int64_t>(d_P, R, err) || alloc<int64_t>(d_Mp, R, err)) return 1;
+  if (R > 0) {
+    props_kernel<<<std::max(1, std::min((R + 255) / 256, 1184)), 256>>>(
+        R, mode, S.d_coloff.as<int32_t>(), S.d_col.as<int32_t>(), S.d_cnt.as<int32_t>(),
+        S.d_M.as<int64_t>(), S.d_xr.as<int32_t>(), S.d_wsum.as<unsigned long long>(),
+        d_P.as<int64_t>(), d_Mp.as<int64_t>());
+    LAUNCHED();
+    CK(cudaGetLastError());
+    CK(cudaMemcpy(P, d_P.p, 8ull * R, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(Mplus, d_Mp.p, 8ull * R, cudaMemcpyDeviceToHost));
+  }
+  // per-op rows back to the host formatter
+  const int W = S.rw.W, w64 = std::max(1, (R + 63) / 64);
+  std::vector<uint32_t> bits(static_cast<size_t>(std::max(S.rw.nrows, 1)) * W);
+  std::vector<int64_t> rowM(std::max(S.rw.nrows, 1));
+  if (S.rw.nrows > 0) {
+    CK(cudaMemcpy(bits.data(), S.d_bits.p, 4ull * S.rw.nrows * W, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(rowM.data(), S.d_M.p, 8ull * S.rw.nrows, cudaMemcpyDeviceToHost));
+  }
+  for (int32_t v = 0; v < g->n; ++v) {
+    const int32_t k = S.rw.row_of[v];
+    uint64_t* dst = dep_bits + static_cast<size_t>(v) * w64;
+    for (int q = 0; q < w64; ++q) dst[q] = 0;
+    for (int q = 0; q < W; ++q)
+      dst[q >> 1] |= static_cast<uint64_t>(bits[static_cast<size_t>(k) * W + q]) << (32 * (q & 1));
+    M[v] = rowM[k];
+  }
+  return 0;
+}
+
+extern "C" int csk_tic(DeviceGraph* g, int mode, int32_t* prio, int* total, char* err) {
+  const int R = g->R;
+  *total = 1;
+  if (R == 0) return 0;
+  std::vector<int64_t> unit(g->n);
+  for (int32_t v = 0; v < g->n; ++v) unit[v] = g->h_kind[v] == 1 ? 1 : 0;  // general oracle
+  GroupState S;
+  if (group_setup(g, unit.data(), S, err)) return 1;
+  DevArr d_P, d_Mp, d_sorted, d_unique, d_nu, d_tmp, d_prio;
+  if (alloc<int64_t>(d_P, R, err) || alloc<int64_t>(d_Mp, R, err) || alloc<int64_t>(d_sorted, R, err) ||
+      alloc<int64_t>(d_unique, R, err) || alloc<int32_t>(d_nu, 1, err) || alloc<int32_t>(d_prio, R, err))
+    return 1;
+  props_kernel<<<std::max(1, std::min((R + 255) / 256, 1184)), 256>>>(
+      R, mode, S.d_coloff.as<int32_t>(), S.d_col.as<int32_t>(), S.d_cnt.as<int32_t>(),
+      S.d_M.as<int64_t>(), S.d_xr.as<int32_t>(), S.d_wsum.as<unsigned long long>(), d_P.as<int64_t>(),
+      d_Mp.as<int64_t>());
+  LAUNCHED();
+  // dense rank: radix sort, unique, binary search (schedule.cpp:27-40)
+  size_t b1 = 0, b2 = 0;
+  CK(cub::DeviceRadixSort::SortKeys(nullptr, b1, d_Mp.as<int64_t>(), d_sorted.as<int64_t>(), R));
+  CK(cub::DeviceSelect::Unique(nullptr, b2, d_sorted.as<int64_t>(), d_unique.as<int64_t>(),
+                               d_nu.as<int32_t>(), R));
+  CK(cudaMalloc(&d_tmp.p, std::max<size_t>(std::max(b1, b2), 16)));
+  CK(cub::DeviceRadixSort::SortKeys(d_tmp.p, b1, d_Mp.as<int64_t>(), d_sorted.as<int64_t>(), R));
+  CK(cub::DeviceSelect::Unique(d_tmp.p, b2, d_sorted.as<int64_t>(), d_unique.as<int64_t>(),
+                               d_nu.as<int32_t>(), R));
+  LAUNCHED();
+  LAUNCHED();
+  int32_t u = 0;
+  CK(cudaMemcpy(&u, d_nu.p, 4, cudaMemcpyDeviceToHost));
+  dense_rank_kernel<<<std::max(1, std::min((R + 255) / 256, 1184)), 256>>>(
+      R, d_unique.as<int64_t>(), u, d_Mp.as<int64_t>(), d_prio.as<int32_t>());
+  LAUNCHED();
+  CK(cudaGetLastError());
+  CK(cudaMemcpy(prio, d_prio.p, 4ull * R, cudaMemcpyDeviceToHost));
+  *total = u == R;
+  return 0;
+}
+
+extern "C" int csk_tac(DeviceGraph* g, const int64_t* dur, int32_t* prio, char* err) {
+  const int R = g->R;
+  if (R == 0) return 0;
+  GroupState S;
+  if (group_setup(g, dur, S, err)) return 1;
+  DevArr d_P, d_Mp, d_out, d_prio, d_succoff, d_succ;
+  if (alloc<int64_t>(d_P, R, err) || alloc<int64_t>(d_Mp, R, err) || alloc<uint8_t>(d_out, R, err) ||
+      alloc<int32_t>(d_prio, R, err) || put(d_succoff, S.rw.succ_off, err) || put(d_succ, S.rw.succ, err))
+    return 1;
+  CK(cudaMemset(d_out.p, 1, R));
+  // initial P (amended M+ is recomputed inside the rounds)
+  props_kernel<<<std::max(1, std::min((R + 255) / 256, 1184)), 256>>>(
+      R, 1, S.d_coloff.as<int32_t>(), S.d_col.as<int32_t>(), S.d_cnt.as<int32_t>(), S.d_M.as<int64_t>(),
+      S.d_xr.as<int32_t>(), S.d_wsum.as<unsigned long long>(), d_P.as<int64_t>(), d_Mp.as<int64_t>());
+  LAUNCHED();
+  CK(cudaGetLastError());
+  TacArgs a{R,
+            S.d_tcol.as<int64_t>(),
+            d_succoff.as<int32_t>(),
+            d_succ.as<int32_t>(),
+            S.d_coloff.as<int32_t>(),
+            S.d_col.as<int32_t>(),
+            S.d_wsum.as<unsigned long long>(),
+            S.d_cnt.as<int32_t>(),
+            S.d_M.as<int64_t>(),
+            S.d_xr.as<int32_t>(),
+            d_P.as<int64_t>(),
+            d_Mp.as<int64_t>(),
+            d_out.as<uint8_t>(),
+            d_prio.as<int32_t>()};
+  // One block is latency-optimal until the per-round work (retire list and
+  // candidate scan) outgrows it; then spread over the SMs.
+  int dev = 0, sms = 148, per_sm = 1;
+  CK(cudaGetDevice(&dev));
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tac_kernel, 1024, 0));
+  const int64_t work = S.nnz / std::max(R, 1) + R;
+  int blocks = work > 65536 ? std::min<int64_t>(sms * std::max(per_sm, 1), (work + 8191) / 8192) : 1;
+  blocks = std::max(blocks, 1);
+  void* args[] = {&a};
+  CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(tac_kernel), blocks, 1024, args, 0, nullptr));
+  LAUNCHED();
+  CK(cudaGetLastError());
+  CK(cudaMemcpy(prio, d_prio.p, 4ull * R, cudaMemcpyDeviceToHost));
+  return 0;
+}

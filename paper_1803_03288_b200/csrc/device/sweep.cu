@@ -1,0 +1,435 @@
+// Batched random-order sweep — the throughput kernel (SURVEY §8a rows
+// a8/a10/a11/a12, Appendix A.2).
+//
+// One thread owns one seed end to end: the reference's random_schedule
+// (mt19937_64(seed) + bounded() + Fisher–Yates from the top, rng.hpp:21-46,
+// schedule.cpp:73-84) and the closed-form makespan of a gated, fully
+// prioritized run, fused so that nothing per-ordering touches HBM.
+//
+// Closed form on "chain-class" graphs (host analysis in csrc/host/sweep.cpp):
+// group compute ops by their recv-ancestor set; when these sets are nested
+// (C_0 ⊂ C_1 ⊂ … ⊂ C_{nc-1}) a compute class j is released when the last of
+// its recvs completes, i.e. at position lp(C_j) = max{k : first[perm[k]] ≤ j}.
+// With G_k = min_{k' ≥ k} first[perm[k']] (a suffix minimum), the single-core
+// earliest-release-date pass gives
+//     T_cpu = max over k with G_k < G_{k+1} of  c_k + S(G_k),
+// c_k = completion of the k-th transfer = Ctot − Σ_{k' > k} d, S(j) = Σ weights
+// of classes ≥ j. Every term is available right-to-left, and Fisher–Yates
+// finalises positions right-to-left, so each draw is folded the moment its
+// slot is final: O(R) work, O(R) bytes of shared memory per seed, no arrays.
+//   worker graph:   m   = max(T_cpu, Ctot)
+//   cluster worker: m_w = max(T_cpu, max(Ctot, T_cpu) + Σ sends)
+// The shuffle array lives in shared memory as bytes (R ≤ 256) or halves,
+// laid out [k/4][thread] so every lane always hits its own bank.
+#include <algorithm>
+#include <vector>
+
+#include "common.cuh"
+#include "csk.h"
+
+namespace tictac_dev {
+namespace {
+
+constexpr int kSweepThreads = 128;
+constexpr int kBins = 1000;
+
+struct ChainArgs {
+  int W, R, stride;  // workers, recvs per worker, pwsuf stride (nc+1)
+  int nc;
+  const uint2* tab;         // [W][R] {first class, duration}
+  const int64_t* pwsuf;     // [W][stride]
+  const int64_t* ctot;      // [W]
+  const int64_t* send_tot;  // [W]
+  int cluster;
+  const uint64_t* lim;  // [R+1] bounded() constants
+  const uint64_t* mag;
+  uint64_t seed_lo, key_base;
+  int64_t count;
+  int64_t U, L;
+  int do_e;
+  const int32_t* orders;  // explicit orders mode (W == 1)
+  int64_t* makespans;
+  int64_t* worker_ms;
+  unsigned long long* i64;
+  double* f64;
+};
+
+// Rare path: the stream needs output >= 311 (only after ≥ 312-R+1
+// rejections of bounded(), probability < 1e-15) or R > 312.
+__device__ __noinline__ uint64_t mt_output_at(uint64_t seed, int idx) {
+  uint64_t st[312];
+  MtFull m{st, 0};
+  m.seed(seed);
+  uint64_t v = 0;
+  for (int k = 0; k <= idx; ++k) v = m.next();
+  return v;
+}
+
+struct PermStream {
+  MtLazy lz;
+  __device__ __forceinline__ void init(uint64_t s) { lz.init(s); }
+  __device__ __forceinline__ uint64_t next() {
+    if (!lz.exhausted()) return lz.next_raw();
+    return mt_output_at(lz.seed, lz.i++);
+  }
+};
+
+template <typename T>
+struct Items;  // shared-memory shuffle array, [k / per_word][thread]
+
+template <>
+struct Items<uint8_t> {
+  uint32_t* base;
+  __device__ __forceinline__ uint8_t* at(int k) const {
+    return reinterpret_cast<uint8_t*>(base + (k >> 2) * kSweepThreads) + (k & 3);
+  }
+  __device__ __forceinline__ void init(int R) const {
+    for (int q = 0; q < (R + 3) >> 2; ++q)
+      base[q * kSweepThreads] = 0x03020100u + 0x04040404u * static_cast<uint32_t>(q);
+  }
+};
+template <>
+struct Items<uint16_t> {
+  uint32_t* base;
+  __device__ __forceinline__ uint16_t* at(int k) const {
+    return reinterpret_cast<uint16_t*>(base + (k >> 1) * kSweepThreads) + (k & 1);
+  }
+  __device__ __forceinline__ void init(int R) const {
+    for (int q = 0; q < (R + 1) >> 1; ++q)
+      base[q * kSweepThreads] = (static_cast<uint32_t>(2 * q + 1) << 16) | static_cast<uint32_t>(2 * q);
+  }
+};
+
+struct Fold {  // right-to-left suffix-min fold of one ordering
+  int G;
+  int64_t suffix, best;
+  __device__ __forceinline__ void add(uint2 e, int64_t ctot, const int64_t* pw) {
+    const int gk = min(static_cast<int>(e.x), G);
+    if (gk < G) best = max(best, ctot - suffix + pw[gk]);
+    G = gk;
+    suffix += e.y;
+  }
+};
+
+template <typename T, bool kOrders>
+__global__ void __launch_bounds__(kSweepThreads) chain_sweep_kernel(ChainArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int R = a.R, W = a.W;
+  uint2* s_tab = reinterpret_cast<uint2*>(smem);
+  int64_t* s_pw = reinterpret_cast<int64_t*>(s_tab + W * R);
+  int* s_hist = reinterpret_cast<int*>(s_pw + W * a.stride);
+  int* s_shist = s_hist + kBins;
+  uint32_t* s_items = reinterpret_cast<uint32_t*>(s_shist + kBins);
+  for (int k = threadIdx.x; k < W * R; k += blockDim.x) s_tab[k] = a.tab[k];
+  for (int k = threadIdx.x; k < W * a.stride; k += blockDim.x) s_pw[k] = a.pwsuf[k];
+  for (int k = threadIdx.x; k < 2 * kBins; k += blockDim.x) s_hist[k] = 0;
+  __syncthreads();
+  const Items<T> items{s_items + threadIdx.x};
+
+  unsigned long long kmin = ~0ULL, kmax = 0;
+  long long msum = 0, cnt = 0;
+  double sq = 0.0, ssum = 0.0;
+  const int64_t nthreads = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; idx < a.count;
+       idx += nthreads) {
+    const uint64_t seed = a.seed_lo + static_cast<uint64_t>(idx);
+    int64_t hi = 0, lo = INT64_MAX;
+    for (int w = 0; w < W; ++w) {
+      const uint2* tab = s_tab + w * R;
+      const int64_t* pw = s_pw + w * a.stride;
+      const int64_t ctot = a.ctot[w];
+      Fold f{a.nc, 0, -1};
+      if constexpr (kOrders) {
+        const int32_t* o = a.orders + idx * R;
+        for (int k = R - 1; k >= 0; --k) f.add(tab[o[k]], ctot, pw);
+      } else {
+        const uint64_t ws = a.cluster ? splitmix64(seed ^ (kPhi * static_cast<uint64_t>(w + 1))) : seed;
+        PermStream rng;
+        rng.init(ws);
+        items.init(R);
+        for (int i = R; i > 1; --i) {
+          const uint64_t lim = a.lim[i], mag = a.mag[i];
+          uint64_t v = rng.next();
+          while (v > lim) v = rng.next();
+          const int j = static_cast<int>(fastmod(v, static_cast<uint64_t>(i), mag));
+          T* pj = items.at(j);
+          const T x = *pj;
+          *pj = *items.at(i - 1);
+          f.add(tab[x], ctot, pw);  // slot i-1 is final: it holds x
+        }
+        if (R >= 1) f.add(tab[*items.at(0)], ctot, pw);
+      }
+      if (f.G > 0) f.best = max(f.best, pw[0]);  // bin 0: computes needing no recv
+      const int64_t tcpu = f.best < 0 ? 0 : f.best;
+      const int64_t mw = a.cluster ? max(tcpu, max(ctot, tcpu) + a.send_tot[w]) : max(tcpu, ctot);
+      if (a.worker_ms) a.worker_ms[idx * W + w] = mw;
+      hi = max(hi, mw);
+      lo = min(lo, mw);
+    }
+    const int64_t m = hi;  // worker graph: the makespan; cluster: iteration time
+    if (a.makespans) a.makespans[idx] = m;
+    const unsigned long long off = seed - a.key_base;
+    kmin = min(kmin, (static_cast<unsigned long long>(m) << 26) | off);
+    kmax = max(kmax, (static_cast<unsigned long long>(m) << 26) | ((1ULL << 26) - 1 - off));
+    msum += m;
+    ++cnt;
+    sq += static_cast<double>(m) * static_cast<double>(m);
+    if (a.do_e) {
+      int bin = static_cast<int>(floor(1000.0 * static_cast<double>(a.U - m) /
+                                       static_cast<double>(a.U - a.L)));
+      atomicAdd(&s_hist[min(max(bin, 0), kBins - 1)], 1);
+    }
+    if (a.cluster) {
+      int bin = 0;
+      if (hi > 0) {
+        const double fr = static_cast<double>(hi - lo) / static_cast<double>(hi);
+        ssum += fr;
+        bin = min(static_cast<int>(floor(1000.0 * static_cast<double>(hi - lo) / static_cast<double>(hi))),
+                  kBins - 1);
+      }
+      atomicAdd(&s_shist[bin], 1);
+    }
+  }
+  // warp then block reduction, one set of global atomics per block
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    kmin = min(kmin, __shfl_xor_sync(~0u, kmin, o));
+    kmax = max(kmax, __shfl_xor_sync(~0u, kmax, o));
+    msum += __shfl_xor_sync(~0u, msum, o);
+    cnt += __shfl_xor_sync(~0u, cnt, o);
+    sq += __shfl_xor_sync(~0u, sq, o);
+    ssum += __shfl_xor_sync(~0u, ssum, o);
+  }
+  if ((threadIdx.x & 31) == 0 && cnt > 0) {
+    atomicMin(&a.i64[0], kmin);
+    atomicMax(&a.i64[1], kmax);
+    atomicAdd(&a.i64[2], static_cast<unsigned long long>(msum));
+    atomicAdd(&a.i64[3], static_cast<unsigned long long>(cnt));
+    atomicAdd(&a.f64[0], sq);
+    atomicAdd(&a.f64[1], ssum);
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < 2 * kBins; k += blockDim.x)
+    if (s_hist[k]) atomicAdd(&a.i64[8 + k], static_cast<unsigned long long>(s_hist[k]));
+}
+
+__global__ void reset_kernel(unsigned long long* i64, double* f64) {
+  for (int k = threadIdx.x; k < 2008; k += blockDim.x) i64[k] = k == 0 ? ~0ULL : 0ULL;
+  if (threadIdx.x < 2) f64[threadIdx.x] = 0.0;
+}
+
+__global__ void random_orders_kernel(int R, int S, const uint64_t* __restrict__ seeds,
+                                     const uint64_t* __restrict__ lim, const uint64_t* __restrict__ mag,
+                                     int32_t* __restrict__ perms) {
+  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < S; s += gridDim.x * blockDim.x) {
+    int32_t* p = perms + static_cast<int64_t>(s) * R;
+    for (int k = 0; k < R; ++k) p[k] = k;
+    PermStream rng;
+    rng.init(seeds[s]);
+    for (int i = R; i > 1; --i) {
+      uint64_t v = rng.next(), j;
+      if (i < 4096) {
+        while (v > lim[i]) v = rng.next();
+        j = fastmod(v, static_cast<uint64_t>(i), mag[i]);
+      } else {
+        const uint64_t n = static_cast<uint64_t>(i);
+        const uint64_t limit = UINT64_MAX - (UINT64_MAX % n + 1) % n;
+        while (v > limit) v = rng.next();
+        j = v % n;
+      }
+      const int32_t t = p[i - 1];
+      p[i - 1] = p[j];
+      p[j] = t;
+    }
+  }
+}
+
+}  // namespace
+}  // namespace tictac_dev
+
+using namespace tictac_dev;
+
+struct SweepPlan {
+  int W = 1, R = 0, nc = 0, cluster = 0, stride = 1;
+  int64_t U = 0, L = 0;
+  void *tab = nullptr, *pwsuf = nullptr, *ctot = nullptr, *send = nullptr, *lim = nullptr, *mag = nullptr;
+  size_t smem = 0;
+  int blocks = 0;
+};
+
+extern "C" SweepPlan* csk_sweep_plan(int32_t W, int32_t R, int32_t nc, const int64_t* d,
+                                     const int32_t* first, const int64_t* pwsuf,
+                                     const int64_t* send_total, int cluster, int64_t U, int64_t L,
+                                     char* err) {
+  if (ensure_device(err)) return nullptr;
+  auto* p = new SweepPlan();
+  p->W = W;
+  p->R = R;
+  p->nc = nc;
+  p->cluster = cluster;
+  p->stride = nc + 1;
+  p->U = U;
+  p->L = L;
+  std::vector<uint2> tab(static_cast<size_t>(W) * R);
+  std::vector<int64_t> ctot(W, 0);
+  for (int w = 0; w < W; ++w)
+    for (int c = 0; c < R; ++c) {
+      tab[w * R + c] = make_uint2(static_cast<unsigned>(first[w * R + c]),
+                                  static_cast<unsigned>(d[w * R + c]));
+      ctot[w] += d[w * R + c];
+    }
+  std::vector<uint64_t> lim(R + 2), mag(R + 2);
+  for (int n = 0; n <= R + 1; ++n) bounded_consts(static_cast<uint64_t>(n), &lim[n], &mag[n]);
+  auto up = [&](void** dst, const void* src, size_t bytes) {
+    if (cudaMalloc(dst, bytes ? bytes : 8) != cudaSuccess) return false;
+    return bytes == 0 || cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice) == cudaSuccess;
+  };
+  if (!up(&p->tab, tab.data(), tab.size() * sizeof(uint2)) ||
+      !up(&p->pwsuf, pwsuf, sizeof(int64_t) * W * p->stride) ||
+      !up(&p->ctot, ctot.data(), sizeof(int64_t) * W) ||
+      !up(&p->send, send_total, sizeof(int64_t) * W) ||
+      !up(&p->lim, lim.data(), sizeof(uint64_t) * lim.size()) ||
+      !up(&p->mag, mag.data(), sizeof(uint64_t) * mag.size())) {
+    std::snprintf(err, 256, "CUDA allocation for the sweep plan failed");
+    csk_sweep_plan_free(p);
+    return nullptr;
+  }
+  const int per_word = R <= 256 ? 4 : 2;
+  p->smem = sizeof(uint2) * W * R + sizeof(int64_t) * W * p->stride + sizeof(int) * 2 * kBins +
+            sizeof(uint32_t) * kSweepThreads * ((R + per_word - 1) / per_word + 1);
+  int dev = 0, sms = 148, occ = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const void* fn = R <= 256 ? reinterpret_cast<const void*>(chain_sweep_kernel<uint8_t, false>)
+                            : reinterpret_cast<const void*>(chain_sweep_kernel<uint16_t, false>);
+  if (p->smem > 48 * 1024) {
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(p->smem));
+    cudaFuncSetAttribute(reinterpret_cast<const void*>(chain_sweep_kernel<uint8_t, true>),
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(p->smem));
+  }
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kSweepThreads, p->smem);
+  if (occ < 1) {
+    std::snprintf(err, 256, "sweep plan needs %zu bytes of shared memory per block", p->smem);
+    csk_sweep_plan_free(p);
+    return nullptr;
+  }
+  p->blocks = sms * occ;
+  return p;
+}
+
+extern "C" void csk_sweep_plan_free(SweepPlan* p) {
+  if (!p) return;
+  void* ptrs[] = {p->tab, p->pwsuf, p->ctot, p->send, p->lim, p->mag};
+  for (void* q : ptrs)
+    if (q) cudaFree(q);
+  delete p;
+}
+
+extern "C" int csk_sweep_reset(SweepPlan*, void* stream, int64_t* d_i64, double* d_f64, char* err) {
+  reset_kernel<<<1, 1024, 0, static_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<unsigned long long*>(d_i64), d_f64);
+  LAUNCHED();
+  CK(cudaGetLastError());
+  return 0;
+}
+
+static ChainArgs chain_args(SweepPlan* p) {
+  ChainArgs a{};
+  a.W = p->W;
+  a.R = p->R;
+  a.stride = p->stride;
+  a.nc = p->nc;
+  a.tab = static_cast<const uint2*>(p->tab);
+  a.pwsuf = static_cast<const int64_t*>(p->pwsuf);
+  a.ctot = static_cast<const int64_t*>(p->ctot);
+  a.send_tot = static_cast<const int64_t*>(p->send);
+  a.cluster = p->cluster;
+  a.lim = static_cast<const uint64_t*>(p->lim);
+  a.mag = static_cast<const uint64_t*>(p->mag);
+  a.U = p->U;
+  a.L = p->L;
+  a.do_e = !p->cluster && p->U != p->L;
+  return a;
+}
+
+extern "C" int csk_sweep_run(SweepPlan* p, uint64_t seed_lo, int64_t count, uint64_t key_base,
+                             void* stream, int64_t* d_makespans, int64_t* d_worker_makespans,
+                             int64_t* d_i64, double* d_f64, char* err) {
+  if (count <= 0) return 0;
+  ChainArgs a = chain_args(p);
+  a.seed_lo = seed_lo;
+  a.key_base = key_base;
+  a.count = count;
+  a.makespans = d_makespans;
+  a.worker_ms = d_worker_makespans;
+  a.i64 = reinterpret_cast<unsigned long long*>(d_i64);
+  a.f64 = d_f64;
+  const int64_t need = (count + kSweepThreads - 1) / kSweepThreads;
+  const int blocks = static_cast<int>(std::min<int64_t>(p->blocks, need));
+  auto st = static_cast<cudaStream_t>(stream);
+  if (p->R <= 256)
+    chain_sweep_kernel<uint8_t, false><<<blocks, kSweepThreads, p->smem, st>>>(a);
+  else
+    chain_sweep_kernel<uint16_t, false><<<blocks, kSweepThreads, p->smem, st>>>(a);
+  LAUNCHED();
+  CK(cudaGetLastError());
+  return 0;
+}
+
+extern "C" int csk_sweep_orders(SweepPlan* p, const int32_t* d_orders, int64_t n, void* stream,
+                                int64_t* d_makespans, char* err) {
+  if (p->W != 1) {
+    std::snprintf(err, 256, "explicit orders need a worker graph plan");
+    return 4;
+  }
+  if (n <= 0) return 0;
+  void *i64 = nullptr, *f64 = nullptr;
+  CK(cudaMalloc(&i64, 8 * 2008));
+  CK(cudaMalloc(&f64, 16));
+  auto st = static_cast<cudaStream_t>(stream);
+  reset_kernel<<<1, 1024, 0, st>>>(static_cast<unsigned long long*>(i64), static_cast<double*>(f64));
+  LAUNCHED();
+  ChainArgs a = chain_args(p);
+  a.count = n;
+  a.orders = d_orders;
+  a.makespans = d_makespans;
+  a.i64 = static_cast<unsigned long long*>(i64);
+  a.f64 = static_cast<double*>(f64);
+  a.do_e = 0;
+  const int blocks = static_cast<int>(std::min<int64_t>(p->blocks, (n + kSweepThreads - 1) / kSweepThreads));
+  chain_sweep_kernel<uint8_t, true><<<blocks, kSweepThreads, p->smem, st>>>(a);
+  LAUNCHED();
+  cudaError_t e = cudaGetLastError();
+  cudaStreamSynchronize(st);
+  cudaFree(i64);
+  cudaFree(f64);
+  CK(e);
+  return 0;
+}
+
+extern "C" int csk_random_orders(int32_t R, int32_t S, const uint64_t* seeds, int32_t* perms, char* err) {
+  if (ensure_device(err)) return 1;
+  if (R <= 0 || S <= 0) return 0;
+  std::vector<uint64_t> lim(4096), mag(4096);
+  for (uint64_t k = 0; k < 4096; ++k) bounded_consts(k, &lim[k], &mag[k]);
+  void *d_seeds = nullptr, *d_lim = nullptr, *d_mag = nullptr, *d_perm = nullptr;
+  CK(cudaMalloc(&d_seeds, 8ull * S));
+  CK(cudaMalloc(&d_lim, 8ull * lim.size()));
+  CK(cudaMalloc(&d_mag, 8ull * mag.size()));
+  CK(cudaMalloc(&d_perm, 4ull * R * S));
+  CK(cudaMemcpy(d_seeds, seeds, 8ull * S, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(d_lim, lim.data(), 8ull * lim.size(), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(d_mag, mag.data(), 8ull * mag.size(), cudaMemcpyHostToDevice));
+  random_orders_kernel<<<std::max(1, std::min((S + 127) / 128, 1184)), 128>>>(
+      R, S, static_cast<uint64_t*>(d_seeds), static_cast<uint64_t*>(d_lim),
+      static_cast<uint64_t*>(d_mag), static_cast<int32_t*>(d_perm));
+  LAUNCHED();
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaMemcpy(perms, d_perm, 4ull * R * S, cudaMemcpyDeviceToHost);
+  cudaFree(d_seeds);
+  cudaFree(d_lim);
+  cudaFree(d_mag);
+  cudaFree(d_perm);
+  CK(e);
+  return 0;
+}

@@ -1,0 +1,598 @@
+// The drop-in C ABI (include/commsched.h): the reference's 40 cs_* entry
+// points with identical signatures, status codes, ownership and
+// thread-local error messages (reference capi.cpp:21-424), plus the batched
+// extensions. Compute entry points run on the GPU through ../device/csk.h.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <string>
+
+#include "../../../include/commsched.h"
+#include "../device/csk.h"
+#include "core.hpp"
+#include "sweep.hpp"
+
+using namespace tictac;
+
+struct cs_graph {
+  std::shared_ptr<Graph> g;
+};
+struct cs_oracle {
+  TimeOracle o;
+};
+struct cs_schedule {
+  Schedule s;
+};
+struct cs_report {
+  Report r;
+};
+struct cs_sweep_plan {
+  std::unique_ptr<SweepCtx> ctx;
+};
+
+namespace {
+
+thread_local std::string t_error;
+
+template <typename F>
+int guarded(F&& f) {  // capi.cpp:39-52: exceptions -> status + message
+  try {
+    t_error.clear();
+    f();
+    return CS_OK;
+  } catch (const Failure& e) {
+    t_error = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    t_error = e.what();
+    return CS_ERR_INTERNAL;
+  }
+}
+
+void need(const void* p, const char* what) {
+  if (!p) fail(kValidation, std::string("null argument: ") + what);
+}
+
+char* dup(const std::string& s) {
+  char* out = new char[s.size() + 1];
+  std::memcpy(out, s.c_str(), s.size() + 1);
+  return out;
+}
+
+Policy policy_of(const cs_sim_policy* p) {  // capi.cpp:64-73 defaults
+  Policy q;
+  if (p) {
+    q.gated = p->counter_gate != 0;
+    q.choice_seed = p->choice_seed;
+    q.noise = p->reorder_noise;
+  }
+  return q;
+}
+
+}  // namespace
+
+#pragma GCC visibility push(default)
+extern "C" {
+
+int cs_graph_parse(const char* json_text, cs_graph** out) {
+  return guarded([&] {
+    need(json_text, "json_text");
+    need(out, "out");
+    *out = new cs_graph{Graph::parse(json_text)};
+  });
+}
+
+int cs_graph_serialize(const cs_graph* g, char** out_json) {
+  return guarded([&] {
+    need(g, "graph");
+    need(out_json, "out_json");
+    *out_json = dup(g->g->serialize());
+  });
+}
+
+int cs_graph_generate(const char* shape, int layers, int params_per_layer,
+                      const char* comm_comp_ratio, uint64_t seed, cs_graph** out) {
+  return guarded([&] {
+    need(shape, "shape");
+    need(comm_comp_ratio, "comm_comp_ratio");
+    need(out, "out");
+    *out = new cs_graph{generate_synthetic(shape, layers, params_per_layer, comm_comp_ratio, seed)};
+  });
+}
+
+int cs_graph_expand(const cs_graph* worker, int n_workers, int n_ps, int64_t ps_op_time_us,
+                    cs_graph** out) {
+  return guarded([&] {
+    need(worker, "worker");
+    need(out, "out");
+    *out = new cs_graph{expand_mr(*worker->g, n_workers, n_ps, ps_op_time_us)};
+  });
+}
+
+int cs_graph_name(const cs_graph* g, char** out) {
+  return guarded([&] {
+    need(g, "graph");
+    need(out, "out");
+    *out = dup(g->g->name());
+  });
+}
+
+int cs_graph_op_count(const cs_graph* g, int64_t* out) {
+  return guarded([&] {
+    need(g, "graph");
+    need(out, "out");
+    *out = g->g->n();
+  });
+}
+
+int cs_graph_edge_count(const cs_graph* g, int64_t* out) {
+  return guarded([&] {
+    need(g, "graph");
+    need(out, "out");
+    *out = static_cast<int64_t>(g->g->edges().size());
+  });
+}
+
+int cs_graph_recv_count(const cs_graph* g, int64_t* out) {
+  return guarded([&] {
+    need(g, "graph");
+    need(out, "out");
+    *out = static_cast<int64_t>(g->g->recv_ops().size());
+  });
+}
+
+int cs_graph_is_cluster(const cs_graph* g, int* out) {
+  return guarded([&] {
+    need(g, "graph");
+    need(out, "out");
+    *out = g->g->cluster() ? 1 : 0;
+  });
+}
+
+int cs_graph_topo_order(const cs_graph* g, char** out_json) {
+  return guarded([&] {
+    need(g, "graph");
+    need(out_json, "out_json");
+    *out_json = dup(dump_doc(Json(g->g->topo_order())));
+  });
+}
+
+int cs_graph_worker_devices(const cs_graph* g, char** out_json) {
+  return guarded([&] {
+    need(g, "graph");
+    need(out_json, "out_json");
+    *out_json = dup(dump_doc(Json(g->g->worker_devices())));
+  });
+}
+
+int cs_graph_worker_partition(const cs_graph* g, const char* device, cs_graph** out) {
+  return guarded([&] {
+    need(g, "graph");
+    need(device, "device");
+    need(out, "out");
+    *out = new cs_graph{g->g->partition(device)};
+  });
+}
+
+void cs_graph_free(cs_graph* g) { delete g; }
+
+int cs_oracle_declared(const cs_graph* g, cs_oracle** out) {
+  return guarded([&] {
+    need(g, "graph");
+    need(out, "out");
+    *out = new cs_oracle{TimeOracle::declared(*g->g)};
+  });
+}
+
+int cs_oracle_general(const cs_graph* g, cs_oracle** out) {
+  return guarded([&] {
+    need(g, "graph");
+    need(out, "out");
+    *out = new cs_oracle{TimeOracle::general(*g->g)};
+  });
+}
+
+int cs_oracle_from_traces(const cs_graph* g, const char* trace_jsonl, cs_oracle** out) {
+  return guarded([&] {
+    need(g, "graph");
+    need(trace_jsonl, "trace_jsonl");
+    need(out, "out");
+    *out = new cs_oracle{TimeOracle::traces(*g->g, trace_jsonl)};
+  });
+}
+
+int cs_oracle_bandwidth(const cs_graph* g, int64_t bytes_per_us, cs_oracle** out) {
+  return guarded([&] {
+    need(g, "graph");
+    need(out, "out");
+    *out = new cs_oracle{TimeOracle::bandwidth(*g->g, bytes_per_us)};
+  });
+}
+
+int cs_oracle_json(const cs_oracle* o, char** out_json) {
+  return guarded([&] {
+    need(o, "oracle");
+    need(out_json, "out_json");
+    *out_json = dup(dump_doc(o->o.to_json()));
+  });
+}
+
+void cs_oracle_free(cs_oracle* o) { delete o; }
+
+int cs_properties_json(const cs_graph* g, const cs_oracle* o, const char* mode, char** out_json) {
+  return guarded([&] {
+    need(g, "graph");
+    need(o, "oracle");
+    need(mode, "mode");
+    need(out_json, "out_json");
+    const PropMode m = prop_mode(mode);
+    *out_json = dup(dump_doc(properties_json(*g->g, o->o, m)));
+  });
+}
+
+int cs_schedule_tic(const cs_graph* g, const char* mode, cs_schedule** out) {
+  return guarded([&] {
+    need(g, "graph");
+    need(mode, "mode");
+    need(out, "out");
+    *out = new cs_schedule{schedule_for(*g->g, "tic", prop_mode(mode), 0, nullptr)};
+  });
+}
+
+int cs_schedule_tac(const cs_graph* g, const cs_oracle* o, cs_schedule** out) {
+  return guarded([&] {
+    need(g, "graph");
+    need(o, "oracle");
+    need(out, "out");
+    *out = new cs_schedule{schedule_for(*g->g, "tac", PropMode::Amended, 0, &o->o)};
+  });
+}
+
+int cs_schedule_random(const cs_graph* g, uint64_t seed, cs_schedule** out) {
+  return guarded([&] {
+    need(g, "graph");
+    need(out, "out");
+    *out = new cs_schedule{schedule_for(*g->g, "random", PropMode::Amended, seed, nullptr)};
+  });
+}
+
+int cs_schedule_parse(const char* json_text, cs_schedule** out) {
+  return guarded([&] {
+    need(json_text, "json_text");
+    need(out, "out");
+    *out = new cs_schedule{Schedule::parse(json_text)};
+  });
+}
+
+int cs_schedule_serialize(const cs_schedule* s, char** out_json) {
+  return guarded([&] {
+    need(s, "schedule");
+    need(out_json, "out_json");
+    *out_json = dup(s->s.serialize());
+  });
+}
+
+int cs_schedule_total_order(const cs_schedule* s, int* out) {
+  return guarded([&] {
+    need(s, "schedule");
+    need(out, "out");
+    *out = s->s.total ? 1 : 0;
+  });
+}
+
+void cs_schedule_free(cs_schedule* s) { delete s; }
+
+int cs_simulate(const cs_graph* g, const cs_oracle* o, const cs_schedule* s,
+                const cs_sim_policy* policy, cs_report** out) {
+  return guarded([&] {
+    need(g, "graph");
+    need(o, "oracle");
+    need(out, "out");
+    auto* rep = new cs_report{simulate(*g->g, o->o, s ? &s->s : nullptr, policy_of(policy))};
+    *out = rep;
+  });
+}
+
+int cs_report_makespan(const cs_report* r, int64_t* out_us) {
+  return guarded([&] {
+    need(r, "report");
+    need(out_us, "out_us");
+    *out_us = r->r.makespan;
+  });
+}
+
+int cs_report_violations(const cs_report* r, int64_t* out) {
+  return guarded([&] {
+    need(r, "report");
+    need(out, "out");
+    *out = r->r.violations;
+  });
+}
+
+int cs_report_json(const cs_report* r, char** out_json) {
+  return guarded([&] {
+    need(r, "report");
+    need(out_json, "out_json");
+    *out_json = dup(dump_doc(r->r.to_json()));
+  });
+}
+
+int cs_report_chrome_trace(const cs_report* r, char** out_json) {
+  return guarded([&] {
+    need(r, "report");
+    need(out_json, "out_json");
+    *out_json = dup(dump_doc(r->r.chrome_trace()));
+  });
+}
+
+int cs_report_iteration_json(const cs_report* r, char** out_json) {
+  return guarded([&] {
+    need(r, "report");
+    need(out_json, "out_json");
+    if (!r->r.has_stats) fail(kValidation, "iteration stats need a cluster simulation");
+    *out_json = dup(dump_doc(r->r.iteration_json()));
+  });
+}
+
+void cs_report_free(cs_report* r) { delete r; }
+
+int cs_makespan_bounds(const cs_graph* g, const cs_oracle* o, int64_t* upper_us, int64_t* lower_us) {
+  return guarded([&] {
+    need(g, "graph");
+    need(o, "oracle");
+    need(upper_us, "upper_us");
+    need(lower_us, "lower_us");
+    const auto b = bounds(*g->g, o->o);
+    *upper_us = b.first;
+    *lower_us = b.second;
+  });
+}
+
+int cs_metrics_json(const cs_graph* g, const cs_oracle* o, const cs_report* r, char** out_json) {
+  return guarded([&] {
+    need(g, "graph");
+    need(o, "oracle");
+    need(r, "report");
+    need(out_json, "out_json");
+    const auto b = bounds(*g->g, o->o);
+    *out_json = dup(dump_doc(metrics_json(b.first, b.second, r->r.makespan, &r->r)));
+  });
+}
+
+int cs_brute_force(const cs_graph* g, const cs_oracle* o, const cs_sim_policy* policy, int max_recvs,
+                   char** out_json) {
+  return guarded([&] {
+    need(g, "graph");
+    need(o, "oracle");
+    need(out_json, "out_json");
+    *out_json = dup(dump_doc(brute_force(*g->g, o->o, policy_of(policy), max_recvs)));
+  });
+}
+
+const char* cs_last_error(void) { return t_error.c_str(); }
+
+void cs_string_free(char* s) { delete[] s; }
+
+const char* cs_version(void) { return "0.1.0"; }
+
+// ---------------------------------------------------------------------------
+// Batched extensions
+
+int cs_sweep_random(const cs_graph* g, const cs_oracle* o, uint64_t seed_lo, int64_t count,
+                    const cs_sim_policy* policy, int64_t* makespans_out, int64_t* worker_makespans_out,
+                    cs_sweep_stats* stats_out) {
+  return guarded([&] {
+    need(g, "graph");
+    need(o, "oracle");
+    if (count < 0) fail(kParameter, "count must be non-negative");
+    Policy p = policy_of(policy);
+    auto ctx = make_sweep(g->g, o->o, p);
+    const bool cluster_m = ctx->cluster && makespans_out;  // needs the full event replica
+    if (!ctx->fast || cluster_m) {
+      sweep_exact(*ctx, seed_lo, count, makespans_out, worker_makespans_out, stats_out);
+      return;
+    }
+    // fast path: device buffers, one launch per 2^26 seeds
+    char err[256] = {0};
+    auto cudacheck = [&](cudaError_t e) {
+      if (e != cudaSuccess) fail(kInternal, std::string("CUDA error: ") + cudaGetErrorString(e));
+    };
+    int64_t *d_i64 = nullptr, *d_ms = nullptr, *d_wms = nullptr;
+    double* d_f64 = nullptr;
+    const int64_t W = ctx->cluster ? static_cast<int64_t>(ctx->workers.size()) : 1;
+    const int64_t chunk = int64_t{1} << 26;
+    cudacheck(cudaMalloc(&d_i64, 8 * CS_DSTATS_I64));
+    cudacheck(cudaMalloc(&d_f64, 8 * CS_DSTATS_F64));
+    const int64_t cap = std::min(count, chunk);
+    if (makespans_out) cudacheck(cudaMalloc(&d_ms, 8 * std::max<int64_t>(cap, 1)));
+    if (worker_makespans_out && ctx->cluster)
+      cudacheck(cudaMalloc(&d_wms, 8 * std::max<int64_t>(cap * W, 1)));
+    cs_sweep_stats total{};
+    bool first = true;
+    try {
+      for (int64_t base = 0; base < count || (first && count == 0); base += chunk) {
+        const int64_t n = std::min(chunk, count - base);
+        if (csk_sweep_reset(ctx->plan, nullptr, d_i64, d_f64, err)) fail(kInternal, err);
+        const uint64_t lo = seed_lo + static_cast<uint64_t>(base);
+        if (csk_sweep_run(ctx->plan, lo, n, lo, nullptr, d_ms, d_wms, d_i64, d_f64, err))
+          fail(kInternal, err);
+        std::vector<int64_t> i64(CS_DSTATS_I64);
+        std::vector<double> f64(CS_DSTATS_F64);
+        cudacheck(cudaMemcpy(i64.data(), d_i64, 8 * CS_DSTATS_I64, cudaMemcpyDeviceToHost));
+        cudacheck(cudaMemcpy(f64.data(), d_f64, 8 * CS_DSTATS_F64, cudaMemcpyDeviceToHost));
+        if (d_ms) cudacheck(cudaMemcpy(makespans_out + base, d_ms, 8 * n, cudaMemcpyDeviceToHost));
+        if (d_wms)
+          cudacheck(cudaMemcpy(worker_makespans_out + base * W, d_wms, 8 * n * W, cudaMemcpyDeviceToHost));
+        cs_sweep_stats part{};
+        finish_stats(*ctx, i64.data(), f64.data(), lo, &part);
+        if (first) {
+          total = part;
+        } else if (part.count > 0) {  // merge chunk statistics
+          if (part.min_us < total.min_us) total.min_us = part.min_us, total.argmin_seed = part.argmin_seed;
+          if (part.max_us > total.max_us) total.max_us = part.max_us, total.argmax_seed = part.argmax_seed;
+          total.count += part.count;
+          total.sum_us += part.sum_us;
+          total.sumsq_us += part.sumsq_us;
+          total.straggler_sum += part.straggler_sum;
+          for (int k = 0; k < CS_HIST_BINS; ++k) {
+            total.e_hist[k] += part.e_hist[k];
+            total.straggler_hist[k] += part.straggler_hist[k];
+          }
+        }
+        first = false;
+        if (count == 0) break;
+      }
+    } catch (...) {
+      cudaFree(d_i64);
+      cudaFree(d_f64);
+      cudaFree(d_ms);
+      cudaFree(d_wms);
+      throw;
+    }
+    cudaFree(d_i64);
+    cudaFree(d_f64);
+    cudaFree(d_ms);
+    cudaFree(d_wms);
+    if (stats_out) *stats_out = total;
+  });
+}
+
+int cs_simulate_orders(const cs_graph* g, const cs_oracle* o, const int32_t* orders, int64_t n,
+                       const cs_sim_policy* policy, int64_t* makespans_out, int64_t* violations_out) {
+  return guarded([&] {
+    need(g, "graph");
+    need(o, "oracle");
+    need(makespans_out, "makespans_out");
+    if (n < 0) fail(kParameter, "n must be non-negative");
+    if (n > 0) need(orders, "orders");
+    const Graph& G = *g->g;
+    const int32_t R = static_cast<int32_t>(G.recv_ops().size());
+    for (int64_t k = 0; k < n * R; ++k)
+      if (orders[k] < 0 || orders[k] >= R) fail(kParameter, "order entry out of range");
+    const Policy p = policy_of(policy);
+    auto ctx = make_sweep(g->g, o->o, p);
+    if (n == 0) return;
+    if (ctx->fast && !ctx->cluster) {
+      int32_t* d_o = nullptr;
+      int64_t* d_m = nullptr;
+      auto cudacheck = [&](cudaError_t e) {
+        if (e != cudaSuccess) fail(kInternal, std::string("CUDA error: ") + cudaGetErrorString(e));
+      };
+      cudacheck(cudaMalloc(&d_o, 4 * n * R + 4));
+      cudacheck(cudaMalloc(&d_m, 8 * n));
+      cudacheck(cudaMemcpy(d_o, orders, 4 * n * R, cudaMemcpyHostToDevice));
+      char err[256] = {0};
+      const int rc = csk_sweep_orders(ctx->plan, d_o, n, nullptr, d_m, err);
+      cudaError_t e = cudaMemcpy(makespans_out, d_m, 8 * n, cudaMemcpyDeviceToHost);
+      cudaFree(d_o);
+      cudaFree(d_m);
+      if (rc) fail(kInternal, err);
+      cudacheck(e);
+      if (violations_out)
+        for (int64_t k = 0; k < n; ++k) violations_out[k] = 0;  // gated, noiseless, roots
+      return;
+    }
+    std::vector<uint64_t> seeds(static_cast<size_t>(n), p.choice_seed);
+    std::vector<int64_t> viol(static_cast<size_t>(n));
+    std::vector<int32_t> st(static_cast<size_t>(n));
+    char err[256] = {0};
+    const int64_t chunk = 1 << 16;
+    for (int64_t b = 0; b < n; b += chunk) {
+      const int32_t B = static_cast<int32_t>(std::min(chunk, n - b));
+      if (csk_event_sim(G.device(), ctx->dur.data(), B, nullptr, orders + b * R, R, seeds.data() + b,
+                        p.gated ? 1 : 0, p.noise, makespans_out + b, viol.data() + b, st.data() + b,
+                        nullptr, nullptr, nullptr, err))
+        fail(kInternal, err);
+    }
+    for (int64_t k = 0; k < n; ++k)
+      if (st[k]) fail(kValidation, "simulation stalled with no runnable op");
+    if (violations_out) std::memcpy(violations_out, viol.data(), 8 * n);
+  });
+}
+
+int cs_sweep_plan_create(const cs_graph* g, const cs_oracle* o, const cs_sim_policy* policy,
+                         cs_sweep_plan** out) {
+  return guarded([&] {
+    need(g, "graph");
+    need(o, "oracle");
+    need(out, "out");
+    auto ctx = make_sweep(g->g, o->o, policy_of(policy));
+    if (!ctx->fast) fail(kParameter, "closed-form sweep does not apply: " + ctx->why);
+    *out = new cs_sweep_plan{std::move(ctx)};
+  });
+}
+
+int cs_sweep_plan_info(const cs_sweep_plan* p, char** out_json) {
+  return guarded([&] {
+    need(p, "plan");
+    need(out_json, "out_json");
+    const SweepCtx& c = *p->ctx;
+    Json j;
+    j["graph"] = c.g->name();
+    j["ops"] = c.g->n();
+    j["edges"] = static_cast<int64_t>(c.g->edges().size());
+    j["recvs_per_worker"] = c.R;
+    j["classes"] = c.nc;
+    j["workers"] = c.cluster ? static_cast<int64_t>(c.workers.size()) : 1;
+    int64_t erecv = 0;
+    for (int32_t r : c.g->recv_ops()) erecv += c.g->nsucc(r);
+    j["recv_edges"] = erecv;
+    j["U_us"] = c.U;
+    j["L_us"] = c.L;
+    j["cluster"] = c.cluster;
+    *out_json = dup(dump_doc(j));
+  });
+}
+
+int cs_sweep_plan_reset(const cs_sweep_plan* p, void* stream, int64_t* d_stats_i64, double* d_stats_f64) {
+  return guarded([&] {
+    need(p, "plan");
+    need(d_stats_i64, "d_stats_i64");
+    need(d_stats_f64, "d_stats_f64");
+    char err[256] = {0};
+    if (csk_sweep_reset(p->ctx->plan, stream, d_stats_i64, d_stats_f64, err)) fail(kInternal, err);
+  });
+}
+
+int cs_sweep_plan_run(const cs_sweep_plan* p, uint64_t seed_lo, int64_t count, uint64_t key_base,
+                      void* stream, int64_t* d_makespans, int64_t* d_stats_i64, double* d_stats_f64) {
+  return guarded([&] {
+    need(p, "plan");
+    need(d_stats_i64, "d_stats_i64");
+    need(d_stats_f64, "d_stats_f64");
+    if (count < 0) fail(kParameter, "count must be non-negative");
+    if (seed_lo < key_base || seed_lo - key_base + static_cast<uint64_t>(count) > (uint64_t{1} << 26))
+      fail(kParameter, "seed - key_base must stay below 2^26");
+    char err[256] = {0};
+    if (csk_sweep_run(p->ctx->plan, seed_lo, count, key_base, stream, d_makespans, nullptr, d_stats_i64,
+                      d_stats_f64, err))
+      fail(kInternal, err);
+  });
+}
+
+int cs_sweep_stats_finish(const cs_sweep_plan* p, const int64_t* h_stats_i64, const double* h_stats_f64,
+                          uint64_t key_base, cs_sweep_stats* out) {
+  return guarded([&] {
+    need(p, "plan");
+    need(h_stats_i64, "h_stats_i64");
+    need(h_stats_f64, "h_stats_f64");
+    need(out, "out");
+    finish_stats(*p->ctx, h_stats_i64, h_stats_f64, key_base, out);
+  });
+}
+
+void cs_sweep_plan_free(cs_sweep_plan* p) { delete p; }
+
+int cs_graph_generate_model(const char* model, uint64_t seed, cs_graph** out) {
+  return guarded([&] {
+    need(model, "model");
+    need(out, "out");
+    *out = new cs_graph{generate_model(model, seed)};
+  });
+}
+
+int64_t cs_device_launches(void) { return csk_launches(); }
+
+}  // extern "C"
+#pragma GCC visibility pop

@@ -1,0 +1,313 @@
+// Batched sweeps (new entry points; the reference's loop is
+// tools/sched_main.cpp:452-502). Host work here is once-per-graph analysis:
+// decide whether the closed form of SURVEY Appendix A.2 applies and, if so,
+// build the chain-class tables the device kernel folds over. Otherwise every
+// seed runs through the exact device event simulator.
+#include "sweep.hpp"
+
+#include <algorithm>
+#include <cstring>
+#include <set>
+
+#include "../device/csk.h"
+#include "rng_host.hpp"
+
+namespace tictac {
+
+namespace {
+
+// Chain-class tables of one worker (graph or cluster worker partition).
+struct ChainTables {
+  int32_t R = 0, nc = 0;
+  std::vector<int64_t> d;      // per recv column
+  std::vector<int32_t> first;  // per recv column
+  std::vector<int64_t> pwsuf;  // nc + 1
+  int64_t send_total = 0;
+};
+
+// Preconditions of A.2 plus nested recv-ancestor sets. Returns false (with
+// a reason) when the closed form does not apply.
+bool chain_tables(const Graph& g, const std::vector<int64_t>& dur, bool allow_sends,
+                  ChainTables& t, std::string& why) {
+  const int32_t n = g.n();
+  const auto& ops = g.ops();
+  const int32_t R = static_cast<int32_t>(g.recv_ops().size());
+  if (R == 0) return why = "no recv ops", false;
+  int32_t chan = -1, cpu = -1;
+  for (int32_t i = 0; i < n; ++i) {
+    const int32_t r = g.res_of()[i];
+    if (ops[i].kind == kRecv || ops[i].kind == kSend) {
+      if (ops[i].kind == kSend && !allow_sends) return why = "send ops on the worker", false;
+      if (chan >= 0 && chan != r) return why = "more than one channel", false;
+      chan = r;
+    } else {
+      if (cpu >= 0 && cpu != r) return why = "more than one compute unit", false;
+      cpu = r;
+    }
+    if (ops[i].kind == kRecv && g.npred(i) > 0) return why = "recv with predecessors", false;
+  }
+  // recv-ancestor sets of every compute op (bitsets over recv columns)
+  const int32_t W = (R + 63) / 64;
+  if (static_cast<int64_t>(n) * W > (int64_t{1} << 27)) return why = "graph too large for tables", false;
+  std::vector<int32_t> col(n, -1);
+  for (int32_t c = 0; c < R; ++c) col[g.recv_ops()[c]] = c;
+  std::vector<int32_t> order, missing(n);
+  for (int32_t i = 0; i < n; ++i)
+    if ((missing[i] = g.npred(i)) == 0) order.push_back(i);
+  for (size_t h = 0; h < order.size(); ++h)
+    for (int32_t e = g.succ_off()[order[h]]; e < g.succ_off()[order[h] + 1]; ++e)
+      if (--missing[g.succ_idx()[e]] == 0) order.push_back(g.succ_idx()[e]);
+  std::vector<uint64_t> bits(static_cast<size_t>(n) * W, 0);
+  for (int32_t v : order) {
+    uint64_t* row = &bits[static_cast<size_t>(v) * W];
+    for (int32_t e = g.pred_off()[v]; e < g.pred_off()[v + 1]; ++e) {
+      const uint64_t* pr = &bits[static_cast<size_t>(g.pred_idx()[e]) * W];
+      for (int32_t q = 0; q < W; ++q) row[q] |= pr[q];
+    }
+    if (col[v] >= 0) row[col[v] >> 6] |= 1ULL << (col[v] & 63);
+  }
+  // classes = distinct sets among non-transfer ops, ordered by size
+  std::vector<int32_t> comp;
+  for (int32_t i = 0; i < n; ++i)
+    if (!transfer(ops[i].kind)) comp.push_back(i);
+  auto pc = [&](int32_t v) {
+    int64_t k = 0;
+    for (int32_t q = 0; q < W; ++q) k += __builtin_popcountll(bits[static_cast<size_t>(v) * W + q]);
+    return k;
+  };
+  auto less = [&](int32_t a, int32_t b) {
+    const int64_t ka = pc(a), kb = pc(b);
+    if (ka != kb) return ka < kb;
+    return std::lexicographical_compare(&bits[static_cast<size_t>(a) * W], &bits[static_cast<size_t>(a) * W] + W,
+                                        &bits[static_cast<size_t>(b) * W], &bits[static_cast<size_t>(b) * W] + W);
+  };
+  std::sort(comp.begin(), comp.end(), less);
+  std::vector<int32_t> rep;  // class representative
+  std::vector<int64_t> weight;
+  for (int32_t v : comp) {
+    if (rep.empty() || less(rep.back(), v)) {
+      rep.push_back(v);
+      weight.push_back(0);
+    }
+    weight.back() += dur[v];
+  }
+  const int32_t nc = static_cast<int32_t>(rep.size());
+  for (int32_t j = 1; j < nc; ++j) {  // nested?
+    const uint64_t* a = &bits[static_cast<size_t>(rep[j - 1]) * W];
+    const uint64_t* b = &bits[static_cast<size_t>(rep[j]) * W];
+    for (int32_t q = 0; q < W; ++q)
+      if (a[q] & ~b[q]) return why = "recv-ancestor sets are not nested", false;
+  }
+  t.R = R;
+  t.nc = nc;
+  t.d.resize(R);
+  t.first.assign(R, nc);
+  for (int32_t c = 0; c < R; ++c) t.d[c] = dur[g.recv_ops()[c]];
+  for (int32_t j = nc - 1; j >= 0; --j)
+    for (int32_t c = 0; c < R; ++c)
+      if ((bits[static_cast<size_t>(rep[j]) * W + (c >> 6)] >> (c & 63)) & 1) t.first[c] = j;
+  t.pwsuf.assign(nc + 1, 0);
+  for (int32_t j = nc - 1; j >= 0; --j) t.pwsuf[j] = t.pwsuf[j + 1] + weight[j];
+  // sends: must be released exactly when the last compute finishes, i.e.
+  // depend on every compute op that has no compute successor.
+  if (allow_sends) {
+    std::set<int32_t> sinks;
+    for (int32_t v : comp) {
+      bool has = false;
+      for (int32_t e = g.succ_off()[v]; e < g.succ_off()[v + 1]; ++e)
+        has |= !transfer(ops[g.succ_idx()[e]].kind);
+      if (!has) sinks.insert(v);
+    }
+    for (int32_t i = 0; i < n; ++i) {
+      if (ops[i].kind != kSend) continue;
+      std::set<int32_t> pre(g.pred_idx().begin() + g.pred_off()[i], g.pred_idx().begin() + g.pred_off()[i + 1]);
+      for (int32_t p : pre)
+        if (transfer(ops[p].kind)) return why = "send depends on a transfer", false;
+      if (sinks.empty() || !std::includes(pre.begin(), pre.end(), sinks.begin(), sinks.end()))
+        return why = "send not released by the last compute", false;
+      t.send_total += dur[i];
+    }
+  }
+  for (int64_t x : t.d)
+    if (x >= (int64_t{1} << 31)) return why = "recv duration beyond 32 bits", false;
+  return true;
+}
+
+}  // namespace
+
+SweepCtx::~SweepCtx() {
+  if (plan) csk_sweep_plan_free(plan);
+}
+
+std::unique_ptr<SweepCtx> make_sweep(std::shared_ptr<const Graph> g, const TimeOracle& o,
+                                     const Policy& p) {
+  auto s = std::make_unique<SweepCtx>();
+  s->g = g;
+  s->dur = o.durations(*g);
+  if (p.noise < 0.0 || p.noise > 1.0) fail(kParameter, "reorder_noise must be within [0, 1]");
+  s->policy = p;
+  std::tie(s->U, s->L) = bounds(*g, o);
+  s->cluster = g->cluster();
+  if (s->cluster) {
+    s->workers = g->worker_devices();
+    std::unordered_map<std::string, int32_t> widx;
+    for (size_t i = 0; i < s->workers.size(); ++i) widx[s->workers[i]] = static_cast<int32_t>(i);
+    for (int32_t r : g->recv_ops()) {
+      auto it = widx.find(g->ops()[r].res.device);
+      s->recv_worker.push_back(it == widx.end() ? 0 : it->second);
+    }
+    // every worker partition must validate, as schedule_for builds them
+    for (const auto& dv : s->workers) (void)g->partition(dv);
+  } else {
+    s->workers = {};
+    s->recv_worker.assign(g->recv_ops().size(), 0);
+  }
+  // fast path?
+  bool ok = p.gated && p.noise == 0.0 && s->U < (int64_t{1} << 37);
+  if (!ok) s->why = "policy outside the closed form (ungated or noisy)";
+  std::vector<ChainTables> tabs;
+  if (ok && !s->cluster) {
+    tabs.emplace_back();
+    ok = chain_tables(*g, s->dur, false, tabs.back(), s->why);
+  } else if (ok) {
+    // devices other than workers must not feed back into workers
+    for (const auto& dv : s->workers) {
+      auto part = g->partition(dv);
+      std::vector<int64_t> pd(part->n());
+      for (int32_t i = 0; i < part->n(); ++i) pd[i] = s->dur[g->at(part->ops()[i].id)];
+      for (int32_t i = 0; i < g->n(); ++i)
+        if (g->ops()[i].res.device != dv)
+          for (int32_t e = g->succ_off()[i]; e < g->succ_off()[i + 1]; ++e)
+            if (g->ops()[g->succ_idx()[e]].res.device == dv) {
+              ok = false;
+              s->why = "worker depends on another device";
+            }
+      if (!ok) break;
+      tabs.emplace_back();
+      if (!(ok = chain_tables(*part, pd, true, tabs.back(), s->why))) break;
+      if (tabs.back().R != tabs[0].R || tabs.back().nc != tabs[0].nc) {
+        ok = false;
+        s->why = "workers differ in shape";
+        break;
+      }
+    }
+  }
+  if (ok) {
+    const int32_t W = static_cast<int32_t>(tabs.size()), R = tabs[0].R, nc = tabs[0].nc;
+    std::vector<int64_t> d, pw, send;
+    std::vector<int32_t> first;
+    for (const auto& t : tabs) {
+      d.insert(d.end(), t.d.begin(), t.d.end());
+      first.insert(first.end(), t.first.begin(), t.first.end());
+      pw.insert(pw.end(), t.pwsuf.begin(), t.pwsuf.end());
+      send.push_back(t.send_total);
+    }
+    char err[256] = {0};
+    s->plan = csk_sweep_plan(W, R, nc, d.data(), first.data(), pw.data(), send.data(),
+                             s->cluster ? 1 : 0, s->U, s->L, err);
+    if (!s->plan) fail(kInternal, err);
+    s->fast = true;
+    s->nc = nc;
+    s->R = R;
+  }
+  return s;
+}
+
+void finish_stats(const SweepCtx& s, const int64_t* i64, const double* f64, uint64_t key_base,
+                  cs_sweep_stats* out) {
+  std::memset(out, 0, sizeof(*out));
+  out->count = i64[3];
+  out->upper_us = s.U;
+  out->lower_us = s.L;
+  if (out->count > 0) {
+    const uint64_t kmin = static_cast<uint64_t>(i64[0]), kmax = static_cast<uint64_t>(i64[1]);
+    const uint64_t mask = (1ULL << 26) - 1;
+    out->min_us = static_cast<int64_t>(kmin >> 26);
+    out->argmin_seed = key_base + (kmin & mask);
+    out->max_us = static_cast<int64_t>(kmax >> 26);
+    out->argmax_seed = key_base + (mask - (kmax & mask));
+  }
+  out->sum_us = i64[2];
+  out->sumsq_us = f64[0];
+  for (int k = 0; k < CS_HIST_BINS; ++k) {
+    out->e_hist[k] = i64[8 + k];
+    out->straggler_hist[k] = i64[1008 + k];
+  }
+  out->n_workers = s.cluster ? static_cast<int64_t>(s.workers.size()) : 0;
+  out->straggler_sum = f64[1];
+}
+
+// Exact path: device event simulator over seeds, stats on the host (these
+// inputs are outside the closed form, so this is the general replica).
+void sweep_exact(SweepCtx& s, uint64_t seed_lo, int64_t count, int64_t* makespans,
+                 int64_t* worker_ms, cs_sweep_stats* stats) {
+  const Graph& g = *s.g;
+  DeviceGraph* dg = g.device();
+  const int32_t nw = s.cluster ? static_cast<int32_t>(s.workers.size()) : 1;
+  // device index per worker (devices sorted as in the DeviceGraph upload)
+  std::vector<std::string> devs;
+  for (const Resource& r : g.resources()) devs.push_back(r.device);
+  std::sort(devs.begin(), devs.end());
+  devs.erase(std::unique(devs.begin(), devs.end()), devs.end());
+  std::vector<int32_t> wdev;
+  for (const auto& w : s.workers)
+    wdev.push_back(static_cast<int32_t>(std::lower_bound(devs.begin(), devs.end(), w) - devs.begin()));
+  std::vector<int64_t> i64(CS_DSTATS_I64, 0);
+  std::vector<double> f64(CS_DSTATS_F64, 0.0);
+  i64[0] = -1;  // as unsigned: max
+  const int64_t chunk = 1 << 16;
+  std::vector<int64_t> ms, viol, dev_end;
+  std::vector<int32_t> st;
+  for (int64_t base = 0; base < count; base += chunk) {
+    const int32_t B = static_cast<int32_t>(std::min(chunk, count - base));
+    ms.resize(B);
+    viol.resize(B);
+    st.resize(B);
+    dev_end.resize(static_cast<size_t>(B) * devs.size());
+    char err[256] = {0};
+    const int rc = csk_event_sweep(dg, s.dur.data(), seed_lo + static_cast<uint64_t>(base), B,
+                                   s.cluster ? 1 : 0, s.recv_worker.data(), nw, s.policy.gated ? 1 : 0,
+                                   s.policy.noise, ms.data(), viol.data(), st.data(),
+                                   s.cluster ? dev_end.data() : nullptr, err);
+    if (rc) fail(kInternal, err);
+    for (int32_t b = 0; b < B; ++b) {
+      if (st[b]) fail(kValidation, "simulation stalled with no runnable op");
+      const int64_t idx = base + b;
+      const uint64_t seed = seed_lo + static_cast<uint64_t>(idx);
+      const int64_t m = ms[b];
+      if (makespans) makespans[idx] = m;
+      int64_t hi = 0, lo = INT64_MAX;
+      if (s.cluster) {
+        for (int32_t w = 0; w < nw; ++w) {
+          const int64_t mw = dev_end[static_cast<size_t>(b) * devs.size() + wdev[w]];
+          if (worker_ms) worker_ms[idx * nw + w] = mw;
+          hi = std::max(hi, mw);
+          lo = std::min(lo, mw);
+        }
+        int bin = 0;
+        if (hi > 0) {
+          f64[1] += static_cast<double>(hi - lo) / static_cast<double>(hi);
+          bin = std::min(999, static_cast<int>((1000 * (hi - lo)) / hi));
+        }
+        i64[1008 + bin]++;
+      }
+      // cluster statistics are over the iteration time, as in the fast path
+      const int64_t mstat = s.cluster ? hi : m;
+      const uint64_t off = seed - seed_lo;
+      const uint64_t kmin = (static_cast<uint64_t>(mstat) << 26) | off;
+      const uint64_t kmax = (static_cast<uint64_t>(mstat) << 26) | (((1ULL << 26) - 1) - off);
+      if (kmin < static_cast<uint64_t>(i64[0])) i64[0] = static_cast<int64_t>(kmin);
+      if (kmax > static_cast<uint64_t>(i64[1])) i64[1] = static_cast<int64_t>(kmax);
+      i64[2] += mstat;
+      i64[3] += 1;
+      f64[0] += static_cast<double>(mstat) * static_cast<double>(mstat);
+      if (!s.cluster && s.U != s.L) {
+        const int64_t bin = (1000 * (s.U - m)) / (s.U - s.L);
+        i64[8 + std::min<int64_t>(999, std::max<int64_t>(0, bin))]++;
+      }
+    }
+  }
+  if (stats) finish_stats(s, i64.data(), f64.data(), seed_lo, stats);
+}
+
+}  // namespace tictac

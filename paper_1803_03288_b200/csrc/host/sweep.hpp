@@ -1,0 +1,36 @@
+// Batched sweep context shared by the C ABI (capi.cpp) and sweep.cpp.
+#pragma once
+
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../../include/commsched.h"
+#include "core.hpp"
+
+struct SweepPlan;  // device/csk.h
+
+namespace tictac {
+
+struct SweepCtx {
+  std::shared_ptr<const Graph> g;
+  std::vector<int64_t> dur;
+  Policy policy;
+  int64_t U = 0, L = 0;
+  bool cluster = false, fast = false;
+  std::vector<std::string> workers;  // worker_devices() order (clusters)
+  std::vector<int32_t> recv_worker;  // per recv column
+  SweepPlan* plan = nullptr;
+  int32_t R = 0, nc = 0;
+  std::string why;  // why the closed form does not apply
+  ~SweepCtx();
+};
+
+std::unique_ptr<SweepCtx> make_sweep(std::shared_ptr<const Graph> g, const TimeOracle& o,
+                                     const Policy& p);
+void finish_stats(const SweepCtx& s, const int64_t* i64, const double* f64, uint64_t key_base,
+                  cs_sweep_stats* out);
+void sweep_exact(SweepCtx& s, uint64_t seed_lo, int64_t count, int64_t* makespans,
+                 int64_t* worker_ms, cs_sweep_stats* stats);
+
+}  // namespace tictac

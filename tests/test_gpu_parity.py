@@ -1,0 +1,189 @@
+"""GPU parity: the product library (CUDA path) against the reference's own
+known answers and against the reference library built from
+/root/reference (oracle/_ref), byte for byte, through the same C ABI."""
+import json
+
+import numpy as np
+import pytest
+
+import corpus
+from paper_1803_03288_b200.capi import CsError, policy
+
+pytestmark = pytest.mark.gpu
+
+
+def outcome(fn):
+    try:
+        return ("ok", fn())
+    except CsError as e:
+        return ("err", e.code, e.message)
+
+
+# ---------------------------------------------------------------- KATs ----
+
+def test_toy_simulation_kats(lib, toy_text):
+    """test_sim.cpp:43-103 and capi_tests.cpp:236-283 known answers."""
+    g = lib.graph(toy_text)
+    o = g.declared()
+    fwd = lib.schedule_parse('{"graph":"toy","algorithm":"tic","priorities":{"recv1":0,"recv2":1}}')
+    r = g.simulate(o, fwd)
+    assert r.makespan() == 9 and r.violations() == 0
+    ev = {e["op"]: (e["start_us"], e["end_us"]) for e in json.loads(r.json())["events"]}
+    assert ev == {"recv1": (0, 3), "recv2": (3, 4), "op1": (3, 7), "op2": (7, 9)}
+    assert json.loads(r.json())["busy"] == {"w0/channel/net0": 4, "w0/compute/cpu0": 6}
+    rev = lib.schedule_parse('{"graph":"toy","algorithm":"tic","priorities":{"recv1":1,"recv2":0}}')
+    r2 = g.simulate(o, rev)
+    ev2 = {e["op"]: (e["start_us"], e["end_us"]) for e in json.loads(r2.json())["events"]}
+    assert r2.makespan() == 10 and ev2["recv2"][1] == 1 and ev2["op1"][0] == 4 and ev2["op2"][0] == 8
+    tie = lib.schedule_parse('{"graph":"toy","algorithm":"tic","priorities":{"recv1":0,"recv2":0}}')
+    for seed in range(6):
+        rt = g.simulate(o, tie, policy(True, seed, 0.0))
+        chan = [e["op"] for e in json.loads(rt.json())["events"] if "channel" in e["resource"]]
+        assert rt.makespan() == 9 and chan == ["recv1", "recv2"]
+    orders = set()
+    for seed in range(16):
+        ru = g.simulate(o, None, policy(False, seed, 0.0))
+        assert ru.makespan() in (9, 10)
+        orders.add(tuple(e["op"] for e in json.loads(ru.json())["events"] if "channel" in e["resource"]))
+    assert len(orders) == 2
+    rn = g.simulate(o, fwd, policy(True, 0, 1.0))
+    chan = [e["op"] for e in json.loads(rn.json())["events"] if "channel" in e["resource"]]
+    assert chan == ["recv2", "recv1"] and rn.makespan() == 10 and rn.violations() == 1
+
+
+def test_forced_release_kat(lib):
+    """test_sim.cpp:126-145: recv1 outranks recv2 but waits on it."""
+    doc = {"name": "g", "partition": "cluster", "ops": [
+        {"id": "recv1", "kind": "recv", "resource": {"device": "w0", "unit": "channel", "name": "net0"}, "time_us": 2},
+        {"id": "recv2", "kind": "recv", "resource": {"device": "w0", "unit": "channel", "name": "net0"}, "time_us": 3},
+        {"id": "c", "kind": "compute", "resource": {"device": "w0", "unit": "compute", "name": "cpu0"}, "time_us": 1}],
+        "edges": [["recv2", "c"], ["c", "recv1"]]}
+    g = lib.graph(json.dumps(doc))
+    s = lib.schedule_parse('{"graph":"g","algorithm":"tic","priorities":{"recv1":0,"recv2":1}}')
+    r = g.simulate(g.declared(), s)
+    chan = [e["op"] for e in json.loads(r.json())["events"] if "channel" in e["resource"]]
+    assert r.makespan() == 6 and chan == ["recv2", "recv1"] and r.violations() == 2
+
+
+def test_toy_schedule_and_metrics_kats(lib, toy_text):
+    """test_schedule.cpp:37-82, test_properties.cpp:40-79, test_metrics.cpp."""
+    g = lib.graph(toy_text)
+    o = g.declared()
+    assert g.tic("amended").priorities() == {"recv1": 0, "recv2": 1}
+    assert g.tic("amended").total_order()
+    assert g.tic("literal").priorities() == {"recv1": 0, "recv2": 0}
+    assert not g.tic("literal").total_order()
+    assert g.tac(o).priorities() == {"recv1": 0, "recv2": 1}
+    lit, amd = g.properties(o, "literal"), g.properties(o, "amended")
+    assert lit["M"] == {"op1": 3, "op2": 4, "recv1": 3, "recv2": 1}
+    assert lit["P"] == {"recv1": 4, "recv2": 0}
+    assert lit["M_plus"] == {"recv1": 4, "recv2": 4} and amd["M_plus"] == {"recv1": 3, "recv2": 4}
+    assert amd["dep"]["op2"] == ["recv1", "recv2"]
+    assert g.bounds(o) == (10, 6)
+    r = g.simulate(o, g.tac(o))
+    m = json.loads(g.metrics_text(o, r))
+    assert m == {"U_us": 10, "L_us": 6, "m_us": 9, "E": {"num": 1, "den": 4},
+                 "S": {"num": 2, "den": 3}, "straggler": None}
+    bf = json.loads(g.brute_force_text(o))
+    assert bf == {"order": ["recv1", "recv2"], "makespan_us": 9, "distribution": [9, 10]}
+    with pytest.raises(CsError) as e:
+        g.brute_force_text(o, None, 1)
+    assert e.value.code == 4
+
+
+def test_dense_tic_ranks_and_unbounded(lib):
+    """test_schedule.cpp:55-73 and test_properties.cpp:81-92."""
+    def op(i, k, unit, t):
+        return {"id": i, "kind": k, "resource": {"device": "w0", "unit": unit,
+                                                   "name": "net0" if unit == "channel" else "cpu0"}, "time_us": t}
+    doc = {"name": "g", "partition": "worker",
+           "ops": [op("r1", "recv", "channel", 1), op("r2", "recv", "channel", 1), op("r3", "recv", "channel", 1),
+                   op("c1", "compute", "compute", 5), op("c2", "compute", "compute", 5)],
+           "edges": [["r1", "c1"], ["r2", "c2"]]}
+    g = lib.graph(json.dumps(doc))
+    s = g.tic()
+    assert s.priorities() == {"r1": 0, "r2": 0, "r3": 1} and not s.total_order()
+    doc2 = {"name": "g", "partition": "worker", "ops": [op("r1", "recv", "channel", 2), op("r2", "recv", "channel", 5)], "edges": []}
+    g2 = lib.graph(json.dumps(doc2))
+    p = g2.properties(g2.declared())
+    assert p["M_plus"] == {"r1": None, "r2": None} and p["P"]["r1"] == 0
+
+
+# ------------------------------------------------ byte parity vs reference --
+
+def _both(lib, ref, text, fn):
+    a = outcome(lambda: fn(lib, lib.graph(text)))
+    b = outcome(lambda: fn(ref, ref.graph(text)))
+    assert a == b, (a[:2], b[:2])
+    return a
+
+
+@pytest.mark.parametrize("kind", ["worker", "cluster", "model"])
+def test_schedules_match_reference(lib, ref, kind):
+    graphs = {"worker": corpus.worker_graphs, "cluster": corpus.cluster_graphs,
+              "model": corpus.model_graphs}[kind](lib)
+    for name, text in graphs:
+        for mode in ("amended", "literal"):
+            _both(lib, ref, text, lambda L, g: g.tic(mode).serialize() + str(g.tic(mode).total_order()))
+        _both(lib, ref, text, lambda L, g: g.tac(g.declared()).serialize())
+        for seed in (0, 1, 7, 123456789):
+            _both(lib, ref, text, lambda L, g: g.random(seed).serialize())
+        if kind != "model":
+            for mode in ("amended", "literal"):
+                _both(lib, ref, text, lambda L, g: g.properties_text(g.declared(), mode))
+
+
+@pytest.mark.parametrize("kind", ["worker", "cluster", "model"])
+def test_simulation_matches_reference(lib, ref, kind):
+    graphs = {"worker": corpus.worker_graphs, "cluster": corpus.cluster_graphs,
+              "model": corpus.model_graphs}[kind](lib)
+    pols = [None, policy(True, 3, 0.0), policy(False, 5, 0.0), policy(True, 9, 0.3), policy(True, 2, 1.0)]
+    for name, text in graphs:
+        def run(L, g, algo, pol):
+            o = g.declared()
+            s = {"none": None, "tic": g.tic(), "tac": g.tac(o), "random": g.random(17)}[algo]
+            r = g.simulate(o, s, pol)
+            out = r.json() + r.chrome_trace() + g.metrics_text(o, r) + str(r.violations())
+            if g.is_cluster():
+                out += r.iteration_json()
+            return out
+        for algo in ("none", "tic", "tac", "random"):
+            for pol in pols:
+                _both(lib, ref, text, lambda L, g: run(L, g, algo, pol))
+
+
+def test_brute_force_matches_reference(lib, ref):
+    for name, text in corpus.worker_graphs(lib)[:7]:
+        for pol in (None, policy(True, 4, 0.0), policy(True, 1, 0.5)):
+            _both(lib, ref, text, lambda L, g: g.brute_force_text(g.declared(), pol, 8))
+
+
+def test_sweep_matches_reference(lib, ref):
+    """cs_sweep_random == the CLI sweep loop over the reference ABI."""
+    for name, text in corpus.worker_graphs(lib) + corpus.model_graphs(lib):
+        g = lib.graph(text)
+        o = g.declared()
+        res = g.sweep_random(o, 1, 300, None, makespans=True)
+        rg = ref.graph(text)
+        ro = rg.declared()
+        want = []
+        for s in range(1, 301):
+            want.append(rg.simulate(ro, rg.random(s), policy(True, s, 0.0)).makespan())
+        want = np.array(want)
+        assert np.array_equal(res["makespans"], want), name
+        assert res["min_us"] == want.min() and res["argmin_seed"] == 1 + int(np.argmin(want))
+        assert res["sum_us"] == want.sum() and res["count"] == 300
+
+
+def test_cluster_sweep_matches_reference(lib, ref):
+    for name, text in corpus.cluster_graphs(lib):
+        g = lib.graph(text)
+        o = g.declared()
+        res = g.sweep_random(o, 1, 100, None, makespans=True, worker_makespans=True)
+        rg = ref.graph(text)
+        ro = rg.declared()
+        for i, s in enumerate(range(1, 101)):
+            r = rg.simulate(ro, rg.random(s), policy(True, s, 0.0))
+            it = json.loads(r.iteration_json())
+            assert res["makespans"][i] == r.makespan()
+            assert list(res["worker_makespans"][i]) == list(it["per_worker_makespan_us"].values())
