@@ -133,6 +133,14 @@ __device__ __forceinline__ uint64_t fastmod(uint64_t v, uint64_t n, uint64_t mag
   return r;
 }
 
+// Same, remainder only: r = v - q*n < 2n < 2^32 is exact in the low word.
+__device__ __forceinline__ uint32_t fastmod32(uint64_t v, uint32_t n, uint64_t magic) {
+  const uint64_t q = __umul64hi(v, magic);
+  uint32_t r = static_cast<uint32_t>(v) - static_cast<uint32_t>(q) * n;
+  if (r >= n) r -= n;
+  return r;
+}
+
 inline void bounded_consts(uint64_t n, uint64_t* limit, uint64_t* magic) {
   if (n < 2) {
     *limit = ~0ULL;

@@ -30,7 +30,7 @@
 namespace tictac_dev {
 namespace {
 
-constexpr int kSweepThreads = 128;
+constexpr int kSweepThreads = 256;
 constexpr int kBins = 1000;
 
 struct ChainArgs {
@@ -100,29 +100,190 @@ struct Items<uint16_t> {
   }
 };
 
-struct Fold {  // right-to-left suffix-min fold of one ordering
+// Right-to-left suffix-min fold of one ordering; V = int32_t when every
+// time sum fits 31 bits (U < 2^31, checked on the host), else int64_t.
+template <typename V>
+struct FoldT {
   int G;
-  int64_t suffix, best;
-  __device__ __forceinline__ void add(uint2 e, int64_t ctot, const int64_t* pw) {
+  V suffix, best;
+  __device__ __forceinline__ void add(uint2 e, V ctot, const V* pw) {
     const int gk = min(static_cast<int>(e.x), G);
     if (gk < G) best = max(best, ctot - suffix + pw[gk]);
     G = gk;
-    suffix += e.y;
+    suffix += static_cast<V>(e.y);
   }
 };
 
-template <typename T, bool kOrders>
+// One Fisher–Yates draw at slot i (1-based count of unfinished slots) with
+// bounded() value j: the element landing in its final slot i-1 is folded.
+template <typename T, typename V>
+__device__ __forceinline__ void fy_draw(const Items<T>& items, int i, int j, FoldT<V>& f, const uint2* tab,
+                                        V ctot, const V* pw) {
+  T* pj = items.at(j);
+  const T x = *pj;
+  *pj = *items.at(i - 1);
+  f.add(tab[x], ctot, pw);
+}
+
+// Generic continuation after a bounded() rejection (probability ~R·2^-64
+// per draw) or past the first 311 outputs: full mt19937_64 state in local
+// memory, advanced to output `out` (0-based), then the reference loop.
+template <typename T, typename V>
+__device__ __noinline__ void shuffle_slow(uint64_t seed, int out, int i, const Items<T>* items, FoldT<V>* f,
+                                          const uint2* tab, V ctot, const V* pw) {
+  uint64_t st[312];
+  MtFull m{st, 0};
+  m.seed(seed);
+  for (int k = 0; k < out; ++k) m.next();
+  for (; i > 1; --i) {
+    const uint64_t n = static_cast<uint64_t>(i);
+    const uint64_t limit = UINT64_MAX - (UINT64_MAX % n + 1) % n;
+    uint64_t v;
+    do v = m.next();
+    while (v > limit);
+    fy_draw(*items, i, static_cast<int>(v % n), *f, tab, ctot, pw);
+  }
+  f->add(tab[*items->at(0)], ctot, pw);
+}
+
+// random_schedule(seed) over R recv columns folded right-to-left. Fast path:
+// draw d uses mt output d (no rejection) computed by register cursors —
+// phase 1 (d < 156): t_d = f(s_d, s_d+1) ^ s_{d+156}; phase 2 (d < 311):
+// t_d = f(s_d, s_d+1) ^ t_{d-156}, t_{d-156} = f(s_{d-156}, s_{d-155}) ^ s_d.
+template <typename T, typename V>
+__device__ __forceinline__ void shuffle_fold(uint64_t seed, int R, const Items<T>& items, FoldT<V>& f,
+                                             const uint2* tab, V ctot, const V* pw,
+                                             const uint64_t* s_lim, const uint64_t* s_mag) {
+  items.init(R);
+  uint64_t a0 = seed, a1 = mt_step(seed, 1), b = seed;
+#pragma unroll 4
+  for (uint32_t k = 1; k <= 156; ++k) b = mt_step(b, k);
+  const int draws = R - 1;
+  const int n1 = min(draws, 156);
+  int d = 0;
+  // Pairs of draws: both mt outputs, rejection tests and bounded() values
+  // are computed before the two dependent shared-memory swaps, giving the
+  // scheduler two independent 64-bit chains per iteration.
+  for (; d + 1 < n1; d += 2) {
+    const uint64_t t0 = mt_twist(a0, a1, b);
+    const uint64_t a2 = mt_step(a1, static_cast<uint32_t>(d + 2));
+    const uint64_t b1 = mt_step(b, static_cast<uint32_t>(d + 157));
+    const uint64_t t1 = mt_twist(a1, a2, b1);
+    a0 = a2;
+    a1 = mt_step(a2, static_cast<uint32_t>(d + 3));
+    b = mt_step(b1, static_cast<uint32_t>(d + 158));
+    const uint64_t v0 = mt_temper(t0), v1 = mt_temper(t1);
+    const int i0 = R - d, i1 = i0 - 1;
+    const bool r0 = v0 > s_lim[i0], r1 = v1 > s_lim[i1];
+    const int j0 = static_cast<int>(fastmod32(v0, static_cast<uint32_t>(i0), s_mag[i0]));
+    const int j1 = static_cast<int>(fastmod32(v1, static_cast<uint32_t>(i1), s_mag[i1]));
+    if (r0 | r1) {
+      if (r0) {
+        shuffle_slow(seed, d + 1, i0, &items, &f, tab, ctot, pw);
+      } else {
+        fy_draw(items, i0, j0, f, tab, ctot, pw);
+        shuffle_slow(seed, d + 2, i1, &items, &f, tab, ctot, pw);
+      }
+      return;
+    }
+    fy_draw(items, i0, j0, f, tab, ctot, pw);
+    fy_draw(items, i1, j1, f, tab, ctot, pw);
+  }
+  for (; d < n1; ++d) {
+    const uint64_t t = mt_twist(a0, a1, b);
+    a0 = a1;
+    a1 = mt_step(a1, static_cast<uint32_t>(d + 2));
+    b = mt_step(b, static_cast<uint32_t>(d + 157));
+    const uint64_t v = mt_temper(t);
+    const int i = R - d;
+    if (v > s_lim[i]) {
+      shuffle_slow(seed, d + 1, i, &items, &f, tab, ctot, pw);
+      return;
+    }
+    fy_draw(items, i, static_cast<int>(fastmod32(v, static_cast<uint32_t>(i), s_mag[i])), f, tab, ctot, pw);
+  }
+  if (d < draws) {
+    uint64_t c0 = seed, c1 = mt_step(seed, 1);
+    const int n2 = min(draws, 311);
+    for (; d + 1 < n2; d += 2) {
+      const uint64_t back0 = mt_twist(c0, c1, a0);
+      const uint64_t t0 = mt_twist(a0, a1, back0);
+      const uint64_t a2 = mt_step(a1, static_cast<uint32_t>(d + 2));
+      const uint64_t c2 = mt_step(c1, static_cast<uint32_t>(d - 154));
+      const uint64_t back1 = mt_twist(c1, c2, a1);
+      const uint64_t t1 = mt_twist(a1, a2, back1);
+      a0 = a2;
+      a1 = mt_step(a2, static_cast<uint32_t>(d + 3));
+      c0 = c2;
+      c1 = mt_step(c2, static_cast<uint32_t>(d - 153));
+      const uint64_t v0 = mt_temper(t0), v1 = mt_temper(t1);
+      const int i0 = R - d, i1 = i0 - 1;
+      const bool r0 = v0 > s_lim[i0], r1 = v1 > s_lim[i1];
+      const int j0 = static_cast<int>(fastmod32(v0, static_cast<uint32_t>(i0), s_mag[i0]));
+      const int j1 = static_cast<int>(fastmod32(v1, static_cast<uint32_t>(i1), s_mag[i1]));
+      if (r0 | r1) {
+        if (r0) {
+          shuffle_slow(seed, d + 1, i0, &items, &f, tab, ctot, pw);
+        } else {
+          fy_draw(items, i0, j0, f, tab, ctot, pw);
+          shuffle_slow(seed, d + 2, i1, &items, &f, tab, ctot, pw);
+        }
+        return;
+      }
+      fy_draw(items, i0, j0, f, tab, ctot, pw);
+      fy_draw(items, i1, j1, f, tab, ctot, pw);
+    }
+    for (; d < n2; ++d) {
+      const uint64_t back = mt_twist(c0, c1, a0);
+      const uint64_t t = mt_twist(a0, a1, back);
+      a0 = a1;
+      a1 = mt_step(a1, static_cast<uint32_t>(d + 2));
+      c0 = c1;
+      c1 = mt_step(c1, static_cast<uint32_t>(d - 154));
+      const uint64_t v = mt_temper(t);
+      const int i = R - d;
+      if (v > s_lim[i]) {
+        shuffle_slow(seed, d + 1, i, &items, &f, tab, ctot, pw);
+        return;
+      }
+      fy_draw(items, i, static_cast<int>(fastmod32(v, static_cast<uint32_t>(i), s_mag[i])), f, tab, ctot, pw);
+    }
+    if (d < draws) {
+      shuffle_slow(seed, d, R - d, &items, &f, tab, ctot, pw);
+      return;
+    }
+  }
+  if (R >= 1) f.add(tab[*items.at(0)], ctot, pw);
+}
+
+// Shared-memory layout of one block (bytes); hist bins only when used.
+__host__ __device__ inline size_t sweep_smem(int R, int W, int stride, int nhist, size_t vbytes) {
+  const int per_word = R <= 256 ? 4 : 2;
+  return 16 * static_cast<size_t>(R + 2) + 8 * static_cast<size_t>(W) * R +
+         ((vbytes * W * stride + 7) & ~size_t(7)) + 4 * static_cast<size_t>(nhist) * kBins +
+         4 * static_cast<size_t>(kSweepThreads) * ((R + per_word - 1) / per_word + 1);
+}
+
+template <typename T, bool kOrders, typename V>
 __global__ void __launch_bounds__(kSweepThreads) chain_sweep_kernel(ChainArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int R = a.R, W = a.W;
-  uint2* s_tab = reinterpret_cast<uint2*>(smem);
-  int64_t* s_pw = reinterpret_cast<int64_t*>(s_tab + W * R);
-  int* s_hist = reinterpret_cast<int*>(s_pw + W * a.stride);
-  int* s_shist = s_hist + kBins;
-  uint32_t* s_items = reinterpret_cast<uint32_t*>(s_shist + kBins);
+  uint64_t* s_lim = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* s_mag = s_lim + (R + 2);
+  uint2* s_tab = reinterpret_cast<uint2*>(s_mag + (R + 2));
+  V* s_pw = reinterpret_cast<V*>(s_tab + W * R);
+  const size_t pw_bytes = (sizeof(V) * W * a.stride + 7) & ~size_t(7);
+  int* s_hist = reinterpret_cast<int*>(reinterpret_cast<unsigned char*>(s_pw) + pw_bytes);
+  const int nhist = (a.do_e ? 1 : 0) + (a.cluster ? 1 : 0);
+  int* s_shist = s_hist + (a.do_e ? kBins : 0);  // straggler bins (clusters)
+  uint32_t* s_items = reinterpret_cast<uint32_t*>(s_hist + nhist * kBins);
+  for (int k = threadIdx.x; k < R + 2; k += blockDim.x) {
+    s_lim[k] = a.lim[k];
+    s_mag[k] = a.mag[k];
+  }
   for (int k = threadIdx.x; k < W * R; k += blockDim.x) s_tab[k] = a.tab[k];
-  for (int k = threadIdx.x; k < W * a.stride; k += blockDim.x) s_pw[k] = a.pwsuf[k];
-  for (int k = threadIdx.x; k < 2 * kBins; k += blockDim.x) s_hist[k] = 0;
+  for (int k = threadIdx.x; k < W * a.stride; k += blockDim.x) s_pw[k] = static_cast<V>(a.pwsuf[k]);
+  for (int k = threadIdx.x; k < nhist * kBins; k += blockDim.x) s_hist[k] = 0;
   __syncthreads();
   const Items<T> items{s_items + threadIdx.x};
 
@@ -136,32 +297,20 @@ __global__ void __launch_bounds__(kSweepThreads) chain_sweep_kernel(ChainArgs a)
     int64_t hi = 0, lo = INT64_MAX;
     for (int w = 0; w < W; ++w) {
       const uint2* tab = s_tab + w * R;
-      const int64_t* pw = s_pw + w * a.stride;
-      const int64_t ctot = a.ctot[w];
-      Fold f{a.nc, 0, -1};
+      const V* pw = s_pw + w * a.stride;
+      const V ctot = static_cast<V>(a.ctot[w]);
+      FoldT<V> f{a.nc, 0, -1};
       if constexpr (kOrders) {
         const int32_t* o = a.orders + idx * R;
         for (int k = R - 1; k >= 0; --k) f.add(tab[o[k]], ctot, pw);
       } else {
         const uint64_t ws = a.cluster ? splitmix64(seed ^ (kPhi * static_cast<uint64_t>(w + 1))) : seed;
-        PermStream rng;
-        rng.init(ws);
-        items.init(R);
-        for (int i = R; i > 1; --i) {
-          const uint64_t lim = a.lim[i], mag = a.mag[i];
-          uint64_t v = rng.next();
-          while (v > lim) v = rng.next();
-          const int j = static_cast<int>(fastmod(v, static_cast<uint64_t>(i), mag));
-          T* pj = items.at(j);
-          const T x = *pj;
-          *pj = *items.at(i - 1);
-          f.add(tab[x], ctot, pw);  // slot i-1 is final: it holds x
-        }
-        if (R >= 1) f.add(tab[*items.at(0)], ctot, pw);
+        shuffle_fold(ws, R, items, f, tab, ctot, pw, s_lim, s_mag);
       }
       if (f.G > 0) f.best = max(f.best, pw[0]);  // bin 0: computes needing no recv
-      const int64_t tcpu = f.best < 0 ? 0 : f.best;
-      const int64_t mw = a.cluster ? max(tcpu, max(ctot, tcpu) + a.send_tot[w]) : max(tcpu, ctot);
+      const int64_t tcpu = f.best < 0 ? 0 : static_cast<int64_t>(f.best);
+      const int64_t c64 = static_cast<int64_t>(ctot);
+      const int64_t mw = a.cluster ? max(tcpu, max(c64, tcpu) + a.send_tot[w]) : max(tcpu, c64);
       if (a.worker_ms) a.worker_ms[idx * W + w] = mw;
       hi = max(hi, mw);
       lo = min(lo, mw);
@@ -209,8 +358,12 @@ __global__ void __launch_bounds__(kSweepThreads) chain_sweep_kernel(ChainArgs a)
     atomicAdd(&a.f64[1], ssum);
   }
   __syncthreads();
-  for (int k = threadIdx.x; k < 2 * kBins; k += blockDim.x)
-    if (s_hist[k]) atomicAdd(&a.i64[8 + k], static_cast<unsigned long long>(s_hist[k]));
+  if (a.do_e)
+    for (int k = threadIdx.x; k < kBins; k += blockDim.x)
+      if (s_hist[k]) atomicAdd(&a.i64[8 + k], static_cast<unsigned long long>(s_hist[k]));
+  if (a.cluster)
+    for (int k = threadIdx.x; k < kBins; k += blockDim.x)
+      if (s_shist[k]) atomicAdd(&a.i64[8 + kBins + k], static_cast<unsigned long long>(s_shist[k]));
 }
 
 __global__ void reset_kernel(unsigned long long* i64, double* f64) {
@@ -250,12 +403,19 @@ __global__ void random_orders_kernel(int R, int S, const uint64_t* __restrict__ 
 using namespace tictac_dev;
 
 struct SweepPlan {
-  int W = 1, R = 0, nc = 0, cluster = 0, stride = 1;
+  int W = 1, R = 0, nc = 0, cluster = 0, stride = 1, narrow = 0;
   int64_t U = 0, L = 0;
   void *tab = nullptr, *pwsuf = nullptr, *ctot = nullptr, *send = nullptr, *lim = nullptr, *mag = nullptr;
-  size_t smem = 0;
+  size_t smem = 0, smem_orders = 0;
   int blocks = 0;
 };
+
+using SweepFn = void (*)(ChainArgs);
+static SweepFn sweep_fn(const SweepPlan* p) {
+  if (p->R <= 256)
+    return p->narrow ? chain_sweep_kernel<uint8_t, false, int32_t> : chain_sweep_kernel<uint8_t, false, int64_t>;
+  return p->narrow ? chain_sweep_kernel<uint16_t, false, int32_t> : chain_sweep_kernel<uint16_t, false, int64_t>;
+}
 
 extern "C" SweepPlan* csk_sweep_plan(int32_t W, int32_t R, int32_t nc, const int64_t* d,
                                      const int32_t* first, const int64_t* pwsuf,
@@ -294,19 +454,18 @@ extern "C" SweepPlan* csk_sweep_plan(int32_t W, int32_t R, int32_t nc, const int
     csk_sweep_plan_free(p);
     return nullptr;
   }
-  const int per_word = R <= 256 ? 4 : 2;
-  p->smem = sizeof(uint2) * W * R + sizeof(int64_t) * W * p->stride + sizeof(int) * 2 * kBins +
-            sizeof(uint32_t) * kSweepThreads * ((R + per_word - 1) / per_word + 1);
+  // 32-bit fold when every prefix/suffix time sum fits (U bounds them all)
+  p->narrow = U < (int64_t{1} << 31) ? 1 : 0;
+  const int nhist = (!cluster && U != L ? 1 : 0) + (cluster ? 1 : 0);
+  p->smem = sweep_smem(R, W, p->stride, nhist, p->narrow ? 4 : 8);
+  p->smem_orders = sweep_smem(R, W, p->stride, nhist, 8);
   int dev = 0, sms = 148, occ = 1;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const void* fn = R <= 256 ? reinterpret_cast<const void*>(chain_sweep_kernel<uint8_t, false>)
-                            : reinterpret_cast<const void*>(chain_sweep_kernel<uint16_t, false>);
-  if (p->smem > 48 * 1024) {
-    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(p->smem));
-    cudaFuncSetAttribute(reinterpret_cast<const void*>(chain_sweep_kernel<uint8_t, true>),
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(p->smem));
-  }
+  const void* fn = reinterpret_cast<const void*>(sweep_fn(p));
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(p->smem));
+  cudaFuncSetAttribute(reinterpret_cast<const void*>(chain_sweep_kernel<uint8_t, true, int64_t>),
+                       cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(p->smem_orders));
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kSweepThreads, p->smem);
   if (occ < 1) {
     std::snprintf(err, 256, "sweep plan needs %zu bytes of shared memory per block", p->smem);
@@ -367,10 +526,7 @@ extern "C" int csk_sweep_run(SweepPlan* p, uint64_t seed_lo, int64_t count, uint
   const int64_t need = (count + kSweepThreads - 1) / kSweepThreads;
   const int blocks = static_cast<int>(std::min<int64_t>(p->blocks, need));
   auto st = static_cast<cudaStream_t>(stream);
-  if (p->R <= 256)
-    chain_sweep_kernel<uint8_t, false><<<blocks, kSweepThreads, p->smem, st>>>(a);
-  else
-    chain_sweep_kernel<uint16_t, false><<<blocks, kSweepThreads, p->smem, st>>>(a);
+  sweep_fn(p)<<<blocks, kSweepThreads, p->smem, st>>>(a);
   LAUNCHED();
   CK(cudaGetLastError());
   return 0;
@@ -397,7 +553,7 @@ extern "C" int csk_sweep_orders(SweepPlan* p, const int32_t* d_orders, int64_t n
   a.f64 = static_cast<double*>(f64);
   a.do_e = 0;
   const int blocks = static_cast<int>(std::min<int64_t>(p->blocks, (n + kSweepThreads - 1) / kSweepThreads));
-  chain_sweep_kernel<uint8_t, true><<<blocks, kSweepThreads, p->smem, st>>>(a);
+  chain_sweep_kernel<uint8_t, true, int64_t><<<blocks, kSweepThreads, p->smem_orders, st>>>(a);
   LAUNCHED();
   cudaError_t e = cudaGetLastError();
   cudaStreamSynchronize(st);
