@@ -133,12 +133,18 @@ __device__ __forceinline__ uint64_t fastmod(uint64_t v, uint64_t n, uint64_t mag
   return r;
 }
 
-// Same, remainder only: r = v - q*n < 2n < 2^32 is exact in the low word.
+// Same, remainder only: r = v - q*n < 2n < 2^32 is exact in the low word;
+// the conditional subtract is an unsigned min (r - n wraps when r < n).
 __device__ __forceinline__ uint32_t fastmod32(uint64_t v, uint32_t n, uint64_t magic) {
   const uint64_t q = __umul64hi(v, magic);
-  uint32_t r = static_cast<uint32_t>(v) - static_cast<uint32_t>(q) * n;
-  if (r >= n) r -= n;
-  return r;
+  const uint32_t r = static_cast<uint32_t>(v) - static_cast<uint32_t>(q) * n;
+  return min(r, r - n);
+}
+
+// bounded() rejects v > UINT64_MAX - (2^64 mod n); for n < 2^32 that needs
+// the high word to be all ones, so the common test is one 32-bit compare.
+__device__ __forceinline__ bool maybe_reject(uint64_t v) {
+  return static_cast<uint32_t>(v >> 32) == 0xFFFFFFFFu;
 }
 
 inline void bounded_consts(uint64_t n, uint64_t* limit, uint64_t* magic) {

@@ -128,9 +128,10 @@ __device__ __forceinline__ void fy_draw(const Items<T>& items, int i, int j, Fol
 // Generic continuation after a bounded() rejection (probability ~R·2^-64
 // per draw) or past the first 311 outputs: full mt19937_64 state in local
 // memory, advanced to output `out` (0-based), then the reference loop.
+// (Everything by value: no address-taken locals in the hot caller.)
 template <typename T, typename V>
-__device__ __noinline__ void shuffle_slow(uint64_t seed, int out, int i, const Items<T>* items, FoldT<V>* f,
-                                          const uint2* tab, V ctot, const V* pw) {
+__device__ __noinline__ FoldT<V> shuffle_slow(uint64_t seed, int out, int i, Items<T> items, FoldT<V> f,
+                                              const uint2* tab, V ctot, const V* pw) {
   uint64_t st[312];
   MtFull m{st, 0};
   m.seed(seed);
@@ -141,15 +142,50 @@ __device__ __noinline__ void shuffle_slow(uint64_t seed, int out, int i, const I
     uint64_t v;
     do v = m.next();
     while (v > limit);
-    fy_draw(*items, i, static_cast<int>(v % n), *f, tab, ctot, pw);
+    fy_draw(items, i, static_cast<int>(v % n), f, tab, ctot, pw);
   }
-  f->add(tab[*items->at(0)], ctot, pw);
+  f.add(tab[*items.at(0)], ctot, pw);
+  return f;
+}
+
+// Draws d..d+K-1 with outputs v[] (pre-checked only by maybe_reject):
+// precise bounded() rejection test, then the swaps. Returns true when a
+// rejection sent the rest of the shuffle to the exact slow path.
+template <int K, typename T, typename V>
+__device__ __forceinline__ bool draw_group(uint64_t seed, int R, int d, const uint64_t (&v)[K],
+                                           const Items<T>& items, FoldT<V>& f, const uint2* tab, V ctot,
+                                           const V* pw, const uint64_t* s_lim, const uint64_t* s_mag) {
+  int j[K];
+  bool any = false;
+#pragma unroll
+  for (int q = 0; q < K; ++q) {
+    const int i = R - d - q;
+    j[q] = static_cast<int>(fastmod32(v[q], static_cast<uint32_t>(i), s_mag[i]));
+    any |= maybe_reject(v[q]);
+  }
+  if (any) {  // probability ~2^-32 per draw; exact handling, draw by draw
+#pragma unroll  // (static indices: keeps v[] and j[] in registers)
+    for (int q = 0; q < K; ++q) {
+      const int i = R - d - q;
+      if (v[q] > s_lim[i]) {
+        f = shuffle_slow(seed, d + q + 1, i, items, f, tab, ctot, pw);
+        return true;
+      }
+      fy_draw(items, i, j[q], f, tab, ctot, pw);
+    }
+    return false;
+  }
+#pragma unroll
+  for (int q = 0; q < K; ++q) fy_draw(items, R - d - q, j[q], f, tab, ctot, pw);
+  return false;
 }
 
 // random_schedule(seed) over R recv columns folded right-to-left. Fast path:
 // draw d uses mt output d (no rejection) computed by register cursors —
 // phase 1 (d < 156): t_d = f(s_d, s_d+1) ^ s_{d+156}; phase 2 (d < 311):
 // t_d = f(s_d, s_d+1) ^ t_{d-156}, t_{d-156} = f(s_{d-156}, s_{d-155}) ^ s_d.
+// Four draws per iteration: four independent twist/temper/bounded chains
+// before the dependent shared-memory swaps.
 template <typename T, typename V>
 __device__ __forceinline__ void shuffle_fold(uint64_t seed, int R, const Items<T>& items, FoldT<V>& f,
                                              const uint2* tab, V ctot, const V* pw,
@@ -161,95 +197,51 @@ __device__ __forceinline__ void shuffle_fold(uint64_t seed, int R, const Items<T
   const int draws = R - 1;
   const int n1 = min(draws, 156);
   int d = 0;
-  // Pairs of draws: both mt outputs, rejection tests and bounded() values
-  // are computed before the two dependent shared-memory swaps, giving the
-  // scheduler two independent 64-bit chains per iteration.
-  for (; d + 1 < n1; d += 2) {
-    const uint64_t t0 = mt_twist(a0, a1, b);
-    const uint64_t a2 = mt_step(a1, static_cast<uint32_t>(d + 2));
-    const uint64_t b1 = mt_step(b, static_cast<uint32_t>(d + 157));
-    const uint64_t t1 = mt_twist(a1, a2, b1);
-    a0 = a2;
-    a1 = mt_step(a2, static_cast<uint32_t>(d + 3));
-    b = mt_step(b1, static_cast<uint32_t>(d + 158));
-    const uint64_t v0 = mt_temper(t0), v1 = mt_temper(t1);
-    const int i0 = R - d, i1 = i0 - 1;
-    const bool r0 = v0 > s_lim[i0], r1 = v1 > s_lim[i1];
-    const int j0 = static_cast<int>(fastmod32(v0, static_cast<uint32_t>(i0), s_mag[i0]));
-    const int j1 = static_cast<int>(fastmod32(v1, static_cast<uint32_t>(i1), s_mag[i1]));
-    if (r0 | r1) {
-      if (r0) {
-        shuffle_slow(seed, d + 1, i0, &items, &f, tab, ctot, pw);
-      } else {
-        fy_draw(items, i0, j0, f, tab, ctot, pw);
-        shuffle_slow(seed, d + 2, i1, &items, &f, tab, ctot, pw);
-      }
-      return;
-    }
-    fy_draw(items, i0, j0, f, tab, ctot, pw);
-    fy_draw(items, i1, j1, f, tab, ctot, pw);
+  for (; d + 3 < n1; d += 4) {  // phase 1, a = (s_d, s_d+1), b = s_d+156
+    const uint32_t u = static_cast<uint32_t>(d);
+    const uint64_t a2 = mt_step(a1, u + 2), a3 = mt_step(a2, u + 3), a4 = mt_step(a3, u + 4);
+    const uint64_t b1 = mt_step(b, u + 157), b2 = mt_step(b1, u + 158), b3 = mt_step(b2, u + 159);
+    const uint64_t v[4] = {mt_temper(mt_twist(a0, a1, b)), mt_temper(mt_twist(a1, a2, b1)),
+                           mt_temper(mt_twist(a2, a3, b2)), mt_temper(mt_twist(a3, a4, b3))};
+    a0 = a4;
+    a1 = mt_step(a4, u + 5);
+    b = mt_step(b3, u + 160);
+    if (draw_group<4>(seed, R, d, v, items, f, tab, ctot, pw, s_lim, s_mag)) return;
   }
   for (; d < n1; ++d) {
-    const uint64_t t = mt_twist(a0, a1, b);
+    const uint64_t v[1] = {mt_temper(mt_twist(a0, a1, b))};
     a0 = a1;
     a1 = mt_step(a1, static_cast<uint32_t>(d + 2));
     b = mt_step(b, static_cast<uint32_t>(d + 157));
-    const uint64_t v = mt_temper(t);
-    const int i = R - d;
-    if (v > s_lim[i]) {
-      shuffle_slow(seed, d + 1, i, &items, &f, tab, ctot, pw);
-      return;
-    }
-    fy_draw(items, i, static_cast<int>(fastmod32(v, static_cast<uint32_t>(i), s_mag[i])), f, tab, ctot, pw);
+    if (draw_group<1>(seed, R, d, v, items, f, tab, ctot, pw, s_lim, s_mag)) return;
   }
-  if (d < draws) {
+  if (d < draws) {  // phase 2, c = (s_d-156, s_d-155)
     uint64_t c0 = seed, c1 = mt_step(seed, 1);
     const int n2 = min(draws, 311);
-    for (; d + 1 < n2; d += 2) {
-      const uint64_t back0 = mt_twist(c0, c1, a0);
-      const uint64_t t0 = mt_twist(a0, a1, back0);
-      const uint64_t a2 = mt_step(a1, static_cast<uint32_t>(d + 2));
-      const uint64_t c2 = mt_step(c1, static_cast<uint32_t>(d - 154));
-      const uint64_t back1 = mt_twist(c1, c2, a1);
-      const uint64_t t1 = mt_twist(a1, a2, back1);
-      a0 = a2;
-      a1 = mt_step(a2, static_cast<uint32_t>(d + 3));
-      c0 = c2;
-      c1 = mt_step(c2, static_cast<uint32_t>(d - 153));
-      const uint64_t v0 = mt_temper(t0), v1 = mt_temper(t1);
-      const int i0 = R - d, i1 = i0 - 1;
-      const bool r0 = v0 > s_lim[i0], r1 = v1 > s_lim[i1];
-      const int j0 = static_cast<int>(fastmod32(v0, static_cast<uint32_t>(i0), s_mag[i0]));
-      const int j1 = static_cast<int>(fastmod32(v1, static_cast<uint32_t>(i1), s_mag[i1]));
-      if (r0 | r1) {
-        if (r0) {
-          shuffle_slow(seed, d + 1, i0, &items, &f, tab, ctot, pw);
-        } else {
-          fy_draw(items, i0, j0, f, tab, ctot, pw);
-          shuffle_slow(seed, d + 2, i1, &items, &f, tab, ctot, pw);
-        }
-        return;
-      }
-      fy_draw(items, i0, j0, f, tab, ctot, pw);
-      fy_draw(items, i1, j1, f, tab, ctot, pw);
+    for (; d + 3 < n2; d += 4) {
+      const uint32_t u = static_cast<uint32_t>(d);
+      const uint64_t a2 = mt_step(a1, u + 2), a3 = mt_step(a2, u + 3), a4 = mt_step(a3, u + 4);
+      const uint64_t c2 = mt_step(c1, u - 154), c3 = mt_step(c2, u - 153), c4 = mt_step(c3, u - 152);
+      const uint64_t v[4] = {mt_temper(mt_twist(a0, a1, mt_twist(c0, c1, a0))),
+                             mt_temper(mt_twist(a1, a2, mt_twist(c1, c2, a1))),
+                             mt_temper(mt_twist(a2, a3, mt_twist(c2, c3, a2))),
+                             mt_temper(mt_twist(a3, a4, mt_twist(c3, c4, a3)))};
+      a0 = a4;
+      a1 = mt_step(a4, u + 5);
+      c0 = c4;
+      c1 = mt_step(c4, u - 151);
+      if (draw_group<4>(seed, R, d, v, items, f, tab, ctot, pw, s_lim, s_mag)) return;
     }
     for (; d < n2; ++d) {
-      const uint64_t back = mt_twist(c0, c1, a0);
-      const uint64_t t = mt_twist(a0, a1, back);
+      const uint64_t v[1] = {mt_temper(mt_twist(a0, a1, mt_twist(c0, c1, a0)))};
       a0 = a1;
       a1 = mt_step(a1, static_cast<uint32_t>(d + 2));
       c0 = c1;
       c1 = mt_step(c1, static_cast<uint32_t>(d - 154));
-      const uint64_t v = mt_temper(t);
-      const int i = R - d;
-      if (v > s_lim[i]) {
-        shuffle_slow(seed, d + 1, i, &items, &f, tab, ctot, pw);
-        return;
-      }
-      fy_draw(items, i, static_cast<int>(fastmod32(v, static_cast<uint32_t>(i), s_mag[i])), f, tab, ctot, pw);
+      if (draw_group<1>(seed, R, d, v, items, f, tab, ctot, pw, s_lim, s_mag)) return;
     }
-    if (d < draws) {
-      shuffle_slow(seed, d, R - d, &items, &f, tab, ctot, pw);
+    if (d < draws) {  // beyond the first block (R > 312)
+      f = shuffle_slow(seed, d, R - d, items, f, tab, ctot, pw);
       return;
     }
   }
@@ -265,7 +257,7 @@ __host__ __device__ inline size_t sweep_smem(int R, int W, int stride, int nhist
 }
 
 template <typename T, bool kOrders, typename V>
-__global__ void __launch_bounds__(kSweepThreads) chain_sweep_kernel(ChainArgs a) {
+__global__ void __launch_bounds__(kSweepThreads, 3) chain_sweep_kernel(ChainArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int R = a.R, W = a.W;
   uint64_t* s_lim = reinterpret_cast<uint64_t*>(smem);
