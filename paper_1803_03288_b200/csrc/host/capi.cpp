@@ -5,7 +5,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstring>
+#include <mutex>
 #include <string>
 
 #include "../../../include/commsched.h"
@@ -15,11 +17,23 @@
 
 using namespace tictac;
 
+namespace {
+std::atomic<uint64_t> g_oracle_ids{1};
+}
+
 struct cs_graph {
   std::shared_ptr<Graph> g;
+  // Last sweep plan built for (oracle id, policy): graph and oracle handles
+  // are immutable, so repeated sweeps reuse the device tables.
+  std::mutex mu;
+  std::shared_ptr<SweepCtx> sweep;
+  uint64_t sweep_oracle = 0;
+  bool sweep_gated = true;
+  double sweep_noise = 0.0;
 };
 struct cs_oracle {
   TimeOracle o;
+  uint64_t id = g_oracle_ids.fetch_add(1);
 };
 struct cs_schedule {
   Schedule s;
@@ -387,7 +401,21 @@ int cs_sweep_random(const cs_graph* g, const cs_oracle* o, uint64_t seed_lo, int
     need(o, "oracle");
     if (count < 0) fail(kParameter, "count must be non-negative");
     Policy p = policy_of(policy);
-    auto ctx = make_sweep(g->g, o->o, p);
+    std::shared_ptr<SweepCtx> ctx;
+    {
+      auto* gm = const_cast<cs_graph*>(g);
+      std::lock_guard<std::mutex> lock(gm->mu);
+      if (gm->sweep && gm->sweep_oracle == o->id && gm->sweep_gated == p.gated &&
+          gm->sweep_noise == p.noise) {
+        ctx = gm->sweep;
+      } else {
+        ctx = make_sweep(g->g, o->o, p);
+        gm->sweep = ctx;
+        gm->sweep_oracle = o->id;
+        gm->sweep_gated = p.gated;
+        gm->sweep_noise = p.noise;
+      }
+    }
     const bool cluster_m = ctx->cluster && makespans_out;  // needs the full event replica
     if (!ctx->fast || cluster_m) {
       sweep_exact(*ctx, seed_lo, count, makespans_out, worker_makespans_out, stats_out);
