@@ -21,6 +21,7 @@ namespace tictac_dev {
 namespace {
 
 constexpr int kWarpsPerBlock = 4;
+constexpr int kEmptyLo = 1 << 29;  // "no ready word" (no overflow when lanes are added)
 constexpr uint64_t kNoiseSalt = 0x9e3779b97f4a7c15ULL;  // sim.cpp:14
 
 struct GraphView {
@@ -56,53 +57,58 @@ struct RunSpec {
   int64_t* dev_end;  // [B][ndev]
 };
 
-// Scratch carved per warp slot.
+// Per-run state. "Hot" arrays (touched every event) live in shared memory
+// when a slot fits, else in global scratch; "cold" arrays always in global.
 struct Slot {
-  int32_t *missing, *gate, *orig, *seq, *prio, *items, *comp, *running, *comp_len, *ready_cnt;
+  // hot
+  int32_t *missing, *gate, *running, *comp_len, *ready_cnt, *lo, *hi, *haspri;
   uint32_t *ready, *forced;
-  int64_t *run_end, *counter, *dev_end;
-  uint64_t *mt, *mt2;
+  int64_t *run_end, *counter;
+  uint64_t* mt;
+  // cold
+  int32_t *orig, *seq, *prio, *items, *comp;
+  int64_t* dev_end;
+  uint64_t* mt2;
 };
 
 __host__ __device__ inline size_t align8(size_t x) { return (x + 7) & ~size_t(7); }
 
-__host__ __device__ inline size_t slot_bytes(int n, int nres, int ndev, int rbw, int R) {
-  size_t b = 0;
-  b += align8(4ull * n) * 6;         // missing gate orig seq prio comp
-  b += align8(4ull * (R + 1));       // items
-  b += align8(4ull * nres) * 3;      // running comp_len ready_cnt
-  b += align8(4ull * (rbw + 1));     // ready
-  b += align8(4ull * ((n + 31) / 32 + 1));  // forced
-  b += align8(8ull * nres) * 2;      // run_end counter
-  b += align8(8ull * (ndev + 1));    // dev_end
-  b += 8ull * 312 * 2;               // mt mt2
-  return b;
+__host__ __device__ inline size_t hot_bytes(int n, int nres, int rbw) {
+  return align8(4ull * n) * 2 + align8(4ull * nres) * 6 + align8(4ull * (rbw + 1)) +
+         align8(4ull * ((n + 31) / 32 + 1)) + align8(8ull * nres) * 2 + 8ull * 312;
 }
 
-__device__ Slot carve(char* base, int n, int nres, int ndev, int rbw, int R) {
+__host__ __device__ inline size_t cold_bytes(int n, int ndev, int R) {
+  return align8(4ull * n) * 4 + align8(4ull * (R + 1)) + align8(8ull * (ndev + 1)) + 8ull * 312;
+}
+
+__device__ Slot carve(char* hot, char* cold, int n, int nres, int ndev, int rbw, int R) {
   Slot s;
-  auto take = [&](size_t bytes) {
+  auto take = [](char*& base, size_t bytes) {
     char* p = base;
     base += align8(bytes);
     return p;
   };
-  s.missing = reinterpret_cast<int32_t*>(take(4ull * n));
-  s.gate = reinterpret_cast<int32_t*>(take(4ull * n));
-  s.orig = reinterpret_cast<int32_t*>(take(4ull * n));
-  s.seq = reinterpret_cast<int32_t*>(take(4ull * n));
-  s.prio = reinterpret_cast<int32_t*>(take(4ull * n));
-  s.comp = reinterpret_cast<int32_t*>(take(4ull * n));
-  s.items = reinterpret_cast<int32_t*>(take(4ull * (R + 1)));
-  s.running = reinterpret_cast<int32_t*>(take(4ull * nres));
-  s.comp_len = reinterpret_cast<int32_t*>(take(4ull * nres));
-  s.ready_cnt = reinterpret_cast<int32_t*>(take(4ull * nres));
-  s.ready = reinterpret_cast<uint32_t*>(take(4ull * (rbw + 1)));
-  s.forced = reinterpret_cast<uint32_t*>(take(4ull * ((n + 31) / 32 + 1)));
-  s.run_end = reinterpret_cast<int64_t*>(take(8ull * nres));
-  s.counter = reinterpret_cast<int64_t*>(take(8ull * nres));
-  s.dev_end = reinterpret_cast<int64_t*>(take(8ull * (ndev + 1)));
-  s.mt = reinterpret_cast<uint64_t*>(take(8ull * 312));
-  s.mt2 = reinterpret_cast<uint64_t*>(take(8ull * 312));
+  s.missing = reinterpret_cast<int32_t*>(take(hot, 4ull * n));
+  s.gate = reinterpret_cast<int32_t*>(take(hot, 4ull * n));
+  s.running = reinterpret_cast<int32_t*>(take(hot, 4ull * nres));
+  s.comp_len = reinterpret_cast<int32_t*>(take(hot, 4ull * nres));
+  s.ready_cnt = reinterpret_cast<int32_t*>(take(hot, 4ull * nres));
+  s.lo = reinterpret_cast<int32_t*>(take(hot, 4ull * nres));
+  s.hi = reinterpret_cast<int32_t*>(take(hot, 4ull * nres));
+  s.haspri = reinterpret_cast<int32_t*>(take(hot, 4ull * nres));
+  s.ready = reinterpret_cast<uint32_t*>(take(hot, 4ull * (rbw + 1)));
+  s.forced = reinterpret_cast<uint32_t*>(take(hot, 4ull * ((n + 31) / 32 + 1)));
+  s.run_end = reinterpret_cast<int64_t*>(take(hot, 8ull * nres));
+  s.counter = reinterpret_cast<int64_t*>(take(hot, 8ull * nres));
+  s.mt = reinterpret_cast<uint64_t*>(take(hot, 8ull * 312));
+  s.orig = reinterpret_cast<int32_t*>(take(cold, 4ull * n));
+  s.seq = reinterpret_cast<int32_t*>(take(cold, 4ull * n));
+  s.prio = reinterpret_cast<int32_t*>(take(cold, 4ull * n));
+  s.comp = reinterpret_cast<int32_t*>(take(cold, 4ull * n));
+  s.items = reinterpret_cast<int32_t*>(take(cold, 4ull * (R + 1)));
+  s.dev_end = reinterpret_cast<int64_t*>(take(cold, 8ull * (ndev + 1)));
+  s.mt2 = reinterpret_cast<uint64_t*>(take(cold, 8ull * 312));
   return s;
 }
 
@@ -188,11 +194,14 @@ __device__ void fill_priorities(const GraphView& G, const RunSpec& rs, const Slo
 }
 
 __global__ void __launch_bounds__(32 * kWarpsPerBlock)
-    event_sim_kernel(GraphView G, RunSpec rs, int64_t B, char* scratch, size_t slot_sz, int rbw) {
+    event_sim_kernel(GraphView G, RunSpec rs, int64_t B, char* hot_global, size_t hot_sz, char* cold_scr,
+                     size_t cold_sz, int rbw) {
+  extern __shared__ __align__(16) char smem_hot[];
   const int lane = threadIdx.x & 31;
   const int64_t slot_id = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nslots = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
-  const Slot s = carve(scratch + slot_id * slot_sz, G.n, G.nres, G.ndev, rbw, G.R);
+  char* hot = hot_global ? hot_global + slot_id * hot_sz : smem_hot + (threadIdx.x >> 5) * hot_sz;
+  const Slot s = carve(hot, cold_scr + slot_id * cold_sz, G.n, G.nres, G.ndev, rbw, G.R);
   const int n = G.n, nres = G.nres;
 
   for (int64_t b = slot_id; b < B; b += nslots) {
@@ -212,15 +221,22 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock)
       s.counter[r] = 0;
       s.comp_len[r] = 0;
       s.ready_cnt[r] = 0;
+      s.lo[r] = kEmptyLo;  // scan window of non-empty ready words (empty: lo > hi)
+      s.hi[r] = -1;
+      s.haspri[r] = 0;
     }
     for (int d = lane; d < G.ndev; d += 32) s.dev_end[d] = 0;
     __syncwarp();
-    for (int i = lane; i < n; i += 32)
+    for (int i = lane; i < n; i += 32) {
+      if (s.prio[i] >= 0) s.haspri[G.res[i]] = 1;
       if (s.missing[i] == 0) {
         const int r = G.res[i], l = G.lidx[i];
         atomicOr(&s.ready[G.rb_off[r] + (l >> 5)], 1u << (l & 31));
         atomicAdd(&s.ready_cnt[r], 1);
+        atomicMin(&s.lo[r], l >> 5);
+        atomicMax(&s.hi[r], l >> 5);
       }
+    }
     // dense per-channel ranks from (priority, id), then noise swaps
     MtFull noise{s.mt2, 0};
     const bool noisy = rs.gated && rs.noise > 0.0;
@@ -290,8 +306,10 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock)
     };
 
     // candidate mask of one ready word (word w of resource r)
-    auto cand_mask = [&](int r, int w, int best) -> uint32_t {
-      uint32_t bits = s.ready[G.rb_off[r] + w], m = 0;
+    auto cand_mask = [&](int r, int w, int best, bool pri) -> uint32_t {
+      uint32_t bits = s.ready[G.rb_off[r] + w];
+      if (!pri) return bits;  // no priorities on r: every ready op is a candidate
+      uint32_t m = 0;
       const int base = G.rops_off[r] + (w << 5);
       while (bits) {
         const int bit = __ffs(bits) - 1;
@@ -305,10 +323,17 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock)
 
     auto try_start = [&](int r) -> bool {  // sim.cpp:163-192
       if (s.running[r] >= 0 || s.ready_cnt[r] == 0) return false;
-      const int nw = G.rb_off[r + 1] - G.rb_off[r];
-      int best = 0x7fffffff;
-      for (int w = lane; w < nw; w += 32) {
-        uint32_t bits = s.ready[G.rb_off[r] + w];
+      const bool pri = s.haspri[r] != 0;
+      const int w0 = s.lo[r], w1 = s.hi[r];  // every ready bit lies in [w0, w1]
+      int best = 0x7fffffff, nlo = kEmptyLo, nhi = -1;
+      for (int c = w0; c <= w1; c += 32) {
+        const int w = c + lane;
+        uint32_t bits = w <= w1 ? s.ready[G.rb_off[r] + w] : 0u;
+        if (bits) {
+          nlo = min(nlo, w);
+          nhi = max(nhi, w);
+        }
+        if (!pri) continue;
         const int base = G.rops_off[r] + (w << 5);
         while (bits) {
           const int bit = __ffs(bits) - 1;
@@ -319,13 +344,25 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock)
         }
       }
 #pragma unroll
-      for (int o = 16; o; o >>= 1) best = min(best, __shfl_xor_sync(~0u, best, o));
+      for (int o = 16; o; o >>= 1) {
+        best = min(best, __shfl_xor_sync(~0u, best, o));
+        nlo = min(nlo, __shfl_xor_sync(~0u, nlo, o));
+        nhi = max(nhi, __shfl_xor_sync(~0u, nhi, o));
+      }
+      __syncwarp();
+      if (lane == 0) {  // tighten the window to the non-empty words
+        s.lo[r] = nlo;
+        s.hi[r] = nhi;
+      }
       int total = 0;
-      for (int c = 0; c < nw; c += 32) {
-        const uint32_t m = (c + lane < nw) ? cand_mask(r, c + lane, best) : 0u;
+      for (int c = nlo; c <= nhi; c += 32) {
+        const uint32_t m = (c + lane <= nhi) ? cand_mask(r, c + lane, best, pri) : 0u;
         total += warp_sum(__popc(m));
       }
-      if (total == 0) return false;
+      if (total == 0) {
+        __syncwarp();
+        return false;
+      }
       int k = 0;
       if (total > 1) {
         uint64_t kk = 0;
@@ -333,8 +370,8 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock)
         k = static_cast<int>(__shfl_sync(~0u, kk, 0));
       }
       int pick = -1;
-      for (int c = 0; c < nw && pick < 0; c += 32) {
-        const uint32_t m = (c + lane < nw) ? cand_mask(r, c + lane, best) : 0u;
+      for (int c = nlo; c <= nhi && pick < 0; c += 32) {
+        const uint32_t m = (c + lane <= nhi) ? cand_mask(r, c + lane, best, pri) : 0u;
         const int cnt = __popc(m);
         int incl = cnt;
 #pragma unroll
@@ -381,6 +418,8 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock)
             const int rw = G.res[w], l = G.lidx[w];
             atomicOr(&s.ready[G.rb_off[rw] + (l >> 5)], 1u << (l & 31));
             atomicAdd(&s.ready_cnt[rw], 1);
+            atomicMin(&s.lo[rw], l >> 5);
+            atomicMax(&s.hi[rw], l >> 5);
           }
         }
         __syncwarp();
@@ -403,8 +442,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock)
       if (next_t == INT64_MAX) {  // forced release, sim.cpp:211-229
         int64_t key = INT64_MAX;
         for (int r = 0; r < nres; ++r) {
-          const int nw = G.rb_off[r + 1] - G.rb_off[r];
-          for (int w = lane; w < nw; w += 32) {
+          for (int w = s.lo[r] + lane; w <= s.hi[r]; w += 32) {
             uint32_t bits = s.ready[G.rb_off[r] + w];
             const int base = G.rops_off[r] + (w << 5);
             while (bits) {
@@ -472,7 +510,7 @@ int run_event(DeviceGraph* g, const int64_t* dur, int64_t B, RunSpec rs, int64_t
               char* err) {
   if (ensure_device(err)) return 1;
   if (B <= 0) return 0;
-  DevBuf d_dur, d_ms, d_vio, d_st, d_start, d_end, d_dev, d_scr, d_lim, d_mag;
+  DevBuf d_dur, d_ms, d_vio, d_st, d_start, d_end, d_dev, d_scr, d_hot, d_lim, d_mag;
   if (dev_copy(d_dur, dur, g->n, err)) return 1;
   std::vector<uint64_t> lim(4096), mag(4096);
   for (uint64_t k = 0; k < 4096; ++k) bounded_consts(k, &lim[k], &mag[k]);
@@ -507,14 +545,31 @@ int run_event(DeviceGraph* g, const int64_t* dur, int64_t B, RunSpec rs, int64_t
     CK(cudaGetDevice(&dev));
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   }
-  const int64_t max_slots = static_cast<int64_t>(sms) * 16;
-  const int64_t slots = std::min<int64_t>(B, max_slots);
-  const int blocks = static_cast<int>((slots + kWarpsPerBlock - 1) / kWarpsPerBlock);
-  const int64_t total_slots = static_cast<int64_t>(blocks) * kWarpsPerBlock;
-  const size_t ssz = align8(slot_bytes(g->n, g->nres, g->ndev, g->rb_words, g->R));
-  CK(cudaMalloc(&d_scr.p, ssz * static_cast<size_t>(total_slots)));
-  event_sim_kernel<<<blocks, 32 * kWarpsPerBlock>>>(G, rs, B, static_cast<char*>(d_scr.p), ssz,
-                                                    g->rb_words);
+  // Hot per-run state in shared memory when a slot fits (up to
+  // kWarpsPerBlock runs per block), otherwise in global scratch.
+  const size_t hsz = align8(hot_bytes(g->n, g->nres, g->rb_words));
+  const size_t csz = align8(cold_bytes(g->n, g->ndev, g->R));
+  // Shared memory wins per run (~1.7x) but caps runs per SM; large batches
+  // of long runs keep more warps in flight with global scratch instead.
+  constexpr size_t kSmemBudget = 200 * 1024;
+  const int64_t smem_runs = static_cast<int64_t>(sms) * std::max<int64_t>(1, (227 * 1024) / std::max<size_t>(hsz, 1));
+  const bool in_smem = hsz <= kSmemBudget && (B <= smem_runs || hsz <= 16 * 1024);
+  const int wpb = in_smem ? static_cast<int>(std::min<size_t>(kWarpsPerBlock, kSmemBudget / hsz)) : kWarpsPerBlock;
+  int per_sm = 16;
+  if (in_smem) {
+    CK(cudaFuncSetAttribute(event_sim_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            static_cast<int>(hsz * wpb)));
+    int occ = 1;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, event_sim_kernel, 32 * wpb, hsz * wpb));
+    per_sm = std::max(1, occ) * wpb;
+  }
+  const int64_t slots = std::min<int64_t>(B, static_cast<int64_t>(sms) * per_sm);
+  const int blocks = static_cast<int>((slots + wpb - 1) / wpb);
+  const int64_t total_slots = static_cast<int64_t>(blocks) * wpb;
+  CK(cudaMalloc(&d_scr.p, csz * static_cast<size_t>(total_slots)));
+  if (!in_smem) CK(cudaMalloc(&d_hot.p, hsz * static_cast<size_t>(total_slots)));
+  event_sim_kernel<<<blocks, 32 * wpb, in_smem ? hsz * wpb : 0>>>(
+      G, rs, B, static_cast<char*>(d_hot.p), hsz, static_cast<char*>(d_scr.p), csz, g->rb_words);
   LAUNCHED();
   CK(cudaGetLastError());
   CK(cudaDeviceSynchronize());
