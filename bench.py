@@ -152,22 +152,99 @@ def cpu_baseline(path, target_s=10.0):
     rate = cal["sims"] / max(cal["seconds"], 1e-9)
     n = max(cores, int(rate * target_s))
     r = ref_sweep(path, SEED_LO, n, cores)
-    return {"value": r["sims"] / r["seconds"], "unit": "sims/s", "cores": cores, "kind": "reference",
-            "sample": f"seeds {SEED_LO}..{SEED_LO + n - 1} of the same workload ({n} sims, "
-                      f"{r['seconds']:.1f} s wall, {cores} threads, oracle/_ref libcommsched -O3)"}
+    out = {"value": r["sims"] / r["seconds"], "unit": "sims/s", "cores": cores, "kind": "reference",
+           "sample": f"seeds {SEED_LO}..{SEED_LO + n - 1} of the same workload ({n} sims, "
+                     f"{r['seconds']:.1f} s wall, {cores} threads, oracle/_ref libcommsched -O3)"}
+    # reference TIC/TAC wall time on config 1 (single thread: the reference has none)
+    try:
+        from paper_1803_03288_b200 import capi
+        g1 = capi.Lib().model("resnet_v2_50_inference", 1)
+        p1 = os.path.join(os.path.dirname(path), "config1.json")
+        with open(p1, "w") as f:
+            f.write(g1.serialize())
+        for algo, arg in (("tac", "declared"), ("tic", "amended")):
+            rr = subprocess.run([oracle.REF_SWEEP, algo, p1, arg], capture_output=True, text=True, check=True)
+            out[f"{algo}_config1_seconds"] = json.loads(rr.stderr.strip().splitlines()[-1])["seconds"]
+    except Exception as e:  # reported, not fatal
+        out["tac_error"] = str(e)[:200]
+    return out
 
 
-def tac_times(lib):
-    """TAC wall time (device) on the config DAGs, seconds."""
+def tac_times(lib, top=False):
+    """TAC wall time through cs_schedule_tac (device), seconds; SURVEY §8d
+    configs 1, 2, 4 and the config-5 layered sweep."""
     out = {}
-    for name in ("resnet_v2_50_inference", "inception_v3_training", "resnet_v2_101_training",
-                 "layered:10000:1000", "layered:100000:10000"):
+    names = ["resnet_v2_50_inference", "inception_v3_training", "resnet_v2_101_training",
+             "layered:10000:1000", "layered:100000:10000"] + (["layered:1000000:100000"] if top else [])
+    for name in names:
         g = lib.model(name, 1)
         o = g.declared()
-        g.tac(o)  # warm (upload + context)
+        if not name.startswith("layered:1000000"):
+            g.tac(o)  # warm (upload + context)
         t = time.perf_counter()
         g.tac(o)
         out[name] = round(time.perf_counter() - t, 6)
+    return out
+
+
+def sweep_rate(g, o, count):
+    g.sweep_random(o, 1, min(count, 1 << 16))  # plan + warm
+    t = time.perf_counter()
+    st = g.sweep_random(o, 1, count)
+    return st, count / (time.perf_counter() - t)
+
+
+def other_configs(lib):
+    """SURVEY §8d configs 1-3 through the public C ABI (e2e, host buffers)."""
+    from paper_1803_03288_b200 import capi
+    out = {}
+    # config 1: ResNet-v2-50 inference — TIC (both modes) + TAC, each simulated
+    g = lib.model("resnet_v2_50_inference", 1)
+    o = g.declared()
+    U, L = g.bounds(o)
+    c1 = {"ops": g.op_count(), "recvs": g.recv_count()}
+    for name, fn in (("tic_amended", lambda: g.tic("amended")), ("tic_literal", lambda: g.tic("literal")),
+                     ("tac", lambda: g.tac(o))):
+        fn()
+        t = time.perf_counter()
+        s = fn()
+        dt = time.perf_counter() - t
+        r = g.simulate(o, s)
+        m = json.loads(g.metrics_text(o, r))
+        c1[name] = {"seconds": round(dt, 6), "makespan_us": r.makespan(), "E": m["E"]}
+    st, rate = sweep_rate(g, o, 1000)
+    c1["random_1000"] = {"min_us": st["min_us"], "mean_us": st["sum_us"] / st["count"], "sims_per_s": rate}
+    out["config1_resnet_v2_50_inference"] = c1
+    # config 2: Inception-v3 training — TAC + 1M random orders, E histogram
+    g = lib.model("inception_v3_training", 1)
+    o = g.declared()
+    U, L = g.bounds(o)
+    g.tac(o)
+    t = time.perf_counter()
+    s = g.tac(o)
+    tac_s = time.perf_counter() - t
+    m_tac = g.simulate(o, s).makespan()
+    st, rate = sweep_rate(g, o, 1_000_000)
+    h = st["e_hist"]
+    mean_e = (U * st["count"] - st["sum_us"]) / (st["count"] * (U - L))
+    out["config2_inception_v3_training"] = {
+        "tac_seconds": round(tac_s, 6), "tac_makespan_us": m_tac,
+        "tac_E": (U - m_tac) / (U - L), "random_orders": st["count"], "sims_per_s": rate,
+        "min_us": st["min_us"], "argmin_seed": st["argmin_seed"], "mean_E": mean_e,
+        "E_hist_nonzero_bins": int((h > 0).sum()), "E_best_bin": int(max(i for i in range(1000) if h[i]))}
+    # config 3: VGG-16 training, 4 workers / 1 PS — straggler spread
+    v = lib.model("vgg16_training", 1).expand(4, 1, 0)
+    o = v.declared()
+    st, rate = sweep_rate(v, o, 1_000_000)
+    sh = st["straggler_hist"]
+    r_tic = v.simulate(o, v.tic())
+    strag_tic = json.loads(r_tic.iteration_json())["straggler"]
+    out["config3_vgg16_4workers"] = {
+        "random_orders": st["count"], "sims_per_s": rate, "workers": st["n_workers"],
+        "straggler_mean": st["straggler_sum"] / st["count"],
+        "straggler_max_bin": int(max(i for i in range(1000) if sh[i])),
+        "iteration_min_us": st["min_us"], "iteration_max_us": st["max_us"],
+        "tic_common_order_straggler": strag_tic}
     return out
 
 
@@ -216,6 +293,8 @@ def main():
     ap.add_argument("--count", type=int, default=COUNT)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-tac", action="store_true")
+    ap.add_argument("--no-configs", action="store_true")
+    ap.add_argument("--config5-top", action="store_true", help="also TAC at 10^6 ops / 10^5 recvs")
     args = ap.parse_args()
     rank, world, local = env_rank()
     if args.impl == "reference":
@@ -350,7 +429,9 @@ def main():
             "clocks": clocks.summary(),
         }
         if not args.no_tac:
-            out["tac_seconds"] = tac_times(lib)
+            out["tac_seconds"] = tac_times(lib, top=args.config5_top)
+        if not args.no_configs and world == 1:
+            out["configs"] = other_configs(lib)
         if not args.no_cpu and world == 1:
             out["cpu_baseline"] = cpu_baseline(path)
         print(json.dumps(out))
