@@ -318,9 +318,8 @@ def main():
     d_f64 = torch.zeros(capi.DSTATS_F64, dtype=torch.float64, device="cuda")
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device="cuda")
     count = args.count
-    per = (count + world - 1) // world
-    lo = SEED_LO + rank * per
-    n = max(0, min(per, count - rank * per))
+    from paper_1803_03288_b200 import dist as pdist
+    lo, n = pdist.shard(SEED_LO, count, rank, world)
     slots = torch.zeros(2 * world, dtype=torch.int64, device="cuda")
 
     def step():
@@ -328,15 +327,8 @@ def main():
         k0.record(stream)
         plan.run(lo, n, SEED_LO, sptr, None, d_i64.data_ptr(), d_f64.data_ptr())
         k1.record(stream)
-        if world > 1:  # min/argmin + max via per-rank slots, histogram + sums: one SUM each
-            slots.zero_()
-            slots[rank] = d_i64[0]
-            slots[world + rank] = d_i64[1]
-            dist.all_reduce(slots)
-            dist.all_reduce(d_i64[2:])
-            dist.all_reduce(d_f64)
-            d_i64[0] = slots[:world].min()
-            d_i64[1] = slots[world:].max()
+        if world > 1:  # the step's one reduction (paper_1803_03288_b200/dist.py)
+            pdist.reduce_stats(d_i64, d_f64, rank, world, slots)
 
     k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     for _ in range(max(3, args.warmup)):

@@ -1,0 +1,89 @@
+"""Parity at the BASELINE configs' full sizes, where the reference is too slow
+to run: the CPU oracle (pinned against the reference in
+test_oracle_pins.py) on spread samples, committed oracle digests for the
+config-5 TAC orders, and size-independent properties of the full sweeps."""
+import hashlib
+import json
+import os
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+TAC_LARGE = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "tac_large.json")))
+
+
+@pytest.mark.parametrize("model", ["inception_v3_training", "resnet_v2_101_training", "resnet_v2_50_training"])
+def test_model_tac_tic_match_oracle(lib, orc, model):
+    g = lib.model(model, 1)
+    og = orc.OracleGraph(json.loads(g.serialize()))
+    assert g.tac(g.declared()).priorities() == og.tac(incremental=True)
+    for mode in ("amended", "literal"):
+        p, total = og.tic(mode)
+        s = g.tic(mode)
+        assert s.priorities() == p and s.total_order() == total
+
+
+@pytest.mark.parametrize("spec", sorted(TAC_LARGE))
+def test_layered_tac_matches_oracle_digest(lib, spec):
+    if spec == "layered:1000000:100000" and not os.environ.get("TICTAC_SLOW"):
+        pytest.skip("config-5 top point (≈7 s on B200): set TICTAC_SLOW=1")
+    g = lib.model(spec, 1)
+    prio = g.tac(g.declared()).priorities()
+    text = json.dumps(prio, sort_keys=True)
+    assert len(prio) == TAC_LARGE[spec]["recvs"]
+    assert sorted(prio.values()) == list(range(len(prio)))
+    assert hashlib.sha256(text.encode()).hexdigest() == TAC_LARGE[spec]["sha256"]
+
+
+def test_config4_full_sweep(lib, orc):
+    """2^24 orders of config 4: spread seeds against the oracle; exact
+    statistics against the per-seed makespans; the E identity."""
+    g = lib.model("resnet_v2_101_training", 1)
+    o = g.declared()
+    U, L = g.bounds(o)
+    n = 1 << 24
+    res = g.sweep_random(o, 1, n, None, makespans=True)
+    ms = res["makespans"]
+    assert res["count"] == n and ms.shape == (n,)
+    assert res["min_us"] == ms.min() and res["argmin_seed"] == 1 + int(np.argmin(ms))
+    assert res["max_us"] == ms.max() and res["argmax_seed"] == 1 + int(np.argmax(ms))
+    assert res["sum_us"] == int(ms.sum())
+    assert L <= ms.min() and ms.max() <= U
+    bins = np.minimum((1000 * (U - ms)) // (U - L), 999)
+    assert np.array_equal(res["e_hist"], np.bincount(bins, minlength=1000))
+    og = orc.OracleGraph(json.loads(g.serialize()))
+    for s in np.linspace(1, n, 600, dtype=np.int64):
+        s = int(s)
+        m, v = og.simulate(og.random_schedule(s), True, s, 0.0)
+        assert ms[s - 1] == m and v == 0, s
+        e = Fraction(U - m, U - L)
+        assert U - e * (U - L) == m  # acceptance.cpp check 2, exact
+    # chunked == whole (statistics merge is exact)
+    a = g.sweep_random(o, 1, n // 2)
+    b = g.sweep_random(o, 1 + n // 2, n // 2)
+    assert a["sum_us"] + b["sum_us"] == res["sum_us"]
+    assert np.array_equal(a["e_hist"] + b["e_hist"], res["e_hist"])
+    assert min(a["min_us"], b["min_us"]) == res["min_us"]
+
+
+def test_config3_cluster_sweep_properties(lib, orc):
+    """VGG-16 x 4 workers: per-worker makespans of spread seeds against the
+    oracle's full cluster simulation; straggler statistics consistent."""
+    v = lib.model("vgg16_training", 1).expand(4, 1, 0)
+    o = v.declared()
+    n = 1 << 20
+    res = v.sweep_random(o, 1, n, None, worker_makespans=True)
+    wm = res["worker_makespans"]
+    hi, lo = wm.max(axis=1), wm.min(axis=1)
+    assert res["min_us"] == hi.min() and res["max_us"] == hi.max()
+    assert res["straggler_hist"].sum() == n
+    assert np.isclose(res["straggler_sum"], ((hi - lo) / hi).sum())
+    og = orc.OracleGraph(json.loads(v.serialize()))
+    for s in np.linspace(1, n, 40, dtype=np.int64):
+        s = int(s)
+        pr = orc.schedule_for(og, "random", s)
+        m, vi, st, en = og.simulate(pr, True, s, 0.0, events=True)
+        pw, _ = og.iteration_stats(en)
+        assert list(wm[s - 1]) == list(pw.values()), s
