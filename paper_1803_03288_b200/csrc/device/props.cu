@@ -329,6 +329,66 @@ __global__ void __launch_bounds__(1024) tac_kernel(TacArgs a) {
   }
 }
 
+// Multi-block TAC: the selection fold is distributed too. Every find-first
+// step is a grid-wide min (per-block reduction + atomicMin into a 3-slot
+// ring; the slot for step p+1 is reset during step p, two barriers after its
+// last reader). Rounds cost (chain length + 3) grid barriers but the O(R_t)
+// candidate scan is spread over every SM instead of repeated per block.
+__device__ __forceinline__ int grid_min_step(int v, int* ring, int& p, int* red, cg::grid_group& grid) {
+  v = block_min_int(v, red);
+  if (threadIdx.x == 0 && v != 0x7fffffff) atomicMin(&ring[p % 3], v);
+  if (blockIdx.x == 0 && threadIdx.x == 0) ring[(p + 1) % 3] = 0x7fffffff;
+  grid.sync();
+  const int r = *reinterpret_cast<volatile int*>(&ring[p % 3]);
+  ++p;
+  return r;
+}
+
+__global__ void __launch_bounds__(1024) tac_dist_kernel(TacArgs a, int* ring) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ int red[32];
+  const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t nthreads = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int R = a.R;
+  int p = 0;  // ring slot of the next grid-wide min (ring[0] preset by the host)
+  for (int round = 0; round < R; ++round) {
+    int first = 0x7fffffff;
+    for (int64_t c = tid; c < R; c += nthreads) {
+      if (!a.out[c]) continue;
+      int64_t m = kInf;
+      for (int32_t e = a.succ_off[c]; e < a.succ_off[c + 1]; ++e) m = min(m, a.M[a.succ[e]]);
+      a.mp[c] = m;
+      first = min(first, static_cast<int>(c));
+    }
+    int best = grid_min_step(first, ring, p, red, grid);  // also publishes mp[]
+    for (;;) {
+      const int64_t bp = a.P[best], bm = a.tcol[best], bmp = a.mp[best];
+      int nxt = 0x7fffffff;
+      for (int64_t c = best + 1 + tid; c < R; c += nthreads)
+        if (a.out[c] && precedes(static_cast<int>(c), a.P[c], a.tcol[c], a.mp[c], best, bp, bm, bmp)) {
+          nxt = static_cast<int>(c);
+          break;
+        }
+      nxt = grid_min_step(nxt, ring, p, red, grid);
+      if (nxt == 0x7fffffff) break;
+      best = nxt;
+    }
+    const int64_t t = a.tcol[best];
+    for (int64_t e = a.col_off[best] + tid; e < a.col_off[best + 1]; e += nthreads) {
+      const int32_t g = a.col[e];
+      const int k = --a.cnt[g];
+      a.M[g] -= t;
+      const int x = (a.xr[g] ^= best);
+      if (k == 1) atomicAdd(reinterpret_cast<unsigned long long*>(&a.P[x]), a.wsum[g]);
+    }
+    if (tid == 0) {
+      a.prio[best] = round;
+      a.out[best] = 0;
+    }
+    grid.sync();
+  }
+}
+
 // Shared setup for properties / tic / tac: rows, closure, group state,
 // column lists. `dur` per op (host).
 struct GroupState {
@@ -538,12 +598,26 @@ extern "C" int csk_tac(DeviceGraph* g, const int64_t* dur, int32_t* prio, char* 
   int dev = 0, sms = 148, per_sm = 1;
   CK(cudaGetDevice(&dev));
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tac_kernel, 1024, 0));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tac_dist_kernel, 1024, 0));
+  // Per-round work = candidate scan (R_t) + retire list (nnz/R on average).
   const int64_t work = S.nnz / std::max(R, 1) + R;
-  int blocks = work > 65536 ? std::min<int64_t>(sms * std::max(per_sm, 1), (work + 8191) / 8192) : 1;
+  int blocks = work > 16384 ? static_cast<int>(std::min<int64_t>(sms * std::max(per_sm, 1), (work + 1023) / 1024)) : 1;
   blocks = std::max(blocks, 1);
-  void* args[] = {&a};
-  CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(tac_kernel), blocks, 1024, args, 0, nullptr));
+  if (blocks == 1) {
+    void* args[] = {&a};
+    CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(tac_kernel), 1, 1024, args, 0, nullptr));
+  } else {
+    DevArr d_ring;
+    const std::vector<int32_t> ring = {0x7fffffff, 0x7fffffff, 0x7fffffff};
+    if (put(d_ring, ring, err)) return 1;
+    int* rp = d_ring.as<int>();
+    void* args[] = {&a, &rp};
+    CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(tac_dist_kernel), blocks, 1024, args, 0, nullptr));
+    LAUNCHED();
+    CK(cudaGetLastError());
+    CK(cudaMemcpy(prio, d_prio.p, 4ull * R, cudaMemcpyDeviceToHost));
+    return 0;
+  }
   LAUNCHED();
   CK(cudaGetLastError());
   CK(cudaMemcpy(prio, d_prio.p, 4ull * R, cudaMemcpyDeviceToHost));

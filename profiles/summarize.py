@@ -24,12 +24,25 @@ def raw_metrics(rep):
     return kernels
 
 
-def num(d, key):
-    v = d.get(key, ("", ""))[0].replace(",", "")
+SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-6, "us": 1e-3, "usecond": 1e-3,
+         "msecond": 1, "ms": 1, "s": 1e3, "second": 1e3, "nsecond": 1e-6, "hz": 1e-6, "Khz": 1e-3,
+         "Mhz": 1, "Ghz": 1e3}
+
+
+def num(d, key, base=False):
+    """Metric value; with base=True bytes -> bytes, times -> ms, rates -> MHz."""
+    v, u = d.get(key, ("", ""))
     try:
-        return float(v)
+        x = float(v.replace(",", ""))
     except ValueError:
         return None
+    return x * SCALE.get(u, 1) if base else x
+
+
+def short(name):
+    import re
+    m = re.search(r"(\w*kernel\w*)", name) or re.search(r"(\w+)\s*(<|\()", name)
+    return m.group(1) if m else name[:40]
 
 
 def launch_list(path):
@@ -41,7 +54,7 @@ def launch_list(path):
     for r in rows[1:]:
         d = dict(zip(h, r))
         if d.get("Metric Name") == "gpu__time_duration.sum":
-            name = d["Kernel Name"].split("(")[0].split("<")[0].split("::")[-1]
+            name = short(d["Kernel Name"])
             per[name].append(float(d["Metric Value"].replace(",", "")))
     unit = "ns"
     total = sum(sum(v) for v in per.values())
@@ -53,17 +66,17 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("rep")
     ap.add_argument("launches", nargs="?")
-    ap.add_argument("--count", type=int, required=True, help="orderings in the profiled launch")
-    ap.add_argument("--bsim", type=int, required=True, help="algorithmic bytes per ordering")
+    ap.add_argument("--count", type=int, default=0, help="units (orderings) in the profiled launch")
+    ap.add_argument("--bsim", type=int, default=0, help="algorithmic bytes per unit")
     ap.add_argument("--out", required=True)
     a = ap.parse_args()
     k = raw_metrics(a.rep)[0]
-    dur_ns = num(k, "gpu__time_duration.sum")
-    dram = (num(k, "dram__bytes_read.sum") or 0) + (num(k, "dram__bytes_write.sum") or 0)
+    dur_ms = num(k, "gpu__time_duration.sum", base=True)
+    dram = (num(k, "dram__bytes_read.sum", base=True) or 0) + (num(k, "dram__bytes_write.sum", base=True) or 0)
     s = {
         "kernel": k.get("Kernel Name", ("",))[0],
         "orderings": a.count,
-        "duration_ms_profiled_cold": dur_ns / 1e6 if dur_ns else None,
+        "duration_ms_profiled_cold": dur_ms,
         "dram_bytes_per_launch": dram,
         "algorithmic_bytes_per_launch": a.count * a.bsim,
         "sm_throughput_pct": num(k, "sm__throughput.avg.pct_of_peak_sustained_elapsed"),
@@ -77,10 +90,15 @@ def main():
         "achieved_occupancy_pct": num(k, "sm__warps_active.avg.pct_of_peak_sustained_active"),
         "registers_per_thread": num(k, "launch__registers_per_thread"),
         "warp_instructions": num(k, "smsp__inst_executed.sum"),
-        "sm_mhz": num(k, "sm__cycles_elapsed.avg.per_second") / 1e6 if num(k, "sm__cycles_elapsed.avg.per_second") else None,
+        "sm_mhz": num(k, "sm__cycles_elapsed.avg.per_second", base=True),
     }
-    if s["warp_instructions"]:
+    if s["warp_instructions"] and a.count:
         s["warp_instructions_per_ordering"] = s["warp_instructions"] / a.count
+        if s["sm_mhz"] and dur_ms:
+            peak = 148 * 4 * s["sm_mhz"] * 1e6  # warp-instruction issue slots per second
+            s["issue_roofline"] = {"achieved_warp_inst_per_s": s["warp_instructions"] / (dur_ms / 1e3),
+                                   "peak_warp_inst_per_s": peak,
+                                   "frac": s["warp_instructions"] / (dur_ms / 1e3) / peak}
     stalls = {kk.replace("smsp__average_warps_issue_stalled_", "").replace("_per_issue_active.ratio", ""):
               num(k, kk) for kk in k if kk.startswith("smsp__average_warps_issue_stalled_")
               and kk.endswith("_per_issue_active.ratio")}
