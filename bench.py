@@ -385,15 +385,26 @@ def main():
     h2d = 8 * R + 8 * (nc + 1) + 16 * (R + 2) + 8 + 8
     d2h = 8 * capi.DSTATS_I64 + 8 * capi.DSTATS_F64
 
+    clocks_summary = clocks.summary()
     if rank == 0:
         hbm, peak_src = peaks()
         bsim = b_sim(info)
         achieved = bsim * count / world / (kern_per_step / 1000.0) / 1e9  # per GPU
-        traffic = None
+        traffic, issue = None, None
         prof = os.path.join(ROOT, "profiles", "sweep_ncu_summary.json")
         if os.path.exists(prof):
             try:
-                traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+                ps = json.load(open(prof))
+                # ncu dram bytes scaled to this launch's orderings
+                traffic = ps["dram_bytes_per_launch"] * (count / world) / ps["orderings"]
+                ipo = ps["warp_instructions_per_ordering"]
+                mhz = clocks_summary.get("sm_mhz") or ps.get("sm_mhz") or 1965.0
+                peak_issue = 148 * 4 * mhz * 1e6
+                ach = ipo * (count / world) / (kern_per_step / 1000.0)
+                issue = {"bound": "issue", "achieved": ach, "peak": peak_issue, "unit": "warp-inst/s",
+                         "frac": ach / peak_issue, "warp_inst_per_order": ipo,
+                         "source": "instructions per ordering from profiles/sweep_ncu_summary.json (ncu), "
+                                   "time from this run's CUDA events, peak = 148 SMs x 4 schedulers x SM clock"}
             except Exception:
                 traffic = None
         out = {
@@ -411,14 +422,18 @@ def main():
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": traffic, "peak_source": peak_src,
                          "algorithmic_bytes_per_order": bsim,
-                         "note": "B_sim per SURVEY §8d; the fused kernel keeps all per-order state on "
-                                 "chip, so frac > 1 means issue-bound, see profiles/"},
+                         "note": "achieved = SURVEY §8d's B_sim = 12R+2V+2E+16 bytes per ordering x "
+                                 "orderings / kernel time (per GPU). The fused kernel keeps every "
+                                 "per-ordering byte on chip (traffic = measured DRAM bytes, ~0), so the "
+                                 "HBM-equivalent frac exceeds 1; the binding roofline is instruction "
+                                 "issue, reported in roofline_issue (ncu: DRAM ~0%, ALU pipe ~72%)"},
             "e2e": {"value": e2e_value, "unit": "sims/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "ms_per_step": e2e_t.item(), "call": "cs_sweep_random (host stats out)"},
             "result": {"min_us": stats["min_us"], "argmin_seed": stats["argmin_seed"],
                        "max_us": stats["max_us"], "mean_us": stats["sum_us"] / max(1, stats["count"]),
                        "count_checked": int(stats["count"])},
-            "clocks": clocks.summary(),
+            "clocks": clocks_summary,
+            "roofline_issue": issue,
         }
         if not args.no_tac:
             out["tac_seconds"] = tac_times(lib, top=args.config5_top)
