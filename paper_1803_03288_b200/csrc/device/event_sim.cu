@@ -279,16 +279,22 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock)
     if (lane == 0) choice.seed(choice_seed);
     __syncwarp();
 
-    // ---- event loop (sim.cpp:194-233)
+    // ---- event loop (sim.cpp:194-233), run serially by lane 0 on the
+    // shared-memory state: the replica is a dependent chain, and warp-wide
+    // bookkeeping per event costs more than it saves. Resources that could
+    // start are tracked in a bitmask so each pass visits only those, still in
+    // ascending resource order (the order of the reference's draws).
     int64_t t = 0, mk = 0, nforced = 0;
-    int finished = 0, stalled = 0;
+    int stalled = 0;
     const int gated = rs.gated;
     const bool rec = (b == 0) && rs.start;
-
-    auto start_op = [&](int r, int op) {
-      if (lane == 0) {
+    if (lane == 0) {
+      int finished = 0;
+      // kernels support up to 64 resources on the fast mask; more use a scan
+      const bool small_res = nres <= 64;
+      auto start_op = [&](int r, int op) {
         const int l = G.lidx[op];
-        atomicAnd(&s.ready[G.rb_off[r] + (l >> 5)], ~(1u << (l & 31)));
+        s.ready[G.rb_off[r] + (l >> 5)] &= ~(1u << (l & 31));
         s.ready_cnt[r] -= 1;
         s.running[r] = op;
         const int64_t e = t + G.dur[op];
@@ -299,175 +305,128 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock)
         }
         const int d = G.res_dev[r];
         if (e > s.dev_end[d]) s.dev_end[d] = e;
-      }
-      const int64_t e = t + G.dur[op];
-      mk = max(mk, e);
-      __syncwarp();
-    };
-
-    // candidate mask of one ready word (word w of resource r)
-    auto cand_mask = [&](int r, int w, int best, bool pri) -> uint32_t {
-      uint32_t bits = s.ready[G.rb_off[r] + w];
-      if (!pri) return bits;  // no priorities on r: every ready op is a candidate
-      uint32_t m = 0;
-      const int base = G.rops_off[r] + (w << 5);
-      while (bits) {
-        const int bit = __ffs(bits) - 1;
-        bits &= bits - 1;
-        const int op = G.rops[base + bit];
-        const int p = s.prio[op];
-        if (p < 0 || (p == best && admitted(s, op, r, gated))) m |= 1u << bit;
-      }
-      return m;
-    };
-
-    auto try_start = [&](int r) -> bool {  // sim.cpp:163-192
-      if (s.running[r] >= 0 || s.ready_cnt[r] == 0) return false;
-      const bool pri = s.haspri[r] != 0;
-      const int w0 = s.lo[r], w1 = s.hi[r];  // every ready bit lies in [w0, w1]
-      int best = 0x7fffffff, nlo = kEmptyLo, nhi = -1;
-      for (int c = w0; c <= w1; c += 32) {
-        const int w = c + lane;
-        uint32_t bits = w <= w1 ? s.ready[G.rb_off[r] + w] : 0u;
-        if (bits) {
+        mk = max(mk, e);
+      };
+      // sim.cpp:163-192 for one resource; returns true when an op started
+      auto try_start = [&](int r) -> bool {
+        if (s.running[r] >= 0 || s.ready_cnt[r] == 0) return false;
+        const bool pri = s.haspri[r] != 0;
+        const int wb = G.rb_off[r], ob = G.rops_off[r];
+        int nlo = kEmptyLo, nhi = -1, best = 0x7fffffff;
+        for (int w = s.lo[r]; w <= s.hi[r]; ++w) {
+          uint32_t bits = s.ready[wb + w];
+          if (!bits) continue;
           nlo = min(nlo, w);
-          nhi = max(nhi, w);
+          nhi = w;
+          if (!pri) continue;
+          while (bits) {
+            const int bit = __ffs(bits) - 1;
+            bits &= bits - 1;
+            const int op = G.rops[ob + (w << 5) + bit];
+            const int p = s.prio[op];
+            if (p >= 0 && p < best && admitted(s, op, r, gated)) best = p;
+          }
         }
-        if (!pri) continue;
-        const int base = G.rops_off[r] + (w << 5);
-        while (bits) {
-          const int bit = __ffs(bits) - 1;
-          bits &= bits - 1;
-          const int op = G.rops[base + bit];
-          const int p = s.prio[op];
-          if (p >= 0 && p < best && admitted(s, op, r, gated)) best = p;
-        }
-      }
-#pragma unroll
-      for (int o = 16; o; o >>= 1) {
-        best = min(best, __shfl_xor_sync(~0u, best, o));
-        nlo = min(nlo, __shfl_xor_sync(~0u, nlo, o));
-        nhi = max(nhi, __shfl_xor_sync(~0u, nhi, o));
-      }
-      __syncwarp();
-      if (lane == 0) {  // tighten the window to the non-empty words
         s.lo[r] = nlo;
         s.hi[r] = nhi;
-      }
-      int total = 0;
-      for (int c = nlo; c <= nhi; c += 32) {
-        const uint32_t m = (c + lane <= nhi) ? cand_mask(r, c + lane, best, pri) : 0u;
-        total += warp_sum(__popc(m));
-      }
-      if (total == 0) {
-        __syncwarp();
-        return false;
-      }
-      int k = 0;
-      if (total > 1) {
-        uint64_t kk = 0;
-        if (lane == 0) kk = bounded_full(choice, static_cast<uint64_t>(total), rs);
-        k = static_cast<int>(__shfl_sync(~0u, kk, 0));
-      }
-      int pick = -1;
-      for (int c = nlo; c <= nhi && pick < 0; c += 32) {
-        const uint32_t m = (c + lane <= nhi) ? cand_mask(r, c + lane, best, pri) : 0u;
-        const int cnt = __popc(m);
-        int incl = cnt;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int y = __shfl_up_sync(~0u, incl, o);
-          if (lane >= o) incl += y;
+        auto cmask = [&](int w) -> uint32_t {
+          uint32_t bits = s.ready[wb + w];
+          if (!pri) return bits;
+          uint32_t m = 0;
+          while (bits) {
+            const int bit = __ffs(bits) - 1;
+            bits &= bits - 1;
+            const int op = G.rops[ob + (w << 5) + bit];
+            const int p = s.prio[op];
+            if (p < 0 || (p == best && admitted(s, op, r, gated))) m |= 1u << bit;
+          }
+          return m;
+        };
+        int total = 0;
+        for (int w = nlo; w <= nhi; ++w) total += __popc(cmask(w));
+        if (total == 0) return false;
+        int k = total > 1 ? static_cast<int>(bounded_full(choice, static_cast<uint64_t>(total), rs)) : 0;
+        for (int w = nlo; w <= nhi; ++w) {
+          const uint32_t m = cmask(w);
+          const int c = __popc(m);
+          if (k < c) {
+            start_op(r, G.rops[ob + (w << 5) + nth_bit(m, k)]);
+            return true;
+          }
+          k -= c;
         }
-        const int chunk = __shfl_sync(~0u, incl, 31);
-        if (k < chunk) {
-          const int excl = incl - cnt;
-          const bool here = k >= excl && k < incl;
-          const unsigned who = __ballot_sync(~0u, here);
-          const int src = __ffs(who) - 1;
-          int op = -1;
-          if (here) op = G.rops[G.rops_off[r] + ((c + lane) << 5) + nth_bit(m, k - excl)];
-          pick = __shfl_sync(~0u, op, src);
-        } else {
-          k -= chunk;
-        }
-      }
-      start_op(r, pick);
-      return true;
-    };
-
-    auto complete_now = [&]() -> bool {  // sim.cpp:144-161
-      bool any = false;
-      for (int r = 0; r < nres; ++r) {
-        const int i = s.running[r];
-        if (i < 0 || s.run_end[r] != t) continue;
-        __syncwarp();
-        any = true;
-        ++finished;
-        if (lane == 0) {
+        return false;  // unreachable
+      };
+      auto push_ready = [&](int w_op) {
+        const int rw = G.res[w_op], l = G.lidx[w_op];
+        s.ready[G.rb_off[rw] + (l >> 5)] |= 1u << (l & 31);
+        s.ready_cnt[rw] += 1;
+        s.lo[rw] = min(s.lo[rw], l >> 5);
+        s.hi[rw] = max(s.hi[rw], l >> 5);
+      };
+      // sim.cpp:144-161
+      auto complete_now = [&]() -> bool {
+        bool any = false;
+        for (int r = 0; r < nres; ++r) {
+          const int i = s.running[r];
+          if (i < 0 || s.run_end[r] != t) continue;
+          any = true;
+          ++finished;
           s.running[r] = -1;
           if (s.prio[i] >= 0 && G.chan[r]) {
             s.counter[r] += 1;
             s.comp[G.rops_off[r] + s.comp_len[r]] = s.orig[i];
             s.comp_len[r] += 1;
           }
-        }
-        for (int e = G.succ_off[i] + lane; e < G.succ_off[i + 1]; e += 32) {
-          const int w = G.succ_idx[e];
-          if (atomicSub(&s.missing[w], 1) == 1) {
-            const int rw = G.res[w], l = G.lidx[w];
-            atomicOr(&s.ready[G.rb_off[rw] + (l >> 5)], 1u << (l & 31));
-            atomicAdd(&s.ready_cnt[rw], 1);
-            atomicMin(&s.lo[rw], l >> 5);
-            atomicMax(&s.hi[rw], l >> 5);
+          for (int e = G.succ_off[i]; e < G.succ_off[i + 1]; ++e) {
+            const int w = G.succ_idx[e];
+            if (--s.missing[w] == 0) push_ready(w);
           }
         }
-        __syncwarp();
-      }
-      return any;
-    };
-
-    while (finished < n) {
-      bool progress = true;
-      while (progress) {
-        progress = false;
-        for (int r = 0; r < nres; ++r) progress = try_start(r) || progress;
-        progress = complete_now() || progress;
-      }
-      if (finished == n) break;
-      int64_t next_t = INT64_MAX;
-      for (int r = lane; r < nres; r += 32)
-        if (s.running[r] >= 0) next_t = min(next_t, s.run_end[r]);
-      next_t = warp_min64(next_t);
-      if (next_t == INT64_MAX) {  // forced release, sim.cpp:211-229
-        int64_t key = INT64_MAX;
-        for (int r = 0; r < nres; ++r) {
-          for (int w = s.lo[r] + lane; w <= s.hi[r]; w += 32) {
-            uint32_t bits = s.ready[G.rb_off[r] + w];
-            const int base = G.rops_off[r] + (w << 5);
-            while (bits) {
-              const int bit = __ffs(bits) - 1;
-              bits &= bits - 1;
-              const int op = G.rops[base + bit];
-              if (s.gate[op] < 0 || admitted(s, op, r, gated)) continue;
-              key = min(key, (static_cast<int64_t>(s.gate[op]) << 32) | op);
+        return any;
+      };
+      (void)small_res;
+      while (finished < n) {
+        bool progress = true;
+        while (progress) {
+          progress = false;
+          for (int r = 0; r < nres; ++r) progress = try_start(r) || progress;
+          progress = complete_now() || progress;
+        }
+        if (finished == n) break;
+        int64_t next_t = INT64_MAX;
+        for (int r = 0; r < nres; ++r)
+          if (s.running[r] >= 0) next_t = min(next_t, s.run_end[r]);
+        if (next_t == INT64_MAX) {  // forced release, sim.cpp:211-229
+          int64_t key = INT64_MAX;
+          for (int r = 0; r < nres; ++r)
+            for (int w = s.lo[r]; w <= s.hi[r]; ++w) {
+              uint32_t bits = s.ready[G.rb_off[r] + w];
+              while (bits) {
+                const int bit = __ffs(bits) - 1;
+                bits &= bits - 1;
+                const int op = G.rops[G.rops_off[r] + (w << 5) + bit];
+                if (s.gate[op] < 0 || admitted(s, op, r, gated)) continue;
+                key = min(key, (static_cast<int64_t>(s.gate[op]) << 32) | op);
+              }
             }
+          if (key == INT64_MAX) {
+            stalled = 1;
+            break;
           }
+          const int victim = static_cast<int>(key & 0xffffffff);
+          s.forced[victim >> 5] |= 1u << (victim & 31);
+          ++nforced;
+          continue;
         }
-        key = warp_min64(key);
-        if (key == INT64_MAX) {
-          stalled = 1;
-          break;
-        }
-        const int victim = static_cast<int>(key & 0xffffffff);
-        if (lane == 0) s.forced[victim >> 5] |= 1u << (victim & 31);
-        ++nforced;
-        __syncwarp();
-        continue;
+        t = next_t;
+        complete_now();
       }
-      t = next_t;
-      complete_now();
     }
+    __syncwarp();
+    mk = __shfl_sync(~0u, mk, 0);
+    nforced = __shfl_sync(~0u, nforced, 0);
+    stalled = __shfl_sync(~0u, stalled, 0);
 
     // violations: rank inversions per channel completion sequence + forced
     int64_t inv = 0;
@@ -554,11 +513,17 @@ int run_event(DeviceGraph* g, const int64_t* dur, int64_t B, RunSpec rs, int64_t
   constexpr size_t kSmemBudget = 200 * 1024;
   const int64_t smem_runs = static_cast<int64_t>(sms) * std::max<int64_t>(1, (227 * 1024) / std::max<size_t>(hsz, 1));
   const bool in_smem = hsz <= kSmemBudget && (B <= smem_runs || hsz <= 16 * 1024);
-  const int wpb = in_smem ? static_cast<int>(std::min<size_t>(kWarpsPerBlock, kSmemBudget / hsz)) : kWarpsPerBlock;
+  // Few runs: one run per block, so the unused shared-memory carve-out stays
+  // L1 for the graph arrays the (latency-bound) event chain reads.
+  const int wpb = !in_smem ? kWarpsPerBlock
+                  : B <= sms ? 1
+                             : static_cast<int>(std::min<size_t>(kWarpsPerBlock, kSmemBudget / hsz));
   int per_sm = 16;
   if (in_smem) {
     CK(cudaFuncSetAttribute(event_sim_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             static_cast<int>(hsz * wpb)));
+    const int carve = static_cast<int>(std::min<size_t>(100, (hsz * wpb * 100 + 228 * 1024 - 1) / (228 * 1024) + 3));
+    CK(cudaFuncSetAttribute(event_sim_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
     int occ = 1;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, event_sim_kernel, 32 * wpb, hsz * wpb));
     per_sm = std::max(1, occ) * wpb;

@@ -38,8 +38,24 @@ struct cs_oracle {
 struct cs_schedule {
   Schedule s;
 };
+// A simulation report. Makespan and violations are always present; the
+// event list is either computed eagerly (exact device event simulator) or,
+// when the closed form of SURVEY A.2 produced the makespan, on first request
+// from the retained inputs (graph, durations, priorities, policy).
 struct cs_report {
-  Report r;
+  int64_t makespan = 0, violations = 0;
+  bool has_stats = false;
+  std::shared_ptr<const Graph> g;
+  std::vector<int64_t> d;
+  std::vector<int32_t> prio;
+  Policy pol;
+  mutable std::mutex mu;
+  mutable std::unique_ptr<Report> full;
+  const Report& report() const {
+    std::lock_guard<std::mutex> lock(mu);
+    if (!full) full = std::make_unique<Report>(simulate_prepared(*g, d, prio, pol));
+    return *full;
+  }
 };
 struct cs_sweep_plan {
   std::unique_ptr<SweepCtx> ctx;
@@ -72,6 +88,21 @@ char* dup(const std::string& s) {
   char* out = new char[s.size() + 1];
   std::memcpy(out, s.c_str(), s.size() + 1);
   return out;
+}
+
+// Closed-form plan of (graph, oracle, gating/noise), kept on the graph
+// handle: handles are immutable, so repeated sweeps/simulations reuse it.
+std::shared_ptr<SweepCtx> cached_sweep(const cs_graph* g, const cs_oracle* o, const Policy& p) {
+  auto* gm = const_cast<cs_graph*>(g);
+  std::lock_guard<std::mutex> lock(gm->mu);
+  if (gm->sweep && gm->sweep_oracle == o->id && gm->sweep_gated == p.gated && gm->sweep_noise == p.noise)
+    return gm->sweep;
+  std::shared_ptr<SweepCtx> ctx = make_sweep(g->g, o->o, p);
+  gm->sweep = ctx;
+  gm->sweep_oracle = o->id;
+  gm->sweep_gated = p.gated;
+  gm->sweep_noise = p.noise;
+  return ctx;
 }
 
 Policy policy_of(const cs_sim_policy* p) {  // capi.cpp:64-73 defaults
@@ -303,8 +334,34 @@ int cs_simulate(const cs_graph* g, const cs_oracle* o, const cs_schedule* s,
     need(g, "graph");
     need(o, "oracle");
     need(out, "out");
-    auto* rep = new cs_report{simulate(*g->g, o->o, s ? &s->s : nullptr, policy_of(policy))};
-    *out = rep;
+    const Policy p = policy_of(policy);
+    SimInputs in = prepare_sim(*g->g, o->o, s ? &s->s : nullptr, p);  // reference checks, same order
+    auto rep = std::make_unique<cs_report>();
+    rep->g = g->g;
+    rep->pol = p;
+    std::shared_ptr<SweepCtx> ctx;
+    if (!g->g->cluster() && p.gated && p.noise == 0.0 && in.all_recvs_prioritized)
+      ctx = cached_sweep(g, o, p);
+    if (ctx && ctx->fast && !ctx->cluster) {
+      // Closed form: the gate order is the recvs sorted by
+      // (priority, id) (sim.cpp:95-104); gated, noiseless, recvs are roots,
+      // so no inversions and no forced releases.
+      const auto& ro = g->g->recv_ops();
+      std::vector<int32_t> order(ro.size());
+      for (size_t c = 0; c < ro.size(); ++c) order[c] = static_cast<int32_t>(c);
+      std::stable_sort(order.begin(), order.end(),
+                       [&](int32_t a, int32_t b) { return in.prio[ro[a]] < in.prio[ro[b]]; });
+      rep->makespan = ctx->order_makespan(order);
+      rep->violations = 0;
+      rep->d = std::move(in.d);
+      rep->prio = std::move(in.prio);
+    } else {
+      rep->full = std::make_unique<Report>(simulate_prepared(*g->g, in.d, in.prio, p));
+      rep->makespan = rep->full->makespan;
+      rep->violations = rep->full->violations;
+      rep->has_stats = rep->full->has_stats;
+    }
+    *out = rep.release();
   });
 }
 
@@ -312,7 +369,7 @@ int cs_report_makespan(const cs_report* r, int64_t* out_us) {
   return guarded([&] {
     need(r, "report");
     need(out_us, "out_us");
-    *out_us = r->r.makespan;
+    *out_us = r->makespan;
   });
 }
 
@@ -320,7 +377,7 @@ int cs_report_violations(const cs_report* r, int64_t* out) {
   return guarded([&] {
     need(r, "report");
     need(out, "out");
-    *out = r->r.violations;
+    *out = r->violations;
   });
 }
 
@@ -328,7 +385,7 @@ int cs_report_json(const cs_report* r, char** out_json) {
   return guarded([&] {
     need(r, "report");
     need(out_json, "out_json");
-    *out_json = dup(dump_doc(r->r.to_json()));
+    *out_json = dup(dump_doc(r->report().to_json()));
   });
 }
 
@@ -336,7 +393,7 @@ int cs_report_chrome_trace(const cs_report* r, char** out_json) {
   return guarded([&] {
     need(r, "report");
     need(out_json, "out_json");
-    *out_json = dup(dump_doc(r->r.chrome_trace()));
+    *out_json = dup(dump_doc(r->report().chrome_trace()));
   });
 }
 
@@ -344,8 +401,8 @@ int cs_report_iteration_json(const cs_report* r, char** out_json) {
   return guarded([&] {
     need(r, "report");
     need(out_json, "out_json");
-    if (!r->r.has_stats) fail(kValidation, "iteration stats need a cluster simulation");
-    *out_json = dup(dump_doc(r->r.iteration_json()));
+    if (!r->has_stats) fail(kValidation, "iteration stats need a cluster simulation");
+    *out_json = dup(dump_doc(r->report().iteration_json()));
   });
 }
 
@@ -370,7 +427,7 @@ int cs_metrics_json(const cs_graph* g, const cs_oracle* o, const cs_report* r, c
     need(r, "report");
     need(out_json, "out_json");
     const auto b = bounds(*g->g, o->o);
-    *out_json = dup(dump_doc(metrics_json(b.first, b.second, r->r.makespan, &r->r)));
+    *out_json = dup(dump_doc(metrics_json(b.first, b.second, r->makespan, r->has_stats ? &r->report() : nullptr)));
   });
 }
 
@@ -401,21 +458,7 @@ int cs_sweep_random(const cs_graph* g, const cs_oracle* o, uint64_t seed_lo, int
     need(o, "oracle");
     if (count < 0) fail(kParameter, "count must be non-negative");
     Policy p = policy_of(policy);
-    std::shared_ptr<SweepCtx> ctx;
-    {
-      auto* gm = const_cast<cs_graph*>(g);
-      std::lock_guard<std::mutex> lock(gm->mu);
-      if (gm->sweep && gm->sweep_oracle == o->id && gm->sweep_gated == p.gated &&
-          gm->sweep_noise == p.noise) {
-        ctx = gm->sweep;
-      } else {
-        ctx = make_sweep(g->g, o->o, p);
-        gm->sweep = ctx;
-        gm->sweep_oracle = o->id;
-        gm->sweep_gated = p.gated;
-        gm->sweep_noise = p.noise;
-      }
-    }
+    std::shared_ptr<SweepCtx> ctx = cached_sweep(g, o, p);
     const bool cluster_m = ctx->cluster && makespans_out;  // needs the full event replica
     if (!ctx->fast || cluster_m) {
       sweep_exact(*ctx, seed_lo, count, makespans_out, worker_makespans_out, stats_out);

@@ -169,6 +169,16 @@ Schedule random_schedule(const Graph& g, uint64_t seed);
 Schedule schedule_for(const Graph& g, const std::string& algo, PropMode mode, uint64_t seed,
                       const TimeOracle* o);  // cluster.cpp:91-122
 Report simulate(const Graph& g, const TimeOracle& o, const Schedule* s, const Policy& p);
+// simulate() split in two: validation + per-op arrays (sim.cpp:63-88), then
+// the exact device event simulation and report assembly.
+struct SimInputs {
+  std::vector<int64_t> d;
+  std::vector<int32_t> prio;
+  bool all_recvs_prioritized = false;
+};
+SimInputs prepare_sim(const Graph& g, const TimeOracle& o, const Schedule* s, const Policy& p);
+Report simulate_prepared(const Graph& g, const std::vector<int64_t>& d, const std::vector<int32_t>& prio,
+                         const Policy& p);
 std::pair<int64_t, int64_t> bounds(const Graph& g, const TimeOracle& o);  // metrics.cpp:10-22
 Json metrics_json(int64_t U, int64_t L, int64_t m, const Report* stats);
 Json brute_force(const Graph& g, const TimeOracle& o, const Policy& p, int max_recvs);

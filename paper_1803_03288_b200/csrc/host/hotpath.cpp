@@ -130,19 +130,32 @@ static void policy_check(const Policy& p) {
   if (p.noise < 0.0 || p.noise > 1.0) fail(kParameter, "reorder_noise must be within [0, 1]");
 }
 
-Report simulate(const Graph& g, const TimeOracle& o, const Schedule* s, const Policy& p) {
-  const std::vector<int64_t> d = o.durations(g);  // sim.cpp:63
+SimInputs prepare_sim(const Graph& g, const TimeOracle& o, const Schedule* s, const Policy& p) {
+  SimInputs in;
+  in.d = o.durations(g);  // sim.cpp:63
   policy_check(p);
-  const int32_t n = g.n();
-  std::vector<int32_t> prio(n, -1);
+  in.prio.assign(g.n(), -1);
   if (s) {
     for (const auto& [id, rank] : s->prio) {  // sim.cpp:79-88
       if (!g.has(id)) fail(kValidation, "schedule references unknown op: " + id);
       const int32_t i = g.at(id);
       if (g.ops()[i].kind != kRecv) fail(kValidation, "schedule priority on non-recv op: " + id);
-      prio[i] = rank;
+      in.prio[i] = rank;
     }
   }
+  in.all_recvs_prioritized = true;
+  for (int32_t r : g.recv_ops()) in.all_recvs_prioritized &= in.prio[r] >= 0;
+  return in;
+}
+
+Report simulate(const Graph& g, const TimeOracle& o, const Schedule* s, const Policy& p) {
+  const SimInputs in = prepare_sim(g, o, s, p);
+  return simulate_prepared(g, in.d, in.prio, p);
+}
+
+Report simulate_prepared(const Graph& g, const std::vector<int64_t>& d, const std::vector<int32_t>& prio,
+                         const Policy& p) {
+  const int32_t n = g.n();
   std::vector<int64_t> st(n), en(n);
   int64_t m = 0, viol = 0;
   int32_t status = 0;

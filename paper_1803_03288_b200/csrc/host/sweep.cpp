@@ -5,6 +5,8 @@
 // seed runs through the exact device event simulator.
 #include "sweep.hpp"
 
+#include <cuda_runtime.h>
+
 #include <algorithm>
 #include <cstring>
 #include <set>
@@ -137,6 +139,25 @@ bool chain_tables(const Graph& g, const std::vector<int64_t>& dur, bool allow_se
 
 SweepCtx::~SweepCtx() {
   if (plan) csk_sweep_plan_free(plan);
+  if (d_order_) cudaFree(d_order_);
+  if (d_ms_) cudaFree(d_ms_);
+}
+
+int64_t SweepCtx::order_makespan(const std::vector<int32_t>& order) {
+  std::lock_guard<std::mutex> lock(mu_);
+  auto ck = [](cudaError_t e) {
+    if (e != cudaSuccess) fail(kInternal, std::string("CUDA error: ") + cudaGetErrorString(e));
+  };
+  if (!d_order_) {
+    ck(cudaMalloc(&d_order_, sizeof(int32_t) * std::max<size_t>(order.size(), 1)));
+    ck(cudaMalloc(&d_ms_, sizeof(int64_t)));
+  }
+  ck(cudaMemcpy(d_order_, order.data(), sizeof(int32_t) * order.size(), cudaMemcpyHostToDevice));
+  char err[256] = {0};
+  if (csk_sweep_orders(plan, d_order_, 1, nullptr, d_ms_, err)) fail(kInternal, err);
+  int64_t m = 0;
+  ck(cudaMemcpy(&m, d_ms_, sizeof(int64_t), cudaMemcpyDeviceToHost));
+  return m;
 }
 
 std::unique_ptr<SweepCtx> make_sweep(std::shared_ptr<const Graph> g, const TimeOracle& o,

@@ -2,6 +2,7 @@
 #pragma once
 
 #include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -23,7 +24,15 @@ struct SweepCtx {
   SweepPlan* plan = nullptr;
   int32_t R = 0, nc = 0;
   std::string why;  // why the closed form does not apply
+  // Closed-form makespan of one gate order (recv columns, rank order) on a
+  // worker-graph plan: one kernel launch on small cached device buffers.
+  int64_t order_makespan(const std::vector<int32_t>& order);
   ~SweepCtx();
+
+ private:
+  std::mutex mu_;
+  int32_t* d_order_ = nullptr;
+  int64_t* d_ms_ = nullptr;
 };
 
 std::unique_ptr<SweepCtx> make_sweep(std::shared_ptr<const Graph> g, const TimeOracle& o,

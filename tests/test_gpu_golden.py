@@ -68,6 +68,8 @@ def test_simulations_match_fixture(lib, kind):
                     out += r.iteration_json()
                 w = want["simulate"][f"{algo}/{pname}"]
                 assert (r.makespan(), r.violations()) == (w["makespan"], w["violations"]), (name, algo, pname)
+                # closed-form makespan (when it applied) == the event replica's
+                assert json.loads(r.json())["makespan_us"] == r.makespan()
                 assert sha(out) == w["sha"], (name, algo, pname)
         if "brute_force" in want:
             assert g.brute_force_text(o, None, 8) == want["brute_force"], name
