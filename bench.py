@@ -28,6 +28,8 @@ import tempfile
 import threading
 import time
 
+import numpy as np
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
@@ -245,6 +247,17 @@ def other_configs(lib):
         "straggler_max_bin": int(max(i for i in range(1000) if sh[i])),
         "iteration_min_us": st["min_us"], "iteration_max_us": st["max_us"],
         "tic_common_order_straggler": strag_tic}
+    # batched brute force: all R! orders on the device
+    bf = {}
+    for R in (8, 10, 12):
+        g = lib.generate("chain", R, 1, "1", 5)
+        o = g.declared()
+        t = time.perf_counter()
+        res = json.loads(g.brute_force_text(o, None, R))
+        bf[f"R{R}"] = {"permutations": int(np.prod(np.arange(1, R + 1, dtype=np.float64))),
+                       "seconds": round(time.perf_counter() - t, 4), "best_us": res["makespan_us"],
+                       "distinct_makespans": len(res["distribution"])}
+    out["brute_force_chain"] = bf
     return out
 
 

@@ -89,6 +89,15 @@ int csk_sweep_run(SweepPlan* p, uint64_t seed_lo, int64_t count, uint64_t key_ba
 int csk_sweep_orders(SweepPlan* p, const int32_t* d_orders, int64_t n, void* stream,
                      int64_t* d_makespans, char* err);
 
+/* Lexicographic permutations [first, first+count) of a worker plan's recv
+ * columns through the closed form (d_out device, count entries). */
+int csk_sweep_lex(SweepPlan* p, int64_t first, int64_t count, int64_t* d_out, char* err);
+/* Brute force over all `perms` = R! permutations on the closed form: first
+ * minimum in lexicographic order (best_m, best_k) and the ascending distinct
+ * makespans (copied when *n_distinct <= cap). */
+int csk_brute_force_closed(SweepPlan* p, int64_t perms, int64_t* best_m, int64_t* best_k, int64_t* distinct,
+                           int64_t cap, int64_t* n_distinct, char* err);
+
 /* Launch counter (kernels launched by this library, process-wide). */
 int64_t csk_launches(void);
 

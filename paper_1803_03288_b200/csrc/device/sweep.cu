@@ -22,6 +22,8 @@
 // The shuffle array lives in shared memory as bytes (R ≤ 256) or halves,
 // laid out [k/4][thread] so every lane always hits its own bank.
 #include <algorithm>
+#include <cub/cub.cuh>
+#include <iterator>
 #include <vector>
 
 #include "common.cuh"
@@ -359,6 +361,44 @@ __global__ void __launch_bounds__(kSweepThreads, 3) chain_sweep_kernel(ChainArgs
       if (s_shist[k]) atomicAdd(&a.i64[8 + kBins + k], static_cast<unsigned long long>(s_shist[k]));
 }
 
+// Brute force (metrics.cpp:37-72) on the closed form: permutation number k
+// in lexicographic order of the recv columns (std::next_permutation order
+// over ascending ids) is unranked in the factorial number system into a
+// per-thread shared-memory row, then folded right-to-left like a random
+// order. out[k - first] = makespan.
+template <typename V>
+__global__ void __launch_bounds__(kSweepThreads) lex_kernel(ChainArgs a, int64_t first, int64_t count,
+                                                            const unsigned long long* __restrict__ fact,
+                                                            int64_t* __restrict__ out) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int R = a.R;
+  uint2* s_tab = reinterpret_cast<uint2*>(smem);
+  V* s_pw = reinterpret_cast<V*>(s_tab + R);
+  uint8_t* s_row = reinterpret_cast<uint8_t*>(s_pw + a.stride) + threadIdx.x * 32;
+  for (int k = threadIdx.x; k < R; k += blockDim.x) s_tab[k] = a.tab[k];
+  for (int k = threadIdx.x; k < a.stride; k += blockDim.x) s_pw[k] = static_cast<V>(a.pwsuf[k]);
+  __syncthreads();
+  const V ctot = static_cast<V>(a.ctot[0]);
+  const int64_t nthreads = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; idx < count; idx += nthreads) {
+    unsigned long long k = static_cast<unsigned long long>(first + idx);
+    uint32_t left = (R >= 32) ? ~0u : ((1u << R) - 1u);  // remaining columns (R <= 20)
+    for (int pos = 0; pos < R; ++pos) {
+      const unsigned long long f = fact[R - 1 - pos];
+      const int q = static_cast<int>(k / f);
+      k -= static_cast<unsigned long long>(q) * f;
+      const int c = nth_bit(left, q);
+      left &= ~(1u << c);
+      s_row[pos] = static_cast<uint8_t>(c);
+    }
+    FoldT<V> fo{a.nc, 0, -1};
+    for (int pos = R - 1; pos >= 0; --pos) fo.add(s_tab[s_row[pos]], ctot, s_pw);
+    if (fo.G > 0) fo.best = max(fo.best, s_pw[0]);
+    const int64_t tcpu = fo.best < 0 ? 0 : static_cast<int64_t>(fo.best);
+    out[idx] = max(tcpu, static_cast<int64_t>(ctot));
+  }
+}
+
 __global__ void reset_kernel(unsigned long long* i64, double* f64) {
   for (int k = threadIdx.x; k < 2008; k += blockDim.x) i64[k] = k == 0 ? ~0ULL : 0ULL;
   if (threadIdx.x < 2) f64[threadIdx.x] = 0.0;
@@ -545,6 +585,108 @@ extern "C" int csk_sweep_orders(SweepPlan* p, const int32_t* d_orders, int64_t n
   LAUNCHED();
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(st));
+  return 0;
+}
+
+extern "C" int csk_sweep_lex(SweepPlan* p, int64_t first, int64_t count, int64_t* d_out, char* err) {
+  if (p->W != 1 || p->cluster || p->R > 20) {
+    std::snprintf(err, 256, "lexicographic brute force needs a worker plan with at most 20 recvs");
+    return 4;
+  }
+  if (count <= 0) return 0;
+  std::vector<unsigned long long> fact(21, 1);
+  for (int i = 1; i <= 20; ++i) fact[i] = fact[i - 1] * static_cast<unsigned long long>(i);
+  void* d_fact = nullptr;
+  CK(cudaMalloc(&d_fact, sizeof(unsigned long long) * fact.size()));
+  CK(cudaMemcpy(d_fact, fact.data(), sizeof(unsigned long long) * fact.size(), cudaMemcpyHostToDevice));
+  ChainArgs a = chain_args(p);
+  const size_t vb = p->narrow ? 4 : 8;
+  const size_t smem = 8 * static_cast<size_t>(p->R) + ((vb * p->stride + 7) & ~size_t(7)) + 32 * kSweepThreads;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int blocks = static_cast<int>(std::min<int64_t>(sms * 8, (count + kSweepThreads - 1) / kSweepThreads));
+  const auto* f = static_cast<const unsigned long long*>(d_fact);
+  if (p->narrow) {
+    CK(cudaFuncSetAttribute(lex_kernel<int32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    lex_kernel<int32_t><<<blocks, kSweepThreads, smem>>>(a, first, count, f, d_out);
+  } else {
+    CK(cudaFuncSetAttribute(lex_kernel<int64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    lex_kernel<int64_t><<<blocks, kSweepThreads, smem>>>(a, first, count, f, d_out);
+  }
+  LAUNCHED();
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  cudaFree(d_fact);
+  CK(e);
+  return 0;
+}
+
+extern "C" int csk_brute_force_closed(SweepPlan* p, int64_t perms, int64_t* best_m, int64_t* best_k,
+                                      int64_t* distinct, int64_t cap, int64_t* n_distinct, char* err) {
+  // Chunks of <= 2^28 permutations in lexicographic order: makespans, CUB
+  // arg-min (first minimum = the reference's first optimum), then sort +
+  // unique for the distribution; chunk results merge on the host.
+  const int64_t chunk = std::min<int64_t>(perms, int64_t{1} << 28);
+  void *d_ms = nullptr, *d_sorted = nullptr, *d_uniq = nullptr, *d_nu = nullptr, *d_arg = nullptr,
+       *d_tmp = nullptr;
+  size_t tmp_bytes = 0, b1 = 0, b2 = 0, b3 = 0;
+  const int nc = static_cast<int>(chunk);
+  CK(cub::DeviceReduce::ArgMin(nullptr, b1, static_cast<int64_t*>(nullptr),
+                               static_cast<cub::KeyValuePair<int, int64_t>*>(nullptr), nc));
+  CK(cub::DeviceRadixSort::SortKeys(nullptr, b2, static_cast<int64_t*>(nullptr), static_cast<int64_t*>(nullptr), nc));
+  CK(cub::DeviceSelect::Unique(nullptr, b3, static_cast<int64_t*>(nullptr), static_cast<int64_t*>(nullptr),
+                               static_cast<int*>(nullptr), nc));
+  tmp_bytes = std::max(b1, std::max(b2, b3));
+  CK(cudaMalloc(&d_ms, 8 * chunk));
+  CK(cudaMalloc(&d_sorted, 8 * chunk));
+  CK(cudaMalloc(&d_uniq, 8 * chunk));
+  CK(cudaMalloc(&d_nu, 8));
+  CK(cudaMalloc(&d_arg, sizeof(cub::KeyValuePair<int, int64_t>)));
+  CK(cudaMalloc(&d_tmp, std::max<size_t>(tmp_bytes, 16)));
+  std::vector<int64_t> all;
+  bool have = false;
+  int rc = 0;
+  for (int64_t base = 0; base < perms && rc == 0; base += chunk) {
+    const int n = static_cast<int>(std::min(chunk, perms - base));
+    rc = csk_sweep_lex(p, base, n, static_cast<int64_t*>(d_ms), err);
+    if (rc) break;
+    size_t t = tmp_bytes;
+    cudaError_t e = cub::DeviceReduce::ArgMin(d_tmp, t, static_cast<int64_t*>(d_ms),
+                                              static_cast<cub::KeyValuePair<int, int64_t>*>(d_arg), n);
+    cub::KeyValuePair<int, int64_t> h{};
+    if (e == cudaSuccess) e = cudaMemcpy(&h, d_arg, sizeof(h), cudaMemcpyDeviceToHost);
+    t = tmp_bytes;
+    if (e == cudaSuccess)
+      e = cub::DeviceRadixSort::SortKeys(d_tmp, t, static_cast<int64_t*>(d_ms), static_cast<int64_t*>(d_sorted), n);
+    t = tmp_bytes;
+    if (e == cudaSuccess)
+      e = cub::DeviceSelect::Unique(d_tmp, t, static_cast<int64_t*>(d_sorted), static_cast<int64_t*>(d_uniq),
+                                    static_cast<int*>(d_nu), n);
+    int nu = 0;
+    if (e == cudaSuccess) e = cudaMemcpy(&nu, d_nu, sizeof(int), cudaMemcpyDeviceToHost);
+    std::vector<int64_t> u(static_cast<size_t>(nu));
+    if (e == cudaSuccess && nu) e = cudaMemcpy(u.data(), d_uniq, 8ull * nu, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) {
+      std::snprintf(err, 256, "CUDA error %s in brute force", cudaGetErrorString(e));
+      rc = 1;
+      break;
+    }
+    LAUNCHED();
+    if (!have || h.value < *best_m) {
+      *best_m = h.value;
+      *best_k = base + h.key;
+      have = true;
+    }
+    std::vector<int64_t> merged;
+    std::merge(all.begin(), all.end(), u.begin(), u.end(), std::back_inserter(merged));
+    merged.erase(std::unique(merged.begin(), merged.end()), merged.end());
+    all.swap(merged);
+  }
+  for (void* q : {d_ms, d_sorted, d_uniq, d_nu, d_arg, d_tmp}) cudaFree(q);
+  if (rc) return rc;
+  *n_distinct = static_cast<int64_t>(all.size());
+  if (static_cast<int64_t>(all.size()) <= cap) std::copy(all.begin(), all.end(), distinct);
   return 0;
 }
 

@@ -437,7 +437,48 @@ int cs_brute_force(const cs_graph* g, const cs_oracle* o, const cs_sim_policy* p
     need(g, "graph");
     need(o, "oracle");
     need(out_json, "out_json");
-    *out_json = dup(dump_doc(brute_force(*g->g, o->o, policy_of(policy), max_recvs)));
+    const Graph& G = *g->g;
+    const Policy p = policy_of(policy);
+    const int64_t R = static_cast<int64_t>(G.recv_ops().size());
+    if (R > max_recvs)  // metrics.cpp:40-43, checked before anything else
+      fail(kParameter, "brute force refused: " + std::to_string(R) + " recv ops exceed " +
+                           std::to_string(max_recvs));
+    Policy gp = p;
+    gp.gated = true;  // metrics.cpp:45-46
+    if (!G.cluster() && p.noise == 0.0 && R >= 1 && R <= 20) {
+      std::shared_ptr<SweepCtx> ctx = cached_sweep(g, o, gp);  // coverage/noise checks as simulate()
+      if (ctx->fast && !ctx->cluster) {
+        int64_t perms = 1;
+        for (int64_t k = 2; k <= R; ++k) perms *= k;
+        int64_t best_m = 0, best_k = 0, nd = 0;
+        std::vector<int64_t> dist(1 << 16);
+        char err[256] = {0};
+        if (csk_brute_force_closed(ctx->plan, perms, &best_m, &best_k, dist.data(),
+                                   static_cast<int64_t>(dist.size()), &nd, err))
+          fail(kInternal, err);
+        if (nd > static_cast<int64_t>(dist.size())) {
+          dist.resize(static_cast<size_t>(nd));
+          if (csk_brute_force_closed(ctx->plan, perms, &best_m, &best_k, dist.data(), nd, &nd, err))
+            fail(kInternal, err);
+        }
+        dist.resize(static_cast<size_t>(nd));
+        std::vector<std::string> pool = G.recv_ids(), order;  // unrank best_k
+        int64_t rem = best_k, f = perms;
+        for (int64_t k = R; k >= 1; --k) {
+          f /= k;
+          order.push_back(pool[static_cast<size_t>(rem / f)]);
+          pool.erase(pool.begin() + rem / f);
+          rem %= f;
+        }
+        Json j;
+        j["order"] = order;
+        j["makespan_us"] = best_m;
+        j["distribution"] = dist;
+        *out_json = dup(dump_doc(j));
+        return;
+      }
+    }
+    *out_json = dup(dump_doc(brute_force(G, o->o, p, max_recvs)));
   });
 }
 

@@ -158,6 +158,25 @@ def test_brute_force_matches_reference(lib, ref):
             _both(lib, ref, text, lambda L, g: g.brute_force_text(g.declared(), pol, 8))
 
 
+def test_brute_force_closed_form(lib, ref):
+    """Closed-form brute force (lexicographic unranking on the device):
+    byte-equal to the reference at R = 8; at R = 10 consistent with sampled
+    orders and with an exact simulation of the reported optimum."""
+    for shape, layers, params in (("chain", 8, 1), ("layered", 4, 2)):
+        text = lib.generate(shape, layers, params, "1", 21).serialize()
+        _both(lib, ref, text, lambda L, g: g.brute_force_text(g.declared(), None, 8))
+    g = lib.generate("chain", 10, 1, "1/2", 5)
+    o = g.declared()
+    bf = json.loads(g.brute_force_text(o, None, 10))
+    sched = lib.schedule_parse(json.dumps({"graph": g.name(), "algorithm": "random",
+                                           "priorities": {r: i for i, r in enumerate(bf["order"])}}))
+    r = g.simulate(o, sched)
+    assert r.makespan() == bf["makespan_us"] == json.loads(r.json())["makespan_us"]
+    sample = g.sweep_random(o, 1, 20000, None, makespans=True)["makespans"]
+    assert sample.min() >= bf["makespan_us"]
+    assert set(int(x) for x in np.unique(sample)) <= set(bf["distribution"])
+
+
 def test_sweep_matches_reference(lib, ref):
     """cs_sweep_random == the CLI sweep loop over the reference ABI."""
     for name, text in corpus.worker_graphs(lib) + corpus.model_graphs(lib):
