@@ -50,16 +50,32 @@ __host__ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
 __device__ __forceinline__ uint64_t mt_step(uint64_t prev, uint32_t i) {
   return kMtMul * (prev ^ (prev >> 62)) + i;
 }
-// One twist element: c ^ ((a&U | b&L) >> 1) ^ (odd ? MATRIX : 0).
+__device__ __forceinline__ uint32_t lo32(uint64_t x) { return static_cast<uint32_t>(x); }
+__device__ __forceinline__ uint32_t hi32(uint64_t x) { return static_cast<uint32_t>(x >> 32); }
+__device__ __forceinline__ uint64_t join64(uint32_t lo, uint32_t hi) {
+  return (static_cast<uint64_t>(hi) << 32) | lo;
+}
+
+// One twist element: c ^ ((a&U | b&L) >> 1) ^ (odd ? MATRIX : 0), on 32-bit
+// halves (x.hi = a.hi; x.lo = a.lo&0x80000000 | b.lo&0x7fffffff; the odd
+// mask is a 32-bit 0/~0 applied to both halves of MATRIX).
 __device__ __forceinline__ uint64_t mt_twist(uint64_t a, uint64_t b, uint64_t c) {
-  const uint64_t x = (a & kUpper) | (b & kLower);
-  return c ^ (x >> 1) ^ ((x & 1) ? kMtMatrix : 0ULL);
+  const uint32_t xh = hi32(a);
+  const uint32_t xl = (lo32(a) & 0x80000000u) | (lo32(b) & 0x7FFFFFFFu);
+  const uint32_t odd = 0u - (xl & 1u);
+  const uint32_t rl = lo32(c) ^ ((xl >> 1) | (xh << 31)) ^ (odd & 0xA96619E9u);
+  const uint32_t rh = hi32(c) ^ (xh >> 1) ^ (odd & 0xB5026F5Au);
+  return join64(rl, rh);
 }
 __device__ __forceinline__ uint64_t mt_temper(uint64_t y) {
-  y ^= (y >> 29) & 0x5555555555555555ULL;
-  y ^= (y << 17) & 0x71D67FFFEDA60000ULL;
-  y ^= (y << 37) & 0xFFF7EEE000000000ULL;
-  return y ^ (y >> 43);
+  uint32_t l = lo32(y), h = hi32(y);
+  l ^= ((l >> 29) | (h << 3)) & 0x55555555u;  // y ^= (y >> 29) & 0x5555555555555555
+  h ^= (h >> 29) & 0x55555555u;
+  h ^= ((h << 17) | (l >> 15)) & 0x71D67FFFu;  // y ^= (y << 17) & 0x71D67FFFEDA60000
+  l ^= (l << 17) & 0xEDA60000u;
+  h ^= (l << 5) & 0xFFF7EEE0u;                 // y ^= (y << 37) & 0xFFF7EEE000000000
+  l ^= h >> 11;                                // y ^= y >> 43
+  return join64(l, h);
 }
 
 // Full-state engine for streams of any length (state in memory owned by the

@@ -82,8 +82,10 @@ struct Items;  // shared-memory shuffle array, [k / per_word][thread]
 template <>
 struct Items<uint8_t> {
   uint32_t* base;
+  // byte (k & 3) of word (k >> 2) of this thread's column:
+  // (k >> 2) * 4 * kSweepThreads + (k & 3) == k * kSweepThreads - (k & 3) * (kSweepThreads - 1)
   __device__ __forceinline__ uint8_t* at(int k) const {
-    return reinterpret_cast<uint8_t*>(base + (k >> 2) * kSweepThreads) + (k & 3);
+    return reinterpret_cast<uint8_t*>(base) + k * kSweepThreads - (k & 3) * (kSweepThreads - 1);
   }
   __device__ __forceinline__ void init(int R) const {
     for (int q = 0; q < (R + 3) >> 2; ++q)
