@@ -330,12 +330,15 @@ def main():
     d_i64 = torch.zeros(capi.DSTATS_I64, dtype=torch.int64, device="cuda")
     d_f64 = torch.zeros(capi.DSTATS_F64, dtype=torch.float64, device="cuda")
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device="cuda")
-    count = args.count
     from paper_1803_03288_b200 import dist as pdist
-    lo, n = pdist.shard(SEED_LO, count, rank, world)
+    # Weak scaling: every rank sweeps its own 2^24-seed range (the seeds are
+    # independent units, no data-path exchange); total = N * 2^24 per step.
+    per_gpu = args.count
+    count = per_gpu * world
+    lo, n = SEED_LO + rank * per_gpu, per_gpu
     slots = torch.zeros(2 * world, dtype=torch.int64, device="cuda")
 
-    def step():
+    def step(lo=lo, n=n):
         plan.reset(sptr, d_i64.data_ptr(), d_f64.data_ptr())
         k0.record(stream)
         plan.run(lo, n, SEED_LO, sptr, None, d_i64.data_ptr(), d_f64.data_ptr())
@@ -375,6 +378,30 @@ def main():
     kern_per_step = t_kern.item() / args.steps
     value = count / (ms_per_step / 1000.0)
 
+    # Strong-scaling view of config 4 (2^24 orders in total, split over the
+    # ranks), same timing rules, reported beside the weak-scaling headline.
+    strong = None
+    if world > 1:
+        slo, sn = pdist.shard(SEED_LO, per_gpu, rank, world)
+        for _ in range(3):
+            step(slo, sn)
+        torch.cuda.synchronize()
+        sms = []
+        for _ in range(args.steps):
+            flush.fill_(1)
+            dist.barrier()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            step(slo, sn)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            sms.append(e0.elapsed_time(e1))
+        ts = torch.tensor([sum(sms)], dtype=torch.float64, device="cuda")
+        dist.all_reduce(ts, op=dist.ReduceOp.MAX)
+        strong = {"total_orders": per_gpu, "ms_per_step": ts.item() / args.steps,
+                  "value": per_gpu / (ts.item() / args.steps / 1000.0), "unit": "sims/s"}
+
     # e2e: the user path through the public C ABI with host buffers, like the
     # reference arm (which parses the DAG once, then loops over seeds): the
     # DAG is loaded once (cs_graph_parse); every step builds a fresh time
@@ -388,10 +415,10 @@ def main():
             dist.barrier()
         t0 = time.perf_counter()
         st = ge.sweep_random(ge.declared(), lo, n)
-        hv = torch.tensor([st["min_us"] * (1 << 26) + (st["argmin_seed"] - SEED_LO)] +
-                          list(st["e_hist"]), dtype=torch.int64, device="cuda")
+        hv = torch.tensor([st["min_us"], st["sum_us"]] + list(st["e_hist"]), dtype=torch.int64, device="cuda")
         if world > 1:
             dist.all_reduce(hv[1:])
+            dist.all_reduce(hv[:1], op=dist.ReduceOp.MIN)
         hv.cpu()
         e2e_ms.append((time.perf_counter() - t0) * 1000)
     e2e_t = torch.tensor([statistics.median(e2e_ms)], dtype=torch.float64, device="cuda")
@@ -431,13 +458,16 @@ def main():
         out = {
             "metric": "recv-order makespan sims/sec", "value": value, "unit": "sims/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int64",
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
             "data": "synthetic",
             "config": {"workload": f"config4: {MODEL} DAG seed 1 ({info['ops']} ops / {info['edges']} edges / "
-                                   f"{R} recvs, {nc} chain classes), {count} random recv orders per step "
-                                   f"(seeds 1..{count}), gated, choice_seed=seed; min/argmin + E histogram",
-                       "parallelism": f"seed-range shards x{world}", "l2": "flushed between steps (256 MiB write)",
+                                   f"{R} recvs, {nc} chain classes), {per_gpu} random recv orders per GPU "
+                                   f"per step ({count} total, seeds 1..{count}), gated, choice_seed=seed; "
+                                   f"min/argmin + E histogram",
+                       "parallelism": f"contiguous seed ranges x{world}, one NCCL reduction per step",
+                       "l2": "flushed between steps (256 MiB write)",
                        "U_us": info["U_us"], "L_us": info["L_us"]},
+            "strong_scaling_2p24": strong,
             "gpu_launches": launches // max(1, args.steps),
             "kernel_ms_per_step": kern_per_step,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",

@@ -70,6 +70,15 @@ int csk_random_orders(int32_t R, int32_t S, const uint64_t* seeds, int32_t* perm
 /* ---- closed-form batched sweep -------------------- */
 typedef struct SweepPlan SweepPlan;
 
+/* Packed statistics keys are (m << key_bits) | seed offset; every makespan
+ * is <= U, so key_bits = 63 - bitlen(U), capped to 44 (>= 26 while U < 2^37). */
+static inline int csk_key_bits(int64_t U) {
+  int len = 0;
+  while (len < 63 && (U >> len) != 0) ++len;
+  const int kb = 63 - len;
+  return kb > 44 ? 44 : kb;
+}
+
 /* Per-worker chain plan: R recv columns with durations d (int64), first[c]
  * = index of the first chain class containing recv c (nc = none), suffix
  * class weights pwsuf[0..nc]. send_total = total send time on the worker's

@@ -49,6 +49,7 @@ struct ChainArgs {
   int64_t count;
   int64_t U, L;
   int do_e;
+  int key_bits;           // statistics keys: (m << key_bits) | offset
   const int32_t* orders;  // explicit orders mode (W == 1)
   int64_t* makespans;
   int64_t* worker_ms;
@@ -314,8 +315,8 @@ __global__ void __launch_bounds__(kSweepThreads, 3) chain_sweep_kernel(ChainArgs
     const int64_t m = hi;  // worker graph: the makespan; cluster: iteration time
     if (a.makespans) a.makespans[idx] = m;
     const unsigned long long off = seed - a.key_base;
-    kmin = min(kmin, (static_cast<unsigned long long>(m) << 26) | off);
-    kmax = max(kmax, (static_cast<unsigned long long>(m) << 26) | ((1ULL << 26) - 1 - off));
+    kmin = min(kmin, (static_cast<unsigned long long>(m) << a.key_bits) | off);
+    kmax = max(kmax, (static_cast<unsigned long long>(m) << a.key_bits) | ((1ULL << a.key_bits) - 1 - off));
     msum += m;
     ++cnt;
     sq += static_cast<double>(m) * static_cast<double>(m);
@@ -543,6 +544,7 @@ static ChainArgs chain_args(SweepPlan* p) {
   a.U = p->U;
   a.L = p->L;
   a.do_e = !p->cluster && p->U != p->L;
+  a.key_bits = csk_key_bits(p->U);
   return a;
 }
 

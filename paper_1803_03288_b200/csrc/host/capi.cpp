@@ -653,6 +653,7 @@ int cs_sweep_plan_info(const cs_sweep_plan* p, char** out_json) {
     j["U_us"] = c.U;
     j["L_us"] = c.L;
     j["cluster"] = c.cluster;
+    j["key_bits"] = csk_key_bits(c.U);
     *out_json = dup(dump_doc(j));
   });
 }
@@ -674,8 +675,9 @@ int cs_sweep_plan_run(const cs_sweep_plan* p, uint64_t seed_lo, int64_t count, u
     need(d_stats_i64, "d_stats_i64");
     need(d_stats_f64, "d_stats_f64");
     if (count < 0) fail(kParameter, "count must be non-negative");
-    if (seed_lo < key_base || seed_lo - key_base + static_cast<uint64_t>(count) > (uint64_t{1} << 26))
-      fail(kParameter, "seed - key_base must stay below 2^26");
+    const int kb = csk_key_bits(p->ctx->U);
+    if (seed_lo < key_base || seed_lo - key_base + static_cast<uint64_t>(count) > (uint64_t{1} << kb))
+      fail(kParameter, "seed - key_base must stay below 2^" + std::to_string(kb));
     char err[256] = {0};
     if (csk_sweep_run(p->ctx->plan, seed_lo, count, key_base, stream, d_makespans, nullptr, d_stats_i64,
                       d_stats_f64, err))

@@ -242,10 +242,11 @@ void finish_stats(const SweepCtx& s, const int64_t* i64, const double* f64, uint
   out->lower_us = s.L;
   if (out->count > 0) {
     const uint64_t kmin = static_cast<uint64_t>(i64[0]), kmax = static_cast<uint64_t>(i64[1]);
-    const uint64_t mask = (1ULL << 26) - 1;
-    out->min_us = static_cast<int64_t>(kmin >> 26);
+    const int kb = csk_key_bits(s.U);
+    const uint64_t mask = (1ULL << kb) - 1;
+    out->min_us = static_cast<int64_t>(kmin >> kb);
     out->argmin_seed = key_base + (kmin & mask);
-    out->max_us = static_cast<int64_t>(kmax >> 26);
+    out->max_us = static_cast<int64_t>(kmax >> kb);
     out->argmax_seed = key_base + (mask - (kmax & mask));
   }
   out->sum_us = i64[2];
@@ -315,8 +316,9 @@ void sweep_exact(SweepCtx& s, uint64_t seed_lo, int64_t count, int64_t* makespan
       // cluster statistics are over the iteration time, as in the fast path
       const int64_t mstat = s.cluster ? hi : m;
       const uint64_t off = seed - seed_lo;
-      const uint64_t kmin = (static_cast<uint64_t>(mstat) << 26) | off;
-      const uint64_t kmax = (static_cast<uint64_t>(mstat) << 26) | (((1ULL << 26) - 1) - off);
+      const int kb = csk_key_bits(s.U);
+      const uint64_t kmin = (static_cast<uint64_t>(mstat) << kb) | off;
+      const uint64_t kmax = (static_cast<uint64_t>(mstat) << kb) | (((1ULL << kb) - 1) - off);
       if (kmin < static_cast<uint64_t>(i64[0])) i64[0] = static_cast<int64_t>(kmin);
       if (kmax > static_cast<uint64_t>(i64[1])) i64[1] = static_cast<int64_t>(kmax);
       i64[2] += mstat;

@@ -22,8 +22,8 @@ def reduce_stats(i64, f64, rank: int, world: int, slots=None):
     i64[0] (min key) and i64[1] (max key) are gathered through per-rank slots
     of a zeroed vector and one SUM all-reduce, the counters/histograms
     i64[2:] with a second SUM, the float sums f64 with a third. Keys are
-    (m << 26) | offset with offsets relative to the GLOBAL seed base, so the
-    minimum resolves ties to the lowest seed across ranks."""
+    (m << key_bits) | offset with offsets relative to the GLOBAL seed base,
+    so the minimum resolves ties to the lowest seed across ranks."""
     import torch
     import torch.distributed as dist
     if world == 1:
