@@ -5,8 +5,6 @@ per-rank statistics (layout: include/commsched.h CS_DSTATS_*) are combined.
 """
 from __future__ import annotations
 
-KEY_BITS = 26
-
 
 def shard(seed_lo: int, count: int, rank: int, world: int) -> tuple[int, int]:
     """Rank's contiguous seed range [lo, lo + n) of seeds [seed_lo, seed_lo + count)."""
