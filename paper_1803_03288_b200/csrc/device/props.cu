@@ -24,6 +24,7 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cub/cub.cuh>
 #include <mutex>
 #include <vector>
@@ -602,6 +603,12 @@ extern "C" int csk_tac(DeviceGraph* g, const int64_t* dur, int32_t* prio, char* 
   // Per-round work = candidate scan (R_t) + retire list (nnz/R on average).
   const int64_t work = S.nnz / std::max(R, 1) + R;
   int blocks = work > 16384 ? static_cast<int>(std::min<int64_t>(sms * std::max(per_sm, 1), (work + 1023) / 1024)) : 1;
+  // Test knob: force the block count (the multi-block path is otherwise
+  // only taken on graphs too large for the CPU oracle).
+  if (const char* env = std::getenv("TICTAC_TAC_BLOCKS")) {
+    const int forced = std::atoi(env);
+    if (forced > 0) blocks = std::min(forced, sms * std::max(per_sm, 1));
+  }
   blocks = std::max(blocks, 1);
   if (blocks == 1) {
     void* args[] = {&a};

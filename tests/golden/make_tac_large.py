@@ -6,6 +6,10 @@ and the reference library on every graph the reference can finish. Stored
 as SHA-256 of the priorities JSON (schedule serialisation order).
 
     python tests/golden/make_tac_large.py [--top]
+
+(--top, 10^6 ops / 10^5 recvs, takes hours with this oracle's row-major
+retire loop and is not committed; the multi-block TAC kernel that runs there
+is checked by forcing it on the committed sizes, tests/test_gpu_scale.py.)
 """
 import hashlib
 import json

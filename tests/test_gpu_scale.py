@@ -37,6 +37,32 @@ def test_layered_tac_matches_oracle_digest(lib, spec):
     assert hashlib.sha256(text.encode()).hexdigest() == TAC_LARGE[spec]["sha256"]
 
 
+def test_multiblock_tac_matches_single_block(orc):
+    """The distributed-selection TAC kernel (used automatically only on very
+    large graphs) forced on graphs the oracle can check, in a subprocess so
+    the knob is read at call time."""
+    import subprocess
+    import sys
+    code = (
+        "import json,sys,hashlib; sys.path.insert(0,'.'); sys.path.insert(0,'oracle')\n"
+        "from paper_1803_03288_b200.capi import Lib\n"
+        "import oracle\n"
+        "L=Lib(); out={}\n"
+        "for m in ['resnet_v2_50_inference','inception_v3_training','layered:10000:1000','layered:100000:10000']:\n"
+        "    g=L.model(m,1); p=g.tac(g.declared()).priorities()\n"
+        "    out[m]=hashlib.sha256(json.dumps(p,sort_keys=True).encode()).hexdigest()\n"
+        "print(json.dumps(out))\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for blocks in ("1", "7", "64"):
+        r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, check=True,
+                           env={**os.environ, "TICTAC_TAC_BLOCKS": blocks})
+        res[blocks] = json.loads(r.stdout.strip().splitlines()[-1])
+    assert res["1"] == res["7"] == res["64"]
+    for spec in ("layered:10000:1000", "layered:100000:10000"):
+        assert res["64"][spec] == TAC_LARGE[spec]["sha256"]
+
+
 def test_config4_full_sweep(lib, orc):
     """2^24 orders of config 4: spread seeds against the oracle; exact
     statistics against the per-seed makespans; the E identity."""
