@@ -135,11 +135,44 @@ def graph_files(lib, model):
     return g, p
 
 
-def ref_sweep(path, seed_lo, count, threads):
+def ref_sweep(path, seed_lo, count, threads, noise=None, out_path="-"):
     import oracle
-    r = subprocess.run([oracle.REF_SWEEP, "sweep", path, "declared", str(seed_lo), str(count),
-                        str(threads), "-"], capture_output=True, text=True, check=True)
+    cmd = [oracle.REF_SWEEP, "sweep", path, "declared", str(seed_lo), str(count), str(threads), out_path]
+    if noise is not None:
+        cmd.append(repr(float(noise)))
+    r = subprocess.run(cmd, capture_output=True, text=True, check=True)
     return json.loads(r.stdout)
+
+
+def event_replica(lib, path, noise=0.1, count=1 << 18, ref_target_s=5.0):
+    """sweeps outside the closed form run the exact event
+    replica (thread per run at this batch size). Config 4 with reorder noise:
+    device rate through cs_sweep_random (host buffers), the reference library
+    on all host cores for the same seeds, and the makespans of the
+    reference's sample compared value by value."""
+    from paper_1803_03288_b200.capi import policy
+    g = lib.model(MODEL, 1)
+    o = g.declared()
+    pol = policy(True, 0, noise)
+    g.sweep_random(o, SEED_LO, 4096, pol)  # warm
+    t = time.perf_counter()
+    res = g.sweep_random(o, SEED_LO, count, pol, makespans=True)
+    dt = time.perf_counter() - t
+    out = {"workload": f"config4 {MODEL}, counter gate + reorder noise {noise}, seeds {SEED_LO}..",
+           "sims": count, "seconds": round(dt, 4), "sims_per_s": count / dt}
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle
+    if oracle.ref_available():
+        cores = os.cpu_count() or 1
+        cal = ref_sweep(path, SEED_LO, cores * 2, cores, noise)
+        n = min(count, max(cores, int(cal["sims"] / max(cal["seconds"], 1e-9) * ref_target_s)))
+        binp = os.path.join(os.path.dirname(path), "ref_noise.bin")
+        r = ref_sweep(path, SEED_LO, n, cores, noise, binp)
+        ref_ms = np.fromfile(binp, dtype=np.int64)
+        out["reference_cpu"] = {"sims_per_s": r["sims"] / r["seconds"], "cores": cores, "sims": n,
+                                "seconds": round(r["seconds"], 3)}
+        out["sample_identical"] = bool(np.array_equal(ref_ms, res["makespans"][:n]))
+    return out
 
 
 def cpu_baseline(path, target_s=10.0):
@@ -491,6 +524,7 @@ def main():
             out["tac_seconds"] = tac_times(lib, top=args.config5_top)
         if not args.no_configs and world == 1:
             out["configs"] = other_configs(lib)
+            out["configs"]["event_replica_config4_noise"] = event_replica(lib, path)
         if not args.no_cpu and world == 1:
             out["cpu_baseline"] = cpu_baseline(path)
         print(json.dumps(out))

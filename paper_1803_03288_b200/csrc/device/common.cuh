@@ -80,8 +80,10 @@ __device__ __forceinline__ uint64_t mt_temper(uint64_t y) {
 
 // Full-state engine for streams of any length (state in memory owned by the
 // caller: 312 words). Used by single-lane consumers.
-struct MtFull {
-  uint64_t* mt;
+// State behind any indexable P (a pointer, or a strided view).
+template <typename P>
+struct MtFullP {
+  P mt;
   int idx;
   __device__ void seed(uint64_t s) {
     mt[0] = s;
@@ -96,6 +98,7 @@ struct MtFull {
     return mt_temper(mt[idx++]);
   }
 };
+using MtFull = MtFullP<uint64_t*>;
 
 // Register-only engine for the first 311 outputs (SURVEY §7 hard part 2:
 // every random order with R <= 312 lives in the first block). Outputs

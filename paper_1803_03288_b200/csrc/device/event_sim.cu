@@ -10,6 +10,11 @@
 // Used for every cs_simulate call, brute force, and sweeps outside the
 // closed form of SURVEY Appendix A.2.
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <mutex>
+#include <type_traits>
 #include <vector>
 
 #include "common.cuh"
@@ -21,6 +26,8 @@ namespace tictac_dev {
 namespace {
 
 constexpr int kWarpsPerBlock = 4;
+constexpr int64_t kThreadModeMin = 2048;        // batch size from which a thread runs a whole sim
+constexpr size_t kThreadScratch = 16ull << 30;  // cap on thread-mode state in HBM
 constexpr int kEmptyLo = 1 << 29;  // "no ready word" (no overflow when lanes are added)
 constexpr uint64_t kNoiseSalt = 0x9e3779b97f4a7c15ULL;  // sim.cpp:14
 
@@ -59,61 +66,82 @@ struct RunSpec {
 
 // Per-run state. "Hot" arrays (touched every event) live in shared memory
 // when a slot fits, else in global scratch; "cold" arrays always in global.
+//
+// Two run shapes share one kernel body (template kL = lanes per run):
+//  kL = 32: a warp per run — setup and violation counting spread over the
+//           lanes, the event chain on lane 0 (few, long runs);
+//  kL = 1:  a thread per run, 32 runs per warp in lockstep — for large
+//           batches. State is lane-interleaved (element i of lane l at
+//           [i * 32 + l], stride S = 32), so the per-resource loops that all
+//           lanes walk in the same order coalesce into one line per access.
+template <typename T, int S>
+struct Arr {
+  T* p;
+  __device__ __forceinline__ T& operator[](int64_t i) const { return p[i * S]; }
+};
+
+template <int S>
 struct Slot {
   // hot
-  int32_t *missing, *gate, *running, *comp_len, *ready_cnt, *lo, *hi, *haspri;
-  uint32_t *ready, *forced;
-  int64_t *run_end, *counter;
-  uint64_t* mt;
+  Arr<int32_t, S> missing, gate, running, comp_len, ready_cnt, lo, hi, haspri;
+  Arr<uint32_t, S> ready, forced, rready;
+  Arr<int64_t, S> run_end, counter;
+  Arr<uint64_t, S> mt;
   // cold
-  int32_t *orig, *seq, *prio, *items, *comp;
-  int64_t* dev_end;
-  uint64_t* mt2;
+  Arr<int32_t, S> orig, seq, prio, items, comp, rop;
+  Arr<int64_t, S> dev_end;
+  Arr<uint64_t, S> mt2;
 };
 
 __host__ __device__ inline size_t align8(size_t x) { return (x + 7) & ~size_t(7); }
 
-__host__ __device__ inline size_t hot_bytes(int n, int nres, int rbw) {
-  return align8(4ull * n) * 2 + align8(4ull * nres) * 6 + align8(4ull * (rbw + 1)) +
-         align8(4ull * ((n + 31) / 32 + 1)) + align8(8ull * nres) * 2 + 8ull * 312;
+// Bytes of one slot group (S runs interleaved; S = 1 for a warp-per-run slot).
+__host__ __device__ inline size_t hot_bytes(int n, int nres, int rbw, int S = 1) {
+  return align8(4ull * n * S) * 2 + align8(4ull * nres * S) * 6 + align8(4ull * (rbw + 1) * S) * 2 +
+         align8(4ull * ((n + 31) / 32 + 1) * S) + align8(8ull * nres * S) * 2 + 8ull * 312 * S;
 }
 
-__host__ __device__ inline size_t cold_bytes(int n, int ndev, int R) {
-  return align8(4ull * n) * 4 + align8(4ull * (R + 1)) + align8(8ull * (ndev + 1)) + 8ull * 312;
+__host__ __device__ inline size_t cold_bytes(int n, int ndev, int R, int S = 1) {
+  return align8(4ull * n * S) * 5 + align8(4ull * (R + 1) * S) + align8(8ull * (ndev + 1) * S) +
+         8ull * 312 * S;
 }
 
-__device__ Slot carve(char* hot, char* cold, int n, int nres, int ndev, int rbw, int R) {
-  Slot s;
-  auto take = [](char*& base, size_t bytes) {
-    char* p = base;
-    base += align8(bytes);
-    return p;
+template <int S>
+__device__ Slot<S> carve(char* hot, char* cold, int lane, int n, int nres, int ndev, int rbw, int R) {
+  Slot<S> s;
+  auto take = [lane](auto& arr, char*& base, size_t count) {
+    using T = typename std::remove_reference_t<decltype(*arr.p)>;
+    arr.p = reinterpret_cast<T*>(base) + lane;
+    base += align8(sizeof(T) * count * S);
   };
-  s.missing = reinterpret_cast<int32_t*>(take(hot, 4ull * n));
-  s.gate = reinterpret_cast<int32_t*>(take(hot, 4ull * n));
-  s.running = reinterpret_cast<int32_t*>(take(hot, 4ull * nres));
-  s.comp_len = reinterpret_cast<int32_t*>(take(hot, 4ull * nres));
-  s.ready_cnt = reinterpret_cast<int32_t*>(take(hot, 4ull * nres));
-  s.lo = reinterpret_cast<int32_t*>(take(hot, 4ull * nres));
-  s.hi = reinterpret_cast<int32_t*>(take(hot, 4ull * nres));
-  s.haspri = reinterpret_cast<int32_t*>(take(hot, 4ull * nres));
-  s.ready = reinterpret_cast<uint32_t*>(take(hot, 4ull * (rbw + 1)));
-  s.forced = reinterpret_cast<uint32_t*>(take(hot, 4ull * ((n + 31) / 32 + 1)));
-  s.run_end = reinterpret_cast<int64_t*>(take(hot, 8ull * nres));
-  s.counter = reinterpret_cast<int64_t*>(take(hot, 8ull * nres));
-  s.mt = reinterpret_cast<uint64_t*>(take(hot, 8ull * 312));
-  s.orig = reinterpret_cast<int32_t*>(take(cold, 4ull * n));
-  s.seq = reinterpret_cast<int32_t*>(take(cold, 4ull * n));
-  s.prio = reinterpret_cast<int32_t*>(take(cold, 4ull * n));
-  s.comp = reinterpret_cast<int32_t*>(take(cold, 4ull * n));
-  s.items = reinterpret_cast<int32_t*>(take(cold, 4ull * (R + 1)));
-  s.dev_end = reinterpret_cast<int64_t*>(take(cold, 8ull * (ndev + 1)));
-  s.mt2 = reinterpret_cast<uint64_t*>(take(cold, 8ull * 312));
+  take(s.missing, hot, n);
+  take(s.gate, hot, n);
+  take(s.running, hot, nres);
+  take(s.comp_len, hot, nres);
+  take(s.ready_cnt, hot, nres);
+  take(s.lo, hot, nres);
+  take(s.hi, hot, nres);
+  take(s.haspri, hot, nres);
+  take(s.ready, hot, rbw + 1);
+  take(s.rready, hot, rbw + 1);
+  take(s.forced, hot, (n + 31) / 32 + 1);
+  take(s.run_end, hot, nres);
+  take(s.counter, hot, nres);
+  take(s.mt, hot, 312);
+  take(s.orig, cold, n);
+  take(s.seq, cold, n);
+  take(s.prio, cold, n);
+  take(s.comp, cold, n);
+  take(s.rop, cold, n);
+  take(s.items, cold, R + 1);
+  take(s.dev_end, cold, ndev + 1);
+  take(s.mt2, cold, 312);
   return s;
 }
 
-// Lane-0 helpers over a full mt19937_64 state in scratch.
-__device__ uint64_t bounded_full(MtFull& m, uint64_t n, const RunSpec& rs) {
+// Serial helpers over a full mt19937_64 state in scratch.
+template <typename M>
+__device__ uint64_t bounded_full(M& m, uint64_t n, const RunSpec& rs) {
   if (n < 2) return 0;
   uint64_t lim, mag;
   if (n <= static_cast<uint64_t>(0x7fffffff) && rs.lim && n < 4096) {
@@ -131,27 +159,34 @@ __device__ uint64_t bounded_full(MtFull& m, uint64_t n, const RunSpec& rs) {
   return v % n;
 }
 
-__device__ __forceinline__ bool admitted(const Slot& s, int op, int r, int gated) {
+template <int S>
+__device__ __forceinline__ bool admitted(const Slot<S>& s, int op, int r, int gated) {
   const int gt = s.gate[op];
   if (!gated || gt < 0) return true;
   if ((s.forced[op >> 5] >> (op & 31)) & 1u) return true;
   return static_cast<int64_t>(gt) <= s.counter[r];
 }
 
-__device__ void fill_priorities(const GraphView& G, const RunSpec& rs, const Slot& s, int64_t b,
+template <int kL>
+__device__ __forceinline__ void group_sync() {
+  if constexpr (kL == 32) __syncwarp();
+}
+
+template <int kL, int S>
+__device__ void fill_priorities(const GraphView& G, const RunSpec& rs, const Slot<S>& s, int64_t b,
                                 int lane, uint64_t* choice_seed) {
   const int n = G.n;
   if (rs.mode == kPrioExplicit) {
     const int32_t* p = rs.prio + b * n;
-    for (int i = lane; i < n; i += 32) s.prio[i] = p[i];
+    for (int i = lane; i < n; i += kL) s.prio[i] = p[i];
     *choice_seed = rs.seeds[b];
     return;
   }
-  for (int i = lane; i < n; i += 32) s.prio[i] = -1;
-  __syncwarp();
+  for (int i = lane; i < n; i += kL) s.prio[i] = -1;
+  group_sync<kL>();
   if (rs.mode == kPrioOrders) {
     const int32_t* o = rs.orders + b * G.R;
-    for (int k = lane; k < G.R; k += 32) s.prio[G.recv_ops[o[k]]] = k;
+    for (int k = lane; k < G.R; k += kL) s.prio[G.recv_ops[o[k]]] = k;
     *choice_seed = rs.seeds[b];
   } else if (rs.mode == kPrioLex) {
     *choice_seed = rs.seed_lo;
@@ -178,7 +213,7 @@ __device__ void fill_priorities(const GraphView& G, const RunSpec& rs, const Slo
         const int c0 = rs.wcols_off[w], Rw = rs.wcols_off[w + 1] - c0;
         const uint64_t ws = rs.cluster ? splitmix64(seed ^ (kPhi * static_cast<uint64_t>(w + 1))) : seed;
         for (int k = 0; k < Rw; ++k) s.items[k] = k;
-        MtFull m{s.mt2, 0};
+        MtFullP<Arr<uint64_t, S>> m{s.mt2, 0};
         m.seed(ws);
         for (int i = Rw; i > 1; --i) {
           const int j = static_cast<int>(bounded_full(m, static_cast<uint64_t>(i), rs));
@@ -190,32 +225,41 @@ __device__ void fill_priorities(const GraphView& G, const RunSpec& rs, const Slo
       }
     }
   }
-  __syncwarp();
+  group_sync<kL>();
 }
 
+template <int kL, int S>
 __global__ void __launch_bounds__(32 * kWarpsPerBlock)
     event_sim_kernel(GraphView G, RunSpec rs, int64_t B, char* hot_global, size_t hot_sz, char* cold_scr,
                      size_t cold_sz, int rbw) {
+  // S = element stride of the per-run state: 32 = lane-interleaved groups of
+  // 32 runs (one per warp), 1 = each run's state contiguous
   extern __shared__ __align__(16) char smem_hot[];
-  const int lane = threadIdx.x & 31;
-  const int64_t slot_id = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nslots = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
-  char* hot = hot_global ? hot_global + slot_id * hot_sz : smem_hot + (threadIdx.x >> 5) * hot_sz;
-  const Slot s = carve(hot, cold_scr + slot_id * cold_sz, G.n, G.nres, G.ndev, rbw, G.R);
+  const int lane = kL == 32 ? (threadIdx.x & 31) : 0;
+  const int64_t gtid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t slot_id = kL == 32 ? (gtid >> 5) : gtid;
+  const int64_t unit = S == 32 ? (gtid >> 5) : slot_id;  // index of this thread's state block
+  const int64_t nslots = (static_cast<int64_t>(gridDim.x) * blockDim.x) / kL;
+  char* hot = hot_global ? hot_global + unit * hot_sz : smem_hot + (threadIdx.x >> 5) * hot_sz;
+  const Slot<S> s = carve<S>(hot, cold_scr + unit * cold_sz, S == 32 ? (threadIdx.x & 31) : 0, G.n, G.nres,
+                             G.ndev, rbw, G.R);
   const int n = G.n, nres = G.nres;
 
   for (int64_t b = slot_id; b < B; b += nslots) {
     uint64_t choice_seed = 0;
-    fill_priorities(G, rs, s, b, lane, &choice_seed);
+    fill_priorities<kL>(G, rs, s, b, lane, &choice_seed);
     // ---- setup (sim.cpp:74-123)
-    for (int i = lane; i < n; i += 32) {
+    for (int i = lane; i < n; i += kL) {
       s.missing[i] = G.pred_off[i + 1] - G.pred_off[i];
       s.gate[i] = -1;
       s.orig[i] = -1;
     }
-    for (int w = lane; w < rbw; w += 32) s.ready[w] = 0;
-    for (int w = lane; w < (n + 31) / 32; w += 32) s.forced[w] = 0;
-    for (int r = lane; r < nres; r += 32) {
+    for (int w = lane; w < rbw; w += kL) {
+      s.ready[w] = 0;
+      s.rready[w] = 0;
+    }
+    for (int w = lane; w < (n + 31) / 32; w += kL) s.forced[w] = 0;
+    for (int r = lane; r < nres; r += kL) {
       s.running[r] = -1;
       s.run_end[r] = 0;
       s.counter[r] = 0;
@@ -225,27 +269,56 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock)
       s.hi[r] = -1;
       s.haspri[r] = 0;
     }
-    for (int d = lane; d < G.ndev; d += 32) s.dev_end[d] = 0;
-    __syncwarp();
-    for (int i = lane; i < n; i += 32) {
+    for (int d = lane; d < G.ndev; d += kL) s.dev_end[d] = 0;
+    group_sync<kL>();
+    for (int i = lane; i < n; i += kL) {
       if (s.prio[i] >= 0) s.haspri[G.res[i]] = 1;
       if (s.missing[i] == 0) {
         const int r = G.res[i], l = G.lidx[i];
-        atomicOr(&s.ready[G.rb_off[r] + (l >> 5)], 1u << (l & 31));
-        atomicAdd(&s.ready_cnt[r], 1);
-        atomicMin(&s.lo[r], l >> 5);
-        atomicMax(&s.hi[r], l >> 5);
+        if constexpr (kL == 32) {
+          atomicOr(&s.ready[G.rb_off[r] + (l >> 5)], 1u << (l & 31));
+          atomicAdd(&s.ready_cnt[r], 1);
+          atomicMin(&s.lo[r], l >> 5);
+          atomicMax(&s.hi[r], l >> 5);
+        } else {
+          s.ready[G.rb_off[r] + (l >> 5)] |= 1u << (l & 31);
+          s.ready_cnt[r] += 1;
+          s.lo[r] = min(s.lo[r], l >> 5);
+          s.hi[r] = max(s.hi[r], l >> 5);
+        }
       }
     }
     // dense per-channel ranks from (priority, id), then noise swaps
-    MtFull noise{s.mt2, 0};
+    MtFullP<Arr<uint64_t, S>> noise{s.mt2, 0};
     const bool noisy = rs.gated && rs.noise > 0.0;
     if (lane == 0 && noisy) noise.seed(splitmix64(choice_seed ^ kNoiseSalt));
     for (int r = 0; r < nres; ++r) {
       if (!G.chan[r]) continue;
       const int o0 = G.rops_off[r], o1 = G.rops_off[r + 1];
       int mine = 0;
-      for (int a = o0 + lane; a < o1; a += 32) {
+      if (kL == 1 && rs.mode != kPrioExplicit) {
+        // priorities here are positions in a permutation, so distinct: rank
+        // by walking the values instead of counting pairs (items = scratch)
+        int pmin = 0x7fffffff, pmax = -1;
+        for (int a = o0; a < o1; ++a) {
+          const int i = G.rops[a];
+          const int pi = s.prio[i];
+          if (pi < 0) continue;
+          s.items[pi] = i;
+          pmin = min(pmin, pi);
+          pmax = max(pmax, pi);
+        }
+        for (int p = pmin; p <= pmax; ++p) {
+          const int i = s.items[p];
+          // stale (or never written) entry from another channel
+          if (static_cast<unsigned>(i) >= static_cast<unsigned>(n) || G.res[i] != r || s.prio[i] != p) continue;
+          s.orig[i] = mine;
+          s.seq[o0 + mine] = i;
+          s.rop[o0 + mine] = i;
+          ++mine;
+        }
+      } else
+      for (int a = o0 + lane; a < o1; a += kL) {
         const int i = G.rops[a];
         const int pi = s.prio[i];
         if (pi < 0) continue;
@@ -257,10 +330,27 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock)
         }
         s.orig[i] = rank;
         s.seq[o0 + rank] = i;
+        s.rop[o0 + rank] = i;
         ++mine;
       }
-      const int k = warp_sum(mine);
-      __syncwarp();
+      int k = mine;
+      if constexpr (kL == 32) k = warp_sum(mine);
+      group_sync<kL>();
+      if (k > 0 && k == o1 - o0) {
+        // every op on the channel is prioritized: also index ready ops by
+        // rank, so a start walks from the lowest ready rank (try_start)
+        if (lane == 0) s.haspri[r] = 2;
+        for (int a = o0 + lane; a < o1; a += kL) {
+          const int i = G.rops[a];
+          if (s.missing[i] != 0) continue;
+          const int q = s.orig[i];
+          if constexpr (kL == 32)
+            atomicOr(&s.rready[G.rb_off[r] + (q >> 5)], 1u << (q & 31));
+          else
+            s.rready[G.rb_off[r] + (q >> 5)] |= 1u << (q & 31);
+        }
+        group_sync<kL>();
+      }
       if (!rs.gated) continue;
       if (lane == 0 && noisy)
         for (int p = 1; p < k; ++p) {
@@ -271,13 +361,13 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock)
             s.seq[o0 + p] = t;
           }
         }
-      __syncwarp();
-      for (int p = lane; p < k; p += 32) s.gate[s.seq[o0 + p]] = p;
-      __syncwarp();
+      group_sync<kL>();
+      for (int p = lane; p < k; p += kL) s.gate[s.seq[o0 + p]] = p;
+      group_sync<kL>();
     }
-    MtFull choice{s.mt, 0};
+    MtFullP<Arr<uint64_t, S>> choice{s.mt, 0};
     if (lane == 0) choice.seed(choice_seed);
-    __syncwarp();
+    group_sync<kL>();
 
     // ---- event loop (sim.cpp:194-233), run serially by lane 0 on the
     // shared-memory state: the replica is a dependent chain, and warp-wide
@@ -290,11 +380,13 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock)
     const bool rec = (b == 0) && rs.start;
     if (lane == 0) {
       int finished = 0;
-      // kernels support up to 64 resources on the fast mask; more use a scan
-      const bool small_res = nres <= 64;
       auto start_op = [&](int r, int op) {
         const int l = G.lidx[op];
         s.ready[G.rb_off[r] + (l >> 5)] &= ~(1u << (l & 31));
+        if (s.haspri[r] == 2) {
+          const int q = s.orig[op];
+          s.rready[G.rb_off[r] + (q >> 5)] &= ~(1u << (q & 31));
+        }
         s.ready_cnt[r] -= 1;
         s.running[r] = op;
         const int64_t e = t + G.dur[op];
@@ -310,6 +402,49 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock)
       // sim.cpp:163-192 for one resource; returns true when an op started
       auto try_start = [&](int r) -> bool {
         if (s.running[r] >= 0 || s.ready_cnt[r] == 0) return false;
+        if (s.haspri[r] == 2) {
+          // Fully prioritized channel: ranks ascend with (priority, id), so
+          // the reference's candidates (admitted ops at the minimum admitted
+          // priority, in id order) are the admitted ops of one equal-priority
+          // run of ranks, starting at the first admitted ready rank.
+          const int wb = G.rb_off[r], o0 = G.rops_off[r];
+          const int nw = (G.rops_off[r + 1] - o0 + 31) >> 5;
+          int best = -1, total = 0;
+          bool done = false;
+          for (int w = 0; w < nw && !done; ++w) {
+            uint32_t bits = s.rready[wb + w];
+            while (bits) {
+              const int bit = __ffs(bits) - 1;
+              bits &= bits - 1;
+              const int op = s.rop[o0 + (w << 5) + bit];
+              const int p = s.prio[op];
+              if (best >= 0 && p != best) {
+                done = true;
+                break;
+              }
+              if (admitted(s, op, r, gated)) {
+                best = p;
+                ++total;
+              }
+            }
+          }
+          if (total == 0) return false;
+          int k = total > 1 ? static_cast<int>(bounded_full(choice, static_cast<uint64_t>(total), rs)) : 0;
+          for (int w = 0; w < nw; ++w) {
+            uint32_t bits = s.rready[wb + w];
+            while (bits) {
+              const int bit = __ffs(bits) - 1;
+              bits &= bits - 1;
+              const int op = s.rop[o0 + (w << 5) + bit];
+              if (s.prio[op] != best || !admitted(s, op, r, gated)) continue;
+              if (k-- == 0) {
+                start_op(r, op);
+                return true;
+              }
+            }
+          }
+          return false;  // unreachable
+        }
         const bool pri = s.haspri[r] != 0;
         const int wb = G.rb_off[r], ob = G.rops_off[r];
         int nlo = kEmptyLo, nhi = -1, best = 0x7fffffff;
@@ -360,6 +495,10 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock)
       auto push_ready = [&](int w_op) {
         const int rw = G.res[w_op], l = G.lidx[w_op];
         s.ready[G.rb_off[rw] + (l >> 5)] |= 1u << (l & 31);
+        if (s.haspri[rw] == 2) {
+          const int q = s.orig[w_op];
+          s.rready[G.rb_off[rw] + (q >> 5)] |= 1u << (q & 31);
+        }
         s.ready_cnt[rw] += 1;
         s.lo[rw] = min(s.lo[rw], l >> 5);
         s.hi[rw] = max(s.hi[rw], l >> 5);
@@ -385,7 +524,6 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock)
         }
         return any;
       };
-      (void)small_res;
       while (finished < n) {
         bool progress = true;
         while (progress) {
@@ -423,22 +561,26 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock)
         complete_now();
       }
     }
-    __syncwarp();
-    mk = __shfl_sync(~0u, mk, 0);
-    nforced = __shfl_sync(~0u, nforced, 0);
-    stalled = __shfl_sync(~0u, stalled, 0);
+    if constexpr (kL == 32) {
+      __syncwarp();
+      mk = __shfl_sync(~0u, mk, 0);
+      nforced = __shfl_sync(~0u, nforced, 0);
+      stalled = __shfl_sync(~0u, stalled, 0);
+    }
 
     // violations: rank inversions per channel completion sequence + forced
     int64_t inv = 0;
     for (int r = 0; r < nres; ++r) {
       if (!G.chan[r]) continue;
-      const int* seq = s.comp + G.rops_off[r];
+      const int base = G.rops_off[r];
       const int len = s.comp_len[r];
-      for (int a = lane; a < len; a += 32)
-        for (int c = a + 1; c < len; ++c) inv += seq[a] > seq[c];
+      for (int a = lane; a < len; a += kL)
+        for (int c = a + 1; c < len; ++c) inv += s.comp[base + a] > s.comp[base + c];
     }
+    if constexpr (kL == 32) {
 #pragma unroll
-    for (int o = 16; o; o >>= 1) inv += __shfl_xor_sync(~0u, inv, o);
+      for (int o = 16; o; o >>= 1) inv += __shfl_xor_sync(~0u, inv, o);
+    }
     if (lane == 0) {
       rs.makespan[b] = mk;
       rs.violations[b] = inv + nforced;
@@ -446,7 +588,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock)
       if (rs.dev_end)
         for (int d = 0; d < G.ndev; ++d) rs.dev_end[b * G.ndev + d] = s.dev_end[d];
     }
-    __syncwarp();
+    group_sync<kL>();
   }
 }
 
@@ -464,12 +606,42 @@ int dev_copy(DevBuf& buf, const T* src, size_t count, char* err) {
   return 0;
 }
 
+// Grow-only per-device scratch for the per-run state: thread-per-run
+// batches take gigabytes, which are not worth re-allocating each call. The
+// lock is held for the whole (synchronous) run.
+struct ScratchPool {
+  std::mutex m;
+  void* p[64] = {};
+  size_t cap[64] = {};
+  char* get(int dev, size_t bytes, char* err) {
+    if (dev < 0 || dev >= 64) dev = 0;
+    if (cap[dev] < bytes) {
+      if (p[dev]) cudaFree(p[dev]);
+      p[dev] = nullptr;
+      cap[dev] = 0;
+      if (cudaMalloc(&p[dev], bytes) != cudaSuccess) {
+        cudaGetLastError();
+        std::snprintf(err, 256, "cannot allocate %zu bytes of simulator scratch", bytes);
+        return nullptr;
+      }
+      cap[dev] = bytes;
+    }
+    return static_cast<char*>(p[dev]);
+  }
+};
+ScratchPool& scratch_pool() {
+  static ScratchPool* pool = new ScratchPool;  // never destroyed: process-lifetime device memory
+  return *pool;
+}
+
 int run_event(DeviceGraph* g, const int64_t* dur, int64_t B, RunSpec rs, int64_t* makespan,
               int64_t* violations, int32_t* status, int64_t* start, int64_t* end, int64_t* dev_end,
               char* err) {
   if (ensure_device(err)) return 1;
   if (B <= 0) return 0;
-  DevBuf d_dur, d_ms, d_vio, d_st, d_start, d_end, d_dev, d_scr, d_hot, d_lim, d_mag;
+  DevBuf d_dur, d_ms, d_vio, d_st, d_start, d_end, d_dev, d_lim, d_mag;
+  ScratchPool& pool = scratch_pool();
+  std::lock_guard<std::mutex> lock(pool.m);
   if (dev_copy(d_dur, dur, g->n, err)) return 1;
   std::vector<uint64_t> lim(4096), mag(4096);
   for (uint64_t k = 0; k < 4096; ++k) bounded_consts(k, &lim[k], &mag[k]);
@@ -498,46 +670,94 @@ int run_event(DeviceGraph* g, const int64_t* dur, int64_t B, RunSpec rs, int64_t
   GraphView G{g->n,        g->nres,     g->ndev,     g->R,        g->pred_off, g->succ_off,
               g->succ_idx, g->res,      g->res_dev,  g->rops_off, g->rops,     g->lidx,
               g->rb_off,   g->recv_ops, g->chan,     static_cast<int64_t*>(d_dur.p)};
-  int sms = 148;
-  {
-    int dev = 0;
-    CK(cudaGetDevice(&dev));
-    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  int sms = 148, dev = 0;
+  CK(cudaGetDevice(&dev));
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  // Large batches: a thread per run (32 interleaved runs per warp) keeps
+  // 32x more runs in flight than a warp per run; the lockstep lanes walk the
+  // resource loops together, so their state accesses coalesce.
+  const bool trace = std::getenv("TICTAC_EVENT_TRACE") != nullptr;
+  const auto wall0 = std::chrono::steady_clock::now();
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  if (trace) {
+    cudaEventCreate(&ev0);
+    cudaEventCreate(&ev1);
+    cudaEventRecord(ev0);
   }
-  // Hot per-run state in shared memory when a slot fits (up to
-  // kWarpsPerBlock runs per block), otherwise in global scratch.
-  const size_t hsz = align8(hot_bytes(g->n, g->nres, g->rb_words));
-  const size_t csz = align8(cold_bytes(g->n, g->ndev, g->R));
-  // Shared memory wins per run (~1.7x) but caps runs per SM; large batches
-  // of long runs keep more warps in flight with global scratch instead.
-  constexpr size_t kSmemBudget = 200 * 1024;
-  const int64_t smem_runs = static_cast<int64_t>(sms) * std::max<int64_t>(1, (227 * 1024) / std::max<size_t>(hsz, 1));
-  const bool in_smem = hsz <= kSmemBudget && (B <= smem_runs || hsz <= 16 * 1024);
-  // Few runs: one run per block, so the unused shared-memory carve-out stays
-  // L1 for the graph arrays the (latency-bound) event chain reads.
-  const int wpb = !in_smem ? kWarpsPerBlock
-                  : B <= sms ? 1
-                             : static_cast<int>(std::min<size_t>(kWarpsPerBlock, kSmemBudget / hsz));
-  int per_sm = 16;
-  if (in_smem) {
-    CK(cudaFuncSetAttribute(event_sim_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            static_cast<int>(hsz * wpb)));
-    const int carve = static_cast<int>(std::min<size_t>(100, (hsz * wpb * 100 + 228 * 1024 - 1) / (228 * 1024) + 3));
-    CK(cudaFuncSetAttribute(event_sim_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
+  int lanes = B >= kThreadModeMin ? 1 : 32;
+  if (const char* env = std::getenv("TICTAC_EVENT_LANES")) lanes = std::atoi(env) == 1 ? 1 : 32;
+  if (lanes == 1) {
+    bool inter = true;  // lane-interleaved state
+    if (const char* env = std::getenv("TICTAC_EVENT_LAYOUT")) inter = std::atoi(env) != 1;
+    const int lay = inter ? 32 : 1;
+    const size_t hg = align8(hot_bytes(g->n, g->nres, g->rb_words, lay));
+    const size_t cg = align8(cold_bytes(g->n, g->ndev, g->R, lay));
+    const size_t per_group = inter ? 1 : 32;  // state blocks per 32-run warp
+    // as many 32-run warps per SM as are resident (latency-bound chains)
     int occ = 1;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, event_sim_kernel, 32 * wpb, hsz * wpb));
-    per_sm = std::max(1, occ) * wpb;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, event_sim_kernel<1, 32>, 32 * kWarpsPerBlock, 0));
+    int per_sm = std::max(1, occ) * kWarpsPerBlock;
+    if (const char* env = std::getenv("TICTAC_EVENT_GROUPS")) per_sm = std::max(1, std::atoi(env));
+    int64_t groups = std::min<int64_t>((B + 31) / 32, static_cast<int64_t>(sms) * per_sm);
+    groups = std::max<int64_t>(
+        1, std::min<int64_t>(groups, static_cast<int64_t>(kThreadScratch / ((hg + cg) * per_group))));
+    const int blocks = static_cast<int>((groups + kWarpsPerBlock - 1) / kWarpsPerBlock);
+    const size_t total = static_cast<size_t>(blocks) * kWarpsPerBlock * per_group;
+    char* scr = pool.get(dev, (hg + cg) * total, err);
+    if (!scr) return 1;
+    if (inter)
+      event_sim_kernel<1, 32><<<blocks, 32 * kWarpsPerBlock>>>(G, rs, B, scr, hg, scr + hg * total, cg, g->rb_words);
+    else
+      event_sim_kernel<1, 1><<<blocks, 32 * kWarpsPerBlock>>>(G, rs, B, scr, hg, scr + hg * total, cg, g->rb_words);
+  } else {
+    // Hot per-run state in shared memory when a slot fits (up to
+    // kWarpsPerBlock runs per block), otherwise in global scratch.
+    const size_t hsz = align8(hot_bytes(g->n, g->nres, g->rb_words));
+    const size_t csz = align8(cold_bytes(g->n, g->ndev, g->R));
+    // Shared memory wins per run (~1.7x) but caps runs per SM; large batches
+    // of long runs keep more warps in flight with global scratch instead.
+    constexpr size_t kSmemBudget = 200 * 1024;
+    const int64_t smem_runs =
+        static_cast<int64_t>(sms) * std::max<int64_t>(1, (227 * 1024) / std::max<size_t>(hsz, 1));
+    const bool in_smem = hsz <= kSmemBudget && (B <= smem_runs || hsz <= 16 * 1024);
+    // Few runs: one run per block, so the unused shared-memory carve-out stays
+    // L1 for the graph arrays the (latency-bound) event chain reads.
+    const int wpb = !in_smem ? kWarpsPerBlock
+                    : B <= sms ? 1
+                               : static_cast<int>(std::min<size_t>(kWarpsPerBlock, kSmemBudget / hsz));
+    int per_sm = 16;
+    if (in_smem) {
+      CK(cudaFuncSetAttribute(event_sim_kernel<32, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              static_cast<int>(hsz * wpb)));
+      const int carve =
+          static_cast<int>(std::min<size_t>(100, (hsz * wpb * 100 + 228 * 1024 - 1) / (228 * 1024) + 3));
+      CK(cudaFuncSetAttribute(event_sim_kernel<32, 1>, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
+      int occ = 1;
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, event_sim_kernel<32, 1>, 32 * wpb, hsz * wpb));
+      per_sm = std::max(1, occ) * wpb;
+    }
+    const int64_t slots = std::min<int64_t>(B, static_cast<int64_t>(sms) * per_sm);
+    const int blocks = static_cast<int>((slots + wpb - 1) / wpb);
+    const int64_t total_slots = static_cast<int64_t>(blocks) * wpb;
+    const size_t hot_total = in_smem ? 0 : hsz * static_cast<size_t>(total_slots);
+    char* scr = pool.get(dev, hot_total + csz * static_cast<size_t>(total_slots), err);
+    if (!scr) return 1;
+    event_sim_kernel<32, 1><<<blocks, 32 * wpb, in_smem ? hsz * wpb : 0>>>(
+        G, rs, B, in_smem ? nullptr : scr, hsz, scr + hot_total, csz, g->rb_words);
   }
-  const int64_t slots = std::min<int64_t>(B, static_cast<int64_t>(sms) * per_sm);
-  const int blocks = static_cast<int>((slots + wpb - 1) / wpb);
-  const int64_t total_slots = static_cast<int64_t>(blocks) * wpb;
-  CK(cudaMalloc(&d_scr.p, csz * static_cast<size_t>(total_slots)));
-  if (!in_smem) CK(cudaMalloc(&d_hot.p, hsz * static_cast<size_t>(total_slots)));
-  event_sim_kernel<<<blocks, 32 * wpb, in_smem ? hsz * wpb : 0>>>(
-      G, rs, B, static_cast<char*>(d_hot.p), hsz, static_cast<char*>(d_scr.p), csz, g->rb_words);
   LAUNCHED();
   CK(cudaGetLastError());
+  if (trace) cudaEventRecord(ev1);
   CK(cudaDeviceSynchronize());
+  if (trace) {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, ev0, ev1);
+    const double wall = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - wall0).count();
+    std::fprintf(stderr, "[event_sim] B=%lld lanes=%d kernel %.3f ms (run_event so far %.3f ms)\n",
+                 static_cast<long long>(B), lanes, ms, wall);
+    cudaEventDestroy(ev0);
+    cudaEventDestroy(ev1);
+  }
   CK(cudaMemcpy(makespan, d_ms.p, 8 * B, cudaMemcpyDeviceToHost));
   if (violations) CK(cudaMemcpy(violations, d_vio.p, 8 * B, cudaMemcpyDeviceToHost));
   CK(cudaMemcpy(status, d_st.p, 4 * B, cudaMemcpyDeviceToHost));

@@ -6,6 +6,9 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -499,10 +502,18 @@ int cs_sweep_random(const cs_graph* g, const cs_oracle* o, uint64_t seed_lo, int
     need(o, "oracle");
     if (count < 0) fail(kParameter, "count must be non-negative");
     Policy p = policy_of(policy);
+    const auto t0 = std::chrono::steady_clock::now();
     std::shared_ptr<SweepCtx> ctx = cached_sweep(g, o, p);
     const bool cluster_m = ctx->cluster && makespans_out;  // needs the full event replica
     if (!ctx->fast || cluster_m) {
+      const auto t1 = std::chrono::steady_clock::now();
       sweep_exact(*ctx, seed_lo, count, makespans_out, worker_makespans_out, stats_out);
+      if (std::getenv("TICTAC_EVENT_TRACE")) {
+        const auto t2 = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[cs_sweep_random] ctx %.3f ms, exact sweep %.3f ms\n",
+                     std::chrono::duration<double, std::milli>(t1 - t0).count(),
+                     std::chrono::duration<double, std::milli>(t2 - t1).count());
+      }
       return;
     }
     // fast path: device buffers, one launch per 2^26 seeds
@@ -609,7 +620,7 @@ int cs_simulate_orders(const cs_graph* g, const cs_oracle* o, const int32_t* ord
     std::vector<int64_t> viol(static_cast<size_t>(n));
     std::vector<int32_t> st(static_cast<size_t>(n));
     char err[256] = {0};
-    const int64_t chunk = 1 << 16;
+    const int64_t chunk = 1 << 20;
     for (int64_t b = 0; b < n; b += chunk) {
       const int32_t B = static_cast<int32_t>(std::min(chunk, n - b));
       if (csk_event_sim(G.device(), ctx->dur.data(), B, nullptr, orders + b * R, R, seeds.data() + b,

@@ -8,6 +8,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <set>
 
@@ -277,7 +280,7 @@ void sweep_exact(SweepCtx& s, uint64_t seed_lo, int64_t count, int64_t* makespan
   std::vector<int64_t> i64(CS_DSTATS_I64, 0);
   std::vector<double> f64(CS_DSTATS_F64, 0.0);
   i64[0] = -1;  // as unsigned: max
-  const int64_t chunk = 1 << 16;
+  const int64_t chunk = 1 << 20;
   std::vector<int64_t> ms, viol, dev_end;
   std::vector<int32_t> st;
   for (int64_t base = 0; base < count; base += chunk) {
@@ -287,11 +290,15 @@ void sweep_exact(SweepCtx& s, uint64_t seed_lo, int64_t count, int64_t* makespan
     st.resize(B);
     dev_end.resize(static_cast<size_t>(B) * devs.size());
     char err[256] = {0};
+    const auto t0 = std::chrono::steady_clock::now();
     const int rc = csk_event_sweep(dg, s.dur.data(), seed_lo + static_cast<uint64_t>(base), B,
                                    s.cluster ? 1 : 0, s.recv_worker.data(), nw, s.policy.gated ? 1 : 0,
                                    s.policy.noise, ms.data(), viol.data(), st.data(),
                                    s.cluster ? dev_end.data() : nullptr, err);
     if (rc) fail(kInternal, err);
+    if (std::getenv("TICTAC_EVENT_TRACE"))
+      std::fprintf(stderr, "[sweep_exact] csk_event_sweep %.3f ms\n",
+                   std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
     for (int32_t b = 0; b < B; ++b) {
       if (st[b]) fail(kValidation, "simulation stalled with no runnable op");
       const int64_t idx = base + b;

@@ -36,3 +36,72 @@ def cluster_graphs(lib):
 
 def model_graphs(lib):
     return [(m, lib.model(m, 1).serialize()) for m in MODELS]
+
+
+def _op(oid, kind, dev, unit, name, t):
+    return {"id": oid, "kind": kind, "resource": {"device": dev, "unit": unit, "name": name}, "time_us": t}
+
+
+def irregular_worker(seed: int, n_comp=14, n_recv=6, n_send=2, cpus=2, chans=2):
+    """Worker partition outside the closed form's preconditions: several
+    compute units and channels on one device, send ops, zero durations,
+    multi-parent DAG. Seeded python RNG; reference-format JSON."""
+    import json
+    import random
+    rnd = random.Random(seed)
+    ops, edges = [], []
+    recvs = [f"r{k:02d}" for k in range(n_recv)]
+    comps = [f"c{k:02d}" for k in range(n_comp)]
+    sends = [f"s{k:02d}" for k in range(n_send)]
+    for r in recvs:
+        ops.append(_op(r, "recv", "w0", "channel", f"net{rnd.randrange(chans)}", rnd.choice([0, 1, 2, 3, 5, 8])))
+    for k, c in enumerate(comps):
+        ops.append(_op(c, "compute", "w0", "compute", f"cpu{rnd.randrange(cpus)}", rnd.choice([0, 1, 2, 4, 6])))
+        pool = recvs + comps[:k]
+        for p in rnd.sample(pool, min(len(pool), rnd.randint(1, 3))):
+            edges.append([p, c])
+    for s in sends:
+        ops.append(_op(s, "send", "w0", "channel", f"net{rnd.randrange(chans)}", rnd.choice([1, 2, 3])))
+        for p in rnd.sample(comps, 2):
+            edges.append([p, s])
+    rnd.shuffle(ops)
+    return json.dumps({"name": f"irregular-w{seed}", "partition": "worker", "ops": ops, "edges": edges})
+
+
+def irregular_cluster(seed: int, workers=2, n_comp=8, n_recv=4):
+    """Cluster partition where worker recvs have predecessors (PS reads) and
+    sends feed PS aggregation: recvs are not roots, per-worker resources
+    differ in size."""
+    import json
+    import random
+    rnd = random.Random(seed)
+    ops, edges = [], []
+    for k in range(n_recv):
+        ops.append(_op(f"ps/read{k}", "ps_read", "ps0", "compute", "cpu0", rnd.choice([0, 1, 2])))
+        ops.append(_op(f"ps/agg{k}", "ps_aggregate", "ps0", "compute", "cpu0", rnd.choice([1, 2])))
+        ops.append(_op(f"ps/upd{k}", "ps_update", "ps0", "compute", "cpu0", 1))
+        edges.append([f"ps/agg{k}", f"ps/upd{k}"])
+    for w in range(workers):
+        d = f"w{w}"
+        comps = [f"{d}/c{k:02d}" for k in range(n_comp)]
+        recvs = [f"{d}/r{k:02d}" for k in range(n_recv)]
+        for k, r in enumerate(recvs):
+            ops.append(_op(r, "recv", d, "channel", f"net{rnd.randrange(2)}", rnd.choice([1, 2, 3, 5])))
+            edges.append([f"ps/read{k}", r])
+        for k, c in enumerate(comps):
+            ops.append(_op(c, "compute", d, "compute", f"cpu{rnd.randrange(2)}", rnd.choice([0, 1, 3, 4])))
+            pool = recvs + comps[:k]
+            for p in rnd.sample(pool, min(len(pool), rnd.randint(1, 2))):
+                edges.append([p, c])
+        for k in range(n_recv):
+            s = f"{d}/s{k:02d}"
+            ops.append(_op(s, "send", d, "channel", f"net{rnd.randrange(2)}", rnd.choice([1, 2])))
+            edges.append([rnd.choice(comps), s])
+            edges.append([s, f"ps/agg{k}"])
+    return json.dumps({"name": f"irregular-c{seed}", "partition": "cluster", "ops": ops, "edges": edges})
+
+
+def irregular_graphs():
+    return ([(f"irregular-w{s}", irregular_worker(s)) for s in (1, 2, 3, 4)] +
+            [("irregular-w5-wide", irregular_worker(5, n_comp=30, n_recv=9, n_send=3, cpus=3, chans=3))] +
+            [(f"irregular-c{s}", irregular_cluster(s)) for s in (1, 2)])

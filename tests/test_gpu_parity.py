@@ -206,3 +206,89 @@ def test_cluster_sweep_matches_reference(lib, ref):
             it = json.loads(r.iteration_json())
             assert res["makespans"][i] == r.makespan()
             assert list(res["worker_makespans"][i]) == list(it["per_worker_makespan_us"].values())
+
+
+@pytest.mark.parametrize("model", ["resnet_v2_50_inference", "vgg16_training"])
+def test_event_sim_lane_modes_agree(lib, orc, monkeypatch, model):
+    """The event replica's two run shapes (warp per run / thread per run,
+    TICTAC_EVENT_LANES) give identical results outside the closed form, and
+    spread samples match the oracle's simulator."""
+    g = lib.model(model, 1)
+    if model == "vgg16_training":
+        g = g.expand(2, 1, 0)
+    o = g.declared()
+    og = orc.OracleGraph(json.loads(g.serialize()))
+    R = g.recv_count()
+    rng = np.random.default_rng(3)
+    orders = np.argsort(rng.random((3000, R)), axis=1).astype(np.int32)
+    orders[::7, 0] = orders[::7, 1]  # rows that are not permutations: duplicate priorities slots
+    cases = [("sweep", policy(False, 0, 0.0)), ("sweep", policy(True, 0, 0.2)),
+             ("orders", policy(False, 11, 0.0)), ("orders", policy(True, 11, 0.3))]
+    for kind, pol in cases:
+        out = {}
+        for lanes in ("32", "1"):
+            monkeypatch.setenv("TICTAC_EVENT_LANES", lanes)
+            if kind == "sweep":
+                r = g.sweep_random(o, 5, 3000, pol, makespans=True,
+                                   worker_makespans=g.is_cluster())
+                out[lanes] = [r["makespans"]] + ([r["worker_makespans"]] if g.is_cluster() else [])
+            else:
+                out[lanes] = list(g.simulate_orders(o, orders, pol))
+        for a, b in zip(out["32"], out["1"]):
+            assert np.array_equal(a, b), (kind, pol.counter_gate, pol.reorder_noise)
+    # oracle spot checks of the thread-per-run shape (ungated random sweeps)
+    monkeypatch.setenv("TICTAC_EVENT_LANES", "1")
+    ms = g.sweep_random(o, 5, 3000, policy(False, 0, 0.0), makespans=True)["makespans"]
+    for k in (0, 1, 1234, 2999):
+        pr = orc.schedule_for(og, "random", 5 + k)
+        m, _ = og.simulate(pr, False, 5 + k, 0.0)
+        assert ms[k] == m, k
+
+
+def test_irregular_graphs_match_reference(lib, ref):
+    """SURVEY §8f row 1's cases outside the closed form — several compute
+    units and channels per device, sends, zero durations, cluster recvs with
+    predecessors — byte-equal to the reference for every schedule kind and
+    policy, brute force included."""
+    pols = [None, policy(True, 3, 0.0), policy(False, 5, 0.0), policy(True, 9, 0.3), policy(True, 2, 1.0)]
+    for name, text in corpus.irregular_graphs():
+        for mode in ("amended", "literal"):
+            _both(lib, ref, text, lambda L, g: g.tic(mode).serialize() + str(g.tic(mode).total_order()))
+            _both(lib, ref, text, lambda L, g: g.properties_text(g.declared(), mode))
+        _both(lib, ref, text, lambda L, g: g.tac(g.declared()).serialize())
+
+        def run(L, g, algo, pol):
+            o = g.declared()
+            s = {"none": None, "tic": g.tic(), "tac": g.tac(o), "random": g.random(17)}[algo]
+            r = g.simulate(o, s, pol)
+            out = r.json() + r.chrome_trace() + g.metrics_text(o, r) + str(r.violations())
+            if g.is_cluster():
+                out += r.iteration_json()
+            return out
+        for algo in ("none", "tic", "tac", "random"):
+            for pol in pols:
+                _both(lib, ref, text, lambda L, g: run(L, g, algo, pol))
+        if not lib.graph(text).is_cluster():
+            for pol in (None, policy(False, 4, 0.0), policy(True, 1, 0.5)):
+                _both(lib, ref, text, lambda L, g: g.brute_force_text(g.declared(), pol, 8))
+
+
+@pytest.mark.parametrize("gated,noise", [(True, 0.0), (False, 0.0), (True, 0.25)])
+def test_irregular_sweeps_match_reference(lib, ref, gated, noise):
+    """Batched sweeps over the irregular corpus (thread-per-run replica at
+    this batch size) == the reference's per-seed loop."""
+    n = 2500
+    for name, text in corpus.irregular_graphs():
+        g = lib.graph(text)
+        o = g.declared()
+        cl = g.is_cluster()
+        res = g.sweep_random(o, 1, n, policy(gated, 0, noise), makespans=True, worker_makespans=cl)
+        rg = ref.graph(text)
+        ro = rg.declared()
+        for i in range(n):
+            s = 1 + i
+            r = rg.simulate(ro, rg.random(s), policy(gated, s, noise))
+            assert res["makespans"][i] == r.makespan(), (name, s)
+            if cl:
+                it = json.loads(r.iteration_json())
+                assert list(res["worker_makespans"][i]) == list(it["per_worker_makespan_us"].values())
