@@ -154,7 +154,7 @@ def event_replica(lib, path, noise=0.1, count=1 << 18, ref_target_s=5.0):
     g = lib.model(MODEL, 1)
     o = g.declared()
     pol = policy(True, 0, noise)
-    g.sweep_random(o, SEED_LO, 4096, pol)  # warm
+    g.sweep_random(o, SEED_LO, count, pol)  # warm (sizes the simulator scratch)
     t = time.perf_counter()
     res = g.sweep_random(o, SEED_LO, count, pol, makespans=True)
     dt = time.perf_counter() - t

@@ -27,6 +27,7 @@ namespace {
 
 constexpr int kWarpsPerBlock = 4;
 constexpr int64_t kThreadModeMin = 2048;        // batch size from which a thread runs a whole sim
+constexpr int kThreadMinBlocks = 6;            // thread mode: 24 resident warps/SM (<= 85 registers)
 constexpr size_t kThreadScratch = 16ull << 30;  // cap on thread-mode state in HBM
 constexpr int kEmptyLo = 1 << 29;  // "no ready word" (no overflow when lanes are added)
 constexpr uint64_t kNoiseSalt = 0x9e3779b97f4a7c15ULL;  // sim.cpp:14
@@ -229,7 +230,7 @@ __device__ void fill_priorities(const GraphView& G, const RunSpec& rs, const Slo
 }
 
 template <int kL, int S>
-__global__ void __launch_bounds__(32 * kWarpsPerBlock)
+__global__ void __launch_bounds__(32 * kWarpsPerBlock, kL == 1 ? kThreadMinBlocks : 4)
     event_sim_kernel(GraphView G, RunSpec rs, int64_t B, char* hot_global, size_t hot_sz, char* cold_scr,
                      size_t cold_sz, int rbw) {
   // S = element stride of the per-run state: 32 = lane-interleaved groups of
@@ -249,11 +250,6 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock)
     uint64_t choice_seed = 0;
     fill_priorities<kL>(G, rs, s, b, lane, &choice_seed);
     // ---- setup (sim.cpp:74-123)
-    for (int i = lane; i < n; i += kL) {
-      s.missing[i] = G.pred_off[i + 1] - G.pred_off[i];
-      s.gate[i] = -1;
-      s.orig[i] = -1;
-    }
     for (int w = lane; w < rbw; w += kL) {
       s.ready[w] = 0;
       s.rready[w] = 0;
@@ -271,9 +267,14 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock)
     }
     for (int d = lane; d < G.ndev; d += kL) s.dev_end[d] = 0;
     group_sync<kL>();
+    const bool explicit_prio = rs.mode == kPrioExplicit;
     for (int i = lane; i < n; i += kL) {
-      if (s.prio[i] >= 0) s.haspri[G.res[i]] = 1;
-      if (s.missing[i] == 0) {
+      const int deg = G.pred_off[i + 1] - G.pred_off[i];
+      s.missing[i] = deg;
+      s.gate[i] = -1;
+      s.orig[i] = -1;
+      if (explicit_prio && s.prio[i] >= 0) s.haspri[G.res[i]] = 1;
+      if (deg == 0) {
         const int r = G.res[i], l = G.lidx[i];
         if constexpr (kL == 32) {
           atomicOr(&s.ready[G.rb_off[r] + (l >> 5)], 1u << (l & 31));
@@ -288,6 +289,11 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock)
         }
       }
     }
+    if (!explicit_prio)  // only recvs carry priorities
+      for (int k = lane; k < G.R; k += kL) {
+        const int i = G.recv_ops[k];
+        if (s.prio[i] >= 0) s.haspri[G.res[i]] = 1;
+      }
     // dense per-channel ranks from (priority, id), then noise swaps
     MtFullP<Arr<uint64_t, S>> noise{s.mt2, 0};
     const bool noisy = rs.gated && rs.noise > 0.0;
@@ -512,7 +518,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock)
           any = true;
           ++finished;
           s.running[r] = -1;
-          if (s.prio[i] >= 0 && G.chan[r]) {
+          if (G.chan[r] && s.prio[i] >= 0) {
             s.counter[r] += 1;
             s.comp[G.rops_off[r] + s.comp_len[r]] = s.orig[i];
             s.comp_len[r] += 1;
@@ -574,8 +580,24 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock)
       if (!G.chan[r]) continue;
       const int base = G.rops_off[r];
       const int len = s.comp_len[r];
-      for (int a = lane; a < len; a += kL)
-        for (int c = a + 1; c < len; ++c) inv += s.comp[base + a] > s.comp[base + c];
+      if constexpr (kL == 1) {
+        // completion ranks are distinct and < the channel's op count: count
+        // the smaller ranks seen to the right with a bitset (rready's segment
+        // for this channel is free once the loop has ended)
+        const int wb = G.rb_off[r], nw = (G.rops_off[r + 1] - base + 31) >> 5;
+        for (int w = 0; w < nw; ++w) s.rready[wb + w] = 0;
+        for (int a = len - 1; a >= 0; --a) {
+          const int v = s.comp[base + a];
+          int below = 0;
+          for (int w = 0; w < (v >> 5); ++w) below += __popc(s.rready[wb + w]);
+          below += __popc(s.rready[wb + (v >> 5)] & ((1u << (v & 31)) - 1u));
+          inv += below;
+          s.rready[wb + (v >> 5)] |= 1u << (v & 31);
+        }
+      } else {
+        for (int a = lane; a < len; a += kL)
+          for (int c = a + 1; c < len; ++c) inv += s.comp[base + a] > s.comp[base + c];
+      }
     }
     if constexpr (kL == 32) {
 #pragma unroll

@@ -19,7 +19,7 @@ for m in ["resnet_v2_50_inference", "inception_v3_training", "resnet_v2_101_trai
         res = {}
         for lay in ("32", "1"):
             os.environ["TICTAC_EVENT_LAYOUT"] = lay
-            g.sweep_random(o, 1, 4096, pol)
+            g.sweep_random(o, 1, B, pol)
             t = time.perf_counter()
             r = g.sweep_random(o, 1, B, pol, makespans=True)
             dt = time.perf_counter() - t
