@@ -306,11 +306,14 @@ def run_reference(args, rank, world):
     cores = os.cpu_count() or 1
     base = {"metric": "recv-order makespan sims/sec", "unit": "sims/s", "impl": "reference",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
-            "scaling": "strong", "dtype": "int64", "data": "synthetic",
-            "config": {"workload": f"config4 {MODEL} seed 1, random recv orders (bounded CPU sample per step)"}}
+            "scaling": "weak", "dtype": "int64", "data": "synthetic",
+            "config": {"workload": f"config4: {MODEL} DAG seed 1 ({g.op_count()} ops / {g.edge_count()} edges / "
+                                   f"{g.recv_count()} recvs), random recv orders, gated, choice_seed=seed; "
+                                   f"min/argmin (reference library on the host cores: a bounded sample of "
+                                   f"the seed range per step, see cpu_baseline.sample)"}}
     if not oracle.ref_available():
         base["unavailable"] = "oracle/_ref (reference build) missing"
-        print(json.dumps(base))
+        emit(base)
         return
     cal = ref_sweep(path, SEED_LO, cores * 2, cores)
     rate = cal["sims"] / max(cal["seconds"], 1e-9)
@@ -327,10 +330,23 @@ def run_reference(args, rank, world):
                  "cpu_baseline": {"value": v, "unit": "sims/s", "cores": cores, "kind": "reference",
                                   "sample": f"{per_step} seeds per step, {cores} threads"},
                  "e2e": {"value": v, "unit": "sims/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}})
-    print(json.dumps(base))
+    emit(base)
+
+
+_JSON_FD = None
+
+
+def emit(obj):
+    """The one JSON line on stdout. Library/NCCL chatter that would land on
+    fd 1 is routed to stderr for the whole run (see main)."""
+    os.write(_JSON_FD if _JSON_FD is not None else 1, (json.dumps(obj) + "\n").encode())
 
 
 def main():
+    global _JSON_FD
+    sys.stdout.flush()
+    _JSON_FD = os.dup(1)
+    os.dup2(2, 1)  # anything else written to stdout (e.g. NCCL's version banner) goes to stderr
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
@@ -527,7 +543,7 @@ def main():
             out["configs"]["event_replica_config4_noise"] = event_replica(lib, path)
         if not args.no_cpu and world == 1:
             out["cpu_baseline"] = cpu_baseline(path)
-        print(json.dumps(out))
+        emit(out)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()

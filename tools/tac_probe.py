@@ -16,4 +16,5 @@ if which == "tac":
 else:
     s = g.tac(o)
     r = g.simulate(o, s, policy(True, 1, 0.0))
-    print("sim", r.makespan(), time.perf_counter() - t)
+    js = r.json()  # materialises the event list: one exact replica run
+    print("sim", r.makespan(), len(js), time.perf_counter() - t)
