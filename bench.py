@@ -144,6 +144,37 @@ def ref_sweep(path, seed_lo, count, threads, noise=None, out_path="-"):
     return json.loads(r.stdout)
 
 
+def single_report(lib, reps=7):
+    """One cs_simulate + cs_report_json (the event list) for a random order,
+    configs 1 and 4, median of `reps` calls — this library, and the
+    reference library on one host core when oracle/_ref is built."""
+    from paper_1803_03288_b200 import capi
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle
+    libs = {"ours": lib}
+    if oracle.ref_available():
+        libs["reference_cpu"] = capi.Lib(oracle.REF_LIB)
+    out = {}
+    for m in ("resnet_v2_50_inference", MODEL):
+        text = lib.model(m, 1).serialize()
+        row, docs = {}, {}
+        for name, L in libs.items():
+            g = L.graph(text)
+            o = g.declared()
+            s = g.random(1)
+            ts = []
+            for _ in range(reps + 1):
+                t = time.perf_counter()
+                js = g.simulate(o, s, capi.policy(True, 1, 0.0)).json()
+                ts.append(time.perf_counter() - t)
+            row[f"{name}_ms"] = 1000 * sorted(ts[1:])[reps // 2]
+            docs[name] = js
+        if len(docs) == 2:
+            row["identical_json"] = docs["ours"] == docs["reference_cpu"]
+        out[m] = row
+    return out
+
+
 def event_replica(lib, path, noise=0.1, count=1 << 18, ref_target_s=5.0):
     """sweeps outside the closed form run the exact event
     replica (thread per run at this batch size). Config 4 with reorder noise:
@@ -541,6 +572,7 @@ def main():
         if not args.no_configs and world == 1:
             out["configs"] = other_configs(lib)
             out["configs"]["event_replica_config4_noise"] = event_replica(lib, path)
+            out["configs"]["single_report_simulate_json"] = single_report(lib)
         if not args.no_cpu and world == 1:
             out["cpu_baseline"] = cpu_baseline(path)
         emit(out)

@@ -386,6 +386,15 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, kL == 1 ? kThreadMinBlock
     const bool rec = (b == 0) && rs.start;
     if (lane == 0) {
       int finished = 0;
+      // With <= 64 resources, three masks replace the per-step scans over all
+      // resources (same visiting order, ascending r): avail = idle with ready
+      // ops (try_start candidates), busy = running, due = running and ending
+      // at the current t (complete_now). Above 64 the scans run as written.
+      const bool small = nres <= 64;
+      uint64_t avail = 0, busy = 0, due = 0;
+      if (small)
+        for (int r = 0; r < nres; ++r)
+          if (s.ready_cnt[r] > 0) avail |= 1ull << r;
       auto start_op = [&](int r, int op) {
         const int l = G.lidx[op];
         s.ready[G.rb_off[r] + (l >> 5)] &= ~(1u << (l & 31));
@@ -404,6 +413,11 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, kL == 1 ? kThreadMinBlock
         const int d = G.res_dev[r];
         if (e > s.dev_end[d]) s.dev_end[d] = e;
         mk = max(mk, e);
+        if (small) {
+          avail &= ~(1ull << r);
+          busy |= 1ull << r;
+          if (e == t) due |= 1ull << r;
+        }
       };
       // sim.cpp:163-192 for one resource; returns true when an op started
       auto try_start = [&](int r) -> bool {
@@ -453,6 +467,28 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, kL == 1 ? kThreadMinBlock
         }
         const bool pri = s.haspri[r] != 0;
         const int wb = G.rb_off[r], ob = G.rops_off[r];
+        if (!pri) {
+          // no priorities here: every ready op is a candidate, so draw over
+          // ready_cnt and walk once to the k-th ready op (tightening lo)
+          const int total = s.ready_cnt[r];
+          int k = total > 1 ? static_cast<int>(bounded_full(choice, static_cast<uint64_t>(total), rs)) : 0;
+          bool seen = false;
+          for (int w = s.lo[r], wh = s.hi[r]; w <= wh; ++w) {
+            const uint32_t bits = s.ready[wb + w];
+            if (!bits) continue;
+            if (!seen) {
+              s.lo[r] = w;
+              seen = true;
+            }
+            const int c = __popc(bits);
+            if (k < c) {
+              start_op(r, G.rops[ob + (w << 5) + nth_bit(bits, k)]);
+              return true;
+            }
+            k -= c;
+          }
+          return false;  // unreachable: ready_cnt counts the set bits
+        }
         int nlo = kEmptyLo, nhi = -1, best = 0x7fffffff;
         for (int w = s.lo[r]; w <= s.hi[r]; ++w) {
           uint32_t bits = s.ready[wb + w];
@@ -508,25 +544,42 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, kL == 1 ? kThreadMinBlock
         s.ready_cnt[rw] += 1;
         s.lo[rw] = min(s.lo[rw], l >> 5);
         s.hi[rw] = max(s.hi[rw], l >> 5);
+        if (small && s.running[rw] < 0) avail |= 1ull << rw;
       };
       // sim.cpp:144-161
+      auto complete_one = [&](int r, int i) {
+        ++finished;
+        s.running[r] = -1;
+        if (G.chan[r] && s.prio[i] >= 0) {
+          s.counter[r] += 1;
+          s.comp[G.rops_off[r] + s.comp_len[r]] = s.orig[i];
+          s.comp_len[r] += 1;
+        }
+        if (small) {
+          busy &= ~(1ull << r);
+          if (s.ready_cnt[r] > 0) avail |= 1ull << r;
+        }
+        for (int e = G.succ_off[i]; e < G.succ_off[i + 1]; ++e) {
+          const int w = G.succ_idx[e];
+          if (--s.missing[w] == 0) push_ready(w);
+        }
+      };
       auto complete_now = [&]() -> bool {
+        if (small) {  // completions never start anything: `due` is stable here
+          const bool any = due != 0;
+          while (due) {
+            const int r = __ffsll(static_cast<long long>(due)) - 1;
+            due &= due - 1;
+            complete_one(r, s.running[r]);
+          }
+          return any;
+        }
         bool any = false;
         for (int r = 0; r < nres; ++r) {
           const int i = s.running[r];
           if (i < 0 || s.run_end[r] != t) continue;
           any = true;
-          ++finished;
-          s.running[r] = -1;
-          if (G.chan[r] && s.prio[i] >= 0) {
-            s.counter[r] += 1;
-            s.comp[G.rops_off[r] + s.comp_len[r]] = s.orig[i];
-            s.comp_len[r] += 1;
-          }
-          for (int e = G.succ_off[i]; e < G.succ_off[i + 1]; ++e) {
-            const int w = G.succ_idx[e];
-            if (--s.missing[w] == 0) push_ready(w);
-          }
+          complete_one(r, i);
         }
         return any;
       };
@@ -534,13 +587,33 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, kL == 1 ? kThreadMinBlock
         bool progress = true;
         while (progress) {
           progress = false;
-          for (int r = 0; r < nres; ++r) progress = try_start(r) || progress;
+          if (small && (avail | due) == 0) break;  // nothing can start or end at t
+          if (small) {  // a start only clears its own resource's bit
+            for (uint64_t m = avail; m; m &= m - 1)
+              progress = try_start(__ffsll(static_cast<long long>(m)) - 1) || progress;
+          } else {
+            for (int r = 0; r < nres; ++r) progress = try_start(r) || progress;
+          }
           progress = complete_now() || progress;
         }
         if (finished == n) break;
         int64_t next_t = INT64_MAX;
-        for (int r = 0; r < nres; ++r)
-          if (s.running[r] >= 0) next_t = min(next_t, s.run_end[r]);
+        if (small) {  // earliest end over running resources, and which end then
+          due = 0;
+          for (uint64_t m = busy; m; m &= m - 1) {
+            const int r = __ffsll(static_cast<long long>(m)) - 1;
+            const int64_t e = s.run_end[r];
+            if (e < next_t) {
+              next_t = e;
+              due = 1ull << r;
+            } else if (e == next_t) {
+              due |= 1ull << r;
+            }
+          }
+        } else {
+          for (int r = 0; r < nres; ++r)
+            if (s.running[r] >= 0) next_t = min(next_t, s.run_end[r]);
+        }
         if (next_t == INT64_MAX) {  // forced release, sim.cpp:211-229
           int64_t key = INT64_MAX;
           for (int r = 0; r < nres; ++r)
@@ -614,17 +687,39 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, kL == 1 ? kThreadMinBlock
   }
 }
 
+// Per-call buffers: stream-ordered allocations on the legacy stream (the
+// pool keeps its reservation, graph.cu), so a single report costs no
+// cudaMalloc/cudaFree round trips.
 struct DevBuf {
   void* p = nullptr;
   ~DevBuf() {
-    if (p) cudaFree(p);
+    if (p) cudaFreeAsync(p, 0);
   }
 };
 
 template <typename T>
 int dev_copy(DevBuf& buf, const T* src, size_t count, char* err) {
-  CK(cudaMalloc(&buf.p, sizeof(T) * (count ? count : 1)));
+  CK(cudaMallocAsync(&buf.p, sizeof(T) * (count ? count : 1), 0));
   if (count && src) CK(cudaMemcpy(buf.p, src, sizeof(T) * count, cudaMemcpyHostToDevice));
+  return 0;
+}
+
+// bounded() constants for n < 4096, built and uploaded once per device
+int bounded_tables(int dev, const uint64_t** lim, const uint64_t** mag, char* err) {
+  static std::mutex m;
+  static uint64_t* tab[64] = {};
+  std::lock_guard<std::mutex> lock(m);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (!tab[dev]) {
+    std::vector<uint64_t> h(2 * 4096);
+    for (uint64_t k = 0; k < 4096; ++k) bounded_consts(k, &h[k], &h[4096 + k]);
+    void* p = nullptr;
+    CK(cudaMalloc(&p, 8 * h.size()));
+    CK(cudaMemcpy(p, h.data(), 8 * h.size(), cudaMemcpyHostToDevice));
+    tab[dev] = static_cast<uint64_t*>(p);
+  }
+  *lim = tab[dev];
+  *mag = tab[dev] + 4096;
   return 0;
 }
 
@@ -661,16 +756,14 @@ int run_event(DeviceGraph* g, const int64_t* dur, int64_t B, RunSpec rs, int64_t
               char* err) {
   if (ensure_device(err)) return 1;
   if (B <= 0) return 0;
-  DevBuf d_dur, d_ms, d_vio, d_st, d_start, d_end, d_dev, d_lim, d_mag;
+  DevBuf d_dur, d_ms, d_vio, d_st, d_start, d_end, d_dev;
   ScratchPool& pool = scratch_pool();
   std::lock_guard<std::mutex> lock(pool.m);
+  int sms = 148, dev = 0;
+  CK(cudaGetDevice(&dev));
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   if (dev_copy(d_dur, dur, g->n, err)) return 1;
-  std::vector<uint64_t> lim(4096), mag(4096);
-  for (uint64_t k = 0; k < 4096; ++k) bounded_consts(k, &lim[k], &mag[k]);
-  if (dev_copy(d_lim, lim.data(), lim.size(), err) || dev_copy(d_mag, mag.data(), mag.size(), err))
-    return 1;
-  rs.lim = static_cast<uint64_t*>(d_lim.p);
-  rs.mag = static_cast<uint64_t*>(d_mag.p);
+  if (bounded_tables(dev, &rs.lim, &rs.mag, err)) return 1;
   if (dev_copy<int64_t>(d_ms, nullptr, B, err) || dev_copy<int64_t>(d_vio, nullptr, B, err) ||
       dev_copy<int32_t>(d_st, nullptr, B, err))
     return 1;
@@ -692,9 +785,6 @@ int run_event(DeviceGraph* g, const int64_t* dur, int64_t B, RunSpec rs, int64_t
   GraphView G{g->n,        g->nres,     g->ndev,     g->R,        g->pred_off, g->succ_off,
               g->succ_idx, g->res,      g->res_dev,  g->rops_off, g->rops,     g->lidx,
               g->rb_off,   g->recv_ops, g->chan,     static_cast<int64_t*>(d_dur.p)};
-  int sms = 148, dev = 0;
-  CK(cudaGetDevice(&dev));
-  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   // Large batches: a thread per run (32 interleaved runs per warp) keeps
   // 32x more runs in flight than a warp per run; the lockstep lanes walk the
   // resource loops together, so their state accesses coalesce.

@@ -28,6 +28,15 @@ int ensure_device(char* err) {
         ok = 0;
       } else {
         ok = 1;
+        // per-call buffers come from the stream-ordered allocator; keep what
+        // it has reserved instead of returning it to the driver at each sync
+        int dev = 0;
+        cudaMemPool_t pool;
+        if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+          uint64_t keep = UINT64_MAX;
+          cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+        cudaGetLastError();
       }
     }
   }

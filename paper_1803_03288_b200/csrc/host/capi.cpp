@@ -388,7 +388,7 @@ int cs_report_json(const cs_report* r, char** out_json) {
   return guarded([&] {
     need(r, "report");
     need(out_json, "out_json");
-    *out_json = dup(dump_doc(r->report().to_json()));
+    *out_json = dup(r->report().json_text());
   });
 }
 
@@ -396,7 +396,7 @@ int cs_report_chrome_trace(const cs_report* r, char** out_json) {
   return guarded([&] {
     need(r, "report");
     need(out_json, "out_json");
-    *out_json = dup(dump_doc(r->report().chrome_trace()));
+    *out_json = dup(r->report().chrome_trace_text());
   });
 }
 

@@ -156,6 +156,10 @@ struct Report {
   int64_t iteration = 0, strag_num = 0, strag_den = 1;
   Json to_json() const;       // sim.cpp:305-321
   Json chrome_trace() const;  // sim.cpp:323-366
+  // The same documents as dump_doc(to_json()) / dump_doc(chrome_trace()),
+  // written directly (one pass, no per-event JSON nodes).
+  std::string json_text() const;
+  std::string chrome_trace_text() const;
   Json iteration_json() const;  // sim.cpp:368-376
 };
 

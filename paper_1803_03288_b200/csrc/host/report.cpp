@@ -1,10 +1,187 @@
 // Report / metrics JSON formatting (reference sim.cpp:305-376,
 // metrics.cpp:82-105). The numbers come from the device simulator.
 #include <algorithm>
+#include <cstdio>
 
 #include "core.hpp"
 
 namespace tictac {
+
+namespace {
+
+// Streaming writer for nlohmann's dump(2) layout: members/elements on their
+// own lines at 2-space indent, "key": value, empty containers as {} / [],
+// strings escaped as its serializer does with ensure_ascii = false.
+class JsonText {
+ public:
+  std::string s;
+  void open(char c) {
+    s += c;
+    first_.push_back(true);
+  }
+  void close(char c) {
+    const bool empty = first_.back();
+    first_.pop_back();
+    if (!empty) newline();
+    s += c;
+  }
+  void item() {  // before each array element
+    if (!first_.back()) s += ',';
+    first_.back() = false;
+    newline();
+  }
+  void key(const std::string& k) {
+    item();
+    str(k);
+    s += ": ";
+  }
+  void num(int64_t v) { s += std::to_string(v); }
+  void str(const std::string& v) {
+    s += '"';
+    for (const char ch : v) {
+      const unsigned char c = static_cast<unsigned char>(ch);
+      switch (c) {
+        case '"': s += "\\\""; break;
+        case '\\': s += "\\\\"; break;
+        case '\b': s += "\\b"; break;
+        case '\f': s += "\\f"; break;
+        case '\n': s += "\\n"; break;
+        case '\r': s += "\\r"; break;
+        case '\t': s += "\\t"; break;
+        default:
+          if (c <= 0x1f) {
+            char buf[8];
+            std::snprintf(buf, sizeof(buf), "\\u%04x", c);
+            s += buf;
+          } else {
+            s += ch;
+          }
+      }
+    }
+    s += '"';
+  }
+
+ private:
+  std::vector<bool> first_;
+  void newline() {
+    s += '\n';
+    s.append(2 * first_.size(), ' ');
+  }
+};
+
+}  // namespace
+
+std::string Report::json_text() const {
+  std::vector<std::string> keys(resources.size());
+  for (size_t r = 0; r < resources.size(); ++r) keys[r] = resources[r].key();
+  std::map<std::string, int64_t> busy;
+  for (const Event& e : events) busy[keys[e.res]] += e.end - e.start;
+  JsonText w;
+  w.s.reserve(128 * events.size() + 256);
+  w.open('{');
+  w.key("makespan_us");
+  w.num(makespan);
+  w.key("violations");
+  w.num(violations);
+  w.key("busy");
+  w.open('{');
+  for (const auto& [k, us] : busy) {
+    w.key(k);
+    w.num(us);
+  }
+  w.close('}');
+  w.key("events");
+  w.open('[');
+  for (const Event& e : events) {
+    w.item();
+    w.open('{');
+    w.key("op");
+    w.str(op_ids[e.op]);
+    w.key("resource");
+    w.str(keys[e.res]);
+    w.key("start_us");
+    w.num(e.start);
+    w.key("end_us");
+    w.num(e.end);
+    w.close('}');
+  }
+  w.close(']');
+  w.close('}');
+  w.s += '\n';
+  return std::move(w.s);
+}
+
+std::string Report::chrome_trace_text() const {
+  std::vector<std::string> devices;
+  for (const Resource& r : resources) devices.push_back(r.device);
+  std::sort(devices.begin(), devices.end());
+  devices.erase(std::unique(devices.begin(), devices.end()), devices.end());
+  std::vector<int64_t> pid(resources.size());
+  for (size_t r = 0; r < resources.size(); ++r)
+    pid[r] = std::lower_bound(devices.begin(), devices.end(), resources[r].device) - devices.begin();
+  JsonText w;
+  w.s.reserve(160 * events.size() + 256);
+  w.open('{');
+  w.key("traceEvents");
+  w.open('[');
+  for (size_t d = 0; d < devices.size(); ++d) {
+    w.item();
+    w.open('{');
+    w.key("name");
+    w.str("process_name");
+    w.key("ph");
+    w.str("M");
+    w.key("pid");
+    w.num(static_cast<int64_t>(d));
+    w.key("args");
+    w.open('{');
+    w.key("name");
+    w.str(devices[d]);
+    w.close('}');
+    w.close('}');
+  }
+  for (size_t r = 0; r < resources.size(); ++r) {
+    w.item();
+    w.open('{');
+    w.key("name");
+    w.str("thread_name");
+    w.key("ph");
+    w.str("M");
+    w.key("pid");
+    w.num(pid[r]);
+    w.key("tid");
+    w.num(static_cast<int64_t>(r));
+    w.key("args");
+    w.open('{');
+    w.key("name");
+    w.str(std::string(resources[r].channel ? "channel" : "compute") + "/" + resources[r].name);
+    w.close('}');
+    w.close('}');
+  }
+  for (const Event& e : events) {
+    w.item();
+    w.open('{');
+    w.key("name");
+    w.str(op_ids[e.op]);
+    w.key("cat");
+    w.str(resources[e.res].channel ? "channel" : "compute");
+    w.key("ph");
+    w.str("X");
+    w.key("pid");
+    w.num(pid[e.res]);
+    w.key("tid");
+    w.num(e.res);
+    w.key("ts");
+    w.num(e.start);
+    w.key("dur");
+    w.num(e.end - e.start);
+    w.close('}');
+  }
+  w.close(']');
+  w.close('}');
+  w.s += '\n';
+  return std::move(w.s);
+}
 
 Json Report::to_json() const {
   Json j;

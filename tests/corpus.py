@@ -104,4 +104,22 @@ def irregular_cluster(seed: int, workers=2, n_comp=8, n_recv=4):
 def irregular_graphs():
     return ([(f"irregular-w{s}", irregular_worker(s)) for s in (1, 2, 3, 4)] +
             [("irregular-w5-wide", irregular_worker(5, n_comp=30, n_recv=9, n_send=3, cpus=3, chans=3))] +
-            [(f"irregular-c{s}", irregular_cluster(s)) for s in (1, 2)])
+            [(f"irregular-c{s}", irregular_cluster(s)) for s in (1, 2)] +
+            [("irregular-w6-odd-names", odd_names(irregular_worker(6)))])
+
+
+def odd_names(text: str) -> str:
+    """Same graph with op ids / device / resource names that need JSON
+    escaping (quote, backslash, control characters, DEL, non-ASCII)."""
+    import json
+    d = json.loads(text)
+    suffix = ["\"q", "\\b", "\t", "\n", "\x01", "\x7f", "é", "→", "\x1f"]
+    ren = {}
+    for k, op in enumerate(d["ops"]):
+        ren[op["id"]] = op["id"] + suffix[k % len(suffix)]
+        op["id"] = ren[op["id"]]
+        op["resource"]["device"] = op["resource"]["device"] + "µ"
+        op["resource"]["name"] = op["resource"]["name"] + "\"x"
+    d["edges"] = [[ren[a], ren[b]] for a, b in d["edges"]]
+    d["name"] = d["name"] + "☃\\"
+    return json.dumps(d)
