@@ -32,6 +32,21 @@ struct CudaError {
 
 int ensure_device(char* err);  // selects/initialises the current device
 
+// Owned device allocation (freed on every exit path).
+struct DevMem {
+  void* p = nullptr;
+  DevMem() = default;
+  DevMem(const DevMem&) = delete;
+  DevMem& operator=(const DevMem&) = delete;
+  ~DevMem() {
+    if (p) cudaFree(p);
+  }
+  template <typename T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
 // ---------------------------------------------------------------- RNG ----
 constexpr uint64_t kMtMul = 6364136223846793005ULL;
 constexpr uint64_t kMtMatrix = 0xB5026F5AA96619E9ULL;

@@ -600,9 +600,9 @@ extern "C" int csk_sweep_lex(SweepPlan* p, int64_t first, int64_t count, int64_t
   if (count <= 0) return 0;
   std::vector<unsigned long long> fact(21, 1);
   for (int i = 1; i <= 20; ++i) fact[i] = fact[i - 1] * static_cast<unsigned long long>(i);
-  void* d_fact = nullptr;
-  CK(cudaMalloc(&d_fact, sizeof(unsigned long long) * fact.size()));
-  CK(cudaMemcpy(d_fact, fact.data(), sizeof(unsigned long long) * fact.size(), cudaMemcpyHostToDevice));
+  DevMem d_fact;
+  CK(cudaMalloc(&d_fact.p, sizeof(unsigned long long) * fact.size()));
+  CK(cudaMemcpy(d_fact.p, fact.data(), sizeof(unsigned long long) * fact.size(), cudaMemcpyHostToDevice));
   ChainArgs a = chain_args(p);
   const size_t vb = p->narrow ? 4 : 8;
   const size_t smem = 8 * static_cast<size_t>(p->R) + ((vb * p->stride + 7) & ~size_t(7)) + 32 * kSweepThreads;
@@ -610,7 +610,7 @@ extern "C" int csk_sweep_lex(SweepPlan* p, int64_t first, int64_t count, int64_t
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int blocks = static_cast<int>(std::min<int64_t>(sms * 8, (count + kSweepThreads - 1) / kSweepThreads));
-  const auto* f = static_cast<const unsigned long long*>(d_fact);
+  const auto* f = d_fact.as<const unsigned long long>();
   if (p->narrow) {
     CK(cudaFuncSetAttribute(lex_kernel<int32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     lex_kernel<int32_t><<<blocks, kSweepThreads, smem>>>(a, first, count, f, d_out);
@@ -619,10 +619,8 @@ extern "C" int csk_sweep_lex(SweepPlan* p, int64_t first, int64_t count, int64_t
     lex_kernel<int64_t><<<blocks, kSweepThreads, smem>>>(a, first, count, f, d_out);
   }
   LAUNCHED();
-  cudaError_t e = cudaGetLastError();
-  if (e == cudaSuccess) e = cudaDeviceSynchronize();
-  cudaFree(d_fact);
-  CK(e);
+  CK(cudaGetLastError());
+  CK(cudaDeviceSynchronize());
   return 0;
 }
 
@@ -632,8 +630,7 @@ extern "C" int csk_brute_force_closed(SweepPlan* p, int64_t perms, int64_t* best
   // arg-min (first minimum = the reference's first optimum), then sort +
   // unique for the distribution; chunk results merge on the host.
   const int64_t chunk = std::min<int64_t>(perms, int64_t{1} << 28);
-  void *d_ms = nullptr, *d_sorted = nullptr, *d_uniq = nullptr, *d_nu = nullptr, *d_arg = nullptr,
-       *d_tmp = nullptr;
+  DevMem m_ms, m_sorted, m_uniq, m_nu, m_arg, m_tmp;
   size_t tmp_bytes = 0, b1 = 0, b2 = 0, b3 = 0;
   const int nc = static_cast<int>(chunk);
   CK(cub::DeviceReduce::ArgMin(nullptr, b1, static_cast<int64_t*>(nullptr),
@@ -642,12 +639,14 @@ extern "C" int csk_brute_force_closed(SweepPlan* p, int64_t perms, int64_t* best
   CK(cub::DeviceSelect::Unique(nullptr, b3, static_cast<int64_t*>(nullptr), static_cast<int64_t*>(nullptr),
                                static_cast<int*>(nullptr), nc));
   tmp_bytes = std::max(b1, std::max(b2, b3));
-  CK(cudaMalloc(&d_ms, 8 * chunk));
-  CK(cudaMalloc(&d_sorted, 8 * chunk));
-  CK(cudaMalloc(&d_uniq, 8 * chunk));
-  CK(cudaMalloc(&d_nu, 8));
-  CK(cudaMalloc(&d_arg, sizeof(cub::KeyValuePair<int, int64_t>)));
-  CK(cudaMalloc(&d_tmp, std::max<size_t>(tmp_bytes, 16)));
+  CK(cudaMalloc(&m_ms.p, 8 * chunk));
+  CK(cudaMalloc(&m_sorted.p, 8 * chunk));
+  CK(cudaMalloc(&m_uniq.p, 8 * chunk));
+  CK(cudaMalloc(&m_nu.p, 8));
+  CK(cudaMalloc(&m_arg.p, sizeof(cub::KeyValuePair<int, int64_t>)));
+  CK(cudaMalloc(&m_tmp.p, std::max<size_t>(tmp_bytes, 16)));
+  void *d_ms = m_ms.p, *d_sorted = m_sorted.p, *d_uniq = m_uniq.p, *d_nu = m_nu.p, *d_arg = m_arg.p,
+       *d_tmp = m_tmp.p;
   std::vector<int64_t> all;
   bool have = false;
   int rc = 0;
@@ -687,7 +686,6 @@ extern "C" int csk_brute_force_closed(SweepPlan* p, int64_t perms, int64_t* best
     merged.erase(std::unique(merged.begin(), merged.end()), merged.end());
     all.swap(merged);
   }
-  for (void* q : {d_ms, d_sorted, d_uniq, d_nu, d_arg, d_tmp}) cudaFree(q);
   if (rc) return rc;
   *n_distinct = static_cast<int64_t>(all.size());
   if (static_cast<int64_t>(all.size()) <= cap) std::copy(all.begin(), all.end(), distinct);
@@ -699,24 +697,18 @@ extern "C" int csk_random_orders(int32_t R, int32_t S, const uint64_t* seeds, in
   if (R <= 0 || S <= 0) return 0;
   std::vector<uint64_t> lim(4096), mag(4096);
   for (uint64_t k = 0; k < 4096; ++k) bounded_consts(k, &lim[k], &mag[k]);
-  void *d_seeds = nullptr, *d_lim = nullptr, *d_mag = nullptr, *d_perm = nullptr;
-  CK(cudaMalloc(&d_seeds, 8ull * S));
-  CK(cudaMalloc(&d_lim, 8ull * lim.size()));
-  CK(cudaMalloc(&d_mag, 8ull * mag.size()));
-  CK(cudaMalloc(&d_perm, 4ull * R * S));
-  CK(cudaMemcpy(d_seeds, seeds, 8ull * S, cudaMemcpyHostToDevice));
-  CK(cudaMemcpy(d_lim, lim.data(), 8ull * lim.size(), cudaMemcpyHostToDevice));
-  CK(cudaMemcpy(d_mag, mag.data(), 8ull * mag.size(), cudaMemcpyHostToDevice));
+  DevMem d_seeds, d_lim, d_mag, d_perm;
+  CK(cudaMalloc(&d_seeds.p, 8ull * S));
+  CK(cudaMalloc(&d_lim.p, 8ull * lim.size()));
+  CK(cudaMalloc(&d_mag.p, 8ull * mag.size()));
+  CK(cudaMalloc(&d_perm.p, 4ull * R * S));
+  CK(cudaMemcpy(d_seeds.p, seeds, 8ull * S, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(d_lim.p, lim.data(), 8ull * lim.size(), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(d_mag.p, mag.data(), 8ull * mag.size(), cudaMemcpyHostToDevice));
   random_orders_kernel<<<std::max(1, std::min((S + 127) / 128, 1184)), 128>>>(
-      R, S, static_cast<uint64_t*>(d_seeds), static_cast<uint64_t*>(d_lim),
-      static_cast<uint64_t*>(d_mag), static_cast<int32_t*>(d_perm));
+      R, S, d_seeds.as<uint64_t>(), d_lim.as<uint64_t>(), d_mag.as<uint64_t>(), d_perm.as<int32_t>());
   LAUNCHED();
-  cudaError_t e = cudaGetLastError();
-  if (e == cudaSuccess) e = cudaMemcpy(perms, d_perm, 4ull * R * S, cudaMemcpyDeviceToHost);
-  cudaFree(d_seeds);
-  cudaFree(d_lim);
-  cudaFree(d_mag);
-  cudaFree(d_perm);
-  CK(e);
+  CK(cudaGetLastError());
+  CK(cudaMemcpy(perms, d_perm.p, 4ull * R * S, cudaMemcpyDeviceToHost));
   return 0;
 }
