@@ -206,9 +206,11 @@ def event_replica(lib, path, noise=0.1, count=1 << 18, ref_target_s=5.0):
     return out
 
 
-def cpu_baseline(path, target_s=10.0):
+def cpu_baseline(path, target_s=10.0, g=None, o=None):
     """Reference library on this host: calibrate, then ~target_s of wall time
-    with one thread per core over contiguous seed slices."""
+    with one thread per core over contiguous seed slices. When the product
+    graph/oracle are given, the sample's makespans are compared value by
+    value with this library's for the same seeds."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle
     if not oracle.ref_available():
@@ -217,10 +219,14 @@ def cpu_baseline(path, target_s=10.0):
     cal = ref_sweep(path, SEED_LO, cores * 2, cores)
     rate = cal["sims"] / max(cal["seconds"], 1e-9)
     n = max(cores, int(rate * target_s))
-    r = ref_sweep(path, SEED_LO, n, cores)
+    binp = os.path.join(os.path.dirname(path), "ref_sample.bin")
+    r = ref_sweep(path, SEED_LO, n, cores, None, binp)
     out = {"value": r["sims"] / r["seconds"], "unit": "sims/s", "cores": cores, "kind": "reference",
            "sample": f"seeds {SEED_LO}..{SEED_LO + n - 1} of the same workload ({n} sims, "
                      f"{r['seconds']:.1f} s wall, {cores} threads, oracle/_ref libcommsched -O3)"}
+    if g is not None:
+        ours = g.sweep_random(o, SEED_LO, n, None, makespans=True)["makespans"]
+        out["sample_identical_to_ours"] = bool(np.array_equal(ours, np.fromfile(binp, dtype=np.int64)))
     # reference TIC/TAC wall time on config 1 (single thread: the reference has none)
     try:
         from paper_1803_03288_b200 import capi
@@ -574,7 +580,7 @@ def main():
             out["configs"]["event_replica_config4_noise"] = event_replica(lib, path)
             out["configs"]["single_report_simulate_json"] = single_report(lib)
         if not args.no_cpu and world == 1:
-            out["cpu_baseline"] = cpu_baseline(path)
+            out["cpu_baseline"] = cpu_baseline(path, g=g, o=o)
         emit(out)
     if world > 1:
         dist.barrier()

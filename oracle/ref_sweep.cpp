@@ -7,6 +7,8 @@
 //
 // usage:
 //   ref_sweep sweep <graph.json> <oracle> <seed_lo> <count> <threads> [out.bin] [noise]
+//   ref_sweep sweeplist <graph.json> <oracle> <seeds.bin> <threads> [out.bin] [noise]
+//     (seeds.bin: uint64 seeds, any order; results in that order)
 //   ref_sweep tac   <graph.json> <oracle>      -> schedule JSON on stdout, seconds on stderr
 //   ref_sweep tic   <graph.json> <mode>        -> schedule JSON on stdout, seconds on stderr
 // <oracle> is "declared" or "bw:<bytes_per_us>".
@@ -108,17 +110,28 @@ int main(int argc, char** argv) {
     return 0;
   }
 
-  if (mode != "sweep" || argc < 7) {
+  const bool list = mode == "sweeplist";
+  if ((mode != "sweep" || argc < 7) && (!list || argc < 6)) {
     std::fprintf(stderr, "bad arguments\n");
     return 4;
   }
   cs_oracle* o = make_oracle(g, argv[3]);
-  const uint64_t lo = std::strtoull(argv[4], nullptr, 10);
-  const int64_t count = std::atoll(argv[5]);
-  int threads = std::atoi(argv[6]);
+  std::vector<uint64_t> seeds;
+  if (list) {
+    std::ifstream in(argv[4], std::ios::binary);
+    uint64_t v = 0;
+    while (in.read(reinterpret_cast<char*>(&v), sizeof v)) seeds.push_back(v);
+  } else {
+    const uint64_t lo0 = std::strtoull(argv[4], nullptr, 10);
+    const int64_t n0 = std::atoll(argv[5]);
+    for (int64_t i = 0; i < n0; ++i) seeds.push_back(lo0 + static_cast<uint64_t>(i));
+  }
+  const int ai = list ? 5 : 6;  // index of <threads>
+  const int64_t count = static_cast<int64_t>(seeds.size());
+  int threads = std::atoi(argv[ai]);
   if (threads <= 0) threads = static_cast<int>(std::thread::hardware_concurrency());
-  const char* out_path = argc > 7 && std::strcmp(argv[7], "-") != 0 ? argv[7] : nullptr;
-  const double noise = argc > 8 ? std::atof(argv[8]) : 0.0;
+  const char* out_path = argc > ai + 1 && std::strcmp(argv[ai + 1], "-") != 0 ? argv[ai + 1] : nullptr;
+  const double noise = argc > ai + 2 ? std::atof(argv[ai + 2]) : 0.0;
   int cluster = 0;
   check(cs_graph_is_cluster(g, &cluster), "cs_graph_is_cluster");
 
@@ -132,7 +145,7 @@ int main(int argc, char** argv) {
     if (a >= b) break;
     pool.emplace_back([&, a, b] {
       for (int64_t i = a; i < b; ++i) {
-        const uint64_t seed = lo + static_cast<uint64_t>(i);
+        const uint64_t seed = seeds[static_cast<size_t>(i)];
         cs_schedule* s = nullptr;
         check(cs_schedule_random(g, seed, &s), "cs_schedule_random");
         cs_sim_policy policy{1, seed, noise};
@@ -157,7 +170,7 @@ int main(int argc, char** argv) {
   for (int64_t i = 0; i < count; ++i) {
     if (i == 0 || ms[static_cast<size_t>(i)] < best) {
       best = ms[static_cast<size_t>(i)];
-      arg = static_cast<int64_t>(lo) + i;
+      arg = static_cast<int64_t>(seeds[static_cast<size_t>(i)]);
     }
     sum += ms[static_cast<size_t>(i)];
   }

@@ -113,3 +113,27 @@ def test_config3_cluster_sweep_properties(lib, orc):
         m, vi, st, en = og.simulate(pr, True, s, 0.0, events=True)
         pw, _ = og.iteration_stats(en)
         assert list(wm[s - 1]) == list(pw.values()), s
+
+
+def test_config4_sweep_matches_reference_itself(lib, ref, tmp_path):
+    """config 4 sweep makespans against the reference library
+    itself for seeds 1..10^4 plus 10^4 seeds spread evenly over 1..2^24
+    (the reference's per-seed loop, oracle/_ref/ref_sweep, all host cores)."""
+    import subprocess
+    import oracle
+    g = lib.model("resnet_v2_101_training", 1)
+    o = g.declared()
+    n = 1 << 24
+    ms = g.sweep_random(o, 1, n, None, makespans=True)["makespans"]
+    path = tmp_path / "config4.json"
+    path.write_text(g.serialize())
+    spread = np.unique(np.linspace(1, n, 10_000, dtype=np.uint64))
+    seeds = np.concatenate([np.arange(1, 10_001, dtype=np.uint64), spread])
+    sp, op = tmp_path / "seeds.bin", tmp_path / "ms.bin"
+    seeds.tofile(sp)
+    r = subprocess.run([oracle.REF_SWEEP, "sweeplist", str(path), "declared", str(sp), "0", str(op)],
+                       capture_output=True, text=True, check=True)
+    want = np.fromfile(op, dtype=np.int64)
+    assert json.loads(r.stdout)["sims"] == len(seeds) == len(want)
+    got = ms[(seeds - 1).astype(np.int64)]
+    assert np.array_equal(got, want), int(np.flatnonzero(got != want)[0])
