@@ -242,10 +242,11 @@ def cpu_baseline(path, target_s=10.0, g=None, o=None):
     return out
 
 
-def tac_times(lib, top=False):
+def tac_times(lib, top=False, hbm=None):
     """TAC wall time through cs_schedule_tac (device), seconds; SURVEY §8d
-    configs 1, 2, 4 and the config-5 layered sweep."""
-    out = {}
+    configs 1, 2, 4 and the config-5 layered sweep. With `hbm`, also the
+    SURVEY's algorithmic bytes B_TAC (cs_tac_traffic) over that time."""
+    out, roof = {}, {}
     names = ["resnet_v2_50_inference", "inception_v3_training", "resnet_v2_101_training",
              "layered:10000:1000", "layered:100000:10000"] + (["layered:1000000:100000"] if top else [])
     for name in names:
@@ -255,8 +256,14 @@ def tac_times(lib, top=False):
             g.tac(o)  # warm (upload + context)
         t = time.perf_counter()
         g.tac(o)
-        out[name] = round(time.perf_counter() - t, 6)
-    return out
+        dt = time.perf_counter() - t
+        out[name] = round(dt, 6)
+        if hbm:
+            tr = g.tac_traffic(o)
+            gbs = tr["B_TAC"] / dt / 1e9
+            roof[name] = {"B_TAC_bytes": tr["B_TAC"], "achieved_GBps": gbs, "frac_hbm": gbs / hbm,
+                          "nnz": tr["nnz"], "row_nnz": tr["row_nnz"], "rows": tr["rows"]}
+    return (out, roof) if hbm else out
 
 
 def sweep_rate(g, o, count):
@@ -574,7 +581,7 @@ def main():
             "roofline_issue": issue,
         }
         if not args.no_tac:
-            out["tac_seconds"] = tac_times(lib, top=args.config5_top)
+            out["tac_seconds"], out["tac_roofline"] = tac_times(lib, top=args.config5_top, hbm=hbm)
         if not args.no_configs and world == 1:
             out["configs"] = other_configs(lib)
             out["configs"]["event_replica_config4_noise"] = event_replica(lib, path)

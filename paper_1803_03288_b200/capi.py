@@ -92,13 +92,14 @@ _SIGS = {
     "cs_sweep_plan_run": [_vp, C.c_uint64, C.c_int64, C.c_uint64, _vp, _vp, _vp, _vp],
     "cs_sweep_stats_finish": [_vp, _vp, _vp, C.c_uint64, C.POINTER(SweepStats)],
     "cs_graph_generate_model": [_cp, C.c_uint64, _pp],
+    "cs_tac_traffic": [_vp, _vp, _i64p, C.c_int],
 }
 _FREE = ["cs_graph_free", "cs_oracle_free", "cs_schedule_free", "cs_report_free",
          "cs_string_free", "cs_sweep_plan_free"]
 REFERENCE_SYMBOLS = [k for k in _SIGS if k not in (
     "cs_sweep_random", "cs_simulate_orders", "cs_sweep_plan_create", "cs_sweep_plan_info",
     "cs_sweep_plan_reset", "cs_sweep_plan_run", "cs_sweep_stats_finish",
-    "cs_graph_generate_model")] + [f for f in _FREE if f != "cs_sweep_plan_free"] + [
+    "cs_graph_generate_model", "cs_tac_traffic")] + [f for f in _FREE if f != "cs_sweep_plan_free"] + [
     "cs_last_error", "cs_version"]
 
 
@@ -280,6 +281,17 @@ class Graph(_Handle):
         u, l = C.c_int64(), C.c_int64()
         self.lib.call("cs_makespan_bounds", self.h, oracle.h, C.byref(u), C.byref(l))
         return u.value, l.value
+
+    def tac_traffic(self, oracle: "Oracle") -> dict:
+        """SURVEY §8d TAC traffic terms from the device closure, plus B_TAC
+        (algorithmic bytes of one whole TAC ordering)."""
+        out = (C.c_int64 * 7)()
+        self.lib.call("cs_tac_traffic", self.h, oracle.h, out, 7)
+        V, R, E, E_recv, nnz, rows, row_nnz = (int(x) for x in out)
+        words = (R + 31) // 32
+        b_tac = 4 * V * words + 20 * V * R + 6 * E_recv * (R + 1) + 12 * R * (R + 1) + 32 * nnz
+        return {"V": V, "R": R, "E": E, "E_recv": E_recv, "nnz": nnz, "rows": rows,
+                "row_nnz": row_nnz, "B_TAC": b_tac}
 
     def metrics_text(self, oracle: "Oracle", report: "Report") -> str:
         p = C.c_void_p()

@@ -62,6 +62,7 @@ int csk_tic(DeviceGraph* g, int mode, int32_t* prio, int* total, char* err);
 
 /* tac (schedule.cpp:44-71): rank per recv column. */
 int csk_tac(DeviceGraph* g, const int64_t* dur, int32_t* prio, char* err);
+int csk_tac_stats(DeviceGraph* g, const int64_t* dur, int64_t* out, char* err);
 
 /* random_schedule (schedule.cpp:73-84) for several seeds at once:
  * perms[s*R + k] = recv column at rank k for seeds[s]. */

@@ -630,3 +630,27 @@ extern "C" int csk_tac(DeviceGraph* g, const int64_t* dur, int32_t* prio, char* 
   CK(cudaMemcpy(prio, d_prio.p, 4ull * R, cudaMemcpyDeviceToHost));
   return 0;
 }
+
+// SURVEY §8d TAC traffic inputs from the device closure: out[0] V, [1] R,
+// [2] E, [3] E_recv (edges leaving recvs), [4] nnz = Σ_r |{ops depending on
+// r}| (recvs count themselves, properties.cpp:19-66), [5] closure rows,
+// [6] row-level (row, recv) pairs the kernels actually retire over.
+extern "C" int csk_tac_stats(DeviceGraph* g, const int64_t* dur, int64_t* out, char* err) {
+  for (int k = 0; k < 7; ++k) out[k] = 0;
+  out[0] = g->n;
+  out[1] = g->R;
+  out[2] = g->h_succ_off.empty() ? 0 : g->h_succ_off.back();
+  for (int32_t v = 0; v < g->n; ++v)
+    if (g->h_kind[v] == 1) out[3] += g->h_succ_off[v + 1] - g->h_succ_off[v];
+  if (g->R == 0) return 0;
+  GroupState S;
+  if (group_setup(g, dur, S, err)) return 1;
+  std::vector<int32_t> cnt(std::max(S.rw.nrows, 1));
+  if (S.rw.nrows > 0) CK(cudaMemcpy(cnt.data(), S.d_cnt.p, 4ull * S.rw.nrows, cudaMemcpyDeviceToHost));
+  int64_t nnz = 0;
+  for (int32_t v = 0; v < g->n; ++v) nnz += g->h_kind[v] == 1 ? 1 : cnt[S.rw.row_of[v]];
+  out[4] = nnz;
+  out[5] = S.rw.nrows;
+  out[6] = S.nnz;
+  return 0;
+}

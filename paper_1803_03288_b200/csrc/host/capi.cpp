@@ -717,6 +717,19 @@ int cs_graph_generate_model(const char* model, uint64_t seed, cs_graph** out) {
   });
 }
 
+int cs_tac_traffic(const cs_graph* g, const cs_oracle* o, int64_t* out, int n_out) {
+  return guarded([&] {
+    need(g, "graph");
+    need(o, "oracle");
+    need(out, "out");
+    if (n_out < 7) fail(kParameter, "n_out must be at least 7");
+    const Graph& G = *g->g;
+    const std::vector<int64_t> d = o->o.durations(G);
+    char err[256] = {0};
+    if (csk_tac_stats(G.device(), d.data(), out, err)) fail(kInternal, err);
+  });
+}
+
 int64_t cs_device_launches(void) { return csk_launches(); }
 
 }  // extern "C"

@@ -10,6 +10,8 @@ from fractions import Fraction
 import numpy as np
 import pytest
 
+import corpus
+
 pytestmark = pytest.mark.gpu
 TAC_LARGE = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "tac_large.json")))
 
@@ -137,3 +139,29 @@ def test_config4_sweep_matches_reference_itself(lib, ref, tmp_path):
     assert json.loads(r.stdout)["sims"] == len(seeds) == len(want)
     got = ms[(seeds - 1).astype(np.int64)]
     assert np.array_equal(got, want), int(np.flatnonzero(got != want)[0])
+
+
+def test_tac_traffic_terms(lib):
+    """cs_tac_traffic (SURVEY §8d B_TAC inputs from the device closure)
+    against a direct set-based restatement of find_dependencies."""
+    graphs = [lib.graph(t) for _, t in corpus.worker_graphs(lib)[:6]]
+    graphs += [lib.model(m, 1) for m in ("resnet_v2_50_inference", "inception_v3_training", "layered:2000:200")]
+    for g in graphs:
+        d = json.loads(g.serialize())
+        ids = sorted(op["id"] for op in d["ops"])
+        kind = {op["id"]: op["kind"] for op in d["ops"]}
+        preds = {i: [] for i in ids}
+        for a, b in d["edges"]:
+            preds[b].append(a)
+        dep = {}
+        for i in g.topo_order():
+            s = {i} if kind[i] == "recv" else set()
+            for p in preds[i]:
+                s |= dep[p]
+            dep[i] = s
+        t = g.tac_traffic(g.declared())
+        assert t["V"] == len(ids) and t["R"] == sum(k == "recv" for k in kind.values())
+        assert t["E"] == len(d["edges"])
+        assert t["E_recv"] == sum(kind[a] == "recv" for a, _ in d["edges"])
+        assert t["nnz"] == sum(len(s) for s in dep.values())
+        assert t["rows"] <= t["V"] and t["row_nnz"] <= t["nnz"]
