@@ -24,6 +24,7 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdlib>
 #include <cub/cub.cuh>
 #include <mutex>
@@ -267,20 +268,38 @@ struct TacArgs {
   int32_t* prio;
 };
 
-__device__ __forceinline__ int block_min_int(int v, int* red) {
-#pragma unroll
-  for (int o = 16; o; o >>= 1) v = min(v, __shfl_xor_sync(~0u, v, o));
+// Block-wide min with one barrier: warp min, one shared atomicMin per warp
+// into slot sp % 3 of a ring; the slot for the next call is reset now (its
+// last readers finished before the previous call's barrier). `red` holds
+// the 3 slots (all 0x7fffffff at kernel start); `sp` is block-uniform.
+__device__ __forceinline__ int block_min_int(int v, int* red, int& sp) {
+  v = __reduce_min_sync(~0u, v);
+  if ((threadIdx.x & 31) == 0 && v != 0x7fffffff) atomicMin(&red[sp % 3], v);
+  if (threadIdx.x == 0) red[(sp + 1) % 3] = 0x7fffffff;
   __syncthreads();
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
-  __syncthreads();
-  int r = 0x7fffffff;
-  for (int w = 0; w < (blockDim.x + 31) / 32; ++w) r = min(r, red[w]);
+  const int r = *reinterpret_cast<volatile int*>(&red[sp % 3]);
+  ++sp;
   return r;
+}
+
+__device__ __forceinline__ void init_red(int* red) {
+  if (threadIdx.x < 3) red[threadIdx.x] = 0x7fffffff;
+  __syncthreads();
+}
+
+// A one-block cooperative grid only needs a block barrier.
+__device__ __forceinline__ void grid_bar(cg::grid_group& grid) {
+  if (gridDim.x == 1)
+    __syncthreads();
+  else
+    grid.sync();
 }
 
 __global__ void __launch_bounds__(1024) tac_kernel(TacArgs a) {
   cg::grid_group grid = cg::this_grid();
-  __shared__ int red[32];
+  __shared__ int red[3];
+  int sp = 0;
+  init_red(red);
   const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t nthreads = static_cast<int64_t>(gridDim.x) * blockDim.x;
   const int R = a.R;
@@ -293,13 +312,13 @@ __global__ void __launch_bounds__(1024) tac_kernel(TacArgs a) {
       for (int32_t e = a.succ_off[c]; e < a.succ_off[c + 1]; ++e) m = min(m, a.M[a.succ[e]]);
       a.mp[c] = m;
     }
-    grid.sync();
+    grid_bar(grid);
     // Phase B (every block, redundantly): the reference's left fold over
     // outstanding recvs in id order == find-first-beater chain.
     int best = 0x7fffffff;
     for (int c = threadIdx.x; c < R; c += blockDim.x)
       if (a.out[c]) best = min(best, c);
-    best = block_min_int(best, red);
+    best = block_min_int(best, red, sp);
     for (;;) {
       const int64_t bp = a.P[best], bm = a.tcol[best], bmp = a.mp[best];
       int nxt = 0x7fffffff;
@@ -308,12 +327,75 @@ __global__ void __launch_bounds__(1024) tac_kernel(TacArgs a) {
           nxt = c;
           break;
         }
-      nxt = block_min_int(nxt, red);
+      nxt = block_min_int(nxt, red, sp);
       if (nxt == 0x7fffffff) break;
       best = nxt;
     }
-    grid.sync();  // every block has read P/out before anyone retires
+    grid_bar(grid);  // every block has read P/out before anyone retires
     // Phase C: retire `best`.
+    const int64_t t = a.tcol[best];
+    for (int64_t e = a.col_off[best] + tid; e < a.col_off[best + 1]; e += nthreads) {
+      const int32_t g = a.col[e];
+      const int k = --a.cnt[g];
+      a.M[g] -= t;
+      const int x = (a.xr[g] ^= best);
+      if (k == 1) atomicAdd(reinterpret_cast<unsigned long long*>(&a.P[x]), a.wsum[g]);
+    }
+    if (tid == 0) {
+      a.prio[best] = round;
+      a.out[best] = 0;
+    }
+    grid_bar(grid);
+  }
+}
+
+// Multi-block TAC: the selection fold is distributed too. Every find-first
+// step is a grid-wide min (per-block reduction + atomicMin into a 3-slot
+// ring; the slot for step p+1 is reset during step p, two barriers after its
+// last reader). Rounds cost (chain length + 3) grid barriers but the O(R_t)
+// candidate scan is spread over every SM instead of repeated per block.
+__device__ __forceinline__ int grid_min_step(int v, int* ring, int& p, int* red, int& sp,
+                                             cg::grid_group& grid) {
+  v = block_min_int(v, red, sp);
+  if (threadIdx.x == 0 && v != 0x7fffffff) atomicMin(&ring[p % 3], v);
+  if (blockIdx.x == 0 && threadIdx.x == 0) ring[(p + 1) % 3] = 0x7fffffff;
+  grid.sync();
+  const int r = *reinterpret_cast<volatile int*>(&ring[p % 3]);
+  ++p;
+  return r;
+}
+
+__global__ void __launch_bounds__(1024) tac_dist_kernel(TacArgs a, int* ring) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ int red[3];
+  int sp = 0;
+  init_red(red);
+  const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t nthreads = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int R = a.R;
+  int p = 0;  // ring slot of the next grid-wide min (ring[0] preset by the host)
+  for (int round = 0; round < R; ++round) {
+    int first = 0x7fffffff;
+    for (int64_t c = tid; c < R; c += nthreads) {
+      if (!a.out[c]) continue;
+      int64_t m = kInf;
+      for (int32_t e = a.succ_off[c]; e < a.succ_off[c + 1]; ++e) m = min(m, a.M[a.succ[e]]);
+      a.mp[c] = m;
+      first = min(first, static_cast<int>(c));
+    }
+    int best = grid_min_step(first, ring, p, red, sp, grid);  // also publishes mp[]
+    for (;;) {
+      const int64_t bp = a.P[best], bm = a.tcol[best], bmp = a.mp[best];
+      int nxt = 0x7fffffff;
+      for (int64_t c = best + 1 + tid; c < R; c += nthreads)
+        if (a.out[c] && precedes(static_cast<int>(c), a.P[c], a.tcol[c], a.mp[c], best, bp, bm, bmp)) {
+          nxt = static_cast<int>(c);
+          break;
+        }
+      nxt = grid_min_step(nxt, ring, p, red, sp, grid);
+      if (nxt == 0x7fffffff) break;
+      best = nxt;
+    }
     const int64_t t = a.tcol[best];
     for (int64_t e = a.col_off[best] + tid; e < a.col_off[best + 1]; e += nthreads) {
       const int32_t g = a.col[e];
@@ -330,47 +412,59 @@ __global__ void __launch_bounds__(1024) tac_kernel(TacArgs a) {
   }
 }
 
-// Multi-block TAC: the selection fold is distributed too. Every find-first
-// step is a grid-wide min (per-block reduction + atomicMin into a 3-slot
-// ring; the slot for step p+1 is reset during step p, two barriers after its
-// last reader). Rounds cost (chain length + 3) grid barriers but the O(R_t)
-// candidate scan is spread over every SM instead of repeated per block.
-__device__ __forceinline__ int grid_min_step(int v, int* ring, int& p, int* red, cg::grid_group& grid) {
-  v = block_min_int(v, red);
-  if (threadIdx.x == 0 && v != 0x7fffffff) atomicMin(&ring[p % 3], v);
-  if (blockIdx.x == 0 && threadIdx.x == 0) ring[(p + 1) % 3] = 0x7fffffff;
-  grid.sync();
-  const int r = *reinterpret_cast<volatile int*>(&ring[p % 3]);
-  ++p;
-  return r;
-}
-
-__global__ void __launch_bounds__(1024) tac_dist_kernel(TacArgs a, int* ring) {
+// Multi-block TAC with the candidates resident in registers: thread t owns
+// recv columns t, t + T, ... (at most kOwn), caching T(c), its successor
+// range and its outstanding flag across rounds. Amended M+ is evaluated
+// inline (min M over direct-successor groups) when a candidate is compared,
+// so a round is the find-first chain (one grid-wide min per step, the first
+// step starting from the lowest outstanding column, which every thread
+// tracks identically) plus the retire: chain length + 1 grid barriers.
+template <int kOwn>
+__global__ void __launch_bounds__(1024) tac_own_kernel(TacArgs a, int* ring) {
   cg::grid_group grid = cg::this_grid();
-  __shared__ int red[32];
-  const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int64_t nthreads = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  __shared__ int red[3];
+  int sp = 0;
+  init_red(red);
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+  const int nthreads = gridDim.x * blockDim.x;
   const int R = a.R;
-  int p = 0;  // ring slot of the next grid-wide min (ring[0] preset by the host)
+  int64_t t_own[kOwn];
+  int s0[kOwn], s1[kOwn];
+  bool live[kOwn];
+#pragma unroll
+  for (int k = 0; k < kOwn; ++k) {
+    const int c = tid + k * nthreads;
+    live[k] = c < R;
+    t_own[k] = live[k] ? a.tcol[c] : 0;
+    s0[k] = live[k] ? a.succ_off[c] : 0;
+    s1[k] = live[k] ? a.succ_off[c + 1] : 0;
+  }
+  auto mplus = [&](int e0, int e1) {
+    int64_t m = kInf;
+    for (int e = e0; e < e1; ++e) m = min(m, a.M[a.succ[e]]);
+    return m;
+  };
+  int p = 0;
+  int first = 0;  // lowest outstanding column (identical in every thread)
   for (int round = 0; round < R; ++round) {
-    int first = 0x7fffffff;
-    for (int64_t c = tid; c < R; c += nthreads) {
-      if (!a.out[c]) continue;
-      int64_t m = kInf;
-      for (int32_t e = a.succ_off[c]; e < a.succ_off[c + 1]; ++e) m = min(m, a.M[a.succ[e]]);
-      a.mp[c] = m;
-      first = min(first, static_cast<int>(c));
+    // this round's P and amended M+ of the owned outstanding candidates
+    int64_t P_own[kOwn], mp_own[kOwn];
+#pragma unroll
+    for (int k = 0; k < kOwn; ++k) {
+      P_own[k] = live[k] ? a.P[tid + k * nthreads] : 0;
+      mp_own[k] = live[k] ? mplus(s0[k], s1[k]) : kInf;
     }
-    int best = grid_min_step(first, ring, p, red, grid);  // also publishes mp[]
+    int best = first;
     for (;;) {
-      const int64_t bp = a.P[best], bm = a.tcol[best], bmp = a.mp[best];
+      const int64_t bp = a.P[best], bm = a.tcol[best], bmp = mplus(a.succ_off[best], a.succ_off[best + 1]);
       int nxt = 0x7fffffff;
-      for (int64_t c = best + 1 + tid; c < R; c += nthreads)
-        if (a.out[c] && precedes(static_cast<int>(c), a.P[c], a.tcol[c], a.mp[c], best, bp, bm, bmp)) {
-          nxt = static_cast<int>(c);
-          break;
-        }
-      nxt = grid_min_step(nxt, ring, p, red, grid);
+#pragma unroll
+      for (int k = 0; k < kOwn; ++k) {
+        const int c = tid + k * nthreads;
+        if (live[k] && c > best && c < nxt && precedes(c, P_own[k], t_own[k], mp_own[k], best, bp, bm, bmp))
+          nxt = c;
+      }
+      nxt = grid_min_step(nxt, ring, p, red, sp, grid);
       if (nxt == 0x7fffffff) break;
       best = nxt;
     }
@@ -382,11 +476,17 @@ __global__ void __launch_bounds__(1024) tac_dist_kernel(TacArgs a, int* ring) {
       const int x = (a.xr[g] ^= best);
       if (k == 1) atomicAdd(reinterpret_cast<unsigned long long*>(&a.P[x]), a.wsum[g]);
     }
+#pragma unroll
+    for (int k = 0; k < kOwn; ++k)
+      if (tid + k * nthreads == best) live[k] = false;
     if (tid == 0) {
       a.prio[best] = round;
       a.out[best] = 0;
     }
     grid.sync();
+    if (best == first)
+      do ++first;
+      while (first < R && !*reinterpret_cast<volatile uint8_t*>(&a.out[first]));
   }
 }
 
@@ -567,8 +667,14 @@ extern "C" int csk_tic(DeviceGraph* g, int mode, int32_t* prio, int* total, char
 extern "C" int csk_tac(DeviceGraph* g, const int64_t* dur, int32_t* prio, char* err) {
   const int R = g->R;
   if (R == 0) return 0;
+  const bool trace = std::getenv("TICTAC_TAC_TRACE") != nullptr;
+  auto now = [] { return std::chrono::steady_clock::now(); };
+  auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+  const auto t0 = now();
   GroupState S;
   if (group_setup(g, dur, S, err)) return 1;
+  if (trace) cudaDeviceSynchronize();
+  const auto t1 = now();
   DevArr d_P, d_Mp, d_out, d_prio, d_succoff, d_succ;
   if (alloc<int64_t>(d_P, R, err) || alloc<int64_t>(d_Mp, R, err) || alloc<uint8_t>(d_out, R, err) ||
       alloc<int32_t>(d_prio, R, err) || put(d_succoff, S.rw.succ_off, err) || put(d_succ, S.rw.succ, err))
@@ -610,6 +716,7 @@ extern "C" int csk_tac(DeviceGraph* g, const int64_t* dur, int32_t* prio, char* 
     if (forced > 0) blocks = std::min(forced, sms * std::max(per_sm, 1));
   }
   blocks = std::max(blocks, 1);
+  const auto t2 = now();
   if (blocks == 1) {
     void* args[] = {&a};
     CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(tac_kernel), 1, 1024, args, 0, nullptr));
@@ -619,15 +726,32 @@ extern "C" int csk_tac(DeviceGraph* g, const int64_t* dur, int32_t* prio, char* 
     if (put(d_ring, ring, err)) return 1;
     int* rp = d_ring.as<int>();
     void* args[] = {&a, &rp};
-    CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(tac_dist_kernel), blocks, 1024, args, 0, nullptr));
+    // register-resident candidates when every column has an owner slot
+    const int64_t per = (R + static_cast<int64_t>(blocks) * 1024 - 1) / (static_cast<int64_t>(blocks) * 1024);
+    void* kern = reinterpret_cast<void*>(tac_dist_kernel);
+    if (!std::getenv("TICTAC_TAC_NO_OWN")) {
+      if (per <= 1)
+        kern = reinterpret_cast<void*>(tac_own_kernel<1>);
+      else if (per <= 2)
+        kern = reinterpret_cast<void*>(tac_own_kernel<2>);
+      else if (per <= 4)
+        kern = reinterpret_cast<void*>(tac_own_kernel<4>);
+    }
+    CK(cudaLaunchCooperativeKernel(kern, blocks, 1024, args, 0, nullptr));
     LAUNCHED();
     CK(cudaGetLastError());
     CK(cudaMemcpy(prio, d_prio.p, 4ull * R, cudaMemcpyDeviceToHost));
+    if (trace)
+      std::fprintf(stderr, "[tac] setup %.3f ms, state %.3f ms, rounds (%d blocks) %.3f ms\n", ms(t0, t1),
+                   ms(t1, t2), blocks, ms(t2, now()));
     return 0;
   }
   LAUNCHED();
   CK(cudaGetLastError());
   CK(cudaMemcpy(prio, d_prio.p, 4ull * R, cudaMemcpyDeviceToHost));
+  if (trace)
+    std::fprintf(stderr, "[tac] setup %.3f ms, state %.3f ms, rounds (1 block) %.3f ms\n", ms(t0, t1),
+                 ms(t1, t2), ms(t2, now()));
   return 0;
 }
 

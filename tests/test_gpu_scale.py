@@ -56,11 +56,13 @@ def test_multiblock_tac_matches_single_block(orc):
         "print(json.dumps(out))\n")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     res = {}
-    for blocks in ("1", "7", "64"):
+    # 2 blocks: generic distributed kernel at R = 10^4 (5 columns per thread);
+    # 3 / 7 / 64: register-resident candidates (4 / 2 / 1 columns per thread)
+    for blocks in ("1", "2", "3", "7", "64"):
         r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, check=True,
                            env={**os.environ, "TICTAC_TAC_BLOCKS": blocks})
         res[blocks] = json.loads(r.stdout.strip().splitlines()[-1])
-    assert res["1"] == res["7"] == res["64"]
+    assert res["1"] == res["2"] == res["3"] == res["7"] == res["64"]
     for spec in ("layered:10000:1000", "layered:100000:10000"):
         assert res["64"][spec] == TAC_LARGE[spec]["sha256"]
 
