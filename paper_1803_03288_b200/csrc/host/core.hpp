@@ -103,6 +103,18 @@ class Graph {
   DeviceGraph* device() const;
   ~Graph();
 
+  // Per-graph memo of derived, duration-independent analyses (thread-safe;
+  // the graph is immutable, so an entry never goes stale).
+  template <class T, class F>
+  std::shared_ptr<const T> memo(const std::string& key, F&& make) const {
+    std::lock_guard<std::mutex> lock(aux_mu_);
+    auto it = aux_.find(key);
+    if (it != aux_.end()) return std::static_pointer_cast<const T>(it->second);
+    std::shared_ptr<const T> v = std::make_shared<const T>(make());
+    aux_.emplace(key, v);
+    return v;
+  }
+
  private:
   void index_and_validate();
   std::string name_;
@@ -115,6 +127,8 @@ class Graph {
   std::vector<int32_t> res_of_, recv_ops_;
   mutable std::mutex dev_mu_;
   mutable DeviceGraph* dev_ = nullptr;
+  mutable std::mutex aux_mu_;
+  mutable std::map<std::string, std::shared_ptr<const void>> aux_;
 };
 
 // Total map op id -> microseconds (time_oracle.hpp:28-58).

@@ -25,7 +25,7 @@ TimeOracle TimeOracle::declared(const Graph& g) {  // time_oracle.cpp:72-84
   std::map<std::string, int64_t> e;
   std::vector<std::string> missing;
   for (const Op& op : g.ops()) {
-    if (op.time_us) e[op.id] = *op.time_us;
+    if (op.time_us) e.emplace_hint(e.end(), op.id, *op.time_us);  // ops come in id order
     else missing.push_back(op.id);
   }
   if (!missing.empty()) fail(kCoverage, "ops without declared time: " + joined(missing));
@@ -34,7 +34,7 @@ TimeOracle TimeOracle::declared(const Graph& g) {  // time_oracle.cpp:72-84
 
 TimeOracle TimeOracle::general(const Graph& g) {  // time_oracle.cpp:86-91
   std::map<std::string, int64_t> e;
-  for (const Op& op : g.ops()) e[op.id] = op.kind == kRecv ? 1 : 0;
+  for (const Op& op : g.ops()) e.emplace_hint(e.end(), op.id, op.kind == kRecv ? 1 : 0);
   return checked(std::move(e), "general");
 }
 
@@ -76,8 +76,8 @@ TimeOracle TimeOracle::bandwidth(const Graph& g, int64_t bw) {  // time_oracle.c
   std::map<std::string, int64_t> e;
   std::vector<std::string> missing;
   for (const Op& op : g.ops()) {
-    if (transfer(op.kind) && op.bytes) e[op.id] = (2 * *op.bytes + bw) / (2 * bw);
-    else if (op.time_us) e[op.id] = *op.time_us;
+    if (transfer(op.kind) && op.bytes) e.emplace_hint(e.end(), op.id, (2 * *op.bytes + bw) / (2 * bw));
+    else if (op.time_us) e.emplace_hint(e.end(), op.id, *op.time_us);
     else missing.push_back(op.id);
   }
   if (!missing.empty()) fail(kCoverage, "ops without bytes or declared time: " + joined(missing));
@@ -87,9 +87,12 @@ TimeOracle TimeOracle::bandwidth(const Graph& g, int64_t bw) {  // time_oracle.c
 std::vector<int64_t> TimeOracle::durations(const Graph& g) const {
   std::vector<int64_t> d(g.n());
   std::vector<std::string> missing;
+  // ops are indexed in id order, the map iterates in id order: one merge pass
+  auto it = entries.begin();
   for (int32_t i = 0; i < g.n(); ++i) {
-    auto it = entries.find(g.ops()[i].id);
-    if (it == entries.end()) missing.push_back(g.ops()[i].id);
+    const std::string& id = g.ops()[i].id;
+    while (it != entries.end() && it->first < id) ++it;
+    if (it == entries.end() || it->first != id) missing.push_back(id);
     else d[i] = it->second;
   }
   if (!missing.empty()) fail(kCoverage, "oracle missing entries for: " + joined(missing));

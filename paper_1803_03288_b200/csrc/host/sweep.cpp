@@ -30,30 +30,45 @@ struct ChainTables {
   int64_t send_total = 0;
 };
 
-// Preconditions of A.2 plus nested recv-ancestor sets. Returns false (with
-// a reason) when the closed form does not apply.
-bool chain_tables(const Graph& g, const std::vector<int64_t>& dur, bool allow_sends,
-                  ChainTables& t, std::string& why) {
+// Duration-independent part of the closed form for one worker (graph or
+// cluster worker partition): preconditions of A.2, nested recv-ancestor
+// classes, first class of every recv column, the send ops. Computed once per
+// graph (Graph::memo); durations only weight it (chain_tables).
+struct ChainShape {
+  bool ok = false;
+  std::string why;
+  int32_t R = 0, nc = 0;
+  std::vector<int32_t> first;     // per recv column: first class containing it
+  std::vector<int32_t> class_of;  // per op: class of a non-transfer op, else -1
+  std::vector<int32_t> sends;     // send ops (cluster workers)
+};
+
+ChainShape chain_shape(const Graph& g, bool allow_sends) {
+  ChainShape cs;
+  auto no = [&](const char* why) {
+    cs.why = why;
+    return cs;
+  };
   const int32_t n = g.n();
   const auto& ops = g.ops();
   const int32_t R = static_cast<int32_t>(g.recv_ops().size());
-  if (R == 0) return why = "no recv ops", false;
+  if (R == 0) return no("no recv ops");
   int32_t chan = -1, cpu = -1;
   for (int32_t i = 0; i < n; ++i) {
     const int32_t r = g.res_of()[i];
     if (ops[i].kind == kRecv || ops[i].kind == kSend) {
-      if (ops[i].kind == kSend && !allow_sends) return why = "send ops on the worker", false;
-      if (chan >= 0 && chan != r) return why = "more than one channel", false;
+      if (ops[i].kind == kSend && !allow_sends) return no("send ops on the worker");
+      if (chan >= 0 && chan != r) return no("more than one channel");
       chan = r;
     } else {
-      if (cpu >= 0 && cpu != r) return why = "more than one compute unit", false;
+      if (cpu >= 0 && cpu != r) return no("more than one compute unit");
       cpu = r;
     }
-    if (ops[i].kind == kRecv && g.npred(i) > 0) return why = "recv with predecessors", false;
+    if (ops[i].kind == kRecv && g.npred(i) > 0) return no("recv with predecessors");
   }
   // recv-ancestor sets of every compute op (bitsets over recv columns)
   const int32_t W = (R + 63) / 64;
-  if (static_cast<int64_t>(n) * W > (int64_t{1} << 27)) return why = "graph too large for tables", false;
+  if (static_cast<int64_t>(n) * W > (int64_t{1} << 27)) return no("graph too large for tables");
   std::vector<int32_t> col(n, -1);
   for (int32_t c = 0; c < R; ++c) col[g.recv_ops()[c]] = c;
   std::vector<int32_t> order, missing(n);
@@ -75,44 +90,34 @@ bool chain_tables(const Graph& g, const std::vector<int64_t>& dur, bool allow_se
   std::vector<int32_t> comp;
   for (int32_t i = 0; i < n; ++i)
     if (!transfer(ops[i].kind)) comp.push_back(i);
-  auto pc = [&](int32_t v) {
-    int64_t k = 0;
-    for (int32_t q = 0; q < W; ++q) k += __builtin_popcountll(bits[static_cast<size_t>(v) * W + q]);
-    return k;
-  };
+  std::vector<int64_t> pop(n, 0);
+  for (int32_t v : comp)
+    for (int32_t q = 0; q < W; ++q) pop[v] += __builtin_popcountll(bits[static_cast<size_t>(v) * W + q]);
   auto less = [&](int32_t a, int32_t b) {
-    const int64_t ka = pc(a), kb = pc(b);
-    if (ka != kb) return ka < kb;
+    if (pop[a] != pop[b]) return pop[a] < pop[b];
     return std::lexicographical_compare(&bits[static_cast<size_t>(a) * W], &bits[static_cast<size_t>(a) * W] + W,
                                         &bits[static_cast<size_t>(b) * W], &bits[static_cast<size_t>(b) * W] + W);
   };
   std::sort(comp.begin(), comp.end(), less);
   std::vector<int32_t> rep;  // class representative
-  std::vector<int64_t> weight;
+  cs.class_of.assign(n, -1);
   for (int32_t v : comp) {
-    if (rep.empty() || less(rep.back(), v)) {
-      rep.push_back(v);
-      weight.push_back(0);
-    }
-    weight.back() += dur[v];
+    if (rep.empty() || less(rep.back(), v)) rep.push_back(v);
+    cs.class_of[v] = static_cast<int32_t>(rep.size()) - 1;
   }
   const int32_t nc = static_cast<int32_t>(rep.size());
   for (int32_t j = 1; j < nc; ++j) {  // nested?
     const uint64_t* a = &bits[static_cast<size_t>(rep[j - 1]) * W];
     const uint64_t* b = &bits[static_cast<size_t>(rep[j]) * W];
     for (int32_t q = 0; q < W; ++q)
-      if (a[q] & ~b[q]) return why = "recv-ancestor sets are not nested", false;
+      if (a[q] & ~b[q]) return no("recv-ancestor sets are not nested");
   }
-  t.R = R;
-  t.nc = nc;
-  t.d.resize(R);
-  t.first.assign(R, nc);
-  for (int32_t c = 0; c < R; ++c) t.d[c] = dur[g.recv_ops()[c]];
+  cs.R = R;
+  cs.nc = nc;
+  cs.first.assign(R, nc);
   for (int32_t j = nc - 1; j >= 0; --j)
     for (int32_t c = 0; c < R; ++c)
-      if ((bits[static_cast<size_t>(rep[j]) * W + (c >> 6)] >> (c & 63)) & 1) t.first[c] = j;
-  t.pwsuf.assign(nc + 1, 0);
-  for (int32_t j = nc - 1; j >= 0; --j) t.pwsuf[j] = t.pwsuf[j + 1] + weight[j];
+      if ((bits[static_cast<size_t>(rep[j]) * W + (c >> 6)] >> (c & 63)) & 1) cs.first[c] = j;
   // sends: must be released exactly when the last compute finishes, i.e.
   // depend on every compute op that has no compute successor.
   if (allow_sends) {
@@ -127,12 +132,32 @@ bool chain_tables(const Graph& g, const std::vector<int64_t>& dur, bool allow_se
       if (ops[i].kind != kSend) continue;
       std::set<int32_t> pre(g.pred_idx().begin() + g.pred_off()[i], g.pred_idx().begin() + g.pred_off()[i + 1]);
       for (int32_t p : pre)
-        if (transfer(ops[p].kind)) return why = "send depends on a transfer", false;
+        if (transfer(ops[p].kind)) return no("send depends on a transfer");
       if (sinks.empty() || !std::includes(pre.begin(), pre.end(), sinks.begin(), sinks.end()))
-        return why = "send not released by the last compute", false;
-      t.send_total += dur[i];
+        return no("send not released by the last compute");
+      cs.sends.push_back(i);
     }
   }
+  cs.ok = true;
+  return cs;
+}
+
+// Weights the shape with one oracle's durations (O(n)).
+bool chain_tables(const ChainShape& cs, const Graph& g, const std::vector<int64_t>& dur, ChainTables& t,
+                  std::string& why) {
+  if (!cs.ok) return why = cs.why, false;
+  t.R = cs.R;
+  t.nc = cs.nc;
+  t.first = cs.first;
+  t.d.resize(cs.R);
+  for (int32_t c = 0; c < cs.R; ++c) t.d[c] = dur[g.recv_ops()[c]];
+  std::vector<int64_t> weight(cs.nc, 0);
+  for (int32_t v = 0; v < g.n(); ++v)
+    if (cs.class_of[v] >= 0) weight[cs.class_of[v]] += dur[v];
+  t.pwsuf.assign(cs.nc + 1, 0);
+  for (int32_t j = cs.nc - 1; j >= 0; --j) t.pwsuf[j] = t.pwsuf[j + 1] + weight[j];
+  t.send_total = 0;
+  for (int32_t i : cs.sends) t.send_total += dur[i];
   for (int64_t x : t.d)
     if (x >= (int64_t{1} << 31)) return why = "recv duration beyond 32 bits", false;
   return true;
@@ -166,6 +191,7 @@ int64_t SweepCtx::order_makespan(const std::vector<int32_t>& order) {
 std::unique_ptr<SweepCtx> make_sweep(std::shared_ptr<const Graph> g, const TimeOracle& o,
                                      const Policy& p) {
   auto s = std::make_unique<SweepCtx>();
+  const auto t0 = std::chrono::steady_clock::now();
   s->g = g;
   s->dur = o.durations(*g);
   if (p.noise < 0.0 || p.noise > 1.0) fail(kParameter, "reorder_noise must be within [0, 1]");
@@ -192,7 +218,8 @@ std::unique_ptr<SweepCtx> make_sweep(std::shared_ptr<const Graph> g, const TimeO
   std::vector<ChainTables> tabs;
   if (ok && !s->cluster) {
     tabs.emplace_back();
-    ok = chain_tables(*g, s->dur, false, tabs.back(), s->why);
+    const auto shape = g->memo<ChainShape>("chain", [&] { return chain_shape(*g, false); });
+    ok = chain_tables(*shape, *g, s->dur, tabs.back(), s->why);
   } else if (ok) {
     // devices other than workers must not feed back into workers
     for (const auto& dv : s->workers) {
@@ -208,7 +235,8 @@ std::unique_ptr<SweepCtx> make_sweep(std::shared_ptr<const Graph> g, const TimeO
             }
       if (!ok) break;
       tabs.emplace_back();
-      if (!(ok = chain_tables(*part, pd, true, tabs.back(), s->why))) break;
+      const auto shape = g->memo<ChainShape>("chain:" + dv, [&] { return chain_shape(*part, true); });
+      if (!(ok = chain_tables(*shape, *part, pd, tabs.back(), s->why))) break;
       if (tabs.back().R != tabs[0].R || tabs.back().nc != tabs[0].nc) {
         ok = false;
         s->why = "workers differ in shape";
@@ -216,6 +244,7 @@ std::unique_ptr<SweepCtx> make_sweep(std::shared_ptr<const Graph> g, const TimeO
       }
     }
   }
+  const auto t1 = std::chrono::steady_clock::now();
   if (ok) {
     const int32_t W = static_cast<int32_t>(tabs.size()), R = tabs[0].R, nc = tabs[0].nc;
     std::vector<int64_t> d, pw, send;
@@ -233,6 +262,12 @@ std::unique_ptr<SweepCtx> make_sweep(std::shared_ptr<const Graph> g, const TimeO
     s->fast = true;
     s->nc = nc;
     s->R = R;
+  }
+  if (std::getenv("TICTAC_SWEEP_TRACE")) {
+    const auto t2 = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[make_sweep] analysis %.3f ms, plan %.3f ms\n",
+                 std::chrono::duration<double, std::milli>(t1 - t0).count(),
+                 std::chrono::duration<double, std::milli>(t2 - t1).count());
   }
   return s;
 }
