@@ -22,6 +22,7 @@
 // The shuffle array lives in shared memory as bytes (R ≤ 256) or halves,
 // laid out [k/4][thread] so every lane always hits its own bank.
 #include <algorithm>
+#include <cstdlib>
 #include <cub/cub.cuh>
 #include <iterator>
 #include <vector>
@@ -50,6 +51,7 @@ struct ChainArgs {
   int64_t U, L;
   int do_e;
   int key_bits;           // statistics keys: (m << key_bits) | offset
+  int force_slow;         // test knob: every shuffle through the generic engine
   const int32_t* orders;  // explicit orders mode (W == 1)
   int64_t* makespans;
   int64_t* worker_ms;
@@ -302,7 +304,12 @@ __global__ void __launch_bounds__(kSweepThreads, 3) chain_sweep_kernel(ChainArgs
         for (int k = R - 1; k >= 0; --k) f.add(tab[o[k]], ctot, pw);
       } else {
         const uint64_t ws = a.cluster ? splitmix64(seed ^ (kPhi * static_cast<uint64_t>(w + 1))) : seed;
-        shuffle_fold(ws, R, items, f, tab, ctot, pw, s_lim, s_mag);
+        if (a.force_slow) {
+          items.init(R);
+          f = shuffle_slow(ws, 0, R, items, f, tab, ctot, pw);
+        } else {
+          shuffle_fold(ws, R, items, f, tab, ctot, pw, s_lim, s_mag);
+        }
       }
       if (f.G > 0) f.best = max(f.best, pw[0]);  // bin 0: computes needing no recv
       const int64_t tcpu = f.best < 0 ? 0 : static_cast<int64_t>(f.best);
@@ -545,6 +552,7 @@ static ChainArgs chain_args(SweepPlan* p) {
   a.L = p->L;
   a.do_e = !p->cluster && p->U != p->L;
   a.key_bits = csk_key_bits(p->U);
+  a.force_slow = std::getenv("TICTAC_SWEEP_FORCE_SLOW") != nullptr;
   return a;
 }
 

@@ -167,3 +167,38 @@ def test_tac_traffic_terms(lib):
         assert t["E_recv"] == sum(kind[a] == "recv" for a, _ in d["edges"])
         assert t["nnz"] == sum(len(s) for s in dep.values())
         assert t["rows"] <= t["V"] and t["row_nnz"] <= t["nnz"]
+
+
+@pytest.mark.parametrize("spec", ["resnet_v2_101_training", "layered:4000:400"])
+def test_sweep_generic_engine_and_long_streams(lib, orc, ref, monkeypatch, tmp_path, spec):
+    """The closed-form sweep's generic mt19937_64 engine (the path taken after
+    a bounded() rejection and for draws past the first 311 outputs, i.e.
+    R > 312) forced for every seed equals the register fast path; at R = 400
+    (long streams, 16-bit shuffle slots) the makespans also match the oracle
+    and the reference's own per-seed loop."""
+    import subprocess
+    import oracle
+    from paper_1803_03288_b200.capi import SweepPlan
+    g = lib.model(spec, 1)
+    o = g.declared()
+    SweepPlan.create(g, o)  # raises unless the closed form applies
+    n = 20_000
+    fast = g.sweep_random(o, 1, n, None, makespans=True)
+    monkeypatch.setenv("TICTAC_SWEEP_FORCE_SLOW", "1")
+    slow = g.sweep_random(o, 1, n, None, makespans=True)
+    monkeypatch.delenv("TICTAC_SWEEP_FORCE_SLOW")
+    assert np.array_equal(fast["makespans"], slow["makespans"])
+    assert fast["min_us"] == slow["min_us"] and fast["argmin_seed"] == slow["argmin_seed"]
+    assert np.array_equal(fast["e_hist"], slow["e_hist"])
+    if g.recv_count() <= 312:
+        return
+    og = orc.OracleGraph(json.loads(g.serialize()))
+    for s in (1, 2, 777, 19_999):
+        assert fast["makespans"][s - 1] == og.simulate(og.random_schedule(s), True, s, 0.0)[0], s
+    path = tmp_path / "g.json"
+    path.write_text(g.serialize())
+    seeds = np.arange(1, 301, dtype=np.uint64)
+    seeds.tofile(tmp_path / "s.bin")
+    subprocess.run([oracle.REF_SWEEP, "sweeplist", str(path), "declared", str(tmp_path / "s.bin"), "0",
+                    str(tmp_path / "m.bin")], capture_output=True, text=True, check=True)
+    assert np.array_equal(np.fromfile(tmp_path / "m.bin", dtype=np.int64), fast["makespans"][:300])
