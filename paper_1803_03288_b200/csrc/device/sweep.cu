@@ -59,26 +59,6 @@ struct ChainArgs {
   double* f64;
 };
 
-// Rare path: the stream needs output >= 311 (only after ≥ 312-R+1
-// rejections of bounded(), probability < 1e-15) or R > 312.
-__device__ __noinline__ uint64_t mt_output_at(uint64_t seed, int idx) {
-  uint64_t st[312];
-  MtFull m{st, 0};
-  m.seed(seed);
-  uint64_t v = 0;
-  for (int k = 0; k <= idx; ++k) v = m.next();
-  return v;
-}
-
-struct PermStream {
-  MtLazy lz;
-  __device__ __forceinline__ void init(uint64_t s) { lz.init(s); }
-  __device__ __forceinline__ uint64_t next() {
-    if (!lz.exhausted()) return lz.next_raw();
-    return mt_output_at(lz.seed, lz.i++);
-  }
-};
-
 template <typename T>
 struct Items;  // shared-memory shuffle array, [k / per_word][thread]
 
@@ -420,17 +400,31 @@ __global__ void random_orders_kernel(int R, int S, const uint64_t* __restrict__ 
   for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < S; s += gridDim.x * blockDim.x) {
     int32_t* p = perms + static_cast<int64_t>(s) * R;
     for (int k = 0; k < R; ++k) p[k] = k;
-    PermStream rng;
-    rng.init(seeds[s]);
+    // register cursors for the first 311 outputs, then a full state in
+    // local memory continuing the same stream (linear in R)
+    MtLazy lz;
+    lz.init(seeds[s]);
+    uint64_t st[312];
+    MtFull full{st, 0};
+    bool on_full = false;
+    auto next = [&]() -> uint64_t {
+      if (!on_full) {
+        if (!lz.exhausted()) return lz.next_raw();
+        full.seed(lz.seed);
+        for (int k = 0; k < lz.i; ++k) full.next();
+        on_full = true;
+      }
+      return full.next();
+    };
     for (int i = R; i > 1; --i) {
-      uint64_t v = rng.next(), j;
+      uint64_t v = next(), j;
       if (i < 4096) {
-        while (v > lim[i]) v = rng.next();
+        while (v > lim[i]) v = next();
         j = fastmod(v, static_cast<uint64_t>(i), mag[i]);
       } else {
         const uint64_t n = static_cast<uint64_t>(i);
         const uint64_t limit = UINT64_MAX - (UINT64_MAX % n + 1) % n;
-        while (v > limit) v = rng.next();
+        while (v > limit) v = next();
         j = v % n;
       }
       const int32_t t = p[i - 1];

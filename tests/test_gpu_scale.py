@@ -202,3 +202,18 @@ def test_sweep_generic_engine_and_long_streams(lib, orc, ref, monkeypatch, tmp_p
     subprocess.run([oracle.REF_SWEEP, "sweeplist", str(path), "declared", str(tmp_path / "s.bin"), "0",
                     str(tmp_path / "m.bin")], capture_output=True, text=True, check=True)
     assert np.array_equal(np.fromfile(tmp_path / "m.bin", dtype=np.int64), fast["makespans"][:300])
+
+
+def test_random_schedule_large_R_matches_reference(lib, ref):
+    """cs_schedule_random past mt19937_64's first block (R = 2,000 and
+    10,000): the stream continues linearly from a full state, priorities
+    identical to the reference's."""
+    import time
+    for spec in ("layered:20000:2000", "layered:100000:10000"):
+        text = lib.model(spec, 1).serialize()
+        g, rg = lib.graph(text), ref.graph(text)
+        for seed in (0, 5):
+            t = time.perf_counter()
+            ours = g.random(seed).serialize()
+            assert time.perf_counter() - t < 5.0, spec  # linear in R (was quadratic)
+            assert ours == rg.random(seed).serialize(), (spec, seed)
