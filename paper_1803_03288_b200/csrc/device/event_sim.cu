@@ -813,9 +813,16 @@ int run_event(DeviceGraph* g, const int64_t* dur, int64_t B, RunSpec rs, int64_t
     int64_t groups = std::min<int64_t>((B + 31) / 32, static_cast<int64_t>(sms) * per_sm);
     groups = std::max<int64_t>(
         1, std::min<int64_t>(groups, static_cast<int64_t>(kThreadScratch / ((hg + cg) * per_group))));
-    const int blocks = static_cast<int>((groups + kWarpsPerBlock - 1) / kWarpsPerBlock);
-    const size_t total = static_cast<size_t>(blocks) * kWarpsPerBlock * per_group;
-    char* scr = pool.get(dev, (hg + cg) * total, err);
+    // fewer runs in flight when HBM is short (the GPU may be shared)
+    int blocks = 0;
+    size_t total = 0;
+    char* scr = nullptr;
+    for (;;) {
+      blocks = static_cast<int>((groups + kWarpsPerBlock - 1) / kWarpsPerBlock);
+      total = static_cast<size_t>(blocks) * kWarpsPerBlock * per_group;
+      if ((scr = pool.get(dev, (hg + cg) * total, err)) || groups <= kWarpsPerBlock) break;
+      groups /= 2;
+    }
     if (!scr) return 1;
     if (inter)
       event_sim_kernel<1, 32><<<blocks, 32 * kWarpsPerBlock>>>(G, rs, B, scr, hg, scr + hg * total, cg, g->rb_words);
@@ -848,11 +855,18 @@ int run_event(DeviceGraph* g, const int64_t* dur, int64_t B, RunSpec rs, int64_t
       CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, event_sim_kernel<32, 1>, 32 * wpb, hsz * wpb));
       per_sm = std::max(1, occ) * wpb;
     }
-    const int64_t slots = std::min<int64_t>(B, static_cast<int64_t>(sms) * per_sm);
-    const int blocks = static_cast<int>((slots + wpb - 1) / wpb);
-    const int64_t total_slots = static_cast<int64_t>(blocks) * wpb;
-    const size_t hot_total = in_smem ? 0 : hsz * static_cast<size_t>(total_slots);
-    char* scr = pool.get(dev, hot_total + csz * static_cast<size_t>(total_slots), err);
+    int64_t slots = std::min<int64_t>(B, static_cast<int64_t>(sms) * per_sm);
+    int blocks = 0;
+    size_t hot_total = 0;
+    int64_t total_slots = 0;
+    char* scr = nullptr;
+    for (;;) {  // fewer runs in flight when HBM is short
+      blocks = static_cast<int>((slots + wpb - 1) / wpb);
+      total_slots = static_cast<int64_t>(blocks) * wpb;
+      hot_total = in_smem ? 0 : hsz * static_cast<size_t>(total_slots);
+      if ((scr = pool.get(dev, hot_total + csz * static_cast<size_t>(total_slots), err)) || slots <= wpb) break;
+      slots /= 2;
+    }
     if (!scr) return 1;
     event_sim_kernel<32, 1><<<blocks, 32 * wpb, in_smem ? hsz * wpb : 0>>>(
         G, rs, B, in_smem ? nullptr : scr, hsz, scr + hot_total, csz, g->rb_words);

@@ -2,6 +2,7 @@
 known answers and against the reference library built from
 /root/reference (oracle/_ref), byte for byte, through the same C ABI."""
 import json
+import os
 
 import numpy as np
 import pytest
@@ -292,3 +293,25 @@ def test_irregular_sweeps_match_reference(lib, ref, gated, noise):
             if cl:
                 it = json.loads(r.iteration_json())
                 assert list(res["worker_makespans"][i]) == list(it["per_worker_makespan_us"].values())
+
+
+def test_event_sim_backs_off_when_hbm_is_short(lib):
+    """With most of HBM taken by another allocation, a large exact-path batch
+    runs with fewer runs in flight instead of failing (fresh process, so the
+    simulator's scratch pool starts empty)."""
+    import subprocess
+    import sys
+    code = (
+        "import sys, torch; sys.path.insert(0, '.')\n"
+        "from paper_1803_03288_b200.capi import Lib, policy\n"
+        "g = Lib().model('resnet_v2_101_training', 1); o = g.declared()\n"
+        "free, _ = torch.cuda.mem_get_info()\n"
+        "hog = torch.empty(max(0, free - (3 << 30)), dtype=torch.uint8, device='cuda')\n"
+        "r = g.sweep_random(o, 1, 100000, policy(False, 0, 0.0))\n"
+        "print(r['count'], r['min_us'], r['argmin_seed'], r['sum_us'])\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, check=True)
+    got = [int(x) for x in out.stdout.split()[-4:]]
+    g = lib.model("resnet_v2_101_training", 1)
+    r = g.sweep_random(g.declared(), 1, 100000, policy(False, 0, 0.0))
+    assert got == [r["count"], r["min_us"], r["argmin_seed"], r["sum_us"]]
