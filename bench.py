@@ -135,6 +135,16 @@ def graph_files(lib, model):
     return g, p
 
 
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def ref_sweep(path, seed_lo, count, threads, noise=None, out_path="-"):
     import oracle
     cmd = [oracle.REF_SWEEP, "sweep", path, "declared", str(seed_lo), str(count), str(threads), out_path]
@@ -222,6 +232,7 @@ def cpu_baseline(path, target_s=10.0, g=None, o=None):
     binp = os.path.join(os.path.dirname(path), "ref_sample.bin")
     r = ref_sweep(path, SEED_LO, n, cores, None, binp)
     out = {"value": r["sims"] / r["seconds"], "unit": "sims/s", "cores": cores, "kind": "reference",
+           "nproc": os.cpu_count(), "cpu_model": cpu_model(),
            "sample": f"seeds {SEED_LO}..{SEED_LO + n - 1} of the same workload ({n} sims, "
                      f"{r['seconds']:.1f} s wall, {cores} threads, oracle/_ref libcommsched -O3)"}
     if g is not None:
@@ -375,6 +386,7 @@ def run_reference(args, rank, world):
     v = sims / secs
     base.update({"value": v, "ms_per_step": 1000 * secs / args.steps, "vs_baseline": None,
                  "cpu_baseline": {"value": v, "unit": "sims/s", "cores": cores, "kind": "reference",
+                                  "nproc": os.cpu_count(), "cpu_model": cpu_model(),
                                   "sample": f"{per_step} seeds per step, {cores} threads"},
                  "e2e": {"value": v, "unit": "sims/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}})
     emit(base)
