@@ -41,12 +41,14 @@ namespace {
 
 constexpr int64_t kInf = INT64_MAX;
 
+// Per-call device arrays: stream-ordered allocations on the legacy stream
+// (the pool keeps its reservation between calls, graph.cu).
 struct DevArr {
   void* p = nullptr;
   DevArr() = default;
   DevArr(const DevArr&) = delete;
   ~DevArr() {
-    if (p) cudaFree(p);
+    if (p) cudaFreeAsync(p, 0);
   }
   template <typename T>
   T* as() const {
@@ -56,12 +58,12 @@ struct DevArr {
 
 template <typename T>
 int alloc(DevArr& a, size_t count, char* err) {
-  CK(cudaMalloc(&a.p, sizeof(T) * (count ? count : 1)));
+  CK(cudaMallocAsync(&a.p, sizeof(T) * (count ? count : 1), 0));
   return 0;
 }
 template <typename T>
 int put(DevArr& a, const std::vector<T>& v, char* err) {
-  CK(cudaMalloc(&a.p, sizeof(T) * (v.empty() ? 1 : v.size())));
+  CK(cudaMallocAsync(&a.p, sizeof(T) * (v.empty() ? 1 : v.size()), 0));
   if (!v.empty()) CK(cudaMemcpy(a.p, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice));
   return 0;
 }
@@ -295,30 +297,28 @@ __device__ __forceinline__ void grid_bar(cg::grid_group& grid) {
     grid.sync();
 }
 
-__global__ void __launch_bounds__(1024) tac_kernel(TacArgs a) {
-  cg::grid_group grid = cg::this_grid();
-  __shared__ int red[3];
-  int sp = 0;
-  init_red(red);
-  const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int64_t nthreads = static_cast<int64_t>(gridDim.x) * blockDim.x;
+// The R rounds of one-block TAC (phases A-C below) over the state `a` points
+// at — global memory (tac_kernel) or a shared-memory copy (tac_smem_kernel).
+// Three kinds of block barrier per round: the first block-wide min (which also
+// publishes phase A's M+), one per find-first step (the last one orders every
+// read of P/out/M+ before the retire writes them), and one after the retire.
+template <typename ColT>
+__device__ __forceinline__ void tac_rounds(const TacArgs& a, const ColT* __restrict__ col, int* red, int& sp) {
   const int R = a.R;
   for (int round = 0; round < R; ++round) {
     // Phase A: amended M+ of every outstanding recv = min M over its
-    // direct-successor groups.
-    for (int64_t c = tid; c < R; c += nthreads) {
+    // direct-successor groups; the lowest outstanding column.
+    int first = 0x7fffffff;
+    for (int c = threadIdx.x; c < R; c += blockDim.x) {
       if (!a.out[c]) continue;
       int64_t m = kInf;
       for (int32_t e = a.succ_off[c]; e < a.succ_off[c + 1]; ++e) m = min(m, a.M[a.succ[e]]);
       a.mp[c] = m;
+      first = min(first, c);
     }
-    grid_bar(grid);
-    // Phase B (every block, redundantly): the reference's left fold over
-    // outstanding recvs in id order == find-first-beater chain.
-    int best = 0x7fffffff;
-    for (int c = threadIdx.x; c < R; c += blockDim.x)
-      if (a.out[c]) best = min(best, c);
-    best = block_min_int(best, red, sp);
+    // Phase B: the reference's left fold over outstanding recvs in id order
+    // == find-first-beater chain.
+    int best = block_min_int(first, red, sp);
     for (;;) {
       const int64_t bp = a.P[best], bm = a.tcol[best], bmp = a.mp[best];
       int nxt = 0x7fffffff;
@@ -331,22 +331,100 @@ __global__ void __launch_bounds__(1024) tac_kernel(TacArgs a) {
       if (nxt == 0x7fffffff) break;
       best = nxt;
     }
-    grid_bar(grid);  // every block has read P/out before anyone retires
     // Phase C: retire `best`.
     const int64_t t = a.tcol[best];
-    for (int64_t e = a.col_off[best] + tid; e < a.col_off[best + 1]; e += nthreads) {
-      const int32_t g = a.col[e];
+    for (int32_t e = a.col_off[best] + threadIdx.x; e < a.col_off[best + 1]; e += blockDim.x) {
+      const int32_t g = col[e];
       const int k = --a.cnt[g];
       a.M[g] -= t;
       const int x = (a.xr[g] ^= best);
       if (k == 1) atomicAdd(reinterpret_cast<unsigned long long*>(&a.P[x]), a.wsum[g]);
     }
-    if (tid == 0) {
+    if (threadIdx.x == 0) {
       a.prio[best] = round;
       a.out[best] = 0;
     }
-    grid_bar(grid);
+    __syncthreads();
   }
+}
+
+__global__ void __launch_bounds__(1024) tac_kernel(TacArgs a) {  // one block
+  __shared__ int red[3];
+  int sp = 0;
+  init_red(red);
+  tac_rounds(a, a.col, red, sp);
+}
+
+// Shared-memory bytes of tac_smem_kernel's state copy.
+__host__ __device__ inline size_t tac_smem_bytes(int nrows, int R, int nsucc) {
+  return 8ull * (2ull * nrows + 3ull * R) + 4ull * (2ull * nrows + 2ull * (R + 1) + nsucc) + R;
+}
+// plus the column lists as 16-bit row ids, when they fit (ncol > 0)
+__host__ __device__ inline size_t tac_smem_col_bytes(int64_t ncol) { return (2ull * ncol + 15) & ~size_t(15); }
+
+// One block with every per-round array in shared memory: the rounds' dependent
+// reads of values other threads just wrote (M, cnt, xr, P, mp, out) cost a
+// shared-memory round trip instead of an L2 one. Column lists (the retire
+// work lists) and prio stay in global memory.
+__global__ void __launch_bounds__(1024) tac_smem_kernel(TacArgs g, int nrows, int nsucc, int ncol) {
+  extern __shared__ __align__(16) char tac_sm[];
+  __shared__ int red[3];
+  int sp = 0;
+  const int R = g.R;
+  char* q = tac_sm;
+  auto* col16 = reinterpret_cast<uint16_t*>(q);  // first: 16-byte aligned
+  q += ncol > 0 ? tac_smem_col_bytes(ncol) : 0;
+  for (int e = threadIdx.x; e < ncol; e += blockDim.x) col16[e] = static_cast<uint16_t>(g.col[e]);
+  auto take = [&q](size_t bytes) {
+    char* p = q;
+    q += bytes;
+    return p;
+  };
+  auto* M = reinterpret_cast<int64_t*>(take(8ull * nrows));
+  auto* wsum = reinterpret_cast<unsigned long long*>(take(8ull * nrows));
+  auto* P = reinterpret_cast<int64_t*>(take(8ull * R));
+  auto* mp = reinterpret_cast<int64_t*>(take(8ull * R));
+  auto* tcol = reinterpret_cast<int64_t*>(take(8ull * R));
+  auto* cnt = reinterpret_cast<int32_t*>(take(4ull * nrows));
+  auto* xr = reinterpret_cast<int32_t*>(take(4ull * nrows));
+  auto* succ_off = reinterpret_cast<int32_t*>(take(4ull * (R + 1)));
+  auto* col_off = reinterpret_cast<int32_t*>(take(4ull * (R + 1)));
+  auto* succ = reinterpret_cast<int32_t*>(take(4ull * nsucc));
+  auto* out = reinterpret_cast<uint8_t*>(take(R));
+  for (int k = threadIdx.x; k < nrows; k += blockDim.x) {
+    M[k] = g.M[k];
+    wsum[k] = g.wsum[k];
+    cnt[k] = g.cnt[k];
+    xr[k] = g.xr[k];
+  }
+  for (int c = threadIdx.x; c < R; c += blockDim.x) {
+    P[c] = g.P[c];
+    mp[c] = g.mp[c];
+    tcol[c] = g.tcol[c];
+    out[c] = g.out[c];
+  }
+  for (int c = threadIdx.x; c <= R; c += blockDim.x) {
+    succ_off[c] = g.succ_off[c];
+    col_off[c] = g.col_off[c];
+  }
+  for (int e = threadIdx.x; e < nsucc; e += blockDim.x) succ[e] = g.succ[e];
+  init_red(red);  // also the barrier after the copies
+  TacArgs a = g;
+  a.tcol = tcol;
+  a.succ_off = succ_off;
+  a.col_off = col_off;
+  a.succ = succ;
+  a.wsum = wsum;
+  a.cnt = cnt;
+  a.M = M;
+  a.xr = xr;
+  a.P = P;
+  a.mp = mp;
+  a.out = out;
+  if (ncol > 0)
+    tac_rounds(a, col16, red, sp);
+  else
+    tac_rounds(a, a.col, red, sp);
 }
 
 // Multi-block TAC: the selection fold is distributed too. Every find-first
@@ -552,7 +630,7 @@ int group_setup(DeviceGraph* g, const int64_t* dur, GroupState& S, char* err) {
   size_t tmp_bytes = 0;
   CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, S.d_colcount.as<int32_t>(),
                                    S.d_coloff.as<int32_t>(), g->R + 1));
-  CK(cudaMalloc(&S.d_tmp.p, std::max<size_t>(tmp_bytes, 16)));
+  CK(cudaMallocAsync(&S.d_tmp.p, std::max<size_t>(tmp_bytes, 16), 0));
   CK(cub::DeviceScan::ExclusiveSum(S.d_tmp.p, tmp_bytes, S.d_colcount.as<int32_t>(),
                                    S.d_coloff.as<int32_t>(), g->R + 1));
   LAUNCHED();
@@ -647,7 +725,7 @@ extern "C" int csk_tic(DeviceGraph* g, int mode, int32_t* prio, int* total, char
   CK(cub::DeviceRadixSort::SortKeys(nullptr, b1, d_Mp.as<int64_t>(), d_sorted.as<int64_t>(), R));
   CK(cub::DeviceSelect::Unique(nullptr, b2, d_sorted.as<int64_t>(), d_unique.as<int64_t>(),
                                d_nu.as<int32_t>(), R));
-  CK(cudaMalloc(&d_tmp.p, std::max<size_t>(std::max(b1, b2), 16)));
+  CK(cudaMallocAsync(&d_tmp.p, std::max<size_t>(std::max(b1, b2), 16), 0));
   CK(cub::DeviceRadixSort::SortKeys(d_tmp.p, b1, d_Mp.as<int64_t>(), d_sorted.as<int64_t>(), R));
   CK(cub::DeviceSelect::Unique(d_tmp.p, b2, d_sorted.as<int64_t>(), d_unique.as<int64_t>(),
                                d_nu.as<int32_t>(), R));
@@ -718,8 +796,27 @@ extern "C" int csk_tac(DeviceGraph* g, const int64_t* dur, int32_t* prio, char* 
   blocks = std::max(blocks, 1);
   const auto t2 = now();
   if (blocks == 1) {
-    void* args[] = {&a};
-    CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(tac_kernel), 1, 1024, args, 0, nullptr));
+    int nrows = S.rw.nrows, nsucc = static_cast<int>(S.rw.succ.size());
+    size_t smem = tac_smem_bytes(nrows, R, nsucc);
+    constexpr size_t kSmemMax = 220 * 1024;
+    // column lists in shared memory too when 16-bit row ids fit beside the state
+    int ncol = 0;
+    if (nrows < 65536 && S.nnz > 0 && smem + tac_smem_col_bytes(S.nnz) <= kSmemMax &&
+        !std::getenv("TICTAC_TAC_NO_SMEM_COL")) {
+      ncol = static_cast<int>(S.nnz);
+      smem += tac_smem_col_bytes(ncol);
+    }
+    if (smem <= kSmemMax && !std::getenv("TICTAC_TAC_NO_SMEM")) {
+      CK(cudaFuncSetAttribute(tac_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+      void* args[] = {&a, &nrows, &nsucc, &ncol};
+      // a block sized to the per-round work: idle warps only lengthen barriers
+      int threads = R <= 512 ? 512 : 1024;
+      if (const char* env = std::getenv("TICTAC_TAC_THREADS")) threads = std::max(32, std::min(1024, std::atoi(env)));
+      CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(tac_smem_kernel), 1, threads, args, smem, nullptr));
+    } else {
+      void* args[] = {&a};
+      CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(tac_kernel), 1, 1024, args, 0, nullptr));
+    }
   } else {
     DevArr d_ring;
     const std::vector<int32_t> ring = {0x7fffffff, 0x7fffffff, 0x7fffffff};
