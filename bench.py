@@ -157,7 +157,8 @@ def ref_sweep(path, seed_lo, count, threads, noise=None, out_path="-"):
 def single_report(lib, reps=7):
     """One cs_simulate + cs_report_json (the event list) for a random order,
     configs 1 and 4, median of `reps` calls — this library, and the
-    reference library on one host core when oracle/_ref is built."""
+    reference library on one host core when oracle/_ref is built; also
+    cs_simulate + cs_report_makespan alone (no event list requested)."""
     from paper_1803_03288_b200 import capi
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle
@@ -172,12 +173,16 @@ def single_report(lib, reps=7):
             g = L.graph(text)
             o = g.declared()
             s = g.random(1)
-            ts = []
+            ts, tm = [], []
             for _ in range(reps + 1):
                 t = time.perf_counter()
                 js = g.simulate(o, s, capi.policy(True, 1, 0.0)).json()
                 ts.append(time.perf_counter() - t)
+                t = time.perf_counter()
+                g.simulate(o, s, capi.policy(True, 1, 0.0)).makespan()
+                tm.append(time.perf_counter() - t)
             row[f"{name}_ms"] = 1000 * sorted(ts[1:])[reps // 2]
+            row[f"{name}_makespan_only_ms"] = 1000 * sorted(tm[1:])[reps // 2]
             docs[name] = js
         if len(docs) == 2:
             row["identical_json"] = docs["ours"] == docs["reference_cpu"]
