@@ -32,6 +32,22 @@ struct CudaError {
 
 int ensure_device(char* err);  // selects/initialises the current device
 
+// Lets a kernel launch with up to the device's opt-in shared memory. The
+// limit is a per-function attribute, not per launch: setting it to one call's
+// need would race with (or shrink below) another caller's, so every caller
+// sets the same maximum (idempotent).
+inline cudaError_t allow_max_dynamic_smem(const void* fn) {
+  int dev = 0, optin = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  cudaFuncAttributes fa{};
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, fn);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             optin - static_cast<int>(fa.sharedSizeBytes));
+  return e;
+}
+
 // Owned device allocation (freed on every exit path).
 struct DevMem {
   void* p = nullptr;

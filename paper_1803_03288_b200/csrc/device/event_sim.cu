@@ -846,8 +846,7 @@ int run_event(DeviceGraph* g, const int64_t* dur, int64_t B, RunSpec rs, int64_t
                                : static_cast<int>(std::min<size_t>(kWarpsPerBlock, kSmemBudget / hsz));
     int per_sm = 16;
     if (in_smem) {
-      CK(cudaFuncSetAttribute(event_sim_kernel<32, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              static_cast<int>(hsz * wpb)));
+      CK(allow_max_dynamic_smem(reinterpret_cast<const void*>(event_sim_kernel<32, 1>)));
       const int carve =
           static_cast<int>(std::min<size_t>(100, (hsz * wpb * 100 + 228 * 1024 - 1) / (228 * 1024) + 3));
       CK(cudaFuncSetAttribute(event_sim_kernel<32, 1>, cudaFuncAttributePreferredSharedMemoryCarveout, carve));

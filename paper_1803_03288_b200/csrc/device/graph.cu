@@ -1,6 +1,7 @@
 // Device-resident graph structure: CSR adjacency in the reference's index
 // model plus per-resource op lists and ready-bitset offsets for the event
 // simulator. Uploaded once per cs_graph (lazily) and reused by every call.
+#include <mutex>
 #include <vector>
 
 #include "common.cuh"
@@ -14,7 +15,8 @@ std::atomic<int64_t> g_launches{0};
 int ensure_device(char* err) {
   static int ok = -1;
   static char msg[256];
-  if (ok < 0) {
+  static std::once_flag once;  // first calls may come from several threads
+  std::call_once(once, [] {
     int count = 0;
     cudaError_t e = cudaGetDeviceCount(&count);
     if (e != cudaSuccess || count == 0) {
@@ -39,7 +41,7 @@ int ensure_device(char* err) {
         cudaGetLastError();
       }
     }
-  }
+  });
   if (!ok) std::snprintf(err, 256, "%s", msg);
   return ok ? 0 : 1;
 }

@@ -600,8 +600,7 @@ int group_setup(DeviceGraph* g, const int64_t* dur, GroupState& S, char* err) {
   const size_t smem = static_cast<size_t>(rw.nrows) * W * 4;
   if (rw.nrows > 0) {
     if (smem <= 200 * 1024) {
-      CK(cudaFuncSetAttribute(closure_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              static_cast<int>(std::max<size_t>(smem, 4))));
+      CK(allow_max_dynamic_smem(reinterpret_cast<const void*>(closure_smem_kernel)));
       closure_smem_kernel<<<1, 256, smem>>>(rw.nrows, W, S.d_self.as<int32_t>(),
                                             S.d_preoff.as<int32_t>(), S.d_pre.as<int32_t>(),
                                             S.d_bits.as<uint32_t>());
@@ -807,7 +806,7 @@ extern "C" int csk_tac(DeviceGraph* g, const int64_t* dur, int32_t* prio, char* 
       smem += tac_smem_col_bytes(ncol);
     }
     if (smem <= kSmemMax && !std::getenv("TICTAC_TAC_NO_SMEM")) {
-      CK(cudaFuncSetAttribute(tac_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+      CK(allow_max_dynamic_smem(reinterpret_cast<const void*>(tac_smem_kernel)));
       void* args[] = {&a, &nrows, &nsucc, &ncol};
       // a block sized to the per-round work: idle warps only lengthen barriers
       int threads = R <= 512 ? 512 : 1024;

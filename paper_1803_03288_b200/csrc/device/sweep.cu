@@ -500,9 +500,8 @@ extern "C" SweepPlan* csk_sweep_plan(int32_t W, int32_t R, int32_t nc, const int
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const void* fn = reinterpret_cast<const void*>(sweep_fn(p));
-  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(p->smem));
-  cudaFuncSetAttribute(reinterpret_cast<const void*>(chain_sweep_kernel<uint8_t, true, int64_t>),
-                       cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(p->smem_orders));
+  allow_max_dynamic_smem(fn);
+  allow_max_dynamic_smem(reinterpret_cast<const void*>(chain_sweep_kernel<uint8_t, true, int64_t>));
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kSweepThreads, p->smem);
   if (occ < 1) {
     std::snprintf(err, 256, "sweep plan needs %zu bytes of shared memory per block", p->smem);
@@ -614,10 +613,10 @@ extern "C" int csk_sweep_lex(SweepPlan* p, int64_t first, int64_t count, int64_t
   const int blocks = static_cast<int>(std::min<int64_t>(sms * 8, (count + kSweepThreads - 1) / kSweepThreads));
   const auto* f = d_fact.as<const unsigned long long>();
   if (p->narrow) {
-    CK(cudaFuncSetAttribute(lex_kernel<int32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    CK(allow_max_dynamic_smem(reinterpret_cast<const void*>(lex_kernel<int32_t>)));
     lex_kernel<int32_t><<<blocks, kSweepThreads, smem>>>(a, first, count, f, d_out);
   } else {
-    CK(cudaFuncSetAttribute(lex_kernel<int64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    CK(allow_max_dynamic_smem(reinterpret_cast<const void*>(lex_kernel<int64_t>)));
     lex_kernel<int64_t><<<blocks, kSweepThreads, smem>>>(a, first, count, f, d_out);
   }
   LAUNCHED();

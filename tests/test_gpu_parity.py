@@ -315,3 +315,56 @@ def test_event_sim_backs_off_when_hbm_is_short(lib):
     g = lib.model("resnet_v2_101_training", 1)
     r = g.sweep_random(g.declared(), 1, 100000, policy(False, 0, 0.0))
     assert got == [r["count"], r["min_us"], r["argmin_seed"], r["sum_us"]]
+
+
+def test_concurrent_calls_on_shared_handles(lib):
+    """SURVEY §8b threading contract: graphs, oracles and schedules are
+    immutable, so concurrent calls on shared handles are safe. Eight threads
+    hammer the same handles (sweeps on both paths, TAC/TIC, reports, brute
+    force); every result equals the sequential one."""
+    import threading
+    g = lib.model("resnet_v2_50_inference", 1)
+    o = g.declared()
+    toy = lib.generate("chain", 7, 1, "1", 3)
+    to = toy.declared()
+    jobs = {
+        "sweep": lambda: g.sweep_random(o, 1, 1 << 16, None)["sum_us"],
+        "sweep_exact": lambda: g.sweep_random(o, 1, 4096, policy(False, 0, 0.0))["sum_us"],
+        "tac": lambda: g.tac(o).serialize(),
+        "tic": lambda: g.tic("literal").serialize(),
+        "report": lambda: g.simulate(o, g.random(9), policy(True, 9, 0.0)).json(),
+        "brute": lambda: toy.brute_force_text(to, None, 8),
+    }
+    want = {k: f() for k, f in jobs.items()}
+    errors, got = [], []
+
+    def worker(k):
+        try:
+            for name in list(jobs)[k % len(jobs):] + list(jobs)[:k % len(jobs)]:
+                got.append((name, jobs[name]()))
+        except Exception as e:  # reported below
+            errors.append(repr(e))
+
+    threads = [threading.Thread(target=worker, args=(k,)) for k in range(8)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
+    assert len(got) == 8 * len(jobs)
+    for name, v in got:
+        assert v == want[name], name
+
+
+def test_plans_with_different_shared_memory_coexist(lib):
+    """A small plan created after a large one must not shrink the large
+    one's shared-memory limit (the limit is a per-kernel attribute)."""
+    big = lib.model("resnet_v2_101_training", 1)
+    bo = big.declared()
+    want = big.sweep_random(bo, 1, 1 << 16)["sum_us"]
+    for shape in ("chain", "layered"):  # fresh, smaller plans of the same kernel instance
+        small = lib.generate(shape, 5, 1, "1", 2)
+        small.sweep_random(small.declared(), 1, 1000)
+        small.tac(small.declared())
+        assert big.sweep_random(bo, 1, 1 << 16)["sum_us"] == want
+        assert big.sweep_random(big.declared(), 1, 1 << 16)["sum_us"] == want
