@@ -61,8 +61,14 @@ def test_multiblock_tac_matches_single_block(orc):
     # "1g": one block on global-memory state; "1c": state in shared memory,
     # column lists in global (the shared-memory copy of both is the default
     # whenever they fit)
-    for blocks in ("1", "1g", "1c", "2", "3", "7", "64"):
-        env = {**os.environ, "TICTAC_TAC_BLOCKS": blocks.rstrip("gc")}
+    # "cl": one thread-block cluster (the default only where one block's
+    # shared memory cannot hold the state)
+    for blocks in ("1", "1g", "1c", "2", "3", "7", "64", "cl"):
+        env = dict(os.environ)
+        if blocks == "cl":
+            env["TICTAC_TAC_CLUSTER"] = "1"
+        else:
+            env["TICTAC_TAC_BLOCKS"] = blocks.rstrip("gc")
         if blocks == "1g":
             env["TICTAC_TAC_NO_SMEM"] = "1"
         if blocks == "1c":
@@ -70,7 +76,7 @@ def test_multiblock_tac_matches_single_block(orc):
         r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, check=True,
                            env=env)
         res[blocks] = json.loads(r.stdout.strip().splitlines()[-1])
-    assert res["1"] == res["1g"] == res["1c"] == res["2"] == res["3"] == res["7"] == res["64"]
+    assert res["1"] == res["1g"] == res["1c"] == res["2"] == res["3"] == res["7"] == res["64"] == res["cl"]
     for spec in ("layered:10000:1000", "layered:100000:10000"):
         assert res["64"][spec] == TAC_LARGE[spec]["sha256"]
 
