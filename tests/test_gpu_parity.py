@@ -368,3 +368,12 @@ def test_plans_with_different_shared_memory_coexist(lib):
         small.tac(small.declared())
         assert big.sweep_random(bo, 1, 1 << 16)["sum_us"] == want
         assert big.sweep_random(big.declared(), 1, 1 << 16)["sum_us"] == want
+
+
+def test_cluster_brute_force_matches_reference(lib, ref):
+    """cs_brute_force over a cluster graph's recvs (event replica, lexicographic
+    permutations on the device) == the reference, for several policies."""
+    for shape, layers, params, w, ps in (("chain", 2, 1, 2, 1), ("layered", 1, 2, 2, 1), ("chain", 3, 1, 2, 2)):
+        text = lib.generate(shape, layers, params, "1", 5).expand(w, ps, 1).serialize()
+        for pol in (None, policy(True, 3, 0.0), policy(True, 1, 0.5), policy(False, 2, 0.0)):
+            _both(lib, ref, text, lambda L, g: g.brute_force_text(g.declared(), pol, 8))
