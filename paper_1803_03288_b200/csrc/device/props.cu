@@ -58,12 +58,12 @@ struct DevArr {
 
 template <typename T>
 int alloc(DevArr& a, size_t count, char* err) {
-  CK(cudaMallocAsync(&a.p, sizeof(T) * (count ? count : 1), 0));
+  CK(cudaMallocAsync(&a.p, round16(sizeof(T) * (count ? count : 1)), 0));  // padded for bulk copies
   return 0;
 }
 template <typename T>
 int put(DevArr& a, const std::vector<T>& v, char* err) {
-  CK(cudaMallocAsync(&a.p, sizeof(T) * (v.empty() ? 1 : v.size()), 0));
+  CK(cudaMallocAsync(&a.p, round16(sizeof(T) * (v.empty() ? 1 : v.size())), 0));
   if (!v.empty()) CK(cudaMemcpy(a.p, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice));
   return 0;
 }
@@ -356,8 +356,10 @@ __global__ void __launch_bounds__(1024) tac_kernel(TacArgs a) {  // one block
 }
 
 // Shared-memory bytes of tac_smem_kernel's state copy.
+// (every array 16-byte aligned and padded: each is one bulk copy)
 __host__ __device__ inline size_t tac_smem_bytes(int nrows, int R, int nsucc) {
-  return 8ull * (2ull * nrows + 3ull * R) + 4ull * (2ull * nrows + 2ull * (R + 1) + nsucc) + R;
+  return 2 * round16(8ull * nrows) + 3 * round16(8ull * R) + 2 * round16(4ull * nrows) +
+         2 * round16(4ull * (R + 1)) + round16(4ull * nsucc) + round16(R);
 }
 // plus the column lists as 16-bit row ids, when they fit (ncol > 0)
 __host__ __device__ inline size_t tac_smem_col_bytes(int64_t ncol) { return (2ull * ncol + 15) & ~size_t(15); }
@@ -375,40 +377,35 @@ __global__ void __launch_bounds__(1024) tac_smem_kernel(TacArgs g, int nrows, in
   auto* col16 = reinterpret_cast<uint16_t*>(q);  // first: 16-byte aligned
   q += ncol > 0 ? tac_smem_col_bytes(ncol) : 0;
   for (int e = threadIdx.x; e < ncol; e += blockDim.x) col16[e] = static_cast<uint16_t>(g.col[e]);
-  auto take = [&q](size_t bytes) {
+  // Every array arrives by one bulk copy on the TMA engine (device
+  // allocations are padded to 16 bytes, DevArr), all on one mbarrier.
+  __shared__ uint64_t staged;
+  if (threadIdx.x == 0) mbar_init(&staged, 1);
+  __syncthreads();
+  uint32_t total = 0;
+  auto take = [&](const void* src, size_t bytes) {
     char* p = q;
-    q += bytes;
+    const uint32_t b = static_cast<uint32_t>(round16(bytes));
+    q += b;
+    if (threadIdx.x == 0 && b > 0) bulk_g2s(p, src, b, &staged);
+    total += b;
     return p;
   };
-  auto* M = reinterpret_cast<int64_t*>(take(8ull * nrows));
-  auto* wsum = reinterpret_cast<unsigned long long*>(take(8ull * nrows));
-  auto* P = reinterpret_cast<int64_t*>(take(8ull * R));
-  auto* mp = reinterpret_cast<int64_t*>(take(8ull * R));
-  auto* tcol = reinterpret_cast<int64_t*>(take(8ull * R));
-  auto* cnt = reinterpret_cast<int32_t*>(take(4ull * nrows));
-  auto* xr = reinterpret_cast<int32_t*>(take(4ull * nrows));
-  auto* succ_off = reinterpret_cast<int32_t*>(take(4ull * (R + 1)));
-  auto* col_off = reinterpret_cast<int32_t*>(take(4ull * (R + 1)));
-  auto* succ = reinterpret_cast<int32_t*>(take(4ull * nsucc));
-  auto* out = reinterpret_cast<uint8_t*>(take(R));
-  for (int k = threadIdx.x; k < nrows; k += blockDim.x) {
-    M[k] = g.M[k];
-    wsum[k] = g.wsum[k];
-    cnt[k] = g.cnt[k];
-    xr[k] = g.xr[k];
-  }
-  for (int c = threadIdx.x; c < R; c += blockDim.x) {
-    P[c] = g.P[c];
-    mp[c] = g.mp[c];
-    tcol[c] = g.tcol[c];
-    out[c] = g.out[c];
-  }
-  for (int c = threadIdx.x; c <= R; c += blockDim.x) {
-    succ_off[c] = g.succ_off[c];
-    col_off[c] = g.col_off[c];
-  }
-  for (int e = threadIdx.x; e < nsucc; e += blockDim.x) succ[e] = g.succ[e];
-  init_red(red);  // also the barrier after the copies
+  if (threadIdx.x == 0) mbar_expect_tx(&staged, static_cast<uint32_t>(tac_smem_bytes(nrows, R, nsucc)));
+  auto* M = reinterpret_cast<int64_t*>(take(g.M, 8ull * nrows));
+  auto* wsum = reinterpret_cast<unsigned long long*>(take(g.wsum, 8ull * nrows));
+  auto* P = reinterpret_cast<int64_t*>(take(g.P, 8ull * R));
+  auto* mp = reinterpret_cast<int64_t*>(take(g.mp, 8ull * R));
+  auto* tcol = reinterpret_cast<int64_t*>(take(g.tcol, 8ull * R));
+  auto* cnt = reinterpret_cast<int32_t*>(take(g.cnt, 4ull * nrows));
+  auto* xr = reinterpret_cast<int32_t*>(take(g.xr, 4ull * nrows));
+  auto* succ_off = reinterpret_cast<int32_t*>(take(g.succ_off, 4ull * (R + 1)));
+  auto* col_off = reinterpret_cast<int32_t*>(take(g.col_off, 4ull * (R + 1)));
+  auto* succ = reinterpret_cast<int32_t*>(take(g.succ, 4ull * nsucc));
+  auto* out = reinterpret_cast<uint8_t*>(take(g.out, R));
+  (void)total;
+  mbar_wait(&staged, 0);
+  init_red(red);  // also the barrier after the column-list conversion
   TacArgs a = g;
   a.tcol = tcol;
   a.succ_off = succ_off;

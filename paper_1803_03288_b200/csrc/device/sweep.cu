@@ -23,6 +23,7 @@
 // laid out [k/4][thread] so every lane always hits its own bank.
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 #include <cub/cub.cuh>
 #include <iterator>
 #include <vector>
@@ -52,6 +53,9 @@ struct ChainArgs {
   int do_e;
   int key_bits;           // statistics keys: (m << key_bits) | offset
   int force_slow;         // test knob: every shuffle through the generic engine
+  const void* blob;       // table image in the kernel's shared-memory layout (bulk-copied), or null
+  uint32_t blob_bytes;
+  uint32_t mbar_off;      // byte offset of the copy's mbarrier in dynamic shared memory
   const int32_t* orders;  // explicit orders mode (W == 1)
   int64_t* makespans;
   int64_t* worker_ms;
@@ -236,11 +240,16 @@ __device__ __forceinline__ void shuffle_fold(uint64_t seed, int R, const Items<T
 }
 
 // Shared-memory layout of one block (bytes); hist bins only when used.
+// Table image at the start of a block's shared memory: bounded() limits and
+// magics (R+2 each), the {first class, duration} table, the class suffix
+// weights in the fold's width V; 16-byte padded so one bulk copy moves it.
+__host__ __device__ inline size_t sweep_table_bytes(int R, int W, int stride, size_t vbytes) {
+  return round16(16 * static_cast<size_t>(R + 2) + 8 * static_cast<size_t>(W) * R + vbytes * W * stride);
+}
 __host__ __device__ inline size_t sweep_smem(int R, int W, int stride, int nhist, size_t vbytes) {
   const int per_word = R <= 256 ? 4 : 2;
-  return 16 * static_cast<size_t>(R + 2) + 8 * static_cast<size_t>(W) * R +
-         ((vbytes * W * stride + 7) & ~size_t(7)) + 4 * static_cast<size_t>(nhist) * kBins +
-         4 * static_cast<size_t>(kSweepThreads) * ((R + per_word - 1) / per_word + 1);
+  return sweep_table_bytes(R, W, stride, vbytes) + 4 * static_cast<size_t>(nhist) * kBins +
+         4 * static_cast<size_t>(kSweepThreads) * ((R + per_word - 1) / per_word + 1) + 16;  // + mbarrier
 }
 
 template <typename T, bool kOrders, typename V>
@@ -251,18 +260,29 @@ __global__ void __launch_bounds__(kSweepThreads, 3) chain_sweep_kernel(ChainArgs
   uint64_t* s_mag = s_lim + (R + 2);
   uint2* s_tab = reinterpret_cast<uint2*>(s_mag + (R + 2));
   V* s_pw = reinterpret_cast<V*>(s_tab + W * R);
-  const size_t pw_bytes = (sizeof(V) * W * a.stride + 7) & ~size_t(7);
-  int* s_hist = reinterpret_cast<int*>(reinterpret_cast<unsigned char*>(s_pw) + pw_bytes);
+  int* s_hist = reinterpret_cast<int*>(smem + sweep_table_bytes(R, W, a.stride, sizeof(V)));
   const int nhist = (a.do_e ? 1 : 0) + (a.cluster ? 1 : 0);
   int* s_shist = s_hist + (a.do_e ? kBins : 0);  // straggler bins (clusters)
   uint32_t* s_items = reinterpret_cast<uint32_t*>(s_hist + nhist * kBins);
-  for (int k = threadIdx.x; k < R + 2; k += blockDim.x) {
-    s_lim[k] = a.lim[k];
-    s_mag[k] = a.mag[k];
+  // mbarrier in the last 16 bytes of the dynamic region (sweep_smem)
+  uint64_t* tables_ready = reinterpret_cast<uint64_t*>(smem + a.mbar_off);
+  if (a.blob) {  // the whole table image in one bulk copy on the TMA engine
+    if (threadIdx.x == 0) mbar_init(tables_ready, 1);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      mbar_expect_tx(tables_ready, a.blob_bytes);
+      bulk_g2s(smem, a.blob, a.blob_bytes, tables_ready);
+    }
+  } else {
+    for (int k = threadIdx.x; k < R + 2; k += blockDim.x) {
+      s_lim[k] = a.lim[k];
+      s_mag[k] = a.mag[k];
+    }
+    for (int k = threadIdx.x; k < W * R; k += blockDim.x) s_tab[k] = a.tab[k];
+    for (int k = threadIdx.x; k < W * a.stride; k += blockDim.x) s_pw[k] = static_cast<V>(a.pwsuf[k]);
   }
-  for (int k = threadIdx.x; k < W * R; k += blockDim.x) s_tab[k] = a.tab[k];
-  for (int k = threadIdx.x; k < W * a.stride; k += blockDim.x) s_pw[k] = static_cast<V>(a.pwsuf[k]);
   for (int k = threadIdx.x; k < nhist * kBins; k += blockDim.x) s_hist[k] = 0;
+  if (a.blob) mbar_wait(tables_ready, 0);
   __syncthreads();
   const Items<T> items{s_items + threadIdx.x};
 
@@ -443,6 +463,8 @@ struct SweepPlan {
   int W = 1, R = 0, nc = 0, cluster = 0, stride = 1, narrow = 0;
   int64_t U = 0, L = 0;
   void *tab = nullptr, *pwsuf = nullptr, *ctot = nullptr, *send = nullptr, *lim = nullptr, *mag = nullptr;
+  void* blob = nullptr;  // shared-memory table image of the sweep kernels
+  size_t blob_bytes = 0;
   size_t smem = 0, smem_orders = 0;
   int blocks = 0;
 };
@@ -493,6 +515,29 @@ extern "C" SweepPlan* csk_sweep_plan(int32_t W, int32_t R, int32_t nc, const int
   }
   // 32-bit fold when every prefix/suffix time sum fits (U bounds them all)
   p->narrow = U < (int64_t{1} << 31) ? 1 : 0;
+  {  // the sweep kernels' shared-memory table image, built once per plan
+    const size_t vb = p->narrow ? 4 : 8;
+    p->blob_bytes = sweep_table_bytes(R, W, p->stride, vb);
+    std::vector<unsigned char> img(p->blob_bytes, 0);
+    unsigned char* q = img.data();
+    std::memcpy(q, lim.data(), 8ull * (R + 2));
+    std::memcpy(q + 8ull * (R + 2), mag.data(), 8ull * (R + 2));
+    std::memcpy(q + 16ull * (R + 2), tab.data(), 8ull * W * R);
+    unsigned char* pwq = q + 16ull * (R + 2) + 8ull * W * R;
+    for (int k = 0; k < W * p->stride; ++k) {
+      if (p->narrow) {
+        const int32_t v = static_cast<int32_t>(pwsuf[k]);
+        std::memcpy(pwq + 4ull * k, &v, 4);
+      } else {
+        std::memcpy(pwq + 8ull * k, &pwsuf[k], 8);
+      }
+    }
+    if (!up(&p->blob, img.data(), img.size())) {
+      std::snprintf(err, 256, "CUDA allocation for the sweep plan failed");
+      csk_sweep_plan_free(p);
+      return nullptr;
+    }
+  }
   const int nhist = (!cluster && U != L ? 1 : 0) + (cluster ? 1 : 0);
   p->smem = sweep_smem(R, W, p->stride, nhist, p->narrow ? 4 : 8);
   p->smem_orders = sweep_smem(R, W, p->stride, nhist, 8);
@@ -514,7 +559,7 @@ extern "C" SweepPlan* csk_sweep_plan(int32_t W, int32_t R, int32_t nc, const int
 
 extern "C" void csk_sweep_plan_free(SweepPlan* p) {
   if (!p) return;
-  void* ptrs[] = {p->tab, p->pwsuf, p->ctot, p->send, p->lim, p->mag};
+  void* ptrs[] = {p->tab, p->pwsuf, p->ctot, p->send, p->lim, p->mag, p->blob};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   delete p;
@@ -546,6 +591,8 @@ static ChainArgs chain_args(SweepPlan* p) {
   a.do_e = !p->cluster && p->U != p->L;
   a.key_bits = csk_key_bits(p->U);
   a.force_slow = std::getenv("TICTAC_SWEEP_FORCE_SLOW") != nullptr;
+  a.blob = nullptr;  // per-element staging unless the caller's kernel matches the image
+  a.blob_bytes = 0;
   return a;
 }
 
@@ -561,6 +608,11 @@ extern "C" int csk_sweep_run(SweepPlan* p, uint64_t seed_lo, int64_t count, uint
   a.worker_ms = d_worker_makespans;
   a.i64 = reinterpret_cast<unsigned long long*>(d_i64);
   a.f64 = d_f64;
+  if (!std::getenv("TICTAC_SWEEP_NO_BULK")) {  // sweep_fn(p) folds in the image's width
+    a.blob = p->blob;
+    a.blob_bytes = static_cast<uint32_t>(p->blob_bytes);
+    a.mbar_off = static_cast<uint32_t>(p->smem - 16);
+  }
   const int64_t need = (count + kSweepThreads - 1) / kSweepThreads;
   const int blocks = static_cast<int>(std::min<int64_t>(p->blocks, need));
   auto st = static_cast<cudaStream_t>(stream);
