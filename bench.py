@@ -569,6 +569,20 @@ def main():
                                    "time from this run's CUDA events, peak = 148 SMs x 4 schedulers x SM clock"}
             except Exception:
                 traffic = None
+        # SURVEY §8d's secondary roofline: B_sim per ordering against shared
+        # memory bandwidth (148 SMs x 128 B/clk x SM clock under load)
+        mhz = clocks_summary.get("sm_mhz") or 1965.0
+        smem_peak = 148 * 128 * mhz * 1e6 / 1e9
+        smem_roof = {"bound": "smem", "achieved": achieved, "peak": smem_peak, "unit": "GB/s",
+                     "frac": achieved / smem_peak, "algorithmic_bytes_per_order": bsim,
+                     "note": "SURVEY §8d secondary: B_sim x orderings/s against 148 x 128 B/clk x SM clock; "
+                             "the kernel's measured shared-memory traffic is lower (ncu smem wavefronts "
+                             "in profiles/sweep_ncu_summary.json), its binding limit is issue (roofline_issue)"}
+        try:
+            smem_roof["ncu_smem_wavefronts_pct"] = json.load(
+                open(os.path.join(ROOT, "profiles", "sweep_ncu_summary.json")))["smem_wavefronts_pct"]
+        except Exception:
+            pass
         out = {
             "metric": "recv-order makespan sims/sec", "value": value, "unit": "sims/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
@@ -600,6 +614,7 @@ def main():
                        "count_checked": int(stats["count"])},
             "clocks": clocks_summary,
             "roofline_issue": issue,
+            "roofline_smem": smem_roof,
         }
         if not args.no_tac:
             out["tac_seconds"], out["tac_roofline"], out["tic_amended_seconds"] = tac_times(
