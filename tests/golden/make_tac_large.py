@@ -6,6 +6,7 @@ and the reference library on every graph the reference can finish. Stored
 as SHA-256 of the priorities JSON (schedule serialisation order).
 
     python tests/golden/make_tac_large.py [--top]
+    python tests/golden/make_tac_large.py --tic   # TIC digests, every config-5 size
 
 (--top, 10^6 ops / 10^5 recvs, takes hours with this oracle's row-major
 retire loop and is not committed; the multi-block TAC kernel that runs there
@@ -33,6 +34,21 @@ def main():
     path = os.path.join(HERE, "tac_large.json")
     out = json.load(open(path)) if os.path.exists(path) else {}
     lib = Lib()
+    if "--tic" in sys.argv:  # TIC (both modes) at every config-5 size, the top included
+        for spec in ["layered:10000:1000", "layered:100000:10000", "layered:1000000:100000"]:
+            t = time.time()
+            g = lib.model(spec, 1)
+            og = oracle.OracleGraph(json.loads(g.serialize()))
+            for mode in ("amended", "literal"):
+                prio, total = og.tic(mode)
+                text = json.dumps(prio, sort_keys=True)
+                out[f"tic:{mode}:{spec}"] = {"sha256": hashlib.sha256(text.encode()).hexdigest(),
+                                             "recvs": len(prio), "total_order": bool(total),
+                                             "oracle_seconds": round(time.time() - t, 1)}
+                print(spec, mode, out[f"tic:{mode}:{spec}"], flush=True)
+        with open(path, "w") as f:
+            json.dump(out, f, indent=1, sort_keys=True)
+        return
     for spec in specs:
         t = time.time()
         g = lib.model(spec, 1)
