@@ -377,3 +377,23 @@ def test_cluster_brute_force_matches_reference(lib, ref):
         text = lib.generate(shape, layers, params, "1", 5).expand(w, ps, 1).serialize()
         for pol in (None, policy(True, 3, 0.0), policy(True, 1, 0.5), policy(False, 2, 0.0)):
             _both(lib, ref, text, lambda L, g: g.brute_force_text(g.declared(), pol, 8))
+
+
+def test_config3_cluster_schedules_and_reports_match_reference(lib, ref):
+    """Config 3 (VGG-16-shaped DAG, 4 workers / 1 PS): TIC (both modes), TAC,
+    random schedules (per-worker derived seeds), and the cluster report /
+    iteration statistics, byte for byte against the reference."""
+    text = lib.model("vgg16_training", 1).expand(4, 1, 0).serialize()
+    for mode in ("amended", "literal"):
+        _both(lib, ref, text, lambda L, g: g.tic(mode).serialize())
+    _both(lib, ref, text, lambda L, g: g.tac(g.declared()).serialize())
+    for seed in (1, 99):
+        _both(lib, ref, text, lambda L, g: g.random(seed).serialize())
+
+    def rep(L, g, algo):
+        o = g.declared()
+        s = {"tic": g.tic(), "tac": g.tac(o), "random": g.random(5)}[algo]
+        r = g.simulate(o, s, policy(True, 5, 0.0))
+        return r.iteration_json() + g.metrics_text(o, r) + str(r.makespan())
+    for algo in ("tic", "tac", "random"):
+        _both(lib, ref, text, lambda L, g: rep(L, g, algo))
