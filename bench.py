@@ -619,6 +619,10 @@ def main():
         if not args.no_tac:
             out["tac_seconds"], out["tac_roofline"], out["tic_amended_seconds"] = tac_times(
                 lib, top=args.config5_top, hbm=hbm)
+            if world > 1:
+                out["tac_note"] = ("TAC is R dependent rounds and runs on one GPU (rank 0) at any N: a "
+                                   "sharded round would add an all-reduce (~1.25 us grid-sync class latency "
+                                   "per round or more over NVLink) to rounds of 1.3-8 us; DESIGN.md section 5")
         if not args.no_configs and world == 1:
             out["configs"] = other_configs(lib)
             out["configs"]["event_replica_config4_noise"] = event_replica(lib, path)
