@@ -397,3 +397,33 @@ def test_config3_cluster_schedules_and_reports_match_reference(lib, ref):
         return r.iteration_json() + g.metrics_text(o, r) + str(r.makespan())
     for algo in ("tic", "tac", "random"):
         _both(lib, ref, text, lambda L, g: rep(L, g, algo))
+
+
+@pytest.mark.parametrize("scale", [10**5, 10**7])
+def test_sweep_with_huge_durations_matches_reference(lib, ref, scale):
+    """Durations scaled so U >= 2^31 (the sweep's 64-bit fold) and U >= 2^37
+    (outside the closed form's key range: the exact event replica) — sweep
+    makespans and statistics equal the reference's per-seed loop."""
+    base = json.loads(lib.model("resnet_v2_50_inference", 1).serialize())
+    for op in base["ops"]:
+        op["time_us"] = op["time_us"] * scale
+        op.pop("bytes", None)
+    text = json.dumps(base)
+    g = lib.graph(text)
+    o = g.declared()
+    from paper_1803_03288_b200.capi import SweepPlan
+    U, _ = g.bounds(o)
+    if scale == 10**5:  # closed form with the 64-bit fold
+        assert (1 << 31) <= U < (1 << 37)
+        SweepPlan.create(g, o)
+    else:  # beyond the closed form's key range: exact replica
+        assert U >= (1 << 37)
+        with pytest.raises(CsError):
+            SweepPlan.create(g, o)
+    res = g.sweep_random(o, 1, 200, None, makespans=True)
+    rg = ref.graph(text)
+    ro = rg.declared()
+    want = np.array([rg.simulate(ro, rg.random(s), policy(True, s, 0.0)).makespan() for s in range(1, 201)])
+    assert np.array_equal(res["makespans"], want)
+    assert res["min_us"] == want.min() and res["argmin_seed"] == 1 + int(np.argmin(want))
+    assert res["sum_us"] == want.sum()
