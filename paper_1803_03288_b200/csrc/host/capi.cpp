@@ -108,6 +108,22 @@ std::shared_ptr<SweepCtx> cached_sweep(const cs_graph* g, const cs_oracle* o, co
   return ctx;
 }
 
+// Per-call device buffer from the stream-ordered pool (legacy stream, like
+// the kernels these calls launch); freed on every exit path.
+struct DevPtr {
+  void* p = nullptr;
+  DevPtr() = default;
+  DevPtr(const DevPtr&) = delete;
+  DevPtr& operator=(const DevPtr&) = delete;
+  ~DevPtr() {
+    if (p) cudaFreeAsync(p, 0);
+  }
+  template <typename T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
 Policy policy_of(const cs_sim_policy* p) {  // capi.cpp:64-73 defaults
   Policy q;
   if (p) {
@@ -521,19 +537,20 @@ int cs_sweep_random(const cs_graph* g, const cs_oracle* o, uint64_t seed_lo, int
     auto cudacheck = [&](cudaError_t e) {
       if (e != cudaSuccess) fail(kInternal, std::string("CUDA error: ") + cudaGetErrorString(e));
     };
-    int64_t *d_i64 = nullptr, *d_ms = nullptr, *d_wms = nullptr;
-    double* d_f64 = nullptr;
+    DevPtr b_i64, b_f64, b_ms, b_wms;
     const int64_t W = ctx->cluster ? static_cast<int64_t>(ctx->workers.size()) : 1;
     const int64_t chunk = int64_t{1} << 26;
-    cudacheck(cudaMalloc(&d_i64, 8 * CS_DSTATS_I64));
-    cudacheck(cudaMalloc(&d_f64, 8 * CS_DSTATS_F64));
+    cudacheck(cudaMallocAsync(&b_i64.p, 8 * CS_DSTATS_I64, 0));
+    cudacheck(cudaMallocAsync(&b_f64.p, 8 * CS_DSTATS_F64, 0));
     const int64_t cap = std::min(count, chunk);
-    if (makespans_out) cudacheck(cudaMalloc(&d_ms, 8 * std::max<int64_t>(cap, 1)));
+    if (makespans_out) cudacheck(cudaMallocAsync(&b_ms.p, 8 * std::max<int64_t>(cap, 1), 0));
     if (worker_makespans_out && ctx->cluster)
-      cudacheck(cudaMalloc(&d_wms, 8 * std::max<int64_t>(cap * W, 1)));
+      cudacheck(cudaMallocAsync(&b_wms.p, 8 * std::max<int64_t>(cap * W, 1), 0));
+    int64_t *d_i64 = b_i64.as<int64_t>(), *d_ms = b_ms.as<int64_t>(), *d_wms = b_wms.as<int64_t>();
+    double* d_f64 = b_f64.as<double>();
     cs_sweep_stats total{};
     bool first = true;
-    try {
+    {
       for (int64_t base = 0; base < count || (first && count == 0); base += chunk) {
         const int64_t n = std::min(chunk, count - base);
         if (csk_sweep_reset(ctx->plan, nullptr, d_i64, d_f64, err)) fail(kInternal, err);
@@ -566,17 +583,7 @@ int cs_sweep_random(const cs_graph* g, const cs_oracle* o, uint64_t seed_lo, int
         first = false;
         if (count == 0) break;
       }
-    } catch (...) {
-      cudaFree(d_i64);
-      cudaFree(d_f64);
-      cudaFree(d_ms);
-      cudaFree(d_wms);
-      throw;
     }
-    cudaFree(d_i64);
-    cudaFree(d_f64);
-    cudaFree(d_ms);
-    cudaFree(d_wms);
     if (stats_out) *stats_out = total;
   });
 }
@@ -597,21 +604,16 @@ int cs_simulate_orders(const cs_graph* g, const cs_oracle* o, const int32_t* ord
     auto ctx = make_sweep(g->g, o->o, p);
     if (n == 0) return;
     if (ctx->fast && !ctx->cluster) {
-      int32_t* d_o = nullptr;
-      int64_t* d_m = nullptr;
       auto cudacheck = [&](cudaError_t e) {
         if (e != cudaSuccess) fail(kInternal, std::string("CUDA error: ") + cudaGetErrorString(e));
       };
-      cudacheck(cudaMalloc(&d_o, 4 * n * R + 4));
-      cudacheck(cudaMalloc(&d_m, 8 * n));
-      cudacheck(cudaMemcpy(d_o, orders, 4 * n * R, cudaMemcpyHostToDevice));
+      DevPtr b_o, b_m;
+      cudacheck(cudaMallocAsync(&b_o.p, 4 * n * R + 4, 0));
+      cudacheck(cudaMallocAsync(&b_m.p, 8 * n, 0));
+      cudacheck(cudaMemcpy(b_o.p, orders, 4 * n * R, cudaMemcpyHostToDevice));
       char err[256] = {0};
-      const int rc = csk_sweep_orders(ctx->plan, d_o, n, nullptr, d_m, err);
-      cudaError_t e = cudaMemcpy(makespans_out, d_m, 8 * n, cudaMemcpyDeviceToHost);
-      cudaFree(d_o);
-      cudaFree(d_m);
-      if (rc) fail(kInternal, err);
-      cudacheck(e);
+      if (csk_sweep_orders(ctx->plan, b_o.as<int32_t>(), n, nullptr, b_m.as<int64_t>(), err)) fail(kInternal, err);
+      cudacheck(cudaMemcpy(makespans_out, b_m.p, 8 * n, cudaMemcpyDeviceToHost));
       if (violations_out)
         for (int64_t k = 0; k < n; ++k) violations_out[k] = 0;  // gated, noiseless, roots
       return;
