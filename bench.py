@@ -621,8 +621,8 @@ def main():
                 lib, top=args.config5_top, hbm=hbm)
             if world > 1:
                 out["tac_note"] = ("TAC is R dependent rounds and runs on one GPU (rank 0) at any N: a "
-                                   "sharded round would add an all-reduce (~1.25 us grid-sync class latency "
-                                   "per round or more over NVLink) to rounds of 1.3-8 us; DESIGN.md section 5")
+                                   "sharded round would add an NCCL all-reduce (16-29 us measured over NVLink, "
+                                   "tools/allreduce_latency.py) to rounds of 1.3-8 us; DESIGN.md section 5")
         if not args.no_configs and world == 1:
             out["configs"] = other_configs(lib)
             out["configs"]["event_replica_config4_noise"] = event_replica(lib, path)
