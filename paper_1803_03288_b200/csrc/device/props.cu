@@ -495,7 +495,10 @@ __global__ void __launch_bounds__(1024) tac_dist_kernel(TacArgs a, int* ring) {
 // step starting from the lowest outstanding column, which every thread
 // tracks identically) plus the retire: chain length + 1 grid barriers.
 template <int kOwn>
-__global__ void __launch_bounds__(1024) tac_own_kernel(TacArgs a, int* ring) {
+__global__ void __launch_bounds__(1024) tac_own_kernel(TacArgs a, int* ring, longlong4* win) {
+  // win[slot][block]: {P, T, M+} of the block's winning candidate of a
+  // find-first step, written before the step's grid barrier, so the next
+  // step reads the new incumbent with one load instead of a dependent chain
   cg::grid_group grid = cg::this_grid();
   __shared__ int red[3];
   int sp = 0;
@@ -530,18 +533,37 @@ __global__ void __launch_bounds__(1024) tac_own_kernel(TacArgs a, int* ring) {
       mp_own[k] = live[k] ? mplus(s0[k], s1[k]) : kInf;
     }
     int best = first;
+    int64_t bp = a.P[best], bm = a.tcol[best], bmp = mplus(a.succ_off[best], a.succ_off[best + 1]);
     for (;;) {
-      const int64_t bp = a.P[best], bm = a.tcol[best], bmp = mplus(a.succ_off[best], a.succ_off[best + 1]);
       int nxt = 0x7fffffff;
+      int64_t np = 0, nt = 0, nm = 0;
 #pragma unroll
       for (int k = 0; k < kOwn; ++k) {
         const int c = tid + k * nthreads;
-        if (live[k] && c > best && c < nxt && precedes(c, P_own[k], t_own[k], mp_own[k], best, bp, bm, bmp))
+        if (live[k] && c > best && c < nxt && precedes(c, P_own[k], t_own[k], mp_own[k], best, bp, bm, bmp)) {
           nxt = c;
+          np = P_own[k];
+          nt = t_own[k];
+          nm = mp_own[k];
+        }
       }
-      nxt = grid_min_step(nxt, ring, p, red, sp, grid);
+      // grid-wide min (grid_min_step, inlined to publish the block winner)
+      const int slot = p % 3;
+      const int v = block_min_int(nxt, red, sp);
+      if (nxt == v && v != 0x7fffffff) {
+        win[slot * gridDim.x + blockIdx.x] = make_longlong4(np, nt, nm, 0);
+        atomicMin(&ring[slot], v);
+      }
+      if (blockIdx.x == 0 && threadIdx.x == 0) ring[(p + 1) % 3] = 0x7fffffff;
+      grid.sync();
+      nxt = *reinterpret_cast<volatile int*>(&ring[slot]);
+      ++p;
       if (nxt == 0x7fffffff) break;
       best = nxt;
+      const longlong4 w = win[slot * gridDim.x + (nxt % nthreads) / blockDim.x];  // ordered by grid.sync
+      bp = w.x;
+      bm = w.y;
+      bmp = w.z;
     }
     const int64_t t = a.tcol[best];
     for (int64_t e = a.col_off[best] + tid; e < a.col_off[best + 1]; e += nthreads) {
@@ -980,6 +1002,10 @@ extern "C" int csk_tac(DeviceGraph* g, const int64_t* dur, int32_t* prio, char* 
     void* args[] = {&a, &rp};
     // register-resident candidates when every column has an owner slot
     const int64_t per = (R + static_cast<int64_t>(blocks) * 1024 - 1) / (static_cast<int64_t>(blocks) * 1024);
+    DevArr d_win;  // per-block winner slots of tac_own_kernel (3-slot ring)
+    if (alloc<longlong4>(d_win, 3ull * blocks, err)) return 1;
+    longlong4* wp = d_win.as<longlong4>();
+    void* args_own[] = {&a, &rp, &wp};
     void* kern = reinterpret_cast<void*>(tac_dist_kernel);
     if (!std::getenv("TICTAC_TAC_NO_OWN")) {
       if (per <= 1)
@@ -989,7 +1015,8 @@ extern "C" int csk_tac(DeviceGraph* g, const int64_t* dur, int32_t* prio, char* 
       else if (per <= 4)
         kern = reinterpret_cast<void*>(tac_own_kernel<4>);
     }
-    CK(cudaLaunchCooperativeKernel(kern, blocks, 1024, args, 0, nullptr));
+    CK(cudaLaunchCooperativeKernel(kern, blocks, 1024, kern == reinterpret_cast<void*>(tac_dist_kernel) ? args : args_own,
+                                   0, nullptr));
     LAUNCHED();
     CK(cudaGetLastError());
     CK(cudaMemcpy(prio, d_prio.p, 4ull * R, cudaMemcpyDeviceToHost));
