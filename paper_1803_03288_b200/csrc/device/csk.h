@@ -31,6 +31,11 @@ void csk_graph_free(DeviceGraph* g);
  * start/end (n each) are filled for run 0 when non-NULL; dev_end (B*n_dev)
  * gets the max event end per device when non-NULL.
  * status[b]: 0 ok, 2 stalled ("simulation stalled with no runnable op"). */
+/* One run inside SURVEY A.2's regime (worker graph, one compute unit and one
+ * channel, gated, noiseless, recvs prioritized, compute ops not), for its
+ * event list: gate_order = recv op indices sorted by (priority, id). */
+int csk_event_a2(DeviceGraph* g, const int64_t* dur, const int32_t* gate_order, int32_t R,
+                 uint64_t choice_seed, int64_t* makespan, int64_t* start, int64_t* end, char* err);
 int csk_event_sim(DeviceGraph* g, const int64_t* dur, int32_t B, const int32_t* prio,
                   const int32_t* orders, int32_t R, const uint64_t* seeds, int gated,
                   double noise, int64_t* makespan, int64_t* violations, int32_t* status,

@@ -894,6 +894,164 @@ int run_event(DeviceGraph* g, const int64_t* dur, int64_t B, RunSpec rs, int64_t
   return 0;
 }
 
+// One exact run inside SURVEY A.2's regime — worker graph with one compute
+// unit and one channel, counter gate, no noise, every recv prioritized (and
+// no compute op prioritized) — for its event list. The round structure is the
+// generic replica's (try_start compute then channel, complete compute then
+// channel, repeat while anything moved, then advance time); what the regime
+// removes is every per-resource lookup: the channel always starts the next
+// recv of the gate order (its only admitted candidate, no draw), both
+// resources' state lives in registers, and only the compute unit draws from
+// the choice stream. One thread runs the chain; the block initialises.
+constexpr int kA2Tab = 256;  // bounded() constants staged for n < kA2Tab
+
+// Shared-memory bytes of event_a2_kernel; `staged` adds copies of the graph
+// arrays the chain reads (durations, successor CSR, local indices, the unit's
+// op list, gate order) so each dependent load is a shared-memory round trip.
+__host__ __device__ inline size_t a2_smem(int n, int E, int R, int ncpu, bool staged) {
+  const size_t base = 8 * 312 + 16ull * kA2Tab + 4ull * n + 4ull * ((ncpu + 31) / 32 + 1);
+  if (!staged) return base;
+  return base + 8ull * n + 4ull * (n + 1) + 4ull * E + 4ull * n + 4ull * ncpu + 4ull * R + 16;
+}
+
+template <bool kStaged>
+__global__ void __launch_bounds__(256) event_a2_kernel(GraphView G, const int32_t* __restrict__ gate_order,
+                                                       int cpu_r, uint64_t choice_seed, const uint64_t* lim,
+                                                       const uint64_t* mag, int64_t* start, int64_t* end,
+                                                       int64_t* makespan) {
+  extern __shared__ __align__(16) char a2_sm[];
+  const int n = G.n, R = G.R;
+  const int ncpu = cpu_r >= 0 ? G.rops_off[cpu_r + 1] - G.rops_off[cpu_r] : 0;
+  const int nw = (ncpu + 31) / 32;
+  const int E = G.succ_off[n];
+  auto* mt = reinterpret_cast<uint64_t*>(a2_sm);
+  auto* s_lim = mt + 312;
+  auto* s_mag = s_lim + kA2Tab;
+  auto* missing = reinterpret_cast<int32_t*>(s_mag + kA2Tab);
+  auto* ready = reinterpret_cast<uint32_t*>(missing + n);
+  // graph arrays: shared copies when staged, else the global ones
+  const int64_t* dur = G.dur;
+  const int32_t *succ_off = G.succ_off, *succ_idx = G.succ_idx, *lidx = G.lidx, *order = gate_order;
+  const int32_t* cpu_ops = cpu_r >= 0 ? G.rops + G.rops_off[cpu_r] : nullptr;
+  if constexpr (kStaged) {
+    char* q = reinterpret_cast<char*>(ready + nw + 1);
+    q = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(q) + 15) & ~uintptr_t(15));
+    auto* s_dur = reinterpret_cast<int64_t*>(q);
+    auto* s_soff = reinterpret_cast<int32_t*>(s_dur + n);
+    auto* s_sidx = s_soff + n + 1;
+    auto* s_lidx = s_sidx + E;
+    auto* s_cpu = s_lidx + n;
+    auto* s_ord = s_cpu + ncpu;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      s_dur[i] = G.dur[i];
+      s_lidx[i] = G.lidx[i];
+    }
+    for (int i = threadIdx.x; i <= n; i += blockDim.x) s_soff[i] = G.succ_off[i];
+    for (int e = threadIdx.x; e < E; e += blockDim.x) s_sidx[e] = G.succ_idx[e];
+    for (int k = threadIdx.x; k < ncpu; k += blockDim.x) s_cpu[k] = cpu_ops[k];
+    for (int k = threadIdx.x; k < R; k += blockDim.x) s_ord[k] = gate_order[k];
+    dur = s_dur;
+    succ_off = s_soff;
+    succ_idx = s_sidx;
+    lidx = s_lidx;
+    cpu_ops = s_cpu;
+    order = s_ord;
+  }
+  for (int k = threadIdx.x; k < kA2Tab; k += blockDim.x) {
+    s_lim[k] = lim[k];
+    s_mag[k] = mag[k];
+  }
+  for (int w = threadIdx.x; w < nw; w += blockDim.x) ready[w] = 0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const int deg = G.pred_off[i + 1] - G.pred_off[i];
+    missing[i] = deg;
+    if (deg == 0 && G.res[i] == cpu_r) atomicOr(&ready[G.lidx[i] >> 5], 1u << (G.lidx[i] & 31));
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  MtFullP<uint64_t*> choice{mt, 0};
+  choice.seed(choice_seed);
+  // bounded(n) (rng.hpp:21-30): staged constants for small n (the ready set
+  // of a compute unit is small), the host-built table otherwise
+  auto bounded = [&](uint64_t m) -> uint64_t {
+    const bool small = m < kA2Tab;
+    const uint64_t lm = small ? s_lim[m] : lim[m], mg = small ? s_mag[m] : mag[m];
+    uint64_t v;
+    do v = choice.next();
+    while (v > lm);
+    return fastmod(v, m, mg);
+  };
+  int ready_cnt = 0, lo = 0;  // lo: no set bit below word lo
+  for (int w = 0; w < nw; ++w) ready_cnt += __popc(ready[w]);
+  int64_t t = 0, cpu_end = 0, chan_end = 0;
+  int cpu_op = -1, chan_op = -1, chan_next = 0, finished = 0;
+  auto complete = [&](int op) {
+    ++finished;
+    for (int e = succ_off[op]; e < succ_off[op + 1]; ++e) {
+      const int w = succ_idx[e];
+      if (--missing[w] == 0) {  // successors are compute ops (recvs are roots)
+        const int l = lidx[w];
+        ready[l >> 5] |= 1u << (l & 31);
+        ++ready_cnt;
+        lo = min(lo, l >> 5);
+      }
+    }
+  };
+  while (finished < n) {
+    bool progress = true;
+    while (progress) {
+      progress = false;
+      if (cpu_op < 0 && ready_cnt > 0) {  // try_start(compute): every ready op is a candidate
+        int k = ready_cnt > 1 ? static_cast<int>(bounded(static_cast<uint64_t>(ready_cnt))) : 0;
+        while (!ready[lo]) ++lo;
+        int w = lo;
+        for (;; ++w) {
+          const int c = __popc(ready[w]);
+          if (k < c) break;
+          k -= c;
+        }
+        const int bit = nth_bit(ready[w], k);
+        ready[w] &= ~(1u << bit);
+        --ready_cnt;
+        cpu_op = cpu_ops[(w << 5) + bit];
+        cpu_end = t + dur[cpu_op];
+        start[cpu_op] = t;
+        end[cpu_op] = cpu_end;
+        progress = true;
+      }
+      if (chan_op < 0 && chan_next < R) {  // try_start(channel): next in gate order
+        chan_op = order[chan_next++];
+        chan_end = t + dur[chan_op];
+        start[chan_op] = t;
+        end[chan_op] = chan_end;
+        progress = true;
+      }
+      if (cpu_op >= 0 && cpu_end == t) {  // complete_now, resource order
+        complete(cpu_op);
+        cpu_op = -1;
+        progress = true;
+      }
+      if (chan_op >= 0 && chan_end == t) {
+        complete(chan_op);
+        chan_op = -1;
+        progress = true;
+      }
+    }
+    if (finished == n) break;
+    t = min(cpu_op >= 0 ? cpu_end : INT64_MAX, chan_op >= 0 ? chan_end : INT64_MAX);
+    if (cpu_op >= 0 && cpu_end == t) {
+      complete(cpu_op);
+      cpu_op = -1;
+    }
+    if (chan_op >= 0 && chan_end == t) {
+      complete(chan_op);
+      chan_op = -1;
+    }
+  }
+  *makespan = t;  // every op has ended by the time of the last completion
+}
+
 }  // namespace
 
 }  // namespace tictac_dev
@@ -971,5 +1129,70 @@ extern "C" int csk_brute_force(DeviceGraph* g, const int64_t* dur, int32_t R, ui
     return 1;
   for (int64_t k = 0; k < perms; ++k)
     if (status[k]) makespans[k] = -1;
+  return 0;
+}
+
+extern "C" int csk_event_a2(DeviceGraph* g, const int64_t* dur, const int32_t* gate_order, int32_t R,
+                            uint64_t choice_seed, int64_t* makespan, int64_t* start, int64_t* end, char* err) {
+  if (ensure_device(err)) return 1;
+  if (R != g->R) {
+    std::snprintf(err, 256, "gate order has %d recvs, graph has %d", R, g->R);
+    return 4;
+  }
+  int cpu_r = -1;  // the compute unit: the resource of any non-recv op
+  for (int32_t i = 0; i < g->n && cpu_r < 0; ++i)
+    if (g->h_kind[i] != 1) cpu_r = g->h_res[i];
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  DevBuf d_dur, d_order, d_start, d_end, d_ms;
+  if (dev_copy(d_dur, dur, g->n, err) || dev_copy(d_order, gate_order, R, err) ||
+      dev_copy<int64_t>(d_start, nullptr, g->n, err) || dev_copy<int64_t>(d_end, nullptr, g->n, err) ||
+      dev_copy<int64_t>(d_ms, nullptr, 1, err))
+    return 1;
+  RunSpec tabs{};
+  if (bounded_tables(dev, &tabs.lim, &tabs.mag, err)) return 1;
+  GraphView G{g->n,        g->nres,     g->ndev,     g->R,        g->pred_off, g->succ_off,
+              g->succ_idx, g->res,      g->res_dev,  g->rops_off, g->rops,     g->lidx,
+              g->rb_off,   g->recv_ops, g->chan,     static_cast<int64_t*>(d_dur.p)};
+  int ncpu = 0;
+  for (int32_t i = 0; i < g->n; ++i) ncpu += g->h_res[i] == cpu_r;
+  const int E = g->h_succ_off.empty() ? 0 : g->h_succ_off.back();
+  const bool staged = a2_smem(g->n, E, R, ncpu, true) <= 220 * 1024;
+  const size_t smem = a2_smem(g->n, E, R, ncpu, staged);
+  if (smem > 220 * 1024) {
+    std::snprintf(err, 256, "graph too large for the single-report kernel");
+    return 4;
+  }
+  const void* kfn = staged ? reinterpret_cast<const void*>(event_a2_kernel<true>)
+                           : reinterpret_cast<const void*>(event_a2_kernel<false>);
+  CK(allow_max_dynamic_smem(kfn));
+  const bool trace = std::getenv("TICTAC_EVENT_TRACE") != nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  if (trace) {
+    cudaEventCreate(&ev0);
+    cudaEventCreate(&ev1);
+    cudaEventRecord(ev0);
+  }
+  auto* ordp = static_cast<int32_t*>(d_order.p);
+  auto *stp = static_cast<int64_t*>(d_start.p), *enp = static_cast<int64_t*>(d_end.p),
+       *msp = static_cast<int64_t*>(d_ms.p);
+  if (staged)
+    event_a2_kernel<true><<<1, 256, smem>>>(G, ordp, cpu_r, choice_seed, tabs.lim, tabs.mag, stp, enp, msp);
+  else
+    event_a2_kernel<false><<<1, 256, smem>>>(G, ordp, cpu_r, choice_seed, tabs.lim, tabs.mag, stp, enp, msp);
+  LAUNCHED();
+  CK(cudaGetLastError());
+  if (trace) {
+    cudaEventRecord(ev1);
+    cudaEventSynchronize(ev1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, ev0, ev1);
+    std::fprintf(stderr, "[event_a2] n=%d kernel %.3f ms\n", g->n, ms);
+    cudaEventDestroy(ev0);
+    cudaEventDestroy(ev1);
+  }
+  CK(cudaMemcpy(makespan, d_ms.p, 8, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(start, d_start.p, 8ull * g->n, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(end, d_end.p, 8ull * g->n, cudaMemcpyDeviceToHost));
   return 0;
 }

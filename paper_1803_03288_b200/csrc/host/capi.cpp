@@ -56,7 +56,17 @@ struct cs_report {
   mutable std::unique_ptr<Report> full;
   const Report& report() const {
     std::lock_guard<std::mutex> lock(mu);
-    if (!full) full = std::make_unique<Report>(simulate_prepared(*g, d, prio, pol));
+    if (!full) {
+      // Deferred reports exist only inside the closed form's regime; the
+      // specialised replica also needs the compute ops unprioritized.
+      bool compute_prio = false;
+      for (int32_t i = 0; i < g->n() && !compute_prio; ++i)
+        compute_prio = g->ops()[i].kind != kRecv && prio[i] >= 0;
+      if (compute_prio || std::getenv("TICTAC_NO_A2"))
+        full = std::make_unique<Report>(simulate_prepared(*g, d, prio, pol));
+      else
+        full = std::make_unique<Report>(simulate_a2(*g, d, prio, pol));
+    }
     return *full;
   }
 };

@@ -197,6 +197,11 @@ struct SimInputs {
 SimInputs prepare_sim(const Graph& g, const TimeOracle& o, const Schedule* s, const Policy& p);
 Report simulate_prepared(const Graph& g, const std::vector<int64_t>& d, const std::vector<int32_t>& prio,
                          const Policy& p);
+// One run inside SURVEY A.2's regime (worker graph, one compute unit and one
+// channel, gated, noiseless, every recv prioritized and no compute op): the
+// specialised device replica (csk_event_a2), same Report as simulate_prepared.
+Report simulate_a2(const Graph& g, const std::vector<int64_t>& d, const std::vector<int32_t>& prio,
+                   const Policy& p);
 std::pair<int64_t, int64_t> bounds(const Graph& g, const TimeOracle& o);  // metrics.cpp:10-22
 Json metrics_json(int64_t U, int64_t L, int64_t m, const Report* stats);
 Json brute_force(const Graph& g, const TimeOracle& o, const Policy& p, int max_recvs);

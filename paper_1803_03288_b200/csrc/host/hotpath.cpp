@@ -153,18 +153,12 @@ Report simulate(const Graph& g, const TimeOracle& o, const Schedule* s, const Po
   return simulate_prepared(g, in.d, in.prio, p);
 }
 
-Report simulate_prepared(const Graph& g, const std::vector<int64_t>& d, const std::vector<int32_t>& prio,
-                         const Policy& p) {
+namespace {
+
+// Report from per-op start/end times (events sorted by start, resource, op).
+Report make_report(const Graph& g, const std::vector<int64_t>& st, const std::vector<int64_t>& en, int64_t m,
+                   int64_t viol) {
   const int32_t n = g.n();
-  std::vector<int64_t> st(n), en(n);
-  int64_t m = 0, viol = 0;
-  int32_t status = 0;
-  const uint64_t seed = p.choice_seed;
-  char err[256] = {0};
-  check(csk_event_sim(g.device(), d.data(), 1, prio.data(), nullptr, 0, &seed, p.gated ? 1 : 0,
-                      p.noise, &m, &viol, &status, st.data(), en.data(), nullptr, err),
-        err);
-  if (status) fail(kValidation, "simulation stalled with no runnable op");
   Report r;
   r.makespan = m;
   r.violations = viol;
@@ -204,6 +198,39 @@ Report simulate_prepared(const Graph& g, const std::vector<int64_t>& d, const st
     }
   }
   return r;
+}
+
+}  // namespace
+
+Report simulate_prepared(const Graph& g, const std::vector<int64_t>& d, const std::vector<int32_t>& prio,
+                         const Policy& p) {
+  const int32_t n = g.n();
+  std::vector<int64_t> st(n), en(n);
+  int64_t m = 0, viol = 0;
+  int32_t status = 0;
+  const uint64_t seed = p.choice_seed;
+  char err[256] = {0};
+  check(csk_event_sim(g.device(), d.data(), 1, prio.data(), nullptr, 0, &seed, p.gated ? 1 : 0,
+                      p.noise, &m, &viol, &status, st.data(), en.data(), nullptr, err),
+        err);
+  if (status) fail(kValidation, "simulation stalled with no runnable op");
+  return make_report(g, st, en, m, viol);
+}
+
+Report simulate_a2(const Graph& g, const std::vector<int64_t>& d, const std::vector<int32_t>& prio,
+                   const Policy& p) {
+  // gate sequence: recvs by (priority, id) (sim.cpp:95-104); no violations
+  // in this regime (recvs complete in gate order, nothing is force-released)
+  std::vector<int32_t> order(g.recv_ops().begin(), g.recv_ops().end());
+  std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return prio[a] < prio[b]; });
+  const int32_t n = g.n();
+  std::vector<int64_t> st(n), en(n);
+  int64_t m = 0;
+  char err[256] = {0};
+  check(csk_event_a2(g.device(), d.data(), order.data(), static_cast<int32_t>(order.size()), p.choice_seed, &m,
+                     st.data(), en.data(), err),
+        err);
+  return make_report(g, st, en, m, 0);
 }
 
 std::pair<int64_t, int64_t> bounds(const Graph& g, const TimeOracle& o) {

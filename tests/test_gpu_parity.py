@@ -427,3 +427,45 @@ def test_sweep_with_huge_durations_matches_reference(lib, ref, scale):
     assert np.array_equal(res["makespans"], want)
     assert res["min_us"] == want.min() and res["argmin_seed"] == 1 + int(np.argmin(want))
     assert res["sum_us"] == want.sum()
+
+
+def _zeroed(text, seed, frac=3):
+    """Same graph with roughly every `frac`-th duration set to zero (same-round
+    completions of zero-duration recvs and computes)."""
+    import random
+    d = json.loads(text)
+    rnd = random.Random(seed)
+    for op in d["ops"]:
+        if rnd.randrange(frac) == 0:
+            op["time_us"] = 0
+            op.pop("bytes", None)
+    return json.dumps(d)
+
+
+def test_single_reports_specialised_replica(lib, ref, monkeypatch):
+    """Event lists of single runs inside the closed form's regime come from
+    the specialised two-resource replica (csk_event_a2): byte-identical to the
+    generic replica and to the reference, for TIC (with ties), TAC and random
+    schedules over many choice seeds, including graphs where a third of all
+    durations are zero."""
+    texts = [t for _, t in corpus.worker_graphs(lib)] + [lib.model("resnet_v2_50_inference", 1).serialize()]
+    texts += [_zeroed(t, k) for k, t in enumerate(texts[:6])]
+    for k, text in enumerate(texts):
+        g = lib.graph(text)
+        o = g.declared()
+        scheds = {"tic": g.tic("literal"), "tac": g.tac(o), "random": g.random(k)}
+        for name, s in scheds.items():
+            for seed in (0, 1, 2, 17, 12345):
+                pol = policy(True, seed, 0.0)
+                monkeypatch.delenv("TICTAC_NO_A2", raising=False)
+                a = g.simulate(o, s, pol)
+                fast = (a.json(), a.chrome_trace(), a.makespan(), a.violations())
+                monkeypatch.setenv("TICTAC_NO_A2", "1")
+                b = g.simulate(o, s, pol)
+                generic = (b.json(), b.chrome_trace(), b.makespan(), b.violations())
+                assert fast == generic, (k, name, seed)
+        monkeypatch.delenv("TICTAC_NO_A2", raising=False)
+        if k % 3 == 0:
+            for seed in (0, 5):
+                _both(lib, ref, text, lambda L, g: g.simulate(
+                    g.declared(), g.tic("literal"), policy(True, seed, 0.0)).json())
