@@ -414,7 +414,12 @@ int cs_report_json(const cs_report* r, char** out_json) {
   return guarded([&] {
     need(r, "report");
     need(out_json, "out_json");
-    *out_json = dup(r->report().json_text());
+    const Report& rep = r->report();
+    const auto t0 = std::chrono::steady_clock::now();
+    *out_json = dup(rep.json_text());
+    if (std::getenv("TICTAC_EVENT_TRACE"))
+      std::fprintf(stderr, "[cs_report_json] text %.3f ms\n",
+                   std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
   });
 }
 

@@ -6,6 +6,9 @@
 //   simulate    -> sim.cpp:61-256          (csk_event_sim)
 //   brute force -> metrics.cpp:37-72       (csk_brute_force)
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <set>
 
 #include "../device/csk.h"
@@ -221,6 +224,8 @@ Report simulate_a2(const Graph& g, const std::vector<int64_t>& d, const std::vec
                    const Policy& p) {
   // gate sequence: recvs by (priority, id) (sim.cpp:95-104); no violations
   // in this regime (recvs complete in gate order, nothing is force-released)
+  const bool trace = std::getenv("TICTAC_EVENT_TRACE") != nullptr;
+  const auto t0 = std::chrono::steady_clock::now();
   std::vector<int32_t> order(g.recv_ops().begin(), g.recv_ops().end());
   std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return prio[a] < prio[b]; });
   const int32_t n = g.n();
@@ -230,7 +235,13 @@ Report simulate_a2(const Graph& g, const std::vector<int64_t>& d, const std::vec
   check(csk_event_a2(g.device(), d.data(), order.data(), static_cast<int32_t>(order.size()), p.choice_seed, &m,
                      st.data(), en.data(), err),
         err);
-  return make_report(g, st, en, m, 0);
+  const auto t1 = std::chrono::steady_clock::now();
+  Report r = make_report(g, st, en, m, 0);
+  if (trace)
+    std::fprintf(stderr, "[simulate_a2] device call %.3f ms, report build %.3f ms\n",
+                 std::chrono::duration<double, std::milli>(t1 - t0).count(),
+                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t1).count());
+  return r;
 }
 
 std::pair<int64_t, int64_t> bounds(const Graph& g, const TimeOracle& o) {

@@ -1,7 +1,9 @@
 // Report / metrics JSON formatting (reference sim.cpp:305-376,
 // metrics.cpp:82-105). The numbers come from the device simulator.
 #include <algorithm>
+#include <charconv>
 #include <cstdio>
+#include <string_view>
 
 #include "core.hpp"
 
@@ -30,16 +32,25 @@ class JsonText {
     first_.back() = false;
     newline();
   }
-  void key(const std::string& k) {
+  void key(std::string_view k) {
     item();
     str(k);
     s += ": ";
   }
-  void num(int64_t v) { s += std::to_string(v); }
-  void str(const std::string& v) {
+  void num(int64_t v) {
+    char buf[24];
+    const auto res = std::to_chars(buf, buf + sizeof(buf), v);
+    s.append(buf, res.ptr);
+  }
+  void str(std::string_view v) {
     s += '"';
-    for (const char ch : v) {
-      const unsigned char c = static_cast<unsigned char>(ch);
+    // bulk-append runs that need no escaping
+    size_t run = 0;
+    for (size_t i = 0; i < v.size(); ++i) {
+      const unsigned char c = static_cast<unsigned char>(v[i]);
+      if (c > 0x1f && c != '"' && c != '\\') continue;
+      s.append(v.data() + run, i - run);
+      run = i + 1;
       switch (c) {
         case '"': s += "\\\""; break;
         case '\\': s += "\\\\"; break;
@@ -48,16 +59,14 @@ class JsonText {
         case '\n': s += "\\n"; break;
         case '\r': s += "\\r"; break;
         case '\t': s += "\\t"; break;
-        default:
-          if (c <= 0x1f) {
-            char buf[8];
-            std::snprintf(buf, sizeof(buf), "\\u%04x", c);
-            s += buf;
-          } else {
-            s += ch;
-          }
+        default: {
+          char buf[8];
+          std::snprintf(buf, sizeof(buf), "\\u%04x", c);
+          s += buf;
+        }
       }
     }
+    s.append(v.data() + run, v.size() - run);
     s += '"';
   }
 
@@ -91,21 +100,30 @@ std::string Report::json_text() const {
   }
   w.close('}');
   w.key("events");
-  w.open('[');
-  for (const Event& e : events) {
-    w.item();
-    w.open('{');
-    w.key("op");
-    w.str(op_ids[e.op]);
-    w.key("resource");
-    w.str(keys[e.res]);
-    w.key("start_us");
-    w.num(e.start);
-    w.key("end_us");
-    w.num(e.end);
-    w.close('}');
+  if (events.empty()) {
+    w.s += "[]";
+  } else {  // fixed per-event layout (depths 2 and 3), fragments appended directly
+    std::vector<std::string> qres(resources.size());
+    for (size_t r = 0; r < resources.size(); ++r) {
+      JsonText q;
+      q.str(keys[r]);
+      qres[r] = std::move(q.s);
+    }
+    w.s += '[';
+    for (size_t i = 0; i < events.size(); ++i) {
+      const Event& e = events[i];
+      w.s += i ? ",\n    {\n      \"op\": " : "\n    {\n      \"op\": ";
+      w.str(op_ids[e.op]);
+      w.s += ",\n      \"resource\": ";
+      w.s += qres[e.res];
+      w.s += ",\n      \"start_us\": ";
+      w.num(e.start);
+      w.s += ",\n      \"end_us\": ";
+      w.num(e.end);
+      w.s += "\n    }";
+    }
+    w.s += "\n  ]";
   }
-  w.close(']');
   w.close('}');
   w.s += '\n';
   return std::move(w.s);
@@ -158,24 +176,20 @@ std::string Report::chrome_trace_text() const {
     w.close('}');
     w.close('}');
   }
-  for (const Event& e : events) {
+  for (const Event& e : events) {  // fixed layout: fragments appended directly
     w.item();
-    w.open('{');
-    w.key("name");
+    w.s += "{\n      \"name\": ";
     w.str(op_ids[e.op]);
-    w.key("cat");
-    w.str(resources[e.res].channel ? "channel" : "compute");
-    w.key("ph");
-    w.str("X");
-    w.key("pid");
+    w.s += resources[e.res].channel ? ",\n      \"cat\": \"channel\",\n      \"ph\": \"X\",\n      \"pid\": "
+                                    : ",\n      \"cat\": \"compute\",\n      \"ph\": \"X\",\n      \"pid\": ";
     w.num(pid[e.res]);
-    w.key("tid");
+    w.s += ",\n      \"tid\": ";
     w.num(e.res);
-    w.key("ts");
+    w.s += ",\n      \"ts\": ";
     w.num(e.start);
-    w.key("dur");
+    w.s += ",\n      \"dur\": ";
     w.num(e.end - e.start);
-    w.close('}');
+    w.s += "\n    }";
   }
   w.close(']');
   w.close('}');
