@@ -914,7 +914,7 @@ __host__ __device__ inline size_t a2_smem(int n, int E, int R, int ncpu, bool st
   return base + 8ull * n + 4ull * (n + 1) + 4ull * E + 4ull * n + 4ull * ncpu + 4ull * R + 16;
 }
 
-template <bool kStaged>
+template <bool kStaged, typename Tm>
 __global__ void __launch_bounds__(256) event_a2_kernel(GraphView G, const int32_t* __restrict__ gate_order,
                                                        int cpu_r, uint64_t choice_seed, const uint64_t* lim,
                                                        const uint64_t* mag, int64_t* start, int64_t* end,
@@ -929,21 +929,22 @@ __global__ void __launch_bounds__(256) event_a2_kernel(GraphView G, const int32_
   auto* s_mag = s_lim + kA2Tab;
   auto* missing = reinterpret_cast<int32_t*>(s_mag + kA2Tab);
   auto* ready = reinterpret_cast<uint32_t*>(missing + n);
-  // graph arrays: shared copies when staged, else the global ones
-  const int64_t* dur = G.dur;
+  // graph arrays: shared copies when staged, else the global ones; times in
+  // Tm (32-bit when the host proved every time < 2^31: the staged copy)
+  const Tm* dur = reinterpret_cast<const Tm*>(G.dur);
   const int32_t *succ_off = G.succ_off, *succ_idx = G.succ_idx, *lidx = G.lidx, *order = gate_order;
   const int32_t* cpu_ops = cpu_r >= 0 ? G.rops + G.rops_off[cpu_r] : nullptr;
   if constexpr (kStaged) {
     char* q = reinterpret_cast<char*>(ready + nw + 1);
     q = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(q) + 15) & ~uintptr_t(15));
-    auto* s_dur = reinterpret_cast<int64_t*>(q);
+    auto* s_dur = reinterpret_cast<Tm*>(q);
     auto* s_soff = reinterpret_cast<int32_t*>(s_dur + n);
     auto* s_sidx = s_soff + n + 1;
     auto* s_lidx = s_sidx + E;
     auto* s_cpu = s_lidx + n;
     auto* s_ord = s_cpu + ncpu;
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
-      s_dur[i] = G.dur[i];
+      s_dur[i] = static_cast<Tm>(G.dur[i]);
       s_lidx[i] = G.lidx[i];
     }
     for (int i = threadIdx.x; i <= n; i += blockDim.x) s_soff[i] = G.succ_off[i];
@@ -984,7 +985,9 @@ __global__ void __launch_bounds__(256) event_a2_kernel(GraphView G, const int32_
   };
   int ready_cnt = 0, lo = 0;  // lo: no set bit below word lo
   for (int w = 0; w < nw; ++w) ready_cnt += __popc(ready[w]);
-  int64_t t = 0, cpu_end = 0, chan_end = 0;
+  static_assert(kStaged || sizeof(Tm) == 8, "32-bit times need the staged copy");
+  constexpr Tm kNever = sizeof(Tm) == 8 ? static_cast<Tm>(INT64_MAX) : static_cast<Tm>(INT32_MAX);
+  Tm t = 0, cpu_end = 0, chan_end = 0;
   int cpu_op = -1, chan_op = -1, chan_next = 0, finished = 0;
   auto complete = [&](int op) {
     ++finished;
@@ -1039,7 +1042,7 @@ __global__ void __launch_bounds__(256) event_a2_kernel(GraphView G, const int32_
       }
     }
     if (finished == n) break;
-    t = min(cpu_op >= 0 ? cpu_end : INT64_MAX, chan_op >= 0 ? chan_end : INT64_MAX);
+    t = min(cpu_op >= 0 ? cpu_end : kNever, chan_op >= 0 ? chan_end : kNever);
     if (cpu_op >= 0 && cpu_end == t) {
       complete(cpu_op);
       cpu_op = -1;
@@ -1049,7 +1052,7 @@ __global__ void __launch_bounds__(256) event_a2_kernel(GraphView G, const int32_
       chan_op = -1;
     }
   }
-  *makespan = t;  // every op has ended by the time of the last completion
+  *makespan = static_cast<int64_t>(t);  // every op has ended by the time of the last completion
 }
 
 }  // namespace
@@ -1163,8 +1166,12 @@ extern "C" int csk_event_a2(DeviceGraph* g, const int64_t* dur, const int32_t* g
     std::snprintf(err, 256, "graph too large for the single-report kernel");
     return 4;
   }
-  const void* kfn = staged ? reinterpret_cast<const void*>(event_a2_kernel<true>)
-                           : reinterpret_cast<const void*>(event_a2_kernel<false>);
+  int64_t U = 0;  // every event time is at most the sum of all durations
+  for (int32_t i = 0; i < g->n; ++i) U += dur[i];
+  const bool narrow = staged && U < (int64_t{1} << 31);
+  const void* kfn = narrow   ? reinterpret_cast<const void*>(event_a2_kernel<true, int32_t>)
+                    : staged ? reinterpret_cast<const void*>(event_a2_kernel<true, int64_t>)
+                             : reinterpret_cast<const void*>(event_a2_kernel<false, int64_t>);
   CK(allow_max_dynamic_smem(kfn));
   const bool trace = std::getenv("TICTAC_EVENT_TRACE") != nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -1176,10 +1183,13 @@ extern "C" int csk_event_a2(DeviceGraph* g, const int64_t* dur, const int32_t* g
   auto* ordp = static_cast<int32_t*>(d_order.p);
   auto *stp = static_cast<int64_t*>(d_start.p), *enp = static_cast<int64_t*>(d_end.p),
        *msp = static_cast<int64_t*>(d_ms.p);
-  if (staged)
-    event_a2_kernel<true><<<1, 256, smem>>>(G, ordp, cpu_r, choice_seed, tabs.lim, tabs.mag, stp, enp, msp);
+  if (narrow)
+    event_a2_kernel<true, int32_t><<<1, 256, smem>>>(G, ordp, cpu_r, choice_seed, tabs.lim, tabs.mag, stp, enp, msp);
+  else if (staged)
+    event_a2_kernel<true, int64_t><<<1, 256, smem>>>(G, ordp, cpu_r, choice_seed, tabs.lim, tabs.mag, stp, enp, msp);
   else
-    event_a2_kernel<false><<<1, 256, smem>>>(G, ordp, cpu_r, choice_seed, tabs.lim, tabs.mag, stp, enp, msp);
+    event_a2_kernel<false, int64_t><<<1, 256, smem>>>(G, ordp, cpu_r, choice_seed, tabs.lim, tabs.mag, stp, enp,
+                                                       msp);
   LAUNCHED();
   CK(cudaGetLastError());
   if (trace) {
