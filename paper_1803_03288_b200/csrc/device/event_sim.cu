@@ -1,14 +1,24 @@
-// Exact event simulator on the GPU — a warp-cooperative replica of the
-// reference's discrete-event loop (sim.cpp:61-256), one warp per run.
+// Exact event simulator on the GPU — replicas of the reference's
+// discrete-event loop (sim.cpp:61-256) for everything outside the closed form
+// of SURVEY Appendix A.2, and for event lists.
 //
-// Per-resource ready queues are bitsets over that resource's ops (ascending
-// op index = the reference's sorted queue), so candidate selection is a
-// ballot/popc scan; the k-th candidate of the seeded uniform draw is found
-// with a warp prefix sum. The choice stream is the reference's mt19937_64
-// (shared by all resources, consumed in round order), the reorder-noise
-// stream is Rng(splitmix64(choice_seed ^ salt)) consumed in resource order.
-// Used for every cs_simulate call, brute force, and sweeps outside the
-// closed form of SURVEY Appendix A.2.
+// event_sim_kernel<kL, S>: the general replica. Per-resource ready queues are
+// bitsets over that resource's ops (ascending op index = the reference's
+// sorted queue); fully prioritized channels also index their ready ops by
+// rank, so a start walks from the lowest ready rank. The choice stream is the
+// reference's mt19937_64 (shared by all resources, consumed in round order),
+// the reorder-noise stream is Rng(splitmix64(choice_seed ^ salt)) consumed in
+// resource order. Two run shapes: a thread per run (kL = 1, batches, state
+// lane-interleaved in HBM) and a warp per run (kL = 32, small batches, state in
+// shared memory, the chain on lane 0).
+//
+// event_a2_kernel: one run inside A.2's regime (one compute unit + one
+// channel, gated, noiseless, recvs prioritized) for its event list — the same
+// round structure with the channel reduced to "next recv in gate order" and
+// both resources' state in registers.
+//
+// Used for batches and sweeps outside the closed form, brute force outside
+// it, and every report's event list.
 #include <algorithm>
 #include <chrono>
 #include <cstdio>

@@ -15,12 +15,15 @@
 //    and amended M+ (min of M over col[c] with cnt ≥ 2 / ≥ 1) and TAC's
 //    retire step (cnt−−, M −= T(c), xr ^= c over col[c]; P[owner] += W_g
 //    when a group drops to one outstanding recv).
-//  * TAC rounds run in one cooperative persistent kernel: amended M+ from
-//    each outstanding recv's direct-successor groups (exact because recvs
-//    are roots in every graph tac() sees), the reference's left fold as a
+//  * TAC rounds run in one persistent kernel: amended M+ from each
+//    outstanding recv's direct-successor groups (exact because recvs are
+//    roots in every graph tac() sees), the reference's left fold as a
 //    find-first-beater chain (exact for the non-transitive comparator;
-//    SURVEY A.3), then the retire step. Three grid syncs per round (one
-//    block for small graphs, so they are block barriers there).
+//    SURVEY A.3), then the retire step. Variants by size: one block with the
+//    state in shared memory (tac_smem_kernel; tac_kernel when it does not
+//    fit), one 16-CTA cluster with DSMEM mins (tac_cluster_kernel), and
+//    grid-wide cooperative kernels with register-resident candidates
+//    (tac_own_kernel) or re-read candidates (tac_dist_kernel).
 #include <cooperative_groups.h>
 
 #include <algorithm>
