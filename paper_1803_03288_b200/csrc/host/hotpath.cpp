@@ -3,8 +3,11 @@
 //   properties  -> properties.cpp:68-109   (csk_properties)
 //   tic / tac   -> schedule.cpp:21-71      (csk_tic / csk_tac)
 //   random      -> schedule.cpp:73-84      (csk_random_orders)
-//   simulate    -> sim.cpp:61-256          (csk_event_sim)
-//   brute force -> metrics.cpp:37-72       (csk_brute_force)
+//   simulate    -> sim.cpp:61-256          (csk_event_sim; csk_event_a2 for event
+//                                           lists inside A.2's regime; the
+//                                           closed form via csk_sweep_orders
+//                                           when only the makespan is needed)
+//   brute force -> metrics.cpp:37-72       (csk_brute_force_closed / csk_brute_force)
 #include <algorithm>
 #include <chrono>
 #include <cstdio>

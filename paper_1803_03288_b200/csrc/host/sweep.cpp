@@ -1,8 +1,9 @@
 // Batched sweeps (new entry points; the reference's loop is
-// tools/sched_main.cpp:452-502). Host work here is once-per-graph analysis:
-// decide whether the closed form of SURVEY Appendix A.2 applies and, if so,
-// build the chain-class tables the device kernel folds over. Otherwise every
-// seed runs through the exact device event simulator.
+// tools/sched_main.cpp:452-502). Host work here is once-per-graph analysis
+// (cached on the graph): decide whether the closed form of SURVEY Appendix A.2
+// applies and find the chain classes; per oracle the classes are weighted
+// into the tables the device kernel folds over (O(n)). Otherwise every seed
+// runs through the exact device event simulator.
 #include "sweep.hpp"
 
 #include <cuda_runtime.h>
