@@ -57,6 +57,7 @@ struct ChainArgs {
   uint32_t blob_bytes;
   uint32_t mbar_off;      // byte offset of the copy's mbarrier in dynamic shared memory
   const int32_t* orders;  // explicit orders mode (W == 1)
+  int* bad_order;         // explicit orders: set when an entry is out of [0, R)
   int64_t* makespans;
   int64_t* worker_ms;
   unsigned long long* i64;
@@ -301,7 +302,16 @@ __global__ void __launch_bounds__(kSweepThreads, 3) chain_sweep_kernel(ChainArgs
       FoldT<V> f{a.nc, 0, -1};
       if constexpr (kOrders) {
         const int32_t* o = a.orders + idx * R;
-        for (int k = R - 1; k >= 0; --k) f.add(tab[o[k]], ctot, pw);
+        bool bad = false;
+        for (int k = R - 1; k >= 0; --k) {
+          int32_t c = o[k];
+          if (static_cast<uint32_t>(c) >= static_cast<uint32_t>(R)) {  // validated here, not on the host
+            bad = true;
+            c = 0;
+          }
+          f.add(tab[c], ctot, pw);
+        }
+        if (bad) atomicOr(a.bad_order, 1);
       } else {
         const uint64_t ws = a.cluster ? splitmix64(seed ^ (kPhi * static_cast<uint64_t>(w + 1))) : seed;
         if (a.force_slow) {
@@ -637,11 +647,21 @@ extern "C" int csk_sweep_orders(SweepPlan* p, const int32_t* d_orders, int64_t n
   a.i64 = nullptr;  // per-order makespans only, no statistics
   a.f64 = nullptr;
   a.do_e = 0;
+  DevMem d_bad;
+  CK(cudaMalloc(&d_bad.p, sizeof(int)));
+  CK(cudaMemsetAsync(d_bad.p, 0, sizeof(int), st));
+  a.bad_order = d_bad.as<int>();
   const int blocks = static_cast<int>(std::min<int64_t>(p->blocks, (n + kSweepThreads - 1) / kSweepThreads));
   chain_sweep_kernel<uint8_t, true, int64_t><<<blocks, kSweepThreads, p->smem_orders, st>>>(a);
   LAUNCHED();
   CK(cudaGetLastError());
+  int bad = 0;
+  CK(cudaMemcpyAsync(&bad, d_bad.p, sizeof(int), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
+  if (bad) {
+    std::snprintf(err, 256, "order entry out of range");
+    return 4;
+  }
   return 0;
 }
 

@@ -613,12 +613,10 @@ int cs_simulate_orders(const cs_graph* g, const cs_oracle* o, const int32_t* ord
     if (n > 0) need(orders, "orders");
     const Graph& G = *g->g;
     const int32_t R = static_cast<int32_t>(G.recv_ops().size());
-    for (int64_t k = 0; k < n * R; ++k)
-      if (orders[k] < 0 || orders[k] >= R) fail(kParameter, "order entry out of range");
     const Policy p = policy_of(policy);
     auto ctx = make_sweep(g->g, o->o, p);
     if (n == 0) return;
-    if (ctx->fast && !ctx->cluster) {
+    if (ctx->fast && !ctx->cluster) {  // entries validated by the kernel as it reads them
       auto cudacheck = [&](cudaError_t e) {
         if (e != cudaSuccess) fail(kInternal, std::string("CUDA error: ") + cudaGetErrorString(e));
       };
@@ -627,12 +625,15 @@ int cs_simulate_orders(const cs_graph* g, const cs_oracle* o, const int32_t* ord
       cudacheck(cudaMallocAsync(&b_m.p, 8 * n, 0));
       cudacheck(cudaMemcpy(b_o.p, orders, 4 * n * R, cudaMemcpyHostToDevice));
       char err[256] = {0};
-      if (csk_sweep_orders(ctx->plan, b_o.as<int32_t>(), n, nullptr, b_m.as<int64_t>(), err)) fail(kInternal, err);
+      const int rc = csk_sweep_orders(ctx->plan, b_o.as<int32_t>(), n, nullptr, b_m.as<int64_t>(), err);
+      if (rc) fail(rc == 4 ? kParameter : kInternal, err);
       cudacheck(cudaMemcpy(makespans_out, b_m.p, 8 * n, cudaMemcpyDeviceToHost));
       if (violations_out)
         for (int64_t k = 0; k < n; ++k) violations_out[k] = 0;  // gated, noiseless, roots
       return;
     }
+    for (int64_t k = 0; k < n * R; ++k)  // the event replica indexes recvs by these
+      if (orders[k] < 0 || orders[k] >= R) fail(kParameter, "order entry out of range");
     std::vector<uint64_t> seeds(static_cast<size_t>(n), p.choice_seed);
     std::vector<int64_t> viol(static_cast<size_t>(n));
     std::vector<int32_t> st(static_cast<size_t>(n));

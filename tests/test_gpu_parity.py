@@ -469,3 +469,22 @@ def test_single_reports_specialised_replica(lib, ref, monkeypatch):
             for seed in (0, 5):
                 _both(lib, ref, text, lambda L, g: g.simulate(
                     g.declared(), g.tic("literal"), policy(True, seed, 0.0)).json())
+
+
+def test_simulate_orders_rejects_out_of_range_entries(lib):
+    """cs_simulate_orders: entries outside [0, R) are a parameter error on
+    both paths (validated by the closed-form kernel as it reads them, by the
+    host before the event replica)."""
+    g = lib.model("resnet_v2_50_inference", 1)
+    o = g.declared()
+    R = g.recv_count()
+    orders = np.tile(np.arange(R, dtype=np.int32), (300, 1))
+    ms, _ = g.simulate_orders(o, orders, policy(True, 1, 0.0))
+    assert (ms > 0).all()
+    for bad in (R, -1):
+        broken = orders.copy()
+        broken[123, 7] = bad
+        for pol in (policy(True, 1, 0.0), policy(False, 1, 0.0)):
+            with pytest.raises(CsError) as e:
+                g.simulate_orders(o, broken, pol)
+            assert e.value.code == 4 and "order entry out of range" in e.value.message
