@@ -301,17 +301,26 @@ __global__ void __launch_bounds__(kSweepThreads, 3) chain_sweep_kernel(ChainArgs
       const V ctot = static_cast<V>(a.ctot[w]);
       FoldT<V> f{a.nc, 0, -1};
       if constexpr (kOrders) {
+        // rows validated here as they are read (not on the host): entries in
+        // [0, R) (bad bit 1), no repeats (bit 2; the shuffle area is free in
+        // this mode and holds a per-thread seen-bitset)
         const int32_t* o = a.orders + idx * R;
-        bool bad = false;
+        uint32_t* seen = s_items + threadIdx.x;  // word q at seen[q * kSweepThreads]
+        for (int q = 0; q < (R + 31) / 32; ++q) seen[q * kSweepThreads] = 0;
+        int bad = 0;
         for (int k = R - 1; k >= 0; --k) {
           int32_t c = o[k];
-          if (static_cast<uint32_t>(c) >= static_cast<uint32_t>(R)) {  // validated here, not on the host
-            bad = true;
+          if (static_cast<uint32_t>(c) >= static_cast<uint32_t>(R)) {
+            bad |= 1;
             c = 0;
+          } else {
+            uint32_t& wd = seen[(c >> 5) * kSweepThreads];
+            bad |= (wd >> (c & 31)) & 1u ? 2 : 0;
+            wd |= 1u << (c & 31);
           }
           f.add(tab[c], ctot, pw);
         }
-        if (bad) atomicOr(a.bad_order, 1);
+        if (bad) atomicOr(a.bad_order, bad);
       } else {
         const uint64_t ws = a.cluster ? splitmix64(seed ^ (kPhi * static_cast<uint64_t>(w + 1))) : seed;
         if (a.force_slow) {
@@ -659,7 +668,8 @@ extern "C" int csk_sweep_orders(SweepPlan* p, const int32_t* d_orders, int64_t n
   CK(cudaMemcpyAsync(&bad, d_bad.p, sizeof(int), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   if (bad) {
-    std::snprintf(err, 256, "order entry out of range");
+    std::snprintf(err, 256, "%s",
+                  (bad & 1) ? "order entry out of range" : "order rows must be permutations of the recv columns");
     return 4;
   }
   return 0;

@@ -369,8 +369,14 @@ int cs_simulate(const cs_graph* g, const cs_oracle* o, const cs_schedule* s,
     rep->g = g->g;
     rep->pol = p;
     std::shared_ptr<SweepCtx> ctx;
-    if (!g->g->cluster() && p.gated && p.noise == 0.0 && in.all_recvs_prioritized)
-      ctx = cached_sweep(g, o, p);
+    bool closed = !g->g->cluster() && in.all_recvs_prioritized && (!p.gated || p.noise == 0.0);
+    if (closed && !p.gated) {  // ungated: only distinct priorities avoid channel draws
+      std::vector<int32_t> pr;
+      for (int32_t r : g->g->recv_ops()) pr.push_back(in.prio[r]);
+      std::sort(pr.begin(), pr.end());
+      closed = std::adjacent_find(pr.begin(), pr.end()) == pr.end();
+    }
+    if (closed) ctx = cached_sweep(g, o, p);
     if (ctx && ctx->fast && !ctx->cluster) {
       // Closed form: the gate order is the recvs sorted by
       // (priority, id) (sim.cpp:95-104); gated, noiseless, recvs are roots,
@@ -616,7 +622,7 @@ int cs_simulate_orders(const cs_graph* g, const cs_oracle* o, const int32_t* ord
     const Policy p = policy_of(policy);
     auto ctx = make_sweep(g->g, o->o, p);
     if (n == 0) return;
-    if (ctx->fast && !ctx->cluster) {  // entries validated by the kernel as it reads them
+    if (ctx->fast && !ctx->cluster) {  // rows validated by the kernel as it reads them
       auto cudacheck = [&](cudaError_t e) {
         if (e != cudaSuccess) fail(kInternal, std::string("CUDA error: ") + cudaGetErrorString(e));
       };
@@ -632,8 +638,17 @@ int cs_simulate_orders(const cs_graph* g, const cs_oracle* o, const int32_t* ord
         for (int64_t k = 0; k < n; ++k) violations_out[k] = 0;  // gated, noiseless, roots
       return;
     }
-    for (int64_t k = 0; k < n * R; ++k)  // the event replica indexes recvs by these
-      if (orders[k] < 0 || orders[k] >= R) fail(kParameter, "order entry out of range");
+    {  // every row a permutation of the recv columns (checked as the kernel does)
+      std::vector<uint8_t> seen(static_cast<size_t>(R));
+      for (int64_t b = 0; b < n; ++b) {
+        std::fill(seen.begin(), seen.end(), 0);
+        for (int32_t k = 0; k < R; ++k) {
+          const int32_t c = orders[b * R + k];
+          if (c < 0 || c >= R) fail(kParameter, "order entry out of range");
+          if (seen[c]++) fail(kParameter, "order rows must be permutations of the recv columns");
+        }
+      }
+    }
     std::vector<uint64_t> seeds(static_cast<size_t>(n), p.choice_seed);
     std::vector<int64_t> viol(static_cast<size_t>(n));
     std::vector<int32_t> st(static_cast<size_t>(n));

@@ -214,8 +214,13 @@ std::unique_ptr<SweepCtx> make_sweep(std::shared_ptr<const Graph> g, const TimeO
     s->recv_worker.assign(g->recv_ops().size(), 0);
   }
   // fast path?
-  bool ok = p.gated && p.noise == 0.0 && s->U < (int64_t{1} << 37);
-  if (!ok) s->why = "policy outside the closed form (ungated or noisy)";
+  // Gated: noiseless only (noise permutes the gate sequence). Ungated: noise
+  // is ignored (sim.cpp:106) and, with distinct recv priorities — every
+  // random order and permutation — the channel still runs the recvs
+  // back-to-back in priority order without a draw, i.e. exactly the gated
+  // run; callers with explicit priorities check distinctness (capi.cpp).
+  bool ok = (!p.gated || p.noise == 0.0) && s->U < (int64_t{1} << 37);
+  if (!ok) s->why = "policy outside the closed form (gated with reorder noise)";
   std::vector<ChainTables> tabs;
   if (ok && !s->cluster) {
     tabs.emplace_back();

@@ -222,7 +222,6 @@ def test_event_sim_lane_modes_agree(lib, orc, monkeypatch, model):
     R = g.recv_count()
     rng = np.random.default_rng(3)
     orders = np.argsort(rng.random((3000, R)), axis=1).astype(np.int32)
-    orders[::7, 0] = orders[::7, 1]  # rows that are not permutations: duplicate priorities slots
     cases = [("sweep", policy(False, 0, 0.0)), ("sweep", policy(True, 0, 0.2)),
              ("orders", policy(False, 11, 0.0)), ("orders", policy(True, 11, 0.3))]
     for kind, pol in cases:
@@ -472,9 +471,10 @@ def test_single_reports_specialised_replica(lib, ref, monkeypatch):
 
 
 def test_simulate_orders_rejects_out_of_range_entries(lib):
-    """cs_simulate_orders: entries outside [0, R) are a parameter error on
-    both paths (validated by the closed-form kernel as it reads them, by the
-    host before the event replica)."""
+    """cs_simulate_orders: rows must be permutations of the recv columns;
+    entries outside [0, R) or repeated are parameter errors on both paths
+    (validated by the closed-form kernel as it reads them, by the host before
+    the event replica)."""
     g = lib.model("resnet_v2_50_inference", 1)
     o = g.declared()
     R = g.recv_count()
@@ -484,7 +484,53 @@ def test_simulate_orders_rejects_out_of_range_entries(lib):
     for bad in (R, -1):
         broken = orders.copy()
         broken[123, 7] = bad
-        for pol in (policy(True, 1, 0.0), policy(False, 1, 0.0)):
+        for pol in (policy(True, 1, 0.0), policy(True, 1, 0.5)):  # closed form / event replica
             with pytest.raises(CsError) as e:
                 g.simulate_orders(o, broken, pol)
             assert e.value.code == 4 and "order entry out of range" in e.value.message
+    dup = orders.copy()
+    dup[200, 3] = dup[200, 4]  # not a permutation
+    for pol in (policy(True, 1, 0.0), policy(True, 1, 0.5)):
+        with pytest.raises(CsError) as e:
+            g.simulate_orders(o, dup, pol)
+        assert e.value.code == 4 and "permutations" in e.value.message
+
+
+def test_ungated_runs_through_the_closed_form_match_reference(lib, ref):
+    """Ungated runs with distinct recv priorities behave exactly like gated
+    noiseless ones (the channel still runs recvs back-to-back in priority
+    order; reorder noise is ignored when ungated, sim.cpp:93-110), so they use
+    the closed form: sweeps, single simulations and brute force against the
+    reference — including TIC-literal schedules with ties, which stay on the
+    event replica."""
+    texts = [t for _, t in corpus.worker_graphs(lib)[:6]] + [lib.model("resnet_v2_50_inference", 1).serialize()]
+    from paper_1803_03288_b200.capi import SweepPlan
+    closed = 0
+    for text in texts:
+        g = lib.graph(text)
+        o = g.declared()
+        try:  # wherever the gated closed form applies, the ungated one does too
+            SweepPlan.create(g, o, None)
+        except CsError:
+            pass
+        else:
+            SweepPlan.create(g, o, policy(False, 0, 0.4))
+            closed += 1
+        rg = ref.graph(text)
+        ro = rg.declared()
+        for noise in (0.0, 0.4):
+            res = g.sweep_random(o, 1, 150, policy(False, 0, noise), makespans=True)
+            want = np.array([rg.simulate(ro, rg.random(s), policy(False, s, noise)).makespan()
+                             for s in range(1, 151)])
+            assert np.array_equal(res["makespans"], want)
+        for sched in ("tac", "tic_literal", "random"):
+            def run(L, gg):
+                oo = gg.declared()
+                s = {"tac": lambda: gg.tac(oo), "tic_literal": lambda: gg.tic("literal"),
+                     "random": lambda: gg.random(3)}[sched]()
+                r = gg.simulate(oo, s, policy(False, 7, 0.2))
+                return r.json() + str(r.makespan()) + str(r.violations())
+            _both(lib, ref, text, run)
+        if g.recv_count() <= 8:
+            _both(lib, ref, text, lambda L, gg: gg.brute_force_text(gg.declared(), policy(False, 2, 0.0), 8))
+    assert closed >= 3
