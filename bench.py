@@ -190,35 +190,48 @@ def single_report(lib, reps=7):
     return out
 
 
-def event_replica(lib, path, noise=0.1, count=1 << 18, ref_target_s=5.0):
-    """sweeps outside the closed form run the exact event
-    replica (thread per run at this batch size). Config 4 with reorder noise:
-    device rate through cs_sweep_random (host buffers), the reference library
-    on all host cores for the same seeds, and the makespans of the
-    reference's sample compared value by value."""
+def sweep_vs_reference(lib, g, gpath, workload, noise=None, count=1 << 18, ref_target_s=5.0):
+    """A sweep through cs_sweep_random (host buffers, per-seed makespans out)
+    beside the reference library on all host cores for the same seeds, whose
+    sample's makespans are compared value by value."""
     from paper_1803_03288_b200.capi import policy
-    g = lib.model(MODEL, 1)
     o = g.declared()
-    pol = policy(True, 0, noise)
-    g.sweep_random(o, SEED_LO, count, pol)  # warm (sizes the simulator scratch)
+    pol = policy(True, 0, noise or 0.0)
+    g.sweep_random(o, SEED_LO, count, pol, makespans=True)  # warm (plans, scratch)
     t = time.perf_counter()
     res = g.sweep_random(o, SEED_LO, count, pol, makespans=True)
     dt = time.perf_counter() - t
-    out = {"workload": f"config4 {MODEL}, counter gate + reorder noise {noise}, seeds {SEED_LO}..",
-           "sims": count, "seconds": round(dt, 4), "sims_per_s": count / dt}
+    out = {"workload": workload, "sims": count, "seconds": round(dt, 4), "sims_per_s": count / dt}
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle
     if oracle.ref_available():
         cores = os.cpu_count() or 1
-        cal = ref_sweep(path, SEED_LO, cores * 2, cores, noise)
+        cal = ref_sweep(gpath, SEED_LO, cores * 2, cores, noise)
         n = min(count, max(cores, int(cal["sims"] / max(cal["seconds"], 1e-9) * ref_target_s)))
-        binp = os.path.join(os.path.dirname(path), "ref_noise.bin")
-        r = ref_sweep(path, SEED_LO, n, cores, noise, binp)
-        ref_ms = np.fromfile(binp, dtype=np.int64)
+        binp = os.path.join(os.path.dirname(gpath), "ref_cmp.bin")
+        r = ref_sweep(gpath, SEED_LO, n, cores, noise, binp)
+        ref_ms = np.fromfile(binp, dtype=np.int64)[:n]  # (clusters: per-worker makespans follow)
         out["reference_cpu"] = {"sims_per_s": r["sims"] / r["seconds"], "cores": cores, "sims": n,
                                 "seconds": round(r["seconds"], 3)}
         out["sample_identical"] = bool(np.array_equal(ref_ms, res["makespans"][:n]))
     return out
+
+
+def exact_paths(lib, path):
+    """Outside the plain gated closed form: (a) config 4 with reorder noise
+    0.1 — still the closed form, on the noise-permuted gate sequence; (b)
+    config 3's full iteration makespans, PS operations included, which only
+    the exact event replica (thread per run at this batch size) produces."""
+    g4 = lib.model(MODEL, 1)
+    a = sweep_vs_reference(lib, g4, path, f"config4 {MODEL}, counter gate + reorder noise 0.1 "
+                                          f"(closed form on the noise-permuted gate order)", 0.1, 1 << 22)
+    c3 = lib.model("vgg16_training", 1).expand(4, 1, 0)
+    p3 = os.path.join(os.path.dirname(path), "config3.json")
+    with open(p3, "w") as f:
+        f.write(c3.serialize())
+    b = sweep_vs_reference(lib, c3, p3, "config3 vgg16_training x 4 workers / 1 PS, full iteration makespans "
+                                        "(exact event replica, thread per run)", None, 1 << 18)
+    return {"noise_sweep_config4": a, "event_replica_config3_makespans": b}
 
 
 def cpu_baseline(path, target_s=10.0, g=None, o=None):
@@ -624,7 +637,7 @@ def main():
                                    "tools/allreduce_latency.py) to rounds of 1.3-8 us; DESIGN.md section 5")
         if not args.no_configs and world == 1:
             out["configs"] = other_configs(lib)
-            out["configs"]["event_replica_config4_noise"] = event_replica(lib, path)
+            out["configs"].update(exact_paths(lib, path))
             out["configs"]["single_report_simulate_json"] = single_report(lib)
         if not args.no_cpu and world == 1:
             out["cpu_baseline"] = cpu_baseline(path, g=g, o=o)

@@ -207,6 +207,35 @@ struct MtLazy {
   }
 };
 
+// A stream of any length: the first 311 outputs from MtLazy's register
+// cursors, then a full state in local memory continuing the same sequence.
+struct MtStream {
+  MtLazy lz;
+  uint64_t st[312];
+  int idx;
+  bool full;
+  __device__ __forceinline__ void init(uint64_t s) {
+    lz.init(s);
+    full = false;
+  }
+  __device__ __forceinline__ uint64_t next() {
+    if (!full) {
+      if (!lz.exhausted()) return lz.next_raw();
+      MtFull m{st, 0};
+      m.seed(lz.seed);
+      for (int k = 0; k < lz.i; ++k) m.next();
+      idx = m.idx;
+      full = true;
+    }
+    MtFull m{st, idx};
+    const uint64_t v = m.next();
+    idx = m.idx;
+    return v;
+  }
+};
+
+constexpr uint64_t kNoiseSalt = 0x9e3779b97f4a7c15ULL;  // reorder-noise stream salt, sim.cpp:14
+
 // Bounded draw (rng.hpp:21-30) with host-precomputed per-n constants:
 // limit = UINT64_MAX - (2^64 mod n), magic = floor(2^64 / n).
 __device__ __forceinline__ uint64_t fastmod(uint64_t v, uint64_t n, uint64_t magic) {

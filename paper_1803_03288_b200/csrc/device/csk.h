@@ -90,10 +90,12 @@ static inline int csk_key_bits(int64_t U) {
  * class weights pwsuf[0..nc]. send_total = total send time on the worker's
  * channel (0 for worker graphs). W workers share the layout; worker w uses
  * tables at offset w. seed derivation: worker graphs use the seed itself;
- * clusters use splitmix64(seed ^ phi*(w+1)) (cluster.cpp:112-113). */
+ * clusters use splitmix64(seed ^ phi*(w+1)) (cluster.cpp:112-113).
+ * noise_thr != 0: gated reorder noise, a position swaps when the noise
+ * stream's (output >> 11) < noise_thr (= the reference's unit() < p). */
 SweepPlan* csk_sweep_plan(int32_t W, int32_t R, int32_t nc, const int64_t* d,
                           const int32_t* first, const int64_t* pwsuf, const int64_t* send_total,
-                          int cluster, int64_t U, int64_t L, char* err);
+                          int cluster, int64_t U, int64_t L, uint64_t noise_thr, char* err);
 void csk_sweep_plan_free(SweepPlan* p);
 /* Stats layout documented in include/commsched.h (CS_DSTATS_*). */
 int csk_sweep_reset(SweepPlan* p, void* stream, int64_t* d_i64, double* d_f64, char* err);

@@ -40,7 +40,6 @@ constexpr int64_t kThreadModeMin = 2048;        // batch size from which a threa
 constexpr int kThreadMinBlocks = 6;            // thread mode: 24 resident warps/SM (<= 85 registers)
 constexpr size_t kThreadScratch = 16ull << 30;  // cap on thread-mode state in HBM
 constexpr int kEmptyLo = 1 << 29;  // "no ready word" (no overflow when lanes are added)
-constexpr uint64_t kNoiseSalt = 0x9e3779b97f4a7c15ULL;  // sim.cpp:14
 
 struct GraphView {
   int32_t n, nres, ndev, R;

@@ -58,6 +58,7 @@ struct ChainArgs {
   uint32_t mbar_off;      // byte offset of the copy's mbarrier in dynamic shared memory
   const int32_t* orders;  // explicit orders mode (W == 1)
   int* bad_order;         // explicit orders: set when an entry is out of [0, R)
+  uint64_t noise_thr;     // gated reorder noise: swap when (output >> 11) < thr (0: none)
   int64_t* makespans;
   int64_t* worker_ms;
   unsigned long long* i64;
@@ -253,7 +254,43 @@ __host__ __device__ inline size_t sweep_smem(int R, int W, int stride, int nhist
          4 * static_cast<size_t>(kSweepThreads) * ((R + per_word - 1) / per_word + 1) + 16;  // + mbarrier
 }
 
-template <typename T, bool kOrders, typename V>
+// Gated runs with reorder noise: the noise only permutes the
+// gate sequence up front — adjacent swaps with probability p, one draw of the
+// separate stream Rng(splitmix64(choice_seed ^ salt)) per position, channels
+// in resource order (sim.cpp:94-114) — so the closed form still applies to
+// the permuted sequence. The shuffle then has to be stored whole (the fused
+// right-to-left fold needs the final order), hence a separate path.
+template <bool kOn>
+struct NoiseState {
+  __device__ __forceinline__ void init(uint64_t) {}
+};
+template <>
+struct NoiseState<true> {
+  MtStream m;
+  __device__ __forceinline__ void init(uint64_t s) { m.init(s); }
+};
+
+// random_schedule(seed)'s permutation stored in `items` (rng.hpp:21-46).
+template <typename T>
+__device__ __noinline__ void shuffle_store(uint64_t seed, int R, Items<T> items, const uint64_t* s_lim,
+                                           const uint64_t* s_mag) {
+  items.init(R);
+  MtStream m;
+  m.init(seed);
+  for (int i = R; i > 1; --i) {
+    uint64_t v;
+    do v = m.next();
+    while (v > s_lim[i]);
+    const int j = static_cast<int>(fastmod32(v, static_cast<uint32_t>(i), s_mag[i]));
+    T* pj = items.at(j);
+    T* pl = items.at(i - 1);
+    const T x = *pj;
+    *pj = *pl;
+    *pl = x;
+  }
+}
+
+template <typename T, bool kOrders, typename V, bool kNoisy = false>
 __global__ void __launch_bounds__(kSweepThreads, 3) chain_sweep_kernel(ChainArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int R = a.R, W = a.W;
@@ -295,6 +332,8 @@ __global__ void __launch_bounds__(kSweepThreads, 3) chain_sweep_kernel(ChainArgs
        idx += nthreads) {
     const uint64_t seed = a.seed_lo + static_cast<uint64_t>(idx);
     int64_t hi = 0, lo = INT64_MAX;
+    NoiseState<kNoisy> noise;  // one stream per run, across the workers' channels
+    if constexpr (kNoisy) noise.init(splitmix64(seed ^ kNoiseSalt));
     for (int w = 0; w < W; ++w) {
       const uint2* tab = s_tab + w * R;
       const V* pw = s_pw + w * a.stride;
@@ -323,7 +362,18 @@ __global__ void __launch_bounds__(kSweepThreads, 3) chain_sweep_kernel(ChainArgs
         if (bad) atomicOr(a.bad_order, bad);
       } else {
         const uint64_t ws = a.cluster ? splitmix64(seed ^ (kPhi * static_cast<uint64_t>(w + 1))) : seed;
-        if (a.force_slow) {
+        if constexpr (kNoisy) {
+          shuffle_store(ws, R, items, s_lim, s_mag);  // rank order = the shuffle
+          for (int pos = 1; pos < R; ++pos)            // noise swaps -> gate order
+            if ((noise.m.next() >> 11) < a.noise_thr) {
+              T* p0 = items.at(pos - 1);
+              T* p1 = items.at(pos);
+              const T x = *p0;
+              *p0 = *p1;
+              *p1 = x;
+            }
+          for (int pos = R - 1; pos >= 0; --pos) f.add(tab[*items.at(pos)], ctot, pw);
+        } else if (a.force_slow) {
           items.init(R);
           f = shuffle_slow(ws, 0, R, items, f, tab, ctot, pw);
         } else {
@@ -486,10 +536,18 @@ struct SweepPlan {
   size_t blob_bytes = 0;
   size_t smem = 0, smem_orders = 0;
   int blocks = 0;
+  uint64_t noise_thr = 0;
 };
 
 using SweepFn = void (*)(ChainArgs);
 static SweepFn sweep_fn(const SweepPlan* p) {
+  if (p->noise_thr) {
+    if (p->R <= 256)
+      return p->narrow ? chain_sweep_kernel<uint8_t, false, int32_t, true>
+                       : chain_sweep_kernel<uint8_t, false, int64_t, true>;
+    return p->narrow ? chain_sweep_kernel<uint16_t, false, int32_t, true>
+                     : chain_sweep_kernel<uint16_t, false, int64_t, true>;
+  }
   if (p->R <= 256)
     return p->narrow ? chain_sweep_kernel<uint8_t, false, int32_t> : chain_sweep_kernel<uint8_t, false, int64_t>;
   return p->narrow ? chain_sweep_kernel<uint16_t, false, int32_t> : chain_sweep_kernel<uint16_t, false, int64_t>;
@@ -498,9 +556,10 @@ static SweepFn sweep_fn(const SweepPlan* p) {
 extern "C" SweepPlan* csk_sweep_plan(int32_t W, int32_t R, int32_t nc, const int64_t* d,
                                      const int32_t* first, const int64_t* pwsuf,
                                      const int64_t* send_total, int cluster, int64_t U, int64_t L,
-                                     char* err) {
+                                     uint64_t noise_thr, char* err) {
   if (ensure_device(err)) return nullptr;
   auto* p = new SweepPlan();
+  p->noise_thr = noise_thr;
   p->W = W;
   p->R = R;
   p->nc = nc;
@@ -609,6 +668,7 @@ static ChainArgs chain_args(SweepPlan* p) {
   a.L = p->L;
   a.do_e = !p->cluster && p->U != p->L;
   a.key_bits = csk_key_bits(p->U);
+  a.noise_thr = p->noise_thr;
   a.force_slow = std::getenv("TICTAC_SWEEP_FORCE_SLOW") != nullptr;
   a.blob = nullptr;  // per-element staging unless the caller's kernel matches the image
   a.blob_bytes = 0;

@@ -377,7 +377,7 @@ int cs_simulate(const cs_graph* g, const cs_oracle* o, const cs_schedule* s,
       closed = std::adjacent_find(pr.begin(), pr.end()) == pr.end();
     }
     if (closed) ctx = cached_sweep(g, o, p);
-    if (ctx && ctx->fast && !ctx->cluster) {
+    if (ctx && ctx->fast && !ctx->cluster && !ctx->noisy) {
       // Closed form: the gate order is the recvs sorted by
       // (priority, id) (sim.cpp:95-104); gated, noiseless, recvs are roots,
       // so no inversions and no forced releases.
@@ -487,7 +487,7 @@ int cs_brute_force(const cs_graph* g, const cs_oracle* o, const cs_sim_policy* p
     gp.gated = true;  // metrics.cpp:45-46
     if (!G.cluster() && p.noise == 0.0 && R >= 1 && R <= 20) {
       std::shared_ptr<SweepCtx> ctx = cached_sweep(g, o, gp);  // coverage/noise checks as simulate()
-      if (ctx->fast && !ctx->cluster) {
+      if (ctx->fast && !ctx->cluster && !ctx->noisy) {
         int64_t perms = 1;
         for (int64_t k = 2; k <= R; ++k) perms *= k;
         int64_t best_m = 0, best_k = 0, nd = 0;
@@ -622,7 +622,7 @@ int cs_simulate_orders(const cs_graph* g, const cs_oracle* o, const int32_t* ord
     const Policy p = policy_of(policy);
     auto ctx = make_sweep(g->g, o->o, p);
     if (n == 0) return;
-    if (ctx->fast && !ctx->cluster) {  // rows validated by the kernel as it reads them
+    if (ctx->fast && !ctx->cluster && !ctx->noisy) {  // rows validated by the kernel as it reads them
       auto cudacheck = [&](cudaError_t e) {
         if (e != cudaSuccess) fail(kInternal, std::string("CUDA error: ") + cudaGetErrorString(e));
       };

@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -214,13 +215,16 @@ std::unique_ptr<SweepCtx> make_sweep(std::shared_ptr<const Graph> g, const TimeO
     s->recv_worker.assign(g->recv_ops().size(), 0);
   }
   // fast path?
-  // Gated: noiseless only (noise permutes the gate sequence). Ungated: noise
-  // is ignored (sim.cpp:106) and, with distinct recv priorities — every
-  // random order and permutation — the channel still runs the recvs
-  // back-to-back in priority order without a draw, i.e. exactly the gated
-  // run; callers with explicit priorities check distinctness (capi.cpp).
-  bool ok = (!p.gated || p.noise == 0.0) && s->U < (int64_t{1} << 37);
-  if (!ok) s->why = "policy outside the closed form (gated with reorder noise)";
+  // Gated: reorder noise only permutes the gate sequence up front, which the
+  // sweep kernel applies before folding (explicit-order and single-run
+  // callers, which do not, check `noisy`). Ungated: noise is ignored
+  // (sim.cpp:106) and, with distinct recv priorities — every random order
+  // and permutation — the channel still runs the recvs back-to-back in
+  // priority order without a draw, i.e. exactly the gated run; callers with
+  // explicit priorities check distinctness (capi.cpp).
+  s->noisy = p.gated && p.noise > 0.0;
+  bool ok = s->U < (int64_t{1} << 37);
+  if (!ok) s->why = "makespan bound beyond the statistics key range";
   std::vector<ChainTables> tabs;
   if (ok && !s->cluster) {
     tabs.emplace_back();
@@ -262,8 +266,13 @@ std::unique_ptr<SweepCtx> make_sweep(std::shared_ptr<const Graph> g, const TimeO
       send.push_back(t.send_total);
     }
     char err[256] = {0};
+    uint64_t noise_thr = 0;  // unit() < p  <=>  (output >> 11) < p * 2^53 (integers below 2^53)
+    if (s->noisy) {
+      const double t = std::ldexp(p.noise, 53);
+      noise_thr = t == std::floor(t) ? static_cast<uint64_t>(t) : static_cast<uint64_t>(std::floor(t)) + 1;
+    }
     s->plan = csk_sweep_plan(W, R, nc, d.data(), first.data(), pw.data(), send.data(),
-                             s->cluster ? 1 : 0, s->U, s->L, err);
+                             s->cluster ? 1 : 0, s->U, s->L, noise_thr, err);
     if (!s->plan) fail(kInternal, err);
     s->fast = true;
     s->nc = nc;

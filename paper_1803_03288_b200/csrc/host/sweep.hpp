@@ -19,6 +19,7 @@ struct SweepCtx {
   Policy policy;
   int64_t U = 0, L = 0;
   bool cluster = false, fast = false;
+  bool noisy = false;  // gated with reorder noise: the sweep kernel applies it; explicit orders do not
   std::vector<std::string> workers;  // worker_devices() order (clusters)
   std::vector<int32_t> recv_worker;  // per recv column
   SweepPlan* plan = nullptr;

@@ -534,3 +534,30 @@ def test_ungated_runs_through_the_closed_form_match_reference(lib, ref):
         if g.recv_count() <= 8:
             _both(lib, ref, text, lambda L, gg: gg.brute_force_text(gg.declared(), policy(False, 2, 0.0), 8))
     assert closed >= 3
+
+
+@pytest.mark.parametrize("noise", [0.1, 0.5, 1.0])
+def test_noisy_sweeps_through_the_closed_form_match_reference(lib, ref, noise):
+    """Gated sweeps with reorder noise use the closed form on the noise-
+    permuted gate sequence: makespans equal the reference's
+    per-seed loop on worker graphs, a model DAG and clusters (one noise stream
+    across the workers' channels), and the generic replica on a large batch."""
+    from paper_1803_03288_b200.capi import SweepPlan
+    texts = [t for _, t in corpus.worker_graphs(lib)[:5]] + [lib.model("resnet_v2_50_inference", 1).serialize()]
+    texts += [t for _, t in corpus.cluster_graphs(lib)[:2]]
+    pol = policy(True, 0, noise)
+    closed = 0
+    for text in texts:
+        g = lib.graph(text)
+        o = g.declared()
+        try:
+            SweepPlan.create(g, o, pol)
+            closed += 1
+        except CsError:
+            pass
+        res = g.sweep_random(o, 1, 120, pol, makespans=True)
+        rg = ref.graph(text)
+        ro = rg.declared()
+        want = np.array([rg.simulate(ro, rg.random(s), policy(True, s, noise)).makespan() for s in range(1, 121)])
+        assert np.array_equal(res["makespans"], want), g.name()
+    assert closed >= 3
