@@ -510,7 +510,7 @@ __global__ void __launch_bounds__(1024) tac_own_kernel(TacArgs a, int* ring, lon
   const int nthreads = gridDim.x * blockDim.x;
   const int R = a.R;
   int64_t t_own[kOwn];
-  int s0[kOwn], s1[kOwn];
+  int s0[kOwn], s1[kOwn], g1[kOwn], c0[kOwn], c1[kOwn];
   bool live[kOwn];
 #pragma unroll
   for (int k = 0; k < kOwn; ++k) {
@@ -519,6 +519,11 @@ __global__ void __launch_bounds__(1024) tac_own_kernel(TacArgs a, int* ring, lon
     t_own[k] = live[k] ? a.tcol[c] : 0;
     s0[k] = live[k] ? a.succ_off[c] : 0;
     s1[k] = live[k] ? a.succ_off[c + 1] : 0;
+    // the single direct-successor group, when there is one (the usual case):
+    // M+ is then one load per round instead of a dependent pair
+    g1[k] = live[k] && s1[k] - s0[k] == 1 ? a.succ[s0[k]] : -1;
+    c0[k] = live[k] ? a.col_off[c] : 0;  // this column's retire list
+    c1[k] = live[k] ? a.col_off[c + 1] : 0;
   }
   auto mplus = [&](int e0, int e1) {
     int64_t m = kInf;
@@ -533,13 +538,14 @@ __global__ void __launch_bounds__(1024) tac_own_kernel(TacArgs a, int* ring, lon
 #pragma unroll
     for (int k = 0; k < kOwn; ++k) {
       P_own[k] = live[k] ? a.P[tid + k * nthreads] : 0;
-      mp_own[k] = live[k] ? mplus(s0[k], s1[k]) : kInf;
+      mp_own[k] = !live[k] ? kInf : g1[k] >= 0 ? a.M[g1[k]] : mplus(s0[k], s1[k]);
     }
     int best = first;
     int64_t bp = a.P[best], bm = a.tcol[best], bmp = mplus(a.succ_off[best], a.succ_off[best + 1]);
+    int64_t bcol = -1;  // best's column range, packed (begin << 32 | end), once a step has published it
     for (;;) {
       int nxt = 0x7fffffff;
-      int64_t np = 0, nt = 0, nm = 0;
+      int64_t np = 0, nt = 0, nm = 0, ncol = 0;
 #pragma unroll
       for (int k = 0; k < kOwn; ++k) {
         const int c = tid + k * nthreads;
@@ -548,13 +554,14 @@ __global__ void __launch_bounds__(1024) tac_own_kernel(TacArgs a, int* ring, lon
           np = P_own[k];
           nt = t_own[k];
           nm = mp_own[k];
+          ncol = (static_cast<int64_t>(c0[k]) << 32) | static_cast<uint32_t>(c1[k]);
         }
       }
       // grid-wide min (grid_min_step, inlined to publish the block winner)
       const int slot = p % 3;
       const int v = block_min_int(nxt, red, sp);
       if (nxt == v && v != 0x7fffffff) {
-        win[slot * gridDim.x + blockIdx.x] = make_longlong4(np, nt, nm, 0);
+        win[slot * gridDim.x + blockIdx.x] = make_longlong4(np, nt, nm, ncol);
         atomicMin(&ring[slot], v);
       }
       if (blockIdx.x == 0 && threadIdx.x == 0) ring[(p + 1) % 3] = 0x7fffffff;
@@ -567,9 +574,12 @@ __global__ void __launch_bounds__(1024) tac_own_kernel(TacArgs a, int* ring, lon
       bp = w.x;
       bm = w.y;
       bmp = w.z;
+      bcol = w.w;
     }
-    const int64_t t = a.tcol[best];
-    for (int64_t e = a.col_off[best] + tid; e < a.col_off[best + 1]; e += nthreads) {
+    const int64_t t = bm;  // T(best)
+    const int32_t e0 = bcol >= 0 ? static_cast<int32_t>(bcol >> 32) : a.col_off[best];
+    const int32_t e1 = bcol >= 0 ? static_cast<int32_t>(bcol & 0xffffffff) : a.col_off[best + 1];
+    for (int64_t e = e0 + tid; e < e1; e += nthreads) {
       const int32_t g = a.col[e];
       const int k = --a.cnt[g];
       a.M[g] -= t;
