@@ -109,20 +109,27 @@ struct FoldT {
 
 // One Fisher–Yates draw at slot i (1-based count of unfinished slots) with
 // bounded() value j: the element landing in its final slot i-1 is folded.
-template <typename T, typename V>
+// kStore: keep the permutation instead (the element is written to slot i-1).
+template <typename T, typename V, bool kStore = false>
 __device__ __forceinline__ void fy_draw(const Items<T>& items, int i, int j, FoldT<V>& f, const uint2* tab,
                                         V ctot, const V* pw) {
   T* pj = items.at(j);
   const T x = *pj;
-  *pj = *items.at(i - 1);
-  f.add(tab[x], ctot, pw);
+  if constexpr (kStore) {
+    T* pl = items.at(i - 1);
+    *pj = *pl;
+    *pl = x;
+  } else {
+    *pj = *items.at(i - 1);
+    f.add(tab[x], ctot, pw);
+  }
 }
 
 // Generic continuation after a bounded() rejection (probability ~R·2^-64
 // per draw) or past the first 311 outputs: full mt19937_64 state in local
 // memory, advanced to output `out` (0-based), then the reference loop.
 // (Everything by value: no address-taken locals in the hot caller.)
-template <typename T, typename V>
+template <typename T, typename V, bool kStore = false>
 __device__ __noinline__ FoldT<V> shuffle_slow(uint64_t seed, int out, int i, Items<T> items, FoldT<V> f,
                                               const uint2* tab, V ctot, const V* pw) {
   uint64_t st[312];
@@ -135,16 +142,16 @@ __device__ __noinline__ FoldT<V> shuffle_slow(uint64_t seed, int out, int i, Ite
     uint64_t v;
     do v = m.next();
     while (v > limit);
-    fy_draw(items, i, static_cast<int>(v % n), f, tab, ctot, pw);
+    fy_draw<T, V, kStore>(items, i, static_cast<int>(v % n), f, tab, ctot, pw);
   }
-  f.add(tab[*items.at(0)], ctot, pw);
+  if constexpr (!kStore) f.add(tab[*items.at(0)], ctot, pw);
   return f;
 }
 
 // Draws d..d+K-1 with outputs v[] (pre-checked only by maybe_reject):
 // precise bounded() rejection test, then the swaps. Returns true when a
 // rejection sent the rest of the shuffle to the exact slow path.
-template <int K, typename T, typename V>
+template <int K, typename T, typename V, bool kStore = false>
 __device__ __forceinline__ bool draw_group(uint64_t seed, int R, int d, const uint64_t (&v)[K],
                                            const Items<T>& items, FoldT<V>& f, const uint2* tab, V ctot,
                                            const V* pw, const uint64_t* s_lim, const uint64_t* s_mag) {
@@ -161,15 +168,15 @@ __device__ __forceinline__ bool draw_group(uint64_t seed, int R, int d, const ui
     for (int q = 0; q < K; ++q) {
       const int i = R - d - q;
       if (v[q] > s_lim[i]) {
-        f = shuffle_slow(seed, d + q + 1, i, items, f, tab, ctot, pw);
+        f = shuffle_slow<T, V, kStore>(seed, d + q + 1, i, items, f, tab, ctot, pw);
         return true;
       }
-      fy_draw(items, i, j[q], f, tab, ctot, pw);
+      fy_draw<T, V, kStore>(items, i, j[q], f, tab, ctot, pw);
     }
     return false;
   }
 #pragma unroll
-  for (int q = 0; q < K; ++q) fy_draw(items, R - d - q, j[q], f, tab, ctot, pw);
+  for (int q = 0; q < K; ++q) fy_draw<T, V, kStore>(items, R - d - q, j[q], f, tab, ctot, pw);
   return false;
 }
 
@@ -179,7 +186,7 @@ __device__ __forceinline__ bool draw_group(uint64_t seed, int R, int d, const ui
 // t_d = f(s_d, s_d+1) ^ t_{d-156}, t_{d-156} = f(s_{d-156}, s_{d-155}) ^ s_d.
 // Four draws per iteration: four independent twist/temper/bounded chains
 // before the dependent shared-memory swaps.
-template <typename T, typename V>
+template <typename T, typename V, bool kStore = false>
 __device__ __forceinline__ void shuffle_fold(uint64_t seed, int R, const Items<T>& items, FoldT<V>& f,
                                              const uint2* tab, V ctot, const V* pw,
                                              const uint64_t* s_lim, const uint64_t* s_mag) {
@@ -199,14 +206,14 @@ __device__ __forceinline__ void shuffle_fold(uint64_t seed, int R, const Items<T
     a0 = a4;
     a1 = mt_step(a4, u + 5);
     b = mt_step(b3, u + 160);
-    if (draw_group<4>(seed, R, d, v, items, f, tab, ctot, pw, s_lim, s_mag)) return;
+    if (draw_group<4, T, V, kStore>(seed, R, d, v, items, f, tab, ctot, pw, s_lim, s_mag)) return;
   }
   for (; d < n1; ++d) {
     const uint64_t v[1] = {mt_temper(mt_twist(a0, a1, b))};
     a0 = a1;
     a1 = mt_step(a1, static_cast<uint32_t>(d + 2));
     b = mt_step(b, static_cast<uint32_t>(d + 157));
-    if (draw_group<1>(seed, R, d, v, items, f, tab, ctot, pw, s_lim, s_mag)) return;
+    if (draw_group<1, T, V, kStore>(seed, R, d, v, items, f, tab, ctot, pw, s_lim, s_mag)) return;
   }
   if (d < draws) {  // phase 2, c = (s_d-156, s_d-155)
     uint64_t c0 = seed, c1 = mt_step(seed, 1);
@@ -223,7 +230,7 @@ __device__ __forceinline__ void shuffle_fold(uint64_t seed, int R, const Items<T
       a1 = mt_step(a4, u + 5);
       c0 = c4;
       c1 = mt_step(c4, u - 151);
-      if (draw_group<4>(seed, R, d, v, items, f, tab, ctot, pw, s_lim, s_mag)) return;
+      if (draw_group<4, T, V, kStore>(seed, R, d, v, items, f, tab, ctot, pw, s_lim, s_mag)) return;
     }
     for (; d < n2; ++d) {
       const uint64_t v[1] = {mt_temper(mt_twist(a0, a1, mt_twist(c0, c1, a0)))};
@@ -231,14 +238,15 @@ __device__ __forceinline__ void shuffle_fold(uint64_t seed, int R, const Items<T
       a1 = mt_step(a1, static_cast<uint32_t>(d + 2));
       c0 = c1;
       c1 = mt_step(c1, static_cast<uint32_t>(d - 154));
-      if (draw_group<1>(seed, R, d, v, items, f, tab, ctot, pw, s_lim, s_mag)) return;
+      if (draw_group<1, T, V, kStore>(seed, R, d, v, items, f, tab, ctot, pw, s_lim, s_mag)) return;
     }
     if (d < draws) {  // beyond the first block (R > 312)
-      f = shuffle_slow(seed, d, R - d, items, f, tab, ctot, pw);
+      f = shuffle_slow<T, V, kStore>(seed, d, R - d, items, f, tab, ctot, pw);
       return;
     }
   }
-  if (R >= 1) f.add(tab[*items.at(0)], ctot, pw);
+  if constexpr (!kStore)
+    if (R >= 1) f.add(tab[*items.at(0)], ctot, pw);
 }
 
 // Shared-memory layout of one block (bytes); hist bins only when used.
@@ -269,26 +277,6 @@ struct NoiseState<true> {
   MtStream m;
   __device__ __forceinline__ void init(uint64_t s) { m.init(s); }
 };
-
-// random_schedule(seed)'s permutation stored in `items` (rng.hpp:21-46).
-template <typename T>
-__device__ __noinline__ void shuffle_store(uint64_t seed, int R, Items<T> items, const uint64_t* s_lim,
-                                           const uint64_t* s_mag) {
-  items.init(R);
-  MtStream m;
-  m.init(seed);
-  for (int i = R; i > 1; --i) {
-    uint64_t v;
-    do v = m.next();
-    while (v > s_lim[i]);
-    const int j = static_cast<int>(fastmod32(v, static_cast<uint32_t>(i), s_mag[i]));
-    T* pj = items.at(j);
-    T* pl = items.at(i - 1);
-    const T x = *pj;
-    *pj = *pl;
-    *pl = x;
-  }
-}
 
 template <typename T, bool kOrders, typename V, bool kNoisy = false>
 __global__ void __launch_bounds__(kSweepThreads, 3) chain_sweep_kernel(ChainArgs a) {
@@ -363,7 +351,7 @@ __global__ void __launch_bounds__(kSweepThreads, 3) chain_sweep_kernel(ChainArgs
       } else {
         const uint64_t ws = a.cluster ? splitmix64(seed ^ (kPhi * static_cast<uint64_t>(w + 1))) : seed;
         if constexpr (kNoisy) {
-          shuffle_store(ws, R, items, s_lim, s_mag);  // rank order = the shuffle
+          shuffle_fold<T, V, true>(ws, R, items, f, tab, ctot, pw, s_lim, s_mag);  // rank order = the shuffle
           for (int pos = 1; pos < R; ++pos)            // noise swaps -> gate order
             if ((noise.m.next() >> 11) < a.noise_thr) {
               T* p0 = items.at(pos - 1);
