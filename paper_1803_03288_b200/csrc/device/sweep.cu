@@ -262,6 +262,48 @@ __host__ __device__ inline size_t sweep_smem(int R, int W, int stride, int nhist
          4 * static_cast<size_t>(kSweepThreads) * ((R + per_word - 1) / per_word + 1) + 16;  // + mbarrier
 }
 
+// Outputs 0..n-1 of mt19937_64(seed), four per iteration from the same
+// phase-split register cursors as shuffle_fold (n <= 311: first block only),
+// each handed to `use(d, v)` in order.
+template <typename F>
+__device__ __forceinline__ void mt_outputs(uint64_t seed, int n, F&& use) {
+  uint64_t a0 = seed, a1 = mt_step(seed, 1), b = seed;
+#pragma unroll 4
+  for (uint32_t k = 1; k <= 156; ++k) b = mt_step(b, k);
+  const int n1 = min(n, 156);
+  int d = 0;
+  for (; d + 3 < n1; d += 4) {
+    const uint32_t u = static_cast<uint32_t>(d);
+    const uint64_t a2 = mt_step(a1, u + 2), a3 = mt_step(a2, u + 3), a4 = mt_step(a3, u + 4);
+    const uint64_t b1 = mt_step(b, u + 157), b2 = mt_step(b1, u + 158), b3 = mt_step(b2, u + 159);
+    const uint64_t v0 = mt_temper(mt_twist(a0, a1, b)), v1 = mt_temper(mt_twist(a1, a2, b1)),
+                   v2 = mt_temper(mt_twist(a2, a3, b2)), v3 = mt_temper(mt_twist(a3, a4, b3));
+    a0 = a4;
+    a1 = mt_step(a4, u + 5);
+    b = mt_step(b3, u + 160);
+    use(d, v0);
+    use(d + 1, v1);
+    use(d + 2, v2);
+    use(d + 3, v3);
+  }
+  for (; d < n1; ++d) {
+    use(d, mt_temper(mt_twist(a0, a1, b)));
+    a0 = a1;
+    a1 = mt_step(a1, static_cast<uint32_t>(d + 2));
+    b = mt_step(b, static_cast<uint32_t>(d + 157));
+  }
+  if (d < n) {
+    uint64_t c0 = seed, c1 = mt_step(seed, 1);
+    for (; d < n; ++d) {
+      use(d, mt_temper(mt_twist(a0, a1, mt_twist(c0, c1, a0))));
+      a0 = a1;
+      a1 = mt_step(a1, static_cast<uint32_t>(d + 2));
+      c0 = c1;
+      c1 = mt_step(c1, static_cast<uint32_t>(d - 154));
+    }
+  }
+}
+
 // Gated runs with reorder noise: the noise only permutes the
 // gate sequence up front — adjacent swaps with probability p, one draw of the
 // separate stream Rng(splitmix64(choice_seed ^ salt)) per position, channels
@@ -352,14 +394,20 @@ __global__ void __launch_bounds__(kSweepThreads, 3) chain_sweep_kernel(ChainArgs
         const uint64_t ws = a.cluster ? splitmix64(seed ^ (kPhi * static_cast<uint64_t>(w + 1))) : seed;
         if constexpr (kNoisy) {
           shuffle_fold<T, V, true>(ws, R, items, f, tab, ctot, pw, s_lim, s_mag);  // rank order = the shuffle
-          for (int pos = 1; pos < R; ++pos)            // noise swaps -> gate order
-            if ((noise.m.next() >> 11) < a.noise_thr) {
+          auto swap_at = [&](int pos, uint64_t v) {   // noise swaps -> gate order
+            if ((v >> 11) < a.noise_thr) {
               T* p0 = items.at(pos - 1);
               T* p1 = items.at(pos);
               const T x = *p0;
               *p0 = *p1;
               *p1 = x;
             }
+          };
+          if (W == 1 && R - 1 <= 311) {  // the run's only channel: the stream's first R-1 outputs
+            mt_outputs(splitmix64(seed ^ kNoiseSalt), R - 1, [&](int d, uint64_t v) { swap_at(d + 1, v); });
+          } else {
+            for (int pos = 1; pos < R; ++pos) swap_at(pos, noise.m.next());
+          }
           for (int pos = R - 1; pos >= 0; --pos) f.add(tab[*items.at(pos)], ctot, pw);
         } else if (a.force_slow) {
           items.init(R);
