@@ -914,16 +914,12 @@ int run_event(DeviceGraph* g, const int64_t* dur, int64_t B, RunSpec rs, int64_t
 // the choice stream. One thread runs the chain; the block initialises.
 constexpr int kA2Tab = 256;  // bounded() constants staged for n < kA2Tab
 
-// Shared-memory bytes of event_a2_kernel; `staged` adds copies of the graph
-// arrays the chain reads (durations, successor CSR, local indices, the unit's
-// op list, gate order) so each dependent load is a shared-memory round trip.
-__host__ __device__ inline size_t a2_smem(int n, int E, int R, int ncpu, bool staged) {
-  const size_t base = 8 * 312 + 16ull * kA2Tab + 4ull * n + 4ull * ((ncpu + 31) / 32 + 1);
-  if (!staged) return base;
-  return base + 8ull * n + 4ull * (n + 1) + 4ull * E + 4ull * n + 4ull * ncpu + 4ull * R + 16;
+// Shared-memory bytes of event_a2_kernel (the graph arrays stay in global
+// memory: the fallback for runs whose nodes do not fit event_a2p_kernel).
+__host__ __device__ inline size_t a2_smem(int n, int ncpu) {
+  return 8 * 312 + 16ull * kA2Tab + 4ull * n + 4ull * ((ncpu + 31) / 32 + 1);
 }
 
-template <bool kStaged, typename Tm>
 __global__ void __launch_bounds__(256) event_a2_kernel(GraphView G, const int32_t* __restrict__ gate_order,
                                                        int cpu_r, uint64_t choice_seed, const uint64_t* lim,
                                                        const uint64_t* mag, int64_t* start, int64_t* end,
@@ -932,41 +928,14 @@ __global__ void __launch_bounds__(256) event_a2_kernel(GraphView G, const int32_
   const int n = G.n, R = G.R;
   const int ncpu = cpu_r >= 0 ? G.rops_off[cpu_r + 1] - G.rops_off[cpu_r] : 0;
   const int nw = (ncpu + 31) / 32;
-  const int E = G.succ_off[n];
   auto* mt = reinterpret_cast<uint64_t*>(a2_sm);
   auto* s_lim = mt + 312;
   auto* s_mag = s_lim + kA2Tab;
   auto* missing = reinterpret_cast<int32_t*>(s_mag + kA2Tab);
   auto* ready = reinterpret_cast<uint32_t*>(missing + n);
-  // graph arrays: shared copies when staged, else the global ones; times in
-  // Tm (32-bit when the host proved every time < 2^31: the staged copy)
-  const Tm* dur = reinterpret_cast<const Tm*>(G.dur);
+  const int64_t* dur = G.dur;
   const int32_t *succ_off = G.succ_off, *succ_idx = G.succ_idx, *lidx = G.lidx, *order = gate_order;
   const int32_t* cpu_ops = cpu_r >= 0 ? G.rops + G.rops_off[cpu_r] : nullptr;
-  if constexpr (kStaged) {
-    char* q = reinterpret_cast<char*>(ready + nw + 1);
-    q = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(q) + 15) & ~uintptr_t(15));
-    auto* s_dur = reinterpret_cast<Tm*>(q);
-    auto* s_soff = reinterpret_cast<int32_t*>(s_dur + n);
-    auto* s_sidx = s_soff + n + 1;
-    auto* s_lidx = s_sidx + E;
-    auto* s_cpu = s_lidx + n;
-    auto* s_ord = s_cpu + ncpu;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-      s_dur[i] = static_cast<Tm>(G.dur[i]);
-      s_lidx[i] = G.lidx[i];
-    }
-    for (int i = threadIdx.x; i <= n; i += blockDim.x) s_soff[i] = G.succ_off[i];
-    for (int e = threadIdx.x; e < E; e += blockDim.x) s_sidx[e] = G.succ_idx[e];
-    for (int k = threadIdx.x; k < ncpu; k += blockDim.x) s_cpu[k] = cpu_ops[k];
-    for (int k = threadIdx.x; k < R; k += blockDim.x) s_ord[k] = gate_order[k];
-    dur = s_dur;
-    succ_off = s_soff;
-    succ_idx = s_sidx;
-    lidx = s_lidx;
-    cpu_ops = s_cpu;
-    order = s_ord;
-  }
   for (int k = threadIdx.x; k < kA2Tab; k += blockDim.x) {
     s_lim[k] = lim[k];
     s_mag[k] = mag[k];
@@ -994,9 +963,8 @@ __global__ void __launch_bounds__(256) event_a2_kernel(GraphView G, const int32_
   };
   int ready_cnt = 0, lo = 0;  // lo: no set bit below word lo
   for (int w = 0; w < nw; ++w) ready_cnt += __popc(ready[w]);
-  static_assert(kStaged || sizeof(Tm) == 8, "32-bit times need the staged copy");
-  constexpr Tm kNever = sizeof(Tm) == 8 ? static_cast<Tm>(INT64_MAX) : static_cast<Tm>(INT32_MAX);
-  Tm t = 0, cpu_end = 0, chan_end = 0;
+  constexpr int64_t kNever = INT64_MAX;
+  int64_t t = 0, cpu_end = 0, chan_end = 0;
   int cpu_op = -1, chan_op = -1, chan_next = 0, finished = 0;
   auto complete = [&](int op) {
     ++finished;
@@ -1062,6 +1030,200 @@ __global__ void __launch_bounds__(256) event_a2_kernel(GraphView G, const int32_
     }
   }
   *makespan = static_cast<int64_t>(t);  // every op has ended by the time of the last completion
+}
+
+// The packed single-report replica: the graph re-laid per run node in shared
+// memory, nodes numbered u = compute op's index in the unit's op list (the
+// candidate order of try_start), then R + ... recvs by gate rank. Node u's
+// duration and successor range are one 16-byte load; successors are stored as
+// unit indices, so a completion touches only `missing` and the ready bitset
+// (both by unit index) — each step of the chain is one shared-memory round
+// trip instead of several dependent generic loads. Start times stay in shared
+// memory; the block writes start/end per op id at the end.
+struct alignas(16) A2Node {
+  long long dur;
+  int beg, end;  // successors: a2_succ[beg..end)
+};
+
+__host__ __device__ inline size_t a2p_smem(int n, int E, int ncpu, size_t tbytes) {
+  const int nw = (ncpu + 31) / 32 + 1;
+  return 8 * 312 + 16ull * kA2Tab + 16ull * n + round16(tbytes * n) + round16(4ull * E) + round16(4ull * ncpu) +
+         4ull * nw;
+}
+
+template <typename Tm>
+__global__ void __launch_bounds__(256) event_a2p_kernel(GraphView G, const int32_t* __restrict__ gate_order,
+                                                        int cpu_r, uint64_t choice_seed, const uint64_t* lim,
+                                                        const uint64_t* mag, int64_t* start, int64_t* end,
+                                                        int64_t* makespan) {
+  extern __shared__ __align__(16) char a2_sm[];
+  const int n = G.n, R = G.R;
+  const int ncpu = G.rops_off[cpu_r + 1] - G.rops_off[cpu_r];
+  const int32_t* cpu_ops = G.rops + G.rops_off[cpu_r];
+  const int nw = (ncpu + 31) / 32;
+  const int E = G.succ_off[n];
+  auto* mt = reinterpret_cast<uint64_t*>(a2_sm);
+  auto* s_lim = mt + 312;
+  auto* s_mag = s_lim + kA2Tab;
+  auto* node = reinterpret_cast<A2Node*>(s_mag + kA2Tab);
+  auto* st = reinterpret_cast<Tm*>(node + n);
+  auto* succ = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(st) + round16(sizeof(Tm) * n));
+  auto* missing = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(succ) + round16(4ull * E));
+  auto* ready = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(missing) + round16(4ull * ncpu));
+  for (int u = threadIdx.x; u < n; u += blockDim.x) {
+    const int op = u < ncpu ? cpu_ops[u] : gate_order[u - ncpu];
+    A2Node a;
+    a.dur = G.dur[op];
+    a.beg = G.succ_off[op];
+    a.end = G.succ_off[op + 1];
+    node[u] = a;
+  }
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {  // ~l: the successor has one predecessor
+    const int w = G.succ_idx[e];
+    succ[e] = G.pred_off[w + 1] - G.pred_off[w] == 1 ? ~G.lidx[w] : G.lidx[w];
+  }
+  for (int k = threadIdx.x; k < kA2Tab; k += blockDim.x) {
+    s_lim[k] = lim[k];
+    s_mag[k] = mag[k];
+  }
+  for (int w = threadIdx.x; w <= nw; w += blockDim.x) ready[w] = 0;
+  __syncthreads();
+  for (int l = threadIdx.x; l < ncpu; l += blockDim.x) {
+    const int op = cpu_ops[l];
+    const int deg = G.pred_off[op + 1] - G.pred_off[op];
+    missing[l] = deg;
+    if (deg == 0) atomicOr(&ready[l >> 5], 1u << (l & 31));
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    MtFullP<uint64_t*> choice{mt, 0};
+    choice.seed(choice_seed);
+    int ready_cnt = 0, lo = 0;  // lo: no set bit below word lo
+    for (int w = 0; w < nw; ++w) ready_cnt += __popc(ready[w]);
+    int hint = -1;  // the last op made ready while it stays ready: the pick when it is the only one
+    Tm t = 0, cpu_end = 0, chan_end = 0;
+    int cpu_u = -1, chan_u = -1, chan_next = 0;
+    auto complete = [&](int u) {  // successors are compute ops (recvs are roots)
+      const A2Node nd = node[u];
+      for (int e = nd.beg; e < nd.end; ++e) {
+        int l = succ[e];
+        if (l < 0) {  // single-predecessor op: ready now
+          l = ~l;
+        } else {
+          const int m = missing[l] - 1;
+          missing[l] = m;
+          if (m) continue;
+        }
+        ready[l >> 5] |= 1u << (l & 31);
+        ++ready_cnt;
+        lo = min(lo, l >> 5);
+        hint = l;
+      }
+    };
+    auto start_cpu = [&]() {  // try_start(compute): every ready op is a candidate
+      int u;
+      if (ready_cnt == 1 && hint >= 0) {
+        u = hint;
+        ready[u >> 5] &= ~(1u << (u & 31));
+      } else {
+        int k = 0;
+        if (ready_cnt > 1) {  // bounded(ready_cnt), rng.hpp:21-30
+          const uint64_t m = static_cast<uint64_t>(ready_cnt);
+          const bool small = m < kA2Tab;
+          const uint64_t lm = small ? s_lim[m] : lim[m], mg = small ? s_mag[m] : mag[m];
+          uint64_t v;
+          do v = choice.next();
+          while (v > lm);
+          k = static_cast<int>(fastmod(v, m, mg));
+        }
+        while (!ready[lo]) ++lo;
+        int w = lo;
+        uint32_t word = ready[w];
+        for (;;) {
+          const int c = __popc(word);
+          if (k < c) break;
+          k -= c;
+          word = ready[++w];
+        }
+        const int bit = nth_bit(word, k);
+        ready[w] = word & ~(1u << bit);
+        u = (w << 5) + bit;
+      }
+      if (u == hint) hint = -1;
+      --ready_cnt;
+      cpu_u = u;
+      st[u] = t;
+      cpu_end = t + static_cast<Tm>(node[u].dur);
+    };
+    auto start_chan = [&]() {  // try_start(channel): next in gate order
+      chan_u = ncpu + chan_next++;
+      st[chan_u] = t;
+      chan_end = t + static_cast<Tm>(node[chan_u].dur);
+    };
+    for (;;) {
+      // The round at time t: try_start in resource order. Busy resources end
+      // after t here, so complete_now can only fire for an op started now
+      // with zero duration; then the generic passes take over (sim.cpp:117-233).
+      bool zero = false;
+      if (cpu_u < 0 && ready_cnt > 0) {
+        start_cpu();
+        zero = cpu_end == t;
+      }
+      if (chan_u < 0 && chan_next < R) {
+        start_chan();
+        zero |= chan_end == t;
+      }
+      if (zero) {
+        if (cpu_u >= 0 && cpu_end == t) {
+          complete(cpu_u);
+          cpu_u = -1;
+        }
+        if (chan_u >= 0 && chan_end == t) {
+          complete(chan_u);
+          chan_u = -1;
+        }
+        for (bool progress = true; progress;) {
+          progress = false;
+          if (cpu_u < 0 && ready_cnt > 0) {
+            start_cpu();
+            progress = true;
+          }
+          if (chan_u < 0 && chan_next < R) {
+            start_chan();
+            progress = true;
+          }
+          if (cpu_u >= 0 && cpu_end == t) {
+            complete(cpu_u);
+            cpu_u = -1;
+            progress = true;
+          }
+          if (chan_u >= 0 && chan_end == t) {
+            complete(chan_u);
+            chan_u = -1;
+            progress = true;
+          }
+        }
+      }
+      if (cpu_u < 0 && chan_u < 0) break;  // nothing running or startable: every op of the DAG has ended
+      t = cpu_u < 0 ? chan_end : chan_u < 0 ? cpu_end : min(cpu_end, chan_end);
+      if (cpu_u >= 0 && cpu_end == t) {
+        complete(cpu_u);
+        cpu_u = -1;
+      }
+      if (chan_u >= 0 && chan_end == t) {
+        complete(chan_u);
+        chan_u = -1;
+      }
+    }
+    *makespan = static_cast<int64_t>(t);  // every op has ended by the time of the last completion
+  }
+  __syncthreads();
+  for (int u = threadIdx.x; u < n; u += blockDim.x) {
+    const int op = u < ncpu ? cpu_ops[u] : gate_order[u - ncpu];
+    const int64_t s0 = static_cast<int64_t>(st[u]);
+    start[op] = s0;
+    end[op] = s0 + node[u].dur;
+  }
 }
 
 }  // namespace
@@ -1169,18 +1331,21 @@ extern "C" int csk_event_a2(DeviceGraph* g, const int64_t* dur, const int32_t* g
   int ncpu = 0;
   for (int32_t i = 0; i < g->n; ++i) ncpu += g->h_res[i] == cpu_r;
   const int E = g->h_succ_off.empty() ? 0 : g->h_succ_off.back();
-  const bool staged = a2_smem(g->n, E, R, ncpu, true) <= 220 * 1024;
-  const size_t smem = a2_smem(g->n, E, R, ncpu, staged);
+  int64_t U = 0;  // every event time is at most the sum of all durations
+  for (int32_t i = 0; i < g->n; ++i) U += dur[i];
+  const bool narrow = U < (int64_t{1} << 31);
+  // the packed kernel when the run's nodes fit in shared memory, else the
+  // replica over the global graph arrays
+  const size_t smem_p = a2p_smem(g->n, E, ncpu, narrow ? 4 : 8);
+  const bool packed = cpu_r >= 0 && smem_p <= 220 * 1024 && !std::getenv("TICTAC_A2_GLOBAL");
+  const size_t smem = packed ? smem_p : a2_smem(g->n, ncpu);
   if (smem > 220 * 1024) {
     std::snprintf(err, 256, "graph too large for the single-report kernel");
     return 4;
   }
-  int64_t U = 0;  // every event time is at most the sum of all durations
-  for (int32_t i = 0; i < g->n; ++i) U += dur[i];
-  const bool narrow = staged && U < (int64_t{1} << 31);
-  const void* kfn = narrow   ? reinterpret_cast<const void*>(event_a2_kernel<true, int32_t>)
-                    : staged ? reinterpret_cast<const void*>(event_a2_kernel<true, int64_t>)
-                             : reinterpret_cast<const void*>(event_a2_kernel<false, int64_t>);
+  const void* kfn = !packed ? reinterpret_cast<const void*>(event_a2_kernel)
+                    : narrow ? reinterpret_cast<const void*>(event_a2p_kernel<int32_t>)
+                             : reinterpret_cast<const void*>(event_a2p_kernel<int64_t>);
   CK(allow_max_dynamic_smem(kfn));
   const bool trace = std::getenv("TICTAC_EVENT_TRACE") != nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -1192,13 +1357,12 @@ extern "C" int csk_event_a2(DeviceGraph* g, const int64_t* dur, const int32_t* g
   auto* ordp = static_cast<int32_t*>(d_order.p);
   auto *stp = static_cast<int64_t*>(d_start.p), *enp = static_cast<int64_t*>(d_end.p),
        *msp = static_cast<int64_t*>(d_ms.p);
-  if (narrow)
-    event_a2_kernel<true, int32_t><<<1, 256, smem>>>(G, ordp, cpu_r, choice_seed, tabs.lim, tabs.mag, stp, enp, msp);
-  else if (staged)
-    event_a2_kernel<true, int64_t><<<1, 256, smem>>>(G, ordp, cpu_r, choice_seed, tabs.lim, tabs.mag, stp, enp, msp);
+  if (packed && narrow)
+    event_a2p_kernel<int32_t><<<1, 256, smem>>>(G, ordp, cpu_r, choice_seed, tabs.lim, tabs.mag, stp, enp, msp);
+  else if (packed)
+    event_a2p_kernel<int64_t><<<1, 256, smem>>>(G, ordp, cpu_r, choice_seed, tabs.lim, tabs.mag, stp, enp, msp);
   else
-    event_a2_kernel<false, int64_t><<<1, 256, smem>>>(G, ordp, cpu_r, choice_seed, tabs.lim, tabs.mag, stp, enp,
-                                                       msp);
+    event_a2_kernel<<<1, 256, smem>>>(G, ordp, cpu_r, choice_seed, tabs.lim, tabs.mag, stp, enp, msp);
   LAUNCHED();
   CK(cudaGetLastError());
   if (trace) {

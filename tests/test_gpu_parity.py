@@ -446,7 +446,8 @@ def test_single_reports_specialised_replica(lib, ref, monkeypatch):
     the specialised two-resource replica (csk_event_a2): byte-identical to the
     generic replica and to the reference, for TIC (with ties), TAC and random
     schedules over many choice seeds, including graphs where a third of all
-    durations are zero."""
+    durations are zero — from both of its kernels (graph re-laid in shared
+    memory, or read from the global arrays)."""
     texts = [t for _, t in corpus.worker_graphs(lib)] + [lib.model("resnet_v2_50_inference", 1).serialize()]
     texts += [_zeroed(t, k) for k, t in enumerate(texts[:6])]
     for k, text in enumerate(texts):
@@ -459,10 +460,14 @@ def test_single_reports_specialised_replica(lib, ref, monkeypatch):
                 monkeypatch.delenv("TICTAC_NO_A2", raising=False)
                 a = g.simulate(o, s, pol)
                 fast = (a.json(), a.chrome_trace(), a.makespan(), a.violations())
+                monkeypatch.setenv("TICTAC_A2_GLOBAL", "1")  # the kernel over the global graph arrays
+                c = g.simulate(o, s, pol)
+                fallback = (c.json(), c.chrome_trace(), c.makespan(), c.violations())
+                monkeypatch.delenv("TICTAC_A2_GLOBAL")
                 monkeypatch.setenv("TICTAC_NO_A2", "1")
                 b = g.simulate(o, s, pol)
                 generic = (b.json(), b.chrome_trace(), b.makespan(), b.violations())
-                assert fast == generic, (k, name, seed)
+                assert fast == generic == fallback, (k, name, seed)
         monkeypatch.delenv("TICTAC_NO_A2", raising=False)
         if k % 3 == 0:
             for seed in (0, 5):
