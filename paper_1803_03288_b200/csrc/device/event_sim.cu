@@ -1047,7 +1047,7 @@ struct alignas(16) A2Node {
 
 __host__ __device__ inline size_t a2p_smem(int n, int E, int ncpu, size_t tbytes) {
   const int nw = (ncpu + 31) / 32 + 1;
-  return 8 * 312 + 16ull * kA2Tab + 16ull * n + round16(tbytes * n) + round16(4ull * E) + round16(4ull * ncpu) +
+  return 8 * 312 + 16ull * kA2Tab + 16ull * n + round16(tbytes * n) + round16(4ull * E) + 2 * round16(4ull * ncpu) +
          4ull * nw;
 }
 
@@ -1069,7 +1069,8 @@ __global__ void __launch_bounds__(256) event_a2p_kernel(GraphView G, const int32
   auto* st = reinterpret_cast<Tm*>(node + n);
   auto* succ = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(st) + round16(sizeof(Tm) * n));
   auto* missing = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(succ) + round16(4ull * E));
-  auto* ready = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(missing) + round16(4ull * ncpu));
+  auto* nxt = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(missing) + round16(4ull * ncpu));
+  auto* ready = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(nxt) + round16(4ull * ncpu));
   for (int u = threadIdx.x; u < n; u += blockDim.x) {
     const int op = u < ncpu ? cpu_ops[u] : gate_order[u - ncpu];
     A2Node a;
@@ -1093,6 +1094,15 @@ __global__ void __launch_bounds__(256) event_a2p_kernel(GraphView G, const int32
     const int deg = G.pred_off[op + 1] - G.pred_off[op];
     missing[l] = deg;
     if (deg == 0) atomicOr(&ready[l >> 5], 1u << (l & 31));
+    // chain successor: op's only out-edge goes to an op with one predecessor
+    // and a positive duration (what the unit runs next when nothing else is
+    // ready and the channel completes nothing first)
+    int nx = -1;
+    if (G.succ_off[op + 1] - G.succ_off[op] == 1) {
+      const int w = G.succ_idx[G.succ_off[op]];
+      if (G.pred_off[w + 1] - G.pred_off[w] == 1 && G.dur[w] > 0) nx = G.lidx[w];
+    }
+    nxt[l] = nx;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -1172,6 +1182,18 @@ __global__ void __launch_bounds__(256) event_a2p_kernel(GraphView G, const int32
       if (chan_u < 0 && chan_next < R) {
         start_chan();
         zero |= chan_end == t;
+      }
+      if (!zero && cpu_u >= 0 && ready_cnt == 0) {
+        // Forced picks along a chain: while the running op's only successor
+        // is the next op to become ready and the channel completes nothing
+        // before (or with) it, the rounds in between reduce to "complete it,
+        // start the successor" — no draw, no other state changes.
+        for (int v = nxt[cpu_u]; v >= 0 && (chan_u < 0 || cpu_end < chan_end); v = nxt[v]) {
+          t = cpu_end;
+          cpu_u = v;
+          st[v] = t;
+          cpu_end = t + static_cast<Tm>(node[v].dur);
+        }
       }
       if (zero) {
         if (cpu_u >= 0 && cpu_end == t) {
