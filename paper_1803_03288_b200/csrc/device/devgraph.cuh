@@ -2,7 +2,26 @@
 #pragma once
 
 #include <cstdint>
+#include <memory>
+#include <mutex>
 #include <vector>
+
+// Row structure of the dependency closure (props.cu): ops grouped into rows
+// with identical recv-ancestor sets. Graph-only, so built once per handle.
+struct Rows {
+  int32_t nrows = 0, W = 1;             // W = 32-bit words per row
+  std::vector<int32_t> row_of;          // per op
+  std::vector<int32_t> self_col;        // per row: recv column or -1
+  std::vector<int32_t> pre_off, pre;    // per row: predecessor rows
+  std::vector<int32_t> succ_off, succ;  // per recv column: direct-successor rows (TAC)
+  // Rows with predecessor rows, in topological order, and their closure
+  // terms encoded for closure_seq_kernel: -1 = the previous such row (kept
+  // in a register); -(2 + q) followed by a mask = bits of word q contributed
+  // directly (the row's own column and predecessor rows without predecessors
+  // of their own); else a row index.
+  std::vector<int32_t> nt_row, nt_off, nt_term;
+  std::vector<int32_t> nt_chunk;  // row ranges staged through shared memory together
+};
 
 struct DeviceGraph {
   int32_t n = 0, nres = 0, ndev = 0, R = 0, rb_words = 0;
@@ -18,4 +37,6 @@ struct DeviceGraph {
   std::vector<int32_t> h_pred_off, h_pred_idx, h_succ_off, h_succ_idx, h_res, h_res_dev;
   std::vector<int8_t> h_kind, h_chan;
   std::vector<int32_t> h_recv_ops, h_col;
+  std::mutex rows_mu;
+  std::shared_ptr<const Rows> rows;  // built on first use (props.cu)
 };

@@ -71,14 +71,8 @@ int put(DevArr& a, const std::vector<T>& v, char* err) {
   return 0;
 }
 
-// Host-side row structure (graph-only; built once per call — O(V+E)).
-struct Rows {
-  int32_t nrows = 0, W = 1;             // W = 32-bit words per row
-  std::vector<int32_t> row_of;          // per op
-  std::vector<int32_t> self_col;        // per row: recv column or -1
-  std::vector<int32_t> pre_off, pre;    // per row: predecessor rows
-  std::vector<int32_t> succ_off, succ;  // per recv column: direct-successor rows (TAC)
-};
+// Host-side row structure (graph-only, O(V+E); cached on the graph handle).
+constexpr int kSeqRows = 1024, kSeqTerms = 4096;  // closure_seq_kernel's shared-memory chunk
 
 void build_rows(const DeviceGraph* g, Rows& rw) {
   const int32_t n = g->n;
@@ -115,6 +109,37 @@ void build_rows(const DeviceGraph* g, Rows& rw) {
     rw.pre.insert(rw.pre.end(), tmp.begin(), tmp.end());
     rw.pre_off.push_back(static_cast<int32_t>(rw.pre.size()));
   }
+  rw.nt_off.assign(1, 0);
+  for (int32_t k = 0; k < rw.nrows; ++k) {
+    if (rw.pre_off[k] == rw.pre_off[k + 1]) continue;
+    const int32_t last = rw.nt_row.empty() ? -1 : rw.nt_row.back();
+    tmp.clear();  // recv columns contributed directly: own column, root predecessor rows
+    if (rw.self_col[k] >= 0) tmp.push_back(rw.self_col[k]);
+    for (int32_t e = rw.pre_off[k]; e < rw.pre_off[k + 1]; ++e) {
+      const int32_t p = rw.pre[e];
+      if (p == last) rw.nt_term.push_back(-1);
+      else if (rw.pre_off[p] != rw.pre_off[p + 1]) rw.nt_term.push_back(p);
+      else if (rw.self_col[p] >= 0) tmp.push_back(rw.self_col[p]);
+    }
+    std::sort(tmp.begin(), tmp.end());
+    for (size_t a = 0; a < tmp.size();) {  // one (word, mask) pair per word touched
+      const int32_t q = tmp[a] >> 5;
+      uint32_t mask = 0;
+      for (; a < tmp.size() && (tmp[a] >> 5) == q; ++a) mask |= 1u << (tmp[a] & 31);
+      rw.nt_term.push_back(-2 - q);
+      rw.nt_term.push_back(static_cast<int32_t>(mask));
+    }
+    rw.nt_row.push_back(k);
+    rw.nt_off.push_back(static_cast<int32_t>(rw.nt_term.size()));
+  }
+  const int32_t n_nt = static_cast<int32_t>(rw.nt_row.size());
+  rw.nt_chunk.assign(1, 0);
+  for (int32_t i = 0; i < n_nt;) {  // <= kSeqRows rows and <= kSeqTerms terms (or one oversized row)
+    int32_t j = i + 1;
+    while (j < n_nt && j - i < kSeqRows && rw.nt_off[j + 1] - rw.nt_off[i] <= kSeqTerms) ++j;
+    rw.nt_chunk.push_back(j);
+    i = j;
+  }
   rw.W = std::max(1, (g->R + 31) / 32);
   rw.succ_off.assign(1, 0);
   for (int32_t c = 0; c < g->R; ++c) {
@@ -147,18 +172,62 @@ __global__ void closure_smem_kernel(int32_t nrows, int32_t W, const int32_t* __r
   for (int64_t i = threadIdx.x; i < static_cast<int64_t>(nrows) * W; i += blockDim.x) out[i] = sm[i];
 }
 
-__global__ void closure_global_kernel(int32_t nrows, int32_t W, const int32_t* __restrict__ self_col,
-                                      const int32_t* __restrict__ pre_off,
-                                      const int32_t* __restrict__ pre, uint32_t* __restrict__ out) {
-  const int q = blockIdx.x * blockDim.x + threadIdx.x;
-  if (q >= W) return;
-  for (int32_t k = 0; k < nrows; ++k) {
-    uint32_t w = 0;
-    for (int32_t e = pre_off[k]; e < pre_off[k + 1]; ++e)
-      w |= out[static_cast<int64_t>(pre[e]) * W + q];
+// Large closures: rows without predecessor rows hold their own bit only and
+// are written by one parallel pass; the rows with predecessors follow in
+// topological order, thread q owning word q, with the previous such row's
+// word in a register and bits of root rows folded in from their column — so
+// on backbone/layered DAGs the sequential pass reads no closure words at all.
+__global__ void closure_roots_kernel(int32_t nrows, int32_t W, const int32_t* __restrict__ self_col,
+                                     const int32_t* __restrict__ pre_off, uint32_t* __restrict__ out) {
+  for (int32_t k = blockIdx.x; k < nrows; k += gridDim.x) {
+    if (pre_off[k] != pre_off[k + 1]) continue;
     const int32_t c = self_col[k];
-    if (c >= 0 && (c >> 5) == q) w |= 1u << (c & 31);
-    out[static_cast<int64_t>(k) * W + q] = w;
+    for (int32_t q = threadIdx.x; q < W; q += blockDim.x)
+      out[static_cast<int64_t>(k) * W + q] = c >= 0 && (c >> 5) == q ? 1u << (c & 31) : 0u;
+  }
+}
+
+__global__ void __launch_bounds__(128) closure_seq_kernel(int32_t n_chunks, int32_t W,
+                                                          const int32_t* __restrict__ chunk,
+                                                          const int32_t* __restrict__ nt_row,
+                                                          const int32_t* __restrict__ nt_off,
+                                                          const int32_t* __restrict__ nt_term,
+                                                          uint32_t* __restrict__ out) {
+  // the row metadata is the same for every word: each chunk of rows is
+  // staged once per block, then every thread walks it from shared memory
+  __shared__ int32_t s_off[kSeqRows + 1], s_row[kSeqRows], s_term[kSeqTerms];
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  uint32_t carry = 0;
+  for (int32_t h = 0; h < n_chunks; ++h) {
+    const int32_t i0 = chunk[h], i1 = chunk[h + 1], base = nt_off[i0];
+    const int32_t nterm = nt_off[i1] - base;
+    const bool staged = nterm <= kSeqTerms;
+    for (int32_t j = threadIdx.x; j <= i1 - i0; j += blockDim.x) s_off[j] = nt_off[i0 + j] - base;
+    for (int32_t j = threadIdx.x; j < i1 - i0; j += blockDim.x) s_row[j] = nt_row[i0 + j];
+    if (staged)
+      for (int32_t j = threadIdx.x; j < nterm; j += blockDim.x) s_term[j] = nt_term[base + j];
+    __syncthreads();
+    if (q < W) {
+      const int32_t* term = staged ? s_term : nt_term + base;
+      for (int32_t j = 0; j < i1 - i0; ++j) {
+        uint32_t w = 0;
+        const int32_t e1 = s_off[j + 1];
+        for (int32_t e = s_off[j]; e < e1; ++e) {
+          const int32_t p = term[e];
+          if (p == -1) {
+            w |= carry;
+          } else if (p < -1) {  // (word, mask) pair
+            ++e;
+            if (-2 - p == q) w |= static_cast<uint32_t>(term[e]);
+          } else {
+            w |= out[static_cast<int64_t>(p) * W + q];
+          }
+        }
+        out[static_cast<int64_t>(s_row[j]) * W + q] = w;
+        carry = w;
+      }
+    }
+    __syncthreads();
   }
 }
 
@@ -174,7 +243,9 @@ __global__ void weights_kernel(int32_t n, const int32_t* __restrict__ row_of,
 }
 
 // Per row (warp): cnt, M, xr with every recv outstanding; count col lists.
+// Rows without predecessor rows hold at most their own column: no scan.
 __global__ void rowstate_kernel(int32_t nrows, int32_t W, const uint32_t* __restrict__ bits,
+                                const int32_t* __restrict__ pre_off, const int32_t* __restrict__ self_col,
                                 const int64_t* __restrict__ tcol, const int32_t* __restrict__ has,
                                 int32_t* __restrict__ cnt, int64_t* __restrict__ M,
                                 int32_t* __restrict__ xr, int32_t* __restrict__ colcount) {
@@ -182,6 +253,16 @@ __global__ void rowstate_kernel(int32_t nrows, int32_t W, const uint32_t* __rest
   const int64_t wid = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
   for (int64_t k = wid; k < nrows; k += nw) {
+    if (pre_off[k] == pre_off[k + 1]) {
+      if (lane == 0) {
+        const int32_t c = self_col[k];
+        cnt[k] = c >= 0;
+        M[k] = c >= 0 ? tcol[c] : 0;
+        xr[k] = c >= 0 ? c : 0;
+        if (c >= 0 && has[k]) atomicAdd(&colcount[c], 1);
+      }
+      continue;
+    }
     int c_cnt = 0, c_xr = 0;
     int64_t m = 0;
     for (int q = lane; q < W; q += 32) {
@@ -210,6 +291,7 @@ __global__ void rowstate_kernel(int32_t nrows, int32_t W, const uint32_t* __rest
 }
 
 __global__ void colfill_kernel(int32_t nrows, int32_t W, const uint32_t* __restrict__ bits,
+                               const int32_t* __restrict__ pre_off, const int32_t* __restrict__ self_col,
                                const int32_t* __restrict__ has, int32_t* __restrict__ cursor,
                                int32_t* __restrict__ col) {
   const int lane = threadIdx.x & 31;
@@ -217,6 +299,11 @@ __global__ void colfill_kernel(int32_t nrows, int32_t W, const uint32_t* __restr
   const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
   for (int64_t k = wid; k < nrows; k += nw) {
     if (!has[k]) continue;
+    if (pre_off[k] == pre_off[k + 1]) {
+      const int32_t c = self_col[k];
+      if (lane == 0 && c >= 0) col[atomicAdd(&cursor[c], 1)] = static_cast<int32_t>(k);
+      continue;
+    }
     for (int q = lane; q < W; q += 32) {
       uint32_t w = bits[k * W + q];
       while (w) {
@@ -717,16 +804,24 @@ __global__ void __launch_bounds__(1024) tac_cluster_kernel(TacArgs a, int per) {
 // Shared setup for properties / tic / tac: rows, closure, group state,
 // column lists. `dur` per op (host).
 struct GroupState {
-  Rows rw;
-  DevArr d_self, d_preoff, d_pre, d_bits, d_rowof, d_wsum, d_has, d_cnt, d_M, d_xr, d_colcount,
+  std::shared_ptr<const Rows> rw;
+  DevArr d_self, d_preoff, d_pre, d_ntrow, d_ntoff, d_ntterm, d_ntchunk, d_bits, d_rowof, d_wsum, d_has, d_cnt, d_M, d_xr, d_colcount,
       d_coloff, d_col, d_tcol, d_dur, d_tmp;
   int64_t nnz = 0;
 };
 
 int group_setup(DeviceGraph* g, const int64_t* dur, GroupState& S, char* err) {
   if (ensure_device(err)) return 1;
-  build_rows(g, S.rw);
-  const Rows& rw = S.rw;
+  {
+    std::lock_guard<std::mutex> lock(g->rows_mu);
+    if (!g->rows) {
+      auto r = std::make_shared<Rows>();
+      build_rows(g, *r);
+      g->rows = std::move(r);
+    }
+    S.rw = g->rows;
+  }
+  const Rows& rw = *S.rw;
   const int32_t nrows = std::max(rw.nrows, 1), W = rw.W;
   std::vector<int64_t> tcol(std::max(g->R, 1));
   for (int c = 0; c < g->R; ++c) tcol[c] = dur[g->h_recv_ops[c]];
@@ -751,8 +846,16 @@ int group_setup(DeviceGraph* g, const int64_t* dur, GroupState& S, char* err) {
                                             S.d_preoff.as<int32_t>(), S.d_pre.as<int32_t>(),
                                             S.d_bits.as<uint32_t>());
     } else {
-      closure_global_kernel<<<(W + 127) / 128, 128>>>(rw.nrows, W, S.d_self.as<int32_t>(),
-                                                     S.d_preoff.as<int32_t>(), S.d_pre.as<int32_t>(),
+      if (put(S.d_ntrow, rw.nt_row, err) || put(S.d_ntoff, rw.nt_off, err) ||
+          put(S.d_ntterm, rw.nt_term, err) || put(S.d_ntchunk, rw.nt_chunk, err))
+        return 1;
+      closure_roots_kernel<<<std::min(rw.nrows, 148 * 16), 256>>>(rw.nrows, W, S.d_self.as<int32_t>(),
+                                                                  S.d_preoff.as<int32_t>(), S.d_bits.as<uint32_t>());
+      LAUNCHED();
+      if (!rw.nt_row.empty())
+        closure_seq_kernel<<<(W + 127) / 128, 128>>>(static_cast<int32_t>(rw.nt_chunk.size()) - 1, W,
+                                                     S.d_ntchunk.as<int32_t>(), S.d_ntrow.as<int32_t>(),
+                                                     S.d_ntoff.as<int32_t>(), S.d_ntterm.as<int32_t>(),
                                                      S.d_bits.as<uint32_t>());
     }
     LAUNCHED();
@@ -764,7 +867,8 @@ int group_setup(DeviceGraph* g, const int64_t* dur, GroupState& S, char* err) {
   LAUNCHED();
   const int rblocks = std::max(1, std::min((rw.nrows * 32 + 255) / 256, 2368));
   if (rw.nrows > 0) {
-    rowstate_kernel<<<rblocks, 256>>>(rw.nrows, W, S.d_bits.as<uint32_t>(), S.d_tcol.as<int64_t>(),
+    rowstate_kernel<<<rblocks, 256>>>(rw.nrows, W, S.d_bits.as<uint32_t>(), S.d_preoff.as<int32_t>(),
+                                      S.d_self.as<int32_t>(), S.d_tcol.as<int64_t>(),
                                       S.d_has.as<int32_t>(), S.d_cnt.as<int32_t>(),
                                       S.d_M.as<int64_t>(), S.d_xr.as<int32_t>(),
                                       S.d_colcount.as<int32_t>());
@@ -785,7 +889,8 @@ int group_setup(DeviceGraph* g, const int64_t* dur, GroupState& S, char* err) {
   if (alloc<int32_t>(S.d_col, nnz, err)) return 1;
   CK(cudaMemcpy(S.d_colcount.p, S.d_coloff.p, 4ull * (g->R + 1), cudaMemcpyDeviceToDevice));
   if (rw.nrows > 0) {
-    colfill_kernel<<<rblocks, 256>>>(rw.nrows, W, S.d_bits.as<uint32_t>(), S.d_has.as<int32_t>(),
+    colfill_kernel<<<rblocks, 256>>>(rw.nrows, W, S.d_bits.as<uint32_t>(), S.d_preoff.as<int32_t>(),
+                                     S.d_self.as<int32_t>(), S.d_has.as<int32_t>(),
                                      S.d_colcount.as<int32_t>(), S.d_col.as<int32_t>());
     LAUNCHED();
   }
@@ -830,15 +935,15 @@ extern "C" int csk_properties(DeviceGraph* g, const int64_t* dur, int mode, uint
     CK(cudaMemcpy(Mplus, d_Mp.p, 8ull * R, cudaMemcpyDeviceToHost));
   }
   // per-op rows back to the host formatter
-  const int W = S.rw.W, w64 = std::max(1, (R + 63) / 64);
-  std::vector<uint32_t> bits(static_cast<size_t>(std::max(S.rw.nrows, 1)) * W);
-  std::vector<int64_t> rowM(std::max(S.rw.nrows, 1));
-  if (S.rw.nrows > 0) {
-    CK(cudaMemcpy(bits.data(), S.d_bits.p, 4ull * S.rw.nrows * W, cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(rowM.data(), S.d_M.p, 8ull * S.rw.nrows, cudaMemcpyDeviceToHost));
+  const int W = S.rw->W, w64 = std::max(1, (R + 63) / 64);
+  std::vector<uint32_t> bits(static_cast<size_t>(std::max(S.rw->nrows, 1)) * W);
+  std::vector<int64_t> rowM(std::max(S.rw->nrows, 1));
+  if (S.rw->nrows > 0) {
+    CK(cudaMemcpy(bits.data(), S.d_bits.p, 4ull * S.rw->nrows * W, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(rowM.data(), S.d_M.p, 8ull * S.rw->nrows, cudaMemcpyDeviceToHost));
   }
   for (int32_t v = 0; v < g->n; ++v) {
-    const int32_t k = S.rw.row_of[v];
+    const int32_t k = S.rw->row_of[v];
     uint64_t* dst = dep_bits + static_cast<size_t>(v) * w64;
     for (int q = 0; q < w64; ++q) dst[q] = 0;
     for (int q = 0; q < W; ++q)
@@ -900,7 +1005,7 @@ extern "C" int csk_tac(DeviceGraph* g, const int64_t* dur, int32_t* prio, char* 
   const auto t1 = now();
   DevArr d_P, d_Mp, d_out, d_prio, d_succoff, d_succ;
   if (alloc<int64_t>(d_P, R, err) || alloc<int64_t>(d_Mp, R, err) || alloc<uint8_t>(d_out, R, err) ||
-      alloc<int32_t>(d_prio, R, err) || put(d_succoff, S.rw.succ_off, err) || put(d_succ, S.rw.succ, err))
+      alloc<int32_t>(d_prio, R, err) || put(d_succoff, S.rw->succ_off, err) || put(d_succ, S.rw->succ, err))
     return 1;
   CK(cudaMemset(d_out.p, 1, R));
   // initial P (amended M+ is recomputed inside the rounds)
@@ -977,7 +1082,7 @@ extern "C" int csk_tac(DeviceGraph* g, const int64_t* dur, int32_t* prio, char* 
     }
     return false;
   };
-  int32_t smem_rows = S.rw.nrows, smem_succ = static_cast<int>(S.rw.succ.size());
+  int32_t smem_rows = S.rw->nrows, smem_succ = static_cast<int>(S.rw->succ.size());
   const bool one_block_fits = tac_smem_bytes(smem_rows, R, smem_succ) <= 220 * 1024;
   bool launched = false;
   // (measured: 10^5 ops / 10^4 recvs 61 → 55 ms; at 10^6 / 10^5 the grid
@@ -986,7 +1091,7 @@ extern "C" int csk_tac(DeviceGraph* g, const int64_t* dur, int32_t* prio, char* 
   if (launched) {
     // (cluster kernel in flight; completion below)
   } else if (blocks == 1) {
-    int nrows = S.rw.nrows, nsucc = static_cast<int>(S.rw.succ.size());
+    int nrows = S.rw->nrows, nsucc = static_cast<int>(S.rw->succ.size());
     size_t smem = tac_smem_bytes(nrows, R, nsucc);
     constexpr size_t kSmemMax = 220 * 1024;
     // column lists in shared memory too when 16-bit row ids fit beside the state
@@ -1061,12 +1166,12 @@ extern "C" int csk_tac_stats(DeviceGraph* g, const int64_t* dur, int64_t* out, c
   if (g->R == 0) return 0;
   GroupState S;
   if (group_setup(g, dur, S, err)) return 1;
-  std::vector<int32_t> cnt(std::max(S.rw.nrows, 1));
-  if (S.rw.nrows > 0) CK(cudaMemcpy(cnt.data(), S.d_cnt.p, 4ull * S.rw.nrows, cudaMemcpyDeviceToHost));
+  std::vector<int32_t> cnt(std::max(S.rw->nrows, 1));
+  if (S.rw->nrows > 0) CK(cudaMemcpy(cnt.data(), S.d_cnt.p, 4ull * S.rw->nrows, cudaMemcpyDeviceToHost));
   int64_t nnz = 0;
-  for (int32_t v = 0; v < g->n; ++v) nnz += g->h_kind[v] == 1 ? 1 : cnt[S.rw.row_of[v]];
+  for (int32_t v = 0; v < g->n; ++v) nnz += g->h_kind[v] == 1 ? 1 : cnt[S.rw->row_of[v]];
   out[4] = nnz;
-  out[5] = S.rw.nrows;
+  out[5] = S.rw->nrows;
   out[6] = S.nnz;
   return 0;
 }

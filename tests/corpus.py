@@ -68,6 +68,29 @@ def irregular_worker(seed: int, n_comp=14, n_recv=6, n_send=2, cpus=2, chans=2):
     return json.dumps({"name": f"irregular-w{seed}", "partition": "worker", "ops": ops, "edges": edges})
 
 
+def wide_fanin(seed: int, n_recv=5000):
+    """Worker graph whose dependency closure takes the large (global-memory)
+    path with every kind of closure term: an op fed by every recv (more terms
+    than one shared-memory chunk), ops fed by the previous row, by earlier
+    non-root rows and by recv subsets."""
+    import json
+    import random
+    rnd = random.Random(seed)
+    recvs = [f"r{k:04d}" for k in range(n_recv)]
+    ops = [_op(r, "recv", "w0", "channel", "net0", rnd.randint(1, 9)) for r in recvs]
+    comps = [f"c{k:02d}" for k in range(24)]
+    edges = [[r, comps[0]] for r in recvs]
+    for k, c in enumerate(comps):
+        ops.append(_op(c, "compute", "w0", "compute", "cpu0", rnd.randint(0, 9)))
+        if k == 0:
+            continue
+        preds = {comps[k - 1]} if k % 3 else set(rnd.sample(comps[:k], min(k, 2)))
+        preds |= set(rnd.sample(recvs, rnd.randint(0, 40)))
+        edges += [[p, c] for p in sorted(preds)]
+    rnd.shuffle(ops)
+    return json.dumps({"name": f"wide-fanin{seed}", "partition": "worker", "ops": ops, "edges": edges})
+
+
 def irregular_cluster(seed: int, workers=2, n_comp=8, n_recv=4):
     """Cluster partition where worker recvs have predecessors (PS reads) and
     sends feed PS aggregation: recvs are not roots, per-worker resources

@@ -441,6 +441,18 @@ def _zeroed(text, seed, frac=3):
     return json.dumps(d)
 
 
+def test_large_closure_path_matches_reference(lib, ref):
+    """Closures too large for one block's shared memory (roots written in
+    parallel, the other rows in topological order from staged terms,
+    including a row with more terms than one staged chunk): TIC in both
+    modes and the property tables match the reference library."""
+    for seed in (1, 2):
+        text = corpus.wide_fanin(seed)
+        for mode in ("amended", "literal"):
+            _both(lib, ref, text, lambda L, g: g.tic(mode).serialize() + str(g.tic(mode).total_order()))
+            _both(lib, ref, text, lambda L, g: g.properties_text(g.declared(), mode))
+
+
 def test_single_reports_specialised_replica(lib, ref, monkeypatch):
     """Event lists of single runs inside the closed form's regime come from
     the specialised two-resource replica (csk_event_a2): byte-identical to the

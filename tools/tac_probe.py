@@ -13,6 +13,11 @@ t = time.perf_counter()
 if which == "tac":
     s = g.tac(o)
     print("tac", len(s.priorities()), time.perf_counter() - t)
+elif which == "tic":
+    g.tic("amended")  # warm
+    t = time.perf_counter()
+    s = g.tic("amended")
+    print("tic", time.perf_counter() - t)
 else:
     s = g.tac(o)
     r = g.simulate(o, s, policy(True, 1, 0.0))
