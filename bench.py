@@ -274,8 +274,9 @@ def cpu_baseline(path, target_s=10.0, g=None, o=None):
 def tac_times(lib, top=False, hbm=None):
     """TAC wall time through cs_schedule_tac (device), seconds; SURVEY §8d
     configs 1, 2, 4 and the config-5 layered sweep. With `hbm`, also the
-    SURVEY's algorithmic bytes B_TAC (cs_tac_traffic) over that time."""
-    out, roof, tic = {}, {}, {}
+    SURVEY's algorithmic bytes B_TAC and B_TIC (cs_tac_traffic) over those
+    times."""
+    out, roof, tic, tic_roof = {}, {}, {}, {}
     names = ["resnet_v2_50_inference", "inception_v3_training", "resnet_v2_101_training",
              "layered:10000:1000", "layered:100000:10000"] + (["layered:1000000:100000"] if top else [])
     for name in names:
@@ -288,13 +289,16 @@ def tac_times(lib, top=False, hbm=None):
         out[name] = round(dt, 6)
         t = time.perf_counter()
         g.tic("amended")
-        tic[name] = round(time.perf_counter() - t, 6)
+        dt_tic = time.perf_counter() - t
+        tic[name] = round(dt_tic, 6)
         if hbm:
             tr = g.tac_traffic(o)
             gbs = tr["B_TAC"] / dt / 1e9
             roof[name] = {"B_TAC_bytes": tr["B_TAC"], "achieved_GBps": gbs, "frac_hbm": gbs / hbm,
                           "nnz": tr["nnz"], "row_nnz": tr["row_nnz"], "rows": tr["rows"]}
-    return (out, roof, tic) if hbm else out
+            gbs = tr["B_TIC"] / dt_tic / 1e9
+            tic_roof[name] = {"B_TIC_bytes": tr["B_TIC"], "achieved_GBps": gbs, "frac_hbm": gbs / hbm}
+    return (out, roof, tic, tic_roof) if hbm else out
 
 
 def sweep_rate(g, o, count):
@@ -629,8 +633,8 @@ def main():
             "roofline_smem": smem_roof,
         }
         if not args.no_tac:
-            out["tac_seconds"], out["tac_roofline"], out["tic_amended_seconds"] = tac_times(
-                lib, top=args.config5_top, hbm=hbm)
+            (out["tac_seconds"], out["tac_roofline"], out["tic_amended_seconds"],
+             out["tic_roofline"]) = tac_times(lib, top=args.config5_top, hbm=hbm)
             if world > 1:
                 out["tac_note"] = ("TAC is R dependent rounds and runs on one GPU (rank 0) at any N: a "
                                    "sharded round would add an NCCL all-reduce (16-29 us measured over NVLink, "

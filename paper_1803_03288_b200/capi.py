@@ -284,14 +284,15 @@ class Graph(_Handle):
 
     def tac_traffic(self, oracle: "Oracle") -> dict:
         """SURVEY §8d TAC traffic terms from the device closure, plus B_TAC
-        (algorithmic bytes of one whole TAC ordering)."""
+        (algorithmic bytes of one whole TAC ordering) and B_TIC (one TIC)."""
         out = (C.c_int64 * 7)()
         self.lib.call("cs_tac_traffic", self.h, oracle.h, out, 7)
         V, R, E, E_recv, nnz, rows, row_nnz = (int(x) for x in out)
         words = (R + 31) // 32
         b_tac = 4 * V * words + 20 * V * R + 6 * E_recv * (R + 1) + 12 * R * (R + 1) + 32 * nnz
+        b_tic = 4 * V * words + 20 * V + 12 * E_recv + 24 * R
         return {"V": V, "R": R, "E": E, "E_recv": E_recv, "nnz": nnz, "rows": rows,
-                "row_nnz": row_nnz, "B_TAC": b_tac}
+                "row_nnz": row_nnz, "B_TAC": b_tac, "B_TIC": b_tic}
 
     def metrics_text(self, oracle: "Oracle", report: "Report") -> str:
         p = C.c_void_p()

@@ -21,6 +21,7 @@ struct Rows {
   // of their own); else a row index.
   std::vector<int32_t> nt_row, nt_off, nt_term;
   std::vector<int32_t> nt_chunk;  // row ranges staged through shared memory together
+  std::vector<int32_t> has_rows;  // rows with compute members (column-list entries), ascending
 };
 
 struct DeviceGraph {

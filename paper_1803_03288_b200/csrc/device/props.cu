@@ -132,6 +132,13 @@ void build_rows(const DeviceGraph* g, Rows& rw) {
     rw.nt_row.push_back(k);
     rw.nt_off.push_back(static_cast<int32_t>(rw.nt_term.size()));
   }
+  {
+    std::vector<uint8_t> has(rw.nrows, 0);
+    for (int32_t v = 0; v < n; ++v)
+      if (g->h_kind[v] != 1) has[rw.row_of[v]] = 1;
+    for (int32_t k = 0; k < rw.nrows; ++k)
+      if (has[k]) rw.has_rows.push_back(k);
+  }
   const int32_t n_nt = static_cast<int32_t>(rw.nt_row.size());
   rw.nt_chunk.assign(1, 0);
   for (int32_t i = 0; i < n_nt;) {  // <= kSeqRows rows and <= kSeqTerms terms (or one oversized row)
@@ -242,13 +249,13 @@ __global__ void weights_kernel(int32_t n, const int32_t* __restrict__ row_of,
   }
 }
 
-// Per row (warp): cnt, M, xr with every recv outstanding; count col lists.
-// Rows without predecessor rows hold at most their own column: no scan.
+// Per row (warp): cnt, M, xr with every recv outstanding. Rows without
+// predecessor rows hold at most their own column: no scan.
 __global__ void rowstate_kernel(int32_t nrows, int32_t W, const uint32_t* __restrict__ bits,
                                 const int32_t* __restrict__ pre_off, const int32_t* __restrict__ self_col,
                                 const int64_t* __restrict__ tcol, const int32_t* __restrict__ has,
                                 int32_t* __restrict__ cnt, int64_t* __restrict__ M,
-                                int32_t* __restrict__ xr, int32_t* __restrict__ colcount) {
+                                int32_t* __restrict__ xr) {
   const int lane = threadIdx.x & 31;
   const int64_t wid = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
@@ -259,7 +266,6 @@ __global__ void rowstate_kernel(int32_t nrows, int32_t W, const uint32_t* __rest
         cnt[k] = c >= 0;
         M[k] = c >= 0 ? tcol[c] : 0;
         xr[k] = c >= 0 ? c : 0;
-        if (c >= 0 && has[k]) atomicAdd(&colcount[c], 1);
       }
       continue;
     }
@@ -273,7 +279,6 @@ __global__ void rowstate_kernel(int32_t nrows, int32_t W, const uint32_t* __rest
         ++c_cnt;
         c_xr ^= c;
         m += tcol[c];
-        if (has[k]) atomicAdd(&colcount[c], 1);
       }
     }
 #pragma unroll
@@ -290,49 +295,106 @@ __global__ void rowstate_kernel(int32_t nrows, int32_t W, const uint32_t* __rest
   }
 }
 
-__global__ void colfill_kernel(int32_t nrows, int32_t W, const uint32_t* __restrict__ bits,
-                               const int32_t* __restrict__ pre_off, const int32_t* __restrict__ self_col,
-                               const int32_t* __restrict__ has, int32_t* __restrict__ cursor,
-                               int32_t* __restrict__ col) {
-  const int lane = threadIdx.x & 31;
+// Column lists (recv column -> rows with compute members whose closure holds
+// it) without atomics. A warp owns one closure word q (32 columns) over one
+// chunk of the rows with compute members and walks it 32 rows at a time:
+// lane i loads row i's word, and per column j a ballot gives the rows that
+// hold it. Pass 1 counts per (chunk, column); a per-column scan over chunks
+// turns counts into offsets; pass 2 writes each ballot as one contiguous run,
+// so every list comes out in ascending row order with coalesced stores.
+__global__ void colcount_warp_kernel(int32_t nhas, int32_t W, int32_t R, int32_t nchunks, int32_t chunk_rows,
+                                     const uint32_t* __restrict__ bits, const int32_t* __restrict__ has_rows,
+                                     int32_t* __restrict__ counts) {
   const int64_t wid = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
-  for (int64_t k = wid; k < nrows; k += nw) {
-    if (!has[k]) continue;
-    if (pre_off[k] == pre_off[k + 1]) {
-      const int32_t c = self_col[k];
-      if (lane == 0 && c >= 0) col[atomicAdd(&cursor[c], 1)] = static_cast<int32_t>(k);
-      continue;
+  const int lane = threadIdx.x & 31;
+  if (wid >= static_cast<int64_t>(W) * nchunks) return;
+  const int q = static_cast<int>(wid % W), h = static_cast<int>(wid / W);
+  const int32_t i1 = min(nhas, (h + 1) * chunk_rows);
+  int32_t cnt = 0;
+  for (int32_t i0 = h * chunk_rows; i0 < i1; i0 += 32) {
+    const int32_t i = i0 + lane;
+    const uint32_t w = i < i1 ? bits[static_cast<int64_t>(has_rows[i]) * W + q] : 0u;
+#pragma unroll 8
+    for (int j = 0; j < 32; ++j) {
+      const uint32_t b = __ballot_sync(~0u, (w >> j) & 1u);
+      if (lane == j) cnt += __popc(b);
     }
-    for (int q = lane; q < W; q += 32) {
-      uint32_t w = bits[k * W + q];
-      while (w) {
-        const int c = (q << 5) + __ffs(w) - 1;
-        w &= w - 1;
-        col[atomicAdd(&cursor[c], 1)] = static_cast<int32_t>(k);
-      }
+  }
+  const int c = q * 32 + lane;
+  if (c < R) counts[static_cast<int64_t>(h) * R + c] = cnt;
+}
+
+__global__ void colprefix_kernel(int32_t R, int32_t nchunks, int32_t* __restrict__ counts,
+                                 int32_t* __restrict__ colcount) {
+  for (int32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < R; c += gridDim.x * blockDim.x) {
+    int32_t run = 0;
+    for (int32_t h = 0; h < nchunks; ++h) {
+      int32_t* p = counts + static_cast<int64_t>(h) * R + c;
+      const int32_t v = *p;
+      *p = run;
+      run += v;
+    }
+    colcount[c] = run;
+  }
+}
+
+__global__ void colfill_warp_kernel(int32_t nhas, int32_t W, int32_t R, int32_t nchunks, int32_t chunk_rows,
+                                    const uint32_t* __restrict__ bits, const int32_t* __restrict__ has_rows,
+                                    const int32_t* __restrict__ counts, const int32_t* __restrict__ coloff,
+                                    int32_t* __restrict__ col) {
+  const int64_t wid = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (wid >= static_cast<int64_t>(W) * nchunks) return;
+  const int q = static_cast<int>(wid % W), h = static_cast<int>(wid / W);
+  const int32_t i1 = min(nhas, (h + 1) * chunk_rows);
+  const int c = q * 32 + lane;
+  int32_t pos = c < R ? coloff[c] + counts[static_cast<int64_t>(h) * R + c] : 0;  // lane j: column q*32+j
+  const uint32_t below = (1u << lane) - 1u;
+  for (int32_t i0 = h * chunk_rows; i0 < i1; i0 += 32) {
+    const int32_t i = i0 + lane;
+    const int32_t k = i < i1 ? has_rows[i] : 0;
+    const uint32_t w = i < i1 ? bits[static_cast<int64_t>(k) * W + q] : 0u;
+#pragma unroll 4
+    for (int j = 0; j < 32; ++j) {
+      const uint32_t b = __ballot_sync(~0u, (w >> j) & 1u);
+      if (!b) continue;
+      const int32_t at = __shfl_sync(~0u, pos, j);
+      if ((w >> j) & 1u) col[at + __popc(b & below)] = k;
+      if (lane == j) pos += __popc(b);
     }
   }
 }
 
-// P and M+ with every recv outstanding (properties.cpp:92-107 on groups).
+// P and M+ with every recv outstanding (properties.cpp:92-107 on groups):
+// a warp per recv column, lanes striding its (ascending) row list.
 __global__ void props_kernel(int32_t R, int amended, const int32_t* __restrict__ col_off,
                              const int32_t* __restrict__ col, const int32_t* __restrict__ cnt,
                              const int64_t* __restrict__ M, const int32_t* __restrict__ xr,
                              const unsigned long long* __restrict__ wsum, int64_t* __restrict__ P,
                              int64_t* __restrict__ Mp) {
-  for (int32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < R; c += gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t c = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; c < R; c += nw) {
     int64_t mp = kInf, p = 0;
-    for (int32_t e = col_off[c]; e < col_off[c + 1]; ++e) {
+    for (int32_t e = col_off[c] + lane; e < col_off[c + 1]; e += 32) {
       const int32_t g = col[e];
       const int k = cnt[g];
       if (k >= 2 || (amended && k == 1)) mp = min(mp, M[g]);
       if (k == 1 && xr[g] == c) p += static_cast<int64_t>(wsum[g]);
     }
-    P[c] = p;
-    Mp[c] = mp;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      p += __shfl_xor_sync(~0u, p, o);
+      mp = min(mp, __shfl_xor_sync(~0u, mp, o));
+    }
+    if (lane == 0) {
+      P[c] = p;
+      Mp[c] = mp;
+    }
   }
 }
+
+inline int props_blocks(int32_t R) { return std::max(1, std::min((R * 32 + 255) / 256, 148 * 16)); }
 
 // precedes (schedule.cpp:12-19); kInf = nullopt sorts last.
 __device__ __forceinline__ bool precedes(int a, int64_t ap, int64_t am, int64_t amp, int b, int64_t bp,
@@ -805,7 +867,8 @@ __global__ void __launch_bounds__(1024) tac_cluster_kernel(TacArgs a, int per) {
 // column lists. `dur` per op (host).
 struct GroupState {
   std::shared_ptr<const Rows> rw;
-  DevArr d_self, d_preoff, d_pre, d_ntrow, d_ntoff, d_ntterm, d_ntchunk, d_bits, d_rowof, d_wsum, d_has, d_cnt, d_M, d_xr, d_colcount,
+  DevArr d_self, d_preoff, d_pre, d_ntrow, d_ntoff, d_ntterm, d_ntchunk, d_counts, d_hasrows,
+      d_bits, d_rowof, d_wsum, d_has, d_cnt, d_M, d_xr, d_colcount,
       d_coloff, d_col, d_tcol, d_dur, d_tmp;
   int64_t nnz = 0;
 };
@@ -866,13 +929,30 @@ int group_setup(DeviceGraph* g, const int64_t* dur, GroupState& S, char* err) {
       S.d_has.as<int32_t>());
   LAUNCHED();
   const int rblocks = std::max(1, std::min((rw.nrows * 32 + 255) / 256, 2368));
+  // column-list warps: one per (closure word, chunk of rows with compute
+  // members), enough of them to fill the GPU
+  const int32_t nhas = static_cast<int32_t>(rw.has_rows.size());
+  int32_t nchunks = std::max(1, std::min((nhas + 31) / 32, (148 * 64 + W - 1) / W));
+  const int32_t chunk_rows = std::max(32, ((nhas + nchunks - 1) / nchunks + 31) / 32 * 32);
+  nchunks = std::max(1, (nhas + chunk_rows - 1) / chunk_rows);
+  const int64_t cwarps = static_cast<int64_t>(W) * nchunks;
+  const int cblocks = static_cast<int>((cwarps * 32 + 255) / 256);
+  if (put(S.d_hasrows, rw.has_rows, err)) return 1;
+  if (alloc<int32_t>(S.d_counts, static_cast<size_t>(nchunks) * std::max(g->R, 1), err)) return 1;
   if (rw.nrows > 0) {
     rowstate_kernel<<<rblocks, 256>>>(rw.nrows, W, S.d_bits.as<uint32_t>(), S.d_preoff.as<int32_t>(),
                                       S.d_self.as<int32_t>(), S.d_tcol.as<int64_t>(),
                                       S.d_has.as<int32_t>(), S.d_cnt.as<int32_t>(),
-                                      S.d_M.as<int64_t>(), S.d_xr.as<int32_t>(),
-                                      S.d_colcount.as<int32_t>());
+                                      S.d_M.as<int64_t>(), S.d_xr.as<int32_t>());
     LAUNCHED();
+    if (g->R > 0) {
+      colcount_warp_kernel<<<cblocks, 256>>>(nhas, W, g->R, nchunks, chunk_rows, S.d_bits.as<uint32_t>(),
+                                             S.d_hasrows.as<int32_t>(), S.d_counts.as<int32_t>());
+      LAUNCHED();
+      colprefix_kernel<<<std::max(1, std::min((g->R + 255) / 256, 1184)), 256>>>(
+          g->R, nchunks, S.d_counts.as<int32_t>(), S.d_colcount.as<int32_t>());
+      LAUNCHED();
+    }
   }
   CK(cudaGetLastError());
   // exclusive scan of column counts -> offsets (R+1 entries)
@@ -887,11 +967,10 @@ int group_setup(DeviceGraph* g, const int64_t* dur, GroupState& S, char* err) {
   CK(cudaMemcpy(&nnz, S.d_coloff.as<int32_t>() + g->R, 4, cudaMemcpyDeviceToHost));
   S.nnz = nnz;
   if (alloc<int32_t>(S.d_col, nnz, err)) return 1;
-  CK(cudaMemcpy(S.d_colcount.p, S.d_coloff.p, 4ull * (g->R + 1), cudaMemcpyDeviceToDevice));
-  if (rw.nrows > 0) {
-    colfill_kernel<<<rblocks, 256>>>(rw.nrows, W, S.d_bits.as<uint32_t>(), S.d_preoff.as<int32_t>(),
-                                     S.d_self.as<int32_t>(), S.d_has.as<int32_t>(),
-                                     S.d_colcount.as<int32_t>(), S.d_col.as<int32_t>());
+  if (rw.nrows > 0 && g->R > 0) {
+    colfill_warp_kernel<<<cblocks, 256>>>(nhas, W, g->R, nchunks, chunk_rows, S.d_bits.as<uint32_t>(),
+                                          S.d_hasrows.as<int32_t>(), S.d_counts.as<int32_t>(),
+                                          S.d_coloff.as<int32_t>(), S.d_col.as<int32_t>());
     LAUNCHED();
   }
   CK(cudaGetLastError());
@@ -925,7 +1004,7 @@ extern "C" int csk_properties(DeviceGraph* g, const int64_t* dur, int mode, uint
   DevArr d_P, d_Mp;
   if (alloc<int64_t>(d_P, R, err) || alloc<int64_t>(d_Mp, R, err)) return 1;
   if (R > 0) {
-    props_kernel<<<std::max(1, std::min((R + 255) / 256, 1184)), 256>>>(
+    props_kernel<<<props_blocks(R), 256>>>(
         R, mode, S.d_coloff.as<int32_t>(), S.d_col.as<int32_t>(), S.d_cnt.as<int32_t>(),
         S.d_M.as<int64_t>(), S.d_xr.as<int32_t>(), S.d_wsum.as<unsigned long long>(),
         d_P.as<int64_t>(), d_Mp.as<int64_t>());
@@ -965,7 +1044,7 @@ extern "C" int csk_tic(DeviceGraph* g, int mode, int32_t* prio, int* total, char
   if (alloc<int64_t>(d_P, R, err) || alloc<int64_t>(d_Mp, R, err) || alloc<int64_t>(d_sorted, R, err) ||
       alloc<int64_t>(d_unique, R, err) || alloc<int32_t>(d_nu, 1, err) || alloc<int32_t>(d_prio, R, err))
     return 1;
-  props_kernel<<<std::max(1, std::min((R + 255) / 256, 1184)), 256>>>(
+  props_kernel<<<props_blocks(R), 256>>>(
       R, mode, S.d_coloff.as<int32_t>(), S.d_col.as<int32_t>(), S.d_cnt.as<int32_t>(),
       S.d_M.as<int64_t>(), S.d_xr.as<int32_t>(), S.d_wsum.as<unsigned long long>(), d_P.as<int64_t>(),
       d_Mp.as<int64_t>());
@@ -1009,7 +1088,7 @@ extern "C" int csk_tac(DeviceGraph* g, const int64_t* dur, int32_t* prio, char* 
     return 1;
   CK(cudaMemset(d_out.p, 1, R));
   // initial P (amended M+ is recomputed inside the rounds)
-  props_kernel<<<std::max(1, std::min((R + 255) / 256, 1184)), 256>>>(
+  props_kernel<<<props_blocks(R), 256>>>(
       R, 1, S.d_coloff.as<int32_t>(), S.d_col.as<int32_t>(), S.d_cnt.as<int32_t>(), S.d_M.as<int64_t>(),
       S.d_xr.as<int32_t>(), S.d_wsum.as<unsigned long long>(), d_P.as<int64_t>(), d_Mp.as<int64_t>());
   LAUNCHED();

@@ -68,7 +68,9 @@ static Schedule ranks_to_schedule(const Graph& g, const char* algo, const std::v
   s.graph = g.name();
   s.algorithm = algo;
   const auto& ro = g.recv_ops();
-  for (size_t c = 0; c < ro.size(); ++c) s.prio[g.ops()[ro[c]].id] = pr[c];
+  // recv columns follow op index = byte-lexicographic id order, which is the
+  // map's order: append with an end hint (amortised O(1) per recv)
+  for (size_t c = 0; c < ro.size(); ++c) s.prio.emplace_hint(s.prio.end(), g.ops()[ro[c]].id, pr[c]);
   s.total = total;
   return s;
 }
