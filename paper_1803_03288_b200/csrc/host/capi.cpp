@@ -255,7 +255,7 @@ int cs_oracle_declared(const cs_graph* g, cs_oracle** out) {
   return guarded([&] {
     need(g, "graph");
     need(out, "out");
-    *out = new cs_oracle{TimeOracle::declared(*g->g)};
+    *out = new cs_oracle{TimeOracle::declared(g->g)};
   });
 }
 
@@ -263,7 +263,7 @@ int cs_oracle_general(const cs_graph* g, cs_oracle** out) {
   return guarded([&] {
     need(g, "graph");
     need(out, "out");
-    *out = new cs_oracle{TimeOracle::general(*g->g)};
+    *out = new cs_oracle{TimeOracle::general(g->g)};
   });
 }
 
@@ -272,7 +272,7 @@ int cs_oracle_from_traces(const cs_graph* g, const char* trace_jsonl, cs_oracle*
     need(g, "graph");
     need(trace_jsonl, "trace_jsonl");
     need(out, "out");
-    *out = new cs_oracle{TimeOracle::traces(*g->g, trace_jsonl)};
+    *out = new cs_oracle{TimeOracle::traces(g->g, trace_jsonl)};
   });
 }
 
@@ -280,7 +280,7 @@ int cs_oracle_bandwidth(const cs_graph* g, int64_t bytes_per_us, cs_oracle** out
   return guarded([&] {
     need(g, "graph");
     need(out, "out");
-    *out = new cs_oracle{TimeOracle::bandwidth(*g->g, bytes_per_us)};
+    *out = new cs_oracle{TimeOracle::bandwidth(g->g, bytes_per_us)};
   });
 }
 

@@ -132,13 +132,19 @@ class Graph {
 };
 
 // Total map op id -> microseconds (time_oracle.hpp:28-58).
+// The reference keeps an id -> µs map (time_oracle.hpp:28-58). Every oracle
+// is built from one graph and covers exactly its ops, so here it keeps that
+// graph and the values by its op index (= id order): durations() for the same
+// graph is a copy, for another graph one merge walk over the two id-ordered
+// op lists, and to_json iterates in the map's order without building it.
 struct TimeOracle {
-  std::map<std::string, int64_t> entries;
-  std::string origin;  // measured | declared | general | synthetic
-  static TimeOracle declared(const Graph& g);
-  static TimeOracle general(const Graph& g);
-  static TimeOracle traces(const Graph& g, std::string_view jsonl);
-  static TimeOracle bandwidth(const Graph& g, int64_t bytes_per_us);
+  std::shared_ptr<const Graph> src;
+  std::vector<int64_t> us;  // by src op index
+  std::string origin;       // measured | declared | general | synthetic
+  static TimeOracle declared(std::shared_ptr<const Graph> g);
+  static TimeOracle general(std::shared_ptr<const Graph> g);
+  static TimeOracle traces(std::shared_ptr<const Graph> g, std::string_view jsonl);
+  static TimeOracle bandwidth(std::shared_ptr<const Graph> g, int64_t bytes_per_us);
   // check_covers (time_oracle.cpp:143-149), then durations by op index.
   std::vector<int64_t> durations(const Graph& g) const;
   Json to_json() const;

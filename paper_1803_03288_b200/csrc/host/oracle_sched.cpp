@@ -14,31 +14,32 @@ static std::string joined(const std::vector<std::string>& ids) {
   return s;
 }
 
-static TimeOracle checked(std::map<std::string, int64_t> e, const char* origin) {
+static TimeOracle checked(std::shared_ptr<const Graph> g, std::vector<int64_t> us, const char* origin) {
   // time_oracle.cpp:64-70: every entry must be non-negative.
-  for (const auto& [id, us] : e)
-    if (us < 0) fail(kValidation, "oracle entry " + id + ": negative duration");
-  return TimeOracle{std::move(e), origin};
+  for (size_t i = 0; i < us.size(); ++i)
+    if (us[i] < 0) fail(kValidation, "oracle entry " + g->ops()[i].id + ": negative duration");
+  return TimeOracle{std::move(g), std::move(us), origin};
 }
 
-TimeOracle TimeOracle::declared(const Graph& g) {  // time_oracle.cpp:72-84
-  std::map<std::string, int64_t> e;
+TimeOracle TimeOracle::declared(std::shared_ptr<const Graph> g) {  // time_oracle.cpp:72-84
+  std::vector<int64_t> us(g->n());
   std::vector<std::string> missing;
-  for (const Op& op : g.ops()) {
-    if (op.time_us) e.emplace_hint(e.end(), op.id, *op.time_us);  // ops come in id order
+  for (int32_t i = 0; i < g->n(); ++i) {
+    const Op& op = g->ops()[i];
+    if (op.time_us) us[i] = *op.time_us;
     else missing.push_back(op.id);
   }
   if (!missing.empty()) fail(kCoverage, "ops without declared time: " + joined(missing));
-  return checked(std::move(e), "declared");
+  return checked(std::move(g), std::move(us), "declared");
 }
 
-TimeOracle TimeOracle::general(const Graph& g) {  // time_oracle.cpp:86-91
-  std::map<std::string, int64_t> e;
-  for (const Op& op : g.ops()) e.emplace_hint(e.end(), op.id, op.kind == kRecv ? 1 : 0);
-  return checked(std::move(e), "general");
+TimeOracle TimeOracle::general(std::shared_ptr<const Graph> g) {  // time_oracle.cpp:86-91
+  std::vector<int64_t> us(g->n());
+  for (int32_t i = 0; i < g->n(); ++i) us[i] = g->ops()[i].kind == kRecv ? 1 : 0;
+  return checked(std::move(g), std::move(us), "general");
 }
 
-TimeOracle TimeOracle::traces(const Graph& g, std::string_view text) {
+TimeOracle TimeOracle::traces(std::shared_ptr<const Graph> g, std::string_view text) {
   // parse_trace_jsonl (time_oracle.cpp:22-52) then the min rule (93-112).
   std::map<std::string, int64_t> best;
   size_t pos = 0, line_no = 0;
@@ -63,47 +64,52 @@ TimeOracle TimeOracle::traces(const Graph& g, std::string_view text) {
     else it->second = std::min(it->second, us);
   }
   std::vector<std::string> missing;
-  for (const Op& op : g.ops())
-    if (!best.count(op.id)) missing.push_back(op.id);
+  std::vector<int64_t> us(g->n());
+  for (int32_t i = 0; i < g->n(); ++i) {
+    const auto it = best.find(g->ops()[i].id);
+    if (it == best.end()) missing.push_back(g->ops()[i].id);
+    else us[i] = it->second;
+  }
   if (!missing.empty()) fail(kCoverage, "ops without trace records: " + joined(missing));
-  std::map<std::string, int64_t> kept;
-  for (const Op& op : g.ops()) kept[op.id] = best[op.id];
-  return checked(std::move(kept), "measured");
+  return checked(std::move(g), std::move(us), "measured");
 }
 
-TimeOracle TimeOracle::bandwidth(const Graph& g, int64_t bw) {  // time_oracle.cpp:114-134
+TimeOracle TimeOracle::bandwidth(std::shared_ptr<const Graph> g, int64_t bw) {  // time_oracle.cpp:114-134
   if (bw <= 0) fail(kParameter, "bandwidth must be positive bytes per microsecond");
-  std::map<std::string, int64_t> e;
+  std::vector<int64_t> us(g->n());
   std::vector<std::string> missing;
-  for (const Op& op : g.ops()) {
-    if (transfer(op.kind) && op.bytes) e.emplace_hint(e.end(), op.id, (2 * *op.bytes + bw) / (2 * bw));
-    else if (op.time_us) e.emplace_hint(e.end(), op.id, *op.time_us);
+  for (int32_t i = 0; i < g->n(); ++i) {
+    const Op& op = g->ops()[i];
+    if (transfer(op.kind) && op.bytes) us[i] = (2 * *op.bytes + bw) / (2 * bw);
+    else if (op.time_us) us[i] = *op.time_us;
     else missing.push_back(op.id);
   }
   if (!missing.empty()) fail(kCoverage, "ops without bytes or declared time: " + joined(missing));
-  return checked(std::move(e), "synthetic");
+  return checked(std::move(g), std::move(us), "synthetic");
 }
 
 std::vector<int64_t> TimeOracle::durations(const Graph& g) const {
+  if (&g == src.get()) return us;
   std::vector<int64_t> d(g.n());
   std::vector<std::string> missing;
-  // ops are indexed in id order, the map iterates in id order: one merge pass
-  auto it = entries.begin();
+  // both op lists are in id order: one merge pass
+  const auto& have = src->ops();
+  size_t j = 0;
   for (int32_t i = 0; i < g.n(); ++i) {
     const std::string& id = g.ops()[i].id;
-    while (it != entries.end() && it->first < id) ++it;
-    if (it == entries.end() || it->first != id) missing.push_back(id);
-    else d[i] = it->second;
+    while (j < have.size() && have[j].id < id) ++j;
+    if (j == have.size() || have[j].id != id) missing.push_back(id);
+    else d[i] = us[j];
   }
   if (!missing.empty()) fail(kCoverage, "oracle missing entries for: " + joined(missing));
   return d;
 }
 
-Json TimeOracle::to_json() const {  // time_oracle.cpp:151-157
+Json TimeOracle::to_json() const {  // time_oracle.cpp:151-157 (map order = op index order)
   Json j;
   j["origin"] = origin;
   j["entries"] = Json::object();
-  for (const auto& [id, us] : entries) j["entries"][id] = us;
+  for (int32_t i = 0; i < src->n(); ++i) j["entries"][src->ops()[i].id] = us[i];
   return j;
 }
 
