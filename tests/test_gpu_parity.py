@@ -557,11 +557,13 @@ def test_ungated_runs_through_the_closed_form_match_reference(lib, ref):
 def test_noisy_sweeps_through_the_closed_form_match_reference(lib, ref, noise):
     """Gated sweeps with reorder noise use the closed form on the noise-
     permuted gate sequence: makespans equal the reference's
-    per-seed loop on worker graphs, a model DAG and clusters (one noise stream
-    across the workers' channels), and the generic replica on a large batch."""
+    per-seed loop on worker graphs, model DAGs (one with more than 311 noise
+    draws per run) and clusters (one noise stream across the workers'
+    channels)."""
     from paper_1803_03288_b200.capi import SweepPlan
     texts = [t for _, t in corpus.worker_graphs(lib)[:5]] + [lib.model("resnet_v2_50_inference", 1).serialize()]
     texts += [t for _, t in corpus.cluster_graphs(lib)[:2]]
+    texts.append(lib.model("layered:4000:400", 1).serialize())  # > 311 noise draws: the stream's second block
     pol = policy(True, 0, noise)
     closed = 0
     for text in texts:
