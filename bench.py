@@ -637,8 +637,9 @@ def main():
              out["tic_roofline"]) = tac_times(lib, top=args.config5_top, hbm=hbm)
             if world > 1:
                 out["tac_note"] = ("TAC is R dependent rounds and runs on one GPU (rank 0) at any N: a "
-                                   "sharded round would add an NCCL all-reduce (16-29 us measured over NVLink, "
-                                   "tools/allreduce_latency.py) to rounds of 1.3-8 us; DESIGN.md section 5")
+                                   "sharded round needs >= 2 cross-GPU exchanges (NCCL all-reduce 16-29 us, "
+                                   "NVLink peer-flag round trip 2.6 us; profiles/r01_cross_gpu_latency.json) "
+                                   "on rounds of 1.3-6.3 us; DESIGN.md section 5")
         if not args.no_configs and world == 1:
             out["configs"] = other_configs(lib)
             out["configs"].update(exact_paths(lib, path))
