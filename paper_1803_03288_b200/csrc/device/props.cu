@@ -903,7 +903,8 @@ int group_setup(DeviceGraph* g, const int64_t* dur, GroupState& S, char* err) {
   CK(cudaMemset(S.d_colcount.p, 0, 4ull * (g->R + 1)));
   const size_t smem = static_cast<size_t>(rw.nrows) * W * 4;
   if (rw.nrows > 0) {
-    if (smem <= 200 * 1024) {
+    // (TICTAC_CLOSURE_GLOBAL: test knob forcing the large-closure kernels)
+    if (smem <= 200 * 1024 && !std::getenv("TICTAC_CLOSURE_GLOBAL")) {
       CK(allow_max_dynamic_smem(reinterpret_cast<const void*>(closure_smem_kernel)));
       closure_smem_kernel<<<1, 256, smem>>>(rw.nrows, W, S.d_self.as<int32_t>(),
                                             S.d_preoff.as<int32_t>(), S.d_pre.as<int32_t>(),

@@ -441,16 +441,35 @@ def _zeroed(text, seed, frac=3):
     return json.dumps(d)
 
 
-def test_large_closure_path_matches_reference(lib, ref):
+def test_large_closure_path_matches_reference(lib, ref, orc):
     """Closures too large for one block's shared memory (roots written in
     parallel, the other rows in topological order from staged terms,
     including a row with more terms than one staged chunk): TIC in both
-    modes and the property tables match the reference library."""
+    modes and the property tables match the reference library; TAC (5,003
+    rounds, beyond the reference's reach) matches the oracle's A.1 TAC."""
     for seed in (1, 2):
         text = corpus.wide_fanin(seed)
         for mode in ("amended", "literal"):
             _both(lib, ref, text, lambda L, g: g.tic(mode).serialize() + str(g.tic(mode).total_order()))
             _both(lib, ref, text, lambda L, g: g.properties_text(g.declared(), mode))
+        g = lib.graph(text)
+        og = orc.OracleGraph(json.loads(text))
+        assert g.tac(g.declared()).priorities() == og.tac(incremental=True)
+
+
+def test_large_closure_kernels_on_every_graph_kind(lib, ref, monkeypatch):
+    """The large-closure kernels forced on the parity corpora — worker,
+    cluster (recvs with predecessors: rows with their own bit and
+    predecessor rows), model and irregular graphs: TIC, TAC and property
+    tables still match the reference."""
+    monkeypatch.setenv("TICTAC_CLOSURE_GLOBAL", "1")
+    graphs = (corpus.worker_graphs(lib)[:4] + corpus.cluster_graphs(lib)[:3] + corpus.model_graphs(lib)[:2]
+              + corpus.irregular_graphs())
+    for _, text in graphs:
+        for mode in ("amended", "literal"):
+            _both(lib, ref, text, lambda L, g: g.tic(mode).serialize() + str(g.tic(mode).total_order()))
+            _both(lib, ref, text, lambda L, g: g.properties_text(g.declared(), mode))
+        _both(lib, ref, text, lambda L, g: g.tac(g.declared()).serialize())
 
 
 def test_single_reports_specialised_replica(lib, ref, monkeypatch):
