@@ -558,17 +558,16 @@ int cs_sweep_random(const cs_graph* g, const cs_oracle* o, uint64_t seed_lo, int
     auto cudacheck = [&](cudaError_t e) {
       if (e != cudaSuccess) fail(kInternal, std::string("CUDA error: ") + cudaGetErrorString(e));
     };
-    DevPtr b_i64, b_f64, b_ms, b_wms;
+    DevPtr b_st, b_ms, b_wms;  // statistics: i64 then f64 words, read back with one copy
     const int64_t W = ctx->cluster ? static_cast<int64_t>(ctx->workers.size()) : 1;
     const int64_t chunk = int64_t{1} << 26;
-    cudacheck(cudaMallocAsync(&b_i64.p, 8 * CS_DSTATS_I64, 0));
-    cudacheck(cudaMallocAsync(&b_f64.p, 8 * CS_DSTATS_F64, 0));
+    cudacheck(cudaMallocAsync(&b_st.p, 8 * (CS_DSTATS_I64 + CS_DSTATS_F64), 0));
     const int64_t cap = std::min(count, chunk);
     if (makespans_out) cudacheck(cudaMallocAsync(&b_ms.p, 8 * std::max<int64_t>(cap, 1), 0));
     if (worker_makespans_out && ctx->cluster)
       cudacheck(cudaMallocAsync(&b_wms.p, 8 * std::max<int64_t>(cap * W, 1), 0));
-    int64_t *d_i64 = b_i64.as<int64_t>(), *d_ms = b_ms.as<int64_t>(), *d_wms = b_wms.as<int64_t>();
-    double* d_f64 = b_f64.as<double>();
+    int64_t *d_i64 = b_st.as<int64_t>(), *d_ms = b_ms.as<int64_t>(), *d_wms = b_wms.as<int64_t>();
+    double* d_f64 = reinterpret_cast<double*>(d_i64 + CS_DSTATS_I64);
     cs_sweep_stats total{};
     bool first = true;
     {
@@ -580,8 +579,12 @@ int cs_sweep_random(const cs_graph* g, const cs_oracle* o, uint64_t seed_lo, int
           fail(kInternal, err);
         std::vector<int64_t> i64(CS_DSTATS_I64);
         std::vector<double> f64(CS_DSTATS_F64);
-        cudacheck(cudaMemcpy(i64.data(), d_i64, 8 * CS_DSTATS_I64, cudaMemcpyDeviceToHost));
-        cudacheck(cudaMemcpy(f64.data(), d_f64, 8 * CS_DSTATS_F64, cudaMemcpyDeviceToHost));
+        {
+          std::vector<char> st(8 * (CS_DSTATS_I64 + CS_DSTATS_F64));
+          cudacheck(cudaMemcpy(st.data(), d_i64, st.size(), cudaMemcpyDeviceToHost));
+          std::memcpy(i64.data(), st.data(), 8 * CS_DSTATS_I64);
+          std::memcpy(f64.data(), st.data() + 8 * CS_DSTATS_I64, 8 * CS_DSTATS_F64);
+        }
         if (d_ms) cudacheck(cudaMemcpy(makespans_out + base, d_ms, 8 * n, cudaMemcpyDeviceToHost));
         if (d_wms)
           cudacheck(cudaMemcpy(worker_makespans_out + base * W, d_wms, 8 * n * W, cudaMemcpyDeviceToHost));
