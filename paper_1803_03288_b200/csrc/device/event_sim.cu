@@ -1183,17 +1183,30 @@ __global__ void __launch_bounds__(256) event_a2p_kernel(GraphView G, const int32
         start_chan();
         zero |= chan_end == t;
       }
-      if (!zero && cpu_u >= 0 && ready_cnt == 0) {
-        // Forced picks along a chain: while the running op's only successor
-        // is the next op to become ready and the channel completes nothing
-        // before (or with) it, the rounds in between reduce to "complete it,
-        // start the successor" — no draw, no other state changes.
-        for (int v = nxt[cpu_u]; v >= 0 && (chan_u < 0 || cpu_end < chan_end); v = nxt[v]) {
-          t = cpu_end;
-          cpu_u = v;
-          st[v] = t;
-          cpu_end = t + static_cast<Tm>(node[v].dur);
+      // Compute-only rounds: while the channel is done or completes strictly
+      // after the running compute op, the channel's try_start and
+      // completions are no-ops, so each round is "complete the op at its end,
+      // pick the next one". Along a chain — the op's only successor is a
+      // single-predecessor op with positive duration and nothing else is
+      // ready — the round reduces further to "start the successor" (no draw,
+      // no other state change).
+      while (!zero && cpu_u >= 0 && (chan_u < 0 || cpu_end < chan_end)) {
+        if (ready_cnt == 0) {
+          const int v = nxt[cpu_u];
+          if (v >= 0) {
+            t = cpu_end;
+            cpu_u = v;
+            st[v] = t;
+            cpu_end = t + static_cast<Tm>(node[v].dur);
+            continue;
+          }
         }
+        t = cpu_end;
+        complete(cpu_u);
+        cpu_u = -1;
+        if (ready_cnt == 0) break;
+        start_cpu();
+        zero = cpu_end == t;
       }
       if (zero) {
         if (cpu_u >= 0 && cpu_end == t) {

@@ -69,7 +69,7 @@ struct Op {
 
 // Immutable DAG in the reference index model: ops sorted by id (byte
 // order), edges sorted/deduped, CSR adjacency with ascending lists.
-class Graph {
+class Graph : public std::enable_shared_from_this<Graph> {
  public:
   static std::shared_ptr<Graph> make(std::string name, bool cluster, std::vector<Op> ops,
                                      std::vector<std::pair<std::string, std::string>> edges);
@@ -170,7 +170,8 @@ struct Report {
   std::vector<Resource> resources;
   struct Event { int32_t op; int32_t res; int64_t start, end; };
   std::vector<Event> events;  // sorted (start, resource, op id)
-  std::vector<std::string> op_ids;
+  std::shared_ptr<const Graph> graph;  // op ids by index (kept alive with the report)
+  const std::string& op_id(int32_t op) const { return graph->ops()[op].id; }
   bool has_stats = false;
   std::vector<std::pair<std::string, int64_t>> per_worker;  // ascending device
   int64_t iteration = 0, strag_num = 0, strag_den = 1;

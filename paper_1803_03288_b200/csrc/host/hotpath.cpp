@@ -171,8 +171,7 @@ Report make_report(const Graph& g, const std::vector<int64_t>& st, const std::ve
   r.makespan = m;
   r.violations = viol;
   r.resources = g.resources();
-  r.op_ids.reserve(n);
-  for (const Op& op : g.ops()) r.op_ids.push_back(op.id);
+  r.graph = g.shared_from_this();
   r.events.reserve(n);
   for (int32_t i = 0; i < n; ++i) r.events.push_back({i, g.res_of()[i], st[i], en[i]});
   std::sort(r.events.begin(), r.events.end(), [](const Report::Event& a, const Report::Event& b) {

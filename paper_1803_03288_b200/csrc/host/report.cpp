@@ -113,7 +113,7 @@ std::string Report::json_text() const {
     for (size_t i = 0; i < events.size(); ++i) {
       const Event& e = events[i];
       w.s += i ? ",\n    {\n      \"op\": " : "\n    {\n      \"op\": ";
-      w.str(op_ids[e.op]);
+      w.str(op_id(e.op));
       w.s += ",\n      \"resource\": ";
       w.s += qres[e.res];
       w.s += ",\n      \"start_us\": ";
@@ -179,7 +179,7 @@ std::string Report::chrome_trace_text() const {
   for (const Event& e : events) {  // fixed layout: fragments appended directly
     w.item();
     w.s += "{\n      \"name\": ";
-    w.str(op_ids[e.op]);
+    w.str(op_id(e.op));
     w.s += resources[e.res].channel ? ",\n      \"cat\": \"channel\",\n      \"ph\": \"X\",\n      \"pid\": "
                                     : ",\n      \"cat\": \"compute\",\n      \"ph\": \"X\",\n      \"pid\": ";
     w.num(pid[e.res]);
@@ -208,7 +208,7 @@ Json Report::to_json() const {
   j["events"] = Json::array();
   for (const Event& e : events) {
     Json je;
-    je["op"] = op_ids[e.op];
+    je["op"] = op_id(e.op);
     je["resource"] = resources[e.res].key();
     je["start_us"] = e.start;
     je["end_us"] = e.end;
@@ -246,7 +246,7 @@ Json Report::chrome_trace() const {
   }
   for (const Event& e : events) {
     Json x;
-    x["name"] = op_ids[e.op];
+    x["name"] = op_id(e.op);
     x["cat"] = resources[e.res].channel ? "channel" : "compute";
     x["ph"] = "X";
     x["pid"] = pid(resources[e.res].device);
