@@ -22,6 +22,11 @@ struct Rows {
   std::vector<int32_t> nt_row, nt_off, nt_term;
   std::vector<int32_t> nt_chunk;  // row ranges staged through shared memory together
   std::vector<int32_t> has_rows;  // rows with compute members (column-list entries), ascending
+  // device copies of the arrays above (uploaded with the structure, freed
+  // with the graph by csk_graph_free)
+  int32_t *d_self = nullptr, *d_preoff = nullptr, *d_pre = nullptr, *d_rowof = nullptr, *d_succoff = nullptr,
+          *d_succ = nullptr, *d_ntrow = nullptr, *d_ntoff = nullptr, *d_ntterm = nullptr, *d_ntchunk = nullptr,
+          *d_hasrows = nullptr;
 };
 
 struct DeviceGraph {

@@ -867,8 +867,7 @@ __global__ void __launch_bounds__(1024) tac_cluster_kernel(TacArgs a, int per) {
 // column lists. `dur` per op (host).
 struct GroupState {
   std::shared_ptr<const Rows> rw;
-  DevArr d_self, d_preoff, d_pre, d_ntrow, d_ntoff, d_ntterm, d_ntchunk, d_counts, d_hasrows,
-      d_bits, d_rowof, d_wsum, d_has, d_cnt, d_M, d_xr, d_colcount,
+  DevArr d_counts, d_bits, d_rowof, d_wsum, d_has, d_cnt, d_M, d_xr, d_colcount,
       d_coloff, d_col, d_tcol, d_dur, d_tmp;
   int64_t nnz = 0;
 };
@@ -880,6 +879,21 @@ int group_setup(DeviceGraph* g, const int64_t* dur, GroupState& S, char* err) {
     if (!g->rows) {
       auto r = std::make_shared<Rows>();
       build_rows(g, *r);
+      auto up = [&](int32_t*& d, const std::vector<int32_t>& v) -> int {
+        CK(cudaMalloc(&d, round16(4 * std::max<size_t>(v.size(), 1))));
+        if (!v.empty()) CK(cudaMemcpy(d, v.data(), 4 * v.size(), cudaMemcpyHostToDevice));
+        return 0;
+      };
+      if (up(r->d_self, r->self_col) || up(r->d_preoff, r->pre_off) || up(r->d_pre, r->pre) ||
+          up(r->d_rowof, r->row_of) || up(r->d_succoff, r->succ_off) || up(r->d_succ, r->succ) ||
+          up(r->d_ntrow, r->nt_row) || up(r->d_ntoff, r->nt_off) || up(r->d_ntterm, r->nt_term) ||
+          up(r->d_ntchunk, r->nt_chunk) || up(r->d_hasrows, r->has_rows)) {
+        const int32_t* ps[] = {r->d_self, r->d_preoff, r->d_pre,    r->d_rowof,   r->d_succoff, r->d_succ,
+                               r->d_ntrow, r->d_ntoff, r->d_ntterm, r->d_ntchunk, r->d_hasrows};
+        for (const int32_t* q : ps)
+          if (q) cudaFree(const_cast<int32_t*>(q));
+        return 1;
+      }
       g->rows = std::move(r);
     }
     S.rw = g->rows;
@@ -889,9 +903,7 @@ int group_setup(DeviceGraph* g, const int64_t* dur, GroupState& S, char* err) {
   std::vector<int64_t> tcol(std::max(g->R, 1));
   for (int c = 0; c < g->R; ++c) tcol[c] = dur[g->h_recv_ops[c]];
   std::vector<int64_t> hd(dur, dur + g->n);
-  if (put(S.d_self, rw.self_col, err) || put(S.d_preoff, rw.pre_off, err) || put(S.d_pre, rw.pre, err) ||
-      put(S.d_rowof, rw.row_of, err) || put(S.d_tcol, tcol, err) || put(S.d_dur, hd, err))
-    return 1;
+  if (put(S.d_tcol, tcol, err) || put(S.d_dur, hd, err)) return 1;
   if (alloc<uint32_t>(S.d_bits, static_cast<size_t>(nrows) * W, err) ||
       alloc<unsigned long long>(S.d_wsum, nrows, err) || alloc<int32_t>(S.d_has, nrows, err) ||
       alloc<int32_t>(S.d_cnt, nrows, err) || alloc<int64_t>(S.d_M, nrows, err) ||
@@ -906,27 +918,24 @@ int group_setup(DeviceGraph* g, const int64_t* dur, GroupState& S, char* err) {
     // (TICTAC_CLOSURE_GLOBAL: test knob forcing the large-closure kernels)
     if (smem <= 200 * 1024 && !std::getenv("TICTAC_CLOSURE_GLOBAL")) {
       CK(allow_max_dynamic_smem(reinterpret_cast<const void*>(closure_smem_kernel)));
-      closure_smem_kernel<<<1, 256, smem>>>(rw.nrows, W, S.d_self.as<int32_t>(),
-                                            S.d_preoff.as<int32_t>(), S.d_pre.as<int32_t>(),
+      closure_smem_kernel<<<1, 256, smem>>>(rw.nrows, W, rw.d_self,
+                                            rw.d_preoff, rw.d_pre,
                                             S.d_bits.as<uint32_t>());
     } else {
-      if (put(S.d_ntrow, rw.nt_row, err) || put(S.d_ntoff, rw.nt_off, err) ||
-          put(S.d_ntterm, rw.nt_term, err) || put(S.d_ntchunk, rw.nt_chunk, err))
-        return 1;
-      closure_roots_kernel<<<std::min(rw.nrows, 148 * 16), 256>>>(rw.nrows, W, S.d_self.as<int32_t>(),
-                                                                  S.d_preoff.as<int32_t>(), S.d_bits.as<uint32_t>());
+      closure_roots_kernel<<<std::min(rw.nrows, 148 * 16), 256>>>(rw.nrows, W, rw.d_self,
+                                                                  rw.d_preoff, S.d_bits.as<uint32_t>());
       LAUNCHED();
       if (!rw.nt_row.empty())
         closure_seq_kernel<<<(W + 127) / 128, 128>>>(static_cast<int32_t>(rw.nt_chunk.size()) - 1, W,
-                                                     S.d_ntchunk.as<int32_t>(), S.d_ntrow.as<int32_t>(),
-                                                     S.d_ntoff.as<int32_t>(), S.d_ntterm.as<int32_t>(),
+                                                     rw.d_ntchunk, rw.d_ntrow,
+                                                     rw.d_ntoff, rw.d_ntterm,
                                                      S.d_bits.as<uint32_t>());
     }
     LAUNCHED();
     CK(cudaGetLastError());
   }
   weights_kernel<<<std::max(1, std::min((g->n + 255) / 256, 1184)), 256>>>(
-      g->n, S.d_rowof.as<int32_t>(), g->kind, S.d_dur.as<int64_t>(), S.d_wsum.as<unsigned long long>(),
+      g->n, rw.d_rowof, g->kind, S.d_dur.as<int64_t>(), S.d_wsum.as<unsigned long long>(),
       S.d_has.as<int32_t>());
   LAUNCHED();
   const int rblocks = std::max(1, std::min((rw.nrows * 32 + 255) / 256, 2368));
@@ -938,17 +947,16 @@ int group_setup(DeviceGraph* g, const int64_t* dur, GroupState& S, char* err) {
   nchunks = std::max(1, (nhas + chunk_rows - 1) / chunk_rows);
   const int64_t cwarps = static_cast<int64_t>(W) * nchunks;
   const int cblocks = static_cast<int>((cwarps * 32 + 255) / 256);
-  if (put(S.d_hasrows, rw.has_rows, err)) return 1;
   if (alloc<int32_t>(S.d_counts, static_cast<size_t>(nchunks) * std::max(g->R, 1), err)) return 1;
   if (rw.nrows > 0) {
-    rowstate_kernel<<<rblocks, 256>>>(rw.nrows, W, S.d_bits.as<uint32_t>(), S.d_preoff.as<int32_t>(),
-                                      S.d_self.as<int32_t>(), S.d_tcol.as<int64_t>(),
+    rowstate_kernel<<<rblocks, 256>>>(rw.nrows, W, S.d_bits.as<uint32_t>(), rw.d_preoff,
+                                      rw.d_self, S.d_tcol.as<int64_t>(),
                                       S.d_has.as<int32_t>(), S.d_cnt.as<int32_t>(),
                                       S.d_M.as<int64_t>(), S.d_xr.as<int32_t>());
     LAUNCHED();
     if (g->R > 0) {
       colcount_warp_kernel<<<cblocks, 256>>>(nhas, W, g->R, nchunks, chunk_rows, S.d_bits.as<uint32_t>(),
-                                             S.d_hasrows.as<int32_t>(), S.d_counts.as<int32_t>());
+                                             rw.d_hasrows, S.d_counts.as<int32_t>());
       LAUNCHED();
       colprefix_kernel<<<std::max(1, std::min((g->R + 255) / 256, 1184)), 256>>>(
           g->R, nchunks, S.d_counts.as<int32_t>(), S.d_colcount.as<int32_t>());
@@ -970,7 +978,7 @@ int group_setup(DeviceGraph* g, const int64_t* dur, GroupState& S, char* err) {
   if (alloc<int32_t>(S.d_col, nnz, err)) return 1;
   if (rw.nrows > 0 && g->R > 0) {
     colfill_warp_kernel<<<cblocks, 256>>>(nhas, W, g->R, nchunks, chunk_rows, S.d_bits.as<uint32_t>(),
-                                          S.d_hasrows.as<int32_t>(), S.d_counts.as<int32_t>(),
+                                          rw.d_hasrows, S.d_counts.as<int32_t>(),
                                           S.d_coloff.as<int32_t>(), S.d_col.as<int32_t>());
     LAUNCHED();
   }
@@ -1083,9 +1091,9 @@ extern "C" int csk_tac(DeviceGraph* g, const int64_t* dur, int32_t* prio, char* 
   if (group_setup(g, dur, S, err)) return 1;
   if (trace) cudaDeviceSynchronize();
   const auto t1 = now();
-  DevArr d_P, d_Mp, d_out, d_prio, d_succoff, d_succ;
+  DevArr d_P, d_Mp, d_out, d_prio;
   if (alloc<int64_t>(d_P, R, err) || alloc<int64_t>(d_Mp, R, err) || alloc<uint8_t>(d_out, R, err) ||
-      alloc<int32_t>(d_prio, R, err) || put(d_succoff, S.rw->succ_off, err) || put(d_succ, S.rw->succ, err))
+      alloc<int32_t>(d_prio, R, err))
     return 1;
   CK(cudaMemset(d_out.p, 1, R));
   // initial P (amended M+ is recomputed inside the rounds)
@@ -1096,8 +1104,8 @@ extern "C" int csk_tac(DeviceGraph* g, const int64_t* dur, int32_t* prio, char* 
   CK(cudaGetLastError());
   TacArgs a{R,
             S.d_tcol.as<int64_t>(),
-            d_succoff.as<int32_t>(),
-            d_succ.as<int32_t>(),
+            S.rw->d_succoff,
+            S.rw->d_succ,
             S.d_coloff.as<int32_t>(),
             S.d_col.as<int32_t>(),
             S.d_wsum.as<unsigned long long>(),
