@@ -364,6 +364,7 @@ def other_configs(lib):
     for R in (8, 10, 12):
         g = lib.generate("chain", R, 1, "1", 5)
         o = g.declared()
+        g.brute_force_text(o, None, R)  # warm (plan, pool buffers)
         t = time.perf_counter()
         res = json.loads(g.brute_force_text(o, None, R))
         bf[f"R{R}"] = {"permutations": int(np.prod(np.arange(1, R + 1, dtype=np.float64))),

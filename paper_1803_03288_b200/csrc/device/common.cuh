@@ -49,13 +49,15 @@ inline cudaError_t allow_max_dynamic_smem(const void* fn) {
 }
 
 // Owned device allocation (freed on every exit path).
+// Per-call device buffer from the stream-ordered pool (allocate with
+// cudaMallocAsync on the legacy stream; freed in stream order).
 struct DevMem {
   void* p = nullptr;
   DevMem() = default;
   DevMem(const DevMem&) = delete;
   DevMem& operator=(const DevMem&) = delete;
   ~DevMem() {
-    if (p) cudaFree(p);
+    if (p) cudaFreeAsync(p, 0);
   }
   template <typename T>
   T* as() const {

@@ -753,7 +753,7 @@ extern "C" int csk_sweep_orders(SweepPlan* p, const int32_t* d_orders, int64_t n
   a.f64 = nullptr;
   a.do_e = 0;
   DevMem d_bad;
-  CK(cudaMalloc(&d_bad.p, sizeof(int)));
+  CK(cudaMallocAsync(&d_bad.p, sizeof(int), 0));
   CK(cudaMemsetAsync(d_bad.p, 0, sizeof(int), st));
   a.bad_order = d_bad.as<int>();
   const int blocks = static_cast<int>(std::min<int64_t>(p->blocks, (n + kSweepThreads - 1) / kSweepThreads));
@@ -780,7 +780,7 @@ extern "C" int csk_sweep_lex(SweepPlan* p, int64_t first, int64_t count, int64_t
   std::vector<unsigned long long> fact(21, 1);
   for (int i = 1; i <= 20; ++i) fact[i] = fact[i - 1] * static_cast<unsigned long long>(i);
   DevMem d_fact;
-  CK(cudaMalloc(&d_fact.p, sizeof(unsigned long long) * fact.size()));
+  CK(cudaMallocAsync(&d_fact.p, sizeof(unsigned long long) * fact.size(), 0));
   CK(cudaMemcpy(d_fact.p, fact.data(), sizeof(unsigned long long) * fact.size(), cudaMemcpyHostToDevice));
   ChainArgs a = chain_args(p);
   const size_t vb = p->narrow ? 4 : 8;
@@ -805,10 +805,11 @@ extern "C" int csk_sweep_lex(SweepPlan* p, int64_t first, int64_t count, int64_t
 
 extern "C" int csk_brute_force_closed(SweepPlan* p, int64_t perms, int64_t* best_m, int64_t* best_k,
                                       int64_t* distinct, int64_t cap, int64_t* n_distinct, char* err) {
-  // Chunks of <= 2^28 permutations in lexicographic order: makespans, CUB
+  // Chunks of <= 2^26 permutations in lexicographic order: makespans, CUB
   // arg-min (first minimum = the reference's first optimum), then sort +
-  // unique for the distribution; chunk results merge on the host.
-  const int64_t chunk = std::min<int64_t>(perms, int64_t{1} << 28);
+  // unique for the distribution; chunk results merge on the host. Buffers
+  // come from the stream-ordered pool, so repeated calls reuse them.
+  const int64_t chunk = std::min<int64_t>(perms, int64_t{1} << 26);
   DevMem m_ms, m_sorted, m_uniq, m_nu, m_arg, m_tmp;
   size_t tmp_bytes = 0, b1 = 0, b2 = 0, b3 = 0;
   const int nc = static_cast<int>(chunk);
@@ -818,12 +819,12 @@ extern "C" int csk_brute_force_closed(SweepPlan* p, int64_t perms, int64_t* best
   CK(cub::DeviceSelect::Unique(nullptr, b3, static_cast<int64_t*>(nullptr), static_cast<int64_t*>(nullptr),
                                static_cast<int*>(nullptr), nc));
   tmp_bytes = std::max(b1, std::max(b2, b3));
-  CK(cudaMalloc(&m_ms.p, 8 * chunk));
-  CK(cudaMalloc(&m_sorted.p, 8 * chunk));
-  CK(cudaMalloc(&m_uniq.p, 8 * chunk));
-  CK(cudaMalloc(&m_nu.p, 8));
-  CK(cudaMalloc(&m_arg.p, sizeof(cub::KeyValuePair<int, int64_t>)));
-  CK(cudaMalloc(&m_tmp.p, std::max<size_t>(tmp_bytes, 16)));
+  CK(cudaMallocAsync(&m_ms.p, 8 * chunk, 0));
+  CK(cudaMallocAsync(&m_sorted.p, 8 * chunk, 0));
+  CK(cudaMallocAsync(&m_uniq.p, 8 * chunk, 0));
+  CK(cudaMallocAsync(&m_nu.p, 8, 0));
+  CK(cudaMallocAsync(&m_arg.p, sizeof(cub::KeyValuePair<int, int64_t>), 0));
+  CK(cudaMallocAsync(&m_tmp.p, std::max<size_t>(tmp_bytes, 16), 0));
   void *d_ms = m_ms.p, *d_sorted = m_sorted.p, *d_uniq = m_uniq.p, *d_nu = m_nu.p, *d_arg = m_arg.p,
        *d_tmp = m_tmp.p;
   std::vector<int64_t> all;
@@ -877,10 +878,10 @@ extern "C" int csk_random_orders(int32_t R, int32_t S, const uint64_t* seeds, in
   std::vector<uint64_t> lim(4096), mag(4096);
   for (uint64_t k = 0; k < 4096; ++k) bounded_consts(k, &lim[k], &mag[k]);
   DevMem d_seeds, d_lim, d_mag, d_perm;
-  CK(cudaMalloc(&d_seeds.p, 8ull * S));
-  CK(cudaMalloc(&d_lim.p, 8ull * lim.size()));
-  CK(cudaMalloc(&d_mag.p, 8ull * mag.size()));
-  CK(cudaMalloc(&d_perm.p, 4ull * R * S));
+  CK(cudaMallocAsync(&d_seeds.p, 8ull * S, 0));
+  CK(cudaMallocAsync(&d_lim.p, 8ull * lim.size(), 0));
+  CK(cudaMallocAsync(&d_mag.p, 8ull * mag.size(), 0));
+  CK(cudaMallocAsync(&d_perm.p, 4ull * R * S, 0));
   CK(cudaMemcpy(d_seeds.p, seeds, 8ull * S, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(d_lim.p, lim.data(), 8ull * lim.size(), cudaMemcpyHostToDevice));
   CK(cudaMemcpy(d_mag.p, mag.data(), 8ull * mag.size(), cudaMemcpyHostToDevice));
