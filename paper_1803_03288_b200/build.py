@@ -4,7 +4,9 @@
 
 Output: paper_1803_03288_b200/libcommsched.so exporting only the cs_*
 symbols of include/commsched.h (linker version script). CUDA runtime is
-linked statically so the library only needs the driver at run time.
+linked statically so the library only needs the driver at run time. Then
+paper_1803_03288_b200/tictac_sched, the native sweep/bruteforce CLI over
+the C ABI.
 """
 from __future__ import annotations
 
@@ -21,6 +23,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 OBJ = os.path.join(PKG, "_obj")
 LIB = os.path.join(PKG, "libcommsched.so")
+CLI = os.path.join(PKG, "tictac_sched")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -101,6 +104,16 @@ def build(verbose: bool = False, force: bool = False) -> str:
         if r.returncode != 0:
             raise RuntimeError(f"link failed: {' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
         os.replace(tmp, LIB)
+    # the native batched CLI driver: a client of the C ABI only
+    src = os.path.join(CSRC, "cli", "sched_main.cpp")
+    if force or _stale(CLI, [src, LIB, os.path.join(ROOT, "include", "commsched.h")]):
+        tmp = CLI + ".tmp"
+        cmd = [cxx, "-std=c++20", "-O2", "-Wall", f"-I{jdir}", f"-I{os.path.join(ROOT, 'include')}", src,
+               "-o", tmp, f"-L{PKG}", "-l:libcommsched.so", "-Wl,-rpath,$ORIGIN"]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"CLI build failed: {' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
+        os.replace(tmp, CLI)
     return LIB
 
 

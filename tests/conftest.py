@@ -69,6 +69,15 @@ def lib():
 
 
 @pytest.fixture(scope="session")
+def cli(lib):
+    """The native sweep/bruteforce driver (paper_1803_03288_b200/tictac_sched)."""
+    from paper_1803_03288_b200 import build
+    if not os.path.exists(build.CLI):
+        build.build()
+    return build.CLI
+
+
+@pytest.fixture(scope="session")
 def orc():
     import oracle
     oracle.build()

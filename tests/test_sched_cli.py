@@ -1,9 +1,12 @@
-"""The batched `sweep` / `bruteforce` drivers (paper_1803_03288_b200/sched.py)
+"""The batched `sweep` / `bruteforce` drivers — paper_1803_03288_b200/sched.py
+and the native paper_1803_03288_b200/tictac_sched (csrc/cli/sched_main.cpp) —
 against the reference CLI's behaviour (tools/sched_main.cpp): seed parsing,
-decimal6, config defaults, and — on the GPU — CSV bytes equal to the
-reference library driven seed by seed exactly as cmd_sweep does."""
+decimal6, config defaults, error codes and messages, and — on the GPU — CSV
+bytes equal to the reference library driven seed by seed exactly as
+cmd_sweep does."""
 import json
 import os
+import subprocess
 
 import pytest
 
@@ -36,6 +39,49 @@ def test_config_defaults_and_required_flags(tmp_path, lib, toy_text):
     assert sched.main(["sweep", "--config", str(bad)], lib=lib) == 2
 
 
+def run_native(cli, args):
+    r = subprocess.run([cli, *args], capture_output=True, text=True, timeout=300)
+    return r.returncode, r.stdout, r.stderr
+
+
+def test_native_cli_arguments_and_errors(tmp_path, cli, toy_text):
+    """Argument handling of the native driver mirrors sched.py: required
+    flags, seed-list errors (same codes and messages), config files (flags
+    win, bad documents are validation errors), unknown options."""
+    gp = tmp_path / "g.json"
+    gp.write_text(toy_text)
+    cases = [
+        (["sweep", "--seeds", "1..2"], 4, "error: --out is required"),
+        (["sweep", "--out", str(tmp_path / "x.csv")], 4, "error: --seeds is required"),
+        (["sweep", "--seeds", "5..4", "--out", "x"], 4, "error: seed range is empty: 5..4"),
+        (["sweep", "--seeds", "0..1000000", "--out", "x"], 4, "error: seed range too large: 0..1000000"),
+        (["sweep", "--seeds", ",,", "--out", "x"], 4, "error: no seeds in: ,,"),
+        (["sweep", "--seeds", "1..2x", "--out", "x"], 4, "error: bad seed value: 2x"),
+        (["sweep", "--seeds", "1", "--out", "x"], 4, "error: --graph is required"),
+        (["sweep", "--seeds", "1", "--out", "x", "--graph", str(tmp_path / "none.json")], 5,
+         "error: cannot read " + str(tmp_path / "none.json")),
+        (["sweep", "--bogus", "1"], 4, "error: unknown option: --bogus"),
+        (["bruteforce", "--seeds", "1"], 4, "error: unknown option: --seeds"),
+        (["sweep", "--seeds", "1", "--out", "x", "--graph", str(gp), "--enforce", "maybe"], 4,
+         "error: unknown enforcement: maybe"),
+        (["sweep", "--seeds", "1", "--out", "x", "--graph", str(gp), "--oracle", "psychic"], 4,
+         "error: unknown oracle source: psychic"),
+    ]
+    for args, code, msg in cases:
+        rc, _, err = run_native(cli, args)
+        assert (rc, err.strip()) == (code, msg), args
+        if code == 4 and "--graph" not in args:  # the Python driver agrees
+            assert sched.main(args) == code
+    bad = tmp_path / "bad.json"
+    bad.write_text("[1]")
+    rc, _, err = run_native(cli, ["sweep", "--config", str(bad)])
+    assert (rc, err.strip()) == (2, "error: config must be a JSON object")
+    cfg = tmp_path / "c.json"
+    cfg.write_text(json.dumps({"seeds": "1..3", "out": str(tmp_path / "cfg.csv")}))
+    rc, _, err = run_native(cli, ["sweep", "--config", str(cfg), "--seeds", "9..8"])
+    assert (rc, err.strip()) == (4, "error: seed range is empty: 9..8")  # the flag won
+
+
 def reference_csv(ref, text, seeds, algo):
     """cmd_sweep's loop (sched_main.cpp:452-502) over the reference library."""
     g = ref.graph(text)
@@ -57,7 +103,7 @@ def reference_csv(ref, text, seeds, algo):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("algo", ["random", "tic", "none"])
-def test_sweep_csv_matches_reference_loop(tmp_path, lib, ref, algo, capsys):
+def test_sweep_csv_matches_reference_loop(tmp_path, lib, ref, cli, algo, capsys):
     graphs = corpus.worker_graphs(lib)[:4] + corpus.cluster_graphs(lib)[:2]
     for name, text in graphs:
         gp = tmp_path / "g.json"
@@ -72,10 +118,16 @@ def test_sweep_csv_matches_reference_loop(tmp_path, lib, ref, algo, capsys):
         line = capsys.readouterr().out.strip().splitlines()[-1]
         ms = [int(x.split(",")[1]) for x in want.splitlines()[1:]]
         assert line == f"sweep seeds={len(ms)} min_us={min(ms)} max_us={max(ms)}"
+        native = tmp_path / "n.csv"  # the native driver: same bytes, same summary line
+        rc, stdout, err = run_native(cli, ["sweep", "--graph", str(gp), "--algo", algo, "--seeds", seeds,
+                                           "--out", str(native)])
+        assert rc == 0, err
+        assert native.read_text() == want, name
+        assert stdout.strip() == line
 
 
 @pytest.mark.gpu
-def test_bruteforce_driver(tmp_path, lib, ref):
+def test_bruteforce_driver(tmp_path, lib, ref, cli):
     text = lib.generate("layered", 3, 2, "1", 4).serialize()
     gp = tmp_path / "g.json"
     gp.write_text(text)
@@ -84,3 +136,9 @@ def test_bruteforce_driver(tmp_path, lib, ref):
     g = ref.graph(text)
     assert out.read_text() == g.brute_force_text(g.declared(), policy(True, 0, 0.0), 8)
     assert os.path.getsize(out) > 0
+    native = tmp_path / "bf_native.json"
+    rc, stdout, err = run_native(cli, ["bruteforce", "--graph", str(gp), "--out", str(native)])
+    assert rc == 0, err
+    assert native.read_text() == out.read_text()
+    res = json.loads(native.read_text())
+    assert stdout.strip() == f"best m_us={res['makespan_us']} order={','.join(res['order'])}"
