@@ -1,8 +1,9 @@
 """The reference's acceptance gate (proj/tests/acceptance.cpp), run against
 the CUDA library through the C ABI with the reference's pinned constants
 (acceptance.cpp:43-52). Check 7 (byte-identical CLI artifacts) is restated
-for this repository's batched driver (paper_1803_03288_b200/sched.py) and the
-report/trace documents; the reference's `sched` binary is not built here."""
+for this repository's batched drivers (the native tictac_sched and sched.py)
+and the report/trace documents; the reference's `sched` binary is not built
+here."""
 import json
 from fractions import Fraction
 
@@ -125,7 +126,8 @@ def test_6_straggler_reduction(lib):
     assert positive > 0
 
 
-def test_7_artifact_determinism(lib, tmp_path):
+def test_7_artifact_determinism(lib, cli, tmp_path):
+    import subprocess
     from paper_1803_03288_b200 import sched
     gpath = tmp_path / "g.json"
     gpath.write_text(lib.generate("layered", 2, 2, "1", 9).serialize())
@@ -135,9 +137,16 @@ def test_7_artifact_determinism(lib, tmp_path):
         o = g.declared()
         r = g.simulate(o, g.tac(o), policy(True, 0, 0.0))
         csv = tmp_path / f"sweep-{tag}.csv"
-        assert sched.main(["sweep", "--graph", str(gpath), "--oracle", "declared", "--algo", "random",
-                           "--seeds", "1..20", "--out", str(csv)], lib=lib) == 0
-        return r.json() + "\x1e" + r.chrome_trace() + "\x1e" + csv.read_text()
+        args = ["sweep", "--graph", str(gpath), "--oracle", "declared", "--algo", "random", "--seeds", "1..20"]
+        assert sched.main(args + ["--out", str(csv)], lib=lib) == 0
+        native = tmp_path / f"sweep-native-{tag}.csv"  # the native CLI, a separate process
+        assert subprocess.run([cli, *args, "--out", str(native)], capture_output=True).returncode == 0
+        bf = tmp_path / f"bf-{tag}.json"
+        assert subprocess.run([cli, "bruteforce", "--graph", str(gpath), "--out", str(bf)],
+                              capture_output=True).returncode == 0
+        assert native.read_text() == csv.read_text()
+        return (r.json() + "\x1e" + r.chrome_trace() + "\x1e" + csv.read_text() + "\x1e" + native.read_text()
+                + "\x1e" + bf.read_text())
 
     assert artifacts("a") == artifacts("b")
 
