@@ -174,11 +174,39 @@ Report make_report(const Graph& g, const std::vector<int64_t>& st, const std::ve
   r.graph = g.shared_from_this();
   r.events.reserve(n);
   for (int32_t i = 0; i < n; ++i) r.events.push_back({i, g.res_of()[i], st[i], en[i]});
-  std::sort(r.events.begin(), r.events.end(), [](const Report::Event& a, const Report::Event& b) {
-    if (a.start != b.start) return a.start < b.start;
-    if (a.res != b.res) return a.res < b.res;
-    return a.op < b.op;
-  });
+  // order by (start, resource, op id): one LSD radix sort over the packed key
+  // when start | resource | op fit 64 bits (always, for real graphs)
+  auto bits = [](uint64_t v) { return v ? 64 - __builtin_clzll(v) : 0; };
+  int64_t smax = 0;
+  bool nonneg = true;
+  for (int32_t i = 0; i < n; ++i) smax = std::max(smax, st[i]), nonneg = nonneg && st[i] >= 0;
+  const int bo = bits(static_cast<uint64_t>(std::max(n - 1, 0))), br = bits(r.resources.size());
+  const int bs = bits(static_cast<uint64_t>(smax));
+  if (nonneg && n > 1 && bs + br + bo <= 64) {
+    std::vector<uint64_t> key(n), tmp(n);
+    for (int32_t i = 0; i < n; ++i)
+      key[i] = (static_cast<uint64_t>(st[i]) << (br + bo)) | (static_cast<uint64_t>(g.res_of()[i]) << bo) |
+               static_cast<uint64_t>(i);
+    const int total = bs + br + bo;
+    for (int shift = 0; shift < total; shift += 11) {
+      size_t cnt[2049] = {0};
+      for (uint64_t k : key) ++cnt[((k >> shift) & 2047) + 1];
+      for (int d = 0; d < 2048; ++d) cnt[d + 1] += cnt[d];
+      for (uint64_t k : key) tmp[cnt[(k >> shift) & 2047]++] = k;
+      key.swap(tmp);
+    }
+    const uint64_t mask = bo ? (~uint64_t{0} >> (64 - bo)) : 0;
+    for (int32_t k = 0; k < n; ++k) {
+      const int32_t i = static_cast<int32_t>(key[k] & mask);
+      r.events[k] = {i, g.res_of()[i], st[i], en[i]};
+    }
+  } else {
+    std::sort(r.events.begin(), r.events.end(), [](const Report::Event& a, const Report::Event& b) {
+      if (a.start != b.start) return a.start < b.start;
+      if (a.res != b.res) return a.res < b.res;
+      return a.op < b.op;
+    });
+  }
   if (g.cluster()) {  // iteration_stats, sim.cpp:258-279
     std::map<std::string, int64_t> pw;
     for (const std::string& dv : g.worker_devices()) pw[dv] = 0;
