@@ -613,7 +613,8 @@ def main():
                        "l2": "flushed between steps (256 MiB write)",
                        "U_us": info["U_us"], "L_us": info["L_us"]},
             "strong_scaling_2p24": strong,
-            "gpu_launches": launches // max(1, args.steps),
+            "gpu_launches": launches,  # this library's kernels inside the timed region (all K steps)
+            "gpu_launches_per_step": launches // max(1, args.steps),
             "kernel_ms_per_step": kern_per_step,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": traffic, "peak_source": peak_src,
