@@ -1,4 +1,6 @@
-"""Thread-per-run event replica: throughput vs warps (32-run groups) per SM."""
+"""Thread-per-run event replica: throughput vs warps (32-run groups) per SM,
+for a worker DAG run ungated with tied priorities (unprioritized recvs) and
+for config 3's full cluster makespans."""
 import os
 import sys
 import time
@@ -7,17 +9,25 @@ sys.path.insert(0, ".")
 from paper_1803_03288_b200.capi import Lib, policy  # noqa: E402
 
 L = Lib()
-os.environ["TICTAC_EVENT_LANES"] = "1"
 B = 262144
-for m in ["resnet_v2_50_inference", "resnet_v2_101_training"]:
-    g = L.model(m, 1)
-    o = g.declared()
-    g.sweep_random(o, 1, B, policy(False, 0, 0.0))
-    for per_sm in (1, 2, 4, 8, 16, 32, 8):
-        os.environ["TICTAC_EVENT_GROUPS"] = str(per_sm)
+cases = []
+g = L.model("resnet_v2_50_inference", 1)
+cases.append(("resnet50 inference, no schedule", lambda: g.sweep_random(g.declared(), 1, B, policy(False, 0, 0.0))))
+c = L.model("vgg16_training", 1).expand(4, 1, 0)
+co = c.declared()
+cases.append(("config3 cluster makespans", lambda: c.sweep_random(co, 1, B, None, makespans=True)))
+for name, fn in cases:
+    os.environ.pop("TICTAC_EVENT_GROUPS", None)
+    fn()
+    for per_sm in (0, 2, 4, 8, 16, 32):
+        if per_sm:
+            os.environ["TICTAC_EVENT_GROUPS"] = str(per_sm)
+        else:
+            os.environ.pop("TICTAC_EVENT_GROUPS", None)
         ts = []
-        for _ in range(3):
+        for _ in range(2):
             t = time.perf_counter()
-            g.sweep_random(o, 1, B, policy(False, 0, 0.0))
+            fn()
             ts.append((time.perf_counter() - t) * 1e3)
-        print(f"{m:24s} groups/SM={per_sm:3d} " + " ".join(f"{x:8.1f}" for x in ts) + " ms", flush=True)
+        print(f"{name:34s} groups/SM={per_sm or 'default':>7} " + " ".join(f"{x:8.1f}" for x in ts) + " ms",
+              flush=True)

@@ -1,12 +1,14 @@
-"""One exact-path sweep launch (thread per run) for profiling:
-config 4, counter gate + reorder noise 0.1, 65536 seeds."""
+"""One exact-path sweep launch (thread per run) for profiling: config 3
+(VGG-16 x 4 workers / 1 PS), full cluster iteration makespans through the
+exact event replica — the bench's `event_replica_config3_makespans`."""
 import sys
 
 sys.path.insert(0, ".")
-from paper_1803_03288_b200.capi import Lib, policy  # noqa: E402
+from paper_1803_03288_b200.capi import Lib  # noqa: E402
 
-g = Lib().model("resnet_v2_101_training", 1)
-o = g.declared()
+L = Lib()
+c = L.model("vgg16_training", 1).expand(4, 1, 0)
+o = c.declared()
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 65536
-r = g.sweep_random(o, 1, n, policy(True, 0, 0.1))
+r = c.sweep_random(o, 1, n, None, makespans=True)
 print(r["count"], r["min_us"], r["argmin_seed"])
