@@ -3,6 +3,7 @@
 #include <algorithm>
 #include <charconv>
 #include <cstdio>
+#include <cstring>
 #include <string_view>
 
 #include "core.hpp"
@@ -109,20 +110,48 @@ std::string Report::json_text() const {
       q.str(keys[r]);
       qres[r] = std::move(q.s);
     }
-    w.s += '[';
+    // one pass into a buffer sized from the fragments' exact lengths
+    static constexpr std::string_view kOpen = ",\n    {\n      \"op\": ", kRes = ",\n      \"resource\": ",
+                                      kStart = ",\n      \"start_us\": ", kEnd = ",\n      \"end_us\": ",
+                                      kClose = "\n    }";
+    size_t bound = w.s.size() + 8;
+    for (const Event& e : events)
+      bound += kOpen.size() + kRes.size() + kStart.size() + kEnd.size() + kClose.size() + 6 * op_id(e.op).size() +
+               2 + qres[e.res].size() + 40;
+    const size_t at = w.s.size();
+    w.s.resize(bound);
+    char* p = w.s.data() + at;
+    auto put = [&p](std::string_view f) {
+      std::memcpy(p, f.data(), f.size());
+      p += f.size();
+    };
+    *p++ = '[';
     for (size_t i = 0; i < events.size(); ++i) {
       const Event& e = events[i];
-      w.s += i ? ",\n    {\n      \"op\": " : "\n    {\n      \"op\": ";
-      w.str(op_id(e.op));
-      w.s += ",\n      \"resource\": ";
-      w.s += qres[e.res];
-      w.s += ",\n      \"start_us\": ";
-      w.num(e.start);
-      w.s += ",\n      \"end_us\": ";
-      w.num(e.end);
-      w.s += "\n    }";
+      put(i ? kOpen : kOpen.substr(1));
+      const std::string& id = op_id(e.op);
+      *p++ = '"';
+      if (std::all_of(id.begin(), id.end(), [](char c) {
+            const unsigned char u = static_cast<unsigned char>(c);
+            return u > 0x1f && u != '"' && u != '\\';
+          })) {
+        put(id);
+      } else {  // rare: ids that need escaping
+        JsonText q;
+        q.str(id);
+        put(std::string_view(q.s).substr(1, q.s.size() - 2));
+      }
+      *p++ = '"';
+      put(kRes);
+      put(qres[e.res]);
+      put(kStart);
+      p = std::to_chars(p, p + 24, e.start).ptr;
+      put(kEnd);
+      p = std::to_chars(p, p + 24, e.end).ptr;
+      put(kClose);
     }
-    w.s += "\n  ]";
+    put("\n  ]");
+    w.s.resize(static_cast<size_t>(p - w.s.data()));
   }
   w.close('}');
   w.s += '\n';
