@@ -236,7 +236,8 @@ def exact_paths(lib, path):
 
 def cpu_baseline(path, target_s=10.0, g=None, o=None):
     """Reference library on this host: calibrate, then ~target_s of wall time
-    with one thread per core over contiguous seed slices. When the product
+    (and at least 100,000 seeds) with one thread per core over contiguous
+    seed slices. When the product
     graph/oracle are given, the sample's makespans are compared value by
     value with this library's for the same seeds."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
@@ -246,7 +247,7 @@ def cpu_baseline(path, target_s=10.0, g=None, o=None):
     cores = os.cpu_count() or 1
     cal = ref_sweep(path, SEED_LO, cores * 2, cores)
     rate = cal["sims"] / max(cal["seconds"], 1e-9)
-    n = max(cores, int(rate * target_s))
+    n = max(cores, int(rate * target_s), 100_000)  # >= 100k seeds at config 4
     binp = os.path.join(os.path.dirname(path), "ref_sample.bin")
     r = ref_sweep(path, SEED_LO, n, cores, None, binp)
     out = {"value": r["sims"] / r["seconds"], "unit": "sims/s", "cores": cores, "kind": "reference",
