@@ -599,3 +599,20 @@ def test_noisy_sweeps_through_the_closed_form_match_reference(lib, ref, noise):
         want = np.array([rg.simulate(ro, rg.random(s), policy(True, s, noise)).makespan() for s in range(1, 121)])
         assert np.array_equal(res["makespans"], want), g.name()
     assert closed >= 3
+
+
+def test_handles_outlive_their_graph(lib, ref):
+    """Oracles, schedules and reports stay valid after their graph handle is
+    freed (the reference's keep strings; here they keep the graph alive):
+    same bytes as the reference, freed in the same order."""
+    text = lib.model("resnet_v2_50_inference", 1).serialize()
+    out = {}
+    for name, L in (("ours", lib), ("ref", ref)):
+        g = L.graph(text)
+        o, s = g.declared(), g.tac(g.declared())
+        r = g.simulate(o, s, policy(True, 3, 0.0))
+        L.L.cs_graph_free(g.h)  # the graph goes first
+        g.h = None
+        del g
+        out[name] = (o.json(), s.serialize(), r.makespan(), r.json(), r.chrome_trace())
+    assert out["ours"] == out["ref"]
