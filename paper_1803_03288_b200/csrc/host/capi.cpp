@@ -134,6 +134,57 @@ struct DevPtr {
   }
 };
 
+// Page-locked staging buffers for pipelined read-backs, kept for the life of
+// the process (pinning is expensive per call); leased one call at a time.
+class PinnedPool {
+ public:
+  struct Lease {
+    PinnedPool* pool = nullptr;
+    char* p = nullptr;
+    size_t bytes = 0;
+    Lease() = default;
+    Lease(const Lease&) = delete;
+    Lease& operator=(const Lease&) = delete;
+    ~Lease() {
+      if (p) pool->put(p, bytes);
+    }
+  };
+  static PinnedPool& get() {
+    static PinnedPool* pool = new PinnedPool();  // never destroyed: the OS reclaims at exit
+    return *pool;
+  }
+  bool lease(size_t bytes, Lease& out) {
+    {
+      std::lock_guard<std::mutex> lock(mu_);
+      for (size_t i = 0; i < free_.size(); ++i)
+        if (free_[i].second >= bytes) {
+          out.pool = this;
+          out.p = free_[i].first;
+          out.bytes = free_[i].second;
+          free_.erase(free_.begin() + static_cast<std::ptrdiff_t>(i));
+          return true;
+        }
+    }
+    void* h = nullptr;
+    if (cudaMallocHost(&h, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    out.pool = this;
+    out.p = static_cast<char*>(h);
+    out.bytes = bytes;
+    return true;
+  }
+
+ private:
+  std::mutex mu_;
+  std::vector<std::pair<char*, size_t>> free_;
+  void put(char* p, size_t bytes) {
+    std::lock_guard<std::mutex> lock(mu_);
+    free_.emplace_back(p, bytes);
+  }
+};
+
 Policy policy_of(const cs_sim_policy* p) {  // capi.cpp:64-73 defaults
   Policy q;
   if (p) {
@@ -575,8 +626,71 @@ int cs_sweep_random(const cs_graph* g, const cs_oracle* o, uint64_t seed_lo, int
         const int64_t n = std::min(chunk, count - base);
         if (csk_sweep_reset(ctx->plan, nullptr, d_i64, d_f64, err)) fail(kInternal, err);
         const uint64_t lo = seed_lo + static_cast<uint64_t>(base);
-        if (csk_sweep_run(ctx->plan, lo, n, lo, nullptr, d_ms, d_wms, d_i64, d_f64, err))
+        // Per-seed outputs of a large chunk: launches of kSub seeds on one
+        // stream, each slice read back on a second stream through pinned
+        // staging while the next ones run, then copied to the caller's
+        // buffers — the transfer overlaps the kernels instead of following.
+        constexpr int64_t kSub = int64_t{1} << 19;
+        PinnedPool::Lease stage;
+        const size_t slice_bytes = 8 * static_cast<size_t>(kSub) * ((d_ms ? 1 : 0) + (d_wms ? W : 0));
+        const bool piped = (d_ms || d_wms) && n >= 4 * kSub && PinnedPool::get().lease(2 * slice_bytes, stage);
+        if (piped) {
+          cudaStream_t sa = nullptr, sb = nullptr;
+          cudaEvent_t ready = nullptr;
+          cudacheck(cudaStreamCreateWithFlags(&sa, cudaStreamNonBlocking));
+          cudacheck(cudaStreamCreateWithFlags(&sb, cudaStreamNonBlocking));
+          cudacheck(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+          const int64_t K = (n + kSub - 1) / kSub;
+          std::vector<cudaEvent_t> ran(static_cast<size_t>(K)), copied(static_cast<size_t>(K));
+          for (int64_t k = 0; k < K; ++k) {
+            cudacheck(cudaEventCreateWithFlags(&ran[k], cudaEventDisableTiming));
+            cudacheck(cudaEventCreateWithFlags(&copied[k], cudaEventDisableTiming));
+          }
+          cudacheck(cudaEventRecord(ready, 0));  // buffers and the reset, issued on the legacy stream
+          cudacheck(cudaStreamWaitEvent(sa, ready, 0));
+          int rc = 0;
+          for (int64_t k = 0; k < K && !rc; ++k) {
+            const int64_t off = k * kSub, nk = std::min(kSub, n - off);
+            rc = csk_sweep_run(ctx->plan, lo + static_cast<uint64_t>(off), nk, lo, sa, d_ms ? d_ms + off : nullptr,
+                               d_wms ? d_wms + off * W : nullptr, d_i64, d_f64, err);
+            if (!rc) cudacheck(cudaEventRecord(ran[k], sa));
+          }
+          auto land = [&](int64_t k) {  // staging slot k % 2 -> the caller's buffers
+            cudacheck(cudaEventSynchronize(copied[k]));
+            const int64_t off = k * kSub, nk = std::min(kSub, n - off);
+            const char* src = stage.p + (k & 1) * slice_bytes;
+            if (d_ms) {
+              std::memcpy(makespans_out + base + off, src, 8 * nk);
+              src += 8 * kSub;
+            }
+            if (d_wms) std::memcpy(worker_makespans_out + (base + off) * W, src, 8 * nk * W);
+          };
+          for (int64_t k = 0; k < K && !rc; ++k) {
+            const int64_t off = k * kSub, nk = std::min(kSub, n - off);
+            char* dst = stage.p + (k & 1) * slice_bytes;
+            cudacheck(cudaStreamWaitEvent(sb, ran[k], 0));
+            if (d_ms) {
+              cudacheck(cudaMemcpyAsync(dst, d_ms + off, 8 * nk, cudaMemcpyDeviceToHost, sb));
+              dst += 8 * kSub;
+            }
+            if (d_wms) cudacheck(cudaMemcpyAsync(dst, d_wms + off * W, 8 * nk * W, cudaMemcpyDeviceToHost, sb));
+            cudacheck(cudaEventRecord(copied[k], sb));
+            if (k >= 1) land(k - 1);
+          }
+          if (!rc) land(K - 1);
+          cudaStreamSynchronize(sa);
+          cudaStreamSynchronize(sb);
+          for (int64_t k = 0; k < K; ++k) {
+            cudaEventDestroy(ran[k]);
+            cudaEventDestroy(copied[k]);
+          }
+          cudaEventDestroy(ready);
+          cudaStreamDestroy(sa);
+          cudaStreamDestroy(sb);
+          if (rc) fail(kInternal, err);
+        } else if (csk_sweep_run(ctx->plan, lo, n, lo, nullptr, d_ms, d_wms, d_i64, d_f64, err)) {
           fail(kInternal, err);
+        }
         std::vector<int64_t> i64(CS_DSTATS_I64);
         std::vector<double> f64(CS_DSTATS_F64);
         {
@@ -585,8 +699,8 @@ int cs_sweep_random(const cs_graph* g, const cs_oracle* o, uint64_t seed_lo, int
           std::memcpy(i64.data(), st.data(), 8 * CS_DSTATS_I64);
           std::memcpy(f64.data(), st.data() + 8 * CS_DSTATS_I64, 8 * CS_DSTATS_F64);
         }
-        if (d_ms) cudacheck(cudaMemcpy(makespans_out + base, d_ms, 8 * n, cudaMemcpyDeviceToHost));
-        if (d_wms)
+        if (d_ms && !piped) cudacheck(cudaMemcpy(makespans_out + base, d_ms, 8 * n, cudaMemcpyDeviceToHost));
+        if (d_wms && !piped)
           cudacheck(cudaMemcpy(worker_makespans_out + base * W, d_wms, 8 * n * W, cudaMemcpyDeviceToHost));
         cs_sweep_stats part{};
         finish_stats(*ctx, i64.data(), f64.data(), lo, &part);
