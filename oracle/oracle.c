@@ -338,6 +338,130 @@ void orc_tac_incremental(const orc_graph* g, int32_t* prio) {
   free(col);
 }
 
+void orc_tac_rows(const orc_graph* g, int32_t* prio) {
+  /* The same SURVEY A.1 incremental TAC as orc_tac_incremental, with the
+   * dependency closure kept per ROW instead of per op: a non-recv op whose
+   * predecessors all sit in one non-recv row shares that row's set (its
+   * dep set is the union of its predecessors', properties.cpp:44-58), so
+   * cnt/M/xr are per row and a row's ops are weighed together when its cnt
+   * drops to one. Retire walks a column-major (recv x row) bitset. Needed
+   * where the op-level closure is 12.5 GB and the retire loop O(V) per round
+   * (config 5's top point: 10^6 ops / 10^5 recvs); checked against
+   * orc_tac_incremental and orc_tac in tests/test_oracle_pins.py. */
+  const int32_t n = g->n;
+  int32_t nr;
+  int32_t* col_op;
+  int32_t* col = recv_columns(g, &nr, &col_op);
+  const int32_t w = (nr + 63) / 64;
+  int32_t* order = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n ? n : 1));
+  int32_t* miss = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n ? n : 1));
+  int32_t head = 0, tail = 0;
+  for (int32_t v = 0; v < n; ++v)
+    if ((miss[v] = g->pred_off[v + 1] - g->pred_off[v]) == 0) order[tail++] = v;
+  while (head < tail) {
+    const int32_t v = order[head++];
+    for (int32_t e = g->succ_off[v]; e < g->succ_off[v + 1]; ++e)
+      if (--miss[g->succ_idx[e]] == 0) order[tail++] = g->succ_idx[e];
+  }
+  /* row of every op: recvs -> -1 (their set is {own column}); a non-recv op
+   * aliases the row of its predecessors when they all share one non-recv
+   * row, else opens a new row = OR of its predecessors' sets. */
+  int32_t* row = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n ? n : 1));
+  size_t cap = 1024, nrows = 0;
+  uint64_t* rbits = (uint64_t*)calloc(cap * (size_t)(w ? w : 1), sizeof(uint64_t));
+  for (int32_t h = 0; h < tail; ++h) {
+    const int32_t v = order[h];
+    if (col[v] >= 0) { row[v] = -1; continue; }
+    int32_t same = -2;
+    for (int32_t e = g->pred_off[v]; e < g->pred_off[v + 1]; ++e) {
+      const int32_t p = g->pred_idx[e], rp = row[p];
+      if (rp < 0 || (same != -2 && same != rp)) { same = -1; break; }
+      same = rp;
+    }
+    if (same >= 0) { row[v] = same; continue; }
+    if (nrows == cap) {
+      rbits = (uint64_t*)realloc(rbits, sizeof(uint64_t) * 2 * cap * (size_t)(w ? w : 1));
+      memset(rbits + cap * (size_t)w, 0, sizeof(uint64_t) * cap * (size_t)w);
+      cap *= 2;
+    }
+    uint64_t* dst = rbits + nrows * (size_t)w;
+    for (int32_t e = g->pred_off[v]; e < g->pred_off[v + 1]; ++e) {
+      const int32_t p = g->pred_idx[e];
+      if (row[p] < 0) {
+        dst[col[p] >> 6] |= 1ULL << (col[p] & 63);
+      } else {
+        const uint64_t* src = rbits + (size_t)row[p] * (size_t)w;
+        for (int32_t q = 0; q < w; ++q) dst[q] |= src[q];
+      }
+    }
+    row[v] = (int32_t)nrows++;
+  }
+  const size_t R_ = nrows, rw = (R_ + 63) / 64;
+  int64_t* wt = (int64_t*)calloc(R_ + 1, sizeof(int64_t));
+  int32_t* cnt = (int32_t*)calloc(R_ + 1, sizeof(int32_t));
+  int64_t* M = (int64_t*)calloc(R_ + 1, sizeof(int64_t));
+  int32_t* xr = (int32_t*)calloc(R_ + 1, sizeof(int32_t));
+  int64_t* P = (int64_t*)calloc((size_t)nr + 1, sizeof(int64_t));
+  uint64_t* cbits = (uint64_t*)calloc((size_t)(nr ? nr : 1) * (rw ? rw : 1), sizeof(uint64_t));
+  for (int32_t v = 0; v < n; ++v)
+    if (row[v] >= 0) wt[row[v]] += g->dur[v];
+  for (size_t r = 0; r < R_; ++r) {
+    const uint64_t* b = rbits + r * (size_t)w;
+    for (int32_t q = 0; q < w; ++q) {
+      uint64_t x = b[q];
+      while (x) {
+        const int32_t c = q * 64 + __builtin_ctzll(x);
+        cnt[r]++;
+        M[r] += g->dur[col_op[c]];
+        xr[r] ^= c;
+        cbits[(size_t)c * rw + (r >> 6)] |= 1ULL << (r & 63);
+        x &= x - 1;
+      }
+    }
+    if (cnt[r] == 1) P[xr[r]] += wt[r];
+  }
+  free(rbits);
+  uint8_t* out = (uint8_t*)malloc((size_t)nr + 1);
+  memset(out, 1, (size_t)nr + 1);
+  for (int32_t next = 0; next < nr; ++next) {
+    int32_t best = -1;
+    int64_t bp = 0, bm = 0, bmp = 0;
+    for (int32_t c = 0; c < nr; ++c) {
+      if (!out[c]) continue;
+      const int32_t r = col_op[c];
+      int64_t mp = ORC_INF;
+      for (int32_t e = g->succ_off[r]; e < g->succ_off[r + 1]; ++e) {
+        const int32_t s = row[g->succ_idx[e]];
+        if (s >= 0 && M[s] < mp) mp = M[s];
+      }
+      const int64_t m = g->dur[r]; /* an outstanding recv's own M */
+      if (best < 0 || orc_precedes(c, P[c], m, mp, best, bp, bm, bmp)) {
+        best = c;
+        bp = P[c];
+        bm = m;
+        bmp = mp;
+      }
+    }
+    prio[best] = next;
+    out[best] = 0;
+    const int64_t t = g->dur[col_op[best]];
+    const uint64_t* cb = cbits + (size_t)best * rw;
+    for (size_t q = 0; q < rw; ++q) {
+      uint64_t x = cb[q];
+      while (x) {
+        const size_t r = q * 64 + (size_t)__builtin_ctzll(x);
+        cnt[r]--;
+        M[r] -= t;
+        xr[r] ^= best;
+        if (cnt[r] == 1) P[xr[r]] += wt[r];
+        x &= x - 1;
+      }
+    }
+  }
+  free(out); free(cbits); free(P); free(xr); free(M); free(cnt); free(wt);
+  free(row); free(miss); free(order); free(col_op); free(col);
+}
+
 /* --------------------------------------------------------------- sim.cpp */
 
 typedef struct { int32_t* v; int32_t n, cap; } ivec;

@@ -76,6 +76,9 @@ void orc_tac(const orc_graph* g, int32_t* prio);
 /* tac via SURVEY Appendix A.1 (incremental O(V+E) rounds); valid when recvs
  * are roots (every graph tac() sees). Checked against orc_tac in tests. */
 void orc_tac_incremental(const orc_graph* g, int32_t* prio);
+/* the same with the closure kept per row of ops sharing one dependency set
+ * (large graphs: config 5's top point). */
+void orc_tac_rows(const orc_graph* g, int32_t* prio);
 
 /* simulate (sim.cpp:61-256). prio per op (-1 = unprioritized). Outputs the
  * makespan, violations, and per-op start/end. Returns 0, or 2 when the run

@@ -76,6 +76,7 @@ def lib():
         L.orc_tic.argtypes = [P(_OrcGraph), C.c_int, P(C.c_int32)]
         L.orc_tac.argtypes = [P(_OrcGraph), P(C.c_int32)]
         L.orc_tac_incremental.argtypes = [P(_OrcGraph), P(C.c_int32)]
+        L.orc_tac_rows.argtypes = [P(_OrcGraph), P(C.c_int32)]
         L.orc_simulate.argtypes = [P(_OrcGraph), P(C.c_int32), C.c_int, C.c_uint64,
                                    C.c_double, P(C.c_int64), P(C.c_int64),
                                    P(C.c_int64), P(C.c_int64)]
@@ -212,9 +213,10 @@ class OracleGraph:
                               _ptr(prio, C.c_int32))
         return {s: int(prio[c]) for c, s in enumerate(self.recv_ids)}, bool(total)
 
-    def tac(self, incremental: bool = False):
+    def tac(self, incremental: bool = False, rows: bool = False):
         prio = np.zeros(max(1, len(self.recv_cols)), dtype=np.int32)
-        f = lib().orc_tac_incremental if incremental else lib().orc_tac
+        f = (lib().orc_tac_rows if rows else
+             lib().orc_tac_incremental if incremental else lib().orc_tac)
         f(C.byref(self._s), _ptr(prio, C.c_int32))
         return {s: int(prio[c]) for c, s in enumerate(self.recv_ids)}
 

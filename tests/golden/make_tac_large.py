@@ -8,9 +8,11 @@ as SHA-256 of the priorities JSON (schedule serialisation order).
     python tests/golden/make_tac_large.py [--top]
     python tests/golden/make_tac_large.py --tic   # TIC digests, every config-5 size
 
-(--top, 10^6 ops / 10^5 recvs, takes hours with this oracle's row-major
-retire loop and is not committed; the multi-block TAC kernel that runs there
-is checked by forcing it on the committed sizes, tests/test_gpu_scale.py.)
+The orders come from the row-aliased form of the same restatement
+(orc_tac_rows: the closure per row of ops sharing one dependency set, a
+column-major retire), which reproduces orc_tac_incremental's digests at
+10^4 and 10^5 and finishes the top point (10^6 ops / 10^5 recvs, --top) in
+minutes; tests/test_oracle_pins.py checks all three forms on the corpus.
 """
 import hashlib
 import json
@@ -53,7 +55,7 @@ def main():
         t = time.time()
         g = lib.model(spec, 1)
         og = oracle.OracleGraph(json.loads(g.serialize()))
-        prio = og.tac(incremental=True)
+        prio = og.tac(rows=True)
         text = json.dumps(prio, sort_keys=True)
         out[spec] = {"sha256": hashlib.sha256(text.encode()).hexdigest(), "recvs": len(prio),
                      "first": min(prio, key=prio.get), "oracle_seconds": round(time.time() - t, 1)}

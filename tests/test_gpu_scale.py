@@ -29,8 +29,6 @@ def test_model_tac_tic_match_oracle(lib, orc, model):
 
 @pytest.mark.parametrize("spec", sorted(k for k in TAC_LARGE if not k.startswith("tic:")))
 def test_layered_tac_matches_oracle_digest(lib, spec):
-    if spec == "layered:1000000:100000" and not os.environ.get("TICTAC_SLOW"):
-        pytest.skip("config-5 top point (≈7 s on B200): set TICTAC_SLOW=1")
     g = lib.model(spec, 1)
     prio = g.tac(g.declared()).priorities()
     text = json.dumps(prio, sort_keys=True)
@@ -145,17 +143,25 @@ def test_config3_cluster_sweep_properties(lib, orc):
         assert list(wm[s - 1]) == list(pw.values()), s
 
 
-def test_config4_sweep_matches_reference_itself(lib, ref, tmp_path):
-    """config 4 sweep makespans against the reference library
-    itself for seeds 1..10^4 plus 10^4 seeds spread evenly over 1..2^24
-    (the reference's per-seed loop, oracle/_ref/ref_sweep, all host cores)."""
+@pytest.mark.parametrize("model,n", [("inception_v3_training", 1_000_000), ("resnet_v2_101_training", 1 << 24)])
+def test_config_sweep_matches_reference_itself(lib, ref, tmp_path, model, n):
+    """the config 2 (1M orders) and config 4 (2^24 orders) sweep
+    makespans against the reference library itself for seeds 1..10^4 plus
+    10^4 seeds spread evenly over the whole range (the reference's per-seed
+    loop, oracle/_ref/ref_sweep, all host cores); the sweep's min/argmin and
+    E histogram are checked against the returned per-seed makespans."""
     import subprocess
     import oracle
-    g = lib.model("resnet_v2_101_training", 1)
+    g = lib.model(model, 1)
     o = g.declared()
-    n = 1 << 24
-    ms = g.sweep_random(o, 1, n, None, makespans=True)["makespans"]
-    path = tmp_path / "config4.json"
+    res = g.sweep_random(o, 1, n, None, makespans=True)
+    ms = res["makespans"]
+    U, L = g.bounds(o)
+    assert res["min_us"] == ms.min() and res["argmin_seed"] == 1 + int(np.argmin(ms))
+    assert res["max_us"] == ms.max() and res["sum_us"] == int(ms.sum())
+    bins = np.minimum((1000 * (U - ms)) // (U - L), 999)
+    assert np.array_equal(res["e_hist"], np.bincount(bins, minlength=1000))
+    path = tmp_path / "config.json"
     path.write_text(g.serialize())
     spread = np.unique(np.linspace(1, n, 10_000, dtype=np.uint64))
     seeds = np.concatenate([np.arange(1, 10_001, dtype=np.uint64), spread])
