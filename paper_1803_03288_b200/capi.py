@@ -43,7 +43,9 @@ class SweepStats(C.Structure):
                 ("min_us", C.c_int64), ("argmin_seed", C.c_uint64), ("max_us", C.c_int64),
                 ("argmax_seed", C.c_uint64), ("sum_us", C.c_int64), ("sumsq_us", C.c_double),
                 ("e_hist", C.c_int64 * HIST_BINS), ("n_workers", C.c_int64),
-                ("straggler_sum", C.c_double), ("straggler_hist", C.c_int64 * HIST_BINS)]
+                ("straggler_sum", C.c_double), ("straggler_hist", C.c_int64 * HIST_BINS),
+                ("iter_min_us", C.c_int64), ("iter_argmin_seed", C.c_uint64), ("iter_max_us", C.c_int64),
+                ("iter_argmax_seed", C.c_uint64), ("iter_sum_us", C.c_int64)]
 
     def to_dict(self) -> dict:
         d = {k: getattr(self, k) for k, _ in self._fields_ if k not in ("e_hist", "straggler_hist")}

@@ -65,32 +65,35 @@ struct ChainArgs {
   double* f64;
 };
 
-template <typename T>
-struct Items;  // shared-memory shuffle array, [k / per_word][thread]
+template <typename T, int NT = kSweepThreads>
+struct Items;  // per-thread array in shared memory, [k / per_word][thread]
 
-template <>
-struct Items<uint8_t> {
+template <int NT>
+struct Items<uint8_t, NT> {
+  using value_type = uint8_t;
   uint32_t* base;
   // byte (k & 3) of word (k >> 2) of this thread's column:
-  // (k >> 2) * 4 * kSweepThreads + (k & 3) == k * kSweepThreads - (k & 3) * (kSweepThreads - 1)
+  // (k >> 2) * 4 * NT + (k & 3) == k * NT - (k & 3) * (NT - 1)
   __device__ __forceinline__ uint8_t* at(int k) const {
-    return reinterpret_cast<uint8_t*>(base) + k * kSweepThreads - (k & 3) * (kSweepThreads - 1);
+    return reinterpret_cast<uint8_t*>(base) + k * NT - (k & 3) * (NT - 1);
   }
   __device__ __forceinline__ void init(int R) const {
-    for (int q = 0; q < (R + 3) >> 2; ++q)
-      base[q * kSweepThreads] = 0x03020100u + 0x04040404u * static_cast<uint32_t>(q);
+    for (int q = 0; q < (R + 3) >> 2; ++q) base[q * NT] = 0x03020100u + 0x04040404u * static_cast<uint32_t>(q);
   }
+  static constexpr int words(int n) { return (n + 3) >> 2; }
 };
-template <>
-struct Items<uint16_t> {
+template <int NT>
+struct Items<uint16_t, NT> {
+  using value_type = uint16_t;
   uint32_t* base;
   __device__ __forceinline__ uint16_t* at(int k) const {
-    return reinterpret_cast<uint16_t*>(base + (k >> 1) * kSweepThreads) + (k & 1);
+    return reinterpret_cast<uint16_t*>(base + (k >> 1) * NT) + (k & 1);
   }
   __device__ __forceinline__ void init(int R) const {
     for (int q = 0; q < (R + 1) >> 1; ++q)
-      base[q * kSweepThreads] = (static_cast<uint32_t>(2 * q + 1) << 16) | static_cast<uint32_t>(2 * q);
+      base[q * NT] = (static_cast<uint32_t>(2 * q + 1) << 16) | static_cast<uint32_t>(2 * q);
   }
+  static constexpr int words(int n) { return (n + 1) >> 1; }
 };
 
 // Right-to-left suffix-min fold of one ordering; V = int32_t when every
@@ -110,9 +113,10 @@ struct FoldT {
 // One Fisher–Yates draw at slot i (1-based count of unfinished slots) with
 // bounded() value j: the element landing in its final slot i-1 is folded.
 // kStore: keep the permutation instead (the element is written to slot i-1).
-template <typename T, typename V, bool kStore = false>
-__device__ __forceinline__ void fy_draw(const Items<T>& items, int i, int j, FoldT<V>& f, const uint2* tab,
+template <typename It, typename V, bool kStore = false>
+__device__ __forceinline__ void fy_draw(const It& items, int i, int j, FoldT<V>& f, const uint2* tab,
                                         V ctot, const V* pw) {
+  using T = typename It::value_type;
   T* pj = items.at(j);
   const T x = *pj;
   if constexpr (kStore) {
@@ -129,8 +133,8 @@ __device__ __forceinline__ void fy_draw(const Items<T>& items, int i, int j, Fol
 // per draw) or past the first 311 outputs: full mt19937_64 state in local
 // memory, advanced to output `out` (0-based), then the reference loop.
 // (Everything by value: no address-taken locals in the hot caller.)
-template <typename T, typename V, bool kStore = false>
-__device__ __noinline__ FoldT<V> shuffle_slow(uint64_t seed, int out, int i, Items<T> items, FoldT<V> f,
+template <typename It, typename V, bool kStore = false>
+__device__ __noinline__ FoldT<V> shuffle_slow(uint64_t seed, int out, int i, It items, FoldT<V> f,
                                               const uint2* tab, V ctot, const V* pw) {
   uint64_t st[312];
   MtFull m{st, 0};
@@ -142,7 +146,7 @@ __device__ __noinline__ FoldT<V> shuffle_slow(uint64_t seed, int out, int i, Ite
     uint64_t v;
     do v = m.next();
     while (v > limit);
-    fy_draw<T, V, kStore>(items, i, static_cast<int>(v % n), f, tab, ctot, pw);
+    fy_draw<It, V, kStore>(items, i, static_cast<int>(v % n), f, tab, ctot, pw);
   }
   if constexpr (!kStore) f.add(tab[*items.at(0)], ctot, pw);
   return f;
@@ -151,9 +155,9 @@ __device__ __noinline__ FoldT<V> shuffle_slow(uint64_t seed, int out, int i, Ite
 // Draws d..d+K-1 with outputs v[] (pre-checked only by maybe_reject):
 // precise bounded() rejection test, then the swaps. Returns true when a
 // rejection sent the rest of the shuffle to the exact slow path.
-template <int K, typename T, typename V, bool kStore = false>
+template <int K, typename It, typename V, bool kStore = false>
 __device__ __forceinline__ bool draw_group(uint64_t seed, int R, int d, const uint64_t (&v)[K],
-                                           const Items<T>& items, FoldT<V>& f, const uint2* tab, V ctot,
+                                           const It& items, FoldT<V>& f, const uint2* tab, V ctot,
                                            const V* pw, const uint64_t* s_lim, const uint64_t* s_mag) {
   int j[K];
   bool any = false;
@@ -168,15 +172,15 @@ __device__ __forceinline__ bool draw_group(uint64_t seed, int R, int d, const ui
     for (int q = 0; q < K; ++q) {
       const int i = R - d - q;
       if (v[q] > s_lim[i]) {
-        f = shuffle_slow<T, V, kStore>(seed, d + q + 1, i, items, f, tab, ctot, pw);
+        f = shuffle_slow<It, V, kStore>(seed, d + q + 1, i, items, f, tab, ctot, pw);
         return true;
       }
-      fy_draw<T, V, kStore>(items, i, j[q], f, tab, ctot, pw);
+      fy_draw<It, V, kStore>(items, i, j[q], f, tab, ctot, pw);
     }
     return false;
   }
 #pragma unroll
-  for (int q = 0; q < K; ++q) fy_draw<T, V, kStore>(items, R - d - q, j[q], f, tab, ctot, pw);
+  for (int q = 0; q < K; ++q) fy_draw<It, V, kStore>(items, R - d - q, j[q], f, tab, ctot, pw);
   return false;
 }
 
@@ -186,8 +190,8 @@ __device__ __forceinline__ bool draw_group(uint64_t seed, int R, int d, const ui
 // t_d = f(s_d, s_d+1) ^ t_{d-156}, t_{d-156} = f(s_{d-156}, s_{d-155}) ^ s_d.
 // Four draws per iteration: four independent twist/temper/bounded chains
 // before the dependent shared-memory swaps.
-template <typename T, typename V, bool kStore = false>
-__device__ __forceinline__ void shuffle_fold(uint64_t seed, int R, const Items<T>& items, FoldT<V>& f,
+template <typename It, typename V, bool kStore = false>
+__device__ __forceinline__ void shuffle_fold(uint64_t seed, int R, const It& items, FoldT<V>& f,
                                              const uint2* tab, V ctot, const V* pw,
                                              const uint64_t* s_lim, const uint64_t* s_mag) {
   items.init(R);
@@ -206,14 +210,14 @@ __device__ __forceinline__ void shuffle_fold(uint64_t seed, int R, const Items<T
     a0 = a4;
     a1 = mt_step(a4, u + 5);
     b = mt_step(b3, u + 160);
-    if (draw_group<4, T, V, kStore>(seed, R, d, v, items, f, tab, ctot, pw, s_lim, s_mag)) return;
+    if (draw_group<4, It, V, kStore>(seed, R, d, v, items, f, tab, ctot, pw, s_lim, s_mag)) return;
   }
   for (; d < n1; ++d) {
     const uint64_t v[1] = {mt_temper(mt_twist(a0, a1, b))};
     a0 = a1;
     a1 = mt_step(a1, static_cast<uint32_t>(d + 2));
     b = mt_step(b, static_cast<uint32_t>(d + 157));
-    if (draw_group<1, T, V, kStore>(seed, R, d, v, items, f, tab, ctot, pw, s_lim, s_mag)) return;
+    if (draw_group<1, It, V, kStore>(seed, R, d, v, items, f, tab, ctot, pw, s_lim, s_mag)) return;
   }
   if (d < draws) {  // phase 2, c = (s_d-156, s_d-155)
     uint64_t c0 = seed, c1 = mt_step(seed, 1);
@@ -230,7 +234,7 @@ __device__ __forceinline__ void shuffle_fold(uint64_t seed, int R, const Items<T
       a1 = mt_step(a4, u + 5);
       c0 = c4;
       c1 = mt_step(c4, u - 151);
-      if (draw_group<4, T, V, kStore>(seed, R, d, v, items, f, tab, ctot, pw, s_lim, s_mag)) return;
+      if (draw_group<4, It, V, kStore>(seed, R, d, v, items, f, tab, ctot, pw, s_lim, s_mag)) return;
     }
     for (; d < n2; ++d) {
       const uint64_t v[1] = {mt_temper(mt_twist(a0, a1, mt_twist(c0, c1, a0)))};
@@ -238,10 +242,10 @@ __device__ __forceinline__ void shuffle_fold(uint64_t seed, int R, const Items<T
       a1 = mt_step(a1, static_cast<uint32_t>(d + 2));
       c0 = c1;
       c1 = mt_step(c1, static_cast<uint32_t>(d - 154));
-      if (draw_group<1, T, V, kStore>(seed, R, d, v, items, f, tab, ctot, pw, s_lim, s_mag)) return;
+      if (draw_group<1, It, V, kStore>(seed, R, d, v, items, f, tab, ctot, pw, s_lim, s_mag)) return;
     }
     if (d < draws) {  // beyond the first block (R > 312)
-      f = shuffle_slow<T, V, kStore>(seed, d, R - d, items, f, tab, ctot, pw);
+      f = shuffle_slow<It, V, kStore>(seed, d, R - d, items, f, tab, ctot, pw);
       return;
     }
   }
@@ -304,6 +308,66 @@ __device__ __forceinline__ void mt_outputs(uint64_t seed, int n, F&& use) {
   }
 }
 
+// Per-thread sweep statistics: packed min/max keys (m << key_bits) | offset
+// (lowest seed wins ties), sums, the E histogram and, for clusters, the
+// straggler histogram in shared memory; reduced per warp, then one set of
+// global atomics per block (flush).
+struct StatAcc {
+  unsigned long long kmin = ~0ULL, kmax = 0;
+  long long msum = 0, cnt = 0;
+  double sq = 0.0, ssum = 0.0;
+  __device__ __forceinline__ void add(const ChainArgs& a, uint64_t seed, int64_t m, int64_t hi, int64_t lo,
+                                      int* s_hist, int* s_shist) {
+    const unsigned long long off = seed - a.key_base;
+    kmin = min(kmin, (static_cast<unsigned long long>(m) << a.key_bits) | off);
+    kmax = max(kmax, (static_cast<unsigned long long>(m) << a.key_bits) | ((1ULL << a.key_bits) - 1 - off));
+    msum += m;
+    ++cnt;
+    sq += static_cast<double>(m) * static_cast<double>(m);
+    if (a.do_e) {
+      const int bin = static_cast<int>(floor(1000.0 * static_cast<double>(a.U - m) /
+                                             static_cast<double>(a.U - a.L)));
+      atomicAdd(&s_hist[min(max(bin, 0), kBins - 1)], 1);
+    }
+    if (a.cluster) {
+      int bin = 0;
+      if (hi > 0) {
+        ssum += static_cast<double>(hi - lo) / static_cast<double>(hi);
+        bin = min(static_cast<int>(floor(1000.0 * static_cast<double>(hi - lo) / static_cast<double>(hi))),
+                  kBins - 1);
+      }
+      atomicAdd(&s_shist[bin], 1);
+    }
+  }
+  __device__ __forceinline__ void flush(const ChainArgs& a, const int* s_hist, const int* s_shist) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      kmin = min(kmin, __shfl_xor_sync(~0u, kmin, o));
+      kmax = max(kmax, __shfl_xor_sync(~0u, kmax, o));
+      msum += __shfl_xor_sync(~0u, msum, o);
+      cnt += __shfl_xor_sync(~0u, cnt, o);
+      sq += __shfl_xor_sync(~0u, sq, o);
+      ssum += __shfl_xor_sync(~0u, ssum, o);
+    }
+    if (!a.i64) return;  // explicit-orders calls without statistics
+    if ((threadIdx.x & 31) == 0 && cnt > 0) {
+      atomicMin(&a.i64[0], kmin);
+      atomicMax(&a.i64[1], kmax);
+      atomicAdd(&a.i64[2], static_cast<unsigned long long>(msum));
+      atomicAdd(&a.i64[3], static_cast<unsigned long long>(cnt));
+      atomicAdd(&a.f64[0], sq);
+      atomicAdd(&a.f64[1], ssum);
+    }
+    __syncthreads();
+    if (a.do_e)
+      for (int k = threadIdx.x; k < kBins; k += blockDim.x)
+        if (s_hist[k]) atomicAdd(&a.i64[8 + k], static_cast<unsigned long long>(s_hist[k]));
+    if (a.cluster)
+      for (int k = threadIdx.x; k < kBins; k += blockDim.x)
+        if (s_shist[k]) atomicAdd(&a.i64[8 + kBins + k], static_cast<unsigned long long>(s_shist[k]));
+  }
+};
+
 // Gated runs with reorder noise: the noise only permutes the
 // gate sequence up front — adjacent swaps with probability p, one draw of the
 // separate stream Rng(splitmix64(choice_seed ^ salt)) per position, channels
@@ -354,9 +418,7 @@ __global__ void __launch_bounds__(kSweepThreads, 3) chain_sweep_kernel(ChainArgs
   __syncthreads();
   const Items<T> items{s_items + threadIdx.x};
 
-  unsigned long long kmin = ~0ULL, kmax = 0;
-  long long msum = 0, cnt = 0;
-  double sq = 0.0, ssum = 0.0;
+  StatAcc acc;
   const int64_t nthreads = static_cast<int64_t>(gridDim.x) * blockDim.x;
   for (int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; idx < a.count;
        idx += nthreads) {
@@ -393,7 +455,7 @@ __global__ void __launch_bounds__(kSweepThreads, 3) chain_sweep_kernel(ChainArgs
       } else {
         const uint64_t ws = a.cluster ? splitmix64(seed ^ (kPhi * static_cast<uint64_t>(w + 1))) : seed;
         if constexpr (kNoisy) {
-          shuffle_fold<T, V, true>(ws, R, items, f, tab, ctot, pw, s_lim, s_mag);  // rank order = the shuffle
+          shuffle_fold<Items<T>, V, true>(ws, R, items, f, tab, ctot, pw, s_lim, s_mag);  // rank order = the shuffle
           auto swap_at = [&](int pos, uint64_t v) {   // noise swaps -> gate order
             if ((v >> 11) < a.noise_thr) {
               T* p0 = items.at(pos - 1);
@@ -426,54 +488,198 @@ __global__ void __launch_bounds__(kSweepThreads, 3) chain_sweep_kernel(ChainArgs
     }
     const int64_t m = hi;  // worker graph: the makespan; cluster: iteration time
     if (a.makespans) a.makespans[idx] = m;
-    const unsigned long long off = seed - a.key_base;
-    kmin = min(kmin, (static_cast<unsigned long long>(m) << a.key_bits) | off);
-    kmax = max(kmax, (static_cast<unsigned long long>(m) << a.key_bits) | ((1ULL << a.key_bits) - 1 - off));
-    msum += m;
-    ++cnt;
-    sq += static_cast<double>(m) * static_cast<double>(m);
-    if (a.do_e) {
-      int bin = static_cast<int>(floor(1000.0 * static_cast<double>(a.U - m) /
-                                       static_cast<double>(a.U - a.L)));
-      atomicAdd(&s_hist[min(max(bin, 0), kBins - 1)], 1);
-    }
-    if (a.cluster) {
-      int bin = 0;
-      if (hi > 0) {
-        const double fr = static_cast<double>(hi - lo) / static_cast<double>(hi);
-        ssum += fr;
-        bin = min(static_cast<int>(floor(1000.0 * static_cast<double>(hi - lo) / static_cast<double>(hi))),
-                  kBins - 1);
-      }
-      atomicAdd(&s_shist[bin], 1);
-    }
+    acc.add(a, seed, m, hi, lo, s_hist, s_shist);
   }
-  // warp then block reduction, one set of global atomics per block
-#pragma unroll
-  for (int o = 16; o; o >>= 1) {
-    kmin = min(kmin, __shfl_xor_sync(~0u, kmin, o));
-    kmax = max(kmax, __shfl_xor_sync(~0u, kmax, o));
-    msum += __shfl_xor_sync(~0u, msum, o);
-    cnt += __shfl_xor_sync(~0u, cnt, o);
-    sq += __shfl_xor_sync(~0u, sq, o);
-    ssum += __shfl_xor_sync(~0u, ssum, o);
-  }
-  if (!a.i64) return;  // explicit-orders calls without statistics
-  if ((threadIdx.x & 31) == 0 && cnt > 0) {
-    atomicMin(&a.i64[0], kmin);
-    atomicMax(&a.i64[1], kmax);
-    atomicAdd(&a.i64[2], static_cast<unsigned long long>(msum));
-    atomicAdd(&a.i64[3], static_cast<unsigned long long>(cnt));
-    atomicAdd(&a.f64[0], sq);
-    atomicAdd(&a.f64[1], ssum);
-  }
+  acc.flush(a, s_hist, s_shist);
+}
+
+// ---- general worker DAGs: SURVEY Appendix A.2 without the nesting ------
+//
+// When the compute ops' recv-ancestor sets are not nested (branches, series-
+// parallel DAGs) the fold above does not apply, but A.2 still does: the
+// channel runs the gate order back to back (completion of position k is the
+// prefix sum c_k), and the single compute server's completion is the ERD
+// value over release positions,
+//     T_cpu = max over k in [-1, R) of  c_k + S(k),   S(k) = Σ w_j [lp_j >= k],
+// where class j (compute ops sharing one recv-ancestor set) is released at
+// its latest recv position lp_j = max{pos[r] : r in set(j)} (c_{-1} = 0, the
+// classes with no recv ancestor count only at k = -1). The host compiles the
+// graph once into a straight-line program over "join" classes (sets with two
+// or more recvs), each as the max over a few generators — recv positions or
+// earlier joins held in live slots (csrc/host/sweep.cpp) — so one ordering
+// costs the shuffle, one scatter of positions, the program (a few shared-
+// memory reads per generator) and one right-to-left pass over the position
+// bins. Classes whose set is a single recv {r} are weighed with the recv's
+// table entry instead of a bin. One thread owns one ordering; its arrays
+// (gate order, positions + slots, bins) sit in shared memory as
+// [index][thread] columns so every access hits the thread's own bank
+// whatever the index; the program and tables are read by all lanes at the
+// same address (broadcast).
+constexpr int kDagThreads = 64;
+
+template <typename V>
+struct DagEnt {  // per recv column: duration, weight of the classes whose set is {recv}
+  V d, wr;
+};
+
+struct DagArgs {
+  int J, L, P;                      // join classes, live slots, program words
+  int64_t lex_first;                // lexicographic source: permutation number of idx 0
+  const unsigned long long* fact;   // k! for k <= 20 (lexicographic source)
+};
+
+// Table image: lim/mag (R+2 each), DagEnt [W][R], join weights [W][J],
+// empty-set weights [W], program [P] u16; 16-byte padded (one bulk copy).
+__host__ __device__ inline size_t dag_table_bytes(int R, int W, int J, int P, size_t vb) {
+  return round16(16 * static_cast<size_t>(R + 2) + 2 * vb * W * R + vb * W * J + vb * W + 2 * static_cast<size_t>(P));
+}
+__host__ __device__ inline size_t dag_thread_bytes(int R, int L, size_t tb, size_t vb) {
+  const int per = tb == 1 ? 4 : 2;
+  return 4 * static_cast<size_t>((R + per - 1) / per + (R + L + per - 1) / per) + vb * (R + 1);
+}
+__host__ __device__ inline size_t dag_hist_off(int R, int W, int J, int P, size_t vb) {
+  return dag_table_bytes(R, W, J, P, vb);
+}
+__host__ __device__ inline size_t dag_smem(int R, int W, int J, int L, int P, int nhist, size_t tb, size_t vb) {
+  return round16(dag_table_bytes(R, W, J, P, vb) + 4 * static_cast<size_t>(nhist) * kBins +
+                 kDagThreads * dag_thread_bytes(R, L, tb, vb)) + 16;  // + mbarrier
+}
+
+// kSrc: 0 random_schedule(seed) (per-worker derived seeds on clusters),
+// 1 explicit orders (rows validated as read), 2 lexicographic permutation
+// number lex_first + idx (brute force; R <= 20, worker plans).
+template <typename T, typename V, bool kNoisy, int kSrc>
+__global__ void __launch_bounds__(kDagThreads) dag_sweep_kernel(ChainArgs a, DagArgs g) {
+  constexpr int NT = kDagThreads;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int R = a.R, W = a.W, J = g.J;
+  const size_t vb = sizeof(V);
+  const uint64_t* s_lim = reinterpret_cast<const uint64_t*>(smem);
+  const uint64_t* s_mag = s_lim + (R + 2);
+  const DagEnt<V>* s_ent = reinterpret_cast<const DagEnt<V>*>(s_mag + (R + 2));
+  const V* s_wj = reinterpret_cast<const V*>(s_ent + W * R);
+  const V* s_w0 = s_wj + W * J;
+  const uint16_t* s_prog = reinterpret_cast<const uint16_t*>(s_w0 + W);
+  const int nhist = (a.do_e ? 1 : 0) + (a.cluster ? 1 : 0);
+  int* s_hist = reinterpret_cast<int*>(smem + dag_hist_off(R, W, J, g.P, vb));
+  int* s_shist = s_hist + (a.do_e ? kBins : 0);
+  V* s_bins = reinterpret_cast<V*>(s_hist + nhist * kBins) + threadIdx.x;  // [k][NT]
+  uint32_t* s_words = reinterpret_cast<uint32_t*>(reinterpret_cast<V*>(s_hist + nhist * kBins) + (R + 1) * NT);
+  const Items<T, NT> perm{s_words + threadIdx.x};
+  const Items<T, NT> val{s_words + Items<T, NT>::words(R) * NT + threadIdx.x};
+  uint64_t* tables_ready = reinterpret_cast<uint64_t*>(smem + a.mbar_off);
+  if (threadIdx.x == 0) mbar_init(tables_ready, 1);
   __syncthreads();
-  if (a.do_e)
-    for (int k = threadIdx.x; k < kBins; k += blockDim.x)
-      if (s_hist[k]) atomicAdd(&a.i64[8 + k], static_cast<unsigned long long>(s_hist[k]));
-  if (a.cluster)
-    for (int k = threadIdx.x; k < kBins; k += blockDim.x)
-      if (s_shist[k]) atomicAdd(&a.i64[8 + kBins + k], static_cast<unsigned long long>(s_shist[k]));
+  if (threadIdx.x == 0) {
+    mbar_expect_tx(tables_ready, a.blob_bytes);
+    bulk_g2s(smem, a.blob, a.blob_bytes, tables_ready);
+  }
+  for (int k = threadIdx.x; k < nhist * kBins; k += blockDim.x) s_hist[k] = 0;
+  mbar_wait(tables_ready, 0);
+  __syncthreads();
+
+  StatAcc acc;
+  const int64_t nthreads = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; idx < a.count;
+       idx += nthreads) {
+    const uint64_t seed = a.seed_lo + static_cast<uint64_t>(idx);
+    int64_t hi = 0, lo = INT64_MAX;
+    NoiseState<kNoisy> noise;
+    if constexpr (kNoisy) noise.init(splitmix64(seed ^ kNoiseSalt));
+    for (int w = 0; w < W; ++w) {
+      const DagEnt<V>* ent = s_ent + w * R;
+      // 1. gate order (recv column at each position) and positions
+      if constexpr (kSrc == 1) {
+        const int32_t* o = a.orders + idx * R;
+        const T none = static_cast<T>(~T(0));
+        for (int c = 0; c < R; ++c) *val.at(c) = none;
+        int bad = 0;
+        for (int k = 0; k < R; ++k) {
+          int32_t c = o[k];
+          if (static_cast<uint32_t>(c) >= static_cast<uint32_t>(R)) {
+            bad |= 1;
+            c = 0;
+          } else if (*val.at(c) != none) {
+            bad |= 2;
+          }
+          *val.at(c) = static_cast<T>(k);
+          *perm.at(k) = static_cast<T>(c);
+        }
+        if (bad) atomicOr(a.bad_order, bad);
+      } else {
+        if constexpr (kSrc == 2) {
+          unsigned long long k = static_cast<unsigned long long>(g.lex_first + idx);
+          uint32_t left = (R >= 32) ? ~0u : ((1u << R) - 1u);
+          for (int pos = 0; pos < R; ++pos) {
+            const unsigned long long f = g.fact[R - 1 - pos];
+            const int q = static_cast<int>(k / f);
+            k -= static_cast<unsigned long long>(q) * f;
+            const int c = nth_bit(left, q);
+            left &= ~(1u << c);
+            *perm.at(pos) = static_cast<T>(c);
+          }
+        } else {
+          const uint64_t ws = a.cluster ? splitmix64(seed ^ (kPhi * static_cast<uint64_t>(w + 1))) : seed;
+          FoldT<V> f{0, 0, 0};
+          shuffle_fold<Items<T, NT>, V, true>(ws, R, perm, f, nullptr, V(0), nullptr, s_lim, s_mag);
+          if constexpr (kNoisy) {  // noise swaps on the rank order -> gate order (sim.cpp:106-114)
+            auto swap_at = [&](int pos, uint64_t v) {
+              if ((v >> 11) < a.noise_thr) {
+                T* p0 = perm.at(pos - 1);
+                T* p1 = perm.at(pos);
+                const T x = *p0;
+                *p0 = *p1;
+                *p1 = x;
+              }
+            };
+            if (W == 1 && R - 1 <= 311) {
+              mt_outputs(splitmix64(seed ^ kNoiseSalt), R - 1, [&](int d, uint64_t v) { swap_at(d + 1, v); });
+            } else {
+              for (int pos = 1; pos < R; ++pos) swap_at(pos, noise.m.next());
+            }
+          }
+        }
+        for (int k = 0; k < R; ++k) *val.at(*perm.at(k)) = static_cast<T>(k);
+      }
+      for (int k = 0; k <= R; ++k) s_bins[k * NT] = V(0);
+      // 2. latest recv position of every join class, weights into bins
+      {
+        const uint16_t* pc = s_prog;
+        const V* wj = s_wj + w * J;
+        for (int j = 0; j < J; ++j) {
+          const uint32_t h = pc[0];
+          const int n = static_cast<int>(h & 0x3FFFu);
+          int lp = *val.at(pc[1]);
+          for (int q = 2; q <= n; ++q) lp = max(lp, static_cast<int>(*val.at(pc[q])));
+          pc += n + 1;
+          if (h & 0x4000u) {
+            *val.at(*pc) = static_cast<T>(lp);
+            ++pc;
+          }
+          s_bins[lp * NT] += wj[j];
+        }
+      }
+      // 3. right-to-left: c_k + S(k)
+      const V ctot = static_cast<V>(a.ctot[w]);
+      V S = 0, suffix = 0, best = 0;
+      for (int k = R - 1; k >= 0; --k) {
+        const DagEnt<V> e = ent[*perm.at(k)];
+        S += s_bins[k * NT] + e.wr;
+        best = max(best, ctot - suffix + S);
+        suffix += e.d;
+      }
+      best = max(best, S + s_w0[w]);
+      const int64_t tcpu = static_cast<int64_t>(best);
+      const int64_t c64 = static_cast<int64_t>(ctot);
+      const int64_t mw = a.cluster ? max(tcpu, max(c64, tcpu) + a.send_tot[w]) : max(tcpu, c64);
+      if (a.worker_ms) a.worker_ms[idx * W + w] = mw;
+      hi = max(hi, mw);
+      lo = min(lo, mw);
+    }
+    if (a.makespans) a.makespans[idx] = hi;
+    acc.add(a, seed, hi, hi, lo, s_hist, s_shist);
+  }
+  acc.flush(a, s_hist, s_shist);
 }
 
 // Brute force (metrics.cpp:37-72) on the closed form: permutation number k
@@ -573,7 +779,24 @@ struct SweepPlan {
   size_t smem = 0, smem_orders = 0;
   int blocks = 0;
   uint64_t noise_thr = 0;
+  // general-DAG plans (dag_sweep_kernel): join classes, slots, program words,
+  // shared-memory item width (1: R <= 255, else 2)
+  int dag = 0, J = 0, Ls = 0, P = 0, tb = 1;
+  int blocks_orders = 0;
 };
+
+using DagFn = void (*)(ChainArgs, DagArgs);
+template <int kSrc>
+static DagFn dag_fn(const SweepPlan* p, bool noisy) {
+  if (kSrc == 0 && noisy) {
+    if (p->tb == 1)
+      return p->narrow ? dag_sweep_kernel<uint8_t, int32_t, true, 0> : dag_sweep_kernel<uint8_t, int64_t, true, 0>;
+    return p->narrow ? dag_sweep_kernel<uint16_t, int32_t, true, 0> : dag_sweep_kernel<uint16_t, int64_t, true, 0>;
+  }
+  if (p->tb == 1)
+    return p->narrow ? dag_sweep_kernel<uint8_t, int32_t, false, kSrc> : dag_sweep_kernel<uint8_t, int64_t, false, kSrc>;
+  return p->narrow ? dag_sweep_kernel<uint16_t, int32_t, false, kSrc> : dag_sweep_kernel<uint16_t, int64_t, false, kSrc>;
+}
 
 using SweepFn = void (*)(ChainArgs);
 static SweepFn sweep_fn(const SweepPlan* p) {
@@ -652,7 +875,7 @@ extern "C" SweepPlan* csk_sweep_plan(int32_t W, int32_t R, int32_t nc, const int
       return nullptr;
     }
   }
-  const int nhist = (!cluster && U != L ? 1 : 0) + (cluster ? 1 : 0);
+  const int nhist = (U != L ? 1 : 0) + (cluster ? 1 : 0);
   p->smem = sweep_smem(R, W, p->stride, nhist, p->narrow ? 4 : 8);
   p->smem_orders = sweep_smem(R, W, p->stride, nhist, 8);
   int dev = 0, sms = 148, occ = 1;
@@ -668,6 +891,85 @@ extern "C" SweepPlan* csk_sweep_plan(int32_t W, int32_t R, int32_t nc, const int
     return nullptr;
   }
   p->blocks = sms * occ;
+  return p;
+}
+
+extern "C" SweepPlan* csk_sweep_plan_dag(int32_t W, int32_t R, const int64_t* d, const int64_t* wr, int32_t J,
+                                         const int64_t* wj, const int64_t* w0, int32_t Ls, const uint16_t* prog,
+                                         int32_t P, const int64_t* send_total, int cluster, int64_t U, int64_t L,
+                                         uint64_t noise_thr, char* err) {
+  if (ensure_device(err)) return nullptr;
+  auto* p = new SweepPlan();
+  p->dag = 1;
+  p->noise_thr = noise_thr;
+  p->W = W;
+  p->R = R;
+  p->J = J;
+  p->Ls = Ls;
+  p->P = P;
+  p->cluster = cluster;
+  p->U = U;
+  p->L = L;
+  p->tb = R <= 255 ? 1 : 2;
+  p->narrow = U < (int64_t{1} << 31) ? 1 : 0;
+  std::vector<int64_t> ctot(W, 0);
+  for (int w = 0; w < W; ++w)
+    for (int c = 0; c < R; ++c) ctot[w] += d[w * R + c];
+  std::vector<uint64_t> lim(R + 2), mag(R + 2);
+  for (int n = 0; n <= R + 1; ++n) bounded_consts(static_cast<uint64_t>(n), &lim[n], &mag[n]);
+  const size_t vb = p->narrow ? 4 : 8;
+  p->blob_bytes = dag_table_bytes(R, W, J, P, vb);
+  std::vector<unsigned char> img(p->blob_bytes, 0);
+  unsigned char* q = img.data();
+  auto put = [&](int64_t v) {  // one value in the fold's width
+    if (p->narrow) {
+      const int32_t x = static_cast<int32_t>(v);
+      std::memcpy(q, &x, 4);
+    } else {
+      std::memcpy(q, &v, 8);
+    }
+    q += vb;
+  };
+  std::memcpy(q, lim.data(), 8ull * (R + 2));
+  q += 8ull * (R + 2);
+  std::memcpy(q, mag.data(), 8ull * (R + 2));
+  q += 8ull * (R + 2);
+  for (int k = 0; k < W * R; ++k) {
+    put(d[k]);
+    put(wr[k]);
+  }
+  for (int k = 0; k < W * J; ++k) put(wj[k]);
+  for (int w = 0; w < W; ++w) put(w0[w]);
+  std::memcpy(q, prog, 2ull * P);
+  auto up = [&](void** dst, const void* src, size_t bytes) {
+    if (cudaMalloc(dst, bytes ? bytes : 8) != cudaSuccess) return false;
+    return bytes == 0 || cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice) == cudaSuccess;
+  };
+  if (!up(&p->blob, img.data(), img.size()) || !up(&p->ctot, ctot.data(), sizeof(int64_t) * W) ||
+      !up(&p->send, send_total, sizeof(int64_t) * W)) {
+    std::snprintf(err, 256, "CUDA allocation for the sweep plan failed");
+    csk_sweep_plan_free(p);
+    return nullptr;
+  }
+  const int nhist = (U != L ? 1 : 0) + (cluster ? 1 : 0);
+  p->smem = dag_smem(R, W, J, Ls, P, nhist, p->tb, vb);
+  p->smem_orders = dag_smem(R, W, J, Ls, P, 0, p->tb, vb);
+  int dev = 0, sms = 148, occ = 0, occ_o = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const void* fns[] = {reinterpret_cast<const void*>(dag_fn<0>(p, noise_thr != 0)),
+                       reinterpret_cast<const void*>(dag_fn<1>(p, false)),
+                       reinterpret_cast<const void*>(dag_fn<2>(p, false))};
+  for (const void* fn : fns) allow_max_dynamic_smem(fn);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fns[0], kDagThreads, p->smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_o, fns[1], kDagThreads, p->smem_orders);
+  if (occ < 1 || occ_o < 1) {
+    std::snprintf(err, 256, "DAG sweep plan needs %zu bytes of shared memory per block", p->smem);
+    csk_sweep_plan_free(p);
+    return nullptr;
+  }
+  p->blocks = sms * occ;
+  p->blocks_orders = sms * occ_o;
   return p;
 }
 
@@ -702,7 +1004,7 @@ static ChainArgs chain_args(SweepPlan* p) {
   a.mag = static_cast<const uint64_t*>(p->mag);
   a.U = p->U;
   a.L = p->L;
-  a.do_e = !p->cluster && p->U != p->L;
+  a.do_e = p->U != p->L;
   a.key_bits = csk_key_bits(p->U);
   a.noise_thr = p->noise_thr;
   a.force_slow = std::getenv("TICTAC_SWEEP_FORCE_SLOW") != nullptr;
@@ -728,9 +1030,20 @@ extern "C" int csk_sweep_run(SweepPlan* p, uint64_t seed_lo, int64_t count, uint
     a.blob_bytes = static_cast<uint32_t>(p->blob_bytes);
     a.mbar_off = static_cast<uint32_t>(p->smem - 16);
   }
+  auto st = static_cast<cudaStream_t>(stream);
+  if (p->dag) {
+    a.blob = p->blob;
+    a.blob_bytes = static_cast<uint32_t>(p->blob_bytes);
+    a.mbar_off = static_cast<uint32_t>(p->smem - 16);
+    const int64_t need = (count + kDagThreads - 1) / kDagThreads;
+    const int blocks = static_cast<int>(std::min<int64_t>(p->blocks, need));
+    dag_fn<0>(p, p->noise_thr != 0)<<<blocks, kDagThreads, p->smem, st>>>(a, DagArgs{p->J, p->Ls, p->P, 0, nullptr});
+    LAUNCHED();
+    CK(cudaGetLastError());
+    return 0;
+  }
   const int64_t need = (count + kSweepThreads - 1) / kSweepThreads;
   const int blocks = static_cast<int>(std::min<int64_t>(p->blocks, need));
-  auto st = static_cast<cudaStream_t>(stream);
   sweep_fn(p)<<<blocks, kSweepThreads, p->smem, st>>>(a);
   LAUNCHED();
   CK(cudaGetLastError());
@@ -756,8 +1069,17 @@ extern "C" int csk_sweep_orders(SweepPlan* p, const int32_t* d_orders, int64_t n
   CK(cudaMallocAsync(&d_bad.p, sizeof(int), 0));
   CK(cudaMemsetAsync(d_bad.p, 0, sizeof(int), st));
   a.bad_order = d_bad.as<int>();
-  const int blocks = static_cast<int>(std::min<int64_t>(p->blocks, (n + kSweepThreads - 1) / kSweepThreads));
-  chain_sweep_kernel<uint8_t, true, int64_t><<<blocks, kSweepThreads, p->smem_orders, st>>>(a);
+  if (p->dag) {
+    a.blob = p->blob;
+    a.blob_bytes = static_cast<uint32_t>(p->blob_bytes);
+    a.mbar_off = static_cast<uint32_t>(p->smem_orders - 16);
+    a.cluster = 0;
+    const int blocks = static_cast<int>(std::min<int64_t>(p->blocks_orders, (n + kDagThreads - 1) / kDagThreads));
+    dag_fn<1>(p, false)<<<blocks, kDagThreads, p->smem_orders, st>>>(a, DagArgs{p->J, p->Ls, p->P, 0, nullptr});
+  } else {
+    const int blocks = static_cast<int>(std::min<int64_t>(p->blocks, (n + kSweepThreads - 1) / kSweepThreads));
+    chain_sweep_kernel<uint8_t, true, int64_t><<<blocks, kSweepThreads, p->smem_orders, st>>>(a);
+  }
   LAUNCHED();
   CK(cudaGetLastError());
   int bad = 0;
@@ -783,6 +1105,24 @@ extern "C" int csk_sweep_lex(SweepPlan* p, int64_t first, int64_t count, int64_t
   CK(cudaMallocAsync(&d_fact.p, sizeof(unsigned long long) * fact.size(), 0));
   CK(cudaMemcpy(d_fact.p, fact.data(), sizeof(unsigned long long) * fact.size(), cudaMemcpyHostToDevice));
   ChainArgs a = chain_args(p);
+  if (p->dag) {
+    a.blob = p->blob;
+    a.blob_bytes = static_cast<uint32_t>(p->blob_bytes);
+    a.mbar_off = static_cast<uint32_t>(p->smem_orders - 16);
+    a.do_e = 0;
+    a.cluster = 0;
+    a.count = count;
+    a.makespans = d_out;
+    a.i64 = nullptr;
+    a.f64 = nullptr;
+    const int blocks = static_cast<int>(std::min<int64_t>(p->blocks_orders, (count + kDagThreads - 1) / kDagThreads));
+    dag_fn<2>(p, false)<<<blocks, kDagThreads, p->smem_orders>>>(a, DagArgs{p->J, p->Ls, p->P, first,
+                                                                   d_fact.as<const unsigned long long>()});
+    LAUNCHED();
+    CK(cudaGetLastError());
+    CK(cudaDeviceSynchronize());
+    return 0;
+  }
   const size_t vb = p->narrow ? 4 : 8;
   const size_t smem = 8 * static_cast<size_t>(p->R) + ((vb * p->stride + 7) & ~size_t(7)) + 32 * kSweepThreads;
   int dev = 0, sms = 148;

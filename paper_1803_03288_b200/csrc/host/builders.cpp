@@ -237,7 +237,7 @@ std::shared_ptr<Graph> generate_model(const std::string& model, uint64_t seed) {
   bool training = false;
   std::vector<int64_t> bytes;
   std::string name = model;
-  bool layered = false;
+  bool layered = false, branchy = false;
   int64_t lay_v = 0, lay_r = 0;
   if (model.rfind("layered:", 0) == 0) {
     // layered:<V>:<R> — R/10 layers, 10 recvs feeding the head of a
@@ -250,15 +250,23 @@ std::shared_ptr<Graph> generate_model(const std::string& model, uint64_t seed) {
     R = static_cast<int>(lay_r);
     V = static_cast<int>(lay_v);
   } else {
+    // "<model>_branchy": the same recvs, bytes and compute times, arranged
+    // as Inception-style modules (below) instead of a backbone chain.
+    std::string base = model;
+    const std::string suffix = "_branchy";
+    if (base.size() > suffix.size() && base.compare(base.size() - suffix.size(), suffix.size(), suffix) == 0) {
+      base.resize(base.size() - suffix.size());
+      branchy = true;
+    }
     const Shape* s = nullptr;
     for (const Shape& k : kShapes)
-      if (model == k.name) s = &k;
+      if (base == k.name) s = &k;
     if (!s) fail(kParameter, "unknown model: " + model);
     R = s->R;
     V = s->V;
     training = s->training;
     const double total = s->mib * 1024.0 * 1024.0;
-    if (model == "vgg16_training") {
+    if (base == "vgg16_training") {
       for (int64_t e : vgg16_params()) bytes.push_back(4 * e);
     } else {
       // log-uniform over [2^8, 2^24) bytes, then scaled to the total.
@@ -315,6 +323,66 @@ std::shared_ptr<Graph> generate_model(const std::string& model, uint64_t seed) {
       if (l) edges.emplace_back(comp(head - 1), comp(head));
     }
     name = "layered-v" + std::to_string(V) + "-r" + std::to_string(R);
+  } else if (branchy) {
+    // Inception-style modules: split -> four parallel branches of 1, 3, 4
+    // and 2 ops -> concat (12 ops), after a short stem chain. Recvs (one per
+    // parameter tensor) attach evenly to the forward convolutions (stem and
+    // branch ops, not split/concat), so ops in different branches of a
+    // module depend on different recvs: recv-ancestor sets are not nested.
+    // Training appends a mirrored backward pass whose branch ops also read
+    // their forward counterpart's activations.
+    constexpr int kBranch[4] = {1, 3, 4, 2};
+    constexpr int kMod = 12;
+    const int F = training ? std::max(1, nc / 2) : nc;
+    std::vector<int> conv;  // forward convolutions, in order
+    // lays out `count` ops starting at `first`; returns per-module op lists
+    auto lay = [&](int first, int count, bool fwd, std::vector<std::vector<int>>* mods) {
+      const int nm = count >= kMod + 8 ? (count - 8) / kMod : 0;
+      const int stem = count - nm * kMod;
+      int prev = -1;
+      if (!fwd && first > 0) prev = first - 1;  // backward starts after the forward pass
+      for (int i = first; i < first + stem; ++i) {
+        if (prev >= 0) edges.emplace_back(comp(prev), comp(i));
+        if (fwd) conv.push_back(i);
+        prev = i;
+      }
+      int at = first + stem;
+      for (int m = 0; m < nm; ++m) {
+        std::vector<int> ids;
+        const int split = at++;
+        ids.push_back(split);
+        if (prev >= 0) edges.emplace_back(comp(prev), comp(split));
+        std::vector<int> tails;
+        for (int b = 0; b < 4; ++b) {
+          int p = split;
+          for (int k = 0; k < kBranch[b]; ++k) {
+            const int op = at++;
+            ids.push_back(op);
+            edges.emplace_back(comp(p), comp(op));
+            if (fwd) conv.push_back(op);
+            p = op;
+          }
+          tails.push_back(p);
+        }
+        const int cat = at++;
+        ids.push_back(cat);
+        for (int t : tails) edges.emplace_back(comp(t), comp(cat));
+        prev = cat;
+        if (mods) mods->push_back(std::move(ids));
+      }
+    };
+    std::vector<std::vector<int>> fmods, bmods;
+    lay(0, F, true, &fmods);
+    if (nc > F) {
+      lay(F, nc - F, false, &bmods);
+      for (size_t m = 0; m < bmods.size() && m < fmods.size(); ++m) {
+        const auto& f = fmods[fmods.size() - 1 - m];
+        for (int k = 1; k + 1 < kMod; ++k) edges.emplace_back(comp(f[k]), comp(bmods[m][k]));
+      }
+    }
+    const int ncv = static_cast<int>(conv.size());
+    for (int i = 0; i < R; ++i)
+      edges.emplace_back(padded("recv", i, R), comp(conv[static_cast<size_t>(int64_t{i} * ncv / R)]));
   } else {
     for (int i = 1; i < nc; ++i) {
       edges.emplace_back(comp(i - 1), comp(i));

@@ -592,8 +592,7 @@ int cs_sweep_random(const cs_graph* g, const cs_oracle* o, uint64_t seed_lo, int
     Policy p = policy_of(policy);
     const auto t0 = std::chrono::steady_clock::now();
     std::shared_ptr<SweepCtx> ctx = cached_sweep(g, o, p);
-    const bool cluster_m = ctx->cluster && makespans_out;  // needs the full event replica
-    if (!ctx->fast || cluster_m) {
+    if (!ctx->fast) {
       const auto t1 = std::chrono::steady_clock::now();
       sweep_exact(*ctx, seed_lo, count, makespans_out, worker_makespans_out, stats_out);
       if (std::getenv("TICTAC_EVENT_TRACE")) {
@@ -807,6 +806,12 @@ int cs_sweep_plan_info(const cs_sweep_plan* p, char** out_json) {
     j["edges"] = static_cast<int64_t>(c.g->edges().size());
     j["recvs_per_worker"] = c.R;
     j["classes"] = c.nc;
+    j["kernel"] = c.dag ? "dag_sweep_kernel" : "chain_sweep_kernel";
+    if (c.dag) {
+      j["joins"] = c.joins;
+      j["slots"] = c.slots;
+      j["program_words"] = c.prog_words;
+    }
     j["workers"] = c.cluster ? static_cast<int64_t>(c.workers.size()) : 1;
     int64_t erecv = 0;
     for (int32_t r : c.g->recv_ops()) erecv += c.g->nsucc(r);

@@ -30,6 +30,25 @@ struct ChainTables {
   std::vector<int32_t> first;  // per recv column
   std::vector<int64_t> pwsuf;  // nc + 1
   int64_t send_total = 0;
+  // general DAGs (not nested): weights of the join classes (program order),
+  // of the classes whose set is one recv (per recv column), of the classes
+  // with no recv ancestor
+  std::vector<int64_t> wj, wr;
+  int64_t w0 = 0;
+};
+
+// Straight-line program for general worker DAGs (sweep.cu dag_sweep_kernel):
+// per join class (recv-ancestor set with >= 2 recvs), in increasing set
+// size, its latest recv position = max over generators, each a recv column
+// (value index c < R: that recv's position) or an earlier join held in a
+// live slot (value index R + slot). Words: header n | 0x4000 (result kept in
+// a slot), n generator indices, [slot index]. Duration-independent.
+struct DagProgram {
+  int32_t J = 0, L = 0;            // join classes, live slots
+  std::vector<uint16_t> prog;
+  std::vector<int32_t> join_class;  // class id of every join, program order
+  std::vector<int32_t> single;      // per class: recv column when its set is {recv}, else -1
+  std::vector<int32_t> empty;       // classes with no recv ancestor
 };
 
 // Duration-independent part of the closed form for one worker (graph or
@@ -43,7 +62,138 @@ struct ChainShape {
   std::vector<int32_t> first;     // per recv column: first class containing it
   std::vector<int32_t> class_of;  // per op: class of a non-transfer op, else -1
   std::vector<int32_t> sends;     // send ops (cluster workers)
+  bool nested = true;             // chain classes (fold kernel), else `dag`
+  DagProgram dag;
 };
+
+// Compiles the join program from the classes' recv-ancestor bitsets (rep[j]
+// = a member op, sets ordered by size). Generators of class j: the classes
+// of the predecessors of one member that has no predecessor in j (its set
+// is their union), minus generators whose set is contained in another's.
+bool dag_program(const Graph& g, const std::vector<uint64_t>& bits, int32_t W, const std::vector<int32_t>& col,
+                 const std::vector<int32_t>& rep, const std::vector<int32_t>& class_of, DagProgram& out,
+                 std::string& why) {
+  const int32_t nc = static_cast<int32_t>(rep.size());
+  const int32_t R = static_cast<int32_t>(g.recv_ops().size());
+  auto set_of = [&](int32_t j) { return &bits[static_cast<size_t>(rep[j]) * W]; };
+  std::vector<int32_t> pop(nc, 0);
+  for (int32_t j = 0; j < nc; ++j)
+    for (int32_t q = 0; q < W; ++q) pop[j] += __builtin_popcountll(set_of(j)[q]);
+  auto subset = [&](int32_t a, int32_t b) {  // set(a) within set(b)
+    const uint64_t *x = set_of(a), *y = set_of(b);
+    for (int32_t q = 0; q < W; ++q)
+      if (x[q] & ~y[q]) return false;
+    return true;
+  };
+  auto has = [&](int32_t j, int32_t c) { return (set_of(j)[c >> 6] >> (c & 63)) & 1; };
+  // generators per class: g >= 0 class, g < 0 recv column -(g+1)
+  std::vector<std::vector<int32_t>> gens(nc);
+  std::vector<char> done(nc, 0);
+  out.single.assign(nc, -1);
+  out.empty.clear();
+  for (int32_t v = 0; v < g.n(); ++v) {
+    const int32_t j = class_of[v];
+    if (j < 0) continue;
+    std::vector<int32_t> gl;
+    bool own = false;
+    for (int32_t e = g.pred_off()[v]; e < g.pred_off()[v + 1]; ++e) {
+      const int32_t p = g.pred_idx()[e];
+      if (col[p] >= 0) {
+        gl.push_back(-(col[p] + 1));
+      } else if (class_of[p] >= 0) {
+        own |= class_of[p] == j;
+        gl.push_back(class_of[p]);
+      } else {
+        return why = "compute op depends on a non-recv transfer", false;
+      }
+    }
+    if (own) continue;  // not a first member of its class
+    std::sort(gl.begin(), gl.end());
+    gl.erase(std::unique(gl.begin(), gl.end()), gl.end());
+    std::vector<int32_t> red;
+    for (int32_t x : gl) {
+      bool drop = false;
+      for (int32_t y : gl) {
+        if (y < 0 || y == x) continue;
+        if (x < 0 ? has(y, -(x + 1)) : (subset(x, y) && (pop[x] < pop[y] || x > y))) drop = true;
+      }
+      if (!drop) red.push_back(x);
+    }
+    if (!done[j] || red.size() < gens[j].size()) gens[j] = red;
+    done[j] = 1;
+  }
+  // join classes in set-size order (classes are sorted that way already)
+  std::vector<int32_t> joins, jpos(nc, -1);
+  for (int32_t j = 0; j < nc; ++j) {
+    if (pop[j] == 0) {
+      out.empty.push_back(j);
+    } else if (pop[j] == 1) {
+      for (int32_t c = 0; c < R; ++c)
+        if (has(j, c)) out.single[j] = c;
+    } else {
+      if (!done[j] || gens[j].size() < 2) return why = "internal: join class without generators", false;
+      jpos[j] = static_cast<int32_t>(joins.size());
+      joins.push_back(j);
+    }
+  }
+  // last use of every join as a generator (in program order)
+  std::vector<int32_t> last(nc, -1);
+  for (int32_t k = 0; k < static_cast<int32_t>(joins.size()); ++k)
+    for (int32_t x : gens[joins[k]]) {
+      if (x < 0) continue;
+      if (jpos[x] < 0) {
+        // a generator class with a single-recv set stands for that recv
+        continue;
+      }
+      last[x] = k;
+    }
+  std::vector<int32_t> slot(nc, -1), free_slots;
+  int32_t nslots = 0;
+  out.prog.clear();
+  for (int32_t k = 0; k < static_cast<int32_t>(joins.size()); ++k) {
+    const int32_t j = joins[k];
+    std::vector<uint16_t> idx;
+    for (int32_t x : gens[j]) {
+      int32_t v;
+      if (x < 0) {
+        v = -(x + 1);
+      } else if (out.single[x] >= 0) {
+        v = out.single[x];
+      } else if (jpos[x] >= 0) {
+        if (slot[x] < 0) return why = "internal: generator used before its definition", false;
+        v = R + slot[x];
+      } else {
+        continue;  // empty-set generator: position -inf, no effect on the max
+      }
+      idx.push_back(static_cast<uint16_t>(v));
+    }
+    std::sort(idx.begin(), idx.end());
+    idx.erase(std::unique(idx.begin(), idx.end()), idx.end());
+    if (idx.empty()) return why = "internal: join without recv generators", false;
+    for (int32_t x : gens[j])  // release slots whose last use is this join
+      if (x >= 0 && jpos[x] >= 0 && last[x] == k) free_slots.push_back(slot[x]);
+    const bool keep = last[j] > k;
+    uint16_t h = static_cast<uint16_t>(idx.size());
+    if (idx.size() >= 0x4000) return why = "join with too many generators", false;
+    if (keep) {
+      h |= 0x4000;
+      if (free_slots.empty()) {
+        slot[j] = nslots++;
+      } else {
+        slot[j] = free_slots.back();
+        free_slots.pop_back();
+      }
+    }
+    out.prog.push_back(h);
+    out.prog.insert(out.prog.end(), idx.begin(), idx.end());
+    if (keep) out.prog.push_back(static_cast<uint16_t>(R + slot[j]));
+    if (R + nslots >= 0xFFFF) return why = "program too large", false;
+  }
+  out.J = static_cast<int32_t>(joins.size());
+  out.L = nslots;
+  out.join_class = joins;
+  return true;
+}
 
 ChainShape chain_shape(const Graph& g, bool allow_sends) {
   ChainShape cs;
@@ -108,18 +258,24 @@ ChainShape chain_shape(const Graph& g, bool allow_sends) {
     cs.class_of[v] = static_cast<int32_t>(rep.size()) - 1;
   }
   const int32_t nc = static_cast<int32_t>(rep.size());
-  for (int32_t j = 1; j < nc; ++j) {  // nested?
+  for (int32_t j = 1; j < nc && cs.nested; ++j) {  // nested?
     const uint64_t* a = &bits[static_cast<size_t>(rep[j - 1]) * W];
     const uint64_t* b = &bits[static_cast<size_t>(rep[j]) * W];
     for (int32_t q = 0; q < W; ++q)
-      if (a[q] & ~b[q]) return no("recv-ancestor sets are not nested");
+      if (a[q] & ~b[q]) cs.nested = false;
   }
   cs.R = R;
   cs.nc = nc;
-  cs.first.assign(R, nc);
-  for (int32_t j = nc - 1; j >= 0; --j)
-    for (int32_t c = 0; c < R; ++c)
-      if ((bits[static_cast<size_t>(rep[j]) * W + (c >> 6)] >> (c & 63)) & 1) cs.first[c] = j;
+  if (cs.nested && !std::getenv("TICTAC_SWEEP_FORCE_DAG")) {
+    cs.first.assign(R, nc);
+    for (int32_t j = nc - 1; j >= 0; --j)
+      for (int32_t c = 0; c < R; ++c)
+        if ((bits[static_cast<size_t>(rep[j]) * W + (c >> 6)] >> (c & 63)) & 1) cs.first[c] = j;
+  } else {
+    cs.nested = false;
+    std::string why;
+    if (!dag_program(g, bits, W, col, rep, cs.class_of, cs.dag, why)) return no(why.c_str());
+  }
   // sends: must be released exactly when the last compute finishes, i.e.
   // depend on every compute op that has no compute successor.
   if (allow_sends) {
@@ -156,8 +312,18 @@ bool chain_tables(const ChainShape& cs, const Graph& g, const std::vector<int64_
   std::vector<int64_t> weight(cs.nc, 0);
   for (int32_t v = 0; v < g.n(); ++v)
     if (cs.class_of[v] >= 0) weight[cs.class_of[v]] += dur[v];
-  t.pwsuf.assign(cs.nc + 1, 0);
-  for (int32_t j = cs.nc - 1; j >= 0; --j) t.pwsuf[j] = t.pwsuf[j + 1] + weight[j];
+  if (cs.nested) {
+    t.pwsuf.assign(cs.nc + 1, 0);
+    for (int32_t j = cs.nc - 1; j >= 0; --j) t.pwsuf[j] = t.pwsuf[j + 1] + weight[j];
+  } else {
+    t.wj.resize(cs.dag.J);
+    for (int32_t k = 0; k < cs.dag.J; ++k) t.wj[k] = weight[cs.dag.join_class[k]];
+    t.wr.assign(cs.R, 0);
+    for (int32_t j = 0; j < cs.nc; ++j)
+      if (cs.dag.single[j] >= 0) t.wr[cs.dag.single[j]] += weight[j];
+    t.w0 = 0;
+    for (int32_t j : cs.dag.empty) t.w0 += weight[j];
+  }
   t.send_total = 0;
   for (int32_t i : cs.sends) t.send_total += dur[i];
   for (int64_t x : t.d)
@@ -226,11 +392,23 @@ std::unique_ptr<SweepCtx> make_sweep(std::shared_ptr<const Graph> g, const TimeO
   bool ok = s->U < (int64_t{1} << 37);
   if (!ok) s->why = "makespan bound beyond the statistics key range";
   std::vector<ChainTables> tabs;
+  std::shared_ptr<const ChainShape> shape0;  // worker 0's shape (the program the workers share)
   if (ok && !s->cluster) {
     tabs.emplace_back();
-    const auto shape = g->memo<ChainShape>("chain", [&] { return chain_shape(*g, false); });
-    ok = chain_tables(*shape, *g, s->dur, tabs.back(), s->why);
+    shape0 = g->memo<ChainShape>("chain", [&] { return chain_shape(*g, false); });
+    ok = chain_tables(*shape0, *g, s->dur, tabs.back(), s->why);
   } else if (ok) {
+    // The full makespan (every event, the parameter servers' included) is
+    // the slowest worker's when the PS devices add no time: their ops only
+    // wait for the workers' sends and take zero time (config 3's
+    // expand_to_mr(…, ps_op_time = 0)); otherwise only the exact replica
+    // gives it (SURVEY A.2 covers the workers).
+    std::set<std::string> wset(s->workers.begin(), s->workers.end());
+    for (int32_t i = 0; i < g->n() && ok; ++i)
+      if (!wset.count(g->ops()[i].res.device) && s->dur[i] != 0) {
+        ok = false;
+        s->why = "parameter-server ops take time (full makespan needs the event replica)";
+      }
     // devices other than workers must not feed back into workers
     for (const auto& dv : s->workers) {
       auto part = g->partition(dv);
@@ -247,7 +425,9 @@ std::unique_ptr<SweepCtx> make_sweep(std::shared_ptr<const Graph> g, const TimeO
       tabs.emplace_back();
       const auto shape = g->memo<ChainShape>("chain:" + dv, [&] { return chain_shape(*part, true); });
       if (!(ok = chain_tables(*shape, *part, pd, tabs.back(), s->why))) break;
-      if (tabs.back().R != tabs[0].R || tabs.back().nc != tabs[0].nc) {
+      if (!shape0) shape0 = shape;
+      if (tabs.back().R != tabs[0].R || tabs.back().nc != tabs[0].nc || shape->nested != shape0->nested ||
+          (!shape->nested && shape->dag.prog != shape0->dag.prog)) {
         ok = false;
         s->why = "workers differ in shape";
         break;
@@ -255,6 +435,10 @@ std::unique_ptr<SweepCtx> make_sweep(std::shared_ptr<const Graph> g, const TimeO
     }
   }
   const auto t1 = std::chrono::steady_clock::now();
+  if (std::getenv("TICTAC_SWEEP_TRACE") && shape0)
+    std::fprintf(stderr, "[make_sweep] ok=%d nested=%d R=%d classes=%d joins=%d slots=%d words=%zu (%s)\n", ok ? 1 : 0,
+                 shape0->nested ? 1 : 0, shape0->R, shape0->nc, shape0->dag.J, shape0->dag.L,
+                 shape0->dag.prog.size(), s->why.c_str());
   if (ok) {
     const int32_t W = static_cast<int32_t>(tabs.size()), R = tabs[0].R, nc = tabs[0].nc;
     std::vector<int64_t> d, pw, send;
@@ -271,8 +455,25 @@ std::unique_ptr<SweepCtx> make_sweep(std::shared_ptr<const Graph> g, const TimeO
       const double t = std::ldexp(p.noise, 53);
       noise_thr = t == std::floor(t) ? static_cast<uint64_t>(t) : static_cast<uint64_t>(std::floor(t)) + 1;
     }
-    s->plan = csk_sweep_plan(W, R, nc, d.data(), first.data(), pw.data(), send.data(),
-                             s->cluster ? 1 : 0, s->U, s->L, noise_thr, err);
+    if (shape0->nested) {
+      s->plan = csk_sweep_plan(W, R, nc, d.data(), first.data(), pw.data(), send.data(),
+                               s->cluster ? 1 : 0, s->U, s->L, noise_thr, err);
+    } else {
+      const DagProgram& dp = shape0->dag;
+      std::vector<int64_t> wr, wj, w0;
+      for (const auto& t : tabs) {
+        wr.insert(wr.end(), t.wr.begin(), t.wr.end());
+        wj.insert(wj.end(), t.wj.begin(), t.wj.end());
+        w0.push_back(t.w0);
+      }
+      s->plan = csk_sweep_plan_dag(W, R, d.data(), wr.data(), dp.J, wj.data(), w0.data(), dp.L, dp.prog.data(),
+                                   static_cast<int32_t>(dp.prog.size()), send.data(), s->cluster ? 1 : 0, s->U,
+                                   s->L, noise_thr, err);
+      s->dag = true;
+      s->joins = dp.J;
+      s->slots = dp.L;
+      s->prog_words = static_cast<int32_t>(dp.prog.size());
+    }
     if (!s->plan) fail(kInternal, err);
     s->fast = true;
     s->nc = nc;
@@ -310,6 +511,13 @@ void finish_stats(const SweepCtx& s, const int64_t* i64, const double* f64, uint
   }
   out->n_workers = s.cluster ? static_cast<int64_t>(s.workers.size()) : 0;
   out->straggler_sum = f64[1];
+  if (s.cluster) {  // closed-form clusters: the makespan is the iteration time (make_sweep)
+    out->iter_min_us = out->min_us;
+    out->iter_argmin_seed = out->argmin_seed;
+    out->iter_max_us = out->max_us;
+    out->iter_argmax_seed = out->argmax_seed;
+    out->iter_sum_us = out->sum_us;
+  }
 }
 
 // Exact path: device event simulator over seeds, stats on the host (these
@@ -329,7 +537,17 @@ void sweep_exact(SweepCtx& s, uint64_t seed_lo, int64_t count, int64_t* makespan
     wdev.push_back(static_cast<int32_t>(std::lower_bound(devs.begin(), devs.end(), w) - devs.begin()));
   std::vector<int64_t> i64(CS_DSTATS_I64, 0);
   std::vector<double> f64(CS_DSTATS_F64, 0.0);
-  i64[0] = -1;  // as unsigned: max
+  // min/max with their lowest seeds, tracked directly (no packed keys: this
+  // path also serves U beyond the closed form's key range)
+  struct Ext {
+    int64_t lo = INT64_MAX, hi = INT64_MIN;
+    uint64_t alo = 0, ahi = 0;
+    void add(int64_t v, uint64_t seed) {
+      if (v < lo) lo = v, alo = seed;
+      if (v > hi) hi = v, ahi = seed;
+    }
+  } mk, it;
+  int64_t it_sum = 0;
   const int64_t chunk = 1 << 20;
   std::vector<int64_t> ms, viol, dev_end;
   std::vector<int32_t> st;
@@ -370,24 +588,48 @@ void sweep_exact(SweepCtx& s, uint64_t seed_lo, int64_t count, int64_t* makespan
         }
         i64[1008 + bin]++;
       }
-      // cluster statistics are over the iteration time, as in the fast path
-      const int64_t mstat = s.cluster ? hi : m;
-      const uint64_t off = seed - seed_lo;
-      const int kb = csk_key_bits(s.U);
-      const uint64_t kmin = (static_cast<uint64_t>(mstat) << kb) | off;
-      const uint64_t kmax = (static_cast<uint64_t>(mstat) << kb) | (((1ULL << kb) - 1) - off);
-      if (kmin < static_cast<uint64_t>(i64[0])) i64[0] = static_cast<int64_t>(kmin);
-      if (kmax > static_cast<uint64_t>(i64[1])) i64[1] = static_cast<int64_t>(kmax);
-      i64[2] += mstat;
+      // makespan statistics (the reference's sweep summary); iteration time
+      // (slowest worker) separately for clusters
+      mk.add(m, seed);
+      if (s.cluster) {
+        it.add(hi, seed);
+        it_sum += hi;
+      }
+      i64[2] += m;
       i64[3] += 1;
-      f64[0] += static_cast<double>(mstat) * static_cast<double>(mstat);
-      if (!s.cluster && s.U != s.L) {
+      f64[0] += static_cast<double>(m) * static_cast<double>(m);
+      if (s.U != s.L) {
         const int64_t bin = (1000 * (s.U - m)) / (s.U - s.L);
         i64[8 + std::min<int64_t>(999, std::max<int64_t>(0, bin))]++;
       }
     }
   }
-  if (stats) finish_stats(s, i64.data(), f64.data(), seed_lo, stats);
+  if (!stats) return;
+  std::memset(stats, 0, sizeof(*stats));
+  stats->count = i64[3];
+  stats->upper_us = s.U;
+  stats->lower_us = s.L;
+  if (stats->count > 0) {
+    stats->min_us = mk.lo;
+    stats->argmin_seed = mk.alo;
+    stats->max_us = mk.hi;
+    stats->argmax_seed = mk.ahi;
+  }
+  stats->sum_us = i64[2];
+  stats->sumsq_us = f64[0];
+  for (int k = 0; k < CS_HIST_BINS; ++k) {
+    stats->e_hist[k] = i64[8 + k];
+    stats->straggler_hist[k] = i64[1008 + k];
+  }
+  stats->n_workers = s.cluster ? nw : 0;
+  stats->straggler_sum = f64[1];
+  if (s.cluster && stats->count > 0) {
+    stats->iter_min_us = it.lo;
+    stats->iter_argmin_seed = it.alo;
+    stats->iter_max_us = it.hi;
+    stats->iter_argmax_seed = it.ahi;
+    stats->iter_sum_us = it_sum;
+  }
 }
 
 }  // namespace tictac

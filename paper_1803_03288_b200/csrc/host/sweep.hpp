@@ -24,6 +24,8 @@ struct SweepCtx {
   std::vector<int32_t> recv_worker;  // per recv column
   SweepPlan* plan = nullptr;
   int32_t R = 0, nc = 0;
+  bool dag = false;  // general-DAG program (not nested chain classes)
+  int32_t joins = 0, slots = 0, prog_words = 0;
   std::string why;  // why the closed form does not apply
   // Closed-form makespan of one gate order (recv columns, rank order) on a
   // worker-graph plan: one kernel launch on small cached device buffers.
