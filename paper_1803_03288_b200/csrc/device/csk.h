@@ -97,13 +97,16 @@ SweepPlan* csk_sweep_plan(int32_t W, int32_t R, int32_t nc, const int64_t* d,
                           const int32_t* first, const int64_t* pwsuf, const int64_t* send_total,
                           int cluster, int64_t U, int64_t L, uint64_t noise_thr, char* err);
 /* General worker DAGs (recv-ancestor sets not nested): per
- * worker, recv durations d and single-recv class weights wr ([W][R]), join
- * class weights wj ([W][J]), empty-set class weights w0 ([W]); the program
- * (P u16 words, Ls live slots; csrc/host/sweep.cpp) is shared by all
- * workers. Runs through the same csk_sweep_run / _orders / _lex calls. */
-SweepPlan* csk_sweep_plan_dag(int32_t W, int32_t R, const int64_t* d, const int64_t* wr, int32_t J,
-                              const int64_t* wj, const int64_t* w0, int32_t Ls, const uint16_t* prog,
-                              int32_t P, const int64_t* send_total, int cluster, int64_t U, int64_t L,
+ * worker, recv durations d and single-recv class weights wr ([W][R]), record
+ * weights wj ([W][nrec]), empty-set class weights w0 ([W]); the program
+ * (nrec records of 4 value indexes: three generators and the output; -1 =
+ * discard output, -2 = the previous record's result (first generator
+ * only), -3 = padding record; groups of four; Ls live slots;
+ * csrc/host/sweep.cpp) is shared by all workers. Runs through the same
+ * csk_sweep_run / _orders / _lex calls. */
+SweepPlan* csk_sweep_plan_dag(int32_t W, int32_t R, const int64_t* d, const int64_t* wr, int32_t nrec,
+                              const int32_t* recs, const int64_t* wj, const int64_t* w0, int32_t Ls,
+                              const int64_t* send_total, int cluster, int64_t U, int64_t L,
                               uint64_t noise_thr, char* err);
 void csk_sweep_plan_free(SweepPlan* p);
 /* Stats layout documented in include/commsched.h (CS_DSTATS_*). */

@@ -523,26 +523,36 @@ struct DagEnt {  // per recv column: duration, weight of the classes whose set i
 };
 
 struct DagArgs {
-  int J, L, P;                      // join classes, live slots, program words
+  int nrec, L;                      // program records (multiple of 4), live slots
   int64_t lex_first;                // lexicographic source: permutation number of idx 0
   const unsigned long long* fact;   // k! for k <= 20 (lexicographic source)
 };
 
-// Table image: lim/mag (R+2 each), DagEnt [W][R], join weights [W][J],
-// empty-set weights [W], program [P] u16; 16-byte padded (one bulk copy).
-__host__ __device__ inline size_t dag_table_bytes(int R, int W, int J, int P, size_t vb) {
-  return round16(16 * static_cast<size_t>(R + 2) + 2 * vb * W * R + vb * W * J + vb * W + 2 * static_cast<size_t>(P));
+// Table image: lim/mag (R+2 each), program records [nrec] (uint4: byte
+// offsets of three generators and the output inside a thread's value
+// column), DagEnt [W][R], record weights [W][nrec], empty-set weights [W];
+// 16-byte padded (one bulk copy).
+__host__ __device__ inline size_t dag_table_bytes(int R, int W, int nrec, size_t vb) {
+  return round16(16 * static_cast<size_t>(R + 2) + 16 * static_cast<size_t>(nrec) + 2 * vb * W * R +
+                 vb * W * nrec + vb * W);
 }
+// per thread: gate order (R items), values (R recv positions + L slots + 1
+// discard), bins (R + 1)
 __host__ __device__ inline size_t dag_thread_bytes(int R, int L, size_t tb, size_t vb) {
   const int per = tb == 1 ? 4 : 2;
-  return 4 * static_cast<size_t>((R + per - 1) / per + (R + L + per - 1) / per) + vb * (R + 1);
+  return 4 * static_cast<size_t>((R + per - 1) / per + (R + L + 1 + per - 1) / per) + vb * (R + 1);
 }
-__host__ __device__ inline size_t dag_hist_off(int R, int W, int J, int P, size_t vb) {
-  return dag_table_bytes(R, W, J, P, vb);
-}
-__host__ __device__ inline size_t dag_smem(int R, int W, int J, int L, int P, int nhist, size_t tb, size_t vb) {
-  return round16(dag_table_bytes(R, W, J, P, vb) + 4 * static_cast<size_t>(nhist) * kBins +
+__host__ __device__ inline size_t dag_smem(int R, int W, int nrec, int L, int nhist, size_t tb, size_t vb) {
+  return round16(dag_table_bytes(R, W, nrec, vb) + 4 * static_cast<size_t>(nhist) * kBins +
                  kDagThreads * dag_thread_bytes(R, L, tb, vb)) + 16;  // + mbarrier
+}
+// record flags: first generator = the previous record's result (ACC);
+// output of a real record (updates ACC; padding records do not)
+constexpr uint32_t kDagAccFlag = 0x80000000u, kDagRealFlag = 0x80000000u, kDagOffMask = 0x7FFFFFFFu;
+// byte offset of item k inside a thread's Items<T, kDagThreads> column
+__host__ __device__ inline uint32_t dag_item_off(int k, size_t tb) {
+  return tb == 1 ? static_cast<uint32_t>(k * kDagThreads - (k & 3) * (kDagThreads - 1))
+                 : static_cast<uint32_t>((k >> 1) * kDagThreads * 4 + (k & 1) * 2);
 }
 
 // kSrc: 0 random_schedule(seed) (per-worker derived seeds on clusters),
@@ -552,16 +562,16 @@ template <typename T, typename V, bool kNoisy, int kSrc>
 __global__ void __launch_bounds__(kDagThreads) dag_sweep_kernel(ChainArgs a, DagArgs g) {
   constexpr int NT = kDagThreads;
   extern __shared__ __align__(16) unsigned char smem[];
-  const int R = a.R, W = a.W, J = g.J;
+  const int R = a.R, W = a.W, NR = g.nrec;
   const size_t vb = sizeof(V);
   const uint64_t* s_lim = reinterpret_cast<const uint64_t*>(smem);
   const uint64_t* s_mag = s_lim + (R + 2);
-  const DagEnt<V>* s_ent = reinterpret_cast<const DagEnt<V>*>(s_mag + (R + 2));
+  const uint4* s_rec = reinterpret_cast<const uint4*>(s_mag + (R + 2));
+  const DagEnt<V>* s_ent = reinterpret_cast<const DagEnt<V>*>(s_rec + NR);
   const V* s_wj = reinterpret_cast<const V*>(s_ent + W * R);
-  const V* s_w0 = s_wj + W * J;
-  const uint16_t* s_prog = reinterpret_cast<const uint16_t*>(s_w0 + W);
+  const V* s_w0 = s_wj + W * NR;
   const int nhist = (a.do_e ? 1 : 0) + (a.cluster ? 1 : 0);
-  int* s_hist = reinterpret_cast<int*>(smem + dag_hist_off(R, W, J, g.P, vb));
+  int* s_hist = reinterpret_cast<int*>(smem + dag_table_bytes(R, W, NR, vb));
   int* s_shist = s_hist + (a.do_e ? kBins : 0);
   V* s_bins = reinterpret_cast<V*>(s_hist + nhist * kBins) + threadIdx.x;  // [k][NT]
   uint32_t* s_words = reinterpret_cast<uint32_t*>(reinterpret_cast<V*>(s_hist + nhist * kBins) + (R + 1) * NT);
@@ -575,8 +585,10 @@ __global__ void __launch_bounds__(kDagThreads) dag_sweep_kernel(ChainArgs a, Dag
     bulk_g2s(smem, a.blob, a.blob_bytes, tables_ready);
   }
   for (int k = threadIdx.x; k < nhist * kBins; k += blockDim.x) s_hist[k] = 0;
+  for (int k = 0; k <= R; ++k) s_bins[k * NT] = V(0);  // the fold re-zeroes every bin it reads
   mbar_wait(tables_ready, 0);
   __syncthreads();
+  unsigned char* vcol = reinterpret_cast<unsigned char*>(val.base);  // value column (byte offsets)
 
   StatAcc acc;
   const int64_t nthreads = static_cast<int64_t>(gridDim.x) * blockDim.x;
@@ -641,32 +653,72 @@ __global__ void __launch_bounds__(kDagThreads) dag_sweep_kernel(ChainArgs a, Dag
         }
         for (int k = 0; k < R; ++k) *val.at(*perm.at(k)) = static_cast<T>(k);
       }
-      for (int k = 0; k <= R; ++k) s_bins[k * NT] = V(0);
-      // 2. latest recv position of every join class, weights into bins
+      // 2. latest recv position of every join class, weights into bins:
+      // groups of four records, generators loaded before outputs stored
       {
-        const uint16_t* pc = s_prog;
-        const V* wj = s_wj + w * J;
-        for (int j = 0; j < J; ++j) {
-          const uint32_t h = pc[0];
-          const int n = static_cast<int>(h & 0x3FFFu);
-          int lp = *val.at(pc[1]);
-          for (int q = 2; q <= n; ++q) lp = max(lp, static_cast<int>(*val.at(pc[q])));
-          pc += n + 1;
-          if (h & 0x4000u) {
-            *val.at(*pc) = static_cast<T>(lp);
-            ++pc;
+        const V* wj = s_wj + w * NR;
+        int accv = 0;  // the previous real record's result
+        for (int q = 0; q < NR; q += 4) {
+          uint4 rc[4];
+          V wt[4];
+          int lp[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            rc[i] = s_rec[q + i];
+            wt[i] = wj[q + i];
           }
-          s_bins[lp * NT] += wj[j];
+          int x[4], y[4], z[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            x[i] = *reinterpret_cast<const T*>(vcol + (rc[i].x & kDagOffMask));
+            y[i] = *reinterpret_cast<const T*>(vcol + rc[i].y);
+            z[i] = *reinterpret_cast<const T*>(vcol + rc[i].z);
+          }
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            lp[i] = max(max((rc[i].x & kDagAccFlag) ? accv : x[i], y[i]), z[i]);
+            accv = (rc[i].w & kDagRealFlag) ? lp[i] : accv;
+          }
+#pragma unroll
+          for (int i = 0; i < 4; ++i) *reinterpret_cast<T*>(vcol + (rc[i].w & kDagOffMask)) = static_cast<T>(lp[i]);
+          // equal positions inside the group: the later record carries the sum
+#pragma unroll
+          for (int j = 1; j < 4; ++j)
+#pragma unroll
+            for (int i = 0; i < j; ++i)
+              if (lp[i] == lp[j]) {
+                wt[j] += wt[i];
+                wt[i] = V(0);
+              }
+          V old[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) old[i] = s_bins[lp[i] * NT];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) s_bins[lp[i] * NT] = old[i] + wt[i];
         }
       }
-      // 3. right-to-left: c_k + S(k)
+      // 3. right-to-left: c_k + S(k); every bin is re-zeroed as it is read
       const V ctot = static_cast<V>(a.ctot[w]);
       V S = 0, suffix = 0, best = 0;
-      for (int k = R - 1; k >= 0; --k) {
-        const DagEnt<V> e = ent[*perm.at(k)];
+      auto step = [&](int r, int k) {
+        const DagEnt<V> e = ent[r];
         S += s_bins[k * NT] + e.wr;
+        s_bins[k * NT] = V(0);
         best = max(best, ctot - suffix + S);
         suffix += e.d;
+      };
+      int k = R - 1;
+      if constexpr (sizeof(T) == 1) {
+        for (; k >= 0 && (k & 3) != 3; --k) step(*perm.at(k), k);
+        for (; k >= 3; k -= 4) {  // four positions per word of the gate-order column
+          const uint32_t wd = perm.base[(k >> 2) * NT];
+          step(wd >> 24, k);
+          step((wd >> 16) & 0xFF, k - 1);
+          step((wd >> 8) & 0xFF, k - 2);
+          step(wd & 0xFF, k - 3);
+        }
+      } else {
+        for (; k >= 0; --k) step(*perm.at(k), k);
       }
       best = max(best, S + s_w0[w]);
       const int64_t tcpu = static_cast<int64_t>(best);
@@ -779,9 +831,9 @@ struct SweepPlan {
   size_t smem = 0, smem_orders = 0;
   int blocks = 0;
   uint64_t noise_thr = 0;
-  // general-DAG plans (dag_sweep_kernel): join classes, slots, program words,
+  // general-DAG plans (dag_sweep_kernel): program records, slots,
   // shared-memory item width (1: R <= 255, else 2)
-  int dag = 0, J = 0, Ls = 0, P = 0, tb = 1;
+  int dag = 0, J = 0, Ls = 0, tb = 1;
   int blocks_orders = 0;
 };
 
@@ -894,19 +946,22 @@ extern "C" SweepPlan* csk_sweep_plan(int32_t W, int32_t R, int32_t nc, const int
   return p;
 }
 
-extern "C" SweepPlan* csk_sweep_plan_dag(int32_t W, int32_t R, const int64_t* d, const int64_t* wr, int32_t J,
-                                         const int64_t* wj, const int64_t* w0, int32_t Ls, const uint16_t* prog,
-                                         int32_t P, const int64_t* send_total, int cluster, int64_t U, int64_t L,
+extern "C" SweepPlan* csk_sweep_plan_dag(int32_t W, int32_t R, const int64_t* d, const int64_t* wr, int32_t nrec,
+                                         const int32_t* recs, const int64_t* wj, const int64_t* w0, int32_t Ls,
+                                         const int64_t* send_total, int cluster, int64_t U, int64_t L,
                                          uint64_t noise_thr, char* err) {
   if (ensure_device(err)) return nullptr;
+  if (nrec % 4) {
+    std::snprintf(err, 256, "DAG program records must come in groups of four");
+    return nullptr;
+  }
   auto* p = new SweepPlan();
   p->dag = 1;
   p->noise_thr = noise_thr;
   p->W = W;
   p->R = R;
-  p->J = J;
+  p->J = nrec;
   p->Ls = Ls;
-  p->P = P;
   p->cluster = cluster;
   p->U = U;
   p->L = L;
@@ -918,7 +973,7 @@ extern "C" SweepPlan* csk_sweep_plan_dag(int32_t W, int32_t R, const int64_t* d,
   std::vector<uint64_t> lim(R + 2), mag(R + 2);
   for (int n = 0; n <= R + 1; ++n) bounded_consts(static_cast<uint64_t>(n), &lim[n], &mag[n]);
   const size_t vb = p->narrow ? 4 : 8;
-  p->blob_bytes = dag_table_bytes(R, W, J, P, vb);
+  p->blob_bytes = dag_table_bytes(R, W, nrec, vb);
   std::vector<unsigned char> img(p->blob_bytes, 0);
   unsigned char* q = img.data();
   auto put = [&](int64_t v) {  // one value in the fold's width
@@ -934,13 +989,35 @@ extern "C" SweepPlan* csk_sweep_plan_dag(int32_t W, int32_t R, const int64_t* d,
   q += 8ull * (R + 2);
   std::memcpy(q, mag.data(), 8ull * (R + 2));
   q += 8ull * (R + 2);
+  const int discard = R + Ls;  // value index of the discard slot
+  for (int r = 0; r < nrec; ++r) {
+    const bool pad = recs[4 * r + 3] == -3;
+    for (int f = 0; f < 4; ++f) {
+      const int v = recs[4 * r + f];
+      uint32_t off;
+      if (v == -2 && f == 0) {
+        off = kDagAccFlag;  // forwarded: the previous record's result
+      } else if (pad) {
+        off = f == 3 ? dag_item_off(discard, p->tb) : 0;
+      } else if (f == 3) {
+        off = dag_item_off(v < 0 ? discard : v, p->tb) | kDagRealFlag;
+      } else if (v >= 0 && v < discard) {
+        off = dag_item_off(v, p->tb);
+      } else {
+        std::snprintf(err, 256, "DAG program value index out of range");
+        delete p;
+        return nullptr;
+      }
+      std::memcpy(q, &off, 4);
+      q += 4;
+    }
+  }
   for (int k = 0; k < W * R; ++k) {
     put(d[k]);
     put(wr[k]);
   }
-  for (int k = 0; k < W * J; ++k) put(wj[k]);
+  for (int k = 0; k < W * nrec; ++k) put(wj[k]);
   for (int w = 0; w < W; ++w) put(w0[w]);
-  std::memcpy(q, prog, 2ull * P);
   auto up = [&](void** dst, const void* src, size_t bytes) {
     if (cudaMalloc(dst, bytes ? bytes : 8) != cudaSuccess) return false;
     return bytes == 0 || cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice) == cudaSuccess;
@@ -952,8 +1029,8 @@ extern "C" SweepPlan* csk_sweep_plan_dag(int32_t W, int32_t R, const int64_t* d,
     return nullptr;
   }
   const int nhist = (U != L ? 1 : 0) + (cluster ? 1 : 0);
-  p->smem = dag_smem(R, W, J, Ls, P, nhist, p->tb, vb);
-  p->smem_orders = dag_smem(R, W, J, Ls, P, 0, p->tb, vb);
+  p->smem = dag_smem(R, W, nrec, Ls, nhist, p->tb, vb);
+  p->smem_orders = dag_smem(R, W, nrec, Ls, 0, p->tb, vb);
   int dev = 0, sms = 148, occ = 0, occ_o = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -1037,7 +1114,7 @@ extern "C" int csk_sweep_run(SweepPlan* p, uint64_t seed_lo, int64_t count, uint
     a.mbar_off = static_cast<uint32_t>(p->smem - 16);
     const int64_t need = (count + kDagThreads - 1) / kDagThreads;
     const int blocks = static_cast<int>(std::min<int64_t>(p->blocks, need));
-    dag_fn<0>(p, p->noise_thr != 0)<<<blocks, kDagThreads, p->smem, st>>>(a, DagArgs{p->J, p->Ls, p->P, 0, nullptr});
+    dag_fn<0>(p, p->noise_thr != 0)<<<blocks, kDagThreads, p->smem, st>>>(a, DagArgs{p->J, p->Ls, 0, nullptr});
     LAUNCHED();
     CK(cudaGetLastError());
     return 0;
@@ -1075,7 +1152,7 @@ extern "C" int csk_sweep_orders(SweepPlan* p, const int32_t* d_orders, int64_t n
     a.mbar_off = static_cast<uint32_t>(p->smem_orders - 16);
     a.cluster = 0;
     const int blocks = static_cast<int>(std::min<int64_t>(p->blocks_orders, (n + kDagThreads - 1) / kDagThreads));
-    dag_fn<1>(p, false)<<<blocks, kDagThreads, p->smem_orders, st>>>(a, DagArgs{p->J, p->Ls, p->P, 0, nullptr});
+    dag_fn<1>(p, false)<<<blocks, kDagThreads, p->smem_orders, st>>>(a, DagArgs{p->J, p->Ls, 0, nullptr});
   } else {
     const int blocks = static_cast<int>(std::min<int64_t>(p->blocks, (n + kSweepThreads - 1) / kSweepThreads));
     chain_sweep_kernel<uint8_t, true, int64_t><<<blocks, kSweepThreads, p->smem_orders, st>>>(a);
@@ -1116,7 +1193,7 @@ extern "C" int csk_sweep_lex(SweepPlan* p, int64_t first, int64_t count, int64_t
     a.i64 = nullptr;
     a.f64 = nullptr;
     const int blocks = static_cast<int>(std::min<int64_t>(p->blocks_orders, (count + kDagThreads - 1) / kDagThreads));
-    dag_fn<2>(p, false)<<<blocks, kDagThreads, p->smem_orders>>>(a, DagArgs{p->J, p->Ls, p->P, first,
+    dag_fn<2>(p, false)<<<blocks, kDagThreads, p->smem_orders>>>(a, DagArgs{p->J, p->Ls, first,
                                                                    d_fact.as<const unsigned long long>()});
     LAUNCHED();
     CK(cudaGetLastError());

@@ -810,7 +810,7 @@ int cs_sweep_plan_info(const cs_sweep_plan* p, char** out_json) {
     if (c.dag) {
       j["joins"] = c.joins;
       j["slots"] = c.slots;
-      j["program_words"] = c.prog_words;
+      j["program_records"] = c.prog_words;
     }
     j["workers"] = c.cluster ? static_cast<int64_t>(c.workers.size()) : 1;
     int64_t erecv = 0;

@@ -14,6 +14,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <array>
 #include <set>
 
 #include "../device/csk.h"
@@ -41,11 +42,19 @@ struct ChainTables {
 // per join class (recv-ancestor set with >= 2 recvs), in increasing set
 // size, its latest recv position = max over generators, each a recv column
 // (value index c < R: that recv's position) or an earlier join held in a
-// live slot (value index R + slot). Words: header n | 0x4000 (result kept in
-// a slot), n generator indices, [slot index]. Duration-independent.
+// live slot (value index R + slot). Records of three generators and one
+// output (value index; -1 = discard), a join with more generators chained
+// through temporary slots. Records come in groups of four that never read a
+// slot written inside the same group (the kernel loads a group's generators
+// before storing its outputs); groups are padded with no-op records.
+// Duration-independent: per oracle, record r weighs rec_join[r]'s class
+// (-1: no weight).
+constexpr int32_t kDagAcc = -2;  // generator: the previous record's result (register)
+constexpr int32_t kDagPad = -3;  // padding record (no effect)
 struct DagProgram {
-  int32_t J = 0, L = 0;            // join classes, live slots
-  std::vector<uint16_t> prog;
+  int32_t J = 0, L = 0;  // join classes, live slots
+  std::vector<std::array<int32_t, 4>> recs;
+  std::vector<int32_t> rec_join;    // join index per record, -1 for temporaries and padding
   std::vector<int32_t> join_class;  // class id of every join, program order
   std::vector<int32_t> single;      // per class: recv column when its set is {recv}, else -1
   std::vector<int32_t> empty;       // classes with no recv ancestor
@@ -136,58 +145,170 @@ bool dag_program(const Graph& g, const std::vector<uint64_t>& bits, int32_t W, c
       joins.push_back(j);
     }
   }
-  // last use of every join as a generator (in program order)
-  std::vector<int32_t> last(nc, -1);
-  for (int32_t k = 0; k < static_cast<int32_t>(joins.size()); ++k)
-    for (int32_t x : gens[joins[k]]) {
-      if (x < 0) continue;
-      if (jpos[x] < 0) {
-        // a generator class with a single-recv set stands for that recv
-        continue;
-      }
-      last[x] = k;
-    }
-  std::vector<int32_t> slot(nc, -1), free_slots;
-  int32_t nslots = 0;
-  out.prog.clear();
-  for (int32_t k = 0; k < static_cast<int32_t>(joins.size()); ++k) {
+  // 1. records over virtual values (recv column c < R; value v >= R: output
+  //    v - R, joins first, then temporaries for joins of > 3 generators)
+  struct VRec {
+    std::array<int32_t, 3> in;
+    int32_t out;   // virtual value id
+    int32_t join;  // weighted join, or -1
+  };
+  std::vector<VRec> vr;
+  const int32_t J = static_cast<int32_t>(joins.size());
+  int32_t nvals = J;
+  for (int32_t k = 0; k < J; ++k) {
     const int32_t j = joins[k];
-    std::vector<uint16_t> idx;
+    std::vector<int32_t> idx;
     for (int32_t x : gens[j]) {
-      int32_t v;
       if (x < 0) {
-        v = -(x + 1);
+        idx.push_back(-(x + 1));
       } else if (out.single[x] >= 0) {
-        v = out.single[x];
+        idx.push_back(out.single[x]);
       } else if (jpos[x] >= 0) {
-        if (slot[x] < 0) return why = "internal: generator used before its definition", false;
-        v = R + slot[x];
-      } else {
-        continue;  // empty-set generator: position -inf, no effect on the max
-      }
-      idx.push_back(static_cast<uint16_t>(v));
+        if (jpos[x] >= k) return why = "internal: generator used before its definition", false;
+        idx.push_back(R + jpos[x]);
+      }  // else an empty-set generator: position -inf, no effect on the max
     }
     std::sort(idx.begin(), idx.end());
     idx.erase(std::unique(idx.begin(), idx.end()), idx.end());
     if (idx.empty()) return why = "internal: join without recv generators", false;
-    for (int32_t x : gens[j])  // release slots whose last use is this join
-      if (x >= 0 && jpos[x] >= 0 && last[x] == k) free_slots.push_back(slot[x]);
-    const bool keep = last[j] > k;
-    uint16_t h = static_cast<uint16_t>(idx.size());
-    if (idx.size() >= 0x4000) return why = "join with too many generators", false;
-    if (keep) {
-      h |= 0x4000;
-      if (free_slots.empty()) {
-        slot[j] = nslots++;
-      } else {
-        slot[j] = free_slots.back();
-        free_slots.pop_back();
+    while (idx.size() > 3) {  // max of three into a temporary
+      vr.push_back({{idx[0], idx[1], idx[2]}, nvals, -1});
+      idx.erase(idx.begin(), idx.begin() + 3);
+      idx.push_back(R + nvals++);
+    }
+    while (idx.size() < 3) idx.push_back(idx.back());
+    vr.push_back({{idx[0], idx[1], idx[2]}, k, k});
+  }
+  // 2. list schedule into groups of four: a record's first generator may be
+  //    the previous record's result, forwarded in a register (ACC); every
+  //    other value it reads must come from an earlier group. Longest
+  //    remaining dependency chain first; a chain continues through ACC.
+  const int32_t N = static_cast<int32_t>(vr.size());
+  std::vector<int32_t> producer(nvals, -1);
+  for (int32_t r = 0; r < N; ++r) producer[vr[r].out] = r;
+  std::vector<std::vector<int32_t>> users(N);
+  for (int32_t r = 0; r < N; ++r)
+    for (int32_t x : std::set<int32_t>(vr[r].in.begin(), vr[r].in.end()))
+      if (x >= R) users[producer[x - R]].push_back(r);
+  std::vector<int32_t> height(N, 1);
+  for (int32_t r = N - 1; r >= 0; --r)
+    for (int32_t u : users[r]) height[r] = std::max(height[r], height[u] + 1);
+  std::vector<int32_t> group_of(N, -1), order;
+  std::vector<char> acc(N, 0);
+  int32_t placed = 0, gq = 0;
+  while (placed < N) {
+    int32_t prev = -1;  // record at the previous position of this group
+    for (int32_t i = 0; i < 4; ++i) {
+      int32_t best = -1;
+      bool best_acc = false;
+      for (int32_t r = 0; r < N; ++r) {
+        if (group_of[r] >= 0) continue;
+        bool ok = true, via_acc = false;
+        for (int32_t x : vr[r].in) {
+          if (x < R) continue;
+          const int32_t pr = producer[x - R];
+          if (group_of[pr] >= 0 && group_of[pr] < gq) continue;
+          if (pr == prev && prev >= 0) {
+            via_acc = true;
+            continue;
+          }
+          ok = false;
+          break;
+        }
+        if (!ok) continue;
+        if (best < 0 || height[r] > height[best] || (height[r] == height[best] && via_acc && !best_acc)) {
+          best = r;
+          best_acc = via_acc;
+        }
+      }
+      if (best < 0) break;
+      group_of[best] = gq;
+      order.push_back(best);
+      acc[best] = best_acc ? 1 : 0;
+      prev = best;
+      ++placed;
+    }
+    while (order.size() % 4) order.push_back(-1);
+    ++gq;
+  }
+  // the forwarded generator first; its other occurrences become fillers
+  for (size_t i = 1; i < order.size(); ++i) {
+    const int32_t r = order[i];
+    if (r < 0 || !acc[r]) continue;
+    const int32_t pv = R + vr[order[i - 1]].out;
+    auto& in = vr[r].in;
+    for (int q = 0; q < 3; ++q)
+      if (in[q] == pv) {
+        std::swap(in[0], in[q]);
+        break;
+      }
+    for (int u = 1; u < 3; ++u)
+      if (in[u] == pv) in[u] = -1;
+    if (in[1] < 0) std::swap(in[1], in[2]);
+    if (in[1] < 0) return why = "internal: join with one generator", false;
+    if (in[2] < 0) in[2] = in[1];
+  }
+  const int32_t ngroups = static_cast<int32_t>(order.size() / 4);
+  // 3. slots by linear scan over groups: a value lives from its group to
+  //    the group of its last non-forwarded reader (a group reads before it
+  //    writes, so a slot freed by a group's reads can take that group's
+  //    outputs)
+  std::vector<int32_t> last_group(nvals, -1);
+  for (int32_t r = 0; r < N; ++r)
+    for (int q = acc[r] ? 1 : 0; q < 3; ++q)
+      if (vr[r].in[q] >= R) last_group[vr[r].in[q] - R] = std::max(last_group[vr[r].in[q] - R], group_of[r]);
+  std::vector<int32_t> slot(nvals, -1), free_slots;
+  int32_t nslots = 0;
+  out.recs.clear();
+  out.rec_join.clear();
+  for (int32_t gq = 0; gq < ngroups; ++gq) {
+    std::array<std::array<int32_t, 4>, 4> recs{};
+    for (int32_t i = 0; i < 4; ++i) {
+      const int32_t r = order[4 * gq + i];
+      if (r < 0) {
+        recs[i] = {kDagPad, kDagPad, kDagPad, kDagPad};
+        continue;
+      }
+      for (int q = 0; q < 3; ++q) {
+        const int32_t x = vr[r].in[q];
+        if (q == 0 && acc[r]) {
+          recs[i][q] = kDagAcc;
+        } else {
+          recs[i][q] = x < R ? x : R + slot[x - R];
+        }
+      }
+      recs[i][3] = -1;
+    }
+    for (int32_t i = 0; i < 4; ++i) {  // release values last read here
+      const int32_t r = order[4 * gq + i];
+      if (r < 0) continue;
+      for (int q = acc[r] ? 1 : 0; q < 3; ++q) {
+        const int32_t x = vr[r].in[q];
+        if (x >= R && last_group[x - R] == gq && slot[x - R] >= 0) {
+          free_slots.push_back(slot[x - R]);
+          slot[x - R] = -1 - slot[x - R];
+        }
       }
     }
-    out.prog.push_back(h);
-    out.prog.insert(out.prog.end(), idx.begin(), idx.end());
-    if (keep) out.prog.push_back(static_cast<uint16_t>(R + slot[j]));
-    if (R + nslots >= 0xFFFF) return why = "program too large", false;
+    for (int32_t i = 0; i < 4; ++i) {  // outputs read later from a slot
+      const int32_t r = order[4 * gq + i];
+      if (r < 0 || last_group[vr[r].out] < 0) continue;
+      int32_t t;
+      if (free_slots.empty()) {
+        t = nslots++;
+      } else {
+        t = free_slots.back();
+        free_slots.pop_back();
+      }
+      slot[vr[r].out] = t;
+      recs[i][3] = R + t;
+    }
+    for (int32_t i = 0; i < 4; ++i) {
+      out.recs.push_back(recs[i]);
+      const int32_t r = order[4 * gq + i];
+      out.rec_join.push_back(r < 0 ? -1 : vr[r].join);
+    }
+    if (R + nslots >= (1 << 15)) return why = "program too large", false;
   }
   out.J = static_cast<int32_t>(joins.size());
   out.L = nslots;
@@ -316,8 +437,9 @@ bool chain_tables(const ChainShape& cs, const Graph& g, const std::vector<int64_
     t.pwsuf.assign(cs.nc + 1, 0);
     for (int32_t j = cs.nc - 1; j >= 0; --j) t.pwsuf[j] = t.pwsuf[j + 1] + weight[j];
   } else {
-    t.wj.resize(cs.dag.J);
-    for (int32_t k = 0; k < cs.dag.J; ++k) t.wj[k] = weight[cs.dag.join_class[k]];
+    t.wj.resize(cs.dag.recs.size());
+    for (size_t r = 0; r < cs.dag.recs.size(); ++r)
+      t.wj[r] = cs.dag.rec_join[r] < 0 ? 0 : weight[cs.dag.join_class[cs.dag.rec_join[r]]];
     t.wr.assign(cs.R, 0);
     for (int32_t j = 0; j < cs.nc; ++j)
       if (cs.dag.single[j] >= 0) t.wr[cs.dag.single[j]] += weight[j];
@@ -427,7 +549,7 @@ std::unique_ptr<SweepCtx> make_sweep(std::shared_ptr<const Graph> g, const TimeO
       if (!(ok = chain_tables(*shape, *part, pd, tabs.back(), s->why))) break;
       if (!shape0) shape0 = shape;
       if (tabs.back().R != tabs[0].R || tabs.back().nc != tabs[0].nc || shape->nested != shape0->nested ||
-          (!shape->nested && shape->dag.prog != shape0->dag.prog)) {
+          (!shape->nested && (shape->dag.recs != shape0->dag.recs || shape->dag.rec_join != shape0->dag.rec_join))) {
         ok = false;
         s->why = "workers differ in shape";
         break;
@@ -438,7 +560,7 @@ std::unique_ptr<SweepCtx> make_sweep(std::shared_ptr<const Graph> g, const TimeO
   if (std::getenv("TICTAC_SWEEP_TRACE") && shape0)
     std::fprintf(stderr, "[make_sweep] ok=%d nested=%d R=%d classes=%d joins=%d slots=%d words=%zu (%s)\n", ok ? 1 : 0,
                  shape0->nested ? 1 : 0, shape0->R, shape0->nc, shape0->dag.J, shape0->dag.L,
-                 shape0->dag.prog.size(), s->why.c_str());
+                 shape0->dag.recs.size(), s->why.c_str());
   if (ok) {
     const int32_t W = static_cast<int32_t>(tabs.size()), R = tabs[0].R, nc = tabs[0].nc;
     std::vector<int64_t> d, pw, send;
@@ -466,13 +588,15 @@ std::unique_ptr<SweepCtx> make_sweep(std::shared_ptr<const Graph> g, const TimeO
         wj.insert(wj.end(), t.wj.begin(), t.wj.end());
         w0.push_back(t.w0);
       }
-      s->plan = csk_sweep_plan_dag(W, R, d.data(), wr.data(), dp.J, wj.data(), w0.data(), dp.L, dp.prog.data(),
-                                   static_cast<int32_t>(dp.prog.size()), send.data(), s->cluster ? 1 : 0, s->U,
-                                   s->L, noise_thr, err);
+      std::vector<int32_t> recs;
+      for (const auto& r : dp.recs) recs.insert(recs.end(), r.begin(), r.end());
+      const int32_t nrec = static_cast<int32_t>(dp.recs.size());
+      s->plan = csk_sweep_plan_dag(W, R, d.data(), wr.data(), nrec, recs.data(), wj.data(), w0.data(), dp.L,
+                                   send.data(), s->cluster ? 1 : 0, s->U, s->L, noise_thr, err);
       s->dag = true;
       s->joins = dp.J;
       s->slots = dp.L;
-      s->prog_words = static_cast<int32_t>(dp.prog.size());
+      s->prog_words = nrec;
     }
     if (!s->plan) fail(kInternal, err);
     s->fast = true;
