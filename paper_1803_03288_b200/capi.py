@@ -88,6 +88,8 @@ _SIGS = {
     "cs_sweep_random": [_vp, _vp, C.c_uint64, C.c_int64, C.POINTER(SimPolicy), _vp, _vp,
                         C.POINTER(SweepStats)],
     "cs_simulate_orders": [_vp, _vp, _vp, C.c_int64, C.POINTER(SimPolicy), _vp, _vp],
+    "cs_sweep_random_multi": [_vp, _vp, C.c_uint64, C.c_int64, C.POINTER(SimPolicy), C.c_int, _vp, _vp,
+                              C.POINTER(SweepStats)],
     "cs_sweep_plan_create": [_vp, _vp, C.POINTER(SimPolicy), _pp],
     "cs_sweep_plan_info": [_vp, _pp],
     "cs_sweep_plan_reset": [_vp, _vp, _vp, _vp],
@@ -99,7 +101,7 @@ _SIGS = {
 _FREE = ["cs_graph_free", "cs_oracle_free", "cs_schedule_free", "cs_report_free",
          "cs_string_free", "cs_sweep_plan_free"]
 REFERENCE_SYMBOLS = [k for k in _SIGS if k not in (
-    "cs_sweep_random", "cs_simulate_orders", "cs_sweep_plan_create", "cs_sweep_plan_info",
+    "cs_sweep_random", "cs_sweep_random_multi", "cs_simulate_orders", "cs_sweep_plan_create", "cs_sweep_plan_info",
     "cs_sweep_plan_reset", "cs_sweep_plan_run", "cs_sweep_stats_finish",
     "cs_graph_generate_model", "cs_tac_traffic")] + [f for f in _FREE if f != "cs_sweep_plan_free"] + [
     "cs_last_error", "cs_version"]
@@ -316,6 +318,23 @@ class Graph(_Handle):
         st = SweepStats()
         self.lib.call("cs_sweep_random", self.h, oracle.h, seed_lo, count,
                       C.byref(pol) if pol is not None else None,
+                      ms.ctypes.data if ms is not None else None,
+                      wms.ctypes.data if wms is not None else None, C.byref(st))
+        out = st.to_dict()
+        if ms is not None:
+            out["makespans"] = ms[:count]
+        if wms is not None:
+            out["worker_makespans"] = wms[:count * nw].reshape(count, nw)
+        return out
+
+    def sweep_random_multi(self, oracle: "Oracle", seed_lo: int, count: int, n_devices: int,
+                           pol: SimPolicy | None = None, makespans: bool = False, worker_makespans: bool = False):
+        ms = np.zeros(max(count, 1), dtype=np.int64) if makespans else None
+        nw = len(self.worker_devices()) if (worker_makespans and self.is_cluster()) else 0
+        wms = np.zeros(max(count * nw, 1), dtype=np.int64) if nw else None
+        st = SweepStats()
+        self.lib.call("cs_sweep_random_multi", self.h, oracle.h, seed_lo, count,
+                      C.byref(pol) if pol is not None else None, n_devices,
                       ms.ctypes.data if ms is not None else None,
                       wms.ctypes.data if wms is not None else None, C.byref(st))
         out = st.to_dict()

@@ -5,7 +5,7 @@
 // cmd_sweep (sched_main.cpp:452-502) becomes one cs_sweep_random call per
 // contiguous run of seeds when the schedule is random.
 //
-//   tictac_sched sweep --graph g.json --algo random --seeds 1..100000 --out sweep.csv
+//   tictac_sched sweep --graph g.json --algo random --seeds 1..100000 --out sweep.csv [--gpus N]
 //   tictac_sched bruteforce --graph g.json --max-recvs 12 [--out best.json]
 //
 // Flags as `--name value` or `--name=value`; `--config file.json` supplies
@@ -170,9 +170,11 @@ const Flag kFlags[] = {
     {"enforce", "enforce", Type::Str, "counter"}, {"noise", "noise", Type::Float, "0"},
     {"choice-seed", "choice-seed", Type::Int, nullptr}, {"seeds", "seeds", Type::Str, ""},
     {"out", "out", Type::Str, ""},              {"max-recvs", "max-recvs", Type::Int, "8"},
+    {"gpus", "gpus", Type::Int, "1"},
 };
 bool sweep_only(const std::string& f) {
-  return f == "seeds" || f == "algo" || f == "mode" || f == "seed" || f == "schedule" || f == "choice-seed";
+  return f == "seeds" || f == "algo" || f == "mode" || f == "seed" || f == "schedule" || f == "choice-seed" ||
+         f == "gpus";
 }
 
 struct Options {
@@ -343,7 +345,13 @@ int cmd_sweep(const Options& o) {
       const int64_t n = static_cast<int64_t>(b - a);
       std::vector<int64_t> ms(static_cast<size_t>(n)), wms(static_cast<size_t>(n * std::max<int64_t>(workers, 1)));
       cs_sweep_stats st{};
-      check(cs_sweep_random(g.p, oracle.p, seeds[a], n, &pol, ms.data(), cluster ? wms.data() : nullptr, &st));
+      const int gpus = static_cast<int>(o.i("gpus"));
+      if (gpus > 1) setenv("NCCL_DEBUG", "WARN", 0);  // keep NCCL's banner off the summary stream
+      if (gpus > 1)  // seeds sharded over this process's GPUs, one NCCL reduction
+        check(cs_sweep_random_multi(g.p, oracle.p, seeds[a], n, &pol, gpus, ms.data(),
+                                    cluster ? wms.data() : nullptr, &st));
+      else
+        check(cs_sweep_random(g.p, oracle.p, seeds[a], n, &pol, ms.data(), cluster ? wms.data() : nullptr, &st));
       for (int64_t k = 0; k < n; ++k) {
         if (cluster) {
           const std::vector<int64_t> wm(wms.begin() + k * workers, wms.begin() + (k + 1) * workers);

@@ -10,8 +10,11 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <string>
+#include <thread>
+#include <vector>
 
 #include "../../../include/commsched.h"
 #include "../device/csk.h"
@@ -26,13 +29,16 @@ std::atomic<uint64_t> g_oracle_ids{1};
 
 struct cs_graph {
   std::shared_ptr<Graph> g;
-  // Last sweep plan built for (oracle id, policy): graph and oracle handles
-  // are immutable, so repeated sweeps reuse the device tables.
+  // Last sweep plan built per CUDA device for (oracle id, policy): graph and
+  // oracle handles are immutable, so repeated sweeps reuse the device tables.
+  struct Cached {
+    std::shared_ptr<SweepCtx> ctx;
+    uint64_t oracle = 0;
+    bool gated = true;
+    double noise = 0.0;
+  };
   std::mutex mu;
-  std::shared_ptr<SweepCtx> sweep;
-  uint64_t sweep_oracle = 0;
-  bool sweep_gated = true;
-  double sweep_noise = 0.0;
+  std::map<int, Cached> sweep;
 };
 struct cs_oracle {
   TimeOracle o;
@@ -107,14 +113,13 @@ char* dup(const std::string& s) {
 // handle: handles are immutable, so repeated sweeps/simulations reuse it.
 std::shared_ptr<SweepCtx> cached_sweep(const cs_graph* g, const cs_oracle* o, const Policy& p) {
   auto* gm = const_cast<cs_graph*>(g);
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) dev = 0;
   std::lock_guard<std::mutex> lock(gm->mu);
-  if (gm->sweep && gm->sweep_oracle == o->id && gm->sweep_gated == p.gated && gm->sweep_noise == p.noise)
-    return gm->sweep;
+  cs_graph::Cached& c = gm->sweep[dev];
+  if (c.ctx && c.oracle == o->id && c.gated == p.gated && c.noise == p.noise) return c.ctx;
   std::shared_ptr<SweepCtx> ctx = make_sweep(g->g, o->o, p);
-  gm->sweep = ctx;
-  gm->sweep_oracle = o->id;
-  gm->sweep_gated = p.gated;
-  gm->sweep_noise = p.noise;
+  c = {ctx, o->id, p.gated, p.noise};
   return ctx;
 }
 
@@ -131,57 +136,6 @@ struct DevPtr {
   template <typename T>
   T* as() const {
     return static_cast<T*>(p);
-  }
-};
-
-// Page-locked staging buffers for pipelined read-backs, kept for the life of
-// the process (pinning is expensive per call); leased one call at a time.
-class PinnedPool {
- public:
-  struct Lease {
-    PinnedPool* pool = nullptr;
-    char* p = nullptr;
-    size_t bytes = 0;
-    Lease() = default;
-    Lease(const Lease&) = delete;
-    Lease& operator=(const Lease&) = delete;
-    ~Lease() {
-      if (p) pool->put(p, bytes);
-    }
-  };
-  static PinnedPool& get() {
-    static PinnedPool* pool = new PinnedPool();  // never destroyed: the OS reclaims at exit
-    return *pool;
-  }
-  bool lease(size_t bytes, Lease& out) {
-    {
-      std::lock_guard<std::mutex> lock(mu_);
-      for (size_t i = 0; i < free_.size(); ++i)
-        if (free_[i].second >= bytes) {
-          out.pool = this;
-          out.p = free_[i].first;
-          out.bytes = free_[i].second;
-          free_.erase(free_.begin() + static_cast<std::ptrdiff_t>(i));
-          return true;
-        }
-    }
-    void* h = nullptr;
-    if (cudaMallocHost(&h, bytes) != cudaSuccess) {
-      cudaGetLastError();
-      return false;
-    }
-    out.pool = this;
-    out.p = static_cast<char*>(h);
-    out.bytes = bytes;
-    return true;
-  }
-
- private:
-  std::mutex mu_;
-  std::vector<std::pair<char*, size_t>> free_;
-  void put(char* p, size_t bytes) {
-    std::lock_guard<std::mutex> lock(mu_);
-    free_.emplace_back(p, bytes);
   }
 };
 
@@ -603,124 +557,75 @@ int cs_sweep_random(const cs_graph* g, const cs_oracle* o, uint64_t seed_lo, int
       }
       return;
     }
-    // fast path: device buffers, one launch per 2^26 seeds
-    char err[256] = {0};
-    auto cudacheck = [&](cudaError_t e) {
-      if (e != cudaSuccess) fail(kInternal, std::string("CUDA error: ") + cudaGetErrorString(e));
-    };
-    DevPtr b_st, b_ms, b_wms;  // statistics: i64 then f64 words, read back with one copy
-    const int64_t W = ctx->cluster ? static_cast<int64_t>(ctx->workers.size()) : 1;
-    const int64_t chunk = int64_t{1} << 26;
-    cudacheck(cudaMallocAsync(&b_st.p, 8 * (CS_DSTATS_I64 + CS_DSTATS_F64), 0));
-    const int64_t cap = std::min(count, chunk);
-    if (makespans_out) cudacheck(cudaMallocAsync(&b_ms.p, 8 * std::max<int64_t>(cap, 1), 0));
-    if (worker_makespans_out && ctx->cluster)
-      cudacheck(cudaMallocAsync(&b_wms.p, 8 * std::max<int64_t>(cap * W, 1), 0));
-    int64_t *d_i64 = b_st.as<int64_t>(), *d_ms = b_ms.as<int64_t>(), *d_wms = b_wms.as<int64_t>();
-    double* d_f64 = reinterpret_cast<double*>(d_i64 + CS_DSTATS_I64);
-    cs_sweep_stats total{};
-    bool first = true;
+    const cs_sweep_stats total = sweep_fast({ctx.get()}, seed_lo, count, makespans_out, worker_makespans_out,
+                                            nullptr);
+    if (stats_out) *stats_out = total;
+  });
+}
+
+int cs_sweep_random_multi(const cs_graph* g, const cs_oracle* o, uint64_t seed_lo, int64_t count,
+                          const cs_sim_policy* policy, int n_devices, int64_t* makespans_out,
+                          int64_t* worker_makespans_out, cs_sweep_stats* stats_out) {
+  return guarded([&] {
+    need(g, "graph");
+    need(o, "oracle");
+    if (count < 0) fail(kParameter, "count must be non-negative");
+    int avail = 0;
+    if (cudaGetDeviceCount(&avail) != cudaSuccess) avail = 0;
+    if (n_devices < 1 || n_devices > avail)
+      fail(kParameter, "n_devices must be within [1, " + std::to_string(avail) + "]");
+    const Policy p = policy_of(policy);
+    int caller = 0;
+    if (cudaGetDevice(&caller) != cudaSuccess) caller = 0;
+    // one plan per device, built on that device (cached on the graph handle)
+    std::vector<std::shared_ptr<SweepCtx>> ctx(n_devices);
+    std::vector<std::string> errors(n_devices);
     {
-      for (int64_t base = 0; base < count || (first && count == 0); base += chunk) {
-        const int64_t n = std::min(chunk, count - base);
-        if (csk_sweep_reset(ctx->plan, nullptr, d_i64, d_f64, err)) fail(kInternal, err);
-        const uint64_t lo = seed_lo + static_cast<uint64_t>(base);
-        // Per-seed outputs of a large chunk: launches of kSub seeds on one
-        // stream, each slice read back on a second stream through pinned
-        // staging while the next ones run, then copied to the caller's
-        // buffers — the transfer overlaps the kernels instead of following.
-        constexpr int64_t kSub = int64_t{1} << 19;
-        PinnedPool::Lease stage;
-        const size_t slice_bytes = 8 * static_cast<size_t>(kSub) * ((d_ms ? 1 : 0) + (d_wms ? W : 0));
-        const bool piped = (d_ms || d_wms) && n >= 4 * kSub && PinnedPool::get().lease(2 * slice_bytes, stage);
-        if (piped) {
-          cudaStream_t sa = nullptr, sb = nullptr;
-          cudaEvent_t ready = nullptr;
-          cudacheck(cudaStreamCreateWithFlags(&sa, cudaStreamNonBlocking));
-          cudacheck(cudaStreamCreateWithFlags(&sb, cudaStreamNonBlocking));
-          cudacheck(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
-          const int64_t K = (n + kSub - 1) / kSub;
-          std::vector<cudaEvent_t> ran(static_cast<size_t>(K)), copied(static_cast<size_t>(K));
-          for (int64_t k = 0; k < K; ++k) {
-            cudacheck(cudaEventCreateWithFlags(&ran[k], cudaEventDisableTiming));
-            cudacheck(cudaEventCreateWithFlags(&copied[k], cudaEventDisableTiming));
+      std::vector<std::thread> th;
+      for (int d = 0; d < n_devices; ++d)
+        th.emplace_back([&, d] {
+          try {
+            if (cudaSetDevice(d) != cudaSuccess) fail(kInternal, "cudaSetDevice failed");
+            ctx[d] = cached_sweep(g, o, p);
+          } catch (const std::exception& e) {
+            errors[d] = e.what();
           }
-          cudacheck(cudaEventRecord(ready, 0));  // buffers and the reset, issued on the legacy stream
-          cudacheck(cudaStreamWaitEvent(sa, ready, 0));
-          int rc = 0;
-          for (int64_t k = 0; k < K && !rc; ++k) {
-            const int64_t off = k * kSub, nk = std::min(kSub, n - off);
-            rc = csk_sweep_run(ctx->plan, lo + static_cast<uint64_t>(off), nk, lo, sa, d_ms ? d_ms + off : nullptr,
-                               d_wms ? d_wms + off * W : nullptr, d_i64, d_f64, err);
-            if (!rc) cudacheck(cudaEventRecord(ran[k], sa));
-          }
-          auto land = [&](int64_t k) {  // staging slot k % 2 -> the caller's buffers
-            cudacheck(cudaEventSynchronize(copied[k]));
-            const int64_t off = k * kSub, nk = std::min(kSub, n - off);
-            const char* src = stage.p + (k & 1) * slice_bytes;
-            if (d_ms) {
-              std::memcpy(makespans_out + base + off, src, 8 * nk);
-              src += 8 * kSub;
-            }
-            if (d_wms) std::memcpy(worker_makespans_out + (base + off) * W, src, 8 * nk * W);
-          };
-          for (int64_t k = 0; k < K && !rc; ++k) {
-            const int64_t off = k * kSub, nk = std::min(kSub, n - off);
-            char* dst = stage.p + (k & 1) * slice_bytes;
-            cudacheck(cudaStreamWaitEvent(sb, ran[k], 0));
-            if (d_ms) {
-              cudacheck(cudaMemcpyAsync(dst, d_ms + off, 8 * nk, cudaMemcpyDeviceToHost, sb));
-              dst += 8 * kSub;
-            }
-            if (d_wms) cudacheck(cudaMemcpyAsync(dst, d_wms + off * W, 8 * nk * W, cudaMemcpyDeviceToHost, sb));
-            cudacheck(cudaEventRecord(copied[k], sb));
-            if (k >= 1) land(k - 1);
-          }
-          if (!rc) land(K - 1);
-          cudaStreamSynchronize(sa);
-          cudaStreamSynchronize(sb);
-          for (int64_t k = 0; k < K; ++k) {
-            cudaEventDestroy(ran[k]);
-            cudaEventDestroy(copied[k]);
-          }
-          cudaEventDestroy(ready);
-          cudaStreamDestroy(sa);
-          cudaStreamDestroy(sb);
-          if (rc) fail(kInternal, err);
-        } else if (csk_sweep_run(ctx->plan, lo, n, lo, nullptr, d_ms, d_wms, d_i64, d_f64, err)) {
-          fail(kInternal, err);
-        }
-        std::vector<int64_t> i64(CS_DSTATS_I64);
-        std::vector<double> f64(CS_DSTATS_F64);
-        {
-          std::vector<char> st(8 * (CS_DSTATS_I64 + CS_DSTATS_F64));
-          cudacheck(cudaMemcpy(st.data(), d_i64, st.size(), cudaMemcpyDeviceToHost));
-          std::memcpy(i64.data(), st.data(), 8 * CS_DSTATS_I64);
-          std::memcpy(f64.data(), st.data() + 8 * CS_DSTATS_I64, 8 * CS_DSTATS_F64);
-        }
-        if (d_ms && !piped) cudacheck(cudaMemcpy(makespans_out + base, d_ms, 8 * n, cudaMemcpyDeviceToHost));
-        if (d_wms && !piped)
-          cudacheck(cudaMemcpy(worker_makespans_out + base * W, d_wms, 8 * n * W, cudaMemcpyDeviceToHost));
-        cs_sweep_stats part{};
-        finish_stats(*ctx, i64.data(), f64.data(), lo, &part);
-        if (first) {
-          total = part;
-        } else if (part.count > 0) {  // merge chunk statistics
-          if (part.min_us < total.min_us) total.min_us = part.min_us, total.argmin_seed = part.argmin_seed;
-          if (part.max_us > total.max_us) total.max_us = part.max_us, total.argmax_seed = part.argmax_seed;
-          total.count += part.count;
-          total.sum_us += part.sum_us;
-          total.sumsq_us += part.sumsq_us;
-          total.straggler_sum += part.straggler_sum;
-          for (int k = 0; k < CS_HIST_BINS; ++k) {
-            total.e_hist[k] += part.e_hist[k];
-            total.straggler_hist[k] += part.straggler_hist[k];
-          }
-        }
-        first = false;
-        if (count == 0) break;
-      }
+        });
+      for (auto& t : th) t.join();
     }
+    for (const auto& e : errors)
+      if (!e.empty()) fail(kInternal, e);
+    const int64_t W = ctx[0]->cluster ? static_cast<int64_t>(ctx[0]->workers.size()) : 1;
+    if (!ctx[0]->fast) {
+      // exact replica: contiguous shards, one host thread per device, host merge
+      std::vector<cs_sweep_stats> parts(n_devices);
+      const int64_t per = (count + n_devices - 1) / n_devices;
+      std::vector<std::thread> th;
+      for (int d = 0; d < n_devices; ++d)
+        th.emplace_back([&, d] {
+          try {
+            if (cudaSetDevice(d) != cudaSuccess) fail(kInternal, "cudaSetDevice failed");
+            const int64_t off = std::min<int64_t>(count, d * per), n = std::min<int64_t>(per, count - off);
+            sweep_exact(*ctx[d], seed_lo + static_cast<uint64_t>(off), n, makespans_out ? makespans_out + off : nullptr,
+                        worker_makespans_out && ctx[d]->cluster ? worker_makespans_out + off * W : nullptr, &parts[d]);
+          } catch (const std::exception& e) {
+            errors[d] = e.what();
+          }
+        });
+      for (auto& t : th) t.join();
+      for (const auto& e : errors)
+        if (!e.empty()) fail(kInternal, e);
+      cs_sweep_stats total{};
+      for (int d = 0; d < n_devices; ++d) merge_stats(total, parts[d], d == 0);
+      if (stats_out) *stats_out = total;
+      return;
+    }
+    std::vector<SweepCtx*> raw;
+    for (auto& c : ctx) raw.push_back(c.get());
+    std::unique_lock<std::mutex> hold;
+    const DeviceReducer* red = n_devices > 1 ? &nccl_reducer(n_devices, hold) : nullptr;
+    const cs_sweep_stats total = sweep_fast(raw, seed_lo, count, makespans_out, worker_makespans_out, red);
+    cudaSetDevice(caller);
     if (stats_out) *stats_out = total;
   });
 }

@@ -126,7 +126,7 @@ class Graph : public std::enable_shared_from_this<Graph> {
   std::vector<Resource> resources_;
   std::vector<int32_t> res_of_, recv_ops_;
   mutable std::mutex dev_mu_;
-  mutable DeviceGraph* dev_ = nullptr;
+  mutable std::map<int, DeviceGraph*> dev_;  // per CUDA device (multi-GPU sweeps)
   mutable std::mutex aux_mu_;
   mutable std::map<std::string, std::shared_ptr<const void>> aux_;
 };

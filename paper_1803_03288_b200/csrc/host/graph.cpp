@@ -4,6 +4,8 @@
 #include <set>
 
 #include "../device/csk.h"
+#include <cuda_runtime.h>
+
 #include "core.hpp"
 
 namespace tictac {
@@ -155,7 +157,7 @@ void Graph::index_and_validate() {
 }
 
 Graph::~Graph() {
-  if (dev_) csk_graph_free(dev_);
+  for (auto& [d, dg] : dev_) csk_graph_free(dg);
 }
 
 int32_t Graph::at(const std::string& id) const {
@@ -300,7 +302,10 @@ std::shared_ptr<Graph> Graph::partition(const std::string& device) const {  // s
 
 DeviceGraph* Graph::device() const {
   std::lock_guard<std::mutex> lock(dev_mu_);
-  if (!dev_) {
+  int cur = 0;
+  if (cudaGetDevice(&cur) != cudaSuccess) cur = 0;
+  DeviceGraph*& dg = dev_[cur];
+  if (!dg) {
     std::vector<int8_t> kind(n()), chan(resources_.size());
     for (int32_t i = 0; i < n(); ++i) kind[i] = static_cast<int8_t>(ops_[i].kind);
     for (size_t r = 0; r < resources_.size(); ++r) chan[r] = resources_[r].channel ? 1 : 0;
@@ -314,13 +319,16 @@ DeviceGraph* Graph::device() const {
       rdev[r] = static_cast<int32_t>(std::lower_bound(devs.begin(), devs.end(), resources_[r].device) -
                                      devs.begin());
     char err[256] = {0};
-    dev_ = csk_graph_upload(n(), pred_off_.data(), pred_idx_.data(), succ_off_.data(),
-                            succ_idx_.data(), kind.data(), res_of_.data(),
-                            static_cast<int32_t>(resources_.size()), chan.data(), rdev.data(),
-                            static_cast<int32_t>(devs.size()), err);
-    if (!dev_) fail(kInternal, err);
+    dg = csk_graph_upload(n(), pred_off_.data(), pred_idx_.data(), succ_off_.data(),
+                          succ_idx_.data(), kind.data(), res_of_.data(),
+                          static_cast<int32_t>(resources_.size()), chan.data(), rdev.data(),
+                          static_cast<int32_t>(devs.size()), err);
+    if (!dg) {
+      dev_.erase(cur);
+      fail(kInternal, err);
+    }
   }
-  return dev_;
+  return dg;
 }
 
 }  // namespace tictac

@@ -16,6 +16,7 @@
 #include <cstring>
 #include <array>
 #include <set>
+#include <thread>
 
 #include "../device/csk.h"
 #include "rng_host.hpp"
@@ -511,6 +512,7 @@ std::unique_ptr<SweepCtx> make_sweep(std::shared_ptr<const Graph> g, const TimeO
   // priority order without a draw, i.e. exactly the gated run; callers with
   // explicit priorities check distinctness (capi.cpp).
   s->noisy = p.gated && p.noise > 0.0;
+  if (cudaGetDevice(&s->device) != cudaSuccess) s->device = 0;
   bool ok = s->U < (int64_t{1} << 37);
   if (!ok) s->why = "makespan bound beyond the statistics key range";
   std::vector<ChainTables> tabs;
@@ -754,6 +756,273 @@ void sweep_exact(SweepCtx& s, uint64_t seed_lo, int64_t count, int64_t* makespan
     stats->iter_argmax_seed = it.ahi;
     stats->iter_sum_us = it_sum;
   }
+}
+
+// ---------------------------------------------------------------------------
+// Closed-form sweep execution shared by cs_sweep_random (one device) and
+// cs_sweep_random_multi (several devices, one NCCL reduction per round).
+
+namespace {
+
+void cudacheck(cudaError_t e) {
+  if (e != cudaSuccess) fail(kInternal, std::string("CUDA error: ") + cudaGetErrorString(e));
+}
+
+// Per-call device buffer from the stream-ordered pool (legacy stream).
+struct DevBuf {
+  void* p = nullptr;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() {
+    if (p) cudaFreeAsync(p, 0);
+  }
+  void alloc(size_t bytes) { cudacheck(cudaMallocAsync(&p, bytes ? bytes : 8, 0)); }
+  template <typename T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+// Page-locked staging buffers for pipelined read-backs, kept for the life of
+// the process (pinning is expensive per call) up to a cap; a caller that
+// finds none free and would exceed the cap reads back without the pipeline.
+class PinnedPool {
+ public:
+  static constexpr size_t kCapBytes = size_t{1} << 30;
+  struct Lease {
+    PinnedPool* pool = nullptr;
+    char* p = nullptr;
+    size_t bytes = 0;
+    Lease() = default;
+    Lease(const Lease&) = delete;
+    Lease& operator=(const Lease&) = delete;
+    ~Lease() {
+      if (p) pool->put(p, bytes);
+    }
+  };
+  static PinnedPool& get() {
+    static PinnedPool* pool = new PinnedPool();  // never destroyed: the OS reclaims at exit
+    return *pool;
+  }
+  bool lease(size_t bytes, Lease& out) {
+    std::lock_guard<std::mutex> lock(mu_);
+    for (size_t i = 0; i < free_.size(); ++i)
+      if (free_[i].second >= bytes) {
+        out.pool = this;
+        out.p = free_[i].first;
+        out.bytes = free_[i].second;
+        free_.erase(free_.begin() + static_cast<std::ptrdiff_t>(i));
+        return true;
+      }
+    if (total_ + bytes > kCapBytes) return false;
+    void* h = nullptr;
+    if (cudaMallocHost(&h, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    total_ += bytes;
+    out.pool = this;
+    out.p = static_cast<char*>(h);
+    out.bytes = bytes;
+    return true;
+  }
+
+ private:
+  std::mutex mu_;
+  size_t total_ = 0;
+  std::vector<std::pair<char*, size_t>> free_;
+  void put(char* p, size_t bytes) {
+    std::lock_guard<std::mutex> lock(mu_);
+    free_.emplace_back(p, bytes);
+  }
+};
+
+// Streams and events of one pipelined read-back. Declared after the staging
+// lease, so on every exit path (exceptions included) the destructor first
+// waits for both streams — nothing is still copying into the staging buffer
+// when it returns to the pool — then destroys them.
+struct PipeGuard {
+  cudaStream_t sa = nullptr, sb = nullptr;
+  cudaEvent_t ready = nullptr;
+  std::vector<cudaEvent_t> events;
+  PipeGuard() = default;
+  PipeGuard(const PipeGuard&) = delete;
+  PipeGuard& operator=(const PipeGuard&) = delete;
+  cudaEvent_t event() {
+    cudaEvent_t e = nullptr;
+    cudacheck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    events.push_back(e);
+    return e;
+  }
+  ~PipeGuard() {
+    if (sa) cudaStreamSynchronize(sa);
+    if (sb) cudaStreamSynchronize(sb);
+    for (cudaEvent_t e : events) cudaEventDestroy(e);
+    if (ready) cudaEventDestroy(ready);
+    if (sa) cudaStreamDestroy(sa);
+    if (sb) cudaStreamDestroy(sb);
+  }
+};
+
+// Runs seeds [lo, lo + n) (n <= 2^26) on the current device, accumulating
+// into the device statistics (keys relative to key_base) and copying
+// per-seed makespans to the host buffers when given (large spans: launches
+// of kSub seeds on one stream, each slice read back on a second stream
+// through pinned staging while the next ones run).
+void run_span(SweepCtx& ctx, uint64_t lo, int64_t n, uint64_t key_base, int64_t* d_ms, int64_t* d_wms,
+              int64_t* d_i64, double* d_f64, int64_t* ms_host, int64_t* wms_host) {
+  char err[256] = {0};
+  const int64_t W = ctx.cluster ? static_cast<int64_t>(ctx.workers.size()) : 1;
+  constexpr int64_t kSub = int64_t{1} << 19;
+  PinnedPool::Lease stage;
+  const size_t slice_bytes = 8 * static_cast<size_t>(kSub) * ((d_ms ? 1 : 0) + (d_wms ? W : 0));
+  const bool piped = (d_ms || d_wms) && n >= 4 * kSub && PinnedPool::get().lease(2 * slice_bytes, stage);
+  if (!piped) {
+    if (csk_sweep_run(ctx.plan, lo, n, key_base, nullptr, d_ms, d_wms, d_i64, d_f64, err)) fail(kInternal, err);
+    if (d_ms) cudacheck(cudaMemcpy(ms_host, d_ms, 8 * n, cudaMemcpyDeviceToHost));
+    if (d_wms) cudacheck(cudaMemcpy(wms_host, d_wms, 8 * n * W, cudaMemcpyDeviceToHost));
+    return;
+  }
+  PipeGuard pg;
+  cudacheck(cudaStreamCreateWithFlags(&pg.sa, cudaStreamNonBlocking));
+  cudacheck(cudaStreamCreateWithFlags(&pg.sb, cudaStreamNonBlocking));
+  cudacheck(cudaEventCreateWithFlags(&pg.ready, cudaEventDisableTiming));
+  const int64_t K = (n + kSub - 1) / kSub;
+  std::vector<cudaEvent_t> ran(static_cast<size_t>(K)), copied(static_cast<size_t>(K));
+  for (int64_t k = 0; k < K; ++k) {
+    ran[k] = pg.event();
+    copied[k] = pg.event();
+  }
+  cudacheck(cudaEventRecord(pg.ready, 0));  // buffers and the reset, issued on the legacy stream
+  cudacheck(cudaStreamWaitEvent(pg.sa, pg.ready, 0));
+  for (int64_t k = 0; k < K; ++k) {
+    const int64_t off = k * kSub, nk = std::min(kSub, n - off);
+    if (csk_sweep_run(ctx.plan, lo + static_cast<uint64_t>(off), nk, key_base, pg.sa, d_ms ? d_ms + off : nullptr,
+                      d_wms ? d_wms + off * W : nullptr, d_i64, d_f64, err))
+      fail(kInternal, err);
+    cudacheck(cudaEventRecord(ran[k], pg.sa));
+  }
+  auto land = [&](int64_t k) {  // staging slot k % 2 -> the caller's buffers
+    cudacheck(cudaEventSynchronize(copied[k]));
+    const int64_t off = k * kSub, nk = std::min(kSub, n - off);
+    const char* src = stage.p + (k & 1) * slice_bytes;
+    if (d_ms) {
+      std::memcpy(ms_host + off, src, 8 * nk);
+      src += 8 * kSub;
+    }
+    if (d_wms) std::memcpy(wms_host + off * W, src, 8 * nk * W);
+  };
+  for (int64_t k = 0; k < K; ++k) {
+    const int64_t off = k * kSub, nk = std::min(kSub, n - off);
+    char* dst = stage.p + (k & 1) * slice_bytes;
+    cudacheck(cudaStreamWaitEvent(pg.sb, ran[k], 0));
+    if (d_ms) {
+      cudacheck(cudaMemcpyAsync(dst, d_ms + off, 8 * nk, cudaMemcpyDeviceToHost, pg.sb));
+      dst += 8 * kSub;
+    }
+    if (d_wms) cudacheck(cudaMemcpyAsync(dst, d_wms + off * W, 8 * nk * W, cudaMemcpyDeviceToHost, pg.sb));
+    cudacheck(cudaEventRecord(copied[k], pg.sb));
+    if (k >= 1) land(k - 1);
+  }
+  land(K - 1);
+}
+
+}  // namespace
+
+void merge_stats(cs_sweep_stats& total, const cs_sweep_stats& part, bool first) {
+  if (first) {
+    total = part;
+    return;
+  }
+  if (part.count <= 0) return;
+  if (total.count <= 0) {
+    const int64_t U = total.upper_us, L = total.lower_us;
+    total = part;
+    total.upper_us = U;
+    total.lower_us = L;
+    return;
+  }
+  if (part.min_us < total.min_us) total.min_us = part.min_us, total.argmin_seed = part.argmin_seed;
+  if (part.max_us > total.max_us) total.max_us = part.max_us, total.argmax_seed = part.argmax_seed;
+  if (part.iter_min_us < total.iter_min_us)
+    total.iter_min_us = part.iter_min_us, total.iter_argmin_seed = part.iter_argmin_seed;
+  if (part.iter_max_us > total.iter_max_us)
+    total.iter_max_us = part.iter_max_us, total.iter_argmax_seed = part.iter_argmax_seed;
+  total.count += part.count;
+  total.sum_us += part.sum_us;
+  total.iter_sum_us += part.iter_sum_us;
+  total.sumsq_us += part.sumsq_us;
+  total.straggler_sum += part.straggler_sum;
+  for (int k = 0; k < CS_HIST_BINS; ++k) {
+    total.e_hist[k] += part.e_hist[k];
+    total.straggler_hist[k] += part.straggler_hist[k];
+  }
+}
+
+cs_sweep_stats sweep_fast(const std::vector<SweepCtx*>& ctxs, uint64_t seed_lo, int64_t count,
+                          int64_t* makespans, int64_t* worker_ms, const DeviceReducer* reducer) {
+  const int nd = static_cast<int>(ctxs.size());
+  const SweepCtx& c0 = *ctxs[0];
+  const int64_t W = c0.cluster ? static_cast<int64_t>(c0.workers.size()) : 1;
+  const int kb = csk_key_bits(c0.U);
+  // a round's seed offsets must stay below 2^key_bits; a device's span
+  // within a round below 2^26 (its per-seed buffers)
+  const int64_t per_dev_cap = int64_t{1} << 26;
+  const int64_t round = std::min<int64_t>(int64_t{1} << std::min(kb, 40), per_dev_cap * nd);
+  cs_sweep_stats total{};
+  bool first = true;
+  std::vector<int64_t> i64(CS_DSTATS_I64);
+  std::vector<double> f64(CS_DSTATS_F64);
+  for (int64_t base = 0; base < count || (first && count == 0); base += round) {
+    const int64_t rn = std::min(round, count - base);
+    const uint64_t rlo = seed_lo + static_cast<uint64_t>(base);
+    std::vector<std::string> errors(nd);
+    auto device_part = [&](int d) {
+      try {
+        cudacheck(cudaSetDevice(ctxs[d]->device));
+        const int64_t per = (rn + nd - 1) / nd;
+        const int64_t off = std::min<int64_t>(rn, d * per), n = std::min<int64_t>(per, rn - off);
+        DevBuf st, ms, wms;  // statistics: i64 then f64 words
+        st.alloc(8 * (CS_DSTATS_I64 + CS_DSTATS_F64));
+        int64_t* d_i64 = st.as<int64_t>();
+        double* d_f64 = reinterpret_cast<double*>(d_i64 + CS_DSTATS_I64);
+        char err[256] = {0};
+        if (csk_sweep_reset(ctxs[d]->plan, nullptr, d_i64, d_f64, err)) fail(kInternal, err);
+        if (makespans && n > 0) ms.alloc(8 * n);
+        if (worker_ms && c0.cluster && n > 0) wms.alloc(8 * n * W);
+        if (n > 0)
+          run_span(*ctxs[d], rlo + static_cast<uint64_t>(off), n, rlo, ms.as<int64_t>(), wms.as<int64_t>(), d_i64,
+                   d_f64, makespans ? makespans + base + off : nullptr,
+                   worker_ms && c0.cluster ? worker_ms + (base + off) * W : nullptr);
+        if (nd > 1) {
+          reducer->reduce(d, d_i64, d_f64, d == 0 ? i64.data() : nullptr, d == 0 ? f64.data() : nullptr);
+        } else {
+          std::vector<char> h(8 * (CS_DSTATS_I64 + CS_DSTATS_F64));
+          cudacheck(cudaMemcpy(h.data(), d_i64, h.size(), cudaMemcpyDeviceToHost));
+          std::memcpy(i64.data(), h.data(), 8 * CS_DSTATS_I64);
+          std::memcpy(f64.data(), h.data() + 8 * CS_DSTATS_I64, 8 * CS_DSTATS_F64);
+        }
+      } catch (const std::exception& e) {
+        errors[d] = e.what();
+      }
+    };
+    if (nd == 1) {
+      device_part(0);
+    } else {
+      std::vector<std::thread> th;
+      for (int d = 0; d < nd; ++d) th.emplace_back(device_part, d);
+      for (auto& t : th) t.join();
+    }
+    for (const auto& e : errors)
+      if (!e.empty()) fail(kInternal, e);
+    cs_sweep_stats part{};
+    finish_stats(c0, i64.data(), f64.data(), rlo, &part);
+    merge_stats(total, part, first);
+    first = false;
+    if (count == 0) break;
+  }
+  return total;
 }
 
 }  // namespace tictac

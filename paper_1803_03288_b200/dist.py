@@ -14,27 +14,36 @@ def shard(seed_lo: int, count: int, rank: int, world: int) -> tuple[int, int]:
     return lo, n
 
 
-def reduce_stats(i64, f64, rank: int, world: int, slots=None):
-    """In-place all-reduce of one step's statistics.
+def reduce_stats(i64, f64, rank: int, world: int, buf=None):
+    """In-place all-reduce of one step's statistics: ONE SUM all-reduce.
 
-    i64[0] (min key) and i64[1] (max key) are gathered through per-rank slots
-    of a zeroed vector and one SUM all-reduce, the counters/histograms
-    i64[2:] with a second SUM, the float sums f64 with a third. Keys are
-    (m << key_bits) | offset with offsets relative to the GLOBAL seed base,
-    so the minimum resolves ties to the lowest seed across ranks."""
+    Every rank writes into a zeroed int64 vector: its min key i64[0] and max
+    key i64[1] into per-rank slots, its counters and histograms i64[2:] into
+    a shared region, and the bit patterns of its float sums f64 into per-rank
+    slots; after the SUM each slot holds exactly one rank's value, so the
+    min/max and the float sums (in rank order, deterministic) are finished
+    locally. Keys are (m << key_bits) | offset with offsets relative to the
+    GLOBAL seed base, so the minimum resolves ties to the lowest seed across
+    ranks."""
     import torch
     import torch.distributed as dist
     if world == 1:
         return i64, f64
-    if slots is None:
-        slots = torch.zeros(2 * world, dtype=torch.int64, device=i64.device)
-    slots.zero_()
+    n_i = i64.numel() - 2
+    n_f = f64.numel()
+    size = 2 * world + n_i + n_f * world
+    if buf is None or buf.numel() < size:
+        buf = torch.zeros(size, dtype=torch.int64, device=i64.device)
+    buf.zero_()
     # an idle rank's min key is all ones (-1 as int64): it must not win
-    slots[rank] = torch.where(i64[0] < 0, torch.full_like(i64[0], (1 << 63) - 1), i64[0])
-    slots[world + rank] = i64[1]
-    dist.all_reduce(slots)
-    dist.all_reduce(i64[2:])
-    dist.all_reduce(f64)
-    i64[0] = slots[:world].min()
-    i64[1] = slots[world:].max()
+    buf[rank] = torch.where(i64[0] < 0, torch.full_like(i64[0], (1 << 63) - 1), i64[0])
+    buf[world + rank] = i64[1]
+    buf[2 * world:2 * world + n_i] = i64[2:]
+    fo = 2 * world + n_i
+    buf[fo + rank * n_f:fo + (rank + 1) * n_f] = f64.contiguous().view(torch.int64)
+    dist.all_reduce(buf[:size])
+    i64[0] = buf[:world].min()
+    i64[1] = buf[world:2 * world].max()
+    i64[2:] = buf[2 * world:2 * world + n_i]
+    f64.copy_(buf[fo:fo + world * n_f].view(torch.float64).view(world, n_f).sum(0))
     return i64, f64
