@@ -92,6 +92,7 @@ _SIGS = {
                               C.POINTER(SweepStats)],
     "cs_sweep_plan_create": [_vp, _vp, C.POINTER(SimPolicy), _pp],
     "cs_sweep_plan_info": [_vp, _pp],
+    "cs_sweep_path_json": [_vp, _vp, C.POINTER(SimPolicy), _pp],
     "cs_sweep_plan_reset": [_vp, _vp, _vp, _vp],
     "cs_sweep_plan_run": [_vp, C.c_uint64, C.c_int64, C.c_uint64, _vp, _vp, _vp, _vp],
     "cs_sweep_stats_finish": [_vp, _vp, _vp, C.c_uint64, C.POINTER(SweepStats)],
@@ -102,6 +103,7 @@ _FREE = ["cs_graph_free", "cs_oracle_free", "cs_schedule_free", "cs_report_free"
          "cs_string_free", "cs_sweep_plan_free"]
 REFERENCE_SYMBOLS = [k for k in _SIGS if k not in (
     "cs_sweep_random", "cs_sweep_random_multi", "cs_simulate_orders", "cs_sweep_plan_create", "cs_sweep_plan_info",
+    "cs_sweep_path_json",
     "cs_sweep_plan_reset", "cs_sweep_plan_run", "cs_sweep_stats_finish",
     "cs_graph_generate_model", "cs_tac_traffic")] + [f for f in _FREE if f != "cs_sweep_plan_free"] + [
     "cs_last_error", "cs_version"]
@@ -343,6 +345,12 @@ class Graph(_Handle):
         if wms is not None:
             out["worker_makespans"] = wms[:count * nw].reshape(count, nw)
         return out
+
+    def sweep_path(self, oracle: "Oracle", pol: SimPolicy | None = None) -> dict:
+        out = C.c_void_p()
+        self.lib.call("cs_sweep_path_json", self.h, oracle.h, C.byref(pol) if pol is not None else None,
+                      C.byref(out))
+        return json.loads(self.lib.take_str(out))
 
     def simulate_orders(self, oracle: "Oracle", orders: np.ndarray, pol: SimPolicy | None = None):
         orders = np.ascontiguousarray(orders, dtype=np.int32)

@@ -374,7 +374,7 @@ int cs_simulate(const cs_graph* g, const cs_oracle* o, const cs_schedule* s,
     rep->g = g->g;
     rep->pol = p;
     std::shared_ptr<SweepCtx> ctx;
-    bool closed = !g->g->cluster() && in.all_recvs_prioritized && (!p.gated || p.noise == 0.0);
+    bool closed = !g->g->cluster() && in.all_recvs_prioritized;
     if (closed && !p.gated) {  // ungated: only distinct priorities avoid channel draws
       std::vector<int32_t> pr;
       for (int32_t r : g->g->recv_ops()) pr.push_back(in.prio[r]);
@@ -382,17 +382,18 @@ int cs_simulate(const cs_graph* g, const cs_oracle* o, const cs_schedule* s,
       closed = std::adjacent_find(pr.begin(), pr.end()) == pr.end();
     }
     if (closed) ctx = cached_sweep(g, o, p);
-    if (ctx && ctx->fast && !ctx->cluster && !ctx->noisy) {
+    if (ctx && ctx->fast && !ctx->cluster) {
       // Closed form: the gate order is the recvs sorted by
-      // (priority, id) (sim.cpp:95-104); gated, noiseless, recvs are roots,
-      // so no inversions and no forced releases.
+      // (priority, id) (sim.cpp:95-104), then the reorder-noise swaps; recvs
+      // are roots, so the violations are the swaps (A.4) and nothing is
+      // force-released.
       const auto& ro = g->g->recv_ops();
       std::vector<int32_t> order(ro.size());
       for (size_t c = 0; c < ro.size(); ++c) order[c] = static_cast<int32_t>(c);
       std::stable_sort(order.begin(), order.end(),
                        [&](int32_t a, int32_t b) { return in.prio[ro[a]] < in.prio[ro[b]]; });
+      rep->violations = apply_gate_noise(order, p);
       rep->makespan = ctx->order_makespan(order);
-      rep->violations = 0;
       rep->d = std::move(in.d);
       rep->prio = std::move(in.prio);
     } else {
@@ -643,20 +644,34 @@ int cs_simulate_orders(const cs_graph* g, const cs_oracle* o, const int32_t* ord
     const Policy p = policy_of(policy);
     auto ctx = make_sweep(g->g, o->o, p);
     if (n == 0) return;
-    if (ctx->fast && !ctx->cluster && !ctx->noisy) {  // rows validated by the kernel as it reads them
+    if (ctx->fast && !ctx->cluster) {  // rows validated by the kernel as it reads them
+      // every row shares the choice seed, hence the same reorder-noise swaps
+      // (positions whose noise draw fired, sim.cpp:106-114): applied to each
+      // rank-order row they give its gate order; violations = swaps (A.4)
+      std::vector<int32_t> pos(R);
+      for (int32_t k = 0; k < R; ++k) pos[k] = k;
+      const int64_t swaps = apply_gate_noise(pos, p);
+      std::vector<int32_t> gated_rows;
+      const int32_t* rows = orders;
+      if (swaps) {
+        gated_rows.resize(static_cast<size_t>(n) * R);
+        for (int64_t b = 0; b < n; ++b)
+          for (int32_t k = 0; k < R; ++k) gated_rows[b * R + k] = orders[b * R + pos[k]];
+        rows = gated_rows.data();
+      }
       auto cudacheck = [&](cudaError_t e) {
         if (e != cudaSuccess) fail(kInternal, std::string("CUDA error: ") + cudaGetErrorString(e));
       };
       DevPtr b_o, b_m;
       cudacheck(cudaMallocAsync(&b_o.p, 4 * n * R + 4, 0));
       cudacheck(cudaMallocAsync(&b_m.p, 8 * n, 0));
-      cudacheck(cudaMemcpy(b_o.p, orders, 4 * n * R, cudaMemcpyHostToDevice));
+      cudacheck(cudaMemcpy(b_o.p, rows, 4 * n * R, cudaMemcpyHostToDevice));
       char err[256] = {0};
       const int rc = csk_sweep_orders(ctx->plan, b_o.as<int32_t>(), n, nullptr, b_m.as<int64_t>(), err);
       if (rc) fail(rc == 4 ? kParameter : kInternal, err);
       cudacheck(cudaMemcpy(makespans_out, b_m.p, 8 * n, cudaMemcpyDeviceToHost));
       if (violations_out)
-        for (int64_t k = 0; k < n; ++k) violations_out[k] = 0;  // gated, noiseless, roots
+        for (int64_t k = 0; k < n; ++k) violations_out[k] = swaps;
       return;
     }
     {  // every row a permutation of the recv columns (checked as the kernel does)
@@ -697,6 +712,19 @@ int cs_sweep_plan_create(const cs_graph* g, const cs_oracle* o, const cs_sim_pol
     auto ctx = make_sweep(g->g, o->o, policy_of(policy));
     if (!ctx->fast) fail(kParameter, "closed-form sweep does not apply: " + ctx->why);
     *out = new cs_sweep_plan{std::move(ctx)};
+  });
+}
+
+int cs_sweep_path_json(const cs_graph* g, const cs_oracle* o, const cs_sim_policy* policy, char** out_json) {
+  return guarded([&] {
+    need(g, "graph");
+    need(o, "oracle");
+    need(out_json, "out_json");
+    std::shared_ptr<SweepCtx> c = cached_sweep(g, o, policy_of(policy));
+    Json j;
+    j["path"] = !c->fast ? "event_sim_kernel" : c->dag ? "dag_sweep_kernel" : "chain_sweep_kernel";
+    j["why"] = c->fast ? "" : c->why;
+    *out_json = dup(dump_doc(j));
   });
 }
 

@@ -207,6 +207,13 @@ Report simulate_prepared(const Graph& g, const std::vector<int64_t>& d, const st
 // One run inside SURVEY A.2's regime (worker graph, one compute unit and one
 // channel, gated, noiseless, every recv prioritized and no compute op): the
 // specialised device replica (csk_event_a2), same Report as simulate_prepared.
+// Gated reorder noise on a single channel's gate sequence (sim.cpp:106-114):
+// adjacent swaps at positions 1..n-1 whose draw of the separate stream
+// Rng(splitmix64(choice_seed ^ salt)) has unit() < p. Returns the number of
+// swaps, which is the run's violation count in SURVEY A.2's regime (A.4:
+// each left-to-right swap adds exactly one inversion; recvs are roots, so
+// nothing is force-released).
+int64_t apply_gate_noise(std::vector<int32_t>& order, const Policy& p);
 Report simulate_a2(const Graph& g, const std::vector<int64_t>& d, const std::vector<int32_t>& prio,
                    const Policy& p);
 std::pair<int64_t, int64_t> bounds(const Graph& g, const TimeOracle& o);  // metrics.cpp:10-22

@@ -252,14 +252,28 @@ Report simulate_prepared(const Graph& g, const std::vector<int64_t>& d, const st
   return make_report(g, st, en, m, viol);
 }
 
+int64_t apply_gate_noise(std::vector<int32_t>& order, const Policy& p) {
+  if (!p.gated || p.noise <= 0.0) return 0;
+  HostRng nr(splitmix64(p.choice_seed ^ 0x9e3779b97f4a7c15ULL));
+  int64_t swaps = 0;
+  for (size_t pos = 1; pos < order.size(); ++pos)
+    if (nr.unit() < p.noise) {
+      std::swap(order[pos - 1], order[pos]);
+      ++swaps;
+    }
+  return swaps;
+}
+
 Report simulate_a2(const Graph& g, const std::vector<int64_t>& d, const std::vector<int32_t>& prio,
                    const Policy& p) {
-  // gate sequence: recvs by (priority, id) (sim.cpp:95-104); no violations
-  // in this regime (recvs complete in gate order, nothing is force-released)
+  // gate sequence: recvs by (priority, id) (sim.cpp:95-104), then the reorder
+  // noise swaps; recvs complete in gate order, so the violations are the
+  // swaps and nothing is force-released
   const bool trace = std::getenv("TICTAC_EVENT_TRACE") != nullptr;
   const auto t0 = std::chrono::steady_clock::now();
   std::vector<int32_t> order(g.recv_ops().begin(), g.recv_ops().end());
   std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return prio[a] < prio[b]; });
+  const int64_t swaps = apply_gate_noise(order, p);
   const int32_t n = g.n();
   std::vector<int64_t> st(n), en(n);
   int64_t m = 0;
@@ -268,7 +282,7 @@ Report simulate_a2(const Graph& g, const std::vector<int64_t>& d, const std::vec
                      st.data(), en.data(), err),
         err);
   const auto t1 = std::chrono::steady_clock::now();
-  Report r = make_report(g, st, en, m, 0);
+  Report r = make_report(g, st, en, m, swaps);
   if (trace)
     std::fprintf(stderr, "[simulate_a2] device call %.3f ms, report build %.3f ms\n",
                  std::chrono::duration<double, std::milli>(t1 - t0).count(),

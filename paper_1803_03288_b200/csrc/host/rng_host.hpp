@@ -22,6 +22,7 @@ struct HostRng {
     while (v > limit);
     return v % n;
   }
+  double unit() { return static_cast<double>(next() >> 11) * 0x1.0p-53; }  // rng.hpp:33
 };
 
 inline uint64_t splitmix64(uint64_t x) {  // rng.hpp:49-54

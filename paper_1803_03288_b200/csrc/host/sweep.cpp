@@ -515,6 +515,10 @@ std::unique_ptr<SweepCtx> make_sweep(std::shared_ptr<const Graph> g, const TimeO
   if (cudaGetDevice(&s->device) != cudaSuccess) s->device = 0;
   bool ok = s->U < (int64_t{1} << 37);
   if (!ok) s->why = "makespan bound beyond the statistics key range";
+  if (ok && std::getenv("TICTAC_SWEEP_FORCE_EXACT")) {  // test knob: the exact event replica
+    ok = false;
+    s->why = "forced by TICTAC_SWEEP_FORCE_EXACT";
+  }
   std::vector<ChainTables> tabs;
   std::shared_ptr<const ChainShape> shape0;  // worker 0's shape (the program the workers share)
   if (ok && !s->cluster) {

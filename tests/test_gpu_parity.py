@@ -236,8 +236,12 @@ def test_event_sim_lane_modes_agree(lib, orc, monkeypatch, model):
                 out[lanes] = list(g.simulate_orders(o, orders, pol))
         for a, b in zip(out["32"], out["1"]):
             assert np.array_equal(a, b), (kind, pol.counter_gate, pol.reorder_noise)
-    # oracle spot checks of the thread-per-run shape (ungated random sweeps)
+    # oracle spot checks of the thread-per-run shape (ungated random sweeps,
+    # exact replica forced: these orders would otherwise take the closed form)
     monkeypatch.setenv("TICTAC_EVENT_LANES", "1")
+    monkeypatch.setenv("TICTAC_SWEEP_FORCE_EXACT", "1")
+    o = g.declared()  # a fresh oracle: a fresh (forced) plan
+    assert g.sweep_path(o, policy(False, 0, 0.0))["path"] == "event_sim_kernel"
     ms = g.sweep_random(o, 5, 3000, policy(False, 0, 0.0), makespans=True)["makespans"]
     for k in (0, 1, 1234, 2999):
         pr = orc.schedule_for(og, "random", 5 + k)
@@ -304,12 +308,15 @@ def test_event_sim_backs_off_when_hbm_is_short(lib):
         "import sys, torch; sys.path.insert(0, '.')\n"
         "from paper_1803_03288_b200.capi import Lib, policy\n"
         "g = Lib().model('resnet_v2_101_training', 1); o = g.declared()\n"
+        "assert g.sweep_path(o, policy(False, 0, 0.0))['path'] == 'event_sim_kernel'\n"
         "free, _ = torch.cuda.mem_get_info()\n"
         "hog = torch.empty(max(0, free - (3 << 30)), dtype=torch.uint8, device='cuda')\n"
         "r = g.sweep_random(o, 1, 100000, policy(False, 0, 0.0))\n"
         "print(r['count'], r['min_us'], r['argmin_seed'], r['sum_us'])\n")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    out = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, check=True)
+    env = dict(os.environ, TICTAC_SWEEP_FORCE_EXACT="1")  # the exact replica, not the closed form
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, check=True,
+                         env=env)
     got = [int(x) for x in out.stdout.split()[-4:]]
     g = lib.model("resnet_v2_101_training", 1)
     r = g.sweep_random(g.declared(), 1, 100000, policy(False, 0, 0.0))
@@ -326,9 +333,12 @@ def test_concurrent_calls_on_shared_handles(lib):
     o = g.declared()
     toy = lib.generate("chain", 7, 1, "1", 3)
     to = toy.declared()
+    cl = lib.generate("chain", 6, 2, "1/2", 11).expand(2, 1, 3)  # PS ops take time: exact replica
+    co = cl.declared()
+    assert cl.sweep_path(co)["path"] == "event_sim_kernel"
     jobs = {
         "sweep": lambda: g.sweep_random(o, 1, 1 << 16, None)["sum_us"],
-        "sweep_exact": lambda: g.sweep_random(o, 1, 4096, policy(False, 0, 0.0))["sum_us"],
+        "sweep_exact": lambda: cl.sweep_random(co, 1, 4096, None)["sum_us"],
         "tac": lambda: g.tac(o).serialize(),
         "tic": lambda: g.tic("literal").serialize(),
         "report": lambda: g.simulate(o, g.random(9), policy(True, 9, 0.0)).json(),
