@@ -2,19 +2,26 @@
 """Benchmark: recv-order makespan sims/sec (BASELINE.json metric) on B200.
 
 Workload (one "step"): SURVEY §8d config 4 — the ResNet-v2-101-shaped
-training DAG (5,380 ops / 244 recvs, seed 1), 2^24 = 16,777,216 random recv
-orders (seeds 1..2^24), each = random_schedule(seed) + gated simulate with
-choice_seed = seed (the `sched sweep` loop, sched_main.cpp:472-477), reduced
-to min/argmin makespan + 1000-bin efficiency histogram. Sharded contiguously
-over N GPUs (strong scaling, one NCCL reduction per step).
+training DAG (5,380 ops / 7,090 edges / 244 recvs, seed 1; the committed
+bench_data/resnet_v2_101_training-s1.json.gz, which both arms read), 2^24 =
+16,777,216 random recv orders (seeds 1..2^24), each = random_schedule(seed)
++ gated simulate with choice_seed = seed (the `sched sweep` loop,
+sched_main.cpp:472-477), reduced to min/argmin makespan + 1000-bin
+efficiency histogram. At N > 1 GPUs the same fixed 2^24 orders are split
+into contiguous shards (strong scaling, one NCCL all-reduce per step); the
+weak view (2^24 per GPU) is reported beside it.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
 Prints ONE JSON line on rank 0. `value` = device-timed sims/s of the whole
 job; `e2e` = the same through the C ABI with host buffers (cs_sweep_random);
-`roofline` uses SURVEY §8d's algorithmic bytes B_sim = 12R + 2V + 2E + 16 per
-ordering against MEASURED_PEAKS.json hbm_gbs; `cpu_baseline` times the
-reference library (oracle/_ref, built from /root/reference) on this host.
+`roofline` = the binding resource of the dominant kernel (instruction issue,
+warp-instructions per ordering from the committed ncu capture x this run's
+orderings/s), with SURVEY §8d's HBM-equivalent B_sim = 12R + 2V + 2E + 16
+bytes per ordering in `roofline_hbm`; `cpu_baseline` times the reference
+library (oracle/_ref, built from /root/reference) on this host.
+`--impl reference` runs only the reference library (never this one) on the
+same config.
 """
 from __future__ import annotations
 
@@ -34,6 +41,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 MODEL = "resnet_v2_101_training"
+BRANCHY = "resnet_v2_101_training_branchy"
 COUNT = 1 << 24
 SEED_LO = 1
 L2_FLUSH_BYTES = 256 << 20  # > 126 MB L2
@@ -120,19 +128,92 @@ class ClockSampler:
                 "source": "nvml" if self.nvml else "nvidia-smi"}
 
 
+
+def bench_json(model):
+    """The committed input DAG (reference-format JSON, tools/make_bench_data.py)."""
+    import gzip
+    with gzip.open(os.path.join(ROOT, "bench_data", f"{model}-s1.json.gz"), "rb") as f:
+        return f.read().decode()
+
+
+def graph_file(model):
+    d = tempfile.mkdtemp(prefix="tictac_bench_")
+    p = os.path.join(d, f"{model}.json")
+    with open(p, "w") as f:
+        f.write(bench_json(model))
+    return p
+
+
+def shape(text):
+    doc = json.loads(text)
+    return {"ops": len(doc["ops"]), "edges": len(doc["edges"]),
+            "recvs": sum(op["kind"] == "recv" for op in doc["ops"])}
+
+
+def workload_config(world):
+    """The `config` object, identical in both arms."""
+    s = shape(bench_json(MODEL))
+    return {"workload": f"config4: {MODEL} DAG seed 1 ({s['ops']} ops / {s['edges']} edges / {s['recvs']} recvs, "
+                        f"bench_data/{MODEL}-s1.json.gz), {COUNT} random recv orders per step (seeds 1..{COUNT}), "
+                        f"gated, choice_seed=seed; min/argmin makespan + E histogram",
+            "parallelism": f"{COUNT} orders split into {world} contiguous seed shards (one per GPU), "
+                           f"one NCCL all-reduce per step" if world > 1 else "1 GPU",
+            "l2": "flushed between steps (256 MiB write)"}
+
+
 def b_sim(info):
     """SURVEY §8d algorithmic bytes per ordering: 12R + 2V + 2E + 16."""
     return 12 * info["recvs_per_worker"] + 2 * info["ops"] + 2 * info["edges"] + 16
 
 
-def graph_files(lib, model):
-    g = lib.model(model, 1)
-    text = g.serialize()
-    d = tempfile.mkdtemp(prefix="tictac_bench_")
-    p = os.path.join(d, "graph.json")
-    with open(p, "w") as f:
-        f.write(text)
-    return g, p
+def ncu_summary(name):
+    try:
+        with open(os.path.join(ROOT, "profiles", name)) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return None
+
+
+def issue_roofline(summary, orders_per_s, mhz, traffic_scale):
+    """Binding roofline of a sweep kernel: warp-instructions per ordering
+    (ncu, committed summary) x this run's orderings/s against 148 SMs x 4
+    schedulers x SM clock; traffic = ncu DRAM bytes scaled to the launch."""
+    if not summary:
+        return None
+    ipo = summary["warp_instructions_per_ordering"]
+    peak = 148 * 4 * mhz * 1e6
+    ach = ipo * orders_per_s
+    return {"bound": "issue", "achieved": ach, "peak": peak, "unit": "warp-inst/s", "frac": ach / peak,
+            "traffic": summary["dram_bytes_per_launch"] * traffic_scale / summary["orderings"],
+            "warp_inst_per_order": ipo, "kernel": summary["kernel"].split("(")[0],
+            "source": "instructions per ordering and DRAM bytes from the committed ncu capture (profiles/); "
+                      "orderings/s from this run's CUDA events; peak = 148 SMs x 4 schedulers x SM clock under load"}
+
+
+def hbm_roofline(bsim, orders_per_s, hbm, peak_src):
+    ach = bsim * orders_per_s / 1e9
+    return {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+            "algorithmic_bytes_per_order": bsim, "peak_source": peak_src,
+            "note": "SURVEY §8d B_sim = 12R+2V+2E+16 bytes per ordering for a design that streams per-ordering "
+                    "state through HBM; the fused kernels keep it on chip (DRAM traffic ~0), so this "
+                    "HBM-equivalent exceeds 1 and the binding resource is instruction issue (roofline)"}
+
+
+def device_rate(plan, lo, n, key_base, stream, d_i64, d_f64, steps=5, flush=None):
+    """Median kernel time of plan.run over n seeds (CUDA events, launching stream)."""
+    import torch
+    ts = []
+    for _ in range(steps + 2):
+        if flush is not None:
+            flush.fill_(1)
+        plan.reset(stream.cuda_stream, d_i64.data_ptr(), d_f64.data_ptr())
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        plan.run(lo, n, key_base, stream.cuda_stream, None, d_i64.data_ptr(), d_f64.data_ptr())
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    return sorted(ts[2:])[len(ts[2:]) // 2]
 
 
 def cpu_model():
@@ -201,7 +282,8 @@ def sweep_vs_reference(lib, g, gpath, workload, noise=None, count=1 << 18, ref_t
     t = time.perf_counter()
     res = g.sweep_random(o, SEED_LO, count, pol, makespans=True)
     dt = time.perf_counter() - t
-    out = {"workload": workload, "sims": count, "seconds": round(dt, 4), "sims_per_s": count / dt}
+    out = {"workload": workload, "sims": count, "seconds": round(dt, 4), "sims_per_s": count / dt,
+           "path": g.sweep_path(o, pol)["path"]}
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle
     if oracle.ref_available():
@@ -220,18 +302,20 @@ def sweep_vs_reference(lib, g, gpath, workload, noise=None, count=1 << 18, ref_t
 def exact_paths(lib, path):
     """Outside the plain gated closed form: (a) config 4 with reorder noise
     0.1 — still the closed form, on the noise-permuted gate sequence; (b)
-    config 3's full iteration makespans, PS operations included, which only
-    the exact event replica (thread per run at this batch size) produces."""
-    g4 = lib.model(MODEL, 1)
+    config 3 (VGG-16 x 4 workers / 1 PS) with PS operations that take time
+    (100 us each): its makespans come only from the exact event replica
+    (thread per run at this batch size)."""
+    g4 = lib.graph(bench_json(MODEL))
     a = sweep_vs_reference(lib, g4, path, f"config4 {MODEL}, counter gate + reorder noise 0.1 "
                                           f"(closed form on the noise-permuted gate order)", 0.1, 1 << 22)
-    c3 = lib.model("vgg16_training", 1).expand(4, 1, 0)
-    p3 = os.path.join(os.path.dirname(path), "config3.json")
+    c3 = lib.model("vgg16_training", 1).expand(4, 1, 100)
+    p3 = os.path.join(os.path.dirname(path), "config3_ps100.json")
     with open(p3, "w") as f:
         f.write(c3.serialize())
-    b = sweep_vs_reference(lib, c3, p3, "config3 vgg16_training x 4 workers / 1 PS, full iteration makespans "
-                                        "(exact event replica, thread per run)", None, 1 << 18)
-    return {"noise_sweep_config4": a, "event_replica_config3_makespans": b}
+    b = sweep_vs_reference(lib, c3, p3, "config3 vgg16_training x 4 workers / 1 PS with 100 us PS ops, full "
+                                        "makespans (exact event replica, thread per run)", None, 1 << 18)
+    b["path"] = c3.sweep_path(c3.declared())
+    return {"noise_sweep_config4": a, "event_replica_config3_ps100_makespans": b}
 
 
 def cpu_baseline(path, target_s=10.0, g=None, o=None):
@@ -259,11 +343,9 @@ def cpu_baseline(path, target_s=10.0, g=None, o=None):
         out["sample_identical_to_ours"] = bool(np.array_equal(ours, np.fromfile(binp, dtype=np.int64)))
     # reference TIC/TAC wall time on config 1 (single thread: the reference has none)
     try:
-        from paper_1803_03288_b200 import capi
-        g1 = capi.Lib().model("resnet_v2_50_inference", 1)
         p1 = os.path.join(os.path.dirname(path), "config1.json")
         with open(p1, "w") as f:
-            f.write(g1.serialize())
+            f.write(bench_json("resnet_v2_50_inference"))
         for algo, arg in (("tac", "declared"), ("tic", "amended")):
             rr = subprocess.run([oracle.REF_SWEEP, algo, p1, arg], capture_output=True, text=True, check=True)
             out[f"{algo}_config1_seconds"] = json.loads(rr.stderr.strip().splitlines()[-1])["seconds"]
@@ -309,6 +391,60 @@ def sweep_rate(g, o, count):
     return st, count / (time.perf_counter() - t)
 
 
+def config2(lib, model):
+    g = lib.model(model, 1)
+    o = g.declared()
+    U, L = g.bounds(o)
+    g.tac(o)
+    t = time.perf_counter()
+    s = g.tac(o)
+    tac_s = time.perf_counter() - t
+    m_tac = g.simulate(o, s).makespan()
+    st, rate = sweep_rate(g, o, 1_000_000)
+    h = st["e_hist"]
+    mean_e = (U * st["count"] - st["sum_us"]) / (st["count"] * (U - L))
+    return {f"config2_{model}": {
+        "ops": g.op_count(), "edges": g.edge_count(), "recvs": g.recv_count(), "path": g.sweep_path(o)["path"],
+        "tac_seconds": round(tac_s, 6), "tac_makespan_us": m_tac,
+        "tac_E": (U - m_tac) / (U - L), "random_orders": st["count"], "sims_per_s": rate,
+        "min_us": st["min_us"], "argmin_seed": st["argmin_seed"], "mean_E": mean_e,
+        "E_hist_nonzero_bins": int((h > 0).sum()), "E_best_bin": int(max(i for i in range(1000) if h[i]))}}
+
+
+def dag_config4(lib, hbm, peak_src, mhz, stream, d_i64, d_f64, flush):
+    """The general-DAG closed form (dag_sweep_kernel) at config-4 size: the
+    Inception-style branchy ResNet-v2-101-shaped DAG (same recvs, bytes and
+    compute times as config 4, not nested), 2^24 orders per step, device
+    kernel time; e2e through cs_sweep_random; the reference library on the
+    host cores for a bounded sample, compared value by value."""
+    from paper_1803_03288_b200 import capi
+    text = bench_json(BRANCHY)
+    g = lib.graph(text)
+    o = g.declared()
+    plan = capi.SweepPlan.create(g, o)
+    info = plan.info()
+    ms = device_rate(plan, SEED_LO, COUNT, SEED_LO, stream, d_i64, d_f64, flush=flush)
+    rate = COUNT / (ms / 1000.0)
+    st = plan.finish(d_i64.cpu().numpy(), d_f64.cpu().numpy(), SEED_LO)
+    t = time.perf_counter()
+    g.sweep_random(g.declared(), SEED_LO, COUNT)
+    e2e = COUNT / (time.perf_counter() - t)
+    path = os.path.join(tempfile.mkdtemp(prefix="tictac_bench_"), f"{BRANCHY}.json")
+    with open(path, "w") as f:
+        f.write(text)
+    out = {"workload": f"{BRANCHY} DAG seed 1 ({info['ops']} ops / {info['edges']} edges / "
+                       f"{info['recvs_per_worker']} recvs, {info['joins']} join classes, "
+                       f"{info['program_records']} program records), {COUNT} random orders per step",
+           "kernel": info["kernel"], "kernel_ms": ms, "sims_per_s": rate, "e2e_sims_per_s": e2e,
+           "min_us": st["min_us"], "argmin_seed": st["argmin_seed"],
+           "roofline_hbm": hbm_roofline(b_sim(info), rate, hbm, peak_src),
+           "roofline": issue_roofline(ncu_summary("dag_ncu_summary.json"), rate, mhz, COUNT)}
+    ref = sweep_vs_reference(lib, g, path, "reference sample", None, 1 << 18)
+    out["reference_cpu"] = ref.get("reference_cpu")
+    out["sample_identical"] = ref.get("sample_identical")
+    return out
+
+
 def other_configs(lib):
     """SURVEY §8d configs 1-3 through the public C ABI (e2e, host buffers)."""
     from paper_1803_03288_b200 import capi
@@ -330,23 +466,10 @@ def other_configs(lib):
     st, rate = sweep_rate(g, o, 1000)
     c1["random_1000"] = {"min_us": st["min_us"], "mean_us": st["sum_us"] / st["count"], "sims_per_s": rate}
     out["config1_resnet_v2_50_inference"] = c1
-    # config 2: Inception-v3 training — TAC + 1M random orders, E histogram
-    g = lib.model("inception_v3_training", 1)
-    o = g.declared()
-    U, L = g.bounds(o)
-    g.tac(o)
-    t = time.perf_counter()
-    s = g.tac(o)
-    tac_s = time.perf_counter() - t
-    m_tac = g.simulate(o, s).makespan()
-    st, rate = sweep_rate(g, o, 1_000_000)
-    h = st["e_hist"]
-    mean_e = (U * st["count"] - st["sum_us"]) / (st["count"] * (U - L))
-    out["config2_inception_v3_training"] = {
-        "tac_seconds": round(tac_s, 6), "tac_makespan_us": m_tac,
-        "tac_E": (U - m_tac) / (U - L), "random_orders": st["count"], "sims_per_s": rate,
-        "min_us": st["min_us"], "argmin_seed": st["argmin_seed"], "mean_E": mean_e,
-        "E_hist_nonzero_bins": int((h > 0).sum()), "E_best_bin": int(max(i for i in range(1000) if h[i]))}
+    # config 2: Inception-v3 training — TAC + 1M random orders, E histogram,
+    # on the survey's backbone DAG and on the branchy Inception-style one
+    out.update(config2(lib, "inception_v3_training"))
+    out.update(config2(lib, "inception_v3_training_branchy"))
     # config 3: VGG-16 training, 4 workers / 1 PS — straggler spread
     v = lib.model("vgg16_training", 1).expand(4, 1, 0)
     o = v.declared()
@@ -356,9 +479,11 @@ def other_configs(lib):
     strag_tic = json.loads(r_tic.iteration_json())["straggler"]
     out["config3_vgg16_4workers"] = {
         "random_orders": st["count"], "sims_per_s": rate, "workers": st["n_workers"],
+        "path": v.sweep_path(o)["path"],
         "straggler_mean": st["straggler_sum"] / st["count"],
         "straggler_max_bin": int(max(i for i in range(1000) if sh[i])),
-        "iteration_min_us": st["min_us"], "iteration_max_us": st["max_us"],
+        "makespan_min_us": st["min_us"], "makespan_max_us": st["max_us"],
+        "iteration_min_us": st["iter_min_us"], "iteration_max_us": st["iter_max_us"],
         "tic_common_order_straggler": strag_tic}
     # batched brute force: all R! orders on the device
     bf = {}
@@ -376,22 +501,19 @@ def other_configs(lib):
 
 
 def run_reference(args, rank, world):
-    """--impl reference: the reference's CPU path, rank 0 only."""
+    """--impl reference: the reference library's own per-seed loop (oracle/_ref,
+    compiled from /root/reference; this library is never loaded) on the host
+    cores, rank 0 only, on the same committed DAG and config."""
     if rank != 0:
         return
-    from paper_1803_03288_b200 import capi
-    lib = capi.Lib()
-    g, path = graph_files(lib, MODEL)
+    path = graph_file(MODEL)
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle
     cores = os.cpu_count() or 1
     base = {"metric": "recv-order makespan sims/sec", "unit": "sims/s", "impl": "reference",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
-            "scaling": "weak", "dtype": "int64", "data": "synthetic",
-            "config": {"workload": f"config4: {MODEL} DAG seed 1 ({g.op_count()} ops / {g.edge_count()} edges / "
-                                   f"{g.recv_count()} recvs), random recv orders, gated, choice_seed=seed; "
-                                   f"min/argmin (reference library on the host cores: a bounded sample of "
-                                   f"the seed range per step, see cpu_baseline.sample)"}}
+            "scaling": "strong" if world > 1 else "weak", "dtype": "int64", "data": "synthetic",
+            "config": workload_config(world)}
     if not oracle.ref_available():
         base["unavailable"] = "oracle/_ref (reference build) missing"
         emit(base)
@@ -410,7 +532,8 @@ def run_reference(args, rank, world):
     base.update({"value": v, "ms_per_step": 1000 * secs / args.steps, "vs_baseline": None,
                  "cpu_baseline": {"value": v, "unit": "sims/s", "cores": cores, "kind": "reference",
                                   "nproc": os.cpu_count(), "cpu_model": cpu_model(),
-                                  "sample": f"{per_step} seeds per step, {cores} threads"},
+                                  "sample": f"{per_step} seeds per step (a bounded sample of the {COUNT}-order "
+                                            f"step), {cores} threads, oracle/_ref libcommsched -O3"},
                  "e2e": {"value": v, "unit": "sims/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}})
     emit(base)
 
@@ -424,6 +547,35 @@ def emit(obj):
     os.write(_JSON_FD if _JSON_FD is not None else 1, (json.dumps(obj) + "\n").encode())
 
 
+def timed_steps(step, steps, world, stream, flush):
+    """K timed steps (CUDA events on the launching stream), L2 flushed and a
+    barrier before each; returns the per-step times (ms)."""
+    import torch
+    import torch.distributed as dist
+    out = []
+    for _ in range(steps):
+        flush.fill_(1)  # L2 flush between timed steps (outside the timing)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        out.append(e0.elapsed_time(e1))
+    return out
+
+
+def max_over_ranks(x, world):
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return t.item()
+
+
 def main():
     global _JSON_FD
     sys.stdout.flush()
@@ -434,7 +586,6 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--count", type=int, default=COUNT)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-tac", action="store_true")
     ap.add_argument("--no-configs", action="store_true")
@@ -451,8 +602,11 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_1803_03288_b200 import capi
+    from paper_1803_03288_b200 import dist as pdist
     lib = capi.Lib()
-    g, path = graph_files(lib, MODEL)
+    text = bench_json(MODEL)
+    path = graph_file(MODEL)
+    g = lib.graph(text)
     o = g.declared()
     plan = capi.SweepPlan.create(g, o)
     info = plan.info()
@@ -461,88 +615,60 @@ def main():
     d_i64 = torch.zeros(capi.DSTATS_I64, dtype=torch.int64, device="cuda")
     d_f64 = torch.zeros(capi.DSTATS_F64, dtype=torch.float64, device="cuda")
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device="cuda")
-    from paper_1803_03288_b200 import dist as pdist
-    # Weak scaling: every rank sweeps its own 2^24-seed range (the seeds are
-    # independent units, no data-path exchange); total = N * 2^24 per step.
-    per_gpu = args.count
-    count = per_gpu * world
-    lo, n = SEED_LO + rank * per_gpu, per_gpu
-    slots = torch.zeros(2 * world, dtype=torch.int64, device="cuda")
-
-    def step(lo=lo, n=n):
-        plan.reset(sptr, d_i64.data_ptr(), d_f64.data_ptr())
-        k0.record(stream)
-        plan.run(lo, n, SEED_LO, sptr, None, d_i64.data_ptr(), d_f64.data_ptr())
-        k1.record(stream)
-        if world > 1:  # the step's one reduction (paper_1803_03288_b200/dist.py)
-            pdist.reduce_stats(d_i64, d_f64, rank, world, slots)
-
+    buf = torch.zeros(2 * world + capi.DSTATS_I64 + capi.DSTATS_F64 * world, dtype=torch.int64, device="cuda")
     k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    def make_step(lo, n):
+        def step():
+            plan.reset(sptr, d_i64.data_ptr(), d_f64.data_ptr())
+            k0.record(stream)
+            plan.run(lo, n, SEED_LO, sptr, None, d_i64.data_ptr(), d_f64.data_ptr())
+            k1.record(stream)
+            if world > 1:  # the step's one reduction (paper_1803_03288_b200/dist.py)
+                pdist.reduce_stats(d_i64, d_f64, rank, world, buf)
+        return step
+
+    # headline: config 4's fixed 2^24 orders, contiguous shards over the ranks
+    lo, n = pdist.shard(SEED_LO, COUNT, rank, world)
+    step = make_step(lo, n)
     for _ in range(max(3, args.warmup)):
         step()
     torch.cuda.synchronize()
-    step_ms, kern_ms = [], []
     launches0 = lib.launches()
+    kern_ms = []
     with ClockSampler(local) as clocks:
-        for _ in range(args.steps):
-            flush.fill_(1)  # L2 flush between timed steps (outside the timing)
-            if world > 1:
-                dist.barrier()
-            torch.cuda.synchronize()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
+        def kstep():
             step()
-            e1.record(stream)
-            torch.cuda.synchronize()
-            step_ms.append(e0.elapsed_time(e1))
+        step_ms = []
+        for _ in range(args.steps):
+            step_ms += timed_steps(kstep, 1, world, stream, flush)
             kern_ms.append(k0.elapsed_time(k1))
     launches = lib.launches() - launches0
-    h_i64 = d_i64.cpu().numpy()
-    h_f64 = d_f64.cpu().numpy()
-    stats = plan.finish(h_i64, h_f64, SEED_LO)
-    t_step = torch.tensor([sum(step_ms)], dtype=torch.float64, device="cuda")
-    t_kern = torch.tensor([sum(kern_ms)], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(t_step, op=dist.ReduceOp.MAX)
-        dist.all_reduce(t_kern, op=dist.ReduceOp.MAX)
-    ms_per_step = t_step.item() / args.steps
-    kern_per_step = t_kern.item() / args.steps
-    value = count / (ms_per_step / 1000.0)
+    stats = plan.finish(d_i64.cpu().numpy(), d_f64.cpu().numpy(), SEED_LO)
+    ms_per_step = max_over_ranks(sum(step_ms), world) / args.steps
+    kern_per_step = max_over_ranks(sum(kern_ms), world) / args.steps
+    value = COUNT / (ms_per_step / 1000.0)
 
-    # Strong-scaling view of config 4 (2^24 orders in total, split over the
-    # ranks), same timing rules, reported beside the weak-scaling headline.
-    strong = None
+    # weak view at N > 1: 2^24 orders per GPU
+    weak = None
     if world > 1:
-        slo, sn = pdist.shard(SEED_LO, per_gpu, rank, world)
+        wstep = make_step(SEED_LO + rank * COUNT, COUNT)
         for _ in range(3):
-            step(slo, sn)
+            wstep()
         torch.cuda.synchronize()
-        sms = []
-        for _ in range(args.steps):
-            flush.fill_(1)
-            dist.barrier()
-            torch.cuda.synchronize()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            step(slo, sn)
-            e1.record(stream)
-            torch.cuda.synchronize()
-            sms.append(e0.elapsed_time(e1))
-        ts = torch.tensor([sum(sms)], dtype=torch.float64, device="cuda")
-        dist.all_reduce(ts, op=dist.ReduceOp.MAX)
-        strong = {"total_orders": per_gpu, "ms_per_step": ts.item() / args.steps,
-                  "value": per_gpu / (ts.item() / args.steps / 1000.0), "unit": "sims/s"}
+        wms = max_over_ranks(sum(timed_steps(wstep, args.steps, world, stream, flush)), world) / args.steps
+        weak = {"orders_per_gpu": COUNT, "total_orders": COUNT * world, "ms_per_step": wms,
+                "value": COUNT * world / (wms / 1000.0), "unit": "sims/s"}
 
-    # e2e: the user path through the public C ABI with host buffers, like the
-    # reference arm (which parses the DAG once, then loops over seeds): the
-    # DAG is loaded once (cs_graph_parse); every step builds a fresh time
-    # oracle (cs_oracle_declared) and calls cs_sweep_random, which weights the
-    # graph's (cached) chain classes with that oracle's durations, uploads the
-    # tables, runs, and reads the statistics back; then the cross-rank
-    # reduction.
-    ge = lib.graph(g.serialize())
+    # e2e: the user path through the public C ABI with host buffers: the DAG
+    # is parsed once (cs_graph_parse, as the reference's CLI does); every step
+    # builds a fresh time oracle (cs_oracle_declared) and calls cs_sweep_random
+    # on the rank's shard, which weights the graph's cached analysis with the
+    # oracle's durations, uploads the tables, runs and reads the statistics
+    # back; then the cross-rank reduction of the host results.
+    ge = lib.graph(text)
     e2e_ms = []
-    for _ in range(max(1, min(3, args.steps))):
+    for _ in range(max(2, min(4, args.steps)) + 1):
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
@@ -553,88 +679,44 @@ def main():
             dist.all_reduce(hv[:1], op=dist.ReduceOp.MIN)
         hv.cpu()
         e2e_ms.append((time.perf_counter() - t0) * 1000)
-    e2e_t = torch.tensor([statistics.median(e2e_ms)], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
-    e2e_value = count / (e2e_t.item() / 1000.0)
-    # bytes crossing PCIe per e2e step (counted from the copies made):
-    # up: per-recv {first class, duration} (8R), class suffix weights
-    # 8(nc+1), Ctot and send total (16), bounded() limit/magic 16(R+2);
-    # down: the statistics buffers.
-    R, nc = info["recvs_per_worker"], info["classes"]
-    h2d = 8 * R + 8 * (nc + 1) + 16 + 16 * (R + 2)
+    e2e_t = max_over_ranks(statistics.median(e2e_ms[1:]), world)
+    e2e_value = COUNT / (e2e_t / 1000.0)
+    h2d = info["uploaded_bytes"]  # tables and images uploaded per call (counted by the plan builder)
     d2h = 8 * capi.DSTATS_I64 + 8 * capi.DSTATS_F64
 
     clocks_summary = clocks.summary()
     if rank == 0:
         hbm, peak_src = peaks()
-        bsim = b_sim(info)
-        achieved = bsim * count / world / (kern_per_step / 1000.0) / 1e9  # per GPU
-        traffic, issue = None, None
-        prof = os.path.join(ROOT, "profiles", "sweep_ncu_summary.json")
-        if os.path.exists(prof):
-            try:
-                ps = json.load(open(prof))
-                # ncu dram bytes scaled to this launch's orderings
-                traffic = ps["dram_bytes_per_launch"] * (count / world) / ps["orderings"]
-                ipo = ps["warp_instructions_per_ordering"]
-                mhz = clocks_summary.get("sm_mhz") or ps.get("sm_mhz") or 1965.0
-                peak_issue = 148 * 4 * mhz * 1e6
-                ach = ipo * (count / world) / (kern_per_step / 1000.0)
-                issue = {"bound": "issue", "achieved": ach, "peak": peak_issue, "unit": "warp-inst/s",
-                         "frac": ach / peak_issue, "warp_inst_per_order": ipo,
-                         "source": "instructions per ordering from profiles/sweep_ncu_summary.json (ncu), "
-                                   "time from this run's CUDA events, peak = 148 SMs x 4 schedulers x SM clock"}
-            except Exception:
-                traffic = None
-        # SURVEY §8d's secondary roofline: B_sim per ordering against shared
-        # memory bandwidth (148 SMs x 128 B/clk x SM clock under load)
         mhz = clocks_summary.get("sm_mhz") or 1965.0
-        smem_peak = 148 * 128 * mhz * 1e6 / 1e9
-        smem_roof = {"bound": "smem", "achieved": achieved, "peak": smem_peak, "unit": "GB/s",
-                     "frac": achieved / smem_peak, "algorithmic_bytes_per_order": bsim,
-                     "note": "SURVEY §8d secondary: B_sim x orderings/s against 148 x 128 B/clk x SM clock; "
-                             "the kernel's measured shared-memory traffic is lower (ncu smem wavefronts "
-                             "in profiles/sweep_ncu_summary.json), its binding limit is issue (roofline_issue)"}
-        try:
-            smem_roof["ncu_smem_wavefronts_pct"] = json.load(
-                open(os.path.join(ROOT, "profiles", "sweep_ncu_summary.json")))["smem_wavefronts_pct"]
-        except Exception:
-            pass
+        per_gpu_rate = (COUNT / world) / (kern_per_step / 1000.0)
+        summary = ncu_summary("sweep_ncu_summary.json")
+        roof = issue_roofline(summary, per_gpu_rate, mhz, COUNT / world)
         out = {
             "metric": "recv-order makespan sims/sec", "value": value, "unit": "sims/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
-            "data": "synthetic",
-            "config": {"workload": f"config4: {MODEL} DAG seed 1 ({info['ops']} ops / {info['edges']} edges / "
-                                   f"{R} recvs, {nc} chain classes), {per_gpu} random recv orders per GPU "
-                                   f"per step ({count} total, seeds 1..{count}), gated, choice_seed=seed; "
-                                   f"min/argmin + E histogram",
-                       "parallelism": f"contiguous seed ranges x{world}, one NCCL reduction per step",
-                       "l2": "flushed between steps (256 MiB write)",
-                       "U_us": info["U_us"], "L_us": info["L_us"]},
-            "strong_scaling_2p24": strong,
+            "higher_is_better": True, "scaling": "strong" if world > 1 else "weak", "vs_baseline": None,
+            "dtype": "int64", "data": "synthetic",
+            "config": workload_config(world),
             "gpu_launches": launches,  # this library's kernels inside the timed region (all K steps)
             "gpu_launches_per_step": launches // max(1, args.steps),
             "kernel_ms_per_step": kern_per_step,
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                         "frac": achieved / hbm, "traffic": traffic, "peak_source": peak_src,
-                         "algorithmic_bytes_per_order": bsim,
-                         "note": "achieved = SURVEY §8d's B_sim = 12R+2V+2E+16 bytes per ordering x "
-                                 "orderings / kernel time (per GPU). The fused kernel keeps every "
-                                 "per-ordering byte on chip (traffic = measured DRAM bytes, ~0), so the "
-                                 "HBM-equivalent frac exceeds 1; the binding roofline is instruction "
-                                 "issue, reported in roofline_issue (ncu: DRAM ~0%, ALU pipe ~72%)"},
+            "roofline": roof,
+            "roofline_hbm": hbm_roofline(b_sim(info), per_gpu_rate, hbm, peak_src),
+            "roofline_smem": {"bound": "smem", "achieved": b_sim(info) * per_gpu_rate / 1e9,
+                              "peak": 148 * 128 * mhz * 1e6 / 1e9, "unit": "GB/s",
+                              "frac": b_sim(info) * per_gpu_rate / (148 * 128 * mhz * 1e6),
+                              "note": "SURVEY §8d secondary: B_sim against 148 SMs x 128 B/clk x SM clock"},
             "e2e": {"value": e2e_value, "unit": "sims/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "ms_per_step": e2e_t.item(),
-                    "call": "per step: cs_oracle_declared + cs_sweep_random (per-oracle tables built and uploaded, statistics read back to the host); DAG parsed once"},
+                    "ms_per_step": e2e_t,
+                    "call": "per step: cs_oracle_declared + cs_sweep_random on the rank's shard (per-oracle tables "
+                            "built and uploaded, statistics read back to the host); DAG parsed once"},
             "result": {"min_us": stats["min_us"], "argmin_seed": stats["argmin_seed"],
                        "max_us": stats["max_us"], "mean_us": stats["sum_us"] / max(1, stats["count"]),
                        "count_checked": int(stats["count"])},
             "clocks": clocks_summary,
-            "roofline_issue": issue,
-            "roofline_smem": smem_roof,
         }
+        if weak:
+            out["weak_scaling"] = weak
         if not args.no_tac:
             (out["tac_seconds"], out["tac_roofline"], out["tic_amended_seconds"],
              out["tic_roofline"]) = tac_times(lib, top=args.config5_top, hbm=hbm)
@@ -644,7 +726,9 @@ def main():
                                    "NVLink peer-flag round trip 2.6 us; profiles/r01_cross_gpu_latency.json) "
                                    "on rounds of 1.3-6.3 us; DESIGN.md section 5")
         if not args.no_configs and world == 1:
-            out["configs"] = other_configs(lib)
+            out["configs"] = {"dag_branchy_config4": dag_config4(lib, hbm, peak_src, mhz, stream, d_i64, d_f64,
+                                                                 flush)}
+            out["configs"].update(other_configs(lib))
             out["configs"].update(exact_paths(lib, path))
             out["configs"]["single_report_simulate_json"] = single_report(lib)
         if not args.no_cpu and world == 1:

@@ -109,6 +109,8 @@ SweepPlan* csk_sweep_plan_dag(int32_t W, int32_t R, const int64_t* d, const int6
                               const int64_t* send_total, int cluster, int64_t U, int64_t L,
                               uint64_t noise_thr, char* err);
 void csk_sweep_plan_free(SweepPlan* p);
+/* Host-to-device bytes the plan's construction copied (tables, images). */
+int64_t csk_sweep_plan_uploaded(const SweepPlan* p);
 /* Stats layout documented in include/commsched.h (CS_DSTATS_*). */
 int csk_sweep_reset(SweepPlan* p, void* stream, int64_t* d_i64, double* d_f64, char* err);
 int csk_sweep_run(SweepPlan* p, uint64_t seed_lo, int64_t count, uint64_t key_base,

@@ -835,6 +835,7 @@ struct SweepPlan {
   // shared-memory item width (1: R <= 255, else 2)
   int dag = 0, J = 0, Ls = 0, tb = 1;
   int blocks_orders = 0;
+  size_t uploaded = 0;  // host->device bytes copied when the plan was built
 };
 
 using DagFn = void (*)(ChainArgs, DagArgs);
@@ -890,6 +891,7 @@ extern "C" SweepPlan* csk_sweep_plan(int32_t W, int32_t R, int32_t nc, const int
   for (int n = 0; n <= R + 1; ++n) bounded_consts(static_cast<uint64_t>(n), &lim[n], &mag[n]);
   auto up = [&](void** dst, const void* src, size_t bytes) {
     if (cudaMalloc(dst, bytes ? bytes : 8) != cudaSuccess) return false;
+    p->uploaded += bytes;
     return bytes == 0 || cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice) == cudaSuccess;
   };
   if (!up(&p->tab, tab.data(), tab.size() * sizeof(uint2)) ||
@@ -1020,6 +1022,7 @@ extern "C" SweepPlan* csk_sweep_plan_dag(int32_t W, int32_t R, const int64_t* d,
   for (int w = 0; w < W; ++w) put(w0[w]);
   auto up = [&](void** dst, const void* src, size_t bytes) {
     if (cudaMalloc(dst, bytes ? bytes : 8) != cudaSuccess) return false;
+    p->uploaded += bytes;
     return bytes == 0 || cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice) == cudaSuccess;
   };
   if (!up(&p->blob, img.data(), img.size()) || !up(&p->ctot, ctot.data(), sizeof(int64_t) * W) ||
@@ -1049,6 +1052,8 @@ extern "C" SweepPlan* csk_sweep_plan_dag(int32_t W, int32_t R, const int64_t* d,
   p->blocks_orders = sms * occ_o;
   return p;
 }
+
+extern "C" int64_t csk_sweep_plan_uploaded(const SweepPlan* p) { return static_cast<int64_t>(p->uploaded); }
 
 extern "C" void csk_sweep_plan_free(SweepPlan* p) {
   if (!p) return;

@@ -753,6 +753,7 @@ int cs_sweep_plan_info(const cs_sweep_plan* p, char** out_json) {
     j["L_us"] = c.L;
     j["cluster"] = c.cluster;
     j["key_bits"] = csk_key_bits(c.U);
+    j["uploaded_bytes"] = csk_sweep_plan_uploaded(c.plan);
     *out_json = dup(dump_doc(j));
   });
 }
