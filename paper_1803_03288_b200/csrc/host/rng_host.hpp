@@ -1,6 +1,8 @@
-// Host RNG for the input builders only (graph generators). The hot-path
-// streams (random orders, simulator choices, reorder noise) are generated on
-// the device by ../device/mt64.cuh with the same definitions.
+// Host RNG (rng.hpp:14-54): the input builders (graph generators) and the
+// reorder-noise swaps of single closed-form simulations (apply_gate_noise,
+// hotpath.cpp). The batched streams (random orders, simulator choices, noise
+// per seed) are generated on the device by ../device/common.cuh with the
+// same definitions.
 #pragma once
 
 #include <cstdint>
