@@ -313,14 +313,19 @@ __device__ __forceinline__ void mt_outputs(uint64_t seed, int n, F&& use) {
 // straggler histogram in shared memory; reduced per warp, then one set of
 // global atomics per block (flush).
 struct StatAcc {
-  unsigned long long kmin = ~0ULL, kmax = 0;
-  long long msum = 0, cnt = 0;
+  unsigned long long kmin = ~0ULL, kmax = 0, ikmin = ~0ULL, ikmax = 0;  // makespan / iteration-time keys
+  long long msum = 0, cnt = 0, isum = 0;
   double sq = 0.0, ssum = 0.0;
   __device__ __forceinline__ void add(const ChainArgs& a, uint64_t seed, int64_t m, int64_t hi, int64_t lo,
                                       int* s_hist, int* s_shist) {
     const unsigned long long off = seed - a.key_base;
     kmin = min(kmin, (static_cast<unsigned long long>(m) << a.key_bits) | off);
     kmax = max(kmax, (static_cast<unsigned long long>(m) << a.key_bits) | ((1ULL << a.key_bits) - 1 - off));
+    if (a.cluster) {  // iteration time = slowest worker (differs from m when PS ops take time)
+      ikmin = min(ikmin, (static_cast<unsigned long long>(hi) << a.key_bits) | off);
+      ikmax = max(ikmax, (static_cast<unsigned long long>(hi) << a.key_bits) | ((1ULL << a.key_bits) - 1 - off));
+      isum += hi;
+    }
     msum += m;
     ++cnt;
     sq += static_cast<double>(m) * static_cast<double>(m);
@@ -344,6 +349,9 @@ struct StatAcc {
     for (int o = 16; o; o >>= 1) {
       kmin = min(kmin, __shfl_xor_sync(~0u, kmin, o));
       kmax = max(kmax, __shfl_xor_sync(~0u, kmax, o));
+      ikmin = min(ikmin, __shfl_xor_sync(~0u, ikmin, o));
+      ikmax = max(ikmax, __shfl_xor_sync(~0u, ikmax, o));
+      isum += __shfl_xor_sync(~0u, isum, o);
       msum += __shfl_xor_sync(~0u, msum, o);
       cnt += __shfl_xor_sync(~0u, cnt, o);
       sq += __shfl_xor_sync(~0u, sq, o);
@@ -355,6 +363,11 @@ struct StatAcc {
       atomicMax(&a.i64[1], kmax);
       atomicAdd(&a.i64[2], static_cast<unsigned long long>(msum));
       atomicAdd(&a.i64[3], static_cast<unsigned long long>(cnt));
+      if (a.cluster) {
+        atomicMin(&a.i64[4], ikmin);
+        atomicMax(&a.i64[5], ikmax);
+        atomicAdd(&a.i64[6], static_cast<unsigned long long>(isum));
+      }
       atomicAdd(&a.f64[0], sq);
       atomicAdd(&a.f64[1], ssum);
     }
@@ -734,6 +747,298 @@ __global__ void __launch_bounds__(kDagThreads) dag_sweep_kernel(ChainArgs a, Dag
   acc.flush(a, s_hist, s_shist);
 }
 
+// ---- clusters whose parameter-server ops take time ----------------------
+//
+// With PS ops of positive duration the full makespan depends on the order in
+// which each worker's channel sends its gradients, which the reference picks
+// with draws from the run's shared choice stream (sim.cpp:163-186: the sends
+// are unprioritized, so every ready send is a candidate), and on the PS
+// server's choices among ready PS ops (again draws). Everything before a
+// worker's last compute op completes is still SURVEY A.2: on chain-class
+// workers whose compute ops are totally ordered there are no draws there
+// (one candidate at a time on the core; the channel admits only the next
+// recv in gate order, the sends are not ready yet), the recv completions are
+// prefix sums of the gate order and the release of the sends is the fold's
+// T_cpu. So a run is: per worker the shuffle and the fold (as above), then an
+// exact replica of sim.cpp:194-233 restricted to the resources that can draw
+// — the PS core and each worker's channel after its release — with the
+// reference's round structure (completions at t, then passes of try_start in
+// resource order + same-time completions of zero-duration ops until nothing
+// changes). Candidates come in op-index order: a channel's are its unsent
+// ready sends plus the next recv in gate order (the only admitted one),
+// the PS core's are its ready ops. Host checks (csrc/host/sweep.cpp): one PS
+// device with one compute unit fed only by sends, workers as above, the
+// worker's last compute op of positive duration (its completion, hence the
+// release of the sends, happens at the start of a time step).
+struct PsArgs {
+  int S, Q, ps_slot;
+  int sw, qw;                     // 32-bit words of a send bitset / a PS-op bitset
+  const int16_t* recv_sb;         // [R] sends before recv column c in channel order
+  const int64_t* send_d;          // [W][S]
+  const int32_t* send_succ_off;   // [W*S + 1]
+  const int16_t* send_succ;       // PS op indices
+  const int64_t* ps_d;            // [Q]
+  const uint8_t* ps_missing;      // [Q] predecessor counts
+  const int32_t* ps_succ_off;     // [Q + 1]
+  const int16_t* ps_succ;
+};
+constexpr int kPsThreads = 64;
+
+// per thread: gate orders (W x R items), pending-send bits (W x sw words),
+// PS missing counts (Q bytes), PS ready bits (qw words), worker scalars
+// (9 words each)
+__host__ __device__ inline size_t ps_thread_bytes(int W, int R, int S, int Q, size_t tb) {
+  const int per = tb == 1 ? 4 : 2;
+  return 4 * (static_cast<size_t>(W) * ((R + per - 1) / per) + static_cast<size_t>(W) * ((S + 31) / 32) +
+              static_cast<size_t>((Q + 3) / 4) + static_cast<size_t>((Q + 31) / 32) + 9 * static_cast<size_t>(W));
+}
+
+template <typename T, typename V, bool kNoisy>
+__global__ void __launch_bounds__(kPsThreads) cluster_ps_kernel(ChainArgs a, PsArgs q) {
+  constexpr int NT = kPsThreads;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int R = a.R, W = a.W, S = q.S, Q = q.Q;
+  uint64_t* s_lim = reinterpret_cast<uint64_t*>(smem);
+  const int nk = max(S + 2, Q + 1) + 1;  // bounded() constants for n < nk
+  uint64_t* s_mag = s_lim + nk;
+  uint2* s_tab = reinterpret_cast<uint2*>(s_mag + nk);
+  V* s_pw = reinterpret_cast<V*>(s_tab + W * R);
+  int* s_hist = reinterpret_cast<int*>(smem + round16(16ull * nk + 8ull * W * R + sizeof(V) * W * a.stride));
+  const int nhist = (a.do_e ? 1 : 0) + 1;
+  int* s_shist = s_hist + (a.do_e ? kBins : 0);
+  uint32_t* col = reinterpret_cast<uint32_t*>(s_hist + nhist * kBins) + threadIdx.x;  // this thread's column
+  const int gw = Items<T, NT>::words(R);
+  auto gate = [&](int w) { return Items<T, NT>{col + static_cast<size_t>(w) * gw * NT}; };
+  uint32_t* pend = col + static_cast<size_t>(W) * gw * NT;        // [w][sw] words
+  uint32_t* qmiss_base = pend + static_cast<size_t>(W) * q.sw * NT;  // Q bytes
+  const Items<uint8_t, NT> qmiss{qmiss_base};
+  uint32_t* qready = qmiss_base + static_cast<size_t>((Q + 3) / 4) * NT;  // qw words
+  uint32_t* wsc = qready + static_cast<size_t>(q.qw) * NT;                // [w][9] words
+  // per-worker int64 fields (f: 0 release time T, 1 channel end, 2 device end)
+  // as two 32-bit halves at word offsets 9w + 2f, 9w + 2f + 1
+  auto ld64 = [&](int w, int f) -> int64_t {
+    const uint32_t lo = wsc[static_cast<size_t>(9 * w + 2 * f) * NT];
+    const uint32_t hi = wsc[static_cast<size_t>(9 * w + 2 * f + 1) * NT];
+    return static_cast<int64_t>((static_cast<uint64_t>(hi) << 32) | lo);
+  };
+  auto st64 = [&](int w, int f, int64_t v) {
+    wsc[static_cast<size_t>(9 * w + 2 * f) * NT] = static_cast<uint32_t>(v);
+    wsc[static_cast<size_t>(9 * w + 2 * f + 1) * NT] = static_cast<uint32_t>(static_cast<uint64_t>(v) >> 32);
+  };
+  auto i32 = [&](int w, int f) -> int32_t& {  // f: 0 running (-1 idle, -2 recv, s send), 1 next recv, 2 released
+    return *reinterpret_cast<int32_t*>(&wsc[static_cast<size_t>(9 * w + 6 + f) * NT]);
+  };
+  uint64_t* tables_ready = reinterpret_cast<uint64_t*>(smem + a.mbar_off);
+  if (threadIdx.x == 0) mbar_init(tables_ready, 1);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    mbar_expect_tx(tables_ready, a.blob_bytes);
+    bulk_g2s(smem, a.blob, a.blob_bytes, tables_ready);
+  }
+  for (int k = threadIdx.x; k < nhist * kBins; k += blockDim.x) s_hist[k] = 0;
+  mbar_wait(tables_ready, 0);
+  __syncthreads();
+  const int16_t* recv_sb = q.recv_sb;
+
+  StatAcc acc;
+  const int64_t nthreads = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; idx < a.count;
+       idx += nthreads) {
+    const uint64_t seed = a.seed_lo + static_cast<uint64_t>(idx);
+    NoiseState<kNoisy> noise;
+    if constexpr (kNoisy) noise.init(splitmix64(seed ^ kNoiseSalt));
+    int64_t t = INT64_MAX, mk = 0;
+    // 1. per worker: gate order, T_cpu (fold), channel state at the release
+    for (int w = 0; w < W; ++w) {
+      const Items<T, NT> g = gate(w);
+      const uint2* tab = s_tab + w * R;
+      const V* pw = s_pw + w * a.stride;
+      const V ctot = static_cast<V>(a.ctot[w]);
+      FoldT<V> f{a.nc, 0, -1};
+      const uint64_t ws = splitmix64(seed ^ (kPhi * static_cast<uint64_t>(w + 1)));
+      shuffle_fold<Items<T, NT>, V, true>(ws, R, g, f, tab, ctot, pw, s_lim, s_mag);
+      if constexpr (kNoisy)
+        for (int pos = 1; pos < R; ++pos)
+          if ((noise.m.next() >> 11) < a.noise_thr) {
+            T* p0 = g.at(pos - 1);
+            T* p1 = g.at(pos);
+            const T x = *p0;
+            *p0 = *p1;
+            *p1 = x;
+          }
+      for (int pos = R - 1; pos >= 0; --pos) f.add(tab[*g.at(pos)], ctot, pw);
+      if (f.G > 0) f.best = max(f.best, pw[0]);
+      const int64_t T0 = f.best < 0 ? 0 : static_cast<int64_t>(f.best);
+      // recvs starting before T0 ran back to back before the release
+      int64_t c = 0;
+      int k = 0;
+      for (; k < R && c < T0; ++k) c += static_cast<int64_t>(tab[*g.at(k)].y);
+      const bool busy = k > 0 && c > T0;  // position k-1 still running at T0
+      st64(w, 0, T0);
+      st64(w, 1, busy ? c : 0);
+      st64(w, 2, busy ? c : T0);
+      i32(w, 0) = busy ? -2 : -1;
+      i32(w, 1) = k;
+      i32(w, 2) = 0;
+      mk = max(mk, busy ? c : T0);
+      t = min(t, T0);
+      for (int x = 0; x < q.sw; ++x) pend[static_cast<size_t>(w * q.sw + x) * NT] = 0;
+    }
+    for (int x = 0; x < Q; ++x) *qmiss.at(x) = q.ps_missing[x];
+    for (int x = 0; x < q.qw; ++x) qready[static_cast<size_t>(x) * NT] = 0;
+    int ps_run = -1;
+    int64_t ps_end = 0;
+    MtStream choice;
+    choice.init(seed);
+    auto draw = [&](int n) -> int {  // bounded(n) of the shared choice stream
+      if (n < 2) return 0;
+      uint64_t v;
+      do v = choice.next();
+      while (v > s_lim[n]);
+      return static_cast<int>(fastmod32(v, static_cast<uint32_t>(n), s_mag[n]));
+    };
+    auto ps_complete = [&](int op) {
+      for (int e = q.ps_succ_off[op]; e < q.ps_succ_off[op + 1]; ++e) {
+        const int x = q.ps_succ[e];
+        uint8_t* m = qmiss.at(x);
+        if (--*m == 0) qready[static_cast<size_t>(x >> 5) * NT] |= 1u << (x & 31);
+      }
+    };
+    auto chan_complete = [&](int w) {
+      const int sid = i32(w, 0);
+      i32(w, 0) = -1;
+      if (sid < 0) return;  // a recv: nothing downstream after the release
+      const int base = w * S + sid;
+      for (int e = q.send_succ_off[base]; e < q.send_succ_off[base + 1]; ++e) {
+        const int x = q.send_succ[e];
+        uint8_t* m = qmiss.at(x);
+        if (--*m == 0) qready[static_cast<size_t>(x >> 5) * NT] |= 1u << (x & 31);
+      }
+    };
+    auto ps_try = [&]() -> bool {
+      if (ps_run >= 0) return false;
+      int n = 0;
+      for (int x = 0; x < q.qw; ++x) n += __popc(qready[static_cast<size_t>(x) * NT]);
+      if (n == 0) return false;
+      int j = draw(n);
+      for (int x = 0;; ++x) {
+        uint32_t bits = qready[static_cast<size_t>(x) * NT];
+        const int cnt = __popc(bits);
+        if (j < cnt) {
+          const int b = nth_bit(bits, j);
+          qready[static_cast<size_t>(x) * NT] = bits & ~(1u << b);
+          ps_run = (x << 5) + b;
+          ps_end = t + q.ps_d[ps_run];
+          mk = max(mk, ps_end);
+          return true;
+        }
+        j -= cnt;
+      }
+    };
+    auto chan_try = [&](int w) -> bool {
+      if (!i32(w, 2) || i32(w, 0) != -1) return false;
+      const int nr = i32(w, 1);
+      const Items<T, NT> g = gate(w);
+      const int rc = nr < R ? static_cast<int>(*g.at(nr)) : -1;  // next recv column (admitted)
+      uint32_t* pw_ = pend + static_cast<size_t>(w * q.sw) * NT;
+      int ns = 0;
+      for (int x = 0; x < q.sw; ++x) ns += __popc(pw_[static_cast<size_t>(x) * NT]);
+      const int n = ns + (rc >= 0 ? 1 : 0);
+      if (n == 0) return false;
+      int j = draw(n);
+      int64_t d;
+      if (rc >= 0) {  // the recv's place among the candidates: pending sends before it
+        const int sb = recv_sb[rc];
+        int before = 0;
+        for (int x = 0; x < (sb >> 5); ++x) before += __popc(pw_[static_cast<size_t>(x) * NT]);
+        if (sb & 31) before += __popc(pw_[static_cast<size_t>(sb >> 5) * NT] & ((1u << (sb & 31)) - 1u));
+        if (j == before) {
+          i32(w, 0) = -2;
+          i32(w, 1) = nr + 1;
+          d = static_cast<int64_t>(s_tab[w * R + rc].y);
+          goto started;
+        }
+        if (j > before) --j;
+      }
+      for (int x = 0;; ++x) {
+        uint32_t bits = pw_[static_cast<size_t>(x) * NT];
+        const int cnt = __popc(bits);
+        if (j < cnt) {
+          const int b = nth_bit(bits, j);
+          pw_[static_cast<size_t>(x) * NT] = bits & ~(1u << b);
+          const int sid = (x << 5) + b;
+          i32(w, 0) = sid;
+          d = q.send_d[w * S + sid];
+          break;
+        }
+        j -= cnt;
+      }
+    started:
+      const int64_t e = t + d;
+      st64(w, 1, e);
+      if (e > ld64(w, 2)) st64(w, 2, e);
+      mk = max(mk, e);
+      return true;
+    };
+    // 2. the send phase: sim.cpp:194-233 over the PS core and the released channels
+    while (t != INT64_MAX) {
+      // completions at t (positive durations: the op started before t)
+      if (ps_run >= 0 && ps_end == t) {
+        const int op = ps_run;
+        ps_run = -1;
+        ps_complete(op);
+      }
+      for (int w = 0; w < W; ++w) {
+        if (!i32(w, 2) && ld64(w, 0) == t) {  // last compute op done: the sends are ready
+          i32(w, 2) = 1;
+          uint32_t* pw_ = pend + static_cast<size_t>(w * q.sw) * NT;
+          for (int x = 0; x < q.sw; ++x) {
+            const int lo = x << 5;
+            pw_[static_cast<size_t>(x) * NT] = S - lo >= 32 ? ~0u : ((1u << (S - lo)) - 1u);
+          }
+        }
+        if (i32(w, 0) != -1 && ld64(w, 1) == t) chan_complete(w);
+      }
+      bool progress = true;
+      while (progress) {  // passes: try_start in resource order, then same-time completions
+        progress = false;
+        for (int i = 0; i <= W; ++i) {
+          if (i == q.ps_slot) progress = ps_try() || progress;
+          if (i < W) progress = chan_try(i) || progress;
+        }
+        if (ps_run >= 0 && ps_end == t) {
+          const int op = ps_run;
+          ps_run = -1;
+          ps_complete(op);
+          progress = true;
+        }
+        for (int w = 0; w < W; ++w)
+          if (i32(w, 0) != -1 && ld64(w, 1) == t) {
+            chan_complete(w);
+            progress = true;
+          }
+      }
+      int64_t nt = INT64_MAX;
+      if (ps_run >= 0) nt = ps_end;
+      for (int w = 0; w < W; ++w) {
+        if (!i32(w, 2)) nt = min(nt, ld64(w, 0));
+        if (i32(w, 0) != -1) nt = min(nt, ld64(w, 1));
+      }
+      t = nt;
+    }
+    int64_t hi = 0, lo = INT64_MAX;
+    for (int w = 0; w < W; ++w) {
+      const int64_t mw = ld64(w, 2);
+      if (a.worker_ms) a.worker_ms[idx * W + w] = mw;
+      hi = max(hi, mw);
+      lo = min(lo, mw);
+    }
+    if (a.makespans) a.makespans[idx] = mk;
+    acc.add(a, seed, mk, hi, lo, s_hist, s_shist);
+  }
+  acc.flush(a, s_hist, s_shist);
+}
+
 // Brute force (metrics.cpp:37-72) on the closed form: permutation number k
 // in lexicographic order of the recv columns (std::next_permutation order
 // over ascending ids) is unranked in the factorial number system into a
@@ -773,7 +1078,7 @@ __global__ void __launch_bounds__(kSweepThreads) lex_kernel(ChainArgs a, int64_t
 }
 
 __global__ void reset_kernel(unsigned long long* i64, double* f64) {
-  for (int k = threadIdx.x; k < 2008; k += blockDim.x) i64[k] = k == 0 ? ~0ULL : 0ULL;
+  for (int k = threadIdx.x; k < 2008; k += blockDim.x) i64[k] = (k == 0 || k == 4) ? ~0ULL : 0ULL;
   if (threadIdx.x < 2) f64[threadIdx.x] = 0.0;
 }
 
@@ -835,6 +1140,12 @@ struct SweepPlan {
   // shared-memory item width (1: R <= 255, else 2)
   int dag = 0, J = 0, Ls = 0, tb = 1;
   int blocks_orders = 0;
+  // cluster send phase (cluster_ps_kernel): device tables and its own image
+  int ps = 0, ps_blocks = 0;
+  PsArgs psa{};
+  void* ps_blob = nullptr;
+  size_t ps_blob_bytes = 0, ps_smem = 0;
+  std::vector<void*> ps_bufs;
   size_t uploaded = 0;  // host->device bytes copied when the plan was built
 };
 
@@ -1053,12 +1364,112 @@ extern "C" SweepPlan* csk_sweep_plan_dag(int32_t W, int32_t R, const int64_t* d,
   return p;
 }
 
+using PsFn = void (*)(ChainArgs, PsArgs);
+static PsFn ps_fn(const SweepPlan* p) {
+  const bool noisy = p->noise_thr != 0;
+  if (p->R <= 256) {
+    if (noisy) return p->narrow ? cluster_ps_kernel<uint8_t, int32_t, true> : cluster_ps_kernel<uint8_t, int64_t, true>;
+    return p->narrow ? cluster_ps_kernel<uint8_t, int32_t, false> : cluster_ps_kernel<uint8_t, int64_t, false>;
+  }
+  if (noisy) return p->narrow ? cluster_ps_kernel<uint16_t, int32_t, true> : cluster_ps_kernel<uint16_t, int64_t, true>;
+  return p->narrow ? cluster_ps_kernel<uint16_t, int32_t, false> : cluster_ps_kernel<uint16_t, int64_t, false>;
+}
+
+extern "C" int csk_sweep_plan_add_ps(SweepPlan* p, int32_t S, const int16_t* recv_sb, const int64_t* send_d,
+                                     const int32_t* send_succ_off, const int16_t* send_succ, int32_t Q,
+                                     const int64_t* ps_d, const uint8_t* ps_missing, const int32_t* ps_succ_off,
+                                     const int16_t* ps_succ, int32_t ps_slot, char* err) {
+  if (p->dag || !p->cluster) {
+    std::snprintf(err, 256, "the send phase extends cluster chain plans only");
+    return 4;
+  }
+  const int W = p->W, R = p->R;
+  auto up = [&](const void* src, size_t bytes) -> void* {
+    void* d = nullptr;
+    if (cudaMalloc(&d, bytes ? bytes : 8) != cudaSuccess) return nullptr;
+    p->ps_bufs.push_back(d);
+    p->uploaded += bytes;
+    if (bytes && cudaMemcpy(d, src, bytes, cudaMemcpyHostToDevice) != cudaSuccess) return nullptr;
+    return d;
+  };
+  PsArgs& a = p->psa;
+  a.S = S;
+  a.Q = Q;
+  a.ps_slot = ps_slot;
+  a.sw = (S + 31) / 32;
+  a.qw = (Q + 31) / 32;
+  const int32_t nss = send_succ_off[W * S], nqs = ps_succ_off[Q];
+  a.recv_sb = static_cast<const int16_t*>(up(recv_sb, 2ull * R));
+  a.send_d = static_cast<const int64_t*>(up(send_d, 8ull * W * S));
+  a.send_succ_off = static_cast<const int32_t*>(up(send_succ_off, 4ull * (W * S + 1)));
+  a.send_succ = static_cast<const int16_t*>(up(send_succ, 2ull * nss));
+  a.ps_d = static_cast<const int64_t*>(up(ps_d, 8ull * Q));
+  a.ps_missing = static_cast<const uint8_t*>(up(ps_missing, static_cast<size_t>(Q)));
+  a.ps_succ_off = static_cast<const int32_t*>(up(ps_succ_off, 4ull * (Q + 1)));
+  a.ps_succ = static_cast<const int16_t*>(up(ps_succ, 2ull * nqs));
+  for (void* x : p->ps_bufs)
+    if (!x) {
+      std::snprintf(err, 256, "CUDA allocation for the send-phase tables failed");
+      return 1;
+    }
+  // shared-memory image: bounded() constants (n < nk), the chain tables
+  const int nk = std::max(S + 2, Q + 1) + 1;
+  const size_t vb = p->narrow ? 4 : 8;
+  std::vector<uint64_t> lim(nk), mag(nk);
+  for (int n = 0; n < nk; ++n) bounded_consts(static_cast<uint64_t>(n), &lim[n], &mag[n]);
+  std::vector<uint2> tab(static_cast<size_t>(W) * R);
+  std::vector<int64_t> pw(static_cast<size_t>(W) * p->stride);
+  if (cudaMemcpy(tab.data(), p->tab, 8ull * W * R, cudaMemcpyDeviceToHost) != cudaSuccess ||
+      cudaMemcpy(pw.data(), p->pwsuf, 8ull * W * p->stride, cudaMemcpyDeviceToHost) != cudaSuccess) {
+    std::snprintf(err, 256, "CUDA copy of the chain tables failed");
+    return 1;
+  }
+  p->ps_blob_bytes = round16(16ull * nk + 8ull * W * R + vb * W * p->stride);
+  std::vector<unsigned char> img(p->ps_blob_bytes, 0);
+  unsigned char* q = img.data();
+  std::memcpy(q, lim.data(), 8ull * nk);
+  std::memcpy(q + 8ull * nk, mag.data(), 8ull * nk);
+  std::memcpy(q + 16ull * nk, tab.data(), 8ull * W * R);
+  unsigned char* pq = q + 16ull * nk + 8ull * W * R;
+  for (size_t k = 0; k < pw.size(); ++k) {
+    if (p->narrow) {
+      const int32_t v = static_cast<int32_t>(pw[k]);
+      std::memcpy(pq + 4 * k, &v, 4);
+    } else {
+      std::memcpy(pq + 8 * k, &pw[k], 8);
+    }
+  }
+  p->ps_blob = up(img.data(), img.size());
+  if (!p->ps_blob) {
+    std::snprintf(err, 256, "CUDA allocation for the send-phase image failed");
+    return 1;
+  }
+  const int nhist = (p->U != p->L ? 1 : 0) + 1;
+  p->ps_smem = round16(p->ps_blob_bytes + 4ull * nhist * kBins +
+                       kPsThreads * ps_thread_bytes(W, R, S, Q, R <= 256 ? 1 : 2)) + 16;
+  int dev = 0, sms = 148, occ = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const void* fn = reinterpret_cast<const void*>(ps_fn(p));
+  allow_max_dynamic_smem(fn);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kPsThreads, p->ps_smem);
+  if (occ < 1) {
+    std::snprintf(err, 256, "send-phase plan needs %zu bytes of shared memory per block", p->ps_smem);
+    return 1;
+  }
+  p->ps_blocks = sms * occ;
+  p->ps = 1;
+  return 0;
+}
+
 extern "C" int64_t csk_sweep_plan_uploaded(const SweepPlan* p) { return static_cast<int64_t>(p->uploaded); }
 
 extern "C" void csk_sweep_plan_free(SweepPlan* p) {
   if (!p) return;
   void* ptrs[] = {p->tab, p->pwsuf, p->ctot, p->send, p->lim, p->mag, p->blob};
   for (void* q : ptrs)
+    if (q) cudaFree(q);
+  for (void* q : p->ps_bufs)
     if (q) cudaFree(q);
   delete p;
 }
@@ -1113,6 +1524,17 @@ extern "C" int csk_sweep_run(SweepPlan* p, uint64_t seed_lo, int64_t count, uint
     a.mbar_off = static_cast<uint32_t>(p->smem - 16);
   }
   auto st = static_cast<cudaStream_t>(stream);
+  if (p->ps) {
+    a.blob = p->ps_blob;
+    a.blob_bytes = static_cast<uint32_t>(p->ps_blob_bytes);
+    a.mbar_off = static_cast<uint32_t>(p->ps_smem - 16);
+    const int64_t need = (count + kPsThreads - 1) / kPsThreads;
+    const int blocks = static_cast<int>(std::min<int64_t>(p->ps_blocks, need));
+    ps_fn(p)<<<blocks, kPsThreads, p->ps_smem, st>>>(a, p->psa);
+    LAUNCHED();
+    CK(cudaGetLastError());
+    return 0;
+  }
   if (p->dag) {
     a.blob = p->blob;
     a.blob_bytes = static_cast<uint32_t>(p->blob_bytes);

@@ -722,7 +722,10 @@ int cs_sweep_path_json(const cs_graph* g, const cs_oracle* o, const cs_sim_polic
     need(out_json, "out_json");
     std::shared_ptr<SweepCtx> c = cached_sweep(g, o, policy_of(policy));
     Json j;
-    j["path"] = !c->fast ? "event_sim_kernel" : c->dag ? "dag_sweep_kernel" : "chain_sweep_kernel";
+    j["path"] = !c->fast ? "event_sim_kernel"
+                : c->dag ? "dag_sweep_kernel"
+                : c->ps  ? "cluster_ps_kernel"
+                         : "chain_sweep_kernel";
     j["why"] = c->fast ? "" : c->why;
     *out_json = dup(dump_doc(j));
   });
@@ -739,7 +742,7 @@ int cs_sweep_plan_info(const cs_sweep_plan* p, char** out_json) {
     j["edges"] = static_cast<int64_t>(c.g->edges().size());
     j["recvs_per_worker"] = c.R;
     j["classes"] = c.nc;
-    j["kernel"] = c.dag ? "dag_sweep_kernel" : "chain_sweep_kernel";
+    j["kernel"] = c.dag ? "dag_sweep_kernel" : c.ps ? "cluster_ps_kernel" : "chain_sweep_kernel";
     if (c.dag) {
       j["joins"] = c.joins;
       j["slots"] = c.slots;

@@ -3,12 +3,15 @@
 // SUM all-reduce of a packed int64 buffer per round. NCCL is loaded at run
 // time (libnccl.so.2), so single-GPU users of the library never need it.
 //
-// Packed layout (n devices): [0, n) min keys, [n, 2n) max keys (each device
-// writes only its own slot, the others stay 0), [2n, 2n + 2006) counters and
-// histograms (summed), then n pairs of float64 bit patterns (per-device
-// slots; summed in device order on the host, so the result is
-// deterministic). The keys are (m << key_bits) | (seed - round base), as in
-// the single-device statistics (include/commsched.h CS_DSTATS_*).
+// Packed layout (n devices): four per-device key slots each — [0, n) min
+// keys, [n, 2n) max keys, [2n, 3n) iteration-time min keys, [3n, 4n)
+// iteration-time max keys (each device writes only its own slots, the
+// others stay 0) — then words 2..2007 of the statistics (counters and
+// histograms, summed; the key words among them are zeroed), then n pairs of
+// float64 bit patterns (per-device slots; summed in device order on the
+// host, so the result is deterministic). Keys are (m << key_bits) |
+// (seed - round base), as in the single-device statistics
+// (include/commsched.h CS_DSTATS_*).
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>
@@ -75,7 +78,8 @@ class NcclReducer final : public DeviceReducer {
   // Communicators stay alive for the process (like the reference's
   // thread-local error string, they are process-lifetime state).
   void reduce(int d, const int64_t* d_i64, const double* d_f64, int64_t* h_i64, double* h_f64) const override {
-    const size_t words = 2 * static_cast<size_t>(n_) + (CS_DSTATS_I64 - 2) + CS_DSTATS_F64 * static_cast<size_t>(n_);
+    const size_t kw = 4 * static_cast<size_t>(n_), cw = CS_DSTATS_I64 - 2;
+    const size_t words = kw + cw + CS_DSTATS_F64 * static_cast<size_t>(n_);
     int64_t* buf = nullptr;
     ck(cudaMallocAsync(&buf, 8 * words, 0));
     struct Free {
@@ -85,8 +89,11 @@ class NcclReducer final : public DeviceReducer {
     ck(cudaMemsetAsync(buf, 0, 8 * words, 0));
     ck(cudaMemcpyAsync(buf + d, d_i64, 8, cudaMemcpyDeviceToDevice, 0));
     ck(cudaMemcpyAsync(buf + n_ + d, d_i64 + 1, 8, cudaMemcpyDeviceToDevice, 0));
-    ck(cudaMemcpyAsync(buf + 2 * n_, d_i64 + 2, 8 * (CS_DSTATS_I64 - 2), cudaMemcpyDeviceToDevice, 0));
-    const size_t fo = 2 * static_cast<size_t>(n_) + (CS_DSTATS_I64 - 2);
+    ck(cudaMemcpyAsync(buf + 2 * n_ + d, d_i64 + 4, 8, cudaMemcpyDeviceToDevice, 0));
+    ck(cudaMemcpyAsync(buf + 3 * n_ + d, d_i64 + 5, 8, cudaMemcpyDeviceToDevice, 0));
+    ck(cudaMemcpyAsync(buf + kw, d_i64 + 2, 8 * cw, cudaMemcpyDeviceToDevice, 0));
+    ck(cudaMemsetAsync(buf + kw + 2, 0, 16, 0));  // words 4, 5 travel in the key slots
+    const size_t fo = kw + cw;
     ck(cudaMemcpyAsync(buf + fo + CS_DSTATS_F64 * static_cast<size_t>(d), d_f64, 8 * CS_DSTATS_F64,
                        cudaMemcpyDeviceToDevice, 0));
     nccheck(nccl().all_reduce(buf, buf, words, ncclInt64, ncclSum, comms_[d], 0), "ncclAllReduce");
@@ -97,14 +104,18 @@ class NcclReducer final : public DeviceReducer {
     std::vector<int64_t> h(words);
     ck(cudaMemcpyAsync(h.data(), buf, 8 * words, cudaMemcpyDeviceToHost, 0));
     ck(cudaStreamSynchronize(0));
-    uint64_t kmin = ~0ULL, kmax = 0;  // an idle device's min key is all ones
+    uint64_t kmin = ~0ULL, kmax = 0, ikmin = ~0ULL, ikmax = 0;  // an idle device's min keys are all ones
     for (int k = 0; k < n_; ++k) {
       kmin = std::min(kmin, static_cast<uint64_t>(h[k]));
       kmax = std::max(kmax, static_cast<uint64_t>(h[n_ + k]));
+      ikmin = std::min(ikmin, static_cast<uint64_t>(h[2 * n_ + k]));
+      ikmax = std::max(ikmax, static_cast<uint64_t>(h[3 * n_ + k]));
     }
+    std::memcpy(h_i64 + 2, h.data() + kw, 8 * cw);
     h_i64[0] = static_cast<int64_t>(kmin);
     h_i64[1] = static_cast<int64_t>(kmax);
-    std::memcpy(h_i64 + 2, h.data() + 2 * n_, 8 * (CS_DSTATS_I64 - 2));
+    h_i64[4] = static_cast<int64_t>(ikmin);
+    h_i64[5] = static_cast<int64_t>(ikmax);
     for (int f = 0; f < CS_DSTATS_F64; ++f) {
       double acc = 0.0;
       for (int k = 0; k < n_; ++k) {

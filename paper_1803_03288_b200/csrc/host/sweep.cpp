@@ -422,6 +422,141 @@ ChainShape chain_shape(const Graph& g, bool allow_sends) {
   return cs;
 }
 
+// Send phase of clusters whose parameter-server ops take time (sweep.cu
+// cluster_ps_kernel): duration-independent structure, memoised per graph.
+struct PsShape {
+  bool ok = false;
+  std::string why;
+  int32_t S = 0, Q = 0, ps_slot = 0;
+  std::vector<int16_t> recv_sb;                // [R] sends before recv column c (channel op order)
+  std::vector<std::vector<int32_t>> sends;      // per worker: send ops (graph index), op-index order
+  std::vector<int32_t> send_succ_off;           // [W*S + 1]
+  std::vector<int16_t> send_succ;               // PS op indices
+  std::vector<int32_t> ps_ops;                  // graph indices, op-index order
+  std::vector<uint8_t> ps_missing;              // predecessor counts
+  std::vector<int32_t> ps_succ_off;
+  std::vector<int16_t> ps_succ;
+  std::vector<int32_t> last_compute;           // per worker: graph index of its last compute op
+};
+
+PsShape ps_shape(const Graph& g, const std::vector<std::string>& workers) {
+  PsShape ps;
+  auto no = [&](const char* why) {
+    ps.why = why;
+    return ps;
+  };
+  const int32_t n = g.n();
+  const auto& ops = g.ops();
+  std::unordered_map<std::string, int32_t> widx;
+  for (size_t i = 0; i < workers.size(); ++i) widx[workers[i]] = static_cast<int32_t>(i);
+  std::vector<int32_t> wof(n, -1), psix(n, -1);
+  int32_t ps_res = -1;
+  for (int32_t i = 0; i < n; ++i) {
+    auto it = widx.find(ops[i].res.device);
+    if (it != widx.end()) {
+      wof[i] = it->second;
+      continue;
+    }
+    if (transfer(ops[i].kind)) return no("transfer on a parameter-server device");
+    if (ps_res >= 0 && ps_res != g.res_of()[i]) return no("parameter-server ops on more than one resource");
+    ps_res = g.res_of()[i];
+    psix[i] = static_cast<int32_t>(ps.ps_ops.size());
+    ps.ps_ops.push_back(i);  // ascending graph index = op-index order
+  }
+  ps.Q = static_cast<int32_t>(ps.ps_ops.size());
+  if (ps.Q == 0) return no("no parameter-server ops");
+  if (ps.Q >= (1 << 15)) return no("too many parameter-server ops");
+  for (int32_t x = 0; x < ps.Q; ++x) {
+    const int32_t v = ps.ps_ops[x];
+    int32_t np = 0;
+    for (int32_t e = g.pred_off()[v]; e < g.pred_off()[v + 1]; ++e) {
+      const int32_t u = g.pred_idx()[e];
+      if (psix[u] < 0 && ops[u].kind != kSend) return no("parameter-server op fed by a non-send worker op");
+      ++np;
+    }
+    if (np == 0) return no("parameter-server op without predecessors");
+    if (np > 255) return no("parameter-server op with more than 255 predecessors");
+    ps.ps_missing.push_back(static_cast<uint8_t>(np));
+  }
+  ps.ps_succ_off.push_back(0);
+  for (int32_t x = 0; x < ps.Q; ++x) {
+    const int32_t v = ps.ps_ops[x];
+    for (int32_t e = g.succ_off()[v]; e < g.succ_off()[v + 1]; ++e) {
+      const int32_t u = g.succ_idx()[e];
+      if (psix[u] < 0) return no("parameter-server op feeding a worker");
+      ps.ps_succ.push_back(static_cast<int16_t>(psix[u]));
+    }
+    ps.ps_succ_off.push_back(static_cast<int32_t>(ps.ps_succ.size()));
+  }
+  // per worker: channel ops in op-index order, sends, compute total order
+  const int32_t W = static_cast<int32_t>(workers.size());
+  ps.sends.assign(W, {});
+  std::vector<std::vector<int32_t>> recvs(W), comp(W);
+  std::vector<int32_t> chan_res(W, -1);
+  for (int32_t i = 0; i < n; ++i) {
+    const int32_t w = wof[i];
+    if (w < 0) continue;
+    if (ops[i].kind == kSend) ps.sends[w].push_back(i);
+    else if (ops[i].kind == kRecv) recvs[w].push_back(i);
+    else comp[w].push_back(i);
+    if (transfer(ops[i].kind)) chan_res[w] = g.res_of()[i];
+  }
+  ps.S = static_cast<int32_t>(ps.sends[0].size());
+  const int32_t R = static_cast<int32_t>(recvs[0].size());
+  for (int32_t w = 0; w < W; ++w) {
+    if (static_cast<int32_t>(ps.sends[w].size()) != ps.S || static_cast<int32_t>(recvs[w].size()) != R)
+      return no("workers differ in their transfers");
+    if (chan_res[w] < 0) return no("worker without a channel");
+    // recv_sb: sends before each recv column in op-index order, same on every worker
+    std::vector<int16_t> sb(R);
+    for (int32_t c = 0; c < R; ++c)
+      sb[c] = static_cast<int16_t>(std::lower_bound(ps.sends[w].begin(), ps.sends[w].end(), recvs[w][c]) -
+                                   ps.sends[w].begin());
+    if (w == 0) ps.recv_sb = sb;
+    else if (sb != ps.recv_sb) return no("workers differ in their channel op order");
+    // compute ops totally ordered (so the core never has two candidates):
+    // the longest path over compute->compute edges covers all of them
+    if (comp[w].empty()) return no("worker without compute ops");
+    std::unordered_map<int32_t, int32_t> depth;
+    int32_t best = 0, last = -1;
+    for (int32_t v : comp[w]) depth[v] = 0;
+    // graph indices are not topological: relax in a topological order of the worker
+    std::vector<int32_t> miss(n, 0), order;
+    for (int32_t v : comp[w]) {
+      for (int32_t e = g.pred_off()[v]; e < g.pred_off()[v + 1]; ++e)
+        if (depth.count(g.pred_idx()[e])) ++miss[v];
+      if (miss[v] == 0) order.push_back(v);
+    }
+    for (size_t h = 0; h < order.size(); ++h) {
+      const int32_t v = order[h];
+      depth[v] += 1;
+      if (depth[v] > best) best = depth[v], last = v;
+      for (int32_t e = g.succ_off()[v]; e < g.succ_off()[v + 1]; ++e) {
+        const int32_t u = g.succ_idx()[e];
+        auto it = depth.find(u);
+        if (it == depth.end()) continue;
+        it->second = std::max(it->second, depth[v]);
+        if (--miss[u] == 0) order.push_back(u);
+      }
+    }
+    if (best != static_cast<int32_t>(comp[w].size())) return no("worker compute ops not totally ordered");
+    ps.last_compute.push_back(last);
+    for (int32_t s_ : ps.sends[w]) {
+      for (int32_t e = g.succ_off()[s_]; e < g.succ_off()[s_ + 1]; ++e) {
+        const int32_t u = g.succ_idx()[e];
+        if (psix[u] < 0) return no("send feeding a worker op");
+        ps.send_succ.push_back(static_cast<int16_t>(psix[u]));
+      }
+      ps.send_succ_off.push_back(static_cast<int32_t>(ps.send_succ.size()));
+    }
+  }
+  ps.send_succ_off.insert(ps.send_succ_off.begin(), 0);
+  for (int32_t w = 0; w < W; ++w)
+    if (chan_res[w] < ps_res) ++ps.ps_slot;
+  ps.ok = true;
+  return ps;
+}
+
 // Weights the shape with one oracle's durations (O(n)).
 bool chain_tables(const ChainShape& cs, const Graph& g, const std::vector<int64_t>& dur, ChainTables& t,
                   std::string& why) {
@@ -521,6 +656,8 @@ std::unique_ptr<SweepCtx> make_sweep(std::shared_ptr<const Graph> g, const TimeO
   }
   std::vector<ChainTables> tabs;
   std::shared_ptr<const ChainShape> shape0;  // worker 0's shape (the program the workers share)
+  std::shared_ptr<const PsShape> pshape;      // clusters whose PS ops take time
+  bool need_ps = false;
   if (ok && !s->cluster) {
     tabs.emplace_back();
     shape0 = g->memo<ChainShape>("chain", [&] { return chain_shape(*g, false); });
@@ -532,11 +669,24 @@ std::unique_ptr<SweepCtx> make_sweep(std::shared_ptr<const Graph> g, const TimeO
     // expand_to_mr(…, ps_op_time = 0)); otherwise only the exact replica
     // gives it (SURVEY A.2 covers the workers).
     std::set<std::string> wset(s->workers.begin(), s->workers.end());
-    for (int32_t i = 0; i < g->n() && ok; ++i)
-      if (!wset.count(g->ops()[i].res.device) && s->dur[i] != 0) {
+    for (int32_t i = 0; i < g->n(); ++i)
+      if (!wset.count(g->ops()[i].res.device) && s->dur[i] != 0) need_ps = true;
+    if (need_ps && std::getenv("TICTAC_SWEEP_NO_PS")) {
+      ok = false;
+      s->why = "parameter-server ops take time (send phase disabled by TICTAC_SWEEP_NO_PS)";
+    }
+    if (need_ps && ok) {  // the send phase of cluster_ps_kernel
+      pshape = g->memo<PsShape>("ps", [&] { return ps_shape(*g, s->workers); });
+      if (!pshape->ok) {
         ok = false;
-        s->why = "parameter-server ops take time (full makespan needs the event replica)";
+        s->why = "parameter-server ops take time and " + pshape->why;
       }
+      for (size_t w = 0; ok && w < pshape->last_compute.size(); ++w)
+        if (s->dur[pshape->last_compute[w]] <= 0) {
+          ok = false;
+          s->why = "parameter-server ops take time and a worker's last compute op takes none";
+        }
+    }
     // devices other than workers must not feed back into workers
     for (const auto& dv : s->workers) {
       auto part = g->partition(dv);
@@ -583,9 +733,26 @@ std::unique_ptr<SweepCtx> make_sweep(std::shared_ptr<const Graph> g, const TimeO
       const double t = std::ldexp(p.noise, 53);
       noise_thr = t == std::floor(t) ? static_cast<uint64_t>(t) : static_cast<uint64_t>(std::floor(t)) + 1;
     }
-    if (shape0->nested) {
+    const bool fail_ps = need_ps && !shape0->nested;
+    if (fail_ps) {
+    } else if (shape0->nested) {
       s->plan = csk_sweep_plan(W, R, nc, d.data(), first.data(), pw.data(), send.data(),
                                s->cluster ? 1 : 0, s->U, s->L, noise_thr, err);
+      if (s->plan && need_ps) {
+        const PsShape& q = *pshape;
+        std::vector<int64_t> sd, qd;
+        for (const auto& sv : q.sends)
+          for (int32_t x : sv) sd.push_back(s->dur[x]);
+        for (int32_t x : q.ps_ops) qd.push_back(s->dur[x]);
+        if (csk_sweep_plan_add_ps(s->plan, q.S, q.recv_sb.data(), sd.data(), q.send_succ_off.data(),
+                                  q.send_succ.data(), q.Q, qd.data(), q.ps_missing.data(), q.ps_succ_off.data(),
+                                  q.ps_succ.data(), q.ps_slot, err)) {
+          csk_sweep_plan_free(s->plan);
+          s->plan = nullptr;
+          fail(kInternal, err);
+        }
+        s->ps = true;
+      }
     } else {
       const DagProgram& dp = shape0->dag;
       std::vector<int64_t> wr, wj, w0;
@@ -604,8 +771,9 @@ std::unique_ptr<SweepCtx> make_sweep(std::shared_ptr<const Graph> g, const TimeO
       s->slots = dp.L;
       s->prog_words = nrec;
     }
-    if (!s->plan) fail(kInternal, err);
-    s->fast = true;
+    if (!fail_ps && !s->plan) fail(kInternal, err);
+    s->fast = !fail_ps;
+    if (fail_ps) s->why = "parameter-server ops take time and the workers are not chain-class";
     s->nc = nc;
     s->R = R;
   }
@@ -641,12 +809,15 @@ void finish_stats(const SweepCtx& s, const int64_t* i64, const double* f64, uint
   }
   out->n_workers = s.cluster ? static_cast<int64_t>(s.workers.size()) : 0;
   out->straggler_sum = f64[1];
-  if (s.cluster) {  // closed-form clusters: the makespan is the iteration time (make_sweep)
-    out->iter_min_us = out->min_us;
-    out->iter_argmin_seed = out->argmin_seed;
-    out->iter_max_us = out->max_us;
-    out->iter_argmax_seed = out->argmax_seed;
-    out->iter_sum_us = out->sum_us;
+  if (s.cluster && out->count > 0) {  // iteration time (slowest worker), keys as above
+    const int kb = csk_key_bits(s.U);
+    const uint64_t mask = (1ULL << kb) - 1;
+    const uint64_t kmin = static_cast<uint64_t>(i64[4]), kmax = static_cast<uint64_t>(i64[5]);
+    out->iter_min_us = static_cast<int64_t>(kmin >> kb);
+    out->iter_argmin_seed = key_base + (kmin & mask);
+    out->iter_max_us = static_cast<int64_t>(kmax >> kb);
+    out->iter_argmax_seed = key_base + (mask - (kmax & mask));
+    out->iter_sum_us = i64[6];
   }
 }
 
