@@ -209,6 +209,28 @@ struct MtLazy {
   }
 };
 
+// The same over a caller-owned state P (312 words, e.g. a strided view into
+// scratch) that is only seeded and used once the first 311 outputs are spent.
+template <typename P>
+struct MtLazyP {
+  MtLazy lz;
+  MtFullP<P> full;
+  bool on_full;
+  __device__ __forceinline__ void seed(uint64_t s) {
+    lz.init(s);
+    on_full = false;
+  }
+  __device__ __forceinline__ uint64_t next() {
+    if (!on_full) {
+      if (!lz.exhausted()) return lz.next_raw();
+      full.seed(lz.seed);
+      for (int k = 0; k < lz.i; ++k) full.next();
+      on_full = true;
+    }
+    return full.next();
+  }
+};
+
 // A stream of any length: the first 311 outputs from MtLazy's register
 // cursors, then a full state in local memory continuing the same sequence.
 struct MtStream {

@@ -94,7 +94,7 @@ template <int S>
 struct Slot {
   // hot
   Arr<int32_t, S> missing, gate, running, comp_len, ready_cnt, lo, hi, haspri;
-  Arr<uint32_t, S> ready, forced, rready;
+  Arr<uint32_t, S> ready, forced, rready, pmask;
   Arr<int64_t, S> run_end, counter;
   Arr<uint64_t, S> mt;
   // cold
@@ -107,7 +107,7 @@ __host__ __device__ inline size_t align8(size_t x) { return (x + 7) & ~size_t(7)
 
 // Bytes of one slot group (S runs interleaved; S = 1 for a warp-per-run slot).
 __host__ __device__ inline size_t hot_bytes(int n, int nres, int rbw, int S = 1) {
-  return align8(4ull * n * S) * 2 + align8(4ull * nres * S) * 6 + align8(4ull * (rbw + 1) * S) * 2 +
+  return align8(4ull * n * S) * 2 + align8(4ull * nres * S) * 6 + align8(4ull * (rbw + 1) * S) * 3 +
          align8(4ull * ((n + 31) / 32 + 1) * S) + align8(8ull * nres * S) * 2 + 8ull * 312 * S;
 }
 
@@ -134,6 +134,7 @@ __device__ Slot<S> carve(char* hot, char* cold, int lane, int n, int nres, int n
   take(s.haspri, hot, nres);
   take(s.ready, hot, rbw + 1);
   take(s.rready, hot, rbw + 1);
+  take(s.pmask, hot, rbw + 1);
   take(s.forced, hot, (n + 31) / 32 + 1);
   take(s.run_end, hot, nres);
   take(s.counter, hot, nres);
@@ -223,7 +224,8 @@ __device__ void fill_priorities(const GraphView& G, const RunSpec& rs, const Slo
         const int c0 = rs.wcols_off[w], Rw = rs.wcols_off[w + 1] - c0;
         const uint64_t ws = rs.cluster ? splitmix64(seed ^ (kPhi * static_cast<uint64_t>(w + 1))) : seed;
         for (int k = 0; k < Rw; ++k) s.items[k] = k;
-        MtFullP<Arr<uint64_t, S>> m{s.mt2, 0};
+        MtLazyP<Arr<uint64_t, S>> m;  // register cursors (R <= 311 draws), scratch state beyond
+        m.full = {s.mt2, 0};
         m.seed(ws);
         for (int i = Rw; i > 1; --i) {
           const int j = static_cast<int>(bounded_full(m, static_cast<uint64_t>(i), rs));
@@ -262,6 +264,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, kL == 1 ? kThreadMinBlock
     for (int w = lane; w < rbw; w += kL) {
       s.ready[w] = 0;
       s.rready[w] = 0;
+      s.pmask[w] = 0;
     }
     for (int w = lane; w < (n + 31) / 32; w += kL) s.forced[w] = 0;
     for (int r = lane; r < nres; r += kL) {
@@ -304,7 +307,8 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, kL == 1 ? kThreadMinBlock
         if (s.prio[i] >= 0) s.haspri[G.res[i]] = 1;
       }
     // dense per-channel ranks from (priority, id), then noise swaps
-    MtFullP<Arr<uint64_t, S>> noise{s.mt2, 0};
+    MtLazyP<Arr<uint64_t, S>> noise;
+    noise.full = {s.mt2, 0};
     const bool noisy = rs.gated && rs.noise > 0.0;
     if (lane == 0 && noisy) noise.seed(splitmix64(choice_seed ^ kNoiseSalt));
     for (int r = 0; r < nres; ++r) {
@@ -365,6 +369,25 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, kL == 1 ? kThreadMinBlock
             s.rready[G.rb_off[r] + (q >> 5)] |= 1u << (q & 31);
         }
         group_sync<kL>();
+      } else if (k > 0) {
+        // prioritized and unprioritized ops share the channel (a worker's
+        // recvs and gradient sends): prioritized ready ops indexed by rank
+        // as above, the others found through the complement of pmask
+        if (lane == 0) s.haspri[r] = 3;
+        for (int a = o0 + lane; a < o1; a += kL) {
+          const int i = G.rops[a];
+          const int q = s.orig[i];
+          if (q < 0) continue;
+          const int l = G.lidx[i];
+          if constexpr (kL == 32) {
+            atomicOr(&s.pmask[G.rb_off[r] + (l >> 5)], 1u << (l & 31));
+            if (s.missing[i] == 0) atomicOr(&s.rready[G.rb_off[r] + (q >> 5)], 1u << (q & 31));
+          } else {
+            s.pmask[G.rb_off[r] + (l >> 5)] |= 1u << (l & 31);
+            if (s.missing[i] == 0) s.rready[G.rb_off[r] + (q >> 5)] |= 1u << (q & 31);
+          }
+        }
+        group_sync<kL>();
       }
       if (!rs.gated) continue;
       if (lane == 0 && noisy)
@@ -407,9 +430,9 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, kL == 1 ? kThreadMinBlock
       auto start_op = [&](int r, int op) {
         const int l = G.lidx[op];
         s.ready[G.rb_off[r] + (l >> 5)] &= ~(1u << (l & 31));
-        if (s.haspri[r] == 2) {
+        if (s.haspri[r] >= 2) {
           const int q = s.orig[op];
-          s.rready[G.rb_off[r] + (q >> 5)] &= ~(1u << (q & 31));
+          if (q >= 0) s.rready[G.rb_off[r] + (q >> 5)] &= ~(1u << (q & 31));
         }
         s.ready_cnt[r] -= 1;
         s.running[r] = op;
@@ -473,6 +496,57 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, kL == 1 ? kThreadMinBlock
             }
           }
           return false;  // unreachable
+        }
+        if (s.haspri[r] == 3) {
+          // candidates (sim.cpp:170-181): every ready unprioritized op, plus
+          // the admitted ready ops at the minimum admitted priority — the
+          // admitted ops of one equal-priority run of ranks (ranks ascend
+          // with (priority, id)) — merged in op-index order
+          const int wb = G.rb_off[r], o0 = G.rops_off[r];
+          const int nw = (G.rops_off[r + 1] - o0 + 31) >> 5;
+          constexpr int kMaxBest = 2;  // tied best-priority candidates kept in registers
+          int bl0 = -1, bl1 = -1;
+          int best = -1, nb = 0;
+          bool done = false;
+          for (int w = 0; w < nw && !done; ++w) {
+            uint32_t bits = s.rready[wb + w];
+            while (bits) {
+              const int bit = __ffs(bits) - 1;
+              bits &= bits - 1;
+              const int op = s.rop[o0 + (w << 5) + bit];
+              const int p = s.prio[op];
+              if (best >= 0 && p != best) {
+                done = true;
+                break;
+              }
+              if (admitted(s, op, r, gated)) {
+                best = p;
+                if (nb == 0) bl0 = G.lidx[op];
+                else if (nb == 1) bl1 = G.lidx[op];
+                ++nb;
+              }
+            }
+          }
+          if (nb <= kMaxBest) {
+            int nu = 0;
+            for (int w = s.lo[r], wh = s.hi[r]; w <= wh; ++w) nu += __popc(s.ready[wb + w] & ~s.pmask[wb + w]);
+            const int total = nu + nb;
+            if (total == 0) return false;
+            int k = total > 1 ? static_cast<int>(bounded_full(choice, static_cast<uint64_t>(total), rs)) : 0;
+            for (int w = s.lo[r], wh = s.hi[r]; w <= wh; ++w) {
+              uint32_t m = s.ready[wb + w] & ~s.pmask[wb + w];
+              if (nb > 0 && (bl0 >> 5) == w) m |= 1u << (bl0 & 31);
+              if (nb > 1 && (bl1 >> 5) == w) m |= 1u << (bl1 & 31);
+              const int c = __popc(m);
+              if (k < c) {
+                start_op(r, G.rops[o0 + (w << 5) + nth_bit(m, k)]);
+                return true;
+              }
+              k -= c;
+            }
+            return false;  // unreachable
+          }
+          // more than kMaxBest tied candidates: the general scan below
         }
         const bool pri = s.haspri[r] != 0;
         const int wb = G.rb_off[r], ob = G.rops_off[r];
@@ -546,9 +620,9 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, kL == 1 ? kThreadMinBlock
       auto push_ready = [&](int w_op) {
         const int rw = G.res[w_op], l = G.lidx[w_op];
         s.ready[G.rb_off[rw] + (l >> 5)] |= 1u << (l & 31);
-        if (s.haspri[rw] == 2) {
+        if (s.haspri[rw] >= 2) {
           const int q = s.orig[w_op];
-          s.rready[G.rb_off[rw] + (q >> 5)] |= 1u << (q & 31);
+          if (q >= 0) s.rready[G.rb_off[rw] + (q >> 5)] |= 1u << (q & 31);
         }
         s.ready_cnt[rw] += 1;
         s.lo[rw] = min(s.lo[rw], l >> 5);
