@@ -303,8 +303,8 @@ def exact_paths(lib, path):
     """Outside the plain gated closed form: (a) config 4 with reorder noise
     0.1 — still the closed form, on the noise-permuted gate sequence; (b)
     config 3 (VGG-16 x 4 workers / 1 PS) with PS operations that take time
-    (100 us each): its makespans come only from the exact event replica
-    (thread per run at this batch size)."""
+    (100 us each): closed-form workers + the exact send phase; (c) the same
+    with two parameter servers, which only the exact event replica covers."""
     g4 = lib.graph(bench_json(MODEL))
     a = sweep_vs_reference(lib, g4, path, f"config4 {MODEL}, counter gate + reorder noise 0.1 "
                                           f"(closed form on the noise-permuted gate order)", 0.1, 1 << 22)
@@ -313,9 +313,16 @@ def exact_paths(lib, path):
     with open(p3, "w") as f:
         f.write(c3.serialize())
     b = sweep_vs_reference(lib, c3, p3, "config3 vgg16_training x 4 workers / 1 PS with 100 us PS ops, full "
-                                        "makespans (exact event replica, thread per run)", None, 1 << 18)
-    b["path"] = c3.sweep_path(c3.declared())
-    return {"noise_sweep_config4": a, "event_replica_config3_ps100_makespans": b}
+                                        "makespans (closed-form workers + exact send phase, cluster_ps_kernel)",
+                           None, 1 << 22)
+    c4 = lib.model("vgg16_training", 1).expand(4, 2, 100)
+    p4 = os.path.join(os.path.dirname(path), "config3_2ps.json")
+    with open(p4, "w") as f:
+        f.write(c4.serialize())
+    c = sweep_vs_reference(lib, c4, p4, "config3 vgg16_training x 4 workers / 2 PS with 100 us PS ops, full "
+                                        "makespans (two channels per worker: exact event replica, thread per run)",
+                           None, 1 << 18)
+    return {"noise_sweep_config4": a, "ps_send_phase_config3_ps100": b, "event_replica_config3_2ps": c}
 
 
 def cpu_baseline(path, target_s=10.0, g=None, o=None):
