@@ -622,7 +622,7 @@ def main():
     d_i64 = torch.zeros(capi.DSTATS_I64, dtype=torch.int64, device="cuda")
     d_f64 = torch.zeros(capi.DSTATS_F64, dtype=torch.float64, device="cuda")
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device="cuda")
-    buf = torch.zeros(2 * world + capi.DSTATS_I64 + capi.DSTATS_F64 * world, dtype=torch.int64, device="cuda")
+    buf = torch.zeros(pdist.packed_words(world), dtype=torch.int64, device="cuda")
     k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 
     def make_step(lo, n):
@@ -631,8 +631,8 @@ def main():
             k0.record(stream)
             plan.run(lo, n, SEED_LO, sptr, None, d_i64.data_ptr(), d_f64.data_ptr())
             k1.record(stream)
-            if world > 1:  # the step's one reduction (paper_1803_03288_b200/dist.py)
-                pdist.reduce_stats(d_i64, d_f64, rank, world, buf)
+            if world > 1:  # the step's one reduction: pack, one NCCL all-reduce, unpack
+                pdist.reduce_stats_device(lib, d_i64, d_f64, rank, world, buf, sptr)
         return step
 
     # headline: config 4's fixed 2^24 orders, contiguous shards over the ranks

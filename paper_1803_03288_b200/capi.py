@@ -96,6 +96,8 @@ _SIGS = {
     "cs_sweep_plan_reset": [_vp, _vp, _vp, _vp],
     "cs_sweep_plan_run": [_vp, C.c_uint64, C.c_int64, C.c_uint64, _vp, _vp, _vp, _vp],
     "cs_sweep_stats_finish": [_vp, _vp, _vp, C.c_uint64, C.POINTER(SweepStats)],
+    "cs_sweep_stats_pack": [_vp, _vp, C.c_int, C.c_int, _vp, _vp],
+    "cs_sweep_stats_unpack": [_vp, C.c_int, _vp, _vp, _vp],
     "cs_graph_generate_model": [_cp, C.c_uint64, _pp],
     "cs_tac_traffic": [_vp, _vp, _i64p, C.c_int],
 }
@@ -104,7 +106,8 @@ _FREE = ["cs_graph_free", "cs_oracle_free", "cs_schedule_free", "cs_report_free"
 REFERENCE_SYMBOLS = [k for k in _SIGS if k not in (
     "cs_sweep_random", "cs_sweep_random_multi", "cs_simulate_orders", "cs_sweep_plan_create", "cs_sweep_plan_info",
     "cs_sweep_path_json",
-    "cs_sweep_plan_reset", "cs_sweep_plan_run", "cs_sweep_stats_finish",
+    "cs_sweep_plan_reset", "cs_sweep_plan_run", "cs_sweep_stats_finish", "cs_sweep_stats_pack",
+    "cs_sweep_stats_unpack",
     "cs_graph_generate_model", "cs_tac_traffic")] + [f for f in _FREE if f != "cs_sweep_plan_free"] + [
     "cs_last_error", "cs_version"]
 

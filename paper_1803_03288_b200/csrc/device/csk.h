@@ -124,6 +124,10 @@ int csk_sweep_plan_add_ps(SweepPlan* p, int32_t S, const int16_t* recv_sb, const
 /* Host-to-device bytes the plan's construction copied (tables, images). */
 int64_t csk_sweep_plan_uploaded(const SweepPlan* p);
 /* Stats layout documented in include/commsched.h (CS_DSTATS_*). */
+int csk_stats_pack(const int64_t* d_i64, const double* d_f64, int rank, int world, int64_t* d_buf,
+                   void* stream, char* err);
+int csk_stats_unpack(const int64_t* d_buf, int world, int64_t* d_i64, double* d_f64, void* stream,
+                     char* err);
 int csk_sweep_reset(SweepPlan* p, void* stream, int64_t* d_i64, double* d_f64, char* err);
 int csk_sweep_run(SweepPlan* p, uint64_t seed_lo, int64_t count, uint64_t key_base,
                   void* stream, int64_t* d_makespans, int64_t* d_worker_makespans,

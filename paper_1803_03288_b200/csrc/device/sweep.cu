@@ -1077,6 +1077,47 @@ __global__ void __launch_bounds__(kSweepThreads) lex_kernel(ChainArgs a, int64_t
   }
 }
 
+// Multi-process reduction of the statistics (one SUM all-reduce): pack this
+// rank's words into its slots of a zeroed buffer — keys 0, 1, 4, 5 into
+// slots [k*world + rank], words 2..2007 (keys zeroed) summed, the float sums'
+// bit patterns into [kw + 2006 + 2*rank] — and unpack the reduced buffer.
+__global__ void stats_pack_kernel(const unsigned long long* i64, const double* f64, int rank, int world,
+                                  unsigned long long* buf) {
+  const int kw = 4 * world, nw = kw + 2006 + 2 * world;
+  for (int k = threadIdx.x; k < nw; k += blockDim.x) buf[k] = 0;
+  __syncthreads();
+  if (threadIdx.x < 4) {
+    const int word[4] = {0, 1, 4, 5};
+    buf[threadIdx.x * world + rank] = i64[word[threadIdx.x]];
+  }
+  for (int k = threadIdx.x; k < 2006; k += blockDim.x) {
+    const int w = k + 2;
+    buf[kw + k] = (w == 4 || w == 5) ? 0ULL : i64[w];
+  }
+  if (threadIdx.x < 2) buf[kw + 2006 + 2 * rank + threadIdx.x] = __double_as_longlong(f64[threadIdx.x]);
+}
+__global__ void stats_unpack_kernel(const unsigned long long* buf, int world, unsigned long long* i64,
+                                    double* f64) {
+  const int kw = 4 * world;
+  for (int k = threadIdx.x; k < 2006; k += blockDim.x) i64[k + 2] = buf[kw + k];
+  __syncthreads();
+  if (threadIdx.x < 4) {
+    const int word[4] = {0, 1, 4, 5};
+    const bool is_min = threadIdx.x == 0 || threadIdx.x == 2;
+    unsigned long long v = is_min ? ~0ULL : 0ULL;  // an idle rank's min key is all ones
+    for (int r = 0; r < world; ++r) {
+      const unsigned long long x = buf[threadIdx.x * world + r];
+      v = is_min ? min(v, x) : max(v, x);
+    }
+    i64[word[threadIdx.x]] = v;
+  }
+  if (threadIdx.x < 2) {
+    double acc = 0.0;  // rank order: deterministic
+    for (int r = 0; r < world; ++r) acc += __longlong_as_double(buf[kw + 2006 + 2 * r + threadIdx.x]);
+    f64[threadIdx.x] = acc;
+  }
+}
+
 __global__ void reset_kernel(unsigned long long* i64, double* f64) {
   for (int k = threadIdx.x; k < 2008; k += blockDim.x) i64[k] = (k == 0 || k == 4) ? ~0ULL : 0ULL;
   if (threadIdx.x < 2) f64[threadIdx.x] = 0.0;
@@ -1472,6 +1513,26 @@ extern "C" void csk_sweep_plan_free(SweepPlan* p) {
   for (void* q : p->ps_bufs)
     if (q) cudaFree(q);
   delete p;
+}
+
+extern "C" int csk_stats_pack(const int64_t* d_i64, const double* d_f64, int rank, int world, int64_t* d_buf,
+                              void* stream, char* err) {
+  stats_pack_kernel<<<1, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<const unsigned long long*>(d_i64), d_f64, rank, world,
+      reinterpret_cast<unsigned long long*>(d_buf));
+  LAUNCHED();
+  CK(cudaGetLastError());
+  return 0;
+}
+
+extern "C" int csk_stats_unpack(const int64_t* d_buf, int world, int64_t* d_i64, double* d_f64, void* stream,
+                                char* err) {
+  stats_unpack_kernel<<<1, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<const unsigned long long*>(d_buf), world, reinterpret_cast<unsigned long long*>(d_i64),
+      d_f64);
+  LAUNCHED();
+  CK(cudaGetLastError());
+  return 0;
 }
 
 extern "C" int csk_sweep_reset(SweepPlan*, void* stream, int64_t* d_i64, double* d_f64, char* err) {

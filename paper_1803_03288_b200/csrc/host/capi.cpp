@@ -799,6 +799,30 @@ int cs_sweep_stats_finish(const cs_sweep_plan* p, const int64_t* h_stats_i64, co
   });
 }
 
+int cs_sweep_stats_pack(const int64_t* d_stats_i64, const double* d_stats_f64, int rank, int world,
+                        int64_t* d_packed, void* stream) {
+  return guarded([&] {
+    need(d_stats_i64, "d_stats_i64");
+    need(d_stats_f64, "d_stats_f64");
+    need(d_packed, "d_packed");
+    if (world < 1 || rank < 0 || rank >= world) fail(kParameter, "rank must be within [0, world)");
+    char err[256] = {0};
+    if (csk_stats_pack(d_stats_i64, d_stats_f64, rank, world, d_packed, stream, err)) fail(kInternal, err);
+  });
+}
+
+int cs_sweep_stats_unpack(const int64_t* d_packed, int world, int64_t* d_stats_i64, double* d_stats_f64,
+                          void* stream) {
+  return guarded([&] {
+    need(d_packed, "d_packed");
+    need(d_stats_i64, "d_stats_i64");
+    need(d_stats_f64, "d_stats_f64");
+    if (world < 1) fail(kParameter, "world must be positive");
+    char err[256] = {0};
+    if (csk_stats_unpack(d_packed, world, d_stats_i64, d_stats_f64, stream, err)) fail(kInternal, err);
+  });
+}
+
 void cs_sweep_plan_free(cs_sweep_plan* p) { delete p; }
 
 int cs_graph_generate_model(const char* model, uint64_t seed, cs_graph** out) {

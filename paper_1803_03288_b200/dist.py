@@ -18,6 +18,25 @@ MIN_KEYS = (0, 4)  # CS_DSTATS_I64 words holding min keys (makespan, iteration t
 MAX_KEYS = (1, 5)  # ... and max keys; every other word is summed
 
 
+def packed_words(world: int) -> int:
+    """include/commsched.h CS_PACKED_WORDS."""
+    return 6 * world + 2006
+
+
+def reduce_stats_device(lib, i64, f64, rank: int, world: int, buf, stream: int = 0):
+    """The same reduction on CUDA tensors through the library's pack/unpack
+    kernels (cs_sweep_stats_pack / _unpack): two tiny launches around the one
+    all-reduce, all on `stream` (a cudaStream_t)."""
+    import torch.distributed as dist
+    if world == 1:
+        return i64, f64
+    n = packed_words(world)
+    lib.call("cs_sweep_stats_pack", i64.data_ptr(), f64.data_ptr(), rank, world, buf.data_ptr(), stream)
+    dist.all_reduce(buf[:n])
+    lib.call("cs_sweep_stats_unpack", buf.data_ptr(), world, i64.data_ptr(), f64.data_ptr(), stream)
+    return i64, f64
+
+
 def reduce_stats(i64, f64, rank: int, world: int, buf=None):
     """In-place all-reduce of one step's statistics: ONE SUM all-reduce.
 
