@@ -863,6 +863,166 @@ __global__ void __launch_bounds__(1024) tac_cluster_kernel(TacArgs a, int per) {
   }
 }
 
+// TAC on one thread-block cluster with every per-round value in distributed
+// shared memory. CTA k of cs owns recv columns [k*per, (k+1)*per) (P and T
+// in its shared memory, a thread keeps kOwn columns' amended M+ in
+// registers) and the groups g with g % cs == k (cnt, M, owner XOR); every
+// CTA keeps a replica of the outstanding-column bitset, so the lowest
+// outstanding column is tracked locally. A round: amended M+ of the owned
+// columns from the groups' owners (DSMEM loads), the find-first chain (one
+// cluster-wide min per step over a 3-slot ring of per-CTA winner records
+// {column, P, T, M+}), the retire spread over the cluster (DSMEM
+// read-modify-writes of the retired column's groups, DSMEM atomics into the
+// owners' P), one cluster barrier. Nothing on the round's critical path
+// touches global memory but the retired column's group list.
+struct TacRec {
+  long long P, T, mp;
+  int c, pad;
+};
+
+__host__ __device__ inline size_t tac_dsm_smem(int per, int gper, int R) {
+  return 20ull * per + 16ull * gper + 4ull * ((R + 31) / 32) + 3ull * sizeof(TacRec) + 64;
+}
+
+template <int kOwn>
+__global__ void __launch_bounds__(1024) tac_dsm_kernel(TacArgs a, int per, int gper, int ngroups) {
+  cg::cluster_group cluster = cg::this_cluster();
+  extern __shared__ __align__(16) char dsm[];
+  __shared__ int bred[3];
+  __shared__ TacRec bcast;
+  int sp = 0, q = 0;
+  const int R = a.R, cs = static_cast<int>(cluster.num_blocks());
+  const int rank = static_cast<int>(cluster.block_rank());
+  const int base = rank * per, n_own = max(0, min(per, R - base));
+  auto* P_s = reinterpret_cast<long long*>(dsm);          // [per]
+  auto* T_s = P_s + per;                                   // [per]
+  auto* gM = reinterpret_cast<long long*>(T_s + per);      // [gper] groups g = rank + cs*l
+  auto* gcnt = reinterpret_cast<int*>(gM + gper);          // [gper]
+  auto* gxr = gcnt + gper;                                 // [gper]
+  auto* live = reinterpret_cast<uint32_t*>(gxr + gper);    // [(R+31)/32] replicated
+  auto* rec = reinterpret_cast<TacRec*>(live + (R + 31) / 32);  // 3-slot ring
+  auto* g1_s = reinterpret_cast<int*>(rec + 3);           // [per] single successor group, -1 several, -2 none
+  for (int j = threadIdx.x; j < n_own; j += blockDim.x) {
+    P_s[j] = a.P[base + j];
+    T_s[j] = a.tcol[base + j];
+    const int e0 = a.succ_off[base + j], e1 = a.succ_off[base + j + 1];
+    g1_s[j] = e1 - e0 == 1 ? a.succ[e0] : (e1 == e0 ? -2 : -1);
+  }
+  for (int l = threadIdx.x; l < gper; l += blockDim.x) {
+    const int g = rank + cs * l;
+    gM[l] = g < ngroups ? a.M[g] : 0;
+    gcnt[l] = g < ngroups ? a.cnt[g] : 0;
+    gxr[l] = g < ngroups ? a.xr[g] : 0;
+  }
+  for (int w = threadIdx.x; w < (R + 31) / 32; w += blockDim.x) {
+    uint32_t bits = 0;
+    for (int b = 0; b < 32 && w * 32 + b < R; ++b) bits |= (a.out[w * 32 + b] ? 1u : 0u) << b;
+    live[w] = bits;
+  }
+  if (threadIdx.x < 3) {
+    bred[threadIdx.x] = 0x7fffffff;
+    rec[threadIdx.x].c = 0x7fffffff;
+  }
+  cluster.sync();  // every CTA's slices and rings ready
+  auto Mg = [&](int g) -> long long {  // M of group g, at its owner
+    return *cluster.map_shared_rank(&gM[g / cs], g % cs);
+  };
+  auto mplus = [&](int c) -> long long {  // owned or remote column c
+    const int o = c / per;
+    const int g1 = *cluster.map_shared_rank(&g1_s[c - o * per], o);
+    if (g1 >= 0) return Mg(g1);
+    if (g1 == -2) return kInf;
+    long long m = kInf;
+    for (int32_t e = a.succ_off[c]; e < a.succ_off[c + 1]; ++e) m = min(m, Mg(a.succ[e]));
+    return m;
+  };
+  __shared__ long long first_p, first_mp;  // the incumbent's values, fetched once per CTA
+  auto is_live = [&](int c) { return (live[c >> 5] >> (c & 31)) & 1u; };
+  int first = 0;
+  while (first < R && !is_live(first)) ++first;
+  const int tid = rank * blockDim.x + threadIdx.x, nthreads = cs * blockDim.x;
+  for (int round = 0; round < R; ++round) {
+    // owned columns: amended M+ of this round in registers (P and T are
+    // read from this CTA's shared memory where they are compared)
+    long long mk[kOwn];
+#pragma unroll
+    for (int k = 0; k < kOwn; ++k) {
+      const int j = threadIdx.x + k * blockDim.x;
+      mk[k] = j < n_own && is_live(base + j) ? mplus(base + j) : kInf;
+    }
+    int best = first;
+    if (threadIdx.x == 0) {
+      first_p = *cluster.map_shared_rank(&P_s[best - (best / per) * per], best / per);
+      first_mp = mplus(best);
+    }
+    __syncthreads();
+    long long bp = first_p, bm = a.tcol[best], bmp = first_mp;
+    for (;;) {
+      int nxt = 0x7fffffff;
+      long long np = 0, nt = 0, nm = 0;
+#pragma unroll
+      for (int k = 0; k < kOwn; ++k) {
+        const int j = threadIdx.x + k * blockDim.x;
+        const int c = base + j;
+        if (j < n_own && c > best && c < nxt && is_live(c) && precedes(c, P_s[j], T_s[j], mk[k], best, bp, bm, bmp)) {
+          nxt = c;
+          np = P_s[j];
+          nt = T_s[j];
+          nm = mk[k];
+        }
+      }
+      const int slot = q % 3;
+      const int v = block_min_int(nxt, bred, sp);
+      if (nxt == v && v != 0x7fffffff) {
+        rec[slot].P = np;
+        rec[slot].T = nt;
+        rec[slot].mp = nm;
+      }
+      if (threadIdx.x == 0) rec[slot].c = v;
+      cluster.sync();
+      if (threadIdx.x < 32) {
+        int c = 0x7fffffff;
+        if (static_cast<int>(threadIdx.x) < cs) c = cluster.map_shared_rank(&rec[slot], threadIdx.x)->c;
+        const int m = __reduce_min_sync(~0u, c);
+        if (m != 0x7fffffff && c == m) bcast = *cluster.map_shared_rank(&rec[slot], threadIdx.x);
+        if (threadIdx.x == 0 && m == 0x7fffffff) bcast.c = m;
+      }
+      __syncthreads();
+      const TacRec w = bcast;
+      ++q;
+      if (w.c == 0x7fffffff) break;
+      best = w.c;
+      bp = w.P;
+      bm = w.T;
+      bmp = w.mp;
+      __syncthreads();  // bcast is rewritten by the next step
+    }
+    // retire the winner: its groups (each listed once) at their owners
+    const long long t = bm;
+    for (int32_t e = a.col_off[best] + tid; e < a.col_off[best + 1]; e += nthreads) {
+      const int32_t g = a.col[e];
+      const int o = g % cs, l = g / cs;
+      int* cp = cluster.map_shared_rank(&gcnt[l], o);
+      const int k = --*cp;
+      *cluster.map_shared_rank(&gM[l], o) -= t;
+      int* xp = cluster.map_shared_rank(&gxr[l], o);
+      const int x = (*xp ^= best);
+      if (k == 1)
+        atomicAdd(reinterpret_cast<unsigned long long*>(cluster.map_shared_rank(&P_s[x - (x / per) * per], x / per)),
+                  a.wsum[g]);
+    }
+    if (threadIdx.x == 0) live[best >> 5] &= ~(1u << (best & 31));
+    if (tid == 0) {
+      a.prio[best] = round;
+      a.out[best] = 0;
+    }
+    cluster.sync();  // retire and the outstanding bit visible before the next round reads them
+    if (best == first)
+      do ++first;
+      while (first < R && !is_live(first));
+  }
+}
+
 // Shared setup for properties / tic / tac: rows, closure, group state,
 // column lists. `dur` per op (host).
 struct GroupState {
@@ -1173,9 +1333,52 @@ extern "C" int csk_tac(DeviceGraph* g, const int64_t* dur, int32_t* prio, char* 
   int32_t smem_rows = S.rw->nrows, smem_succ = static_cast<int>(S.rw->succ.size());
   const bool one_block_fits = tac_smem_bytes(smem_rows, R, smem_succ) <= 220 * 1024;
   bool launched = false;
+  // The DSMEM cluster kernel: every per-round value in the cluster's shared
+  // memory. TICTAC_TAC_DSM=0 disables it, =1 forces it (tests).
+  const char* dsm_env = std::getenv("TICTAC_TAC_DSM");
+  const bool dsm_force = dsm_env && std::atoi(dsm_env) == 1, dsm_off = dsm_env && std::atoi(dsm_env) == 0;
+  auto try_dsm = [&]() -> bool {
+    const int cs = kClusterMax, per = (R + cs - 1) / cs, gper = (smem_rows + cs - 1) / cs;
+    const int kown = (per + 1023) / 1024;
+    const size_t smem = tac_dsm_smem(per, gper, R);
+    // measured: 10^5 ops / 10^4 recvs 56 -> 47 ms (one column per thread);
+    // with seven columns per thread (10^6 / 10^5) the grid kernels' 103 SMs
+    // win (0.63 s against 1.34 s), so the default stops at two per thread
+    if (smem > 220 * 1024 || kown > 8 || (!dsm_force && kown > 2)) return false;
+    const void* fn = kown <= 1   ? reinterpret_cast<const void*>(tac_dsm_kernel<1>)
+                     : kown <= 2 ? reinterpret_cast<const void*>(tac_dsm_kernel<2>)
+                     : kown <= 4 ? reinterpret_cast<const void*>(tac_dsm_kernel<4>)
+                                 : reinterpret_cast<const void*>(tac_dsm_kernel<8>);
+    CK(allow_max_dynamic_smem(fn));
+    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(cs);
+    cfg.blockDim = dim3(1024);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = cs;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int nclusters = 0;
+    if (cudaOccupancyMaxActiveClusters(&nclusters, fn, &cfg) != cudaSuccess || nclusters < 1) {
+      cudaGetLastError();
+      return false;
+    }
+    if (kown <= 1) CK(cudaLaunchKernelEx(&cfg, tac_dsm_kernel<1>, a, per, gper, smem_rows));
+    else if (kown <= 2) CK(cudaLaunchKernelEx(&cfg, tac_dsm_kernel<2>, a, per, gper, smem_rows));
+    else if (kown <= 4) CK(cudaLaunchKernelEx(&cfg, tac_dsm_kernel<4>, a, per, gper, smem_rows));
+    else CK(cudaLaunchKernelEx(&cfg, tac_dsm_kernel<8>, a, per, gper, smem_rows));
+    if (trace) std::fprintf(stderr, "[tac] DSMEM cluster of %d CTAs, %d columns and %d groups each\n", cs, per, gper);
+    return true;
+  };
+  if (dsm_force || (!dsm_off && !cl_force && !forced_blocks && !one_block_fits)) launched = try_dsm();
   // (measured: 10^5 ops / 10^4 recvs 61 → 55 ms; at 10^6 / 10^5 the grid
   // kernels' memory parallelism over 100+ SMs wins, 0.80 s vs 1.23 s)
-  if (cl_force || (!cl_off && !forced_blocks && blocks == 1 && !one_block_fits)) launched = try_cluster();
+  if (!launched && (cl_force || (!cl_off && !forced_blocks && blocks == 1 && !one_block_fits)))
+    launched = try_cluster();
   if (launched) {
     // (cluster kernel in flight; completion below)
   } else if (blocks == 1) {

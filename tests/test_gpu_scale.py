@@ -73,10 +73,15 @@ def test_multiblock_tac_matches_single_block(orc):
     # whenever they fit)
     # "cl": one thread-block cluster (the default only where one block's
     # shared memory cannot hold the state)
-    for blocks in ("1", "1g", "1c", "2", "3", "7", "64", "cl"):
+    # "dsm": the cluster kernel with every per-round value in distributed
+    # shared memory (the default where one block's shared memory cannot hold
+    # the state)
+    for blocks in ("1", "1g", "1c", "2", "3", "7", "64", "cl", "dsm"):
         env = dict(os.environ)
         if blocks == "cl":
             env["TICTAC_TAC_CLUSTER"] = "1"
+        elif blocks == "dsm":
+            env["TICTAC_TAC_DSM"] = "1"
         else:
             env["TICTAC_TAC_BLOCKS"] = blocks.rstrip("gc")
         if blocks == "1g":
@@ -86,7 +91,8 @@ def test_multiblock_tac_matches_single_block(orc):
         r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, check=True,
                            env=env)
         res[blocks] = json.loads(r.stdout.strip().splitlines()[-1])
-    assert res["1"] == res["1g"] == res["1c"] == res["2"] == res["3"] == res["7"] == res["64"] == res["cl"]
+    assert res["1"] == res["1g"] == res["1c"] == res["2"] == res["3"] == res["7"] == res["64"] == res["cl"] \
+        == res["dsm"]
     for spec in ("layered:10000:1000", "layered:100000:10000"):
         assert res["64"][spec] == TAC_LARGE[spec]["sha256"]
 
