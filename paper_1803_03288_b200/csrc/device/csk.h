@@ -92,10 +92,14 @@ static inline int csk_key_bits(int64_t U) {
  * tables at offset w. seed derivation: worker graphs use the seed itself;
  * clusters use splitmix64(seed ^ phi*(w+1)) (cluster.cpp:112-113).
  * noise_thr != 0: gated reorder noise, a position swaps when the noise
- * stream's (output >> 11) < noise_thr (= the reference's unit() < p). */
+ * stream's (output >> 11) < noise_thr (= the reference's unit() < p).
+ * nch > 1 channels per worker (several parameter servers): chan [W][R] =
+ * channel of each recv column, send_total [W][nch]; such plans serve
+ * random sweeps only (csk_sweep_run). */
 SweepPlan* csk_sweep_plan(int32_t W, int32_t R, int32_t nc, const int64_t* d,
-                          const int32_t* first, const int64_t* pwsuf, const int64_t* send_total,
-                          int cluster, int64_t U, int64_t L, uint64_t noise_thr, char* err);
+                          const int32_t* first, const int64_t* pwsuf, int32_t nch, const int32_t* chan,
+                          const int64_t* send_total, int cluster, int64_t U, int64_t L, uint64_t noise_thr,
+                          char* err);
 /* General worker DAGs (recv-ancestor sets not nested): per
  * worker, recv durations d and single-recv class weights wr ([W][R]), record
  * weights wj ([W][nrec]), empty-set class weights w0 ([W]); the program

@@ -35,11 +35,13 @@ namespace tictac_dev {
 namespace {
 
 constexpr int kSweepThreads = 256;
+constexpr int kMaxChannelsDev = 4;  // channels per worker of chain_multi_kernel
 constexpr int kBins = 1000;
 
 struct ChainArgs {
   int W, R, stride;  // workers, recvs per worker, pwsuf stride (nc+1)
   int nc;
+  int nch;           // channels per worker (ctot / send_tot are [W][nch])
   const uint2* tab;         // [W][R] {first class, duration}
   const int64_t* pwsuf;     // [W][stride]
   const int64_t* ctot;      // [W]
@@ -502,6 +504,105 @@ __global__ void __launch_bounds__(kSweepThreads, 3) chain_sweep_kernel(ChainArgs
     const int64_t m = hi;  // worker graph: the makespan; cluster: iteration time
     if (a.makespans) a.makespans[idx] = m;
     acc.add(a, seed, m, hi, lo, s_hist, s_shist);
+  }
+  acc.flush(a, s_hist, s_shist);
+}
+
+// ---- workers with several channels (clusters with several parameter
+// servers): each channel runs its recvs back to back in the gate order
+// restricted to it, so a recv's completion c(r) is a prefix sum on its own
+// channel. With nested classes the ERD value over release times becomes
+//     T_cpu = max(S(0), max over recvs r of c(r) + S(first[r]))
+// (class j is released at max{c(r) : first[r] <= j}, and S is non-increasing
+// in j), a right-to-left pass over the stored shuffle with one suffix sum per
+// channel. Reorder noise permutes each channel's subsequence with one stream
+// across the channels in resource order (sim.cpp:94-114). tab[].x carries the
+// channel in bits 24..31.
+template <typename T, typename V, bool kNoisy>
+__global__ void __launch_bounds__(kSweepThreads, 3) chain_multi_kernel(ChainArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int R = a.R, W = a.W, nch = a.nch;
+  uint64_t* s_lim = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* s_mag = s_lim + (R + 2);
+  uint2* s_tab = reinterpret_cast<uint2*>(s_mag + (R + 2));
+  V* s_pw = reinterpret_cast<V*>(s_tab + W * R);
+  int* s_hist = reinterpret_cast<int*>(smem + sweep_table_bytes(R, W, a.stride, sizeof(V)));
+  const int nhist = (a.do_e ? 1 : 0) + (a.cluster ? 1 : 0);
+  int* s_shist = s_hist + (a.do_e ? kBins : 0);
+  uint32_t* s_items = reinterpret_cast<uint32_t*>(s_hist + nhist * kBins);
+  uint64_t* tables_ready = reinterpret_cast<uint64_t*>(smem + a.mbar_off);
+  if (threadIdx.x == 0) mbar_init(tables_ready, 1);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    mbar_expect_tx(tables_ready, a.blob_bytes);
+    bulk_g2s(smem, a.blob, a.blob_bytes, tables_ready);
+  }
+  for (int k = threadIdx.x; k < nhist * kBins; k += blockDim.x) s_hist[k] = 0;
+  mbar_wait(tables_ready, 0);
+  __syncthreads();
+  const Items<T> items{s_items + threadIdx.x};
+  StatAcc acc;
+  const int64_t nthreads = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; idx < a.count;
+       idx += nthreads) {
+    const uint64_t seed = a.seed_lo + static_cast<uint64_t>(idx);
+    int64_t hi = 0, lo = INT64_MAX;
+    NoiseState<kNoisy> noise;
+    if constexpr (kNoisy) noise.init(splitmix64(seed ^ kNoiseSalt));
+    for (int w = 0; w < W; ++w) {
+      const uint2* tab = s_tab + w * R;
+      const V* pw = s_pw + w * a.stride;
+      FoldT<V> f{0, 0, 0};
+      const uint64_t ws = a.cluster ? splitmix64(seed ^ (kPhi * static_cast<uint64_t>(w + 1))) : seed;
+      shuffle_fold<Items<T>, V, true>(ws, R, items, f, nullptr, V(0), nullptr, s_lim, s_mag);
+      if constexpr (kNoisy)
+        for (int ch = 0; ch < nch; ++ch) {
+          int prev = -1;
+          for (int pos = 0; pos < R; ++pos) {
+            T* p1 = items.at(pos);
+            if (static_cast<int>(tab[*p1].x >> 24) != ch) continue;
+            if (prev >= 0 && (noise.m.next() >> 11) < a.noise_thr) {
+              T* p0 = items.at(prev);
+              const T x = *p0;
+              *p0 = *p1;
+              *p1 = x;
+            }
+            prev = pos;
+          }
+        }
+      V ct[kMaxChannelsDev], sfx[kMaxChannelsDev];
+#pragma unroll
+      for (int ch = 0; ch < kMaxChannelsDev; ++ch) {
+        ct[ch] = ch < nch ? static_cast<V>(a.ctot[w * nch + ch]) : V(0);
+        sfx[ch] = 0;
+      }
+      V best = pw[0];  // S(0): every class's work after time 0
+      for (int pos = R - 1; pos >= 0; --pos) {
+        const uint2 e = tab[*items.at(pos)];
+        const int ch = static_cast<int>(e.x >> 24);
+        V c = 0;
+#pragma unroll
+        for (int k = 0; k < kMaxChannelsDev; ++k)
+          if (k == ch) c = ct[k] - sfx[k];
+        best = max(best, c + pw[e.x & 0xFFFFFFu]);
+#pragma unroll
+        for (int k = 0; k < kMaxChannelsDev; ++k)
+          if (k == ch) sfx[k] += static_cast<V>(e.y);
+      }
+      const int64_t tcpu = static_cast<int64_t>(best);
+      int64_t mw = tcpu;
+#pragma unroll
+      for (int k = 0; k < kMaxChannelsDev; ++k)
+        if (k < nch) {
+          const int64_t c64 = static_cast<int64_t>(ct[k]);
+          mw = max(mw, a.cluster ? max(c64, tcpu) + a.send_tot[w * nch + k] : c64);
+        }
+      if (a.worker_ms) a.worker_ms[idx * W + w] = mw;
+      hi = max(hi, mw);
+      lo = min(lo, mw);
+    }
+    if (a.makespans) a.makespans[idx] = hi;
+    acc.add(a, seed, hi, hi, lo, s_hist, s_shist);
   }
   acc.flush(a, s_hist, s_shist);
 }
@@ -1169,7 +1270,7 @@ __global__ void random_orders_kernel(int R, int S, const uint64_t* __restrict__ 
 using namespace tictac_dev;
 
 struct SweepPlan {
-  int W = 1, R = 0, nc = 0, cluster = 0, stride = 1, narrow = 0;
+  int W = 1, R = 0, nc = 0, cluster = 0, stride = 1, narrow = 0, nch = 1;
   int64_t U = 0, L = 0;
   void *tab = nullptr, *pwsuf = nullptr, *ctot = nullptr, *send = nullptr, *lim = nullptr, *mag = nullptr;
   void* blob = nullptr;  // shared-memory table image of the sweep kernels
@@ -1205,6 +1306,15 @@ static DagFn dag_fn(const SweepPlan* p, bool noisy) {
 
 using SweepFn = void (*)(ChainArgs);
 static SweepFn sweep_fn(const SweepPlan* p) {
+  if (p->nch > 1) {
+    const bool nz = p->noise_thr != 0;
+    if (p->R <= 256) {
+      if (nz) return p->narrow ? chain_multi_kernel<uint8_t, int32_t, true> : chain_multi_kernel<uint8_t, int64_t, true>;
+      return p->narrow ? chain_multi_kernel<uint8_t, int32_t, false> : chain_multi_kernel<uint8_t, int64_t, false>;
+    }
+    if (nz) return p->narrow ? chain_multi_kernel<uint16_t, int32_t, true> : chain_multi_kernel<uint16_t, int64_t, true>;
+    return p->narrow ? chain_multi_kernel<uint16_t, int32_t, false> : chain_multi_kernel<uint16_t, int64_t, false>;
+  }
   if (p->noise_thr) {
     if (p->R <= 256)
       return p->narrow ? chain_sweep_kernel<uint8_t, false, int32_t, true>
@@ -1218,11 +1328,16 @@ static SweepFn sweep_fn(const SweepPlan* p) {
 }
 
 extern "C" SweepPlan* csk_sweep_plan(int32_t W, int32_t R, int32_t nc, const int64_t* d,
-                                     const int32_t* first, const int64_t* pwsuf,
-                                     const int64_t* send_total, int cluster, int64_t U, int64_t L,
-                                     uint64_t noise_thr, char* err) {
+                                     const int32_t* first, const int64_t* pwsuf, int32_t nch,
+                                     const int32_t* chan, const int64_t* send_total, int cluster, int64_t U,
+                                     int64_t L, uint64_t noise_thr, char* err) {
   if (ensure_device(err)) return nullptr;
+  if (nch < 1 || nch > kMaxChannelsDev || nc >= (1 << 24)) {
+    std::snprintf(err, 256, "sweep plan: unsupported channel or class count");
+    return nullptr;
+  }
   auto* p = new SweepPlan();
+  p->nch = nch;
   p->noise_thr = noise_thr;
   p->W = W;
   p->R = R;
@@ -1232,12 +1347,13 @@ extern "C" SweepPlan* csk_sweep_plan(int32_t W, int32_t R, int32_t nc, const int
   p->U = U;
   p->L = L;
   std::vector<uint2> tab(static_cast<size_t>(W) * R);
-  std::vector<int64_t> ctot(W, 0);
+  std::vector<int64_t> ctot(static_cast<size_t>(W) * nch, 0);
   for (int w = 0; w < W; ++w)
     for (int c = 0; c < R; ++c) {
-      tab[w * R + c] = make_uint2(static_cast<unsigned>(first[w * R + c]),
+      const int ch = nch > 1 ? chan[w * R + c] : 0;
+      tab[w * R + c] = make_uint2(static_cast<unsigned>(first[w * R + c]) | (static_cast<unsigned>(ch) << 24),
                                   static_cast<unsigned>(d[w * R + c]));
-      ctot[w] += d[w * R + c];
+      ctot[w * nch + ch] += d[w * R + c];
     }
   std::vector<uint64_t> lim(R + 2), mag(R + 2);
   for (int n = 0; n <= R + 1; ++n) bounded_consts(static_cast<uint64_t>(n), &lim[n], &mag[n]);
@@ -1248,8 +1364,8 @@ extern "C" SweepPlan* csk_sweep_plan(int32_t W, int32_t R, int32_t nc, const int
   };
   if (!up(&p->tab, tab.data(), tab.size() * sizeof(uint2)) ||
       !up(&p->pwsuf, pwsuf, sizeof(int64_t) * W * p->stride) ||
-      !up(&p->ctot, ctot.data(), sizeof(int64_t) * W) ||
-      !up(&p->send, send_total, sizeof(int64_t) * W) ||
+      !up(&p->ctot, ctot.data(), sizeof(int64_t) * W * nch) ||
+      !up(&p->send, send_total, sizeof(int64_t) * W * nch) ||
       !up(&p->lim, lim.data(), sizeof(uint64_t) * lim.size()) ||
       !up(&p->mag, mag.data(), sizeof(uint64_t) * mag.size())) {
     std::snprintf(err, 256, "CUDA allocation for the sweep plan failed");
@@ -1549,6 +1665,7 @@ static ChainArgs chain_args(SweepPlan* p) {
   a.R = p->R;
   a.stride = p->stride;
   a.nc = p->nc;
+  a.nch = p->nch;
   a.tab = static_cast<const uint2*>(p->tab);
   a.pwsuf = static_cast<const int64_t*>(p->pwsuf);
   a.ctot = static_cast<const int64_t*>(p->ctot);
@@ -1579,7 +1696,7 @@ extern "C" int csk_sweep_run(SweepPlan* p, uint64_t seed_lo, int64_t count, uint
   a.worker_ms = d_worker_makespans;
   a.i64 = reinterpret_cast<unsigned long long*>(d_i64);
   a.f64 = d_f64;
-  if (!std::getenv("TICTAC_SWEEP_NO_BULK")) {  // sweep_fn(p) folds in the image's width
+  if (!std::getenv("TICTAC_SWEEP_NO_BULK") || p->nch > 1) {  // sweep_fn(p) folds in the image's width
     a.blob = p->blob;
     a.blob_bytes = static_cast<uint32_t>(p->blob_bytes);
     a.mbar_off = static_cast<uint32_t>(p->smem - 16);
@@ -1617,7 +1734,7 @@ extern "C" int csk_sweep_run(SweepPlan* p, uint64_t seed_lo, int64_t count, uint
 
 extern "C" int csk_sweep_orders(SweepPlan* p, const int32_t* d_orders, int64_t n, void* stream,
                                 int64_t* d_makespans, char* err) {
-  if (p->W != 1) {
+  if (p->W != 1 || p->nch != 1) {
     std::snprintf(err, 256, "explicit orders need a worker graph plan");
     return 4;
   }
@@ -1659,7 +1776,7 @@ extern "C" int csk_sweep_orders(SweepPlan* p, const int32_t* d_orders, int64_t n
 }
 
 extern "C" int csk_sweep_lex(SweepPlan* p, int64_t first, int64_t count, int64_t* d_out, char* err) {
-  if (p->W != 1 || p->cluster || p->R > 20) {
+  if (p->W != 1 || p->cluster || p->R > 20 || p->nch != 1) {
     std::snprintf(err, 256, "lexicographic brute force needs a worker plan with at most 20 recvs");
     return 4;
   }

@@ -382,7 +382,7 @@ int cs_simulate(const cs_graph* g, const cs_oracle* o, const cs_schedule* s,
       closed = std::adjacent_find(pr.begin(), pr.end()) == pr.end();
     }
     if (closed) ctx = cached_sweep(g, o, p);
-    if (ctx && ctx->fast && !ctx->cluster) {
+    if (ctx && ctx->fast && !ctx->cluster && ctx->nch == 1) {
       // Closed form: the gate order is the recvs sorted by
       // (priority, id) (sim.cpp:95-104), then the reorder-noise swaps; recvs
       // are roots, so the violations are the swaps (A.4) and nothing is
@@ -493,7 +493,7 @@ int cs_brute_force(const cs_graph* g, const cs_oracle* o, const cs_sim_policy* p
     gp.gated = true;  // metrics.cpp:45-46
     if (!G.cluster() && p.noise == 0.0 && R >= 1 && R <= 20) {
       std::shared_ptr<SweepCtx> ctx = cached_sweep(g, o, gp);  // coverage/noise checks as simulate()
-      if (ctx->fast && !ctx->cluster && !ctx->noisy) {
+      if (ctx->fast && !ctx->cluster && !ctx->noisy && ctx->nch == 1) {
         int64_t perms = 1;
         for (int64_t k = 2; k <= R; ++k) perms *= k;
         int64_t best_m = 0, best_k = 0, nd = 0;
@@ -644,7 +644,7 @@ int cs_simulate_orders(const cs_graph* g, const cs_oracle* o, const int32_t* ord
     const Policy p = policy_of(policy);
     auto ctx = make_sweep(g->g, o->o, p);
     if (n == 0) return;
-    if (ctx->fast && !ctx->cluster) {  // rows validated by the kernel as it reads them
+    if (ctx->fast && !ctx->cluster && ctx->nch == 1) {  // rows validated by the kernel as it reads them
       // every row shares the choice seed, hence the same reorder-noise swaps
       // (positions whose noise draw fired, sim.cpp:106-114): applied to each
       // rank-order row they give its gate order; violations = swaps (A.4)

@@ -37,6 +37,9 @@ struct ChainTables {
   // with no recv ancestor
   std::vector<int64_t> wj, wr;
   int64_t w0 = 0;
+  int32_t nch = 1;
+  std::vector<int32_t> ch;          // per recv column: channel
+  std::vector<int64_t> send_by_ch;  // per channel: send time
 };
 
 // Straight-line program for general worker DAGs (sweep.cu dag_sweep_kernel):
@@ -74,7 +77,12 @@ struct ChainShape {
   std::vector<int32_t> sends;     // send ops (cluster workers)
   bool nested = true;             // chain classes (fold kernel), else `dag`
   DagProgram dag;
+  // channels of the worker (resource order; several when the cluster has
+  // several parameter servers): channel of every recv column / send op
+  int32_t nch = 1;
+  std::vector<int32_t> recv_ch, send_ch;
 };
+constexpr int32_t kMaxChannels = 4;
 
 // Compiles the join program from the classes' recv-ancestor bitsets (rep[j]
 // = a member op, sets ordered by size). Generators of class j: the classes
@@ -327,19 +335,26 @@ ChainShape chain_shape(const Graph& g, bool allow_sends) {
   const auto& ops = g.ops();
   const int32_t R = static_cast<int32_t>(g.recv_ops().size());
   if (R == 0) return no("no recv ops");
-  int32_t chan = -1, cpu = -1;
+  int32_t cpu = -1;
+  std::vector<int32_t> chans;  // channel resources, ascending (resource order)
   for (int32_t i = 0; i < n; ++i) {
     const int32_t r = g.res_of()[i];
     if (ops[i].kind == kRecv || ops[i].kind == kSend) {
       if (ops[i].kind == kSend && !allow_sends) return no("send ops on the worker");
-      if (chan >= 0 && chan != r) return no("more than one channel");
-      chan = r;
+      if (std::find(chans.begin(), chans.end(), r) == chans.end()) chans.push_back(r);
     } else {
       if (cpu >= 0 && cpu != r) return no("more than one compute unit");
       cpu = r;
     }
     if (ops[i].kind == kRecv && g.npred(i) > 0) return no("recv with predecessors");
   }
+  std::sort(chans.begin(), chans.end());
+  if (static_cast<int32_t>(chans.size()) > kMaxChannels) return no("more than four channels");
+  cs.nch = std::max<int32_t>(1, static_cast<int32_t>(chans.size()));
+  auto chan_index = [&](int32_t op) {
+    return static_cast<int32_t>(std::lower_bound(chans.begin(), chans.end(), g.res_of()[op]) - chans.begin());
+  };
+  for (int32_t c = 0; c < R; ++c) cs.recv_ch.push_back(chan_index(g.recv_ops()[c]));
   // recv-ancestor sets of every compute op (bitsets over recv columns)
   const int32_t W = (R + 63) / 64;
   if (static_cast<int64_t>(n) * W > (int64_t{1} << 27)) return no("graph too large for tables");
@@ -395,6 +410,7 @@ ChainShape chain_shape(const Graph& g, bool allow_sends) {
         if ((bits[static_cast<size_t>(rep[j]) * W + (c >> 6)] >> (c & 63)) & 1) cs.first[c] = j;
   } else {
     cs.nested = false;
+    if (cs.nch > 1) return no("recv-ancestor sets are not nested and the worker has several channels");
     std::string why;
     if (!dag_program(g, bits, W, col, rep, cs.class_of, cs.dag, why)) return no(why.c_str());
   }
@@ -416,6 +432,7 @@ ChainShape chain_shape(const Graph& g, bool allow_sends) {
       if (sinks.empty() || !std::includes(pre.begin(), pre.end(), sinks.begin(), sinks.end()))
         return no("send not released by the last compute");
       cs.sends.push_back(i);
+      cs.send_ch.push_back(chan_index(i));
     }
   }
   cs.ok = true;
@@ -584,6 +601,10 @@ bool chain_tables(const ChainShape& cs, const Graph& g, const std::vector<int64_
   }
   t.send_total = 0;
   for (int32_t i : cs.sends) t.send_total += dur[i];
+  t.nch = cs.nch;
+  t.ch = cs.recv_ch;
+  t.send_by_ch.assign(cs.nch, 0);
+  for (size_t k = 0; k < cs.sends.size(); ++k) t.send_by_ch[cs.send_ch[k]] += dur[cs.sends[k]];
   for (int64_t x : t.d)
     if (x >= (int64_t{1} << 31)) return why = "recv duration beyond 32 bits", false;
   return true;
@@ -705,6 +726,7 @@ std::unique_ptr<SweepCtx> make_sweep(std::shared_ptr<const Graph> g, const TimeO
       if (!(ok = chain_tables(*shape, *part, pd, tabs.back(), s->why))) break;
       if (!shape0) shape0 = shape;
       if (tabs.back().R != tabs[0].R || tabs.back().nc != tabs[0].nc || shape->nested != shape0->nested ||
+          shape->nch != shape0->nch ||
           (!shape->nested && (shape->dag.recs != shape0->dag.recs || shape->dag.rec_join != shape0->dag.rec_join))) {
         ok = false;
         s->why = "workers differ in shape";
@@ -719,25 +741,30 @@ std::unique_ptr<SweepCtx> make_sweep(std::shared_ptr<const Graph> g, const TimeO
                  shape0->dag.recs.size(), s->why.c_str());
   if (ok) {
     const int32_t W = static_cast<int32_t>(tabs.size()), R = tabs[0].R, nc = tabs[0].nc;
-    std::vector<int64_t> d, pw, send;
-    std::vector<int32_t> first;
+    std::vector<int64_t> d, pw, send, send_ch;
+    std::vector<int32_t> first, ch;
     for (const auto& t : tabs) {
       d.insert(d.end(), t.d.begin(), t.d.end());
       first.insert(first.end(), t.first.begin(), t.first.end());
       pw.insert(pw.end(), t.pwsuf.begin(), t.pwsuf.end());
       send.push_back(t.send_total);
+      ch.insert(ch.end(), t.ch.begin(), t.ch.end());
+      send_ch.insert(send_ch.end(), t.send_by_ch.begin(), t.send_by_ch.end());
     }
+    const int32_t nch = tabs[0].nch;
+    s->nch = nch;
     char err[256] = {0};
     uint64_t noise_thr = 0;  // unit() < p  <=>  (output >> 11) < p * 2^53 (integers below 2^53)
     if (s->noisy) {
       const double t = std::ldexp(p.noise, 53);
       noise_thr = t == std::floor(t) ? static_cast<uint64_t>(t) : static_cast<uint64_t>(std::floor(t)) + 1;
     }
-    const bool fail_ps = need_ps && !shape0->nested;
+    const bool fail_ps = need_ps && (!shape0->nested || nch > 1);
     if (fail_ps) {
     } else if (shape0->nested) {
-      s->plan = csk_sweep_plan(W, R, nc, d.data(), first.data(), pw.data(), send.data(),
-                               s->cluster ? 1 : 0, s->U, s->L, noise_thr, err);
+      s->plan = csk_sweep_plan(W, R, nc, d.data(), first.data(), pw.data(), nch, ch.data(),
+                               nch > 1 ? send_ch.data() : send.data(), s->cluster ? 1 : 0, s->U, s->L, noise_thr,
+                               err);
       if (s->plan && need_ps) {
         const PsShape& q = *pshape;
         std::vector<int64_t> sd, qd;
@@ -773,7 +800,9 @@ std::unique_ptr<SweepCtx> make_sweep(std::shared_ptr<const Graph> g, const TimeO
     }
     if (!fail_ps && !s->plan) fail(kInternal, err);
     s->fast = !fail_ps;
-    if (fail_ps) s->why = "parameter-server ops take time and the workers are not chain-class";
+    if (fail_ps)
+      s->why = nch > 1 ? "parameter-server ops take time and the workers have several channels"
+                       : "parameter-server ops take time and the workers are not chain-class";
     s->nc = nc;
     s->R = R;
   }

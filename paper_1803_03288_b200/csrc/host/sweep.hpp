@@ -26,6 +26,8 @@ struct SweepCtx {
   int32_t R = 0, nc = 0;
   bool dag = false;  // general-DAG program (not nested chain classes)
   bool ps = false;   // cluster send phase (parameter-server ops take time)
+  int32_t nch = 1;   // channels per worker (> 1: statistics sweeps only; explicit
+                     // orders and single runs use the exact replica)
   int32_t joins = 0, slots = 0, prog_words = 0;
   std::string why;  // why the closed form does not apply
   int device = 0;   // CUDA ordinal the plan lives on
