@@ -115,16 +115,19 @@ SweepPlan* csk_sweep_plan_dag(int32_t W, int32_t R, const int64_t* d, const int6
 void csk_sweep_plan_free(SweepPlan* p);
 /* Clusters whose parameter-server ops take time: extends a cluster chain
  * plan with the send phase (sweep.cu cluster_ps_kernel). Per worker S sends
- * (op-index order), recv_sb[c] = sends before recv column c in the
- * channel's op-index order, send durations [W][S], send successors (PS op
- * indices, CSR over w*S + s), Q PS ops in op-index order (durations,
- * predecessor counts, successors CSR), ps_slot = worker channels before the
- * PS compute resource in resource order. csk_sweep_run then simulates full
- * makespans (makespans, per-worker makespans, statistics over the makespan). */
-int csk_sweep_plan_add_ps(SweepPlan* p, int32_t S, const int16_t* recv_sb, const int64_t* send_d,
-                          const int32_t* send_succ_off, const int16_t* send_succ, int32_t Q,
+ * (op-index order) over the plan's nch channels (ch_mask [nch][ceil(S/32)]),
+ * recv_sb[c] = the worker's sends before recv column c in op-index order,
+ * send durations [W][S], send successors (PS op indices, CSR over w*S + s),
+ * Q PS ops in op-index order (durations, predecessor counts, successors CSR)
+ * on nps cores (core_mask [nps][ceil(Q/32)]), and the active resources in
+ * resource order (slots: core k -> -1-k, channel ch of worker w -> w*nch+ch).
+ * csk_sweep_run then simulates full makespans (makespans, per-worker
+ * makespans, statistics over the makespan). */
+int csk_sweep_plan_add_ps(SweepPlan* p, int32_t S, const int16_t* recv_sb, const uint32_t* ch_mask,
+                          const int64_t* send_d, const int32_t* send_succ_off, const int16_t* send_succ, int32_t Q,
                           const int64_t* ps_d, const uint8_t* ps_missing, const int32_t* ps_succ_off,
-                          const int16_t* ps_succ, int32_t ps_slot, char* err);
+                          const int16_t* ps_succ, int32_t nps, const uint32_t* core_mask, int32_t nslot,
+                          const int32_t* slots, char* err);
 /* Host-to-device bytes the plan's construction copied (tables, images). */
 int64_t csk_sweep_plan_uploaded(const SweepPlan* p);
 /* Stats layout documented in include/commsched.h (CS_DSTATS_*). */

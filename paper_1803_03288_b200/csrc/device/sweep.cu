@@ -851,30 +851,32 @@ __global__ void __launch_bounds__(kDagThreads) dag_sweep_kernel(ChainArgs a, Dag
 // ---- clusters whose parameter-server ops take time ----------------------
 //
 // With PS ops of positive duration the full makespan depends on the order in
-// which each worker's channel sends its gradients, which the reference picks
+// which each worker's channels send its gradients, which the reference picks
 // with draws from the run's shared choice stream (sim.cpp:163-186: the sends
 // are unprioritized, so every ready send is a candidate), and on the PS
-// server's choices among ready PS ops (again draws). Everything before a
+// cores' choices among ready PS ops (again draws). Everything before a
 // worker's last compute op completes is still SURVEY A.2: on chain-class
 // workers whose compute ops are totally ordered there are no draws there
-// (one candidate at a time on the core; the channel admits only the next
-// recv in gate order, the sends are not ready yet), the recv completions are
-// prefix sums of the gate order and the release of the sends is the fold's
-// T_cpu. So a run is: per worker the shuffle and the fold (as above), then an
-// exact replica of sim.cpp:194-233 restricted to the resources that can draw
-// — the PS core and each worker's channel after its release — with the
-// reference's round structure (completions at t, then passes of try_start in
-// resource order + same-time completions of zero-duration ops until nothing
-// changes). Candidates come in op-index order: a channel's are its unsent
-// ready sends plus the next recv in gate order (the only admitted one),
-// the PS core's are its ready ops. Host checks (csrc/host/sweep.cpp): one PS
-// device with one compute unit fed only by sends, workers as above, the
-// worker's last compute op of positive duration (its completion, hence the
-// release of the sends, happens at the start of a time step).
+// (one candidate at a time on the core; a channel admits only its next recv
+// in gate order, the sends are not ready yet), each channel's recv
+// completions are prefix sums of its gate order and the release of the
+// sends is the fold's T_cpu (the multi-channel form of chain_multi_kernel).
+// So a run is: per worker the shuffle and the fold, then an exact replica of
+// sim.cpp:194-233 restricted to the resources that can draw — the PS cores
+// and each released channel — with the reference's round structure
+// (completions at t, then passes of try_start in resource order + same-time
+// completions of zero-duration ops until nothing changes). Candidates come
+// in op-index order: a channel's are its unsent ready sends plus its next
+// recv in gate order (the only admitted one), a PS core's are its ready ops.
+// Host checks (csrc/host/sweep.cpp): PS devices with one compute unit each,
+// fed only by sends, workers as above, every worker's last compute op of
+// positive duration (its completion, hence the release of the sends,
+// happens at the start of a time step).
 struct PsArgs {
-  int S, Q, ps_slot;
+  int S, Q, nps, nslot;           // sends per worker, PS ops, PS cores, active resources
   int sw, qw;                     // 32-bit words of a send bitset / a PS-op bitset
-  const int16_t* recv_sb;         // [R] sends before recv column c in channel order
+  const int16_t* recv_sb;         // [R] the worker's sends before recv column c (op-index order)
+  const uint32_t* ch_mask;        // [nch][sw] sends on each channel
   const int64_t* send_d;          // [W][S]
   const int32_t* send_succ_off;   // [W*S + 1]
   const int16_t* send_succ;       // PS op indices
@@ -882,23 +884,27 @@ struct PsArgs {
   const uint8_t* ps_missing;      // [Q] predecessor counts
   const int32_t* ps_succ_off;     // [Q + 1]
   const int16_t* ps_succ;
+  const uint32_t* core_mask;      // [nps][qw] PS ops of each core
+  const int32_t* slots;           // [nslot] resource order: PS core k -> -1 - k, channel (w, ch) -> w * nch + ch
 };
 constexpr int kPsThreads = 64;
 
 // per thread: gate orders (W x R items), pending-send bits (W x sw words),
 // PS missing counts (Q bytes), PS ready bits (qw words), worker scalars
-// (9 words each)
-__host__ __device__ inline size_t ps_thread_bytes(int W, int R, int S, int Q, size_t tb) {
+// (5 words: release time, device end, released), channel scalars (4 words:
+// end, running, next gate position), core scalars (3 words: op, end)
+__host__ __device__ inline size_t ps_thread_bytes(int W, int R, int S, int Q, int nch, int nps, size_t tb) {
   const int per = tb == 1 ? 4 : 2;
   return 4 * (static_cast<size_t>(W) * ((R + per - 1) / per) + static_cast<size_t>(W) * ((S + 31) / 32) +
-              static_cast<size_t>((Q + 3) / 4) + static_cast<size_t>((Q + 31) / 32) + 9 * static_cast<size_t>(W));
+              static_cast<size_t>((Q + 3) / 4) + static_cast<size_t>((Q + 31) / 32) + 5 * static_cast<size_t>(W) +
+              4 * static_cast<size_t>(W) * nch + 3 * static_cast<size_t>(nps));
 }
 
 template <typename T, typename V, bool kNoisy>
 __global__ void __launch_bounds__(kPsThreads) cluster_ps_kernel(ChainArgs a, PsArgs q) {
   constexpr int NT = kPsThreads;
   extern __shared__ __align__(16) unsigned char smem[];
-  const int R = a.R, W = a.W, S = q.S, Q = q.Q;
+  const int R = a.R, W = a.W, S = q.S, Q = q.Q, nch = a.nch, nps = q.nps;
   uint64_t* s_lim = reinterpret_cast<uint64_t*>(smem);
   const int nk = max(S + 2, Q + 1) + 1;  // bounded() constants for n < nk
   uint64_t* s_mag = s_lim + nk;
@@ -914,21 +920,23 @@ __global__ void __launch_bounds__(kPsThreads) cluster_ps_kernel(ChainArgs a, PsA
   uint32_t* qmiss_base = pend + static_cast<size_t>(W) * q.sw * NT;  // Q bytes
   const Items<uint8_t, NT> qmiss{qmiss_base};
   uint32_t* qready = qmiss_base + static_cast<size_t>((Q + 3) / 4) * NT;  // qw words
-  uint32_t* wsc = qready + static_cast<size_t>(q.qw) * NT;                // [w][9] words
-  // per-worker int64 fields (f: 0 release time T, 1 channel end, 2 device end)
-  // as two 32-bit halves at word offsets 9w + 2f, 9w + 2f + 1
-  auto ld64 = [&](int w, int f) -> int64_t {
-    const uint32_t lo = wsc[static_cast<size_t>(9 * w + 2 * f) * NT];
-    const uint32_t hi = wsc[static_cast<size_t>(9 * w + 2 * f + 1) * NT];
+  uint32_t* wsc = qready + static_cast<size_t>(q.qw) * NT;                // [w][5] words
+  uint32_t* csc = wsc + static_cast<size_t>(5 * W) * NT;                   // [w*nch + ch][4] words
+  uint32_t* ksc = csc + static_cast<size_t>(4 * W * nch) * NT;             // [k][3] words
+  auto ld64 = [&](uint32_t* base, int word) -> int64_t {
+    const uint32_t lo = base[static_cast<size_t>(word) * NT], hi = base[static_cast<size_t>(word + 1) * NT];
     return static_cast<int64_t>((static_cast<uint64_t>(hi) << 32) | lo);
   };
-  auto st64 = [&](int w, int f, int64_t v) {
-    wsc[static_cast<size_t>(9 * w + 2 * f) * NT] = static_cast<uint32_t>(v);
-    wsc[static_cast<size_t>(9 * w + 2 * f + 1) * NT] = static_cast<uint32_t>(static_cast<uint64_t>(v) >> 32);
+  auto st64 = [&](uint32_t* base, int word, int64_t v) {
+    base[static_cast<size_t>(word) * NT] = static_cast<uint32_t>(v);
+    base[static_cast<size_t>(word + 1) * NT] = static_cast<uint32_t>(static_cast<uint64_t>(v) >> 32);
   };
-  auto i32 = [&](int w, int f) -> int32_t& {  // f: 0 running (-1 idle, -2 recv, s send), 1 next recv, 2 released
-    return *reinterpret_cast<int32_t*>(&wsc[static_cast<size_t>(9 * w + 6 + f) * NT]);
+  auto w32 = [&](uint32_t* base, int word) -> int32_t& {
+    return *reinterpret_cast<int32_t*>(&base[static_cast<size_t>(word) * NT]);
   };
+  // worker w: T at 5w, device end at 5w+2, released at 5w+4
+  // channel i = w*nch + ch: end at 4i, running at 4i+2 (-1 idle, -2 recv, s send), next gate position at 4i+3
+  // core k: op at 3k, end at 3k+1
   uint64_t* tables_ready = reinterpret_cast<uint64_t*>(smem + a.mbar_off);
   if (threadIdx.x == 0) mbar_init(tables_ready, 1);
   __syncthreads();
@@ -949,46 +957,78 @@ __global__ void __launch_bounds__(kPsThreads) cluster_ps_kernel(ChainArgs a, PsA
     NoiseState<kNoisy> noise;
     if constexpr (kNoisy) noise.init(splitmix64(seed ^ kNoiseSalt));
     int64_t t = INT64_MAX, mk = 0;
-    // 1. per worker: gate order, T_cpu (fold), channel state at the release
+    // 1. per worker: gate order, T_cpu (fold), each channel's state at the release
     for (int w = 0; w < W; ++w) {
       const Items<T, NT> g = gate(w);
       const uint2* tab = s_tab + w * R;
       const V* pw = s_pw + w * a.stride;
-      const V ctot = static_cast<V>(a.ctot[w]);
-      FoldT<V> f{a.nc, 0, -1};
+      FoldT<V> f{0, 0, 0};
       const uint64_t ws = splitmix64(seed ^ (kPhi * static_cast<uint64_t>(w + 1)));
-      shuffle_fold<Items<T, NT>, V, true>(ws, R, g, f, tab, ctot, pw, s_lim, s_mag);
+      shuffle_fold<Items<T, NT>, V, true>(ws, R, g, f, nullptr, V(0), nullptr, s_lim, s_mag);
       if constexpr (kNoisy)
-        for (int pos = 1; pos < R; ++pos)
-          if ((noise.m.next() >> 11) < a.noise_thr) {
-            T* p0 = g.at(pos - 1);
+        for (int ch = 0; ch < nch; ++ch) {
+          int prev = -1;
+          for (int pos = 0; pos < R; ++pos) {
             T* p1 = g.at(pos);
-            const T x = *p0;
-            *p0 = *p1;
-            *p1 = x;
+            if (static_cast<int>(tab[*p1].x >> 24) != ch) continue;
+            if (prev >= 0 && (noise.m.next() >> 11) < a.noise_thr) {
+              T* p0 = g.at(prev);
+              const T x = *p0;
+              *p0 = *p1;
+              *p1 = x;
+            }
+            prev = pos;
           }
-      for (int pos = R - 1; pos >= 0; --pos) f.add(tab[*g.at(pos)], ctot, pw);
-      if (f.G > 0) f.best = max(f.best, pw[0]);
-      const int64_t T0 = f.best < 0 ? 0 : static_cast<int64_t>(f.best);
-      // recvs starting before T0 ran back to back before the release
-      int64_t c = 0;
-      int k = 0;
-      for (; k < R && c < T0; ++k) c += static_cast<int64_t>(tab[*g.at(k)].y);
-      const bool busy = k > 0 && c > T0;  // position k-1 still running at T0
-      st64(w, 0, T0);
-      st64(w, 1, busy ? c : 0);
-      st64(w, 2, busy ? c : T0);
-      i32(w, 0) = busy ? -2 : -1;
-      i32(w, 1) = k;
-      i32(w, 2) = 0;
-      mk = max(mk, busy ? c : T0);
+        }
+      V ct[kMaxChannelsDev], sfx[kMaxChannelsDev];
+#pragma unroll
+      for (int ch = 0; ch < kMaxChannelsDev; ++ch) {
+        ct[ch] = ch < nch ? static_cast<V>(a.ctot[w * nch + ch]) : V(0);
+        sfx[ch] = 0;
+      }
+      V best = pw[0];
+      for (int pos = R - 1; pos >= 0; --pos) {
+        const uint2 e = tab[*g.at(pos)];
+        const int ch = static_cast<int>(e.x >> 24);
+        V c = 0;
+#pragma unroll
+        for (int k = 0; k < kMaxChannelsDev; ++k)
+          if (k == ch) c = ct[k] - sfx[k];
+        best = max(best, c + pw[e.x & 0xFFFFFFu]);
+#pragma unroll
+        for (int k = 0; k < kMaxChannelsDev; ++k)
+          if (k == ch) sfx[k] += static_cast<V>(e.y);
+      }
+      const int64_t T0 = static_cast<int64_t>(best);
+      st64(wsc, 5 * w, T0);
+      int64_t dev = T0;
+      // per channel: recvs starting before T0 ran back to back before the release
+      for (int ch = 0; ch < nch; ++ch) {
+        int64_t c = 0;
+        int pos = 0, last = -1;
+        for (; pos < R; ++pos) {
+          const uint2 e = tab[*g.at(pos)];
+          if (static_cast<int>(e.x >> 24) != ch) continue;
+          if (c >= T0) break;
+          c += static_cast<int64_t>(e.y);
+          last = pos;
+        }
+        const int i = w * nch + ch;
+        const bool busy = last >= 0 && c > T0;  // the channel's last started recv still runs at T0
+        st64(csc, 4 * i, busy ? c : 0);
+        w32(csc, 4 * i + 2) = busy ? -2 : -1;
+        w32(csc, 4 * i + 3) = pos;  // next gate position to consider on this channel
+        if (busy) dev = max(dev, c);
+      }
+      st64(wsc, 5 * w + 2, dev);
+      w32(wsc, 5 * w + 4) = 0;
+      mk = max(mk, dev);
       t = min(t, T0);
       for (int x = 0; x < q.sw; ++x) pend[static_cast<size_t>(w * q.sw + x) * NT] = 0;
     }
     for (int x = 0; x < Q; ++x) *qmiss.at(x) = q.ps_missing[x];
     for (int x = 0; x < q.qw; ++x) qready[static_cast<size_t>(x) * NT] = 0;
-    int ps_run = -1;
-    int64_t ps_end = 0;
+    for (int k = 0; k < nps; ++k) w32(ksc, 3 * k) = -1;
     MtStream choice;
     choice.init(seed);
     auto draw = [&](int n) -> int {  // bounded(n) of the shared choice stream
@@ -998,77 +1038,83 @@ __global__ void __launch_bounds__(kPsThreads) cluster_ps_kernel(ChainArgs a, PsA
       while (v > s_lim[n]);
       return static_cast<int>(fastmod32(v, static_cast<uint32_t>(n), s_mag[n]));
     };
-    auto ps_complete = [&](int op) {
-      for (int e = q.ps_succ_off[op]; e < q.ps_succ_off[op + 1]; ++e) {
-        const int x = q.ps_succ[e];
-        uint8_t* m = qmiss.at(x);
-        if (--*m == 0) qready[static_cast<size_t>(x >> 5) * NT] |= 1u << (x & 31);
-      }
+    auto ps_ready = [&](int x) {
+      uint8_t* m = qmiss.at(x);
+      if (--*m == 0) qready[static_cast<size_t>(x >> 5) * NT] |= 1u << (x & 31);
     };
-    auto chan_complete = [&](int w) {
-      const int sid = i32(w, 0);
-      i32(w, 0) = -1;
+    auto core_complete = [&](int k) {
+      const int op = w32(ksc, 3 * k);
+      w32(ksc, 3 * k) = -1;
+      for (int e = q.ps_succ_off[op]; e < q.ps_succ_off[op + 1]; ++e) ps_ready(q.ps_succ[e]);
+    };
+    auto chan_complete = [&](int w, int i) {
+      const int sid = w32(csc, 4 * i + 2);
+      w32(csc, 4 * i + 2) = -1;
       if (sid < 0) return;  // a recv: nothing downstream after the release
       const int base = w * S + sid;
-      for (int e = q.send_succ_off[base]; e < q.send_succ_off[base + 1]; ++e) {
-        const int x = q.send_succ[e];
-        uint8_t* m = qmiss.at(x);
-        if (--*m == 0) qready[static_cast<size_t>(x >> 5) * NT] |= 1u << (x & 31);
-      }
+      for (int e = q.send_succ_off[base]; e < q.send_succ_off[base + 1]; ++e) ps_ready(q.send_succ[e]);
     };
-    auto ps_try = [&]() -> bool {
-      if (ps_run >= 0) return false;
+    auto core_try = [&](int k) -> bool {
+      if (w32(ksc, 3 * k) >= 0) return false;
+      const uint32_t* cm = q.core_mask + static_cast<size_t>(k) * q.qw;
       int n = 0;
-      for (int x = 0; x < q.qw; ++x) n += __popc(qready[static_cast<size_t>(x) * NT]);
+      for (int x = 0; x < q.qw; ++x) n += __popc(qready[static_cast<size_t>(x) * NT] & cm[x]);
       if (n == 0) return false;
       int j = draw(n);
       for (int x = 0;; ++x) {
-        uint32_t bits = qready[static_cast<size_t>(x) * NT];
+        const uint32_t bits = qready[static_cast<size_t>(x) * NT] & cm[x];
         const int cnt = __popc(bits);
         if (j < cnt) {
           const int b = nth_bit(bits, j);
-          qready[static_cast<size_t>(x) * NT] = bits & ~(1u << b);
-          ps_run = (x << 5) + b;
-          ps_end = t + q.ps_d[ps_run];
-          mk = max(mk, ps_end);
+          qready[static_cast<size_t>(x) * NT] &= ~(1u << b);
+          const int op = (x << 5) + b;
+          w32(ksc, 3 * k) = op;
+          const int64_t e = t + q.ps_d[op];
+          st64(ksc, 3 * k + 1, e);
+          mk = max(mk, e);
           return true;
         }
         j -= cnt;
       }
     };
-    auto chan_try = [&](int w) -> bool {
-      if (!i32(w, 2) || i32(w, 0) != -1) return false;
-      const int nr = i32(w, 1);
+    auto chan_try = [&](int w, int ch) -> bool {
+      const int i = w * nch + ch;
+      if (!w32(wsc, 5 * w + 4) || w32(csc, 4 * i + 2) != -1) return false;
       const Items<T, NT> g = gate(w);
-      const int rc = nr < R ? static_cast<int>(*g.at(nr)) : -1;  // next recv column (admitted)
+      const uint2* tab = s_tab + w * R;
+      int pos = w32(csc, 4 * i + 3);  // next recv of this channel in gate order
+      while (pos < R && static_cast<int>(tab[*g.at(pos)].x >> 24) != ch) ++pos;
+      w32(csc, 4 * i + 3) = pos;
+      const int rc = pos < R ? static_cast<int>(*g.at(pos)) : -1;
       uint32_t* pw_ = pend + static_cast<size_t>(w * q.sw) * NT;
+      const uint32_t* cm = q.ch_mask + static_cast<size_t>(ch) * q.sw;
       int ns = 0;
-      for (int x = 0; x < q.sw; ++x) ns += __popc(pw_[static_cast<size_t>(x) * NT]);
+      for (int x = 0; x < q.sw; ++x) ns += __popc(pw_[static_cast<size_t>(x) * NT] & cm[x]);
       const int n = ns + (rc >= 0 ? 1 : 0);
       if (n == 0) return false;
       int j = draw(n);
       int64_t d;
-      if (rc >= 0) {  // the recv's place among the candidates: pending sends before it
+      if (rc >= 0) {  // the recv's place among the candidates: this channel's pending sends before it
         const int sb = recv_sb[rc];
         int before = 0;
-        for (int x = 0; x < (sb >> 5); ++x) before += __popc(pw_[static_cast<size_t>(x) * NT]);
-        if (sb & 31) before += __popc(pw_[static_cast<size_t>(sb >> 5) * NT] & ((1u << (sb & 31)) - 1u));
+        for (int x = 0; x < (sb >> 5); ++x) before += __popc(pw_[static_cast<size_t>(x) * NT] & cm[x]);
+        if (sb & 31) before += __popc(pw_[static_cast<size_t>(sb >> 5) * NT] & cm[sb >> 5] & ((1u << (sb & 31)) - 1u));
         if (j == before) {
-          i32(w, 0) = -2;
-          i32(w, 1) = nr + 1;
-          d = static_cast<int64_t>(s_tab[w * R + rc].y);
+          w32(csc, 4 * i + 2) = -2;
+          w32(csc, 4 * i + 3) = pos + 1;
+          d = static_cast<int64_t>(tab[rc].y);
           goto started;
         }
         if (j > before) --j;
       }
       for (int x = 0;; ++x) {
-        uint32_t bits = pw_[static_cast<size_t>(x) * NT];
+        const uint32_t bits = pw_[static_cast<size_t>(x) * NT] & cm[x];
         const int cnt = __popc(bits);
         if (j < cnt) {
           const int b = nth_bit(bits, j);
-          pw_[static_cast<size_t>(x) * NT] = bits & ~(1u << b);
+          pw_[static_cast<size_t>(x) * NT] &= ~(1u << b);
           const int sid = (x << 5) + b;
-          i32(w, 0) = sid;
+          w32(csc, 4 * i + 2) = sid;
           d = q.send_d[w * S + sid];
           break;
         }
@@ -1076,60 +1122,65 @@ __global__ void __launch_bounds__(kPsThreads) cluster_ps_kernel(ChainArgs a, PsA
       }
     started:
       const int64_t e = t + d;
-      st64(w, 1, e);
-      if (e > ld64(w, 2)) st64(w, 2, e);
+      st64(csc, 4 * i, e);
+      if (e > ld64(wsc, 5 * w + 2)) st64(wsc, 5 * w + 2, e);
       mk = max(mk, e);
       return true;
     };
-    // 2. the send phase: sim.cpp:194-233 over the PS core and the released channels
+    auto complete_now = [&]() -> bool {  // every op ending at t (completions never draw)
+      bool any = false;
+      for (int k = 0; k < nps; ++k)
+        if (w32(ksc, 3 * k) >= 0 && ld64(ksc, 3 * k + 1) == t) {
+          core_complete(k);
+          any = true;
+        }
+      for (int w = 0; w < W; ++w)
+        for (int ch = 0; ch < nch; ++ch) {
+          const int i = w * nch + ch;
+          if (w32(csc, 4 * i + 2) != -1 && ld64(csc, 4 * i) == t) {
+            chan_complete(w, i);
+            any = true;
+          }
+        }
+      return any;
+    };
+    // 2. the send phase: sim.cpp:194-233 over the PS cores and the released channels
     while (t != INT64_MAX) {
-      // completions at t (positive durations: the op started before t)
-      if (ps_run >= 0 && ps_end == t) {
-        const int op = ps_run;
-        ps_run = -1;
-        ps_complete(op);
-      }
-      for (int w = 0; w < W; ++w) {
-        if (!i32(w, 2) && ld64(w, 0) == t) {  // last compute op done: the sends are ready
-          i32(w, 2) = 1;
+      for (int w = 0; w < W; ++w)  // last compute op done: the sends are ready
+        if (!w32(wsc, 5 * w + 4) && ld64(wsc, 5 * w) == t) {
+          w32(wsc, 5 * w + 4) = 1;
           uint32_t* pw_ = pend + static_cast<size_t>(w * q.sw) * NT;
           for (int x = 0; x < q.sw; ++x) {
             const int lo = x << 5;
             pw_[static_cast<size_t>(x) * NT] = S - lo >= 32 ? ~0u : ((1u << (S - lo)) - 1u);
           }
         }
-        if (i32(w, 0) != -1 && ld64(w, 1) == t) chan_complete(w);
-      }
+      complete_now();
       bool progress = true;
       while (progress) {  // passes: try_start in resource order, then same-time completions
         progress = false;
-        for (int i = 0; i <= W; ++i) {
-          if (i == q.ps_slot) progress = ps_try() || progress;
-          if (i < W) progress = chan_try(i) || progress;
+        for (int si = 0; si < q.nslot; ++si) {
+          const int sl = q.slots[si];
+          if (sl < 0) progress = core_try(-1 - sl) || progress;
+          else progress = chan_try(sl / nch, sl % nch) || progress;
         }
-        if (ps_run >= 0 && ps_end == t) {
-          const int op = ps_run;
-          ps_run = -1;
-          ps_complete(op);
-          progress = true;
-        }
-        for (int w = 0; w < W; ++w)
-          if (i32(w, 0) != -1 && ld64(w, 1) == t) {
-            chan_complete(w);
-            progress = true;
-          }
+        progress = complete_now() || progress;
       }
       int64_t nt = INT64_MAX;
-      if (ps_run >= 0) nt = ps_end;
+      for (int k = 0; k < nps; ++k)
+        if (w32(ksc, 3 * k) >= 0) nt = min(nt, ld64(ksc, 3 * k + 1));
       for (int w = 0; w < W; ++w) {
-        if (!i32(w, 2)) nt = min(nt, ld64(w, 0));
-        if (i32(w, 0) != -1) nt = min(nt, ld64(w, 1));
+        if (!w32(wsc, 5 * w + 4)) nt = min(nt, ld64(wsc, 5 * w));
+        for (int ch = 0; ch < nch; ++ch) {
+          const int i = w * nch + ch;
+          if (w32(csc, 4 * i + 2) != -1) nt = min(nt, ld64(csc, 4 * i));
+        }
       }
       t = nt;
     }
     int64_t hi = 0, lo = INT64_MAX;
     for (int w = 0; w < W; ++w) {
-      const int64_t mw = ld64(w, 2);
+      const int64_t mw = ld64(wsc, 5 * w + 2);
       if (a.worker_ms) a.worker_ms[idx * W + w] = mw;
       hi = max(hi, mw);
       lo = min(lo, mw);
@@ -1532,10 +1583,11 @@ static PsFn ps_fn(const SweepPlan* p) {
   return p->narrow ? cluster_ps_kernel<uint16_t, int32_t, false> : cluster_ps_kernel<uint16_t, int64_t, false>;
 }
 
-extern "C" int csk_sweep_plan_add_ps(SweepPlan* p, int32_t S, const int16_t* recv_sb, const int64_t* send_d,
-                                     const int32_t* send_succ_off, const int16_t* send_succ, int32_t Q,
-                                     const int64_t* ps_d, const uint8_t* ps_missing, const int32_t* ps_succ_off,
-                                     const int16_t* ps_succ, int32_t ps_slot, char* err) {
+extern "C" int csk_sweep_plan_add_ps(SweepPlan* p, int32_t S, const int16_t* recv_sb, const uint32_t* ch_mask,
+                                     const int64_t* send_d, const int32_t* send_succ_off, const int16_t* send_succ,
+                                     int32_t Q, const int64_t* ps_d, const uint8_t* ps_missing,
+                                     const int32_t* ps_succ_off, const int16_t* ps_succ, int32_t nps,
+                                     const uint32_t* core_mask, int32_t nslot, const int32_t* slots, char* err) {
   if (p->dag || !p->cluster) {
     std::snprintf(err, 256, "the send phase extends cluster chain plans only");
     return 4;
@@ -1552,11 +1604,13 @@ extern "C" int csk_sweep_plan_add_ps(SweepPlan* p, int32_t S, const int16_t* rec
   PsArgs& a = p->psa;
   a.S = S;
   a.Q = Q;
-  a.ps_slot = ps_slot;
+  a.nps = nps;
+  a.nslot = nslot;
   a.sw = (S + 31) / 32;
   a.qw = (Q + 31) / 32;
   const int32_t nss = send_succ_off[W * S], nqs = ps_succ_off[Q];
   a.recv_sb = static_cast<const int16_t*>(up(recv_sb, 2ull * R));
+  a.ch_mask = static_cast<const uint32_t*>(up(ch_mask, 4ull * p->nch * a.sw));
   a.send_d = static_cast<const int64_t*>(up(send_d, 8ull * W * S));
   a.send_succ_off = static_cast<const int32_t*>(up(send_succ_off, 4ull * (W * S + 1)));
   a.send_succ = static_cast<const int16_t*>(up(send_succ, 2ull * nss));
@@ -1564,6 +1618,8 @@ extern "C" int csk_sweep_plan_add_ps(SweepPlan* p, int32_t S, const int16_t* rec
   a.ps_missing = static_cast<const uint8_t*>(up(ps_missing, static_cast<size_t>(Q)));
   a.ps_succ_off = static_cast<const int32_t*>(up(ps_succ_off, 4ull * (Q + 1)));
   a.ps_succ = static_cast<const int16_t*>(up(ps_succ, 2ull * nqs));
+  a.core_mask = static_cast<const uint32_t*>(up(core_mask, 4ull * nps * a.qw));
+  a.slots = static_cast<const int32_t*>(up(slots, 4ull * nslot));
   for (void* x : p->ps_bufs)
     if (!x) {
       std::snprintf(err, 256, "CUDA allocation for the send-phase tables failed");
@@ -1603,7 +1659,7 @@ extern "C" int csk_sweep_plan_add_ps(SweepPlan* p, int32_t S, const int16_t* rec
   }
   const int nhist = (p->U != p->L ? 1 : 0) + 1;
   p->ps_smem = round16(p->ps_blob_bytes + 4ull * nhist * kBins +
-                       kPsThreads * ps_thread_bytes(W, R, S, Q, R <= 256 ? 1 : 2)) + 16;
+                       kPsThreads * ps_thread_bytes(W, R, S, Q, p->nch, nps, R <= 256 ? 1 : 2)) + 16;
   int dev = 0, sms = 148, occ = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

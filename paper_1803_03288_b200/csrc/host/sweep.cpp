@@ -15,6 +15,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <array>
+#include <map>
 #include <set>
 #include <thread>
 
@@ -444,8 +445,9 @@ ChainShape chain_shape(const Graph& g, bool allow_sends) {
 struct PsShape {
   bool ok = false;
   std::string why;
-  int32_t S = 0, Q = 0, ps_slot = 0;
-  std::vector<int16_t> recv_sb;                // [R] sends before recv column c (channel op order)
+  int32_t S = 0, Q = 0, nps = 0, nch = 1;
+  std::vector<int16_t> recv_sb;                // [R] the worker's sends before recv column c (op-index order)
+  std::vector<uint32_t> ch_mask;               // [nch][sw] sends on each channel
   std::vector<std::vector<int32_t>> sends;      // per worker: send ops (graph index), op-index order
   std::vector<int32_t> send_succ_off;           // [W*S + 1]
   std::vector<int16_t> send_succ;               // PS op indices
@@ -453,6 +455,8 @@ struct PsShape {
   std::vector<uint8_t> ps_missing;              // predecessor counts
   std::vector<int32_t> ps_succ_off;
   std::vector<int16_t> ps_succ;
+  std::vector<uint32_t> core_mask;             // [nps][qw] PS ops of each core
+  std::vector<int32_t> slots;                  // resource order: core k -> -1-k, channel (w, ch) -> w*nch + ch
   std::vector<int32_t> last_compute;           // per worker: graph index of its last compute op
 };
 
@@ -467,7 +471,7 @@ PsShape ps_shape(const Graph& g, const std::vector<std::string>& workers) {
   std::unordered_map<std::string, int32_t> widx;
   for (size_t i = 0; i < workers.size(); ++i) widx[workers[i]] = static_cast<int32_t>(i);
   std::vector<int32_t> wof(n, -1), psix(n, -1);
-  int32_t ps_res = -1;
+  std::map<std::string, int32_t> ps_res;  // PS device -> its one resource
   for (int32_t i = 0; i < n; ++i) {
     auto it = widx.find(ops[i].res.device);
     if (it != widx.end()) {
@@ -475,14 +479,27 @@ PsShape ps_shape(const Graph& g, const std::vector<std::string>& workers) {
       continue;
     }
     if (transfer(ops[i].kind)) return no("transfer on a parameter-server device");
-    if (ps_res >= 0 && ps_res != g.res_of()[i]) return no("parameter-server ops on more than one resource");
-    ps_res = g.res_of()[i];
+    auto pr = ps_res.emplace(ops[i].res.device, g.res_of()[i]);
+    if (pr.second == false && pr.first->second != g.res_of()[i])
+      return no("a parameter-server device with more than one resource");
     psix[i] = static_cast<int32_t>(ps.ps_ops.size());
     ps.ps_ops.push_back(i);  // ascending graph index = op-index order
   }
   ps.Q = static_cast<int32_t>(ps.ps_ops.size());
+  ps.nps = static_cast<int32_t>(ps_res.size());
   if (ps.Q == 0) return no("no parameter-server ops");
   if (ps.Q >= (1 << 15)) return no("too many parameter-server ops");
+  if (ps.nps > 16) return no("more than 16 parameter servers");
+  std::vector<int32_t> core_res;  // resource of core k, cores in resource order
+  for (const auto& [dev, r] : ps_res) core_res.push_back(r);
+  std::sort(core_res.begin(), core_res.end());
+  const int32_t qw = (ps.Q + 31) / 32;
+  ps.core_mask.assign(static_cast<size_t>(ps.nps) * qw, 0);
+  for (int32_t x = 0; x < ps.Q; ++x) {
+    const int32_t k = static_cast<int32_t>(std::lower_bound(core_res.begin(), core_res.end(),
+                                                            g.res_of()[ps.ps_ops[x]]) - core_res.begin());
+    ps.core_mask[static_cast<size_t>(k) * qw + (x >> 5)] |= 1u << (x & 31);
+  }
   for (int32_t x = 0; x < ps.Q; ++x) {
     const int32_t v = ps.ps_ops[x];
     int32_t np = 0;
@@ -505,45 +522,58 @@ PsShape ps_shape(const Graph& g, const std::vector<std::string>& workers) {
     }
     ps.ps_succ_off.push_back(static_cast<int32_t>(ps.ps_succ.size()));
   }
-  // per worker: channel ops in op-index order, sends, compute total order
+  // per worker: channels (resource order), sends, recvs, compute total order
   const int32_t W = static_cast<int32_t>(workers.size());
   ps.sends.assign(W, {});
-  std::vector<std::vector<int32_t>> recvs(W), comp(W);
-  std::vector<int32_t> chan_res(W, -1);
+  std::vector<std::vector<int32_t>> recvs(W), comp(W), chans(W);
   for (int32_t i = 0; i < n; ++i) {
     const int32_t w = wof[i];
     if (w < 0) continue;
     if (ops[i].kind == kSend) ps.sends[w].push_back(i);
     else if (ops[i].kind == kRecv) recvs[w].push_back(i);
     else comp[w].push_back(i);
-    if (transfer(ops[i].kind)) chan_res[w] = g.res_of()[i];
+    if (transfer(ops[i].kind) &&
+        std::find(chans[w].begin(), chans[w].end(), g.res_of()[i]) == chans[w].end())
+      chans[w].push_back(g.res_of()[i]);
   }
   ps.S = static_cast<int32_t>(ps.sends[0].size());
+  ps.nch = static_cast<int32_t>(chans[0].size());
   const int32_t R = static_cast<int32_t>(recvs[0].size());
+  const int32_t sw = (ps.S + 31) / 32;
   for (int32_t w = 0; w < W; ++w) {
-    if (static_cast<int32_t>(ps.sends[w].size()) != ps.S || static_cast<int32_t>(recvs[w].size()) != R)
+    std::sort(chans[w].begin(), chans[w].end());
+    if (static_cast<int32_t>(ps.sends[w].size()) != ps.S || static_cast<int32_t>(recvs[w].size()) != R ||
+        static_cast<int32_t>(chans[w].size()) != ps.nch)
       return no("workers differ in their transfers");
-    if (chan_res[w] < 0) return no("worker without a channel");
-    // recv_sb: sends before each recv column in op-index order, same on every worker
+    if (ps.nch == 0) return no("worker without a channel");
     std::vector<int16_t> sb(R);
     for (int32_t c = 0; c < R; ++c)
       sb[c] = static_cast<int16_t>(std::lower_bound(ps.sends[w].begin(), ps.sends[w].end(), recvs[w][c]) -
                                    ps.sends[w].begin());
-    if (w == 0) ps.recv_sb = sb;
-    else if (sb != ps.recv_sb) return no("workers differ in their channel op order");
+    std::vector<uint32_t> mask(static_cast<size_t>(ps.nch) * sw, 0);
+    for (int32_t x = 0; x < ps.S; ++x) {
+      const int32_t ch = static_cast<int32_t>(std::lower_bound(chans[w].begin(), chans[w].end(),
+                                                               g.res_of()[ps.sends[w][x]]) - chans[w].begin());
+      mask[static_cast<size_t>(ch) * sw + (x >> 5)] |= 1u << (x & 31);
+    }
+    if (w == 0) {
+      ps.recv_sb = sb;
+      ps.ch_mask = mask;
+    } else if (sb != ps.recv_sb || mask != ps.ch_mask) {
+      return no("workers differ in their channel op order");
+    }
     // compute ops totally ordered (so the core never has two candidates):
     // the longest path over compute->compute edges covers all of them
     if (comp[w].empty()) return no("worker without compute ops");
-    std::unordered_map<int32_t, int32_t> depth;
-    int32_t best = 0, last = -1;
-    for (int32_t v : comp[w]) depth[v] = 0;
-    // graph indices are not topological: relax in a topological order of the worker
-    std::vector<int32_t> miss(n, 0), order;
+    std::unordered_map<int32_t, int32_t> depth, miss;
+    for (int32_t v : comp[w]) depth[v] = 0, miss[v] = 0;
+    std::vector<int32_t> order;
     for (int32_t v : comp[w]) {
       for (int32_t e = g.pred_off()[v]; e < g.pred_off()[v + 1]; ++e)
         if (depth.count(g.pred_idx()[e])) ++miss[v];
       if (miss[v] == 0) order.push_back(v);
     }
+    int32_t best = 0, last = -1;
     for (size_t h = 0; h < order.size(); ++h) {
       const int32_t v = order[h];
       depth[v] += 1;
@@ -568,8 +598,13 @@ PsShape ps_shape(const Graph& g, const std::vector<std::string>& workers) {
     }
   }
   ps.send_succ_off.insert(ps.send_succ_off.begin(), 0);
+  // active resources in resource order: the PS cores and every worker channel
+  std::vector<std::pair<int32_t, int32_t>> act;  // (resource index, slot)
+  for (int32_t k = 0; k < ps.nps; ++k) act.emplace_back(core_res[k], -1 - k);
   for (int32_t w = 0; w < W; ++w)
-    if (chan_res[w] < ps_res) ++ps.ps_slot;
+    for (int32_t ch = 0; ch < ps.nch; ++ch) act.emplace_back(chans[w][ch], w * ps.nch + ch);
+  std::sort(act.begin(), act.end());
+  for (const auto& [r, sl] : act) ps.slots.push_back(sl);
   ps.ok = true;
   return ps;
 }
@@ -759,7 +794,7 @@ std::unique_ptr<SweepCtx> make_sweep(std::shared_ptr<const Graph> g, const TimeO
       const double t = std::ldexp(p.noise, 53);
       noise_thr = t == std::floor(t) ? static_cast<uint64_t>(t) : static_cast<uint64_t>(std::floor(t)) + 1;
     }
-    const bool fail_ps = need_ps && (!shape0->nested || nch > 1);
+    const bool fail_ps = need_ps && (!shape0->nested || pshape->nch != nch);
     if (fail_ps) {
     } else if (shape0->nested) {
       s->plan = csk_sweep_plan(W, R, nc, d.data(), first.data(), pw.data(), nch, ch.data(),
@@ -771,9 +806,10 @@ std::unique_ptr<SweepCtx> make_sweep(std::shared_ptr<const Graph> g, const TimeO
         for (const auto& sv : q.sends)
           for (int32_t x : sv) sd.push_back(s->dur[x]);
         for (int32_t x : q.ps_ops) qd.push_back(s->dur[x]);
-        if (csk_sweep_plan_add_ps(s->plan, q.S, q.recv_sb.data(), sd.data(), q.send_succ_off.data(),
-                                  q.send_succ.data(), q.Q, qd.data(), q.ps_missing.data(), q.ps_succ_off.data(),
-                                  q.ps_succ.data(), q.ps_slot, err)) {
+        if (csk_sweep_plan_add_ps(s->plan, q.S, q.recv_sb.data(), q.ch_mask.data(), sd.data(),
+                                  q.send_succ_off.data(), q.send_succ.data(), q.Q, qd.data(), q.ps_missing.data(),
+                                  q.ps_succ_off.data(), q.ps_succ.data(), q.nps, q.core_mask.data(),
+                                  static_cast<int32_t>(q.slots.size()), q.slots.data(), err)) {
           csk_sweep_plan_free(s->plan);
           s->plan = nullptr;
           fail(kInternal, err);
@@ -800,9 +836,7 @@ std::unique_ptr<SweepCtx> make_sweep(std::shared_ptr<const Graph> g, const TimeO
     }
     if (!fail_ps && !s->plan) fail(kInternal, err);
     s->fast = !fail_ps;
-    if (fail_ps)
-      s->why = nch > 1 ? "parameter-server ops take time and the workers have several channels"
-                       : "parameter-server ops take time and the workers are not chain-class";
+    if (fail_ps) s->why = "parameter-server ops take time and the workers are not chain-class";
     s->nc = nc;
     s->R = R;
   }

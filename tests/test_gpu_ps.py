@@ -32,6 +32,9 @@ def _clusters(lib):
         ("chain x2 ps3", lib.generate("chain", 6, 2, "1/2", 11).expand(2, 1, 3)),
         ("layered x4 ps250", lib.generate("layered", 12, 4, "1", 3).expand(4, 1, 250)),
         ("chain x5 ps100", lib.generate("chain", 40, 1, "2", 8).expand(5, 1, 100)),
+        ("vgg16 x4 / 2 PS ps100", lib.model("vgg16_training", 1).expand(4, 2, 100)),
+        ("resnet50 x3 / 3 PS ps7", lib.model("resnet_v2_50_inference", 1).expand(3, 3, 7)),
+        ("layered x2 / 4 PS ps250", lib.generate("layered", 12, 4, "1", 3).expand(2, 4, 250)),
     ]
 
 
@@ -62,7 +65,7 @@ def test_ps_sweep_matches_reference(lib, ref, tmp_path, noise):
 
 def test_ps_equals_forced_event_replica(lib, monkeypatch):
     from paper_1803_03288_b200.capi import policy
-    for name, c in _clusters(lib)[:4]:
+    for name, c in _clusters(lib)[:4] + _clusters(lib)[6:]:
         for pol in (None, policy(False, 0, 0.0), policy(True, 0, 1.0)):
             text = c.serialize()
             a = lib.graph(text)
