@@ -304,7 +304,8 @@ def exact_paths(lib, path):
     0.1 — still the closed form, on the noise-permuted gate sequence; (b)
     config 3 (VGG-16 x 4 workers / 1 PS) with PS operations that take time
     (100 us each): closed-form workers + the exact send phase; (c) the same
-    with two parameter servers, which only the exact event replica covers."""
+    with two parameter servers; (d) branchy workers in such a cluster, which
+    only the exact event replica covers."""
     g4 = lib.graph(bench_json(MODEL))
     a = sweep_vs_reference(lib, g4, path, f"config4 {MODEL}, counter gate + reorder noise 0.1 "
                                           f"(closed form on the noise-permuted gate order)", 0.1, 1 << 22)
@@ -320,9 +321,18 @@ def exact_paths(lib, path):
     with open(p4, "w") as f:
         f.write(c4.serialize())
     c = sweep_vs_reference(lib, c4, p4, "config3 vgg16_training x 4 workers / 2 PS with 100 us PS ops, full "
-                                        "makespans (two channels per worker: exact event replica, thread per run)",
+                                        "makespans (two channels per worker, two PS cores: cluster_ps_kernel)",
+                           None, 1 << 22)
+    c5 = lib.model("vgg16_training_branchy", 1).expand(4, 1, 100)
+    p5 = os.path.join(os.path.dirname(path), "config3_branchy_ps100.json")
+    with open(p5, "w") as f:
+        f.write(c5.serialize())
+    e = sweep_vs_reference(lib, c5, p5, "vgg16_training_branchy x 4 workers / 1 PS with 100 us PS ops, full "
+                                        "makespans (branchy workers: compute ops compete while PS ops take time, "
+                                        "outside every closed form: exact event replica, thread per run)",
                            None, 1 << 18)
-    return {"noise_sweep_config4": a, "ps_send_phase_config3_ps100": b, "event_replica_config3_2ps": c}
+    return {"noise_sweep_config4": a, "ps_send_phase_config3_ps100": b, "ps_send_phase_config3_2ps": c,
+            "event_replica_branchy_cluster": e}
 
 
 def cpu_baseline(path, target_s=10.0, g=None, o=None):

@@ -14,6 +14,7 @@ struct Rows {
   std::vector<int32_t> self_col;        // per row: recv column or -1
   std::vector<int32_t> pre_off, pre;    // per row: predecessor rows
   std::vector<int32_t> succ_off, succ;  // per recv column: direct-successor rows (TAC)
+  std::vector<int32_t> g1;              // per recv column: its one direct-successor row, -1 several, -2 none
   // Rows with predecessor rows, in topological order, and their closure
   // terms encoded for closure_seq_kernel: -1 = the previous such row (kept
   // in a register); -(2 + q) followed by a mask = bits of word q contributed
@@ -26,7 +27,7 @@ struct Rows {
   // with the graph by csk_graph_free)
   int32_t *d_self = nullptr, *d_preoff = nullptr, *d_pre = nullptr, *d_rowof = nullptr, *d_succoff = nullptr,
           *d_succ = nullptr, *d_ntrow = nullptr, *d_ntoff = nullptr, *d_ntterm = nullptr, *d_ntchunk = nullptr,
-          *d_hasrows = nullptr;
+          *d_hasrows = nullptr, *d_g1 = nullptr;
 };
 
 struct DeviceGraph {

@@ -120,7 +120,7 @@ extern "C" void csk_graph_free(DeviceGraph* g) {
   if (g->rows) {
     const Rows& r = *g->rows;
     const void* rp[] = {r.d_self, r.d_preoff, r.d_pre,    r.d_rowof,   r.d_succoff, r.d_succ,
-                        r.d_ntrow, r.d_ntoff, r.d_ntterm, r.d_ntchunk, r.d_hasrows};
+                        r.d_ntrow, r.d_ntoff, r.d_ntterm, r.d_ntchunk, r.d_hasrows, r.d_g1};
     for (const void* p : rp)
       if (p) cudaFree(const_cast<void*>(p));
   }

@@ -158,6 +158,7 @@ void build_rows(const DeviceGraph* g, Rows& rw) {
     tmp.erase(std::unique(tmp.begin(), tmp.end()), tmp.end());
     rw.succ.insert(rw.succ.end(), tmp.begin(), tmp.end());
     rw.succ_off.push_back(static_cast<int32_t>(rw.succ.size()));
+    rw.g1.push_back(tmp.size() == 1 ? tmp[0] : (tmp.empty() ? -2 : -1));
   }
 }
 
@@ -410,6 +411,7 @@ struct TacArgs {
   const int64_t* tcol;      // T(recv column)
   const int32_t* succ_off;  // direct-successor groups per column
   const int32_t* succ;
+  const int32_t* g1;        // per column: its one direct-successor group, -1 several, -2 none
   const int32_t* col_off;   // groups per column
   const int32_t* col;
   const unsigned long long* wsum;
@@ -681,6 +683,21 @@ __global__ void __launch_bounds__(1024) tac_own_kernel(TacArgs a, int* ring, lon
   };
   int p = 0;
   int first = 0;  // lowest outstanding column (identical in every thread)
+  // the incumbent's static data, loaded as soon as `first` is known (before
+  // the barrier that publishes the round's P and M): T, its one successor
+  // group, its column range, and this thread's retire entry of that column
+  int64_t f_t = 0;
+  int f_g1 = -2;
+  int32_t f_c0 = 0, f_c1 = 0, f_g = -1;
+  auto load_first = [&]() {
+    if (first >= R) return;
+    f_t = a.tcol[first];
+    f_g1 = a.g1[first];
+    f_c0 = a.col_off[first];
+    f_c1 = a.col_off[first + 1];
+    f_g = f_c0 + tid < f_c1 ? a.col[f_c0 + tid] : -1;
+  };
+  load_first();
   for (int round = 0; round < R; ++round) {
     // this round's P and amended M+ of the owned outstanding candidates
     int64_t P_own[kOwn], mp_own[kOwn];
@@ -690,8 +707,9 @@ __global__ void __launch_bounds__(1024) tac_own_kernel(TacArgs a, int* ring, lon
       mp_own[k] = !live[k] ? kInf : g1[k] >= 0 ? a.M[g1[k]] : mplus(s0[k], s1[k]);
     }
     int best = first;
-    int64_t bp = a.P[best], bm = a.tcol[best], bmp = mplus(a.succ_off[best], a.succ_off[best + 1]);
-    int64_t bcol = -1;  // best's column range, packed (begin << 32 | end), once a step has published it
+    int64_t bp = a.P[best], bm = f_t,
+            bmp = f_g1 >= 0 ? a.M[f_g1] : (f_g1 == -2 ? kInf : mplus(a.succ_off[best], a.succ_off[best + 1]));
+    int64_t bcol = (static_cast<int64_t>(f_c0) << 32) | static_cast<uint32_t>(f_c1);  // best's column range
     for (;;) {
       int nxt = 0x7fffffff;
       int64_t np = 0, nt = 0, nm = 0, ncol = 0;
@@ -726,10 +744,17 @@ __global__ void __launch_bounds__(1024) tac_own_kernel(TacArgs a, int* ring, lon
       bcol = w.w;
     }
     const int64_t t = bm;  // T(best)
-    const int32_t e0 = bcol >= 0 ? static_cast<int32_t>(bcol >> 32) : a.col_off[best];
-    const int32_t e1 = bcol >= 0 ? static_cast<int32_t>(bcol & 0xffffffff) : a.col_off[best + 1];
+    const int32_t e0 = static_cast<int32_t>(bcol >> 32);
+    const int32_t e1 = static_cast<int32_t>(bcol & 0xffffffff);
+    const bool won_first = best == first;
+    const int32_t g_pre = f_g;
+    if (won_first) {  // the next incumbent is known now: its static data loads overlap the retire
+      do ++first;
+      while (first < R && (first == best || !*reinterpret_cast<volatile uint8_t*>(&a.out[first])));
+      load_first();
+    }
     for (int64_t e = e0 + tid; e < e1; e += nthreads) {
-      const int32_t g = a.col[e];
+      const int32_t g = (won_first && e == e0 + tid) ? g_pre : a.col[e];  // prefetched when the incumbent won
       const int k = --a.cnt[g];
       a.M[g] -= t;
       const int x = (a.xr[g] ^= best);
@@ -743,9 +768,6 @@ __global__ void __launch_bounds__(1024) tac_own_kernel(TacArgs a, int* ring, lon
       a.out[best] = 0;
     }
     grid.sync();
-    if (best == first)
-      do ++first;
-      while (first < R && !*reinterpret_cast<volatile uint8_t*>(&a.out[first]));
   }
 }
 
@@ -1046,10 +1068,11 @@ int group_setup(DeviceGraph* g, const int64_t* dur, GroupState& S, char* err) {
       };
       if (up(r->d_self, r->self_col) || up(r->d_preoff, r->pre_off) || up(r->d_pre, r->pre) ||
           up(r->d_rowof, r->row_of) || up(r->d_succoff, r->succ_off) || up(r->d_succ, r->succ) ||
+          up(r->d_g1, r->g1) ||
           up(r->d_ntrow, r->nt_row) || up(r->d_ntoff, r->nt_off) || up(r->d_ntterm, r->nt_term) ||
           up(r->d_ntchunk, r->nt_chunk) || up(r->d_hasrows, r->has_rows)) {
-        const int32_t* ps[] = {r->d_self, r->d_preoff, r->d_pre,    r->d_rowof,   r->d_succoff, r->d_succ,
-                               r->d_ntrow, r->d_ntoff, r->d_ntterm, r->d_ntchunk, r->d_hasrows};
+        const int32_t* ps[] = {r->d_self,  r->d_preoff, r->d_pre,    r->d_rowof,   r->d_succoff, r->d_succ,
+                               r->d_ntrow, r->d_ntoff,  r->d_ntterm, r->d_ntchunk, r->d_hasrows, r->d_g1};
         for (const int32_t* q : ps)
           if (q) cudaFree(const_cast<int32_t*>(q));
         return 1;
@@ -1266,6 +1289,7 @@ extern "C" int csk_tac(DeviceGraph* g, const int64_t* dur, int32_t* prio, char* 
             S.d_tcol.as<int64_t>(),
             S.rw->d_succoff,
             S.rw->d_succ,
+            S.rw->d_g1,
             S.d_coloff.as<int32_t>(),
             S.d_col.as<int32_t>(),
             S.d_wsum.as<unsigned long long>(),
