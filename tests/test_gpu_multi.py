@@ -42,7 +42,7 @@ def _cases(lib):
         (lib.model("resnet_v2_50_inference", 1), policy(True, 0, 0.2), 300_000),  # reorder noise
         (lib.model("vgg16_training", 1).expand(4, 1, 0), None, 200_000),      # cluster, closed form
         (lib.generate("chain", 6, 2, "1/2", 11).expand(2, 1, 3), None, 50_000),  # cluster, PS send phase
-        (lib.generate("chain", 6, 2, "1/2", 11).expand(2, 2, 3), None, 5_000),  # cluster, event replica
+        (lib.generate("seriesparallel", 7, 1, "1/2", 1003).expand(2, 1, 3), None, 5_000),  # event replica
     ]
 
 

@@ -333,7 +333,7 @@ def test_concurrent_calls_on_shared_handles(lib):
     o = g.declared()
     toy = lib.generate("chain", 7, 1, "1", 3)
     to = toy.declared()
-    cl = lib.generate("chain", 6, 2, "1/2", 11).expand(2, 2, 3)  # two PS: exact replica
+    cl = lib.generate("seriesparallel", 7, 1, "1/2", 1003).expand(2, 1, 3)  # exact replica
     co = cl.declared()
     assert cl.sweep_path(co)["path"] == "event_sim_kernel"
     jobs = {
