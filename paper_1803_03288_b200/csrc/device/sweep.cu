@@ -663,10 +663,10 @@ __host__ __device__ inline size_t dag_smem(int R, int W, int nrec, int L, int nh
 // record flags: first generator = the previous record's result (ACC);
 // output of a real record (updates ACC; padding records do not)
 constexpr uint32_t kDagAccFlag = 0x80000000u, kDagRealFlag = 0x80000000u, kDagOffMask = 0x7FFFFFFFu;
-// byte offset of item k inside a thread's Items<T, kDagThreads> column
-__host__ __device__ inline uint32_t dag_item_off(int k, size_t tb) {
-  return tb == 1 ? static_cast<uint32_t>(k * kDagThreads - (k & 3) * (kDagThreads - 1))
-                 : static_cast<uint32_t>((k >> 1) * kDagThreads * 4 + (k & 1) * 2);
+// byte offset of item k inside a thread's Items<T, nt> column
+__host__ __device__ inline uint32_t dag_item_off(int k, size_t tb, int nt = kDagThreads) {
+  return tb == 1 ? static_cast<uint32_t>(k * nt - (k & 3) * (nt - 1))
+                 : static_cast<uint32_t>((k >> 1) * nt * 4 + (k & 1) * 2);
 }
 
 // kSrc: 0 random_schedule(seed) (per-worker derived seeds on clusters),
@@ -1191,6 +1191,206 @@ __global__ void __launch_bounds__(kPsThreads) cluster_ps_kernel(ChainArgs a, PsA
   acc.flush(a, s_hist, s_shist);
 }
 
+// ---- dag_pair_kernel: the same sweep with the positions/bins arrays shared
+// by the two warps of a 64-thread block. A run is phase A (the shuffle, and
+// the noise swaps, into the thread's own gate-order column: R bytes) and
+// phase B (positions, the join program, the fold: R + L + 1 bytes of
+// positions and slots and 4(R + 1) bytes of bins). The warps alternate:
+// while one runs phase B on the block's single set of positions/bins
+// columns (lane l uses column l), the other runs phase A, and named barriers
+// hand the columns over in strict alternation. Shared memory per thread drops
+// from ~6R to ~3.5R bytes, which is what bounds occupancy here.
+constexpr int kPairThreads = 64;
+
+__host__ __device__ inline size_t dag_pair_smem(int R, int W, int nrec, int L, int nhist, size_t tb, size_t vb) {
+  const int per = tb == 1 ? 4 : 2;
+  const size_t vbins = vb * (R + 1) * 32, vals = 4ull * ((R + L + 1 + per - 1) / per) * 32;
+  const size_t perms = 4ull * ((R + per - 1) / per) * kPairThreads;
+  return round16(dag_table_bytes(R, W, nrec, vb) + 4 * static_cast<size_t>(nhist) * kBins + vbins + vals + perms) + 16;
+}
+
+__device__ __forceinline__ void named_sync(int id) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(kPairThreads)); }
+__device__ __forceinline__ void named_arrive(int id) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(kPairThreads));
+}
+
+template <typename T, typename V, bool kNoisy>
+__global__ void __launch_bounds__(kPairThreads) dag_pair_kernel(ChainArgs a, DagArgs g) {
+  constexpr int NT = kPairThreads;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int R = a.R, W = a.W, NR = g.nrec;
+  const size_t vb = sizeof(V);
+  const uint64_t* s_lim = reinterpret_cast<const uint64_t*>(smem);
+  const uint64_t* s_mag = s_lim + (R + 2);
+  const uint4* s_rec = reinterpret_cast<const uint4*>(s_mag + (R + 2));
+  const DagEnt<V>* s_ent = reinterpret_cast<const DagEnt<V>*>(s_rec + NR);
+  const V* s_wj = reinterpret_cast<const V*>(s_ent + W * R);
+  const V* s_w0 = s_wj + W * NR;
+  const int nhist = (a.do_e ? 1 : 0) + (a.cluster ? 1 : 0);
+  int* s_hist = reinterpret_cast<int*>(smem + dag_table_bytes(R, W, NR, vb));
+  int* s_shist = s_hist + (a.do_e ? kBins : 0);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  V* s_bins = reinterpret_cast<V*>(s_hist + nhist * kBins) + lane;  // [k][32], shared by the pair
+  uint32_t* vwords = reinterpret_cast<uint32_t*>(reinterpret_cast<V*>(s_hist + nhist * kBins) + (R + 1) * 32);
+  const Items<T, 32> val{vwords + lane};
+  uint32_t* pwords = vwords + Items<T, 32>::words(R + g.L + 1) * 32;
+  const Items<T, NT> perm{pwords + threadIdx.x};
+  uint64_t* tables_ready = reinterpret_cast<uint64_t*>(smem + a.mbar_off);
+  if (threadIdx.x == 0) mbar_init(tables_ready, 1);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    mbar_expect_tx(tables_ready, a.blob_bytes);
+    bulk_g2s(smem, a.blob, a.blob_bytes, tables_ready);
+  }
+  for (int k = threadIdx.x; k < nhist * kBins; k += blockDim.x) s_hist[k] = 0;
+  if (warp == 0)
+    for (int k = 0; k <= R; ++k) s_bins[k * 32] = V(0);  // the fold re-zeroes every bin it reads
+  mbar_wait(tables_ready, 0);
+  __syncthreads();
+  unsigned char* vcol = reinterpret_cast<unsigned char*>(val.base);
+
+  StatAcc acc;
+  const int64_t nthreads = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  // every thread of the block runs the same number of units (ordering x
+  // worker: the count of the block's first thread), so the named barriers
+  // always match; threads past the end only keep the handshake
+  const int64_t first0 = static_cast<int64_t>(blockIdx.x) * blockDim.x;
+  const int64_t n_ord = first0 < a.count ? (a.count - first0 + nthreads - 1) / nthreads : 0;
+  const int64_t units = n_ord * W;
+  const int64_t idx0 = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  int64_t hi = 0, lo = INT64_MAX;
+  NoiseState<kNoisy> noise;
+  auto phase_a = [&](int64_t u) {  // gate order of unit u into this thread's column
+    const int64_t j = u / W;
+    const int w = static_cast<int>(u % W);
+    const int64_t idx = idx0 + j * nthreads;
+    if (idx >= a.count) return;
+    const uint64_t seed = a.seed_lo + static_cast<uint64_t>(idx);
+    if constexpr (kNoisy)
+      if (w == 0) noise.init(splitmix64(seed ^ kNoiseSalt));
+    const uint64_t ws = a.cluster ? splitmix64(seed ^ (kPhi * static_cast<uint64_t>(w + 1))) : seed;
+    FoldT<V> f{0, 0, 0};
+    shuffle_fold<Items<T, NT>, V, true>(ws, R, perm, f, nullptr, V(0), nullptr, s_lim, s_mag);
+    if constexpr (kNoisy) {
+      auto swap_at = [&](int pos, uint64_t v) {
+        if ((v >> 11) < a.noise_thr) {
+          T* p0 = perm.at(pos - 1);
+          T* p1 = perm.at(pos);
+          const T x = *p0;
+          *p0 = *p1;
+          *p1 = x;
+        }
+      };
+      if (W == 1 && R - 1 <= 311) {
+        mt_outputs(splitmix64(seed ^ kNoiseSalt), R - 1, [&](int d, uint64_t v) { swap_at(d + 1, v); });
+      } else {
+        for (int pos = 1; pos < R; ++pos) swap_at(pos, noise.m.next());
+      }
+    }
+  };
+  auto phase_b = [&](int64_t u) {  // positions, program and fold of unit u
+    const int64_t j = u / W;
+    const int w = static_cast<int>(u % W);
+    const int64_t idx = idx0 + j * nthreads;
+    if (idx >= a.count) return;
+    const DagEnt<V>* ent = s_ent + w * R;
+    for (int k = 0; k < R; ++k) *val.at(*perm.at(k)) = static_cast<T>(k);
+    {
+      const V* wj = s_wj + w * NR;
+      int accv = 0;
+      for (int q = 0; q < NR; q += 4) {
+        uint4 rc[4];
+        V wt[4];
+        int lp[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          rc[i] = s_rec[q + i];
+          wt[i] = wj[q + i];
+        }
+        int x[4], y[4], z[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          x[i] = *reinterpret_cast<const T*>(vcol + (rc[i].x & kDagOffMask));
+          y[i] = *reinterpret_cast<const T*>(vcol + rc[i].y);
+          z[i] = *reinterpret_cast<const T*>(vcol + rc[i].z);
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          lp[i] = max(max((rc[i].x & kDagAccFlag) ? accv : x[i], y[i]), z[i]);
+          accv = (rc[i].w & kDagRealFlag) ? lp[i] : accv;
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) *reinterpret_cast<T*>(vcol + (rc[i].w & kDagOffMask)) = static_cast<T>(lp[i]);
+#pragma unroll
+        for (int jj = 1; jj < 4; ++jj)
+#pragma unroll
+          for (int i = 0; i < jj; ++i)
+            if (lp[i] == lp[jj]) {
+              wt[jj] += wt[i];
+              wt[i] = V(0);
+            }
+        V old[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) old[i] = s_bins[lp[i] * 32];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) s_bins[lp[i] * 32] = old[i] + wt[i];
+      }
+    }
+    const V ctot = static_cast<V>(a.ctot[w]);
+    V S = 0, suffix = 0, best = 0;
+    auto step = [&](int r, int k) {
+      const DagEnt<V> e = ent[r];
+      S += s_bins[k * 32] + e.wr;
+      s_bins[k * 32] = V(0);
+      best = max(best, ctot - suffix + S);
+      suffix += e.d;
+    };
+    int k = R - 1;
+    if constexpr (sizeof(T) == 1) {
+      for (; k >= 0 && (k & 3) != 3; --k) step(*perm.at(k), k);
+      for (; k >= 3; k -= 4) {
+        const uint32_t wd = perm.base[(k >> 2) * NT];
+        step(wd >> 24, k);
+        step((wd >> 16) & 0xFF, k - 1);
+        step((wd >> 8) & 0xFF, k - 2);
+        step(wd & 0xFF, k - 3);
+      }
+    } else {
+      for (; k >= 0; --k) step(*perm.at(k), k);
+    }
+    best = max(best, S + s_w0[w]);
+    const int64_t tcpu = static_cast<int64_t>(best);
+    const int64_t c64 = static_cast<int64_t>(ctot);
+    const int64_t mw = a.cluster ? max(tcpu, max(c64, tcpu) + a.send_tot[w]) : max(tcpu, c64);
+    if (a.worker_ms) a.worker_ms[idx * W + w] = mw;
+    hi = max(hi, mw);
+    lo = min(lo, mw);
+    if (w == W - 1) {
+      if (a.makespans) a.makespans[idx] = hi;
+      acc.add(a, a.seed_lo + static_cast<uint64_t>(idx), hi, hi, lo, s_hist, s_shist);
+      hi = 0;
+      lo = INT64_MAX;
+    }
+  };
+  // strict alternation of phase B: warp 0 B(0), warp 1 B(0), warp 0 B(1), ...
+  // barrier 1: warp 0 hands the columns to warp 1; barrier 2: back to warp 0
+  for (int64_t u = 0; u < units; ++u) {
+    phase_a(u);
+    if (warp == 0) {
+      if (u > 0) named_sync(2);
+      phase_b(u);
+      named_arrive(1);
+    } else {
+      named_sync(1);
+      phase_b(u);
+      named_arrive(2);
+    }
+  }
+  if (warp == 0 && units > 0) named_sync(2);  // consume warp 1's last hand-back
+  __syncthreads();
+  acc.flush(a, s_hist, s_shist);
+}
+
 // Brute force (metrics.cpp:37-72) on the closed form: permutation number k
 // in lexicographic order of the recv columns (std::next_permutation order
 // over ascending ids) is unranked in the factorial number system into a
@@ -1333,6 +1533,11 @@ struct SweepPlan {
   // shared-memory item width (1: R <= 255, else 2)
   int dag = 0, J = 0, Ls = 0, tb = 1;
   int blocks_orders = 0;
+  // dag_pair_kernel (random sweeps): its own image (records with offsets in
+  // the 32-column layout), shared memory, grid
+  void* pair_blob = nullptr;
+  size_t pair_smem = 0;
+  int pair_blocks = 0;
   // cluster send phase (cluster_ps_kernel): device tables and its own image
   int ps = 0, ps_blocks = 0;
   PsArgs psa{};
@@ -1343,6 +1548,15 @@ struct SweepPlan {
 };
 
 using DagFn = void (*)(ChainArgs, DagArgs);
+static DagFn pair_fn(const SweepPlan* p) {
+  const bool nz = p->noise_thr != 0;
+  if (p->tb == 1) {
+    if (nz) return p->narrow ? dag_pair_kernel<uint8_t, int32_t, true> : dag_pair_kernel<uint8_t, int64_t, true>;
+    return p->narrow ? dag_pair_kernel<uint8_t, int32_t, false> : dag_pair_kernel<uint8_t, int64_t, false>;
+  }
+  if (nz) return p->narrow ? dag_pair_kernel<uint16_t, int32_t, true> : dag_pair_kernel<uint16_t, int64_t, true>;
+  return p->narrow ? dag_pair_kernel<uint16_t, int32_t, false> : dag_pair_kernel<uint16_t, int64_t, false>;
+}
 template <int kSrc>
 static DagFn dag_fn(const SweepPlan* p, bool noisy) {
   if (kSrc == 0 && noisy) {
@@ -1539,13 +1753,32 @@ extern "C" SweepPlan* csk_sweep_plan_dag(int32_t W, int32_t R, const int64_t* d,
   }
   for (int k = 0; k < W * nrec; ++k) put(wj[k]);
   for (int w = 0; w < W; ++w) put(w0[w]);
+  // the pair kernel's image: the same bytes with the records' offsets in
+  // the 32-column layout of its shared positions array
+  std::vector<unsigned char> pimg = img;
+  {
+    unsigned char* rq = pimg.data() + 16ull * (R + 2);
+    for (int r = 0; r < nrec; ++r) {
+      const bool pad = recs[4 * r + 3] == -3;
+      for (int f = 0; f < 4; ++f) {
+        const int v = recs[4 * r + f];
+        uint32_t off;
+        if (v == -2 && f == 0) off = kDagAccFlag;
+        else if (pad) off = f == 3 ? dag_item_off(discard, p->tb, 32) : 0;
+        else if (f == 3) off = dag_item_off(v < 0 ? discard : v, p->tb, 32) | kDagRealFlag;
+        else off = dag_item_off(v, p->tb, 32);
+        std::memcpy(rq, &off, 4);
+        rq += 4;
+      }
+    }
+  }
   auto up = [&](void** dst, const void* src, size_t bytes) {
     if (cudaMalloc(dst, bytes ? bytes : 8) != cudaSuccess) return false;
     p->uploaded += bytes;
     return bytes == 0 || cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice) == cudaSuccess;
   };
-  if (!up(&p->blob, img.data(), img.size()) || !up(&p->ctot, ctot.data(), sizeof(int64_t) * W) ||
-      !up(&p->send, send_total, sizeof(int64_t) * W)) {
+  if (!up(&p->blob, img.data(), img.size()) || !up(&p->pair_blob, pimg.data(), pimg.size()) ||
+      !up(&p->ctot, ctot.data(), sizeof(int64_t) * W) || !up(&p->send, send_total, sizeof(int64_t) * W)) {
     std::snprintf(err, 256, "CUDA allocation for the sweep plan failed");
     csk_sweep_plan_free(p);
     return nullptr;
@@ -1569,6 +1802,15 @@ extern "C" SweepPlan* csk_sweep_plan_dag(int32_t W, int32_t R, const int64_t* d,
   }
   p->blocks = sms * occ;
   p->blocks_orders = sms * occ_o;
+  {  // the warp-pair kernel for random sweeps, when it fits
+    p->pair_smem = dag_pair_smem(R, W, nrec, Ls, nhist, p->tb, vb);
+    const void* pf = reinterpret_cast<const void*>(pair_fn(p));
+    allow_max_dynamic_smem(pf);
+    int occ_p = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_p, pf, kPairThreads, p->pair_smem) != cudaSuccess)
+      cudaGetLastError();
+    p->pair_blocks = std::getenv("TICTAC_DAG_NO_PAIR") ? 0 : sms * occ_p;
+  }
   return p;
 }
 
@@ -1679,7 +1921,7 @@ extern "C" int64_t csk_sweep_plan_uploaded(const SweepPlan* p) { return static_c
 
 extern "C" void csk_sweep_plan_free(SweepPlan* p) {
   if (!p) return;
-  void* ptrs[] = {p->tab, p->pwsuf, p->ctot, p->send, p->lim, p->mag, p->blob};
+  void* ptrs[] = {p->tab, p->pwsuf, p->ctot, p->send, p->lim, p->mag, p->blob, p->pair_blob};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   for (void* q : p->ps_bufs)
@@ -1765,6 +2007,17 @@ extern "C" int csk_sweep_run(SweepPlan* p, uint64_t seed_lo, int64_t count, uint
     const int64_t need = (count + kPsThreads - 1) / kPsThreads;
     const int blocks = static_cast<int>(std::min<int64_t>(p->ps_blocks, need));
     ps_fn(p)<<<blocks, kPsThreads, p->ps_smem, st>>>(a, p->psa);
+    LAUNCHED();
+    CK(cudaGetLastError());
+    return 0;
+  }
+  if (p->dag && p->pair_blocks > 0) {
+    a.blob = p->pair_blob;
+    a.blob_bytes = static_cast<uint32_t>(p->blob_bytes);
+    a.mbar_off = static_cast<uint32_t>(p->pair_smem - 16);
+    const int64_t need = (count + kPairThreads - 1) / kPairThreads;
+    const int blocks = static_cast<int>(std::min<int64_t>(p->pair_blocks, need));
+    pair_fn(p)<<<blocks, kPairThreads, p->pair_smem, st>>>(a, DagArgs{p->J, p->Ls, 0, nullptr});
     LAUNCHED();
     CK(cudaGetLastError());
     return 0;
