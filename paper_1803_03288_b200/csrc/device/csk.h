@@ -130,6 +130,8 @@ int csk_sweep_plan_add_ps(SweepPlan* p, int32_t S, const int16_t* recv_sb, const
                           const int32_t* slots, char* err);
 /* Host-to-device bytes the plan's construction copied (tables, images). */
 int64_t csk_sweep_plan_uploaded(const SweepPlan* p);
+// The kernel a random sweep on this plan launches.
+const char* csk_sweep_plan_kernel(const SweepPlan* p);
 /* Stats layout documented in include/commsched.h (CS_DSTATS_*). */
 int csk_stats_pack(const int64_t* d_i64, const double* d_f64, int rank, int world, int64_t* d_buf,
                    void* stream, char* err);

@@ -1919,6 +1919,12 @@ extern "C" int csk_sweep_plan_add_ps(SweepPlan* p, int32_t S, const int16_t* rec
 
 extern "C" int64_t csk_sweep_plan_uploaded(const SweepPlan* p) { return static_cast<int64_t>(p->uploaded); }
 
+extern "C" const char* csk_sweep_plan_kernel(const SweepPlan* p) {
+  if (p->ps) return "cluster_ps_kernel";
+  if (p->dag) return p->pair_blocks > 0 ? "dag_pair_kernel" : "dag_sweep_kernel";
+  return p->nch > 1 ? "chain_multi_kernel" : "chain_sweep_kernel";
+}
+
 extern "C" void csk_sweep_plan_free(SweepPlan* p) {
   if (!p) return;
   void* ptrs[] = {p->tab, p->pwsuf, p->ctot, p->send, p->lim, p->mag, p->blob, p->pair_blob};

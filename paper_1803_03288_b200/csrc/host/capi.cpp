@@ -727,6 +727,7 @@ int cs_sweep_path_json(const cs_graph* g, const cs_oracle* o, const cs_sim_polic
                 : c->ps  ? "cluster_ps_kernel"
                          : "chain_sweep_kernel";
     j["why"] = c->fast ? "" : c->why;
+    j["kernel"] = c->fast && c->plan ? csk_sweep_plan_kernel(c->plan) : "event_sim_kernel";
     *out_json = dup(dump_doc(j));
   });
 }
@@ -742,7 +743,7 @@ int cs_sweep_plan_info(const cs_sweep_plan* p, char** out_json) {
     j["edges"] = static_cast<int64_t>(c.g->edges().size());
     j["recvs_per_worker"] = c.R;
     j["classes"] = c.nc;
-    j["kernel"] = c.dag ? "dag_sweep_kernel" : c.ps ? "cluster_ps_kernel" : "chain_sweep_kernel";
+    j["kernel"] = csk_sweep_plan_kernel(c.plan);
     if (c.dag) {
       j["joins"] = c.joins;
       j["slots"] = c.slots;

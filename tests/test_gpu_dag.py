@@ -148,9 +148,11 @@ def test_dag_pair_kernel_equals_single_warp_kernel(lib, monkeypatch):
              (lambda: lib.model("vgg16_training_branchy", 1).expand(3, 1, 0), None)]
     for make, pol in cases:
         a = make()
+        assert a.sweep_path(a.declared(), pol or policy(True, 0, 0.0))["kernel"] == "dag_pair_kernel"
         ra = a.sweep_random(a.declared(), 3, 100_003, pol, makespans=True, worker_makespans=a.is_cluster())
         monkeypatch.setenv("TICTAC_DAG_NO_PAIR", "1")
         b = make()
+        assert b.sweep_path(b.declared(), pol or policy(True, 0, 0.0))["kernel"] == "dag_sweep_kernel"
         rb = b.sweep_random(b.declared(), 3, 100_003, pol, makespans=True, worker_makespans=b.is_cluster())
         monkeypatch.delenv("TICTAC_DAG_NO_PAIR")
         assert np.array_equal(ra["makespans"], rb["makespans"])
