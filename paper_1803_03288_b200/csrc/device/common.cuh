@@ -123,24 +123,43 @@ __device__ __forceinline__ uint64_t join64(uint32_t lo, uint32_t hi) {
 }
 
 // One twist element: c ^ ((a&U | b&L) >> 1) ^ (odd ? MATRIX : 0), on 32-bit
-// halves (x.hi = a.hi; x.lo = a.lo&0x80000000 | b.lo&0x7fffffff; the odd
-// mask is a 32-bit 0/~0 applied to both halves of MATRIX).
+// halves (x.hi = a.hi; x.lo = a.lo&0x80000000 | b.lo&0x7fffffff, one LOP3
+// select; the odd term is (b & 1) * MATRIX half on the FMA pipe, folded
+// into a three-input XOR — the RNG is bound by the ALU pipe).
+__device__ __forceinline__ uint32_t sel_upper(uint32_t a, uint32_t b) {
+  uint32_t r;  // (a & 0x80000000) | (b & 0x7fffffff) as one LOP3 (ptxas would narrow the mask to two)
+  asm("lop3.b32 %0, %1, %2, %3, 0xE4;" : "=r"(r) : "r"(a), "r"(b), "n"(0x80000000u));
+  return r;
+}
+template <uint32_t C>
+__device__ __forceinline__ uint32_t mulc(uint32_t x) {
+  uint32_t r;
+  asm("mul.lo.u32 %0, %1, %2;" : "=r"(r) : "r"(x), "n"(C));
+  return r;
+}
 __device__ __forceinline__ uint64_t mt_twist(uint64_t a, uint64_t b, uint64_t c) {
   const uint32_t xh = hi32(a);
-  const uint32_t xl = (lo32(a) & 0x80000000u) | (lo32(b) & 0x7FFFFFFFu);
-  const uint32_t odd = 0u - (xl & 1u);
-  const uint32_t rl = lo32(c) ^ ((xl >> 1) | (xh << 31)) ^ (odd & 0xA96619E9u);
-  const uint32_t rh = hi32(c) ^ (xh >> 1) ^ (odd & 0xB5026F5Au);
+  const uint32_t xl = sel_upper(lo32(a), lo32(b));
+  const uint32_t odd = lo32(b) & 1u;
+  const uint32_t rl = lo32(c) ^ ((xl >> 1) | (xh << 31)) ^ mulc<0xA96619E9u>(odd);
+  const uint32_t rh = hi32(c) ^ (xh >> 1) ^ mulc<0xB5026F5Au>(odd);
   return join64(rl, rh);
+}
+// x ^ (y & C) as one LOP3 (ptxas tends to split a chain of these into three).
+template <uint32_t C>
+__device__ __forceinline__ uint32_t xor_and(uint32_t x, uint32_t y) {
+  uint32_t r;
+  asm("lop3.b32 %0, %1, %2, %3, 0x78;" : "=r"(r) : "r"(x), "r"(y), "n"(C));
+  return r;
 }
 __device__ __forceinline__ uint64_t mt_temper(uint64_t y) {
   uint32_t l = lo32(y), h = hi32(y);
-  l ^= ((l >> 29) | (h << 3)) & 0x55555555u;  // y ^= (y >> 29) & 0x5555555555555555
-  h ^= (h >> 29) & 0x55555555u;
-  h ^= ((h << 17) | (l >> 15)) & 0x71D67FFFu;  // y ^= (y << 17) & 0x71D67FFFEDA60000
-  l ^= (l << 17) & 0xEDA60000u;
-  h ^= (l << 5) & 0xFFF7EEE0u;                 // y ^= (y << 37) & 0xFFF7EEE000000000
-  l ^= h >> 11;                                // y ^= y >> 43
+  l = xor_and<0x55555555u>(l, (l >> 29) | (h << 3));  // y ^= (y >> 29) & 0x5555555555555555
+  h = xor_and<0x5u>(h, h >> 29);
+  h = xor_and<0x71D67FFFu>(h, (h << 17) | (l >> 15));  // y ^= (y << 17) & 0x71D67FFFEDA60000
+  l = xor_and<0xEDA60000u>(l, l << 17);
+  h = xor_and<0xFFF7EEE0u>(h, l << 5);                  // y ^= (y << 37) & 0xFFF7EEE000000000
+  l ^= h >> 11;                                         // y ^= y >> 43
   return join64(l, h);
 }
 
@@ -275,6 +294,14 @@ __device__ __forceinline__ uint32_t fastmod32(uint64_t v, uint32_t n, uint64_t m
   const uint64_t q = __umul64hi(v, magic);
   const uint32_t r = static_cast<uint32_t>(v) - static_cast<uint32_t>(q) * n;
   return min(r, r - n);
+}
+
+// The same with the negated modulus (-n mod 2^32), which callers stepping
+// through consecutive n keep in a counter.
+__device__ __forceinline__ uint32_t fastmod32n(uint64_t v, uint32_t nneg, uint64_t magic) {
+  const uint64_t q = __umul64hi(v, magic);
+  const uint32_t r = static_cast<uint32_t>(v) + static_cast<uint32_t>(q) * nneg;
+  return min(r, r + nneg);
 }
 
 // bounded() rejects v > UINT64_MAX - (2^64 mod n); for n < 2^32 that needs

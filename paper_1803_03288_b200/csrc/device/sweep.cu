@@ -79,6 +79,11 @@ struct Items<uint8_t, NT> {
   __device__ __forceinline__ uint8_t* at(int k) const {
     return reinterpret_cast<uint8_t*>(base) + k * NT - (k & 3) * (NT - 1);
   }
+  // slot 4m and the byte offset of slot 4m + r from it (aligned groups of
+  // four slots: one address per group, the rest immediate offsets)
+  __device__ __forceinline__ uint8_t* at4(int m) const { return reinterpret_cast<uint8_t*>(base) + m * 4 * NT; }
+  static constexpr int goff(int r) { return r; }
+  static constexpr int kGroupBytes = 4 * NT;  // at4(m) - at4(m - 1)
   __device__ __forceinline__ void init(int R) const {
     for (int q = 0; q < (R + 3) >> 2; ++q) base[q * NT] = 0x03020100u + 0x04040404u * static_cast<uint32_t>(q);
   }
@@ -91,6 +96,9 @@ struct Items<uint16_t, NT> {
   __device__ __forceinline__ uint16_t* at(int k) const {
     return reinterpret_cast<uint16_t*>(base + (k >> 1) * NT) + (k & 1);
   }
+  __device__ __forceinline__ uint16_t* at4(int m) const { return reinterpret_cast<uint16_t*>(base + 2 * m * NT); }
+  static constexpr int goff(int r) { return (r >> 1) * 4 * NT + (r & 1) * 2; }
+  static constexpr int kGroupBytes = 8 * NT;
   __device__ __forceinline__ void init(int R) const {
     for (int q = 0; q < (R + 1) >> 1; ++q)
       base[q * NT] = (static_cast<uint32_t>(2 * q + 1) << 16) | static_cast<uint32_t>(2 * q);
@@ -104,31 +112,52 @@ template <typename V>
 struct FoldT {
   int G;
   V suffix, best;
+  // The term is taken unconditionally: when gk == G it is dominated by the
+  // term taken when G got its value (the suffix only grows), and before the
+  // first class (G == nc, S(nc) = 0) it is a transfer completion c_k <= Ctot,
+  // which every consumer of best already maxes with (m = max(T_cpu, Ctot),
+  // cluster m_w = max(T_cpu, max(Ctot, T_cpu) + sends)). No predicate, one
+  // ALU instruction less per draw.
   __device__ __forceinline__ void add(uint2 e, V ctot, const V* pw) {
     const int gk = min(static_cast<int>(e.x), G);
-    if (gk < G) best = max(best, ctot - suffix + pw[gk]);
+    best = max(best, ctot - suffix + pw[gk]);
     G = gk;
     suffix += static_cast<V>(e.y);
   }
 };
 
+// tab[x] for a table in shared memory, addressed as one IMAD from a 32-bit
+// shared-window base (the compiler's LEA form runs on the ALU pipe, which
+// bounds the shuffle).
+__device__ __forceinline__ uint2 tab_at(const uint2* tab, uint32_t x) {
+  uint32_t base = static_cast<uint32_t>(__cvta_generic_to_shared(tab)), addr;
+  asm("mad.lo.u32 %0, %1, 8, %2;" : "=r"(addr) : "r"(x), "r"(base));
+  uint2 e;
+  asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(e.x), "=r"(e.y) : "r"(addr));  // read-only table
+  return e;
+}
+
 // One Fisher–Yates draw at slot i (1-based count of unfinished slots) with
 // bounded() value j: the element landing in its final slot i-1 is folded.
 // kStore: keep the permutation instead (the element is written to slot i-1).
 template <typename It, typename V, bool kStore = false>
-__device__ __forceinline__ void fy_draw(const It& items, int i, int j, FoldT<V>& f, const uint2* tab,
-                                        V ctot, const V* pw) {
+__device__ __forceinline__ void fy_draw_at(const It& items, typename It::value_type* pl, int j, FoldT<V>& f,
+                                           const uint2* tab, V ctot, const V* pw) {
   using T = typename It::value_type;
   T* pj = items.at(j);
   const T x = *pj;
   if constexpr (kStore) {
-    T* pl = items.at(i - 1);
     *pj = *pl;
     *pl = x;
   } else {
-    *pj = *items.at(i - 1);
-    f.add(tab[x], ctot, pw);
+    *pj = *pl;
+    f.add(tab_at(tab, x), ctot, pw);
   }
+}
+template <typename It, typename V, bool kStore = false>
+__device__ __forceinline__ void fy_draw(const It& items, int i, int j, FoldT<V>& f, const uint2* tab,
+                                        V ctot, const V* pw) {
+  fy_draw_at<It, V, kStore>(items, items.at(i - 1), j, f, tab, ctot, pw);
 }
 
 // Generic continuation after a bounded() rejection (probability ~R·2^-64
@@ -156,20 +185,26 @@ __device__ __noinline__ FoldT<V> shuffle_slow(uint64_t seed, int out, int i, It 
 
 // Draws d..d+K-1 with outputs v[] (pre-checked only by maybe_reject):
 // precise bounded() rejection test, then the swaps. Returns true when a
-// rejection sent the rest of the shuffle to the exact slow path.
-template <int K, typename It, typename V, bool kStore = false>
+// rejection sent the rest of the shuffle to the exact slow path. kAligned
+// (K == 4, (R - d) % 4 == 0): the group's final slots R-1-d .. R-4-d are the
+// four slots of one aligned group, addressed from one pointer.
+template <int K, typename It, typename V, bool kStore = false, bool kAligned = false>
 __device__ __forceinline__ bool draw_group(uint64_t seed, int R, int d, const uint64_t (&v)[K],
                                            const It& items, FoldT<V>& f, const uint2* tab, V ctot,
-                                           const V* pw, const uint64_t* s_lim, const uint64_t* s_mag) {
+                                           const V* pw, const uint64_t* s_lim, const uint64_t* s_mag,
+                                           unsigned char* pg = nullptr) {
+  using T = typename It::value_type;
+  static_assert(!kAligned || K == 4, "aligned groups are four draws");
   int j[K];
-  bool any = false;
+  const uint32_t nneg0 = static_cast<uint32_t>(d - R);  // -(slot count) of draw 0
+  uint32_t low = ~0u;  // min over draws of (high word + 1): 0 iff some high word is all ones
 #pragma unroll
   for (int q = 0; q < K; ++q) {
     const int i = R - d - q;
-    j[q] = static_cast<int>(fastmod32(v[q], static_cast<uint32_t>(i), s_mag[i]));
-    any |= maybe_reject(v[q]);
+    j[q] = static_cast<int>(fastmod32n(v[q], nneg0 + q, s_mag[i]));
+    low = min(low, static_cast<uint32_t>(v[q] >> 32) + 1u);
   }
-  if (any) {  // probability ~2^-32 per draw; exact handling, draw by draw
+  if (low == 0) {  // maybe_reject: probability ~2^-32 per draw; exact handling, draw by draw
 #pragma unroll  // (static indices: keeps v[] and j[] in registers)
     for (int q = 0; q < K; ++q) {
       const int i = R - d - q;
@@ -181,8 +216,14 @@ __device__ __forceinline__ bool draw_group(uint64_t seed, int R, int d, const ui
     }
     return false;
   }
+  if constexpr (kAligned) {  // pg == items.at4((R - 4 - d) >> 2), kept by the caller
 #pragma unroll
-  for (int q = 0; q < K; ++q) fy_draw<It, V, kStore>(items, R - d - q, j[q], f, tab, ctot, pw);
+    for (int q = 0; q < 4; ++q)
+      fy_draw_at<It, V, kStore>(items, reinterpret_cast<T*>(pg + It::goff(3 - q)), j[q], f, tab, ctot, pw);
+  } else {
+#pragma unroll
+    for (int q = 0; q < K; ++q) fy_draw<It, V, kStore>(items, R - d - q, j[q], f, tab, ctot, pw);
+  }
   return false;
 }
 
@@ -203,7 +244,15 @@ __device__ __forceinline__ void shuffle_fold(uint64_t seed, int R, const It& ite
   const int draws = R - 1;
   const int n1 = min(draws, 156);
   int d = 0;
-  for (; d + 3 < n1; d += 4) {  // phase 1, a = (s_d, s_d+1), b = s_d+156
+  for (; d < n1 && ((R - d) & 3) != 0; ++d) {  // single draws up to an aligned group
+    const uint64_t v[1] = {mt_temper(mt_twist(a0, a1, b))};
+    a0 = a1;
+    a1 = mt_step(a1, static_cast<uint32_t>(d + 2));
+    b = mt_step(b, static_cast<uint32_t>(d + 157));
+    if (draw_group<1, It, V, kStore>(seed, R, d, v, items, f, tab, ctot, pw, s_lim, s_mag)) return;
+  }
+  unsigned char* pg = reinterpret_cast<unsigned char*>(items.at4((R - 4 - d) >> 2));  // aligned groups
+  for (; d + 3 < n1; d += 4, pg -= It::kGroupBytes) {  // phase 1, a = (s_d, s_d+1), b = s_d+156
     const uint32_t u = static_cast<uint32_t>(d);
     const uint64_t a2 = mt_step(a1, u + 2), a3 = mt_step(a2, u + 3), a4 = mt_step(a3, u + 4);
     const uint64_t b1 = mt_step(b, u + 157), b2 = mt_step(b1, u + 158), b3 = mt_step(b2, u + 159);
@@ -212,7 +261,7 @@ __device__ __forceinline__ void shuffle_fold(uint64_t seed, int R, const It& ite
     a0 = a4;
     a1 = mt_step(a4, u + 5);
     b = mt_step(b3, u + 160);
-    if (draw_group<4, It, V, kStore>(seed, R, d, v, items, f, tab, ctot, pw, s_lim, s_mag)) return;
+    if (draw_group<4, It, V, kStore, true>(seed, R, d, v, items, f, tab, ctot, pw, s_lim, s_mag, pg)) return;
   }
   for (; d < n1; ++d) {
     const uint64_t v[1] = {mt_temper(mt_twist(a0, a1, b))};
@@ -224,7 +273,16 @@ __device__ __forceinline__ void shuffle_fold(uint64_t seed, int R, const It& ite
   if (d < draws) {  // phase 2, c = (s_d-156, s_d-155)
     uint64_t c0 = seed, c1 = mt_step(seed, 1);
     const int n2 = min(draws, 311);
-    for (; d + 3 < n2; d += 4) {
+    for (; d < n2 && ((R - d) & 3) != 0; ++d) {  // single draws up to an aligned group
+      const uint64_t v[1] = {mt_temper(mt_twist(a0, a1, mt_twist(c0, c1, a0)))};
+      a0 = a1;
+      a1 = mt_step(a1, static_cast<uint32_t>(d + 2));
+      c0 = c1;
+      c1 = mt_step(c1, static_cast<uint32_t>(d - 154));
+      if (draw_group<1, It, V, kStore>(seed, R, d, v, items, f, tab, ctot, pw, s_lim, s_mag)) return;
+    }
+    pg = reinterpret_cast<unsigned char*>(items.at4((R - 4 - d) >> 2));
+    for (; d + 3 < n2; d += 4, pg -= It::kGroupBytes) {
       const uint32_t u = static_cast<uint32_t>(d);
       const uint64_t a2 = mt_step(a1, u + 2), a3 = mt_step(a2, u + 3), a4 = mt_step(a3, u + 4);
       const uint64_t c2 = mt_step(c1, u - 154), c3 = mt_step(c2, u - 153), c4 = mt_step(c3, u - 152);
@@ -236,7 +294,7 @@ __device__ __forceinline__ void shuffle_fold(uint64_t seed, int R, const It& ite
       a1 = mt_step(a4, u + 5);
       c0 = c4;
       c1 = mt_step(c4, u - 151);
-      if (draw_group<4, It, V, kStore>(seed, R, d, v, items, f, tab, ctot, pw, s_lim, s_mag)) return;
+      if (draw_group<4, It, V, kStore, true>(seed, R, d, v, items, f, tab, ctot, pw, s_lim, s_mag, pg)) return;
     }
     for (; d < n2; ++d) {
       const uint64_t v[1] = {mt_temper(mt_twist(a0, a1, mt_twist(c0, c1, a0)))};

@@ -2,9 +2,10 @@
 chain-class and general-DAG graphs: 2^24 seeds, CUDA events on the launching
 stream, median of 5 after warm-up.
 
-    python tools/dag_probe.py [model ...]
+    python tools/dag_probe.py [model ...]      (TICTAC_LIB=path: another build of the library)
 """
 import json
+import os
 import sys
 
 import torch
@@ -14,7 +15,7 @@ from paper_1803_03288_b200 import capi  # noqa: E402
 
 models = sys.argv[1:] or ["resnet_v2_101_training", "resnet_v2_101_training_branchy",
                           "inception_v3_training_branchy", "seriesparallel:244"]
-L = capi.Lib()
+L = capi.Lib(os.environ["TICTAC_LIB"]) if os.environ.get("TICTAC_LIB") else capi.Lib()
 n = 1 << 24
 s = torch.cuda.current_stream()
 d_i64 = torch.zeros(capi.DSTATS_I64, dtype=torch.int64, device="cuda")
