@@ -298,9 +298,28 @@ __device__ __forceinline__ uint32_t fastmod32(uint64_t v, uint32_t n, uint64_t m
 
 // The same with the negated modulus (-n mod 2^32), which callers stepping
 // through consecutive n keep in a counter.
-__device__ __forceinline__ uint32_t fastmod32n(uint64_t v, uint32_t nneg, uint64_t magic) {
+__device__ __forceinline__ uint32_t fastmod32n_exact(uint64_t v, uint32_t nneg, uint64_t magic) {
   const uint64_t q = __umul64hi(v, magic);
   const uint32_t r = static_cast<uint32_t>(v) + static_cast<uint32_t>(q) * nneg;
+  return min(r, r + nneg);
+}
+
+// ... and with a cheaper quotient: bits
+// 64..95 of v * magic without the lo*lo partial product (and without the
+// carries above bit 95), so q is floor(v/n) - {0, 1, 2} (the dropped term is
+// below 2^64, i.e. below one unit of q) and two conditional subtracts finish
+// the remainder (r < 3n < 2^32 is exact in 32 bits).
+__device__ __forceinline__ uint32_t fastmod32n(uint64_t v, uint32_t nneg, uint64_t magic) {
+  const uint32_t vl = static_cast<uint32_t>(v), vh = static_cast<uint32_t>(v >> 32);
+  const uint32_t ml = static_cast<uint32_t>(magic), mh = static_cast<uint32_t>(magic >> 32);
+  uint32_t q;
+  asm("{\n\t.reg .u64 c;\n\t.reg .u32 cl, ch;\n\t"
+      "mul.wide.u32 c, %1, %2;\n\tmad.wide.u32 c, %3, %4, c;\n\t"
+      "mov.b64 {cl, ch}, c;\n\tmad.lo.u32 %0, %1, %4, ch;\n\t}"
+      : "=r"(q)
+      : "r"(vh), "r"(ml), "r"(vl), "r"(mh));
+  uint32_t r = vl + q * nneg;
+  r = min(r, r + nneg);
   return min(r, r + nneg);
 }
 

@@ -201,7 +201,12 @@ __device__ __forceinline__ bool draw_group(uint64_t seed, int R, int d, const ui
 #pragma unroll
   for (int q = 0; q < K; ++q) {
     const int i = R - d - q;
-    j[q] = static_cast<int>(fastmod32n(v[q], nneg0 + q, s_mag[i]));
+    // (the two remainder forms measure differently per kernel: the folding
+    // chain kernels take the cheaper quotient, the storing ones the exact)
+    if constexpr (kStore)
+      j[q] = static_cast<int>(fastmod32n_exact(v[q], nneg0 + q, s_mag[i]));
+    else
+      j[q] = static_cast<int>(fastmod32n(v[q], nneg0 + q, s_mag[i]));
     low = min(low, static_cast<uint32_t>(v[q] >> 32) + 1u);
   }
   if (low == 0) {  // maybe_reject: probability ~2^-32 per draw; exact handling, draw by draw
