@@ -769,6 +769,7 @@ __global__ void __launch_bounds__(1024) tac_own_kernel(TacArgs a, int* ring, lon
     }
     grid.sync();
   }
+  if (tid == 0) ring[3] = p;  // find-first steps taken (trace)
 }
 
 // TAC on one thread-block cluster (kClusterMax CTAs): cluster barriers are
@@ -1429,7 +1430,7 @@ extern "C" int csk_tac(DeviceGraph* g, const int64_t* dur, int32_t* prio, char* 
     }
   } else {
     DevArr d_ring;
-    const std::vector<int32_t> ring = {0x7fffffff, 0x7fffffff, 0x7fffffff};
+    const std::vector<int32_t> ring = {0x7fffffff, 0x7fffffff, 0x7fffffff, 0};  // [3]: steps taken (trace)
     if (put(d_ring, ring, err)) return 1;
     int* rp = d_ring.as<int>();
     void* args[] = {&a, &rp};
@@ -1453,9 +1454,12 @@ extern "C" int csk_tac(DeviceGraph* g, const int64_t* dur, int32_t* prio, char* 
     LAUNCHED();
     CK(cudaGetLastError());
     CK(cudaMemcpy(prio, d_prio.p, 4ull * R, cudaMemcpyDeviceToHost));
-    if (trace)
-      std::fprintf(stderr, "[tac] setup %.3f ms, state %.3f ms, rounds (%d blocks) %.3f ms\n", ms(t0, t1),
-                   ms(t1, t2), blocks, ms(t2, now()));
+    if (trace) {
+      int steps = 0;
+      CK(cudaMemcpy(&steps, rp + 3, 4, cudaMemcpyDeviceToHost));
+      std::fprintf(stderr, "[tac] setup %.3f ms, state %.3f ms, rounds (%d blocks) %.3f ms, %d find-first steps\n",
+                   ms(t0, t1), ms(t1, t2), blocks, ms(t2, now()), steps);
+    }
     return 0;
   }
   LAUNCHED();
