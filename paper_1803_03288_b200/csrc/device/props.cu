@@ -772,6 +772,316 @@ __global__ void __launch_bounds__(1024) tac_own_kernel(TacArgs a, int* ring, lon
   if (tid == 0) ring[3] = p;  // find-first steps taken (trace)
 }
 
+// Speculative multi-block TAC: one grid barrier per round when the lowest
+// outstanding column wins (on the layered config-5 graphs it always does:
+// every find-first chain is empty). Interval r compares every owned
+// candidate against `first` AND retires `first` speculatively; the barrier
+// then either confirms it (no beater: round done) or the retire is undone and
+// the round continues as tac_own_kernel's chain. What makes the overlap
+// race-free: nothing the comparison reads is written in the same interval.
+//   - amended M+: a thread keeps the M of each of its columns' direct-
+//     successor groups in registers (<= kSpecS groups per column) and applies
+//     a retire of column s as M -= T(s) where the closure bit (group, s) is
+//     set (static data); the global group M is not needed at all;
+//   - P: the retire's additions (a group dropping to one outstanding recv)
+//     go to a per-interval delta buffer D[iv % 4] that owners apply one
+//     interval later (zeroed two intervals later, flags reset three later);
+//   - the incumbent's values: the owner of the next outstanding column
+//     publishes them (P without this interval's deltas, M+ after the
+//     speculative retire) for the next interval;
+//   - closure bits of the incumbent-to-be are loaded two intervals ahead.
+// cnt / xr (retire-only state) are touched by one thread per group.
+constexpr int kSpecS = 4;
+
+__device__ __forceinline__ longlong4 ldcg4(const longlong4* p) {  // L2 (another SM wrote it)
+  const longlong2 lo = __ldcg(reinterpret_cast<const longlong2*>(p)), hi = __ldcg(reinterpret_cast<const longlong2*>(p) + 1);
+  return make_longlong4(lo.x, lo.y, hi.x, hi.y);
+}
+
+struct TacSpecWs {
+  const uint32_t* bits;  // closure [row][W]
+  int32_t W;
+  long long* D;          // [4][R] P deltas per interval
+  int* flag;             // [4] interval had deltas
+  longlong4* pub;        // [2] next incumbent {P, M+, T, column}
+  int* ring;             // [3] grid-min slots, [3] trace: misspeculated rounds
+  longlong4* win;        // [3][blocks] per-block winner records
+};
+
+template <int kOwn, int kS>
+__global__ void __launch_bounds__(1024) tac_spec_kernel(TacArgs a, TacSpecWs ws) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ uint32_t live_s[];  // this block's replica of the outstanding set, [(R + 31) / 32]
+  __shared__ int red[3];
+  int sp = 0;
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+  const int nthreads = gridDim.x * blockDim.x;
+  const int R = a.R;
+  const int kInt = 0x7fffffff;
+  for (int w = threadIdx.x; w < (R + 31) / 32; w += blockDim.x) {
+    uint32_t bits = 0;
+    for (int b = 0; b < 32 && w * 32 + b < R; ++b) bits |= (a.out[w * 32 + b] ? 1u : 0u) << b;
+    live_s[w] = bits;
+  }
+  init_red(red);  // (and the bitset's barrier)
+  long long T_[kOwn], P_[kOwn], mg[kOwn][kS];
+  int sg[kOwn][kS], ns[kOwn], c0[kOwn], c1[kOwn];
+  uint32_t bpre[kOwn], bnext[kOwn];
+  bool live[kOwn];
+#pragma unroll
+  for (int k = 0; k < kOwn; ++k) {
+    const int c = tid + k * nthreads;
+    live[k] = c < R && a.out[c];
+    T_[k] = c < R ? a.tcol[c] : 0;
+    P_[k] = c < R ? a.P[c] : 0;
+    ns[k] = c < R ? a.succ_off[c + 1] - a.succ_off[c] : 0;
+#pragma unroll
+    for (int s = 0; s < kS; ++s) {
+      sg[k][s] = s < ns[k] ? a.succ[a.succ_off[c] + s] : 0;
+      mg[k][s] = s < ns[k] ? a.M[sg[k][s]] : kInf;
+    }
+    c0[k] = c < R ? a.col_off[c] : 0;
+    c1[k] = c < R ? a.col_off[c + 1] : 0;
+    bpre[k] = bnext[k] = 0;
+  }
+  auto mplus = [&](int k) {
+    long long m = kInf;
+#pragma unroll
+    for (int s = 0; s < kS; ++s) m = min(m, mg[k][s]);
+    return m;
+  };
+  // bit s: direct-successor group s of owned column k depends on column col
+  auto bitmask = [&](int k, int col) -> uint32_t {
+    uint32_t m = 0;
+    if (col < R && tid + k * nthreads < R) {
+#pragma unroll
+      for (int s = 0; s < kS; ++s)
+        if (s < ns[k])
+          m |= ((__ldg(&ws.bits[static_cast<size_t>(sg[k][s]) * ws.W + (col >> 5)]) >> (col & 31)) & 1u) << s;
+    }
+    return m;
+  };
+  // next outstanding column after c in the replica, skipping columns whose
+  // retirement the replica may not show yet
+  auto next_live = [&](int c, int skip1, int skip2) {
+    do ++c;
+    while (c < R && (c == skip1 || c == skip2 || !((live_s[c >> 5] >> (c & 31)) & 1u)));
+    return c;
+  };
+  auto publish = [&](int col, int iv) {  // owner of col: its values for the next interval
+#pragma unroll
+    for (int k = 0; k < kOwn; ++k)
+      if (tid + k * nthreads == col) ws.pub[iv & 1] = make_longlong4(P_[k], mplus(k), T_[k], col);
+  };
+  // start-of-interval delta bookkeeping: apply the previous interval's P
+  // additions (fl1), zero the buffer of two intervals back (fl2), reset the
+  // flag of two intervals back (every thread read it after that barrier)
+  auto deltas = [&](int iv, bool fl1, bool fl2) {
+#pragma unroll
+    for (int k = 0; k < kOwn; ++k) {
+      const int c = tid + k * nthreads;
+      if (c >= R) continue;
+      if (fl1) P_[k] += __ldcg(&ws.D[static_cast<size_t>((iv - 1) & 3) * R + c]);
+      if (fl2) ws.D[static_cast<size_t>((iv - 2) & 3) * R + c] = 0;
+    }
+    if (tid == 0) ws.flag[(iv - 2) & 3] = 0;
+  };
+  auto add_p = [&](int iv, int x, unsigned long long wsum) {
+    atomicAdd(reinterpret_cast<unsigned long long*>(&ws.D[static_cast<size_t>(iv & 3) * R + x]), wsum);
+    ws.flag[iv & 3] = 1;
+  };
+  // a retire's (sign 1) or an undo's (sign -1) group updates beyond this
+  // thread's first entry of the list
+  auto retire_rest = [&](int col, int e0, int e1, int iv, int sign) {
+    for (int e = e0 + tid + nthreads; e < e1; e += nthreads) {
+      const int32_t g = a.col[e];
+      const int k = (a.cnt[g] -= sign);
+      const int x = (a.xr[g] ^= col);
+      if (sign > 0 && k == 1) add_p(iv, x, a.wsum[g]);
+    }
+  };
+  int iv = 1;
+  int first = next_live(-1, -1, -1), prev = -1;
+  int f_c0 = 0, f_c1 = 0, f_g = -1;  // the incumbent's retire list and this thread's first entry
+  auto load_first = [&](int col) {
+    f_c0 = col < R ? a.col_off[col] : 0;
+    f_c1 = col < R ? a.col_off[col + 1] : 0;
+    f_g = f_c0 + tid < f_c1 ? a.col[f_c0 + tid] : -1;
+  };
+  if (first < R) {
+    publish(first, 0);
+    const int second = next_live(first, -1, -1);
+#pragma unroll
+    for (int k = 0; k < kOwn; ++k) {
+      bpre[k] = bitmask(k, first);
+      bnext[k] = bitmask(k, second);
+    }
+    load_first(first);
+  }
+  int misses = 0;
+  bool fl1 = false, fl2 = false;
+  grid.sync();
+  longlong4 pubv = ldcg4(&ws.pub[0]);
+  for (int round = 0; round < R; ++round) {
+    // ---- speculative interval: compare against `first`, retire `first`
+    if (threadIdx.x == 0 && prev >= 0) live_s[prev >> 5] &= ~(1u << (prev & 31));  // (seen after block_min)
+    const int second = next_live(first, first, prev);
+    const int third = second < R ? next_live(second, first, prev) : R;
+    uint32_t bnn[kOwn];
+#pragma unroll
+    for (int k = 0; k < kOwn; ++k) bnn[k] = bitmask(k, third);  // used two intervals on
+    int g_cnt = 0, g_xr = 0;
+    if (f_g >= 0) {  // the speculative retire's first group, read early
+      g_cnt = __ldcg(&a.cnt[f_g]);
+      g_xr = __ldcg(&a.xr[f_g]);
+    }
+    deltas(iv, fl1, fl2);
+    const long long Pf = pubv.x + (fl1 ? __ldcg(&ws.D[static_cast<size_t>((iv - 1) & 3) * R + first]) : 0);
+    const long long Mf = pubv.y, Tf = pubv.z;
+    int nxt = kInt;
+    longlong4 rec = make_longlong4(0, 0, 0, 0);
+#pragma unroll
+    for (int k = 0; k < kOwn; ++k) {
+      const int c = tid + k * nthreads;
+      if (live[k] && c > first && c < nxt && precedes(c, P_[k], T_[k], mplus(k), first, Pf, Tf, Mf)) {
+        nxt = c;
+        rec = make_longlong4(P_[k], T_[k], mplus(k), (static_cast<long long>(c0[k]) << 32) | static_cast<uint32_t>(c1[k]));
+      }
+    }
+    {
+      const int slot = iv % 3;
+      const int v = block_min_int(nxt, red, sp);
+      if (nxt == v && v != kInt) {
+        ws.win[slot * gridDim.x + blockIdx.x] = rec;
+        atomicMin(&ws.ring[slot], v);
+      }
+      if (blockIdx.x == 0 && threadIdx.x == 0) ws.ring[(iv + 1) % 3] = kInt;
+    }
+    if (f_g >= 0) {
+      a.cnt[f_g] = g_cnt - 1;
+      a.xr[f_g] = g_xr ^ first;
+      if (g_cnt - 1 == 1) add_p(iv, g_xr ^ first, a.wsum[f_g]);
+    }
+    retire_rest(first, f_c0, f_c1, iv, 1);
+    if (tid == 0) {
+      a.out[first] = 0;
+      a.prio[first] = round;
+    }
+#pragma unroll
+    for (int k = 0; k < kOwn; ++k) {
+#pragma unroll
+      for (int s = 0; s < kS; ++s)
+        if ((bpre[k] >> s) & 1u) mg[k][s] -= Tf;
+      if (tid + k * nthreads == first) live[k] = false;
+    }
+    publish(second, iv);
+    const int sf_c0 = f_c0, sf_c1 = f_c1, sf_g = f_g;
+    load_first(second);
+    grid.sync();
+    ++iv;
+    nxt = __ldcg(&ws.ring[(iv - 1) % 3]);
+    fl2 = fl1;
+    fl1 = __ldcg(&ws.flag[(iv - 1) & 3]) != 0;
+    pubv = ldcg4(&ws.pub[(iv - 1) & 1]);
+    if (nxt == kInt) {  // confirmed: `first` was the winner
+      prev = first;
+      first = second;
+#pragma unroll
+      for (int k = 0; k < kOwn; ++k) {
+        bpre[k] = bnext[k];
+        bnext[k] = bnn[k];
+      }
+      continue;
+    }
+    // ---- misspeculation: undo the retire of `first` (its P additions, in
+    // the previous interval's buffer, are never applied), then the chain
+    ++misses;
+    prev = -1;  // (cleared in the replica already)
+    deltas(iv, false, fl2);
+    if (sf_g >= 0) {
+      ++a.cnt[sf_g];
+      a.xr[sf_g] ^= first;
+    }
+    retire_rest(first, sf_c0, sf_c1, iv, -1);
+    if (tid == 0) a.out[first] = 1;
+#pragma unroll
+    for (int k = 0; k < kOwn; ++k) {
+#pragma unroll
+      for (int s = 0; s < kS; ++s)
+        if ((bpre[k] >> s) & 1u) mg[k][s] += Tf;
+      if (tid + k * nthreads == first) live[k] = true;
+    }
+    f_c0 = sf_c0;
+    f_c1 = sf_c1;
+    f_g = sf_g;
+    int best = nxt;
+    longlong4 w = ldcg4(&ws.win[((iv - 1) % 3) * gridDim.x + (nxt % nthreads) / blockDim.x]);
+    for (bool undo_iv = true;; undo_iv = false) {  // one find-first step per interval
+      if (!undo_iv) deltas(iv, fl1, fl2);
+      nxt = kInt;
+#pragma unroll
+      for (int k = 0; k < kOwn; ++k) {
+        const int c = tid + k * nthreads;
+        if (live[k] && c > best && c < nxt && precedes(c, P_[k], T_[k], mplus(k), best, w.x, w.y, w.z)) {
+          nxt = c;
+          rec = make_longlong4(P_[k], T_[k], mplus(k), (static_cast<long long>(c0[k]) << 32) | static_cast<uint32_t>(c1[k]));
+        }
+      }
+      const int slot = iv % 3;
+      const int v = block_min_int(nxt, red, sp);
+      if (nxt == v && v != kInt) {
+        ws.win[slot * gridDim.x + blockIdx.x] = rec;
+        atomicMin(&ws.ring[slot], v);
+      }
+      if (blockIdx.x == 0 && threadIdx.x == 0) ws.ring[(iv + 1) % 3] = kInt;
+      grid.sync();
+      ++iv;
+      nxt = __ldcg(&ws.ring[(iv - 1) % 3]);
+      fl2 = fl1;
+      fl1 = __ldcg(&ws.flag[(iv - 1) & 3]) != 0;
+      if (nxt == kInt) break;
+      best = nxt;
+      w = ldcg4(&ws.win[((iv - 1) % 3) * gridDim.x + (nxt % nthreads) / blockDim.x]);
+    }
+    // ---- retire `best` (the incumbent `first` stays for the next round)
+    deltas(iv, fl1, fl2);
+    if (blockIdx.x == 0 && threadIdx.x == 0) ws.ring[(iv + 1) % 3] = kInt;  // the next interval's min slot
+    {
+      const int e0 = static_cast<int>(w.w >> 32), e1 = static_cast<int>(w.w & 0xffffffff);
+      if (e0 + tid < e1) {
+        const int32_t g = a.col[e0 + tid];
+        const int k = --a.cnt[g];
+        const int x = (a.xr[g] ^= best);
+        if (k == 1) add_p(iv, x, a.wsum[g]);
+      }
+      retire_rest(best, e0, e1, iv, 1);
+    }
+    if (tid == 0) {
+      a.out[best] = 0;
+      a.prio[best] = round;
+    }
+#pragma unroll
+    for (int k = 0; k < kOwn; ++k) {
+      const uint32_t m = bitmask(k, best);
+#pragma unroll
+      for (int s = 0; s < kS; ++s)
+        if ((m >> s) & 1u) mg[k][s] -= w.y;
+      if (tid + k * nthreads == best) live[k] = false;
+    }
+    publish(first, iv);
+    const int second2 = next_live(first, best, -1);
+#pragma unroll
+    for (int k = 0; k < kOwn; ++k) bnext[k] = bitmask(k, second2);
+    grid.sync();
+    ++iv;
+    fl2 = fl1;
+    fl1 = __ldcg(&ws.flag[(iv - 1) & 3]) != 0;
+    pubv = ldcg4(&ws.pub[(iv - 1) & 1]);
+    prev = best;
+  }
+  if (tid == 0) ws.ring[3] = misses;
+}
+
 // TAC on one thread-block cluster (kClusterMax CTAs): cluster barriers are
 // hardware (≈0.3 µs on B200 against ≈1.25 µs for a cooperative grid sync),
 // and the rounds are barrier-bound. CTA k owns recv columns
@@ -1044,6 +1354,347 @@ __global__ void __launch_bounds__(1024) tac_dsm_kernel(TacArgs a, int per, int g
       do ++first;
       while (first < R && !is_live(first));
   }
+}
+
+// Speculative TAC on one 16-CTA thread-block cluster: tac_spec_kernel's
+// one-barrier rounds (compare every candidate against `first` and retire
+// `first` in the same interval) with every per-round value in distributed
+// shared memory, so a round is one hardware cluster barrier (~0.3 us) and
+// DSMEM reads instead of a grid barrier and L2 round trips. CTA k owns
+// columns [k*per, (k+1)*per): P, the direct-successor groups' M (amended M+
+// is their min) and a P-delta slot per column in its shared memory, T in
+// registers; each thread caches the closure words (group, first / 32) of
+// its columns' groups, reloaded when `first` crosses a 32-column boundary.
+// P additions of a retire (rare: a group dropping to one outstanding recv)
+// go to the owners' delta slots and raise a flag in every CTA; the next
+// interval then applies them and republishes the incumbent ("fixup") before
+// speculating again. Group cnt / owner XOR stay in global memory (one
+// thread per group per retire).
+struct CSpecPub {
+  long long P, mp, T;
+  int c, pad;
+};
+
+// V: the value width, int when every time sum fits 31 bits (host check),
+// which makes a candidate's comparison a handful of 32-bit instructions
+// (the rounds are issue-bound at 10^5 candidates on 16 SMs).
+__host__ __device__ inline size_t tac_cspec_smem(int per, int kS, int R, size_t vb) {
+  return (vb + vb * kS + vb) * per + 8ull * ((R + 63) / 64) + 3 * sizeof(TacRec) + 2 * sizeof(CSpecPub) + 64;
+}
+
+template <typename V>
+__device__ __forceinline__ bool precedes_v(int a, V ap, V am, V amp, int b, V bp, V bm, V bmp) {
+  const V ab = min(bp, am), ba = min(ap, bm);
+  if (ab != ba) return ab < ba;
+  if (amp != bmp) return amp < bmp;
+  return a < b;
+}
+
+template <int kOwn, int kS, typename V>
+__global__ void __launch_bounds__(1024) tac_cspec_kernel(TacArgs a, const uint32_t* __restrict__ bits, int W, int per,
+                                                         int* trace) {
+  constexpr V kInfV = sizeof(V) == 8 ? static_cast<V>(kInf) : static_cast<V>(0x7fffffff);
+  constexpr V kDead = sizeof(V) == 8 ? static_cast<V>(INT64_MIN) : static_cast<V>(INT32_MIN);  // P of a retired column
+  cg::cluster_group cluster = cg::this_cluster();
+  extern __shared__ __align__(16) char csp[];
+  __shared__ int bred[3];
+  __shared__ TacRec bcast;
+  __shared__ CSpecPub fpub;
+  __shared__ int dflag[2];  // some retire added to a P of this CTA's columns, per interval parity (set remotely)
+  int sp = 0, q = 0, iv = 0;
+  const int R = a.R, cs = static_cast<int>(cluster.num_blocks());
+  const int rank = static_cast<int>(cluster.block_rank());
+  const int base = rank * per, n_own = max(0, min(per, R - base));
+  auto* P_s = reinterpret_cast<V*>(csp);                     // [per] (kDead once retired)
+  auto* D_s = P_s + per;                                      // [per] P additions of the last retire
+  auto* Mg_s = D_s + per;                                     // [kS][per] M of direct-successor groups
+  auto* live = reinterpret_cast<uint32_t*>(csp + round16((2 + kS) * sizeof(V) * per));  // replicated outstanding bitset
+  auto* rec = reinterpret_cast<TacRec*>(live + 2 * ((R + 63) / 64));  // 3-slot winner ring
+  auto* pub = reinterpret_cast<CSpecPub*>(rec + 3);                    // [2] next incumbent (at its owner)
+  const int kInt = 0x7fffffff;
+  V T_[kOwn];
+  int sg[kOwn][kS], ns[kOwn];
+  uint32_t bwv[kOwn][kS];  // closure words (group, wc) of own columns' groups
+#pragma unroll
+  for (int k = 0; k < kOwn; ++k) {
+    const int j = threadIdx.x + k * blockDim.x, c = base + j;
+    const bool own = j < n_own;
+    T_[k] = own ? static_cast<V>(a.tcol[c]) : V(0);
+    ns[k] = own ? a.succ_off[c + 1] - a.succ_off[c] : 0;
+#pragma unroll
+    for (int s = 0; s < kS; ++s) {
+      sg[k][s] = s < ns[k] ? a.succ[a.succ_off[c] + s] : 0;
+      if (own) Mg_s[s * per + j] = s < ns[k] ? static_cast<V>(a.M[sg[k][s]]) : kInfV;
+      bwv[k][s] = 0;
+    }
+    if (own) {
+      P_s[j] = a.out[c] ? static_cast<V>(a.P[c]) : kDead;
+      D_s[j] = 0;
+    }
+  }
+  for (int w = threadIdx.x; w < (R + 31) / 32; w += blockDim.x) {
+    uint32_t b = 0;
+    for (int i = 0; i < 32 && w * 32 + i < R; ++i) b |= (a.out[w * 32 + i] ? 1u : 0u) << i;
+    live[w] = b;
+  }
+  if (threadIdx.x < 3) {
+    bred[threadIdx.x] = kInt;
+    rec[threadIdx.x].c = kInt;
+  }
+  if (threadIdx.x < 2) dflag[threadIdx.x] = 0;
+  auto is_live = [&](int c) { return (live[c >> 5] >> (c & 31)) & 1u; };
+  auto owner = [&](int c) { return c / per; };
+  auto mplus_j = [&](int j) {
+    V m = kInfV;
+#pragma unroll
+    for (int s = 0; s < kS; ++s) m = min(m, Mg_s[s * per + j]);
+    return m;
+  };
+  auto next_live = [&](int c, int skip) {
+    do ++c;
+    while (c < R && (c == skip || !is_live(c)));
+    return c;
+  };
+  int wc = -1;  // closure word index cached in bwv
+  auto load_words = [&](int word) {
+#pragma unroll
+    for (int k = 0; k < kOwn; ++k)
+#pragma unroll
+      for (int s = 0; s < kS; ++s)
+        bwv[k][s] = s < ns[k] ? __ldg(&bits[static_cast<size_t>(sg[k][s]) * W + word]) : 0u;
+    wc = word;
+  };
+  // M of own columns' groups after retiring column col (sign -1: undo)
+  auto apply_retire = [&](int col, V t, int sign) {
+    if ((col >> 5) != wc) load_words(col >> 5);
+#pragma unroll
+    for (int k = 0; k < kOwn; ++k) {
+      const int j = threadIdx.x + k * blockDim.x;
+      if (j >= n_own) continue;
+#pragma unroll
+      for (int s = 0; s < kS; ++s)
+        if ((bwv[k][s] >> (col & 31)) & 1u) Mg_s[s * per + j] -= sign * t;
+    }
+  };
+  auto publish = [&](int col, int slot) {  // owner thread of col: its values for the next interval
+    if (col < R && owner(col) == rank && threadIdx.x == (col - base) % blockDim.x) {
+      const int j = col - base, kk = j / blockDim.x;
+      V t = 0;
+#pragma unroll
+      for (int k = 0; k < kOwn; ++k)
+        if (k == kk) t = T_[k];
+      pub[slot] = CSpecPub{P_s[j], mplus_j(j), t, col, 0};
+    }
+  };
+  auto apply_deltas = [&]() {
+#pragma unroll
+    for (int k = 0; k < kOwn; ++k) {
+      const int j = threadIdx.x + k * blockDim.x;
+      if (j < n_own && D_s[j] != 0) {
+        P_s[j] += D_s[j];
+        D_s[j] = 0;
+      }
+    }
+  };
+  const int tid = rank * blockDim.x + threadIdx.x, nthreads = cs * blockDim.x;
+  // group updates of a retire (sign 1) or undo (sign -1) over the column's
+  // list from entry e0 + tid + skip on (atomics: the state lives at L2
+  // whatever the L1s hold; one thread per group)
+  auto add_p = [&](int x, unsigned long long wsum) {
+    if constexpr (sizeof(V) == 8)
+      atomicAdd(reinterpret_cast<unsigned long long*>(cluster.map_shared_rank(&D_s[x - owner(x) * per], owner(x))), wsum);
+    else
+      atomicAdd(cluster.map_shared_rank(&D_s[x - owner(x) * per], owner(x)), static_cast<V>(wsum));
+    for (int r = 0; r < cs; ++r) *cluster.map_shared_rank(&dflag[iv & 1], r) = 1;
+  };
+  auto retire_groups = [&](int col, int e0, int e1, int skip, int sign) {
+    for (int e = e0 + tid + skip; e < e1; e += nthreads) {
+      const int32_t g = a.col[e];
+      const int kk = atomicSub(&a.cnt[g], sign) - sign;
+      const int x = atomicXor(&a.xr[g], col) ^ col;
+      if (sign > 0 && kk == 1) add_p(x, a.wsum[g]);
+    }
+  };
+  // end of an interval: the cluster barrier; returns this CTA's delta flag
+  // for the interval just ended (reset after everyone has read it)
+  auto end_interval = [&]() {
+    cluster.sync();
+    ++iv;
+    return dflag[(iv - 1) & 1] != 0;
+  };
+  auto reset_flag = [&]() {  // after a block barrier that follows end_interval's read
+    if (threadIdx.x == 0) dflag[(iv - 1) & 1] = 0;
+  };
+  // cluster-wide min of v with the winners' records (its own interval)
+  auto cluster_min_rec = [&](int v, const TacRec& mine) -> TacRec {
+    const int slot = q % 3;
+    const int bv = block_min_int(v, bred, sp);
+    if (v == bv && bv != kInt) rec[slot] = mine;
+    if (threadIdx.x == 0) rec[slot].c = bv;
+    end_interval();
+    if (threadIdx.x < 32) {
+      int c = kInt;
+      if (static_cast<int>(threadIdx.x) < cs) c = cluster.map_shared_rank(&rec[slot], threadIdx.x)->c;
+      const int m = __reduce_min_sync(~0u, c);
+      if (m != kInt && c == m) bcast = *cluster.map_shared_rank(&rec[slot], threadIdx.x);
+      if (threadIdx.x == 0 && m == kInt) bcast.c = m;
+    }
+    __syncthreads();
+    const TacRec w = bcast;
+    reset_flag();
+    ++q;
+    __syncthreads();  // bcast is rewritten by the next call
+    return w;
+  };
+  auto read_pub = [&](int col, int slot) {  // after the interval that published it
+    if (threadIdx.x == 0) fpub = *cluster.map_shared_rank(&pub[slot], owner(col));
+    __syncthreads();
+    const CSpecPub v = fpub;
+    reset_flag();
+    __syncthreads();
+    return v;
+  };
+  cluster.sync();  // slices, bitsets and rings ready in every CTA
+  int first = next_live(-1, -1);
+  int pslot = 0;  // pub slot holding the incumbent's values
+  publish(first, pslot);
+  int f_c0 = 0, f_c1 = 0, f_g = -1;
+  auto load_first = [&](int col) {
+    f_c0 = col < R ? a.col_off[col] : 0;
+    f_c1 = col < R ? a.col_off[col + 1] : 0;
+    f_g = f_c0 + tid < f_c1 ? a.col[f_c0 + tid] : -1;
+  };
+  load_first(first);
+  if (first < R) load_words(first >> 5);
+  end_interval();
+  CSpecPub fp = read_pub(first, pslot);
+  int misses = 0;
+  for (int round = 0; round < R; ++round) {
+    // ---- speculative interval: retire `first` (its group updates issued
+    // first: nothing this interval reads them), compare against it
+    const int second = next_live(first, first);
+    int rk = 0, rx = 0;
+    if (f_g >= 0) {
+      rk = atomicSub(&a.cnt[f_g], 1) - 1;
+      rx = atomicXor(&a.xr[f_g], first) ^ first;
+    }
+    retire_groups(first, f_c0, f_c1, nthreads, 1);  // entries beyond one per thread (rare)
+    if (tid == 0) a.prio[first] = round;
+    // the next incumbent's list and this thread's entry of it
+    const int n_c0 = second < R ? a.col_off[second] : 0, n_c1 = second < R ? a.col_off[second + 1] : 0;
+    const int n_g = n_c0 + tid < n_c1 ? a.col[n_c0 + tid] : -1;
+    if ((first >> 5) != wc) load_words(first >> 5);
+    int nxt = kInt;
+    TacRec mine{0, 0, 0, kInt, 0};
+    const V fP = static_cast<V>(fp.P), fT = static_cast<V>(fp.T), fM = static_cast<V>(fp.mp);
+#pragma unroll
+    for (int k = 0; k < kOwn; ++k) {  // every column <= first is retired (kDead)
+      const int j = threadIdx.x + k * blockDim.x, c = base + j;
+      if (j < n_own && c < nxt) {
+        const V pc = P_s[j];
+        if (pc != kDead) {
+          const V mc = mplus_j(j);
+          if (precedes_v(c, pc, T_[k], mc, first, fP, fT, fM)) {
+            nxt = c;
+            mine = TacRec{pc, T_[k], mc, c, 0};
+          }
+        }
+      }
+    }
+    const int slot = q % 3;
+    const int bv = block_min_int(nxt, bred, sp);  // (every compare of this CTA is done)
+    if (nxt == bv && bv != kInt) rec[slot] = mine;
+    if (threadIdx.x == 0) rec[slot].c = bv;
+    apply_retire(first, static_cast<V>(fp.T), 1);
+    const int npslot = pslot ^ 1;
+    publish(second, npslot);  // M+ after this retire, P without its additions
+    if (f_g >= 0 && rk == 1) add_p(rx, a.wsum[f_g]);
+    const bool deltas = end_interval();
+    if (threadIdx.x < 32) {
+      int c = kInt;
+      if (static_cast<int>(threadIdx.x) < cs) c = cluster.map_shared_rank(&rec[slot], threadIdx.x)->c;
+      const int m = __reduce_min_sync(~0u, c);
+      if (m != kInt && c == m) bcast = *cluster.map_shared_rank(&rec[slot], threadIdx.x);
+      if (threadIdx.x == 0 && m == kInt) bcast.c = m;
+      if (threadIdx.x == 0 && second < R) fpub = *cluster.map_shared_rank(&pub[npslot], owner(second));
+    }
+    __syncthreads();
+    TacRec w = bcast;
+    const CSpecPub np = fpub;
+    reset_flag();
+    ++q;
+    __syncthreads();  // bcast / fpub are rewritten later
+    if (w.c == kInt) {  // confirmed: `first` was the winner
+      if (threadIdx.x == 0) live[first >> 5] &= ~(1u << (first & 31));
+      if (owner(first) == rank && threadIdx.x == (first - base) % blockDim.x) P_s[first - base] = kDead;
+      first = second;
+      pslot = npslot;
+      fp = np;
+      f_c0 = n_c0;
+      f_c1 = n_c1;
+      f_g = n_g;
+      if (deltas) {  // (every CTA's flag was raised: the fixup is cluster-uniform)
+        apply_deltas();
+        __syncthreads();
+        pslot ^= 1;
+        publish(first, pslot);
+        end_interval();
+        fp = read_pub(first, pslot);
+      }
+      continue;
+    }
+    // ---- misspeculation: undo the retire of `first` (its P additions are
+    // dropped), then the chain from w, then retire the chain's winner
+    ++misses;
+    retire_groups(first, f_c0, f_c1, 0, -1);
+    apply_retire(first, static_cast<V>(fp.T), -1);
+#pragma unroll
+    for (int k = 0; k < kOwn; ++k) {
+      const int j = threadIdx.x + k * blockDim.x;
+      if (j < n_own) D_s[j] = 0;
+    }
+    end_interval();  // undo complete everywhere
+    __syncthreads();
+    reset_flag();
+    for (;;) {
+      const int best = w.c;
+      int nb = kInt;
+      TacRec mb{0, 0, 0, kInt, 0};
+#pragma unroll
+      for (int k = 0; k < kOwn; ++k) {
+        const int j = threadIdx.x + k * blockDim.x, c = base + j;
+        if (j < n_own && c > best && c < nb) {
+          const V pc = P_s[j];
+          if (pc != kDead) {
+            const V mc = mplus_j(j);
+            if (precedes_v(c, pc, T_[k], mc, best, static_cast<V>(w.P), static_cast<V>(w.T), static_cast<V>(w.mp))) {
+              nb = c;
+              mb = TacRec{pc, T_[k], mc, c, 0};
+            }
+          }
+        }
+      }
+      const TacRec nw = cluster_min_rec(nb, mb);
+      if (nw.c == kInt) break;
+      w = nw;
+    }
+    const int best = w.c;
+    retire_groups(best, a.col_off[best], a.col_off[best + 1], 0, 1);
+    if (tid == 0) a.prio[best] = round;
+    apply_retire(best, static_cast<V>(w.T), 1);
+    end_interval();  // the retire's additions have landed
+    if (threadIdx.x == 0) live[best >> 5] &= ~(1u << (best & 31));
+    if (owner(best) == rank && threadIdx.x == (best - base) % blockDim.x) P_s[best - base] = kDead;
+    apply_deltas();
+    __syncthreads();
+    reset_flag();
+    pslot ^= 1;
+    publish(first, pslot);
+    end_interval();
+    fp = read_pub(first, pslot);
+    if ((first >> 5) != wc) load_words(first >> 5);
+  }
+  if (trace && rank == 0 && threadIdx.x == 0) *trace = misses;
 }
 
 // Shared setup for properties / tic / tac: rows, closure, group state,
@@ -1399,7 +2050,68 @@ extern "C" int csk_tac(DeviceGraph* g, const int64_t* dur, int32_t* prio, char* 
     if (trace) std::fprintf(stderr, "[tac] DSMEM cluster of %d CTAs, %d columns and %d groups each\n", cs, per, gper);
     return true;
   };
-  if (dsm_force || (!dsm_off && !cl_force && !forced_blocks && !one_block_fits)) launched = try_dsm();
+  // The speculative cluster kernel: TICTAC_TAC_CSPEC=0 disables it, =1 forces it (tests).
+  const char* cspec_env = std::getenv("TICTAC_TAC_CSPEC");
+  const bool cspec_force = cspec_env && std::atoi(cspec_env) == 1, cspec_off = cspec_env && std::atoi(cspec_env) == 0;
+  int trace_misses = -1;
+  auto try_cspec = [&]() -> bool {
+    const int cs = kClusterMax, per = (R + cs - 1) / cs, kown = (per + 1023) / 1024;
+    int max_succ = 0;
+    for (int c = 0; c < R; ++c) max_succ = std::max(max_succ, S.rw->succ_off[c + 1] - S.rw->succ_off[c]);
+    const int kS = max_succ <= 1 ? 1 : 2;
+    // 32-bit values when every duration sum fits (P <= all compute, M <= all recv time)
+    int64_t total = 0;
+    for (int v = 0; v < g->n; ++v) total += dur[v];
+    const bool narrow = total < 0x7fff0000LL && !std::getenv("TICTAC_TAC_WIDE");
+    const size_t smem = tac_cspec_smem(per, kS, R, narrow ? 4 : 8);
+    if (smem > 220 * 1024 || kown > 8 || max_succ > 2) return false;
+    using KF = void (*)(TacArgs, const uint32_t*, int, int, int*);
+    KF fn = nullptr;
+#define CSPEC_PICK(V)                                                                                          \
+  (kS == 1 ? (kown <= 1   ? tac_cspec_kernel<1, 1, V>                                                          \
+              : kown <= 2 ? tac_cspec_kernel<2, 1, V>                                                          \
+              : kown <= 4 ? tac_cspec_kernel<4, 1, V>                                                          \
+                          : tac_cspec_kernel<8, 1, V>)                                                         \
+           : (kown <= 1   ? tac_cspec_kernel<1, 2, V>                                                          \
+              : kown <= 2 ? tac_cspec_kernel<2, 2, V>                                                          \
+              : kown <= 4 ? tac_cspec_kernel<4, 2, V>                                                          \
+                          : tac_cspec_kernel<8, 2, V>))
+    fn = narrow ? CSPEC_PICK(int) : CSPEC_PICK(long long);
+#undef CSPEC_PICK
+    CK(allow_max_dynamic_smem(reinterpret_cast<const void*>(fn)));
+    CK(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(cs);
+    cfg.blockDim = dim3(1024);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = cs;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int nclusters = 0;
+    if (cudaOccupancyMaxActiveClusters(&nclusters, fn, &cfg) != cudaSuccess || nclusters < 1) {
+      cudaGetLastError();
+      return false;
+    }
+    DevArr d_tr;
+    if (alloc<int>(d_tr, 1, err)) return false;
+    CK(cudaMemset(d_tr.p, 0, 4));
+    int* tp = d_tr.as<int>();
+    const uint32_t* bp = S.d_bits.as<uint32_t>();
+    const int Wd = S.rw->W;
+    CK(cudaLaunchKernelEx(&cfg, fn, a, bp, Wd, per, tp));
+    if (trace) {
+      CK(cudaMemcpy(&trace_misses, tp, 4, cudaMemcpyDeviceToHost));
+      std::fprintf(stderr, "[tac] speculative cluster of %d CTAs, %d columns each, %d misspeculated\n", cs, per,
+                   trace_misses);
+    }
+    return true;
+  };
+  if (cspec_force || (!cspec_off && !dsm_force && !cl_force && !forced_blocks && !one_block_fits)) launched = try_cspec();
+  if (!launched && (dsm_force || (!dsm_off && !cl_force && !forced_blocks && !one_block_fits))) launched = try_dsm();
   // (measured: 10^5 ops / 10^4 recvs 61 → 55 ms; at 10^6 / 10^5 the grid
   // kernels' memory parallelism over 100+ SMs wins, 0.80 s vs 1.23 s)
   if (!launched && (cl_force || (!cl_off && !forced_blocks && blocks == 1 && !one_block_fits)))
@@ -1441,6 +2153,51 @@ extern "C" int csk_tac(DeviceGraph* g, const int64_t* dur, int32_t* prio, char* 
     longlong4* wp = d_win.as<longlong4>();
     void* args_own[] = {&a, &rp, &wp};
     void* kern = reinterpret_cast<void*>(tac_dist_kernel);
+    // the speculative kernel when every column's direct-successor groups fit
+    // its registers (TICTAC_TAC_SPEC=0: tac_own_kernel)
+    int max_succ = 0;
+    for (int c = 0; c < R; ++c) max_succ = std::max(max_succ, S.rw->succ_off[c + 1] - S.rw->succ_off[c]);
+    const char* spec_env = std::getenv("TICTAC_TAC_SPEC");
+    if (!std::getenv("TICTAC_TAC_NO_OWN") && !(spec_env && std::atoi(spec_env) == 0) && per <= 4 &&
+        max_succ <= kSpecS) {
+      DevArr d_D, d_flag, d_pub;
+      if (alloc<long long>(d_D, 4ull * R, err) || alloc<int>(d_flag, 4, err) || alloc<longlong4>(d_pub, 2, err))
+        return 1;
+      CK(cudaMemset(d_D.p, 0, 32ull * R));
+      CK(cudaMemset(d_flag.p, 0, 16));
+      TacSpecWs ws{S.d_bits.as<uint32_t>(), S.rw->W, d_D.as<long long>(), d_flag.as<int>(), d_pub.as<longlong4>(), rp, wp};
+      void* args_spec[] = {&a, &ws};
+      void* sk = nullptr;
+      if (max_succ <= 1)
+        sk = per <= 1 ? reinterpret_cast<void*>(tac_spec_kernel<1, 1>)
+             : per <= 2 ? reinterpret_cast<void*>(tac_spec_kernel<2, 1>)
+                        : reinterpret_cast<void*>(tac_spec_kernel<4, 1>);
+      else if (max_succ <= 2)
+        sk = per <= 1 ? reinterpret_cast<void*>(tac_spec_kernel<1, 2>)
+             : per <= 2 ? reinterpret_cast<void*>(tac_spec_kernel<2, 2>)
+                        : reinterpret_cast<void*>(tac_spec_kernel<4, 2>);
+      else
+        sk = per <= 1 ? reinterpret_cast<void*>(tac_spec_kernel<1, 4>)
+             : per <= 2 ? reinterpret_cast<void*>(tac_spec_kernel<2, 4>)
+                        : reinterpret_cast<void*>(tac_spec_kernel<4, 4>);
+      const size_t spec_smem = 4ull * ((R + 31) / 32);
+      CK(allow_max_dynamic_smem(sk));
+      int per_sm_spec = 0;
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_spec, sk, 1024, spec_smem));
+      if (spec_smem <= 200 * 1024 && per_sm_spec * sms >= blocks) {
+        CK(cudaLaunchCooperativeKernel(sk, blocks, 1024, args_spec, spec_smem, nullptr));
+        LAUNCHED();
+        CK(cudaGetLastError());
+        CK(cudaMemcpy(prio, d_prio.p, 4ull * R, cudaMemcpyDeviceToHost));
+        if (trace) {
+          int misses = 0;
+          CK(cudaMemcpy(&misses, rp + 3, 4, cudaMemcpyDeviceToHost));
+          std::fprintf(stderr, "[tac] setup %.3f ms, state %.3f ms, rounds (%d blocks, speculative) %.3f ms, %d misspeculated\n",
+                       ms(t0, t1), ms(t1, t2), blocks, ms(t2, now()), misses);
+        }
+        return 0;
+      }
+    }
     if (!std::getenv("TICTAC_TAC_NO_OWN")) {
       if (per <= 1)
         kern = reinterpret_cast<void*>(tac_own_kernel<1>);

@@ -76,9 +76,17 @@ def test_multiblock_tac_matches_single_block(orc):
     # "dsm": the cluster kernel with every per-round value in distributed
     # shared memory (the default where one block's shared memory cannot hold
     # the state)
-    for blocks in ("1", "1g", "1c", "2", "3", "7", "64", "cl", "dsm"):
+    # "cspec": the speculative cluster kernel (the default where one block's
+    # shared memory cannot hold the state); "7own": the non-speculative grid
+    # kernel (TICTAC_TAC_SPEC=0)
+    for blocks in ("1", "1g", "1c", "2", "3", "7", "64", "cl", "dsm", "cspec", "7own"):
         env = dict(os.environ)
-        if blocks == "cl":
+        if blocks == "cspec":
+            env["TICTAC_TAC_CSPEC"] = "1"
+        elif blocks == "7own":
+            env["TICTAC_TAC_BLOCKS"] = "7"
+            env["TICTAC_TAC_SPEC"] = "0"
+        elif blocks == "cl":
             env["TICTAC_TAC_CLUSTER"] = "1"
         elif blocks == "dsm":
             env["TICTAC_TAC_DSM"] = "1"
@@ -92,7 +100,7 @@ def test_multiblock_tac_matches_single_block(orc):
                            env=env)
         res[blocks] = json.loads(r.stdout.strip().splitlines()[-1])
     assert res["1"] == res["1g"] == res["1c"] == res["2"] == res["3"] == res["7"] == res["64"] == res["cl"] \
-        == res["dsm"]
+        == res["dsm"] == res["cspec"] == res["7own"]
     for spec in ("layered:10000:1000", "layered:100000:10000"):
         assert res["64"][spec] == TAC_LARGE[spec]["sha256"]
 
