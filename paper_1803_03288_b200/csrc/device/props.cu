@@ -1393,6 +1393,7 @@ __device__ __forceinline__ bool precedes_v(int a, V ap, V am, V amp, int b, V bp
 template <int kOwn, int kS, typename V>
 __global__ void __launch_bounds__(1024) tac_cspec_kernel(TacArgs a, const uint32_t* __restrict__ bits, int W, int per,
                                                          int* trace) {
+  constexpr int kCT = 1024;  // threads per CTA (the launch's block size)
   constexpr V kInfV = sizeof(V) == 8 ? static_cast<V>(kInf) : static_cast<V>(0x7fffffff);
   constexpr V kDead = sizeof(V) == 8 ? static_cast<V>(INT64_MIN) : static_cast<V>(INT32_MIN);  // P of a retired column
   cg::cluster_group cluster = cg::this_cluster();
@@ -1417,7 +1418,7 @@ __global__ void __launch_bounds__(1024) tac_cspec_kernel(TacArgs a, const uint32
   uint32_t bwv[kOwn][kS];  // closure words (group, wc) of own columns' groups
 #pragma unroll
   for (int k = 0; k < kOwn; ++k) {
-    const int j = threadIdx.x + k * blockDim.x, c = base + j;
+    const int j = threadIdx.x + k * kCT, c = base + j;
     const bool own = j < n_own;
     T_[k] = own ? static_cast<V>(a.tcol[c]) : V(0);
     ns[k] = own ? a.succ_off[c + 1] - a.succ_off[c] : 0;
@@ -1432,7 +1433,7 @@ __global__ void __launch_bounds__(1024) tac_cspec_kernel(TacArgs a, const uint32
       D_s[j] = 0;
     }
   }
-  for (int w = threadIdx.x; w < (R + 31) / 32; w += blockDim.x) {
+  for (int w = threadIdx.x; w < (R + 31) / 32; w += kCT) {
     uint32_t b = 0;
     for (int i = 0; i < 32 && w * 32 + i < R; ++i) b |= (a.out[w * 32 + i] ? 1u : 0u) << i;
     live[w] = b;
@@ -1444,6 +1445,11 @@ __global__ void __launch_bounds__(1024) tac_cspec_kernel(TacArgs a, const uint32
   if (threadIdx.x < 2) dflag[threadIdx.x] = 0;
   auto is_live = [&](int c) { return (live[c >> 5] >> (c & 31)) & 1u; };
   auto owner = [&](int c) { return c / per; };
+  // this thread owns column c (columns base + threadIdx.x + k * 1024)
+  auto mine_col = [&](int c) {
+    const unsigned j = static_cast<unsigned>(c - base);
+    return j < static_cast<unsigned>(n_own) && (j & 1023u) == threadIdx.x;
+  };
   auto mplus_j = [&](int j) {
     V m = kInfV;
 #pragma unroll
@@ -1469,7 +1475,7 @@ __global__ void __launch_bounds__(1024) tac_cspec_kernel(TacArgs a, const uint32
     if ((col >> 5) != wc) load_words(col >> 5);
 #pragma unroll
     for (int k = 0; k < kOwn; ++k) {
-      const int j = threadIdx.x + k * blockDim.x;
+      const int j = threadIdx.x + k * kCT;
       if (j >= n_own) continue;
 #pragma unroll
       for (int s = 0; s < kS; ++s)
@@ -1477,8 +1483,8 @@ __global__ void __launch_bounds__(1024) tac_cspec_kernel(TacArgs a, const uint32
     }
   };
   auto publish = [&](int col, int slot) {  // owner thread of col: its values for the next interval
-    if (col < R && owner(col) == rank && threadIdx.x == (col - base) % blockDim.x) {
-      const int j = col - base, kk = j / blockDim.x;
+    if (col < R && mine_col(col)) {
+      const int j = col - base, kk = j >> 10;
       V t = 0;
 #pragma unroll
       for (int k = 0; k < kOwn; ++k)
@@ -1489,14 +1495,14 @@ __global__ void __launch_bounds__(1024) tac_cspec_kernel(TacArgs a, const uint32
   auto apply_deltas = [&]() {
 #pragma unroll
     for (int k = 0; k < kOwn; ++k) {
-      const int j = threadIdx.x + k * blockDim.x;
+      const int j = threadIdx.x + k * kCT;
       if (j < n_own && D_s[j] != 0) {
         P_s[j] += D_s[j];
         D_s[j] = 0;
       }
     }
   };
-  const int tid = rank * blockDim.x + threadIdx.x, nthreads = cs * blockDim.x;
+  const int tid = rank * kCT + threadIdx.x, nthreads = cs * kCT;
   // group updates of a retire (sign 1) or undo (sign -1) over the column's
   // list from entry e0 + tid + skip on (atomics: the state lives at L2
   // whatever the L1s hold; one thread per group)
@@ -1589,7 +1595,7 @@ __global__ void __launch_bounds__(1024) tac_cspec_kernel(TacArgs a, const uint32
     const V fP = static_cast<V>(fp.P), fT = static_cast<V>(fp.T), fM = static_cast<V>(fp.mp);
 #pragma unroll
     for (int k = 0; k < kOwn; ++k) {  // every column <= first is retired (kDead)
-      const int j = threadIdx.x + k * blockDim.x, c = base + j;
+      const int j = threadIdx.x + k * kCT, c = base + j;
       if (j < n_own && c < nxt) {
         const V pc = P_s[j];
         if (pc != kDead) {
@@ -1626,7 +1632,7 @@ __global__ void __launch_bounds__(1024) tac_cspec_kernel(TacArgs a, const uint32
     __syncthreads();  // bcast / fpub are rewritten later
     if (w.c == kInt) {  // confirmed: `first` was the winner
       if (threadIdx.x == 0) live[first >> 5] &= ~(1u << (first & 31));
-      if (owner(first) == rank && threadIdx.x == (first - base) % blockDim.x) P_s[first - base] = kDead;
+      if (mine_col(first)) P_s[first - base] = kDead;
       first = second;
       pslot = npslot;
       fp = np;
@@ -1650,7 +1656,7 @@ __global__ void __launch_bounds__(1024) tac_cspec_kernel(TacArgs a, const uint32
     apply_retire(first, static_cast<V>(fp.T), -1);
 #pragma unroll
     for (int k = 0; k < kOwn; ++k) {
-      const int j = threadIdx.x + k * blockDim.x;
+      const int j = threadIdx.x + k * kCT;
       if (j < n_own) D_s[j] = 0;
     }
     end_interval();  // undo complete everywhere
@@ -1662,7 +1668,7 @@ __global__ void __launch_bounds__(1024) tac_cspec_kernel(TacArgs a, const uint32
       TacRec mb{0, 0, 0, kInt, 0};
 #pragma unroll
       for (int k = 0; k < kOwn; ++k) {
-        const int j = threadIdx.x + k * blockDim.x, c = base + j;
+        const int j = threadIdx.x + k * kCT, c = base + j;
         if (j < n_own && c > best && c < nb) {
           const V pc = P_s[j];
           if (pc != kDead) {
@@ -1684,7 +1690,7 @@ __global__ void __launch_bounds__(1024) tac_cspec_kernel(TacArgs a, const uint32
     apply_retire(best, static_cast<V>(w.T), 1);
     end_interval();  // the retire's additions have landed
     if (threadIdx.x == 0) live[best >> 5] &= ~(1u << (best & 31));
-    if (owner(best) == rank && threadIdx.x == (best - base) % blockDim.x) P_s[best - base] = kDead;
+    if (mine_col(best)) P_s[best - base] = kDead;
     apply_deltas();
     __syncthreads();
     reset_flag();
