@@ -1402,10 +1402,17 @@ __global__ void __launch_bounds__(1024) tac_cspec_kernel(TacArgs a, const uint32
   __shared__ TacRec bcast;
   __shared__ CSpecPub fpub;
   __shared__ int dflag[2];  // some retire added to a P of this CTA's columns, per interval parity (set remotely)
+  __shared__ int mins[3][kClusterMax];     // every CTA's block min, pushed into every CTA (3-slot ring)
+  __shared__ CSpecPub pubs[2];             // the next incumbent's values, pushed by its owner
   int sp = 0, q = 0, iv = 0;
   const int R = a.R, cs = static_cast<int>(cluster.num_blocks());
   const int rank = static_cast<int>(cluster.block_rank());
-  const int base = rank * per, n_own = max(0, min(per, R - base));
+  // columns are interleaved over the CTAs (c % 16 owns c, at local index
+  // c / 16), so every CTA keeps the same share of outstanding columns as
+  // they retire in order
+  constexpr int kCS = kClusterMax;
+  const int n_own = max(0, (R - rank + kCS - 1) / kCS);
+  (void)cs;
   auto* P_s = reinterpret_cast<V*>(csp);                     // [per] (kDead once retired)
   auto* D_s = P_s + per;                                      // [per] P additions of the last retire
   auto* Mg_s = D_s + per;                                     // [kS][per] M of direct-successor groups
@@ -1418,7 +1425,7 @@ __global__ void __launch_bounds__(1024) tac_cspec_kernel(TacArgs a, const uint32
   uint32_t bwv[kOwn][kS];  // closure words (group, wc) of own columns' groups
 #pragma unroll
   for (int k = 0; k < kOwn; ++k) {
-    const int j = threadIdx.x + k * kCT, c = base + j;
+    const int j = threadIdx.x + k * kCT, c = j * kCS + rank;
     const bool own = j < n_own;
     T_[k] = own ? static_cast<V>(a.tcol[c]) : V(0);
     ns[k] = own ? a.succ_off[c + 1] - a.succ_off[c] : 0;
@@ -1444,12 +1451,11 @@ __global__ void __launch_bounds__(1024) tac_cspec_kernel(TacArgs a, const uint32
   }
   if (threadIdx.x < 2) dflag[threadIdx.x] = 0;
   auto is_live = [&](int c) { return (live[c >> 5] >> (c & 31)) & 1u; };
-  auto owner = [&](int c) { return c / per; };
-  // this thread owns column c (columns base + threadIdx.x + k * 1024)
-  auto mine_col = [&](int c) {
-    const unsigned j = static_cast<unsigned>(c - base);
-    return j < static_cast<unsigned>(n_own) && (j & 1023u) == threadIdx.x;
-  };
+  auto owner = [&](int c) { return c & (kCS - 1); };
+  auto local = [&](int c) { return c >> 4; };
+  static_assert(kCS == 16, "interleave");
+  // this thread owns column c (local index threadIdx.x + k * 1024)
+  auto mine_col = [&](int c) { return owner(c) == rank && (local(c) & (kCT - 1)) == static_cast<int>(threadIdx.x); };
   auto mplus_j = [&](int j) {
     V m = kInfV;
 #pragma unroll
@@ -1482,15 +1488,30 @@ __global__ void __launch_bounds__(1024) tac_cspec_kernel(TacArgs a, const uint32
         if ((bwv[k][s] >> (col & 31)) & 1u) Mg_s[s * per + j] -= sign * t;
     }
   };
-  auto publish = [&](int col, int slot) {  // owner thread of col: its values for the next interval
-    if (col < R && mine_col(col)) {
-      const int j = col - base, kk = j >> 10;
+  // the owner of col pushes its values for the next interval into every
+  // CTA: its warp broadcasts them and 16 lanes store one CTA each (called by
+  // every thread)
+  auto publish = [&](int col, int slot) {
+    const bool own = col < R && mine_col(col);
+    const unsigned ball = __ballot_sync(~0u, own);
+    if (ball == 0) return;
+    long long pv = 0, mv = 0, tv = 0;
+    if (own) {
+      const int j = local(col), kk = j >> 10;
       V t = 0;
 #pragma unroll
       for (int k = 0; k < kOwn; ++k)
         if (k == kk) t = T_[k];
-      pub[slot] = CSpecPub{P_s[j], mplus_j(j), t, col, 0};
+      pv = P_s[j];
+      mv = mplus_j(j);
+      tv = t;
     }
+    const int src = __ffs(ball) - 1;
+    pv = __shfl_sync(~0u, pv, src);
+    mv = __shfl_sync(~0u, mv, src);
+    tv = __shfl_sync(~0u, tv, src);
+    const int lane = threadIdx.x & 31;
+    if (lane < kCS) *cluster.map_shared_rank(&pubs[slot], lane) = CSpecPub{pv, mv, tv, col, 0};
   };
   auto apply_deltas = [&]() {
 #pragma unroll
@@ -1508,9 +1529,9 @@ __global__ void __launch_bounds__(1024) tac_cspec_kernel(TacArgs a, const uint32
   // whatever the L1s hold; one thread per group)
   auto add_p = [&](int x, unsigned long long wsum) {
     if constexpr (sizeof(V) == 8)
-      atomicAdd(reinterpret_cast<unsigned long long*>(cluster.map_shared_rank(&D_s[x - owner(x) * per], owner(x))), wsum);
+      atomicAdd(reinterpret_cast<unsigned long long*>(cluster.map_shared_rank(&D_s[local(x)], owner(x))), wsum);
     else
-      atomicAdd(cluster.map_shared_rank(&D_s[x - owner(x) * per], owner(x)), static_cast<V>(wsum));
+      atomicAdd(cluster.map_shared_rank(&D_s[local(x)], owner(x)), static_cast<V>(wsum));
     for (int r = 0; r < cs; ++r) *cluster.map_shared_rank(&dflag[iv & 1], r) = 1;
   };
   auto retire_groups = [&](int col, int e0, int e1, int skip, int sign) {
@@ -1552,12 +1573,10 @@ __global__ void __launch_bounds__(1024) tac_cspec_kernel(TacArgs a, const uint32
     __syncthreads();  // bcast is rewritten by the next call
     return w;
   };
-  auto read_pub = [&](int col, int slot) {  // after the interval that published it
-    if (threadIdx.x == 0) fpub = *cluster.map_shared_rank(&pub[slot], owner(col));
+  auto read_pub = [&](int slot) {  // after the interval that published it (pushed here)
+    const CSpecPub v = pubs[slot];
     __syncthreads();
-    const CSpecPub v = fpub;
     reset_flag();
-    __syncthreads();
     return v;
   };
   cluster.sync();  // slices, bitsets and rings ready in every CTA
@@ -1572,30 +1591,40 @@ __global__ void __launch_bounds__(1024) tac_cspec_kernel(TacArgs a, const uint32
   };
   load_first(first);
   if (first < R) load_words(first >> 5);
+  // the list bounds of the column after the incumbent, one interval ahead
+  int c2_end = 0;
+  auto next_c0 = [&](int col, int skip) {
+    const int c = next_live(col, skip);
+    c2_end = c < R ? a.col_off[c + 1] : 0;
+    return c < R ? a.col_off[c] : 0;
+  };
+  int c2_0 = first < R ? next_c0(first, -1) : 0, c2_1 = c2_end;
   end_interval();
-  CSpecPub fp = read_pub(first, pslot);
+  CSpecPub fp = read_pub(pslot);
   int misses = 0;
   for (int round = 0; round < R; ++round) {
     // ---- speculative interval: retire `first` (its group updates issued
     // first: nothing this interval reads them), compare against it
     const int second = next_live(first, first);
-    int rk = 0, rx = 0;
+    int r_cnt = 0, r_xr = 0;  // the atomics' old values, consumed at the end of the interval
     if (f_g >= 0) {
-      rk = atomicSub(&a.cnt[f_g], 1) - 1;
-      rx = atomicXor(&a.xr[f_g], first) ^ first;
+      r_cnt = atomicSub(&a.cnt[f_g], 1);
+      r_xr = atomicXor(&a.xr[f_g], first);
     }
     retire_groups(first, f_c0, f_c1, nthreads, 1);  // entries beyond one per thread (rare)
     if (tid == 0) a.prio[first] = round;
-    // the next incumbent's list and this thread's entry of it
-    const int n_c0 = second < R ? a.col_off[second] : 0, n_c1 = second < R ? a.col_off[second + 1] : 0;
+    // this thread's entry of the next incumbent's list (its bounds loaded
+    // last interval) and the bounds of the one after it: one memory hop each
+    const int n_c0 = c2_0, n_c1 = c2_1;
     const int n_g = n_c0 + tid < n_c1 ? a.col[n_c0 + tid] : -1;
+    const int c3_0 = second < R ? next_c0(second, first) : 0, c3_1 = second < R ? c2_end : 0;
     if ((first >> 5) != wc) load_words(first >> 5);
     int nxt = kInt;
     TacRec mine{0, 0, 0, kInt, 0};
     const V fP = static_cast<V>(fp.P), fT = static_cast<V>(fp.T), fM = static_cast<V>(fp.mp);
 #pragma unroll
     for (int k = 0; k < kOwn; ++k) {  // every column <= first is retired (kDead)
-      const int j = threadIdx.x + k * kCT, c = base + j;
+      const int j = threadIdx.x + k * kCT, c = j * kCS + rank;
       if (j < n_own && c < nxt) {
         const V pc = P_s[j];
         if (pc != kDead) {
@@ -1609,46 +1638,49 @@ __global__ void __launch_bounds__(1024) tac_cspec_kernel(TacArgs a, const uint32
     }
     const int slot = q % 3;
     const int bv = block_min_int(nxt, bred, sp);  // (every compare of this CTA is done)
-    if (nxt == bv && bv != kInt) rec[slot] = mine;
-    if (threadIdx.x == 0) rec[slot].c = bv;
+    reset_flag();  // the previous interval's flag: every thread read it before this barrier
+    if (nxt == bv && bv != kInt) rec[slot] = mine;  // (pulled only on a misspeculation)
+    if (threadIdx.x < kCS) *cluster.map_shared_rank(&mins[slot][rank], threadIdx.x) = bv;  // push
     apply_retire(first, static_cast<V>(fp.T), 1);
     const int npslot = pslot ^ 1;
     publish(second, npslot);  // M+ after this retire, P without its additions
-    if (f_g >= 0 && rk == 1) add_p(rx, a.wsum[f_g]);
+    // (the asm keeps the compiler from waiting on the atomics where they issue)
+    asm volatile("" : "+r"(r_cnt), "+r"(r_xr));
+    if (f_g >= 0 && r_cnt - 1 == 1) add_p(r_xr ^ first, a.wsum[f_g]);
     const bool deltas = end_interval();
-    if (threadIdx.x < 32) {
-      int c = kInt;
-      if (static_cast<int>(threadIdx.x) < cs) c = cluster.map_shared_rank(&rec[slot], threadIdx.x)->c;
-      const int m = __reduce_min_sync(~0u, c);
-      if (m != kInt && c == m) bcast = *cluster.map_shared_rank(&rec[slot], threadIdx.x);
-      if (threadIdx.x == 0 && m == kInt) bcast.c = m;
-      if (threadIdx.x == 0 && second < R) fpub = *cluster.map_shared_rank(&pub[npslot], owner(second));
-    }
-    __syncthreads();
-    TacRec w = bcast;
-    const CSpecPub np = fpub;
-    reset_flag();
+    int m = kInt;
+#pragma unroll
+    for (int r = 0; r < kCS; ++r) m = min(m, mins[slot][r]);
+    const CSpecPub np = pubs[npslot];
     ++q;
-    __syncthreads();  // bcast / fpub are rewritten later
-    if (w.c == kInt) {  // confirmed: `first` was the winner
+    if (m == kInt) {  // confirmed: `first` was the winner
       if (threadIdx.x == 0) live[first >> 5] &= ~(1u << (first & 31));
-      if (mine_col(first)) P_s[first - base] = kDead;
+      if (mine_col(first)) P_s[local(first)] = kDead;
       first = second;
       pslot = npslot;
       fp = np;
       f_c0 = n_c0;
       f_c1 = n_c1;
       f_g = n_g;
+      c2_0 = c3_0;
+      c2_1 = c3_1;
       if (deltas) {  // (every CTA's flag was raised: the fixup is cluster-uniform)
         apply_deltas();
         __syncthreads();
+        reset_flag();
         pslot ^= 1;
         publish(first, pslot);
         end_interval();
-        fp = read_pub(first, pslot);
+        fp = read_pub(pslot);
       }
       continue;
     }
+    // the winner's record, from the CTA that owns it
+    if (threadIdx.x == 0) bcast = *cluster.map_shared_rank(&rec[slot], owner(m));
+    __syncthreads();
+    TacRec w = bcast;
+    reset_flag();  // (the speculative retire's additions are dropped below)
+    __syncthreads();  // bcast is rewritten later
     // ---- misspeculation: undo the retire of `first` (its P additions are
     // dropped), then the chain from w, then retire the chain's winner
     ++misses;
@@ -1668,7 +1700,7 @@ __global__ void __launch_bounds__(1024) tac_cspec_kernel(TacArgs a, const uint32
       TacRec mb{0, 0, 0, kInt, 0};
 #pragma unroll
       for (int k = 0; k < kOwn; ++k) {
-        const int j = threadIdx.x + k * kCT, c = base + j;
+        const int j = threadIdx.x + k * kCT, c = j * kCS + rank;
         if (j < n_own && c > best && c < nb) {
           const V pc = P_s[j];
           if (pc != kDead) {
@@ -1690,15 +1722,17 @@ __global__ void __launch_bounds__(1024) tac_cspec_kernel(TacArgs a, const uint32
     apply_retire(best, static_cast<V>(w.T), 1);
     end_interval();  // the retire's additions have landed
     if (threadIdx.x == 0) live[best >> 5] &= ~(1u << (best & 31));
-    if (mine_col(best)) P_s[best - base] = kDead;
+    if (mine_col(best)) P_s[local(best)] = kDead;
     apply_deltas();
     __syncthreads();
     reset_flag();
     pslot ^= 1;
     publish(first, pslot);
     end_interval();
-    fp = read_pub(first, pslot);
+    fp = read_pub(pslot);
     if ((first >> 5) != wc) load_words(first >> 5);
+    c2_0 = next_c0(first, -1);
+    c2_1 = c2_0 >= 0 ? c2_end : 0;
   }
   if (trace && rank == 0 && threadIdx.x == 0) *trace = misses;
 }

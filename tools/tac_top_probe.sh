@@ -6,7 +6,7 @@ import sys, json, hashlib; sys.path.insert(0,'.')
 from paper_1803_03288_b200.capi import Lib
 gold=json.load(open('tests/golden/tac_large.json'))
 for spec in sys.argv[1:]:
-    g=Lib().model(spec,1); o=g.declared()
+    import os; g=(Lib(os.environ['TICTAC_LIB']) if os.environ.get('TICTAC_LIB') else Lib()).model(spec,1); o=g.declared()
     for _ in range(2):
         p=g.tac(o).priorities()
     print(spec, 'digest ok' if hashlib.sha256(json.dumps(p,sort_keys=True).encode()).hexdigest()==gold[spec]['sha256'] else 'DIGEST MISMATCH', flush=True)
