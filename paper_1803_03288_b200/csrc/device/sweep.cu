@@ -238,10 +238,17 @@ __device__ __forceinline__ bool draw_group(uint64_t seed, int R, int d, const ui
 // t_d = f(s_d, s_d+1) ^ t_{d-156}, t_{d-156} = f(s_{d-156}, s_{d-155}) ^ s_d.
 // Four draws per iteration: four independent twist/temper/bounded chains
 // before the dependent shared-memory swaps.
-template <typename It, typename V, bool kStore = false>
+// kSave: phase 1 keeps its untempered outputs t_d (d < R - 157) in a local
+// array, and phase 2 reads t_{d-156} back instead of re-walking the seeding
+// from s_0 with a third cursor (about 16 instructions per phase-2 draw for
+// one 8-byte store and load; the array stays in L2 — 87 entries per thread at
+// config 4 — where the shuffle's issue-bound loop hides its latency).
+template <typename It, typename V, bool kStore = false, bool kSave = false>
 __device__ __forceinline__ void shuffle_fold(uint64_t seed, int R, const It& items, FoldT<V>& f,
                                              const uint2* tab, V ctot, const V* pw,
                                              const uint64_t* s_lim, const uint64_t* s_mag) {
+  uint64_t ts[kSave ? 156 : 1];
+  const int save_lim = R - 157;  // t_d is read back by phase 2 iff d < R - 157
   items.init(R);
   uint64_t a0 = seed, a1 = mt_step(seed, 1), b = seed;
 #pragma unroll 4
@@ -250,7 +257,10 @@ __device__ __forceinline__ void shuffle_fold(uint64_t seed, int R, const It& ite
   const int n1 = min(draws, 156);
   int d = 0;
   for (; d < n1 && ((R - d) & 3) != 0; ++d) {  // single draws up to an aligned group
-    const uint64_t v[1] = {mt_temper(mt_twist(a0, a1, b))};
+    const uint64_t t = mt_twist(a0, a1, b);
+    if constexpr (kSave)
+      if (d < save_lim) ts[d] = t;
+    const uint64_t v[1] = {mt_temper(t)};
     a0 = a1;
     a1 = mt_step(a1, static_cast<uint32_t>(d + 2));
     b = mt_step(b, static_cast<uint32_t>(d + 157));
@@ -261,21 +271,59 @@ __device__ __forceinline__ void shuffle_fold(uint64_t seed, int R, const It& ite
     const uint32_t u = static_cast<uint32_t>(d);
     const uint64_t a2 = mt_step(a1, u + 2), a3 = mt_step(a2, u + 3), a4 = mt_step(a3, u + 4);
     const uint64_t b1 = mt_step(b, u + 157), b2 = mt_step(b1, u + 158), b3 = mt_step(b2, u + 159);
-    const uint64_t v[4] = {mt_temper(mt_twist(a0, a1, b)), mt_temper(mt_twist(a1, a2, b1)),
-                           mt_temper(mt_twist(a2, a3, b2)), mt_temper(mt_twist(a3, a4, b3))};
+    const uint64_t t[4] = {mt_twist(a0, a1, b), mt_twist(a1, a2, b1), mt_twist(a2, a3, b2), mt_twist(a3, a4, b3)};
+    if constexpr (kSave)
+      if (d < save_lim) {  // (uniform: R is; the group's tail entries past the limit are never read)
+        ts[d] = t[0];
+        ts[d + 1] = t[1];
+        ts[d + 2] = t[2];
+        ts[d + 3] = t[3];
+      }
+    const uint64_t v[4] = {mt_temper(t[0]), mt_temper(t[1]), mt_temper(t[2]), mt_temper(t[3])};
     a0 = a4;
     a1 = mt_step(a4, u + 5);
     b = mt_step(b3, u + 160);
     if (draw_group<4, It, V, kStore, true>(seed, R, d, v, items, f, tab, ctot, pw, s_lim, s_mag, pg)) return;
   }
   for (; d < n1; ++d) {
-    const uint64_t v[1] = {mt_temper(mt_twist(a0, a1, b))};
+    const uint64_t t = mt_twist(a0, a1, b);
+    if constexpr (kSave)
+      if (d < save_lim) ts[d] = t;
+    const uint64_t v[1] = {mt_temper(t)};
     a0 = a1;
     a1 = mt_step(a1, static_cast<uint32_t>(d + 2));
     b = mt_step(b, static_cast<uint32_t>(d + 157));
     if (draw_group<1, It, V, kStore>(seed, R, d, v, items, f, tab, ctot, pw, s_lim, s_mag)) return;
   }
-  if (d < draws) {  // phase 2, c = (s_d-156, s_d-155)
+  if (kSave && d < draws && d == 156) {  // phase 2 from the saved outputs: t_d = f(s_d, s_d+1) ^ t_{d-156}
+    const int n2 = min(draws, 311);
+    for (; d < n2 && ((R - d) & 3) != 0; ++d) {
+      const uint64_t v[1] = {mt_temper(mt_twist(a0, a1, ts[d - 156]))};
+      a0 = a1;
+      a1 = mt_step(a1, static_cast<uint32_t>(d + 2));
+      if (draw_group<1, It, V, kStore>(seed, R, d, v, items, f, tab, ctot, pw, s_lim, s_mag)) return;
+    }
+    pg = reinterpret_cast<unsigned char*>(items.at4((R - 4 - d) >> 2));
+    for (; d + 3 < n2; d += 4, pg -= It::kGroupBytes) {
+      const uint32_t u = static_cast<uint32_t>(d);
+      const uint64_t a2 = mt_step(a1, u + 2), a3 = mt_step(a2, u + 3), a4 = mt_step(a3, u + 4);
+      const uint64_t v[4] = {mt_temper(mt_twist(a0, a1, ts[d - 156])), mt_temper(mt_twist(a1, a2, ts[d - 155])),
+                             mt_temper(mt_twist(a2, a3, ts[d - 154])), mt_temper(mt_twist(a3, a4, ts[d - 153]))};
+      a0 = a4;
+      a1 = mt_step(a4, u + 5);
+      if (draw_group<4, It, V, kStore, true>(seed, R, d, v, items, f, tab, ctot, pw, s_lim, s_mag, pg)) return;
+    }
+    for (; d < n2; ++d) {
+      const uint64_t v[1] = {mt_temper(mt_twist(a0, a1, ts[d - 156]))};
+      a0 = a1;
+      a1 = mt_step(a1, static_cast<uint32_t>(d + 2));
+      if (draw_group<1, It, V, kStore>(seed, R, d, v, items, f, tab, ctot, pw, s_lim, s_mag)) return;
+    }
+    if (d < draws) {  // beyond the first block (R > 312)
+      f = shuffle_slow<It, V, kStore>(seed, d, R - d, items, f, tab, ctot, pw);
+      return;
+    }
+  } else if (d < draws) {  // phase 2, c = (s_d-156, s_d-155)
     uint64_t c0 = seed, c1 = mt_step(seed, 1);
     const int n2 = min(draws, 311);
     for (; d < n2 && ((R - d) & 3) != 0; ++d) {  // single draws up to an aligned group
@@ -553,7 +601,7 @@ __global__ void __launch_bounds__(kSweepThreads, 3) chain_sweep_kernel(ChainArgs
           items.init(R);
           f = shuffle_slow(ws, 0, R, items, f, tab, ctot, pw);
         } else {
-          shuffle_fold(ws, R, items, f, tab, ctot, pw, s_lim, s_mag);
+          shuffle_fold<Items<T>, V, false, true>(ws, R, items, f, tab, ctot, pw, s_lim, s_mag);
         }
       }
       if (f.G > 0) f.best = max(f.best, pw[0]);  // bin 0: computes needing no recv
