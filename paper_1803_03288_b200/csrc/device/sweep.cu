@@ -260,7 +260,7 @@ __device__ __forceinline__ void shuffle_fold(uint64_t seed, int R, const It& ite
     const uint64_t t = mt_twist(a0, a1, b);
     if constexpr (kSave)
       if (d < save_lim) ts[d] = t;
-    const uint64_t v[1] = {mt_temper(t)};
+    const uint64_t v[1] = {mt_temper(kSave ? t : mt_twist(a0, a1, b))};
     a0 = a1;
     a1 = mt_step(a1, static_cast<uint32_t>(d + 2));
     b = mt_step(b, static_cast<uint32_t>(d + 157));
@@ -271,25 +271,33 @@ __device__ __forceinline__ void shuffle_fold(uint64_t seed, int R, const It& ite
     const uint32_t u = static_cast<uint32_t>(d);
     const uint64_t a2 = mt_step(a1, u + 2), a3 = mt_step(a2, u + 3), a4 = mt_step(a3, u + 4);
     const uint64_t b1 = mt_step(b, u + 157), b2 = mt_step(b1, u + 158), b3 = mt_step(b2, u + 159);
-    const uint64_t t[4] = {mt_twist(a0, a1, b), mt_twist(a1, a2, b1), mt_twist(a2, a3, b2), mt_twist(a3, a4, b3)};
-    if constexpr (kSave)
+    if constexpr (kSave) {
+      const uint64_t t[4] = {mt_twist(a0, a1, b), mt_twist(a1, a2, b1), mt_twist(a2, a3, b2), mt_twist(a3, a4, b3)};
       if (d < save_lim) {  // (uniform: R is; the group's tail entries past the limit are never read)
         ts[d] = t[0];
         ts[d + 1] = t[1];
         ts[d + 2] = t[2];
         ts[d + 3] = t[3];
       }
-    const uint64_t v[4] = {mt_temper(t[0]), mt_temper(t[1]), mt_temper(t[2]), mt_temper(t[3])};
-    a0 = a4;
-    a1 = mt_step(a4, u + 5);
-    b = mt_step(b3, u + 160);
-    if (draw_group<4, It, V, kStore, true>(seed, R, d, v, items, f, tab, ctot, pw, s_lim, s_mag, pg)) return;
+      const uint64_t v[4] = {mt_temper(t[0]), mt_temper(t[1]), mt_temper(t[2]), mt_temper(t[3])};
+      a0 = a4;
+      a1 = mt_step(a4, u + 5);
+      b = mt_step(b3, u + 160);
+      if (draw_group<4, It, V, kStore, true>(seed, R, d, v, items, f, tab, ctot, pw, s_lim, s_mag, pg)) return;
+    } else {
+      const uint64_t v[4] = {mt_temper(mt_twist(a0, a1, b)), mt_temper(mt_twist(a1, a2, b1)),
+                             mt_temper(mt_twist(a2, a3, b2)), mt_temper(mt_twist(a3, a4, b3))};
+      a0 = a4;
+      a1 = mt_step(a4, u + 5);
+      b = mt_step(b3, u + 160);
+      if (draw_group<4, It, V, kStore, true>(seed, R, d, v, items, f, tab, ctot, pw, s_lim, s_mag, pg)) return;
+    }
   }
   for (; d < n1; ++d) {
     const uint64_t t = mt_twist(a0, a1, b);
     if constexpr (kSave)
       if (d < save_lim) ts[d] = t;
-    const uint64_t v[1] = {mt_temper(t)};
+    const uint64_t v[1] = {mt_temper(kSave ? t : mt_twist(a0, a1, b))};
     a0 = a1;
     a1 = mt_step(a1, static_cast<uint32_t>(d + 2));
     b = mt_step(b, static_cast<uint32_t>(d + 157));
