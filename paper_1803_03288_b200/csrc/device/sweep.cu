@@ -1311,31 +1311,31 @@ __global__ void __launch_bounds__(kPsThreads) cluster_ps_kernel(ChainArgs a, PsA
 }
 
 // ---- dag_pair_kernel: the same sweep with the positions/bins arrays shared
-// by the two warps of a 64-thread block. A run is phase A (the shuffle, and
-// the noise swaps, into the thread's own gate-order column: R bytes) and
-// phase B (positions, the join program, the fold: R + L + 1 bytes of
-// positions and slots and 4(R + 1) bytes of bins). The warps alternate:
-// while one runs phase B on the block's single set of positions/bins
-// columns (lane l uses column l), the other runs phase A, and named barriers
-// hand the columns over in strict alternation. Shared memory per thread drops
-// from ~6R to ~3.5R bytes, which is what bounds occupancy here.
-constexpr int kPairThreads = 64;
+// by the kW warps of a block. A run is phase A (the shuffle, and the noise
+// swaps, into the thread's own gate-order column: R bytes) and phase B
+// (positions, the join program, the fold: R + L + 1 bytes of positions and
+// slots and 4(R + 1) bytes of bins). Phase A is about three times phase B,
+// so while one warp runs phase B on the block's single set of
+// positions/bins columns (lane l uses column l) the others run phase A, and
+// named barriers pass the columns round the warps in a fixed ring (barrier
+// 1 + w: warp w - 1 hands them to warp w). Shared memory per thread drops
+// from ~6R to ~R + 5R/kW bytes, which is what bounds occupancy here.
 
-__host__ __device__ inline size_t dag_pair_smem(int R, int W, int nrec, int L, int nhist, size_t tb, size_t vb) {
+__host__ __device__ inline size_t dag_pair_smem(int R, int W, int nrec, int L, int nhist, size_t tb, size_t vb,
+                                                int nwarps = 2) {
   const int per = tb == 1 ? 4 : 2;
   const size_t vbins = vb * (R + 1) * 32, vals = 4ull * ((R + L + 1 + per - 1) / per) * 32;
-  const size_t perms = 4ull * ((R + per - 1) / per) * kPairThreads;
+  const size_t perms = 4ull * ((R + per - 1) / per) * 32 * nwarps;
   return round16(dag_table_bytes(R, W, nrec, vb) + 4 * static_cast<size_t>(nhist) * kBins + vbins + vals + perms) + 16;
 }
 
-__device__ __forceinline__ void named_sync(int id) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(kPairThreads)); }
-__device__ __forceinline__ void named_arrive(int id) {
-  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(kPairThreads));
-}
+// named barriers between two warps (64 threads: one arrives, one waits)
+__device__ __forceinline__ void named_sync(int id) { asm volatile("bar.sync %0, 64;" ::"r"(id)); }
+__device__ __forceinline__ void named_arrive(int id) { asm volatile("bar.arrive %0, 64;" ::"r"(id)); }
 
-template <typename T, typename V, bool kNoisy>
-__global__ void __launch_bounds__(kPairThreads) dag_pair_kernel(ChainArgs a, DagArgs g) {
-  constexpr int NT = kPairThreads;
+template <typename T, typename V, bool kNoisy, int kW>
+__global__ void __launch_bounds__(32 * kW) dag_pair_kernel(ChainArgs a, DagArgs g) {
+  constexpr int NT = 32 * kW;
   extern __shared__ __align__(16) unsigned char smem[];
   const int R = a.R, W = a.W, NR = g.nrec;
   const size_t vb = sizeof(V);
@@ -1491,21 +1491,32 @@ __global__ void __launch_bounds__(kPairThreads) dag_pair_kernel(ChainArgs a, Dag
       lo = INT64_MAX;
     }
   };
-  // strict alternation of phase B: warp 0 B(0), warp 1 B(0), warp 0 B(1), ...
-  // barrier 1: warp 0 hands the columns to warp 1; barrier 2: back to warp 0
-  for (int64_t u = 0; u < units; ++u) {
-    phase_a(u);
-    if (warp == 0) {
-      if (u > 0) named_sync(2);
-      phase_b(u);
-      named_arrive(1);
-    } else {
-      named_sync(1);
-      phase_b(u);
-      named_arrive(2);
+  // phase B in a fixed ring: warp 0 B(0), warp 1 B(0), ..., warp kW-1 B(0),
+  // warp 0 B(1), ...; barrier 1 + w hands the columns from warp w - 1 to w
+  if constexpr (kW == 2) {  // (the two-warp form as straight-line code)
+    for (int64_t u = 0; u < units; ++u) {
+      phase_a(u);
+      if (warp == 0) {
+        if (u > 0) named_sync(2);
+        phase_b(u);
+        named_arrive(1);
+      } else {
+        named_sync(1);
+        phase_b(u);
+        named_arrive(2);
+      }
     }
+    if (warp == 0 && units > 0) named_sync(2);
+  } else {
+    const int next_bar = warp + 1 == kW ? 1 : warp + 2;
+    for (int64_t u = 0; u < units; ++u) {
+      phase_a(u);
+      if (warp != 0 || u > 0) named_sync(1 + warp);
+      phase_b(u);
+      named_arrive(next_bar);
+    }
+    if (warp == 0 && units > 0) named_sync(1);  // consume the last warp's final hand-back
   }
-  if (warp == 0 && units > 0) named_sync(2);  // consume warp 1's last hand-back
   __syncthreads();
   acc.flush(a, s_hist, s_shist);
 }
@@ -1657,6 +1668,7 @@ struct SweepPlan {
   void* pair_blob = nullptr;
   size_t pair_smem = 0;
   int pair_blocks = 0;
+  int pair_warps = 4;  // warps sharing one phase-B set (TICTAC_DAG_WARPS: 2, 3, 4, 6)
   // cluster send phase (cluster_ps_kernel): device tables and its own image
   int ps = 0, ps_blocks = 0;
   PsArgs psa{};
@@ -1667,14 +1679,23 @@ struct SweepPlan {
 };
 
 using DagFn = void (*)(ChainArgs, DagArgs);
-static DagFn pair_fn(const SweepPlan* p) {
+template <int kW>
+static DagFn pair_fn_w(const SweepPlan* p) {
   const bool nz = p->noise_thr != 0;
   if (p->tb == 1) {
-    if (nz) return p->narrow ? dag_pair_kernel<uint8_t, int32_t, true> : dag_pair_kernel<uint8_t, int64_t, true>;
-    return p->narrow ? dag_pair_kernel<uint8_t, int32_t, false> : dag_pair_kernel<uint8_t, int64_t, false>;
+    if (nz) return p->narrow ? dag_pair_kernel<uint8_t, int32_t, true, kW> : dag_pair_kernel<uint8_t, int64_t, true, kW>;
+    return p->narrow ? dag_pair_kernel<uint8_t, int32_t, false, kW> : dag_pair_kernel<uint8_t, int64_t, false, kW>;
   }
-  if (nz) return p->narrow ? dag_pair_kernel<uint16_t, int32_t, true> : dag_pair_kernel<uint16_t, int64_t, true>;
-  return p->narrow ? dag_pair_kernel<uint16_t, int32_t, false> : dag_pair_kernel<uint16_t, int64_t, false>;
+  if (nz) return p->narrow ? dag_pair_kernel<uint16_t, int32_t, true, kW> : dag_pair_kernel<uint16_t, int64_t, true, kW>;
+  return p->narrow ? dag_pair_kernel<uint16_t, int32_t, false, kW> : dag_pair_kernel<uint16_t, int64_t, false, kW>;
+}
+static DagFn pair_fn(const SweepPlan* p) {
+  switch (p->pair_warps) {
+    case 2: return pair_fn_w<2>(p);
+    case 3: return pair_fn_w<3>(p);
+    case 6: return pair_fn_w<6>(p);
+    default: return pair_fn_w<4>(p);
+  }
 }
 template <int kSrc>
 static DagFn dag_fn(const SweepPlan* p, bool noisy) {
@@ -1921,14 +1942,34 @@ extern "C" SweepPlan* csk_sweep_plan_dag(int32_t W, int32_t R, const int64_t* d,
   }
   p->blocks = sms * occ;
   p->blocks_orders = sms * occ_o;
-  {  // the warp-pair kernel for random sweeps, when it fits
-    p->pair_smem = dag_pair_smem(R, W, nrec, Ls, nhist, p->tb, vb);
-    const void* pf = reinterpret_cast<const void*>(pair_fn(p));
-    allow_max_dynamic_smem(pf);
-    int occ_p = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_p, pf, kPairThreads, p->pair_smem) != cudaSuccess)
-      cudaGetLastError();
-    p->pair_blocks = std::getenv("TICTAC_DAG_NO_PAIR") ? 0 : sms * occ_p;
+  {  // the shared-phase-B kernel for random sweeps, when it fits
+    auto occupancy = [&](int w, size_t* smem_out) {
+      p->pair_warps = w;
+      *smem_out = dag_pair_smem(R, W, nrec, Ls, nhist, p->tb, vb, w);
+      const void* pf = reinterpret_cast<const void*>(pair_fn(p));
+      allow_max_dynamic_smem(pf);
+      int occ = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pf, 32 * w, *smem_out) != cudaSuccess) {
+        cudaGetLastError();
+        occ = 0;
+      }
+      return occ;
+    };
+    // two warps per phase-B set unless four of them fit half again as many
+    // warps per SM (measured: phase B serialises beyond two per set unless
+    // occupancy grows that much: branchy Inception 0.62 -> 0.72 G with four,
+    // branchy ResNet-101 slower with four than two)
+    size_t smem2 = 0, smem4 = 0;
+    const int occ4 = occupancy(4, &smem4), occ2 = occupancy(2, &smem2);
+    int w = 4 * occ4 * 2 >= 3 * (2 * occ2) && occ4 > 0 ? 4 : 2;
+    if (const char* e = std::getenv("TICTAC_DAG_WARPS")) {
+      const int f = std::atoi(e);
+      if (f == 2 || f == 3 || f == 4 || f == 6) w = f;
+    }
+    size_t sm = 0;
+    const int occ = occupancy(w, &sm);
+    p->pair_smem = sm;
+    p->pair_blocks = std::getenv("TICTAC_DAG_NO_PAIR") ? 0 : sms * occ;
   }
   return p;
 }
@@ -2140,9 +2181,10 @@ extern "C" int csk_sweep_run(SweepPlan* p, uint64_t seed_lo, int64_t count, uint
     a.blob = p->pair_blob;
     a.blob_bytes = static_cast<uint32_t>(p->blob_bytes);
     a.mbar_off = static_cast<uint32_t>(p->pair_smem - 16);
-    const int64_t need = (count + kPairThreads - 1) / kPairThreads;
+    const int nt = 32 * p->pair_warps;
+    const int64_t need = (count + nt - 1) / nt;
     const int blocks = static_cast<int>(std::min<int64_t>(p->pair_blocks, need));
-    pair_fn(p)<<<blocks, kPairThreads, p->pair_smem, st>>>(a, DagArgs{p->J, p->Ls, 0, nullptr});
+    pair_fn(p)<<<blocks, nt, p->pair_smem, st>>>(a, DagArgs{p->J, p->Ls, 0, nullptr});
     LAUNCHED();
     CK(cudaGetLastError());
     return 0;

@@ -138,10 +138,10 @@ def test_dag_orders_simulate_and_brute_force_match_reference(lib, ref):
 
 
 def test_dag_pair_kernel_equals_single_warp_kernel(lib, monkeypatch):
-    """dag_pair_kernel (random sweeps; the two warps of a block share one set
-    of positions/bins columns) against dag_sweep_kernel forced with
-    TICTAC_DAG_NO_PAIR: identical makespans and statistics, with noise and on
-    cluster workers."""
+    """dag_pair_kernel (random sweeps; the warps of a block share one set of
+    positions/bins columns, 2 / 3 / 4 / 6 of them) against dag_sweep_kernel
+    forced with TICTAC_DAG_NO_PAIR: identical makespans and statistics, with
+    noise and on cluster workers."""
     from paper_1803_03288_b200.capi import policy
     cases = [(lambda: lib.model("resnet_v2_101_training_branchy", 1), None),
              (lambda: lib.generate("seriesparallel", 300, 1, "1", 11), policy(True, 0, 0.2)),
@@ -155,9 +155,17 @@ def test_dag_pair_kernel_equals_single_warp_kernel(lib, monkeypatch):
         assert b.sweep_path(b.declared(), pol or policy(True, 0, 0.0))["kernel"] == "dag_sweep_kernel"
         rb = b.sweep_random(b.declared(), 3, 100_003, pol, makespans=True, worker_makespans=b.is_cluster())
         monkeypatch.delenv("TICTAC_DAG_NO_PAIR")
-        assert np.array_equal(ra["makespans"], rb["makespans"])
-        if a.is_cluster():
-            assert np.array_equal(ra["worker_makespans"], rb["worker_makespans"])
-        for k in ("min_us", "argmin_seed", "max_us", "argmax_seed", "sum_us"):
-            assert ra[k] == rb[k], k
-        assert np.array_equal(ra["e_hist"], rb["e_hist"])
+        others = [rb]
+        for warps in ("2", "3", "4", "6"):  # warps sharing one phase-B set
+            monkeypatch.setenv("TICTAC_DAG_WARPS", warps)
+            c = make()
+            others.append(c.sweep_random(c.declared(), 3, 100_003, pol, makespans=True,
+                                         worker_makespans=c.is_cluster()))
+            monkeypatch.delenv("TICTAC_DAG_WARPS")
+        for rb in others:
+            assert np.array_equal(ra["makespans"], rb["makespans"])
+            if a.is_cluster():
+                assert np.array_equal(ra["worker_makespans"], rb["worker_makespans"])
+            for k in ("min_us", "argmin_seed", "max_us", "argmax_seed", "sum_us"):
+                assert ra[k] == rb[k], k
+            assert np.array_equal(ra["e_hist"], rb["e_hist"])
