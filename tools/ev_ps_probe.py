@@ -6,7 +6,8 @@ import time
 sys.path.insert(0, ".")
 from paper_1803_03288_b200.capi import Lib  # noqa: E402
 
-L = Lib()
+import os
+L = Lib(os.environ["TICTAC_LIB"]) if os.environ.get("TICTAC_LIB") else Lib()
 c = L.model("vgg16_training", 1).expand(4, 1, 100)
 o = c.declared()
 print(c.sweep_path(o))
