@@ -1601,7 +1601,7 @@ __global__ void __launch_bounds__(1024) tac_cspec_kernel(TacArgs a, const uint32
   int c2_0 = first < R ? next_c0(first, -1) : 0, c2_1 = c2_end;
   end_interval();
   CSpecPub fp = read_pub(pslot);
-  int misses = 0;
+  int misses = 0, fixups = 0;
   for (int round = 0; round < R; ++round) {
     // ---- speculative interval: retire `first` (its group updates issued
     // first: nothing this interval reads them), compare against it
@@ -1665,6 +1665,7 @@ __global__ void __launch_bounds__(1024) tac_cspec_kernel(TacArgs a, const uint32
       c2_0 = c3_0;
       c2_1 = c3_1;
       if (deltas) {  // (every CTA's flag was raised: the fixup is cluster-uniform)
+        ++fixups;
         apply_deltas();
         __syncthreads();
         reset_flag();
@@ -1734,7 +1735,10 @@ __global__ void __launch_bounds__(1024) tac_cspec_kernel(TacArgs a, const uint32
     c2_0 = next_c0(first, -1);
     c2_1 = c2_0 >= 0 ? c2_end : 0;
   }
-  if (trace && rank == 0 && threadIdx.x == 0) *trace = misses;
+  if (trace && rank == 0 && threadIdx.x == 0) {
+    trace[0] = misses;
+    trace[1] = fixups;
+  }
 }
 
 // Shared setup for properties / tic / tac: rows, closure, group state,
@@ -2137,16 +2141,18 @@ extern "C" int csk_tac(DeviceGraph* g, const int64_t* dur, int32_t* prio, char* 
       return false;
     }
     DevArr d_tr;
-    if (alloc<int>(d_tr, 1, err)) return false;
-    CK(cudaMemset(d_tr.p, 0, 4));
+    if (alloc<int>(d_tr, 2, err)) return false;
+    CK(cudaMemset(d_tr.p, 0, 8));
     int* tp = d_tr.as<int>();
     const uint32_t* bp = S.d_bits.as<uint32_t>();
     const int Wd = S.rw->W;
     CK(cudaLaunchKernelEx(&cfg, fn, a, bp, Wd, per, tp));
     if (trace) {
-      CK(cudaMemcpy(&trace_misses, tp, 4, cudaMemcpyDeviceToHost));
-      std::fprintf(stderr, "[tac] speculative cluster of %d CTAs, %d columns each, %d misspeculated\n", cs, per,
-                   trace_misses);
+      int tr[2] = {0, 0};
+      CK(cudaMemcpy(tr, tp, 8, cudaMemcpyDeviceToHost));
+      trace_misses = tr[0];
+      std::fprintf(stderr, "[tac] speculative cluster of %d CTAs, %d columns each, %d fixup intervals, %d misspeculated\n",
+                   cs, per, tr[1], tr[0]);
     }
     return true;
   };

@@ -143,6 +143,8 @@ def test_dag_pair_kernel_equals_single_warp_kernel(lib, monkeypatch):
     forced with TICTAC_DAG_NO_PAIR: identical makespans and statistics, with
     noise and on cluster workers."""
     from paper_1803_03288_b200.capi import policy
+    for knob in ("TICTAC_DAG_NO_PAIR", "TICTAC_DAG_WARPS"):  # (a variant run may set them globally)
+        monkeypatch.delenv(knob, raising=False)
     cases = [(lambda: lib.model("resnet_v2_101_training_branchy", 1), None),
              (lambda: lib.generate("seriesparallel", 300, 1, "1", 11), policy(True, 0, 0.2)),
              (lambda: lib.model("vgg16_training_branchy", 1).expand(3, 1, 0), None)]

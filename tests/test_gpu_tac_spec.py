@@ -51,7 +51,10 @@ def _graphs(lib):
 
 
 def _run(path, env_extra):
-    env = dict(os.environ, TICTAC_TAC_TRACE="1", **env_extra)
+    # (the kernel knobs of the calling environment are dropped: each run
+    # forces exactly the path it names)
+    env = {k: v for k, v in os.environ.items() if not k.startswith("TICTAC_TAC")}
+    env.update(TICTAC_TAC_TRACE="1", **env_extra)
     r = subprocess.run([sys.executable, "-c", CODE, path], cwd=ROOT, capture_output=True, text=True, env=env,
                        check=True, timeout=600)
     misses = [int(ln.rsplit(",", 1)[1].split()[0]) for ln in r.stderr.splitlines() if "misspeculated" in ln]
