@@ -44,11 +44,25 @@ int csk_event_sim(DeviceGraph* g, const int64_t* dur, int32_t B, const int32_t* 
  * form): run b uses seed seed_lo+b for both its random schedule (per-worker
  * derived seeds when `cluster`) and its choice stream. dev_end (B*n_dev,
  * max event end per device) may be NULL. recv_worker[c] = index of recv
- * column c's device in worker_devices() order (all 0 for worker graphs). */
+ * column c's device in worker_devices() order (all 0 for worker graphs).
+ * Every per-run output may be NULL. With `stats` non-NULL the batch's
+ * statistics are reduced on the device (csk_event_stats below) and only
+ * that block is read back; worker_dev[w] = device index of worker w (for
+ * the iteration time and straggler figures of clusters), U/L = the bounds
+ * the E histogram is binned over (no histogram when U == L). */
+typedef struct {
+  int64_t min_m, max_m, sum_m, count;       /* makespan */
+  int64_t imin, imax, isum;                 /* iteration time (slowest worker), clusters */
+  int64_t stalled;                          /* runs that stalled */
+  int64_t argmin, argmax, iargmin, iargmax; /* lowest run index reaching the extreme */
+  int64_t e_hist[1000], s_hist[1000];
+  double sumsq, ssum;                       /* sum m^2, sum straggler fraction */
+} csk_event_stats;
 int csk_event_sweep(DeviceGraph* g, const int64_t* dur, uint64_t seed_lo, int32_t B,
                     int cluster, const int32_t* recv_worker, int32_t n_workers, int gated,
                     double noise, int64_t* makespan, int64_t* violations, int32_t* status,
-                    int64_t* dev_end, char* err);
+                    int64_t* dev_end, const int32_t* worker_dev, int64_t U, int64_t L,
+                    csk_event_stats* stats, char* err);
 
 /* Brute force: all R! lexicographic permutations of the recv columns, each
  * simulated gated with the same choice seed / noise (metrics.cpp:37-72).

@@ -20,6 +20,7 @@
 // Used for batches and sweeps outside the closed form, brute force outside
 // it, and every report's event list.
 #include <algorithm>
+#include <climits>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -834,9 +835,149 @@ ScratchPool& scratch_pool() {
   return *pool;
 }
 
+// Sweep statistics of a batch reduced where the runs' outputs already are
+// (the reference's sweep summary, sched_main.cpp:480-502, plus the E and
+// straggler histograms): pass 1 folds extremes, sums and histograms (shared
+// histograms, one atomic per block and field), pass 2 finds the lowest run
+// index reaching each extreme. Integer bins as in the host fold.
+struct StatsReq {
+  int cluster;
+  const int32_t* d_wdev;  // worker w's device index
+  int32_t nw;
+  int64_t U, L;
+  csk_event_stats* out;  // host
+};
+
+struct StatsArgs {
+  const int64_t *ms, *dev_end;
+  const int32_t *status, *wdev;
+  int64_t B;
+  int ndev, nw, cluster;
+  int64_t U, L;
+  csk_event_stats* acc;  // device
+};
+
+__device__ __forceinline__ void run_iter(const StatsArgs& a, int64_t b, int64_t* hi, int64_t* lo) {
+  int64_t h = 0, l = INT64_MAX;
+  for (int w = 0; w < a.nw; ++w) {
+    const int64_t v = a.dev_end[b * a.ndev + a.wdev[w]];
+    h = max(h, v);
+    l = min(l, v);
+  }
+  *hi = h;
+  *lo = l;
+}
+
+__global__ void __launch_bounds__(256) event_stats_kernel(StatsArgs a) {
+  __shared__ int s_e[1000], s_s[1000];
+  for (int k = threadIdx.x; k < 1000; k += blockDim.x) s_e[k] = s_s[k] = 0;
+  __syncthreads();
+  long long mn = LLONG_MAX, mx = LLONG_MIN, imn = LLONG_MAX, imx = LLONG_MIN;
+  unsigned long long sum = 0, isum = 0, cnt = 0, stl = 0;
+  double sq = 0.0, ss = 0.0;
+  for (int64_t b = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; b < a.B;
+       b += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t m = a.ms[b];
+    stl += a.status[b] != 0;
+    mn = min(mn, static_cast<long long>(m));
+    mx = max(mx, static_cast<long long>(m));
+    sum += static_cast<unsigned long long>(m);
+    ++cnt;
+    sq += static_cast<double>(m) * static_cast<double>(m);
+    if (a.U != a.L) {
+      const int64_t bin = (1000 * (a.U - m)) / (a.U - a.L);
+      atomicAdd(&s_e[static_cast<int>(min(int64_t{999}, max(int64_t{0}, bin)))], 1);
+    }
+    if (a.cluster) {
+      int64_t hi, lo;
+      run_iter(a, b, &hi, &lo);
+      int bin = 0;
+      if (hi > 0) {
+        ss += static_cast<double>(hi - lo) / static_cast<double>(hi);
+        bin = static_cast<int>(min(int64_t{999}, (1000 * (hi - lo)) / hi));
+      }
+      atomicAdd(&s_s[bin], 1);
+      imn = min(imn, static_cast<long long>(hi));
+      imx = max(imx, static_cast<long long>(hi));
+      isum += static_cast<unsigned long long>(hi);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    mn = min(mn, __shfl_xor_sync(~0u, mn, o));
+    mx = max(mx, __shfl_xor_sync(~0u, mx, o));
+    imn = min(imn, __shfl_xor_sync(~0u, imn, o));
+    imx = max(imx, __shfl_xor_sync(~0u, imx, o));
+    sum += __shfl_xor_sync(~0u, sum, o);
+    isum += __shfl_xor_sync(~0u, isum, o);
+    cnt += __shfl_xor_sync(~0u, cnt, o);
+    stl += __shfl_xor_sync(~0u, stl, o);
+    sq += __shfl_xor_sync(~0u, sq, o);
+    ss += __shfl_xor_sync(~0u, ss, o);
+  }
+  csk_event_stats* acc = a.acc;
+  if ((threadIdx.x & 31) == 0 && cnt > 0) {
+    atomicMin(reinterpret_cast<long long*>(&acc->min_m), mn);
+    atomicMax(reinterpret_cast<long long*>(&acc->max_m), mx);
+    atomicAdd(reinterpret_cast<unsigned long long*>(&acc->sum_m), sum);
+    atomicAdd(reinterpret_cast<unsigned long long*>(&acc->count), cnt);
+    atomicAdd(reinterpret_cast<unsigned long long*>(&acc->stalled), stl);
+    atomicAdd(&acc->sumsq, sq);
+    if (a.cluster) {
+      atomicMin(reinterpret_cast<long long*>(&acc->imin), imn);
+      atomicMax(reinterpret_cast<long long*>(&acc->imax), imx);
+      atomicAdd(reinterpret_cast<unsigned long long*>(&acc->isum), isum);
+      atomicAdd(&acc->ssum, ss);
+    }
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < 1000; k += blockDim.x) {
+    if (s_e[k]) atomicAdd(reinterpret_cast<unsigned long long*>(&acc->e_hist[k]), static_cast<unsigned long long>(s_e[k]));
+    if (s_s[k]) atomicAdd(reinterpret_cast<unsigned long long*>(&acc->s_hist[k]), static_cast<unsigned long long>(s_s[k]));
+  }
+}
+
+__global__ void __launch_bounds__(256) event_argext_kernel(StatsArgs a) {
+  csk_event_stats* acc = a.acc;
+  const int64_t mn = acc->min_m, mx = acc->max_m, imn = acc->imin, imx = acc->imax;
+  for (int64_t b = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; b < a.B;
+       b += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t m = a.ms[b];
+    if (m == mn) atomicMin(reinterpret_cast<long long*>(&acc->argmin), b);
+    if (m == mx) atomicMin(reinterpret_cast<long long*>(&acc->argmax), b);
+    if (a.cluster) {
+      int64_t hi, lo;
+      run_iter(a, b, &hi, &lo);
+      if (hi == imn) atomicMin(reinterpret_cast<long long*>(&acc->iargmin), b);
+      if (hi == imx) atomicMin(reinterpret_cast<long long*>(&acc->iargmax), b);
+    }
+  }
+}
+
+int reduce_stats(const StatsReq& q, const int64_t* d_ms, const int64_t* d_dev, const int32_t* d_st, int64_t B,
+                 int ndev, int sms, char* err) {
+  DevBuf d_acc;
+  csk_event_stats init{};
+  init.min_m = init.imin = INT64_MAX;
+  init.max_m = init.imax = INT64_MIN;
+  init.argmin = init.argmax = init.iargmin = init.iargmax = INT64_MAX;
+  if (dev_copy(d_acc, &init, 1, err)) return 1;
+  StatsArgs a{d_ms, d_dev, d_st, q.d_wdev, B, ndev, q.cluster ? q.nw : 0, q.cluster, q.U, q.L,
+              static_cast<csk_event_stats*>(d_acc.p)};
+  const int blocks = static_cast<int>(std::min<int64_t>((B + 255) / 256, 2LL * sms));
+  event_stats_kernel<<<blocks, 256>>>(a);
+  LAUNCHED();
+  CK(cudaGetLastError());
+  event_argext_kernel<<<blocks, 256>>>(a);
+  LAUNCHED();
+  CK(cudaGetLastError());
+  CK(cudaMemcpy(q.out, d_acc.p, sizeof(csk_event_stats), cudaMemcpyDeviceToHost));
+  return 0;
+}
+
 int run_event(DeviceGraph* g, const int64_t* dur, int64_t B, RunSpec rs, int64_t* makespan,
               int64_t* violations, int32_t* status, int64_t* start, int64_t* end, int64_t* dev_end,
-              char* err) {
+              char* err, const StatsReq* sreq = nullptr) {
   if (ensure_device(err)) return 1;
   if (B <= 0) return 0;
   DevBuf d_dur, d_ms, d_vio, d_st, d_start, d_end, d_dev;
@@ -861,7 +1002,7 @@ int run_event(DeviceGraph* g, const int64_t* dur, int64_t B, RunSpec rs, int64_t
     rs.end = static_cast<int64_t*>(d_end.p);
   }
   rs.dev_end = nullptr;
-  if (dev_end) {
+  if (dev_end || (sreq && sreq->cluster)) {
     if (dev_copy<int64_t>(d_dev, nullptr, static_cast<size_t>(B) * g->ndev, err)) return 1;
     rs.dev_end = static_cast<int64_t*>(d_dev.p);
   }
@@ -966,9 +1107,14 @@ int run_event(DeviceGraph* g, const int64_t* dur, int64_t B, RunSpec rs, int64_t
     cudaEventDestroy(ev0);
     cudaEventDestroy(ev1);
   }
-  CK(cudaMemcpy(makespan, d_ms.p, 8 * B, cudaMemcpyDeviceToHost));
+  if (sreq &&
+      reduce_stats(*sreq, static_cast<const int64_t*>(d_ms.p), static_cast<const int64_t*>(d_dev.p),
+                   static_cast<const int32_t*>(d_st.p), B, g->ndev, sms, err))
+    return 1;
+  // per-run outputs only where the caller asked for them
+  if (makespan) CK(cudaMemcpy(makespan, d_ms.p, 8 * B, cudaMemcpyDeviceToHost));
   if (violations) CK(cudaMemcpy(violations, d_vio.p, 8 * B, cudaMemcpyDeviceToHost));
-  CK(cudaMemcpy(status, d_st.p, 4 * B, cudaMemcpyDeviceToHost));
+  if (status) CK(cudaMemcpy(status, d_st.p, 4 * B, cudaMemcpyDeviceToHost));
   if (start) {
     CK(cudaMemcpy(start, d_start.p, 8ull * g->n, cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(end, d_end.p, 8ull * g->n, cudaMemcpyDeviceToHost));
@@ -1371,7 +1517,8 @@ extern "C" int csk_event_sim(DeviceGraph* g, const int64_t* dur, int32_t B, cons
 extern "C" int csk_event_sweep(DeviceGraph* g, const int64_t* dur, uint64_t seed_lo, int32_t B,
                                int cluster, const int32_t* recv_worker, int32_t n_workers, int gated,
                                double noise, int64_t* makespan, int64_t* violations, int32_t* status,
-                               int64_t* dev_end, char* err) {
+                               int64_t* dev_end, const int32_t* worker_dev, int64_t U, int64_t L,
+                               csk_event_stats* stats, char* err) {
   if (ensure_device(err)) return 1;
   std::vector<int32_t> off(n_workers + 1, 0), cols(g->R);
   for (int c = 0; c < g->R; ++c) off[recv_worker[c] + 1]++;
@@ -1390,7 +1537,11 @@ extern "C" int csk_event_sweep(DeviceGraph* g, const int64_t* dur, uint64_t seed
   rs.n_workers = n_workers;
   rs.gated = gated;
   rs.noise = noise;
-  return run_event(g, dur, B, rs, makespan, violations, status, nullptr, nullptr, dev_end, err);
+  if (!stats) return run_event(g, dur, B, rs, makespan, violations, status, nullptr, nullptr, dev_end, err);
+  DevBuf d_wdev;
+  if (cluster && dev_copy(d_wdev, worker_dev, static_cast<size_t>(n_workers), err)) return 1;
+  const StatsReq q{cluster, static_cast<const int32_t*>(d_wdev.p), n_workers, U, L, stats};
+  return run_event(g, dur, B, rs, makespan, violations, status, nullptr, nullptr, dev_end, err, &q);
 }
 
 extern "C" int csk_brute_force(DeviceGraph* g, const int64_t* dur, int32_t R, uint64_t choice_seed,

@@ -16,6 +16,7 @@
 #include <cstring>
 #include <array>
 #include <map>
+#include <memory>
 #include <set>
 #include <thread>
 
@@ -884,7 +885,7 @@ void finish_stats(const SweepCtx& s, const int64_t* i64, const double* f64, uint
   }
 }
 
-// Exact path: device event simulator over seeds, stats on the host (these
+// Exact path: device event simulator over seeds, stats reduced on the device (these
 // inputs are outside the closed form, so this is the general replica).
 void sweep_exact(SweepCtx& s, uint64_t seed_lo, int64_t count, int64_t* makespans,
                  int64_t* worker_ms, cs_sweep_stats* stats) {
@@ -899,78 +900,61 @@ void sweep_exact(SweepCtx& s, uint64_t seed_lo, int64_t count, int64_t* makespan
   std::vector<int32_t> wdev;
   for (const auto& w : s.workers)
     wdev.push_back(static_cast<int32_t>(std::lower_bound(devs.begin(), devs.end(), w) - devs.begin()));
-  std::vector<int64_t> i64(CS_DSTATS_I64, 0);
-  std::vector<double> f64(CS_DSTATS_F64, 0.0);
-  // min/max with their lowest seeds, tracked directly (no packed keys: this
-  // path also serves U beyond the closed form's key range)
+  if (wdev.empty()) wdev.push_back(0);
+  // Statistics are reduced on the device per chunk (csk_event_stats: min/max
+  // with their lowest run index, sums, histograms); the host only combines
+  // the chunks' blocks in seed order. Per-run makespans and device ends are
+  // copied back only when the caller asked for them.
   struct Ext {
     int64_t lo = INT64_MAX, hi = INT64_MIN;
     uint64_t alo = 0, ahi = 0;
-    void add(int64_t v, uint64_t seed) {
-      if (v < lo) lo = v, alo = seed;
-      if (v > hi) hi = v, ahi = seed;
+    void add(int64_t clo, int64_t chi, uint64_t slo, uint64_t shi) {
+      if (clo < lo) lo = clo, alo = slo;  // chunks in seed order: ties keep the earlier
+      if (chi > hi) hi = chi, ahi = shi;
     }
   } mk, it;
-  int64_t it_sum = 0;
+  cs_sweep_stats acc;
+  std::memset(&acc, 0, sizeof(acc));
+  auto part = std::make_unique<csk_event_stats>();
   const int64_t chunk = 1 << 20;
-  std::vector<int64_t> ms, viol, dev_end;
-  std::vector<int32_t> st;
+  std::vector<int64_t> dev_end;
   for (int64_t base = 0; base < count; base += chunk) {
     const int32_t B = static_cast<int32_t>(std::min(chunk, count - base));
-    ms.resize(B);
-    viol.resize(B);
-    st.resize(B);
-    dev_end.resize(static_cast<size_t>(B) * devs.size());
+    const bool want_dev = s.cluster && worker_ms;
+    if (want_dev) dev_end.resize(static_cast<size_t>(B) * devs.size());
     char err[256] = {0};
     const auto t0 = std::chrono::steady_clock::now();
-    const int rc = csk_event_sweep(dg, s.dur.data(), seed_lo + static_cast<uint64_t>(base), B,
-                                   s.cluster ? 1 : 0, s.recv_worker.data(), nw, s.policy.gated ? 1 : 0,
-                                   s.policy.noise, ms.data(), viol.data(), st.data(),
-                                   s.cluster ? dev_end.data() : nullptr, err);
+    const uint64_t seed0 = seed_lo + static_cast<uint64_t>(base);
+    const int rc = csk_event_sweep(dg, s.dur.data(), seed0, B, s.cluster ? 1 : 0, s.recv_worker.data(), nw,
+                                   s.policy.gated ? 1 : 0, s.policy.noise, makespans ? makespans + base : nullptr,
+                                   nullptr, nullptr, want_dev ? dev_end.data() : nullptr, wdev.data(), s.U, s.L,
+                                   part.get(), err);
     if (rc) fail(kInternal, err);
     if (std::getenv("TICTAC_EVENT_TRACE"))
       std::fprintf(stderr, "[sweep_exact] csk_event_sweep %.3f ms\n",
                    std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
-    for (int32_t b = 0; b < B; ++b) {
-      if (st[b]) fail(kValidation, "simulation stalled with no runnable op");
-      const int64_t idx = base + b;
-      const uint64_t seed = seed_lo + static_cast<uint64_t>(idx);
-      const int64_t m = ms[b];
-      if (makespans) makespans[idx] = m;
-      int64_t hi = 0, lo = INT64_MAX;
-      if (s.cluster) {
-        for (int32_t w = 0; w < nw; ++w) {
-          const int64_t mw = dev_end[static_cast<size_t>(b) * devs.size() + wdev[w]];
-          if (worker_ms) worker_ms[idx * nw + w] = mw;
-          hi = std::max(hi, mw);
-          lo = std::min(lo, mw);
-        }
-        int bin = 0;
-        if (hi > 0) {
-          f64[1] += static_cast<double>(hi - lo) / static_cast<double>(hi);
-          bin = std::min(999, static_cast<int>((1000 * (hi - lo)) / hi));
-        }
-        i64[1008 + bin]++;
-      }
-      // makespan statistics (the reference's sweep summary); iteration time
-      // (slowest worker) separately for clusters
-      mk.add(m, seed);
-      if (s.cluster) {
-        it.add(hi, seed);
-        it_sum += hi;
-      }
-      i64[2] += m;
-      i64[3] += 1;
-      f64[0] += static_cast<double>(m) * static_cast<double>(m);
-      if (s.U != s.L) {
-        const int64_t bin = (1000 * (s.U - m)) / (s.U - s.L);
-        i64[8 + std::min<int64_t>(999, std::max<int64_t>(0, bin))]++;
-      }
+    const csk_event_stats& c = *part;
+    if (c.stalled) fail(kValidation, "simulation stalled with no runnable op");
+    if (want_dev)
+      for (int32_t b = 0; b < B; ++b)
+        for (int32_t w = 0; w < nw; ++w)
+          worker_ms[(base + b) * nw + w] = dev_end[static_cast<size_t>(b) * devs.size() + wdev[w]];
+    mk.add(c.min_m, c.max_m, seed0 + static_cast<uint64_t>(c.argmin), seed0 + static_cast<uint64_t>(c.argmax));
+    if (s.cluster)
+      it.add(c.imin, c.imax, seed0 + static_cast<uint64_t>(c.iargmin), seed0 + static_cast<uint64_t>(c.iargmax));
+    acc.count += c.count;
+    acc.sum_us += c.sum_m;
+    acc.sumsq_us += c.sumsq;
+    acc.iter_sum_us += c.isum;
+    acc.straggler_sum += c.ssum;
+    for (int k = 0; k < CS_HIST_BINS; ++k) {
+      acc.e_hist[k] += c.e_hist[k];
+      acc.straggler_hist[k] += c.s_hist[k];
     }
   }
   if (!stats) return;
   std::memset(stats, 0, sizeof(*stats));
-  stats->count = i64[3];
+  stats->count = acc.count;
   stats->upper_us = s.U;
   stats->lower_us = s.L;
   if (stats->count > 0) {
@@ -979,20 +963,20 @@ void sweep_exact(SweepCtx& s, uint64_t seed_lo, int64_t count, int64_t* makespan
     stats->max_us = mk.hi;
     stats->argmax_seed = mk.ahi;
   }
-  stats->sum_us = i64[2];
-  stats->sumsq_us = f64[0];
+  stats->sum_us = acc.sum_us;
+  stats->sumsq_us = acc.sumsq_us;
   for (int k = 0; k < CS_HIST_BINS; ++k) {
-    stats->e_hist[k] = i64[8 + k];
-    stats->straggler_hist[k] = i64[1008 + k];
+    stats->e_hist[k] = acc.e_hist[k];
+    stats->straggler_hist[k] = s.cluster ? acc.straggler_hist[k] : 0;
   }
   stats->n_workers = s.cluster ? nw : 0;
-  stats->straggler_sum = f64[1];
+  stats->straggler_sum = acc.straggler_sum;
   if (s.cluster && stats->count > 0) {
     stats->iter_min_us = it.lo;
     stats->iter_argmin_seed = it.alo;
     stats->iter_max_us = it.hi;
     stats->iter_argmax_seed = it.ahi;
-    stats->iter_sum_us = it_sum;
+    stats->iter_sum_us = acc.iter_sum_us;
   }
 }
 

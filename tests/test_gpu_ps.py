@@ -83,3 +83,45 @@ def test_ps_equals_forced_event_replica(lib, monkeypatch):
                 assert ra[k] == rb[k], (name, k)
             assert np.array_equal(ra["e_hist"], rb["e_hist"]) and np.array_equal(ra["straggler_hist"],
                                                                                   rb["straggler_hist"])
+
+
+@pytest.mark.parametrize("cluster", [True, False])
+def test_exact_sweep_stats_reduced_on_device(lib, monkeypatch, cluster):
+    """The exact path's statistics come from the device reduction
+    (event_stats_kernel / event_argext_kernel) with no per-run read-back:
+    a stats-only call over more than one 2^20-run chunk equals numpy over the
+    makespans a second call returns, and the closed form's statistics."""
+    from paper_1803_03288_b200.capi import policy
+    if cluster:
+        text = lib.generate("chain", 6, 2, "1/2", 11).expand(2, 1, 3).serialize()
+        pol = None
+    else:
+        text = lib.generate("layered", 8, 3, "1/3", 5).serialize()
+        pol = policy(True, 0, 0.3)
+    n = (1 << 20) + 4321
+    fast = lib.graph(text)
+    rf = fast.sweep_random(fast.declared(), 7, n, pol, makespans=True, worker_makespans=cluster)
+    monkeypatch.setenv("TICTAC_SWEEP_FORCE_EXACT", "1")
+    g = lib.graph(text)
+    o = g.declared()
+    assert g.sweep_path(o, pol)["path"] == "event_sim_kernel"
+    only = g.sweep_random(o, 7, n, pol)
+    full = g.sweep_random(o, 7, n, pol, makespans=True, worker_makespans=cluster)
+    ms = full["makespans"]
+    assert np.array_equal(ms, rf["makespans"])
+    assert only["count"] == n
+    assert only["min_us"] == ms.min() and only["argmin_seed"] == 7 + int(np.argmin(ms))
+    assert only["max_us"] == ms.max() and only["argmax_seed"] == 7 + int(np.argmax(ms))
+    assert only["sum_us"] == int(ms.sum())
+    assert abs(only["sumsq_us"] - float((ms.astype(np.float64) ** 2).sum())) <= 1e-9 * only["sumsq_us"]
+    keys = ["min_us", "argmin_seed", "max_us", "argmax_seed", "sum_us", "count"]
+    if cluster:
+        it = full["worker_makespans"].max(axis=1)
+        assert only["iter_min_us"] == it.min() and only["iter_argmin_seed"] == 7 + int(np.argmin(it))
+        assert only["iter_max_us"] == it.max() and only["iter_argmax_seed"] == 7 + int(np.argmax(it))
+        assert np.array_equal(full["worker_makespans"], rf["worker_makespans"])
+        keys += ["iter_min_us", "iter_argmin_seed", "iter_max_us", "iter_argmax_seed", "iter_sum_us"]
+    for k in keys:
+        assert only[k] == full[k] == rf[k], k
+    for h in ("e_hist", "straggler_hist"):
+        assert np.array_equal(only[h], rf[h]), h
