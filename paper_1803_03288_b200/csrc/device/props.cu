@@ -1413,7 +1413,11 @@ __global__ void __launch_bounds__(1024) tac_cspec_kernel(TacArgs a, const uint32
   constexpr int kCS = kClusterMax;
   const int n_own = max(0, (R - rank + kCS - 1) / kCS);
   (void)cs;
-  auto* P_s = reinterpret_cast<V*>(csp);                     // [per] (kDead once retired)
+  // [per] P of outstanding columns (>= 0); kDead + 1 + round once retired in
+  // that round (written to a.prio at the end: no global store inside a round,
+  // so the barrier's release fence has nothing of ours in flight); kDead
+  // when not outstanding at the start
+  auto* P_s = reinterpret_cast<V*>(csp);
   auto* D_s = P_s + per;                                      // [per] P additions of the last retire
   auto* Mg_s = D_s + per;                                     // [kS][per] M of direct-successor groups
   auto* live = reinterpret_cast<uint32_t*>(csp + round16((2 + kS) * sizeof(V) * per));  // replicated outstanding bitset
@@ -1612,7 +1616,6 @@ __global__ void __launch_bounds__(1024) tac_cspec_kernel(TacArgs a, const uint32
       r_xr = atomicXor(&a.xr[f_g], first);
     }
     retire_groups(first, f_c0, f_c1, nthreads, 1);  // entries beyond one per thread (rare)
-    if (tid == 0) a.prio[first] = round;
     // this thread's entry of the next incumbent's list (its bounds loaded
     // last interval) and the bounds of the one after it: one memory hop each
     const int n_c0 = c2_0, n_c1 = c2_1;
@@ -1627,7 +1630,7 @@ __global__ void __launch_bounds__(1024) tac_cspec_kernel(TacArgs a, const uint32
       const int j = threadIdx.x + k * kCT, c = j * kCS + rank;
       if (j < n_own && c < nxt) {
         const V pc = P_s[j];
-        if (pc != kDead) {
+        if (pc >= 0) {
           const V mc = mplus_j(j);
           if (precedes_v(c, pc, T_[k], mc, first, fP, fT, fM)) {
             nxt = c;
@@ -1655,7 +1658,7 @@ __global__ void __launch_bounds__(1024) tac_cspec_kernel(TacArgs a, const uint32
     ++q;
     if (m == kInt) {  // confirmed: `first` was the winner
       if (threadIdx.x == 0) live[first >> 5] &= ~(1u << (first & 31));
-      if (mine_col(first)) P_s[local(first)] = kDead;
+      if (mine_col(first)) P_s[local(first)] = kDead + 1 + round;
       first = second;
       pslot = npslot;
       fp = np;
@@ -1704,7 +1707,7 @@ __global__ void __launch_bounds__(1024) tac_cspec_kernel(TacArgs a, const uint32
         const int j = threadIdx.x + k * kCT, c = j * kCS + rank;
         if (j < n_own && c > best && c < nb) {
           const V pc = P_s[j];
-          if (pc != kDead) {
+          if (pc >= 0) {
             const V mc = mplus_j(j);
             if (precedes_v(c, pc, T_[k], mc, best, static_cast<V>(w.P), static_cast<V>(w.T), static_cast<V>(w.mp))) {
               nb = c;
@@ -1719,11 +1722,10 @@ __global__ void __launch_bounds__(1024) tac_cspec_kernel(TacArgs a, const uint32
     }
     const int best = w.c;
     retire_groups(best, a.col_off[best], a.col_off[best + 1], 0, 1);
-    if (tid == 0) a.prio[best] = round;
     apply_retire(best, static_cast<V>(w.T), 1);
     end_interval();  // the retire's additions have landed
     if (threadIdx.x == 0) live[best >> 5] &= ~(1u << (best & 31));
-    if (mine_col(best)) P_s[local(best)] = kDead;
+    if (mine_col(best)) P_s[local(best)] = kDead + 1 + round;
     apply_deltas();
     __syncthreads();
     reset_flag();
@@ -1734,6 +1736,11 @@ __global__ void __launch_bounds__(1024) tac_cspec_kernel(TacArgs a, const uint32
     if ((first >> 5) != wc) load_words(first >> 5);
     c2_0 = next_c0(first, -1);
     c2_1 = c2_0 >= 0 ? c2_end : 0;
+  }
+#pragma unroll
+  for (int k = 0; k < kOwn; ++k) {
+    const int j = threadIdx.x + k * kCT;
+    if (j < n_own && P_s[j] != kDead) a.prio[j * kCS + rank] = static_cast<int32_t>(P_s[j] - kDead - 1);
   }
   if (trace && rank == 0 && threadIdx.x == 0) {
     trace[0] = misses;
