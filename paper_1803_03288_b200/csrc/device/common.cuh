@@ -185,6 +185,37 @@ struct MtFullP {
 };
 using MtFull = MtFullP<uint64_t*>;
 
+// The same sequence with the twist done in place one element per draw:
+// output i of a block needs s[i], s[i+1] and s[i+156] of the previous
+// block, or, for i >= 156, the already-twisted t[i-156] (and t[0] for
+// i = 311) — exactly what the array holds when elements are twisted in draw
+// order. No 312-element burst, so 32 lockstep runs that draw at different
+// times (the event replica's choice streams) do not serialise a whole
+// twist loop each.
+template <typename P>
+struct MtInPlaceP {
+  P mt;
+  int idx;
+  __device__ void seed(uint64_t s) {
+    uint64_t prev = s;
+    mt[0] = s;
+    for (uint32_t i = 1; i < 312; ++i) {
+      prev = mt_step(prev, i);
+      mt[i] = prev;
+    }
+    idx = 0;
+  }
+  __device__ __forceinline__ uint64_t next() {
+    const int i = idx;
+    const int i1 = i == 311 ? 0 : i + 1;
+    const int im = i < 156 ? i + 156 : i - 156;
+    const uint64_t v = mt_twist(mt[i], mt[i1], mt[im]);
+    mt[i] = v;
+    idx = i1;
+    return mt_temper(v);
+  }
+};
+
 // Register-only engine for the first 311 outputs (SURVEY §7 hard part 2:
 // every random order with R <= 312 lives in the first block). Outputs
 // i < 156 need s[i], s[i+1], s[i+156]; outputs 156 <= i < 311 need the

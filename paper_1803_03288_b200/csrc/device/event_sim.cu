@@ -404,7 +404,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, kL == 1 ? kThreadMinBlock
       for (int p = lane; p < k; p += kL) s.gate[s.seq[o0 + p]] = p;
       group_sync<kL>();
     }
-    MtFullP<Arr<uint64_t, S>> choice{s.mt, 0};
+    MtInPlaceP<Arr<uint64_t, S>> choice{s.mt, 0};
     if (lane == 0) choice.seed(choice_seed);
     group_sync<kL>();
 
