@@ -21,6 +21,29 @@ import numpy as np
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
 PRODUCT_LIB = os.path.join(PKG_DIR, "libcommsched.so")
 
+
+def _torch_nccl() -> str | None:
+    """torch's bundled NCCL (nvidia-nccl wheel), found without importing
+    torch: the library's multi-GPU path loads it (TICTAC_NCCL_LIB) instead of
+    an older system copy that a later `import torch` would then be bound to
+    through the shared soname."""
+    import importlib.util
+    try:
+        spec = importlib.util.find_spec("nvidia.nccl")
+    except (ImportError, ValueError):
+        return None
+    for d in (spec.submodule_search_locations or []) if spec else []:
+        p = os.path.join(d, "lib", "libnccl.so.2")
+        if os.path.exists(p):
+            return p
+    return None
+
+
+if not os.environ.get("TICTAC_NCCL_LIB"):
+    _p = _torch_nccl()
+    if _p:
+        os.environ["TICTAC_NCCL_LIB"] = _p
+
 CS_OK, CS_ERR_INTERNAL, CS_ERR_VALIDATION, CS_ERR_COVERAGE, CS_ERR_PARAMETER, CS_ERR_IO = range(6)
 HIST_BINS = 1000
 DSTATS_I64 = 2008

@@ -14,6 +14,7 @@
 // (include/commsched.h CS_DSTATS_*).
 #include <cuda_runtime.h>
 #include <dlfcn.h>
+#include <cstdlib>
 #include <nccl.h>
 
 #include <cstring>
@@ -42,9 +43,17 @@ const NcclApi& nccl() {
   static NcclApi api;
   static std::once_flag once;
   std::call_once(once, [] {
+    // An NCCL already in the process (e.g. torch's) first; then the one
+    // TICTAC_NCCL_LIB names (the Python binding points it at torch's
+    // bundled copy, so a later `import torch` finds the same, newer library
+    // under the shared soname); then the system's. Loaded RTLD_LOCAL: its
+    // symbols never interpose on other libraries.
+    api.h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    const char* env = std::getenv("TICTAC_NCCL_LIB");
+    if (!api.h && env && *env) api.h = dlopen(env, RTLD_NOW | RTLD_LOCAL);
     for (const char* name : {"libnccl.so.2", "libnccl.so"}) {
-      api.h = dlopen(name, RTLD_NOW | RTLD_GLOBAL);
       if (api.h) break;
+      api.h = dlopen(name, RTLD_NOW | RTLD_LOCAL);
     }
     if (!api.h) {
       api.why = std::string("NCCL unavailable: ") + dlerror();

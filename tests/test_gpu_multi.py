@@ -83,3 +83,22 @@ def test_cli_gpus_flag_same_csv(lib, cli, tmp_path):
         assert r.returncode == 0, r.stderr
         outs.append((out.read_text(), r.stdout.strip().splitlines()[-1]))  # the summary line
     assert outs[0] == outs[1]
+
+
+@pytest.mark.skipif(_devices() < 2, reason="needs two GPUs")
+def test_torch_imports_after_multi_sweep():
+    """The multi-GPU path loads NCCL before torch has been imported: it must
+    be torch's own copy (TICTAC_NCCL_LIB, set by the binding), locally bound,
+    so torch's later import resolves every NCCL symbol it needs."""
+    import os
+    import sys
+    code = ("import sys; sys.path.insert(0, '.')\n"
+            "from paper_1803_03288_b200.capi import Lib\n"
+            "g = Lib().model('resnet_v2_50_inference', 1); o = g.declared()\n"
+            "r = g.sweep_random_multi(o, 1, 20000, 2)\n"
+            "import torch\n"
+            "x = torch.ones(4, device='cuda'); print(int(x.sum().item()), r['count'])\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert out.stdout.strip().splitlines()[-1].split() == ["4", "20000"]  # (NCCL may print its version first)
