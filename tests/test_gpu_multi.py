@@ -85,13 +85,14 @@ def test_cli_gpus_flag_same_csv(lib, cli, tmp_path):
     assert outs[0] == outs[1]
 
 
-@pytest.mark.skipif(_devices() < 2, reason="needs two GPUs")
 def test_torch_imports_after_multi_sweep():
     """The multi-GPU path loads NCCL before torch has been imported: it must
     be torch's own copy (TICTAC_NCCL_LIB, set by the binding), locally bound,
     so torch's later import resolves every NCCL symbol it needs."""
     import os
     import sys
+    if _devices() < 2:
+        pytest.skip("needs two GPUs")
     code = ("import sys; sys.path.insert(0, '.')\n"
             "from paper_1803_03288_b200.capi import Lib\n"
             "g = Lib().model('resnet_v2_50_inference', 1); o = g.declared()\n"
