@@ -1390,6 +1390,28 @@ __device__ __forceinline__ bool precedes_v(int a, V ap, V am, V amp, int b, V bp
   return a < b;
 }
 
+// Shared-memory loads/stores through a held 32-bit address (volatile and
+// ordered like the plain accesses they replace).
+template <typename V>
+__device__ __forceinline__ V lds_v(uint32_t a) {
+  if constexpr (sizeof(V) == 8) {
+    long long v;
+    asm volatile("ld.shared.b64 %0, [%1];" : "=l"(v) : "r"(a) : "memory");
+    return static_cast<V>(v);
+  } else {
+    int v;
+    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+    return static_cast<V>(v);
+  }
+}
+template <typename V>
+__device__ __forceinline__ void sts_v(uint32_t a, V v) {
+  if constexpr (sizeof(V) == 8)
+    asm volatile("st.shared.b64 [%0], %1;" :: "r"(a), "l"(static_cast<long long>(v)) : "memory");
+  else
+    asm volatile("st.shared.b32 [%0], %1;" :: "r"(a), "r"(static_cast<int>(v)) : "memory");
+}
+
 template <int kOwn, int kS, typename V>
 __global__ void __launch_bounds__(1024) tac_cspec_kernel(TacArgs a, const uint32_t* __restrict__ bits, int W, int per,
                                                          int* trace) {
@@ -1460,10 +1482,17 @@ __global__ void __launch_bounds__(1024) tac_cspec_kernel(TacArgs a, const uint32
   static_assert(kCS == 16, "interleave");
   // this thread owns column c (local index threadIdx.x + k * 1024)
   auto mine_col = [&](int c) { return owner(c) == rank && (local(c) & (kCT - 1)) == static_cast<int>(threadIdx.x); };
+  // 32-bit shared-window addresses of the per-column arrays, computed once
+  // and held (the hot loops otherwise re-derive the window base from the
+  // CTA's cluster id for every column: an S2R and three dependent
+  // instructions before each load)
+  uint32_t pa = static_cast<uint32_t>(__cvta_generic_to_shared(P_s));
+  uint32_t ma = static_cast<uint32_t>(__cvta_generic_to_shared(Mg_s));
+  asm volatile("" : "+r"(pa), "+r"(ma));
   auto mplus_j = [&](int j) {
     V m = kInfV;
 #pragma unroll
-    for (int s = 0; s < kS; ++s) m = min(m, Mg_s[s * per + j]);
+    for (int s = 0; s < kS; ++s) m = min(m, lds_v<V>(ma + static_cast<uint32_t>(sizeof(V) * (s * per + j))));
     return m;
   };
   auto next_live = [&](int c, int skip) {
@@ -1489,7 +1518,10 @@ __global__ void __launch_bounds__(1024) tac_cspec_kernel(TacArgs a, const uint32
       if (j >= n_own) continue;
 #pragma unroll
       for (int s = 0; s < kS; ++s)
-        if ((bwv[k][s] >> (col & 31)) & 1u) Mg_s[s * per + j] -= sign * t;
+        if ((bwv[k][s] >> (col & 31)) & 1u) {
+          const uint32_t ad = ma + static_cast<uint32_t>(sizeof(V) * (s * per + j));
+          sts_v<V>(ad, lds_v<V>(ad) - sign * t);
+        }
     }
   };
   // the owner of col pushes its values for the next interval into every
@@ -1629,7 +1661,7 @@ __global__ void __launch_bounds__(1024) tac_cspec_kernel(TacArgs a, const uint32
     for (int k = 0; k < kOwn; ++k) {  // every column <= first is retired (kDead)
       const int j = threadIdx.x + k * kCT, c = j * kCS + rank;
       if (j < n_own && c < nxt) {
-        const V pc = P_s[j];
+        const V pc = lds_v<V>(pa + static_cast<uint32_t>(sizeof(V) * j));
         if (pc >= 0) {
           const V mc = mplus_j(j);
           if (precedes_v(c, pc, T_[k], mc, first, fP, fT, fM)) {
@@ -1706,7 +1738,7 @@ __global__ void __launch_bounds__(1024) tac_cspec_kernel(TacArgs a, const uint32
       for (int k = 0; k < kOwn; ++k) {
         const int j = threadIdx.x + k * kCT, c = j * kCS + rank;
         if (j < n_own && c > best && c < nb) {
-          const V pc = P_s[j];
+          const V pc = lds_v<V>(pa + static_cast<uint32_t>(sizeof(V) * j));
           if (pc >= 0) {
             const V mc = mplus_j(j);
             if (precedes_v(c, pc, T_[k], mc, best, static_cast<V>(w.P), static_cast<V>(w.T), static_cast<V>(w.mp))) {
