@@ -2154,6 +2154,7 @@ extern "C" int csk_tac(DeviceGraph* g, const int64_t* dur, int32_t* prio, char* 
   (kS == 1 ? (kown <= 1   ? tac_cspec_kernel<1, 1, V>                                                          \
               : kown <= 2 ? tac_cspec_kernel<2, 1, V>                                                          \
               : kown <= 4 ? tac_cspec_kernel<4, 1, V>                                                          \
+              : kown <= 7 ? tac_cspec_kernel<7, 1, V>                                                          \
                           : tac_cspec_kernel<8, 1, V>)                                                         \
            : (kown <= 1   ? tac_cspec_kernel<1, 2, V>                                                          \
               : kown <= 2 ? tac_cspec_kernel<2, 2, V>                                                          \
