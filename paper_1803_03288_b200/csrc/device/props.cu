@@ -1424,7 +1424,7 @@ __global__ void __launch_bounds__(1024) tac_cspec_kernel(TacArgs a, const uint32
   __shared__ TacRec bcast;
   __shared__ CSpecPub fpub;
   __shared__ int dflag[2];  // some retire added to a P of this CTA's columns, per interval parity (set remotely)
-  __shared__ int mins[3][kClusterMax];     // every CTA's block min, pushed into every CTA (3-slot ring)
+  __shared__ __align__(16) int mins[3][kClusterMax];  // every CTA's block min, pushed into every CTA (3-slot ring)
   __shared__ CSpecPub pubs[2];             // the next incumbent's values, pushed by its owner
   int sp = 0, q = 0, iv = 0;
   const int R = a.R, cs = static_cast<int>(cluster.num_blocks());
@@ -1685,7 +1685,10 @@ __global__ void __launch_bounds__(1024) tac_cspec_kernel(TacArgs a, const uint32
     const bool deltas = end_interval();
     int m = kInt;
 #pragma unroll
-    for (int r = 0; r < kCS; ++r) m = min(m, mins[slot][r]);
+    for (int r = 0; r < kCS / 4; ++r) {  // four 16-byte loads
+      const int4 mv = reinterpret_cast<const int4*>(mins[slot])[r];
+      m = min(m, min(min(mv.x, mv.y), min(mv.z, mv.w)));
+    }
     const CSpecPub np = pubs[npslot];
     ++q;
     if (m == kInt) {  // confirmed: `first` was the winner
